@@ -1,0 +1,155 @@
+/*
+ * sla_b200.h -- C-ABI of the B200-native SLA (Sparse-Linear Attention) operator.
+ *
+ * Drop-in boundary for the reference's C++ operator API (namespace sla, reference paths
+ * relative to /root/reference/proj/core):
+ *
+ *   reference                                         replaced by
+ *   ------------------------------------------------  ------------------------------------
+ *   make_block_layout        layout.cpp:8-26          sla_b200_validate
+ *   validate_config          config.cpp:7-19          sla_b200_validate
+ *   predict_compressed_weights + classify_mask
+ *                            mask.cpp:57-119          sla_b200_classify
+ *   sla_forward              forward.hpp:63-68        sla_b200_forward (mask_in == NULL)
+ *   sla_forward_with_mask    forward.hpp:70-78        sla_b200_forward (mask_in != NULL)
+ *   combine_outputs          forward.hpp:80-83        fused: sla_b200_forward writes o
+ *   proj_backward            backward.hpp:18-23       fused into sla_b200_backward
+ *   sla_backward             backward.hpp:25-38       sla_b200_backward[_ex]
+ *   SlaForwardState          forward.hpp:33-43        the caller-owned `state` buffer
+ *   std::invalid_argument / std::runtime_error        status 2 / 1 + sla_b200_last_error()
+ *
+ * Plain C: no CUDA or C++ types cross this boundary.  Pointers are DEVICE pointers unless
+ * the function name ends in _host.  `stream` is a cudaStream_t passed as void*.
+ * No device allocation happens inside any call; the caller provides `state` (persists
+ * from forward to backward, like SlaForwardState) and `workspace` (scratch) buffers of
+ * the sizes sla_b200_sizes() reports.  Calls are stream-ordered and re-entrant per stream.
+ *
+ * Layout: a problem is B*H independent (batch, head) "units"; every [*, N, d] tensor is
+ * unit-major and per-unit row-major N x d (the reference Mat layout, mat.hpp:11-18).
+ * W is per head, [H, d, d] indexed [in][out] as in OutputProjection (forward.hpp:27-30);
+ * dW is accumulated over the batch per head.
+ */
+#ifndef SLA_B200_H
+#define SLA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SLA_B200_ABI_VERSION 1
+
+/* status codes: mirror the reference CLI exit codes (tools/sla_main.cpp:564-570) */
+#define SLA_B200_OK 0
+#define SLA_B200_ERR_RUNTIME 1 /* std::runtime_error analogue (CUDA error, non-finite out) */
+#define SLA_B200_ERR_INVALID 2 /* std::invalid_argument analogue (shape, config, input)   */
+
+/* feature map phi -- same order as sla::FeatureMapKind (config.hpp:12-16) */
+#define SLA_B200_PHI_ELU1 0
+#define SLA_B200_PHI_RELU 1
+#define SLA_B200_PHI_SOFTMAX 2
+
+/* element type of q/k/v/w/d_out and of the o, o_s, o_l, dq, dk, dv outputs */
+#define SLA_B200_BF16 0
+#define SLA_B200_F32 1
+
+/* arithmetic of the classification stage (K1+K2).  F64 reproduces the reference bit for
+ * bit (mask.hpp:56-58 computes the mask in f64 on every path); F32 is the north-star fp32
+ * variant whose rare disagreements lie on near-ties. */
+#define SLA_B200_MASK_F64 0
+#define SLA_B200_MASK_F32 1
+
+/* flags */
+#define SLA_B200_FLAG_CHECK_FINITE 1u /* reject non-finite q/k/v with "(r, c)" (forward.cpp:15-25)
+                                         and non-finite outputs (forward.cpp:164-170); syncs  */
+#define SLA_B200_FLAG_GENERIC 2u      /* force the shape-generic SIMT kernels                 */
+
+typedef struct sla_b200_problem {
+  int64_t batch;    /* B                                  */
+  int64_t heads;    /* H                                  */
+  int64_t n;        /* sequence length N (multiple of b_q and b_kv) */
+  int64_t d;        /* head dimension                     */
+  int64_t b_q;      /* rows per query block               */
+  int64_t b_kv;     /* rows per key/value block           */
+  double k_h;       /* percent critical per row, (0, 100] */
+  double k_l;       /* percent negligible per row, [0, 100) */
+  int32_t phi;      /* SLA_B200_PHI_*                     */
+  int32_t dtype;    /* SLA_B200_BF16 | SLA_B200_F32       */
+  int32_t mask_precision; /* SLA_B200_MASK_*              */
+  uint32_t flags;   /* SLA_B200_FLAG_*                    */
+} sla_b200_problem;
+
+/* Per-call execution summary (the device analogue of ExecCounters, forward.hpp:46-50). */
+typedef struct sla_b200_info {
+  int32_t path;              /* 0 = generic SIMT kernels, 1 = tcgen05 fast path         */
+  int32_t n1, n_neg;         /* per-row class counts of the dynamic mask (mask.cpp:98-101) */
+  int32_t t_m, t_n;
+  int64_t gpu_launches;      /* kernels launched by the last call on this thread        */
+} sla_b200_info;
+
+/* Thread-local message of the last non-OK status; carries the reference's fragments. */
+const char* sla_b200_last_error(void);
+int sla_b200_abi_version(void);
+
+/* make_block_layout + validate_config (+ kernel support limits). */
+int sla_b200_validate(const sla_b200_problem* p);
+
+/* Bytes of the persistent forward->backward state and of the scratch workspace. */
+int sla_b200_sizes(const sla_b200_problem* p, size_t* state_bytes, size_t* workspace_bytes);
+
+/* Info about how a problem will run (no device work). */
+int sla_b200_query(const sla_b200_problem* p, sla_b200_info* info);
+int64_t sla_b200_last_launch_count(void);
+
+/* K1+K2: block classification of Q, K (predict_compressed_weights + classify_mask).
+ * labels: [B*H, T_m, T_n] int8 in {-1,0,1}.  p_c: optional [B*H, T_m, T_n] f64 weights. */
+int sla_b200_classify(const sla_b200_problem* p, const void* q, const void* k, int8_t* labels,
+                      double* p_c, void* state, void* workspace, void* stream);
+
+/* Fused forward.  mask_in == NULL: dynamic mask from q, k (sla_forward); else the given
+ * label grid (sla_forward_with_mask; rows may have zero critical blocks).
+ * w may be NULL (then o may be NULL): projection skipped.  Outputs o = o_s + o_l W,
+ * o_s (sparse branch), o_l (linear branch) in p->dtype; lse f32 [B*H, N] with the
+ * reference sentinel -1e30 on rows without critical mass.  Any of o/o_s/o_l may be NULL
+ * only if the caller will not run the backward. */
+int sla_b200_forward(const sla_b200_problem* p, const void* q, const void* k, const void* v,
+                     const void* w, const int8_t* mask_in, void* o, void* o_s, void* o_l,
+                     float* lse, void* state, void* workspace, void* stream);
+
+/* Fused backward of O = O^s + O^l W from the combined cotangent d_out
+ * (proj_backward + sla_backward).  dq, dk are the composed totals dq_total / dk_total
+ * (backward.cpp:211-214); dv accumulates both branches; dw f32 [H, d, d]. */
+int sla_b200_backward(const sla_b200_problem* p, const void* q, const void* k, const void* v,
+                      const void* w, const void* o_s, const void* o_l, const float* lse,
+                      const void* d_out, void* dq, void* dk, void* dv, float* dw,
+                      const void* state, void* workspace, void* stream);
+
+/* Optional component gradients of SlaGradients (backward.hpp:10-16), f32 [B*H, N, d]. */
+typedef struct sla_b200_grad_parts {
+  float* dq_sparse;  /* SlaGradients::dq      */
+  float* dk_sparse;  /* SlaGradients::dk      */
+  float* dq_feat;    /* SlaGradients::dq_feat */
+  float* dk_feat;    /* SlaGradients::dk_feat */
+} sla_b200_grad_parts;
+
+int sla_b200_backward_ex(const sla_b200_problem* p, const void* q, const void* k,
+                         const void* v, const void* w, const void* o_s, const void* o_l,
+                         const float* lse, const void* d_out, void* dq, void* dk, void* dv,
+                         float* dw, const sla_b200_grad_parts* parts, const void* state,
+                         void* workspace, void* stream);
+
+/* Per-kernel CUDA-event profiler of this library's own launches (bench/diagnostics).
+ * sla_b200_profiler(1) clears and enables, (0) disables.  The report is text lines
+ * "<kernel> <total_ms> <launches>"; returns the bytes needed (including the NUL). */
+int sla_b200_profiler(int enable);
+size_t sla_b200_profiler_report(char* buf, size_t len);
+
+/* Device pointer to the int8 label grid held in `state` after classify/forward. */
+int sla_b200_state_labels(const sla_b200_problem* p, const void* state, const int8_t** labels);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SLA_B200_H */

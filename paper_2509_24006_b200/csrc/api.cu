@@ -1,0 +1,308 @@
+// api.cu -- the extern "C" boundary (include/sla_b200.h): validation with the reference's
+// messages, buffer carving, path dispatch, error mapping to the reference's exception
+// classes (status 2 = std::invalid_argument, 1 = std::runtime_error).
+#include <cmath>
+#include <cstdio>
+#include <string>
+
+#include "../../include/sla_b200.h"
+#include "buffers.hpp"
+#include "kernels.hpp"
+
+namespace slab {
+
+thread_local std::string g_last_error;
+thread_local long long g_launches = 0;
+void count_launch(int n) { g_launches += n; }
+
+namespace {
+
+size_t round_half_up(double x) { return size_t(std::floor(x + 0.5)); }
+
+// make_block_layout (layout.cpp:8-26) + validate_config (config.cpp:7-19) + support limits
+Dims resolve(const sla_b200_problem* p) {
+  if (!p) throw InvalidArgument("sla_b200: null problem");
+  if (p->batch < 1 || p->heads < 1) throw InvalidArgument("sla_b200: batch and heads must be >= 1");
+  if (p->n <= 0 || p->d <= 0 || p->b_q <= 0 || p->b_kv <= 0)
+    throw InvalidArgument("make_block_layout: all sizes must be positive");
+  if (p->n % p->b_q != 0)
+    throw InvalidArgument("make_block_layout: b_q=" + std::to_string(p->b_q) +
+                          " does not divide N=" + std::to_string(p->n));
+  if (p->n % p->b_kv != 0)
+    throw InvalidArgument("make_block_layout: b_kv=" + std::to_string(p->b_kv) +
+                          " does not divide N=" + std::to_string(p->n));
+  if (!(p->k_h > 0.0 && p->k_h <= 100.0)) throw InvalidArgument("config: k_h must be in (0, 100]");
+  if (!(p->k_l >= 0.0 && p->k_l < 100.0)) throw InvalidArgument("config: k_l must be in [0, 100)");
+  if (p->k_h + p->k_l > 100.0) throw InvalidArgument("config: k_h + k_l must be <= 100");
+  if (p->phi < 0 || p->phi > 2) throw InvalidArgument("unknown feature map");
+  if (p->dtype != SLA_B200_BF16 && p->dtype != SLA_B200_F32)
+    throw InvalidArgument("unknown dtype");
+  if (p->mask_precision != SLA_B200_MASK_F64 && p->mask_precision != SLA_B200_MASK_F32)
+    throw InvalidArgument("unknown mask precision");
+  Dims D{};
+  D.B = p->batch;
+  D.H = p->heads;
+  D.U = p->batch * p->heads;
+  D.N = p->n;
+  D.d = int(p->d);
+  D.bq = int(p->b_q);
+  D.bkv = int(p->b_kv);
+  D.Tm = int(p->n / p->b_q);
+  D.Tn = int(p->n / p->b_kv);
+  D.phi = p->phi;
+  if (D.Tn > 8192 || D.Tm > 65535)
+    throw InvalidArgument("sla_b200: at most 8192 key blocks per row are supported");
+  if (p->d > 1024) throw InvalidArgument("sla_b200: d > 1024 is not supported");
+  // mask.cpp:98-101
+  size_t n1 = std::max<size_t>(1, round_half_up(p->k_h * double(D.Tn) / 100.0));
+  n1 = std::min<size_t>(n1, size_t(D.Tn));
+  size_t nn = round_half_up(p->k_l * double(D.Tn) / 100.0);
+  nn = std::min<size_t>(nn, size_t(D.Tn) - n1);
+  D.n1 = int(n1);
+  D.n_neg = int(nn);
+  D.scale_f = 1.0f / sqrtf(float(D.d));
+  D.inv_sqrt_d = 1.0 / std::sqrt(double(D.d));
+  if (classify_smem_bytes(D, p->mask_precision == 0) > 227 * 1024)
+    throw InvalidArgument("sla_b200: too many key blocks for the classification kernel");
+  return D;
+}
+
+bool use_fast(const sla_b200_problem* p, const Dims& D) {
+  return !(p->flags & SLA_B200_FLAG_GENERIC) && fast_supported(D, p->dtype);
+}
+
+void require_supported(const sla_b200_problem* p, const Dims& D) {
+  if (use_fast(p, D)) return;
+  std::string why;
+  if (!generic_supported(D, &why)) throw InvalidArgument(why);
+}
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    g_last_error.clear();
+    g_launches = 0;
+    f();
+    return SLA_B200_OK;
+  } catch (const InvalidArgument& e) {
+    g_last_error = e.msg;
+    return SLA_B200_ERR_INVALID;
+  } catch (const RuntimeFailure& e) {
+    g_last_error = e.msg;
+    return SLA_B200_ERR_RUNTIME;
+  } catch (const CudaError& e) {
+    g_last_error = "sla_b200: CUDA error: " + e.msg;
+    return SLA_B200_ERR_RUNTIME;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return SLA_B200_ERR_RUNTIME;
+  }
+}
+
+void buffers(const sla_b200_problem* p, const Dims& D, const void* state, void* work,
+             StateBufs& s, WorkBufs& w) {
+  if (!state || !work) throw InvalidArgument("sla_b200: state and workspace are required");
+  const bool fast = use_fast(p, D);
+  carve_state(D, fast, const_cast<void*>(state), s, nullptr);
+  carve_work(D, fast, work, w, nullptr);
+}
+
+long long read_slot(long long* slot, cudaStream_t st) {
+  long long v = 0;
+  SLAB_CUDA(cudaMemcpyAsync(&v, slot, sizeof(v), cudaMemcpyDeviceToHost, st));
+  SLAB_CUDA(cudaStreamSynchronize(st));
+  return v;
+}
+
+void reset_slot(long long* slot, cudaStream_t st) {
+  const long long big = LLONG_MAX;
+  SLAB_CUDA(cudaMemcpyAsync(slot, &big, sizeof(big), cudaMemcpyHostToDevice, st));
+}
+
+// forward.cpp:15-25 check_input: "<name> has non-finite entry at (r, c)"
+void check_inputs(const sla_b200_problem* p, const Dims& D, const WorkBufs& w,
+                  std::initializer_list<std::pair<const char*, const void*>> xs, cudaStream_t st) {
+  for (auto& [name, x] : xs) {
+    reset_slot(w.err, st);
+    launch_check_finite(D, p->dtype, x, w.err, st);
+    const long long bad = read_slot(w.err, st);
+    if (bad != LLONG_MAX) {
+      const long long per = D.N * D.d;
+      const long long u = bad / per, rc = bad % per;
+      std::string msg = std::string("sla_forward: ") + name + " has non-finite entry at (" +
+                        std::to_string(rc / D.d) + ", " + std::to_string(rc % D.d) + ")";
+      if (D.U > 1) msg += " in unit " + std::to_string(u);
+      throw InvalidArgument(msg);
+    }
+  }
+}
+
+void classify_into_state(const sla_b200_problem* p, const Dims& D, const void* q, const void* k,
+                         const int8_t* mask_in, double* p_c, const StateBufs& s,
+                         const WorkBufs& w, cudaStream_t st) {
+  if (mask_in) {
+    const size_t bytes = size_t(D.U) * D.Tm * D.Tn;
+    if (mask_in != s.labels)
+      SLAB_CUDA(cudaMemcpyAsync(s.labels, mask_in, bytes, cudaMemcpyDeviceToDevice, st));
+    const bool check = p->flags & SLA_B200_FLAG_CHECK_FINITE;
+    if (check) reset_slot(w.err + 1, st);
+    launch_build_lut(D, s, check ? w.err + 1 : nullptr, st);
+    if (check && read_slot(w.err + 1, st) != LLONG_MAX)
+      throw InvalidArgument("build_lookup: label must be -1, 0 or 1");
+  } else {
+    launch_classify(D, p->dtype, p->mask_precision, q, k, s, w, p_c, st);
+  }
+}
+
+}  // namespace
+}  // namespace slab
+
+using namespace slab;
+
+extern "C" {
+
+const char* sla_b200_last_error(void) { return g_last_error.c_str(); }
+int sla_b200_abi_version(void) { return SLA_B200_ABI_VERSION; }
+int64_t sla_b200_last_launch_count(void) { return g_launches; }
+
+int sla_b200_validate(const sla_b200_problem* p) {
+  return guarded([&] {
+    const Dims D = resolve(p);
+    require_supported(p, D);
+  });
+}
+
+int sla_b200_sizes(const sla_b200_problem* p, size_t* state_bytes, size_t* workspace_bytes) {
+  return guarded([&] {
+    const Dims D = resolve(p);
+    require_supported(p, D);
+    StateBufs s;
+    WorkBufs w;
+    const bool fast = use_fast(p, D);
+    carve_state(D, fast, nullptr, s, state_bytes);
+    carve_work(D, fast, nullptr, w, workspace_bytes);
+  });
+}
+
+int sla_b200_query(const sla_b200_problem* p, sla_b200_info* info) {
+  return guarded([&] {
+    const Dims D = resolve(p);
+    require_supported(p, D);
+    if (!info) return;
+    info->path = use_fast(p, D) ? 1 : 0;
+    info->n1 = D.n1;
+    info->n_neg = D.n_neg;
+    info->t_m = D.Tm;
+    info->t_n = D.Tn;
+    info->gpu_launches = g_launches;
+  });
+}
+
+int sla_b200_classify(const sla_b200_problem* p, const void* q, const void* k, int8_t* labels,
+                      double* p_c, void* state, void* workspace, void* stream) {
+  return guarded([&] {
+    const Dims D = resolve(p);
+    require_supported(p, D);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    prof_mark("", st);
+    StateBufs s;
+    WorkBufs w;
+    buffers(p, D, state, workspace, s, w);
+    if (p->flags & SLA_B200_FLAG_CHECK_FINITE) check_inputs(p, D, w, {{"Q", q}, {"K", k}}, st);
+    launch_classify(D, p->dtype, p->mask_precision, q, k, s, w, p_c, st);
+    if (labels && labels != s.labels)
+      SLAB_CUDA(cudaMemcpyAsync(labels, s.labels, size_t(D.U) * D.Tm * D.Tn,
+                                cudaMemcpyDeviceToDevice, st));
+  });
+}
+
+int sla_b200_forward(const sla_b200_problem* p, const void* q, const void* k, const void* v,
+                     const void* w, const int8_t* mask_in, void* o, void* o_s, void* o_l,
+                     float* lse, void* state, void* workspace, void* stream) {
+  return guarded([&] {
+    const Dims D = resolve(p);
+    require_supported(p, D);
+    if (!q || !k || !v || !lse) throw InvalidArgument("sla_forward: q, k, v and lse are required");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    prof_mark("", st);
+    StateBufs s;
+    WorkBufs wb;
+    buffers(p, D, state, workspace, s, wb);
+    const bool check = p->flags & SLA_B200_FLAG_CHECK_FINITE;
+    if (check) check_inputs(p, D, wb, {{"Q", q}, {"K", k}, {"V", v}}, st);
+    classify_into_state(p, D, q, k, mask_in, nullptr, s, wb, st);
+    if (use_fast(p, D))
+      fast_forward(D, q, k, v, w, o, o_s, o_l, lse, s, wb, st);
+    else
+      generic_forward(D, p->dtype, q, k, v, w, o, o_s, o_l, lse, s, wb, st);
+    if (check) {  // forward.cpp:164-170
+      const long long per = D.N * D.d;
+      for (const void* out : {static_cast<const void*>(o_s), static_cast<const void*>(o_l)}) {
+        if (!out) continue;
+        reset_slot(wb.err, st);
+        launch_check_finite(D, p->dtype, out, wb.err, st);
+        const long long bad = read_slot(wb.err, st);
+        if (bad != LLONG_MAX) {
+          const long long r = (bad % per) / D.d, c = bad % D.d;
+          throw RuntimeFailure("sla_forward: non-finite output at row " + std::to_string(r) +
+                               ", col " + std::to_string(c) + " (block row " +
+                               std::to_string(r / D.bq) + ")");
+        }
+      }
+    }
+  });
+}
+
+int sla_b200_backward_ex(const sla_b200_problem* p, const void* q, const void* k,
+                         const void* v, const void* w, const void* o_s, const void* o_l,
+                         const float* lse, const void* d_out, void* dq, void* dk, void* dv,
+                         float* dw, const sla_b200_grad_parts* parts, const void* state,
+                         void* workspace, void* stream) {
+  return guarded([&] {
+    const Dims D = resolve(p);
+    require_supported(p, D);
+    if (!q || !k || !v || !w || !o_s || !o_l || !lse || !d_out || !dq || !dk || !dv || !dw)
+      throw InvalidArgument("sla_backward: all tensors are required");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    prof_mark("", st);
+    StateBufs s;
+    WorkBufs wb;
+    buffers(p, D, state, workspace, s, wb);
+    const bool fast = use_fast(p, D);
+    if (fast)
+      fast_backward(D, q, k, v, w, o_s, o_l, lse, d_out, dq, dk, dv, dw, s, wb, st);
+    else
+      generic_backward(D, p->dtype, q, k, v, w, o_s, o_l, lse, d_out, dq, dk, dv, dw, s, wb, st);
+    if (parts) {
+      const size_t bytes = sizeof(float) * size_t(D.U) * D.N * D.d;
+      auto cp = [&](float* dst, const float* src) {
+        if (!dst) return;
+        if (!src) throw InvalidArgument("sla_backward: gradient part unavailable on this path");
+        SLAB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st));
+      };
+      cp(parts->dq_sparse, wb.dq);
+      cp(parts->dk_sparse, wb.dk);
+      cp(parts->dq_feat, wb.dqf);
+      cp(parts->dk_feat, wb.dkf);
+    }
+  });
+}
+
+int sla_b200_backward(const sla_b200_problem* p, const void* q, const void* k, const void* v,
+                      const void* w, const void* o_s, const void* o_l, const float* lse,
+                      const void* d_out, void* dq, void* dk, void* dv, float* dw,
+                      const void* state, void* workspace, void* stream) {
+  return sla_b200_backward_ex(p, q, k, v, w, o_s, o_l, lse, d_out, dq, dk, dv, dw, nullptr,
+                              state, workspace, stream);
+}
+
+int sla_b200_state_labels(const sla_b200_problem* p, const void* state, const int8_t** labels) {
+  return guarded([&] {
+    const Dims D = resolve(p);
+    StateBufs s;
+    carve_state(D, use_fast(p, D), const_cast<void*>(state), s, nullptr);
+    if (labels) *labels = s.labels;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,323 @@
+// classify.cu -- K1+K2: block pooling, compressed-weight prediction and three-way block
+// classification, plus the lookup structures every later kernel iterates.
+//
+// Reference: mask.cpp:40-153 (pool_mean, predict_compressed_weights, classify_mask,
+// build_lookup), forward.cpp:174-185 (the mask is computed in f64 on every path).
+//
+// HBM-bound: Q and K are each read once (vectorised over d, coalesced across threads);
+// everything after pooling works on T x d / T x T data that lives in L2.
+#include <cfloat>
+
+#include "buffers.hpp"
+#include "kernels.hpp"
+
+namespace slab {
+
+// ---------------------------------------------------------------------------------------
+// K0: first non-finite entry (forward.cpp:15-25 check_input), flat index via atomicMin.
+// ---------------------------------------------------------------------------------------
+template <typename In>
+__global__ void k_check_finite(const In* __restrict__ x, long long total,
+                               long long* __restrict__ slot) {
+  long long first = LLONG_MAX;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    if (!isfinite(to_f(x[i]))) {
+      first = i;
+      break;
+    }
+  }
+  if (first != LLONG_MAX) atomicMin(slot, first);
+}
+
+// ---------------------------------------------------------------------------------------
+// K1a: block means (mask.cpp:40-55): ascending row sum, then one division, in R.
+// grid (T, U), threads over the d columns (coalesced).
+// ---------------------------------------------------------------------------------------
+template <typename R, typename In>
+__global__ void k_pool(const In* __restrict__ x, R* __restrict__ out, long long N, int d, int b,
+                       int T) {
+  const long long u = blockIdx.y;
+  const int g = blockIdx.x;
+  const In* base = x + (u * N + (long long)g * b) * d;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    R acc = R(0);
+    for (int r = 0; r < b; ++r) acc = add_rn(acc, R(to_f(base[(long long)r * d + c])));
+    out[(u * T + g) * d + c] = div_rn(acc, R(b));
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// K1b+K2: one CTA per (unit, block row).  Scores in R with the reference's operation order
+// (matmul_nt ascending-k dot, mat.hpp:83-97; then * 1/sqrt(d)), max-shifted softmax with
+// the ascending-j normaliser (mask.cpp:65-79), then a bitonic sort of
+// (weight desc, column asc) -- exactly std::stable_sort's order from an iota start
+// (mask.cpp:105-113) -- and the label / lookup writes (mask.cpp:114-153).
+// ---------------------------------------------------------------------------------------
+template <typename R>
+__device__ __forceinline__ bool before(R ka, int ia, R kb, int ib) {
+  return ka > kb || (ka == kb && ia < ib);
+}
+
+template <typename R>
+__global__ void k_classify(const R* __restrict__ pq, const R* __restrict__ pk, int d, int Tm,
+                           int Tn, int P2, int n1, int n_neg, R inv_sqrt_d,
+                           int8_t* __restrict__ labels, int* __restrict__ crit_cnt,
+                           int* __restrict__ crit_idx, int* __restrict__ marg_cnt,
+                           double* __restrict__ p_c_out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  R* key = reinterpret_cast<R*>(smem_raw);                   // [P2]
+  R* qrow = key + P2;                                         // [d]
+  int* idx = reinterpret_cast<int*>(qrow + d);                // [P2]
+  int8_t* lab = reinterpret_cast<int8_t*>(idx + P2);          // [Tn]
+  __shared__ R red[32];
+
+  const long long u = blockIdx.y;
+  const int i = blockIdx.x;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const R* pku = pk + u * (long long)Tn * d;
+  for (int c = tid; c < d; c += nt) qrow[c] = pq[(u * Tm + i) * d + c];
+  __syncthreads();
+
+  // scores
+  R lmax = -R(INFINITY);
+  for (int j = tid; j < Tn; j += nt) {
+    const R* kr = pku + (long long)j * d;
+    R acc = R(0);
+    for (int c = 0; c < d; ++c) acc = add_rn(acc, mul_rn(qrow[c], kr[c]));
+    const R s = mul_rn(acc, inv_sqrt_d);
+    key[j] = s;
+    lmax = s > lmax ? s : lmax;
+  }
+  // block max (order-independent, exact)
+  for (int o = 16; o > 0; o >>= 1) {
+    const R other = __shfl_xor_sync(0xffffffffu, lmax, o);
+    lmax = other > lmax ? other : lmax;
+  }
+  if ((tid & 31) == 0) red[tid >> 5] = lmax;
+  __syncthreads();
+  if (tid == 0) {
+    R m = red[0];
+    for (int w = 1; w < (nt + 31) / 32; ++w) m = red[w] > m ? red[w] : m;
+    red[0] = m;
+  }
+  __syncthreads();
+  const R m = red[0];
+  for (int j = tid; j < Tn; j += nt) key[j] = exp_r(key[j] - m);
+  __syncthreads();
+  if (tid == 0) {  // the reference's sequential normaliser (mask.cpp:73-77)
+    R sum = R(0);
+    for (int j = 0; j < Tn; ++j) sum = add_rn(sum, key[j]);
+    red[1] = sum;
+  }
+  __syncthreads();
+  const R sum = red[1];
+  for (int j = tid; j < P2; j += nt) {
+    if (j < Tn) {
+      key[j] = div_rn(key[j], sum);
+      if (p_c_out) p_c_out[(u * Tm + i) * Tn + j] = double(key[j]);
+    } else {
+      key[j] = -R(1);  // pads sort after every weight (weights are >= 0)
+    }
+    idx[j] = j;
+  }
+  __syncthreads();
+
+  // bitonic sort into before-order
+  for (int k = 2; k <= P2; k <<= 1) {
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      for (int t = tid; t < P2; t += nt) {
+        const int x = t ^ jj;
+        if (x > t) {
+          const R ka = key[t], kb = key[x];
+          const int ia = idx[t], ib = idx[x];
+          const bool t_first = before(ka, ia, kb, ib);
+          const bool up = (t & k) == 0;
+          if (up ? !t_first : t_first) {
+            key[t] = kb;
+            key[x] = ka;
+            idx[t] = ib;
+            idx[x] = ia;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int r = tid; r < Tn; r += nt) {
+    const int j = idx[r];
+    lab[j] = r < n1 ? int8_t(1) : (r >= Tn - n_neg ? int8_t(-1) : int8_t(0));
+  }
+  __syncthreads();
+  int8_t* lrow = labels + (u * Tm + i) * (long long)Tn;
+  for (int j = tid; j < Tn; j += nt) lrow[j] = lab[j];
+  // ascending critical list + marginal count (warp 0)
+  if (tid < 32) {
+    int base = 0, marg = 0;
+    int* crow = crit_idx + (u * Tm + i) * (long long)Tn;
+    for (int j0 = 0; j0 < Tn; j0 += 32) {
+      const int j = j0 + tid;
+      const int l = j < Tn ? lab[j] : -1;
+      const unsigned bc = __ballot_sync(0xffffffffu, l == 1);
+      const unsigned bm = __ballot_sync(0xffffffffu, l == 0);
+      if (l == 1) crow[base + __popc(bc & ((1u << tid) - 1u))] = j;
+      base += __popc(bc);
+      marg += __popc(bm);
+    }
+    if (tid == 0) {
+      crit_cnt[u * Tm + i] = base;
+      marg_cnt[u * Tm + i] = marg;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// build_lookup for an injected label grid (mask.cpp:121-153); flags invalid labels.
+// ---------------------------------------------------------------------------------------
+__global__ void k_build_lut(const int8_t* __restrict__ labels, int Tm, int Tn,
+                            int* __restrict__ crit_cnt, int* __restrict__ crit_idx,
+                            int* __restrict__ marg_cnt, long long* __restrict__ bad) {
+  const int i = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= Tm) return;
+  const long long row = (long long)blockIdx.y * Tm + i;
+  const int8_t* lrow = labels + row * Tn;
+  int* crow = crit_idx + row * Tn;
+  int base = 0, marg = 0;
+  for (int j0 = 0; j0 < Tn; j0 += 32) {
+    const int j = j0 + lane;
+    const int l = j < Tn ? lrow[j] : -1;
+    if (j < Tn && (l < -1 || l > 1) && bad) atomicMin(bad, row * Tn + j);
+    const unsigned bc = __ballot_sync(0xffffffffu, l == 1);
+    const unsigned bm = __ballot_sync(0xffffffffu, l == 0);
+    if (l == 1) crow[base + __popc(bc & ((1u << lane) - 1u))] = j;
+    base += __popc(bc);
+    marg += __popc(bm);
+  }
+  if (lane == 0) {
+    crit_cnt[row] = base;
+    marg_cnt[row] = marg;
+  }
+}
+
+// Transposed critical lists (backward.cpp:133-137): per column, ascending rows.
+__global__ void k_build_csc(const int8_t* __restrict__ labels, int Tm, int Tn,
+                            int* __restrict__ ccol_cnt, int* __restrict__ ccol_idx) {
+  const long long u = blockIdx.y;
+  const int j = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (j >= Tn) return;
+  const int8_t* lu = labels + u * (long long)Tm * Tn;
+  int* out = ccol_idx + (u * Tn + j) * (long long)Tm;
+  int base = 0;
+  for (int i0 = 0; i0 < Tm; i0 += 32) {
+    const int i = i0 + lane;
+    const bool c = i < Tm && lu[(long long)i * Tn + j] == 1;
+    const unsigned b = __ballot_sync(0xffffffffu, c);
+    if (c) out[base + __popc(b & ((1u << lane) - 1u))] = i;
+    base += __popc(b);
+  }
+  if (lane == 0) ccol_cnt[u * Tn + j] = base;
+}
+
+// Marginal indicator as a bf16 0/1 matrix: the A operand of H = M0 h (fast path).
+__global__ void k_build_m0(const int8_t* __restrict__ labels, long long total,
+                           __nv_bfloat16* __restrict__ m0) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x)
+    m0[e] = __float2bfloat16_rn(labels[e] == 0 ? 1.f : 0.f);
+}
+
+// ---------------------------------------------------------------------------------------
+// host launchers
+// ---------------------------------------------------------------------------------------
+static int next_pow2(int x) {
+  int p = 1;
+  while (p < x) p <<= 1;
+  return p;
+}
+
+size_t classify_smem_bytes(const Dims& D, bool f64) {
+  const int P2 = next_pow2(D.Tn);
+  const size_t rs = f64 ? 8 : 4;
+  return rs * (P2 + D.d) + 4 * size_t(P2) + size_t(D.Tn) + 16;
+}
+
+template <typename In>
+static void check_finite_t(const In* x, long long total, long long* slot, cudaStream_t st) {
+  const int blocks = int(std::min<long long>((total + 255) / 256, 148 * 16));
+  k_check_finite<In><<<blocks, 256, 0, st>>>(x, total, slot);
+  check_launch("k_check_finite", st);
+}
+
+void launch_check_finite(const Dims& D, int dtype, const void* x, long long* slot,
+                         cudaStream_t st) {
+  const long long total = D.U * D.N * D.d;
+  if (dtype == 0)
+    check_finite_t(static_cast<const __nv_bfloat16*>(x), total, slot, st);
+  else
+    check_finite_t(static_cast<const float*>(x), total, slot, st);
+}
+
+template <typename R, typename In>
+static void classify_t(const Dims& D, const In* q, const In* k, const StateBufs& s,
+                       const WorkBufs& w, double* p_c, cudaStream_t st) {
+  R* pq = reinterpret_cast<R*>(w.pq);
+  R* pk = reinterpret_cast<R*>(w.pk);
+  const int pt = D.d < 256 ? ((D.d + 31) / 32) * 32 : 256;
+  k_pool<R, In><<<dim3(D.Tm, unsigned(D.U)), pt, 0, st>>>(q, pq, D.N, D.d, D.bq, D.Tm);
+  check_launch("k_pool(q)", st);
+  k_pool<R, In><<<dim3(D.Tn, unsigned(D.U)), pt, 0, st>>>(k, pk, D.N, D.d, D.bkv, D.Tn);
+  check_launch("k_pool(k)", st);
+  const size_t smem = classify_smem_bytes(D, sizeof(R) == 8);
+  if (smem > 48 * 1024)
+    SLAB_CUDA(cudaFuncSetAttribute(k_classify<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   int(smem)));
+  k_classify<R><<<dim3(D.Tm, unsigned(D.U)), 256, smem, st>>>(
+      pq, pk, D.d, D.Tm, D.Tn, next_pow2(D.Tn), D.n1, D.n_neg, R(D.inv_sqrt_d), s.labels,
+      s.crit_cnt, s.crit_idx, s.marg_cnt, p_c);
+  check_launch("k_classify", st);
+}
+
+void launch_classify(const Dims& D, int dtype, int mask_precision, const void* q, const void* k,
+                     const StateBufs& s, const WorkBufs& w, double* p_c, cudaStream_t st) {
+  // the f32 variant computes 1/sqrt(d) in f32 as well
+  if (dtype == 0) {
+    auto qb = static_cast<const __nv_bfloat16*>(q);
+    auto kb = static_cast<const __nv_bfloat16*>(k);
+    if (mask_precision == 0)
+      classify_t<double>(D, qb, kb, s, w, p_c, st);
+    else
+      classify_t<float>(D, qb, kb, s, w, p_c, st);
+  } else {
+    auto qf = static_cast<const float*>(q);
+    auto kf = static_cast<const float*>(k);
+    if (mask_precision == 0)
+      classify_t<double>(D, qf, kf, s, w, p_c, st);
+    else
+      classify_t<float>(D, qf, kf, s, w, p_c, st);
+  }
+}
+
+void launch_build_lut(const Dims& D, const StateBufs& s, long long* bad, cudaStream_t st) {
+  const int warps = 8;
+  k_build_lut<<<dim3((D.Tm + warps - 1) / warps, unsigned(D.U)), 32 * warps, 0, st>>>(
+      s.labels, D.Tm, D.Tn, s.crit_cnt, s.crit_idx, s.marg_cnt, bad);
+  check_launch("k_build_lut", st);
+}
+
+void launch_build_csc(const Dims& D, const StateBufs& s, cudaStream_t st) {
+  const int warps = 8;
+  k_build_csc<<<dim3((D.Tn + warps - 1) / warps, unsigned(D.U)), 32 * warps, 0, st>>>(
+      s.labels, D.Tm, D.Tn, s.ccol_cnt, s.ccol_idx);
+  check_launch("k_build_csc", st);
+}
+
+void launch_build_m0(const Dims& D, const StateBufs& s, cudaStream_t st) {
+  const long long total = D.U * (long long)D.Tm * D.Tn;
+  const int blocks = int(std::min<long long>((total + 255) / 256, 148 * 8));
+  k_build_m0<<<blocks, 256, 0, st>>>(s.labels, total, s.M0);
+  check_launch("k_build_m0", st);
+}
+
+}  // namespace slab

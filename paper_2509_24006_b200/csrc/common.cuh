@@ -1,0 +1,97 @@
+// common.cuh -- shared device helpers and the problem descriptor used by every kernel.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+
+namespace slab {
+
+// Derived problem dimensions (resolved once on the host from sla_b200_problem).
+struct Dims {
+  int64_t U;     // units = batch * heads
+  int64_t B, H;  // batch, heads
+  int64_t N;     // sequence length
+  int d, bq, bkv;
+  int Tm, Tn;    // query / key-value block counts (layout.hpp:10-20)
+  int phi;       // 0 elu1, 1 relu, 2 softmax
+  int n1, n_neg; // per-row class counts of a dynamic mask (mask.cpp:98-101)
+  float scale_f; // T(1)/sqrt(T(d)) with T=float (block_ops.hpp:16)
+  double inv_sqrt_d;  // 1.0/sqrt(double(d)) (mask.cpp:63)
+};
+
+constexpr float kLseSentinel = -1e30f;  // forward.hpp:18-24 (f32)
+
+__device__ __forceinline__ float to_f(float x) { return x; }
+__device__ __forceinline__ float to_f(__nv_bfloat16 x) { return __bfloat162float(x); }
+template <typename T>
+__device__ __forceinline__ T from_f(float x);
+template <>
+__device__ __forceinline__ float from_f<float>(float x) { return x; }
+template <>
+__device__ __forceinline__ __nv_bfloat16 from_f<__nv_bfloat16>(float x) {
+  return __float2bfloat16_rn(x);
+}
+
+// IEEE round-to-nearest arithmetic that the compiler may not contract into FMA: the
+// reference is built for baseline x86-64 (no FMA), so every a*b+c rounds twice.
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double exp_r(double x) { return exp(x); }
+__device__ __forceinline__ float exp_r(float x) { return expf(x); }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// feature map phi (feature_map.cpp:24-40), elementwise kinds
+__device__ __forceinline__ float phi_elem(int phi, float x) {
+  return phi == 0 ? (x >= 0.f ? x + 1.f : expf(x)) : fmaxf(x, 0.f);
+}
+
+// host-side launch accounting (gpu_launches in bench.py comes from here) and the optional
+// per-kernel event profiler (profiler.cu)
+void count_launch(int n = 1);
+void prof_mark(const char* name, cudaStream_t st);
+
+#define SLAB_CUDA(call)                                                             \
+  do {                                                                              \
+    cudaError_t e_ = (call);                                                        \
+    if (e_ != cudaSuccess) throw ::slab::CudaError(std::string(#call) + ": " +      \
+                                                   cudaGetErrorString(e_));         \
+  } while (0)
+
+struct CudaError {
+  std::string msg;
+  explicit CudaError(std::string m) : msg(std::move(m)) {}
+};
+struct InvalidArgument {
+  std::string msg;
+  explicit InvalidArgument(std::string m) : msg(std::move(m)) {}
+};
+struct RuntimeFailure {
+  std::string msg;
+  explicit RuntimeFailure(std::string m) : msg(std::move(m)) {}
+};
+
+inline void check_launch(const char* what, cudaStream_t st) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+  count_launch();
+  prof_mark(what, st);
+}
+
+}  // namespace slab

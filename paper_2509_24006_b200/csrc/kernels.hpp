@@ -1,0 +1,38 @@
+// kernels.hpp -- host launchers of every kernel family (declared here, defined per .cu).
+#pragma once
+
+#include "buffers.hpp"
+
+namespace slab {
+
+// classify.cu
+size_t classify_smem_bytes(const Dims& D, bool f64);
+void launch_check_finite(const Dims& D, int dtype, const void* x, long long* slot,
+                         cudaStream_t st);
+void launch_classify(const Dims& D, int dtype, int mask_precision, const void* q, const void* k,
+                     const StateBufs& s, const WorkBufs& w, double* p_c, cudaStream_t st);
+void launch_build_lut(const Dims& D, const StateBufs& s, long long* bad, cudaStream_t st);
+void launch_build_csc(const Dims& D, const StateBufs& s, cudaStream_t st);
+void launch_build_m0(const Dims& D, const StateBufs& s, cudaStream_t st);
+
+// generic.cu -- shape-generic SIMT kernels (fp32 math, any b_q, b_kv, d within smem limits)
+bool generic_supported(const Dims& D, std::string* why);
+void generic_forward(const Dims& D, int dtype, const void* q, const void* k, const void* v,
+                     const void* w, void* o, void* o_s, void* o_l, float* lse,
+                     const StateBufs& s, const WorkBufs& wb, cudaStream_t st);
+void generic_backward(const Dims& D, int dtype, const void* q, const void* k, const void* v,
+                      const void* w, const void* o_s, const void* o_l, const float* lse,
+                      const void* d_out, void* dq, void* dk, void* dv, float* dw,
+                      const StateBufs& s, const WorkBufs& wb, cudaStream_t st);
+
+// fast path (tcgen05) -- b_q = b_kv = 64, d in {64, 128}, bf16
+bool fast_supported(const Dims& D, int dtype);
+void fast_forward(const Dims& D, const void* q, const void* k, const void* v, const void* w,
+                  void* o, void* o_s, void* o_l, float* lse, const StateBufs& s,
+                  const WorkBufs& wb, cudaStream_t st);
+void fast_backward(const Dims& D, const void* q, const void* k, const void* v, const void* w,
+                   const void* o_s, const void* o_l, const float* lse, const void* d_out,
+                   void* dq, void* dk, void* dv, float* dw, const StateBufs& s,
+                   const WorkBufs& wb, cudaStream_t st);
+
+}  // namespace slab
