@@ -1,0 +1,266 @@
+// gemm.cu -- batched bf16 tcgen05 GEMM, the workhorse of the linear (marginal) branch:
+//   H   = M0 . h        (aggregation.cpp:40-56 as a GEMM; M0 is the 0/1 marginal indicator)
+//   h_j = phi(K_j)^T V_j (summaries.cpp:17-42, batched over key blocks)
+//   dH_agg = M0^T . dH  (backward.cpp:170-178)
+// C[b] = A[b] . B[b] with A either K-major ([M][K] rows) or M-major ([K][M] rows) and
+// B either N-major ([K][N] rows) or K-major ([N][K] rows); fp32 accumulate in TMEM.
+//
+// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = MMA issuer (one elected
+// thread), warps 2-5 = epilogue (TMEM -> registers -> global).  4-stage smem ring with
+// full/empty mbarriers; the accumulator lives in TMEM (BN columns).
+#include <cstdio>
+
+#include "kernels.hpp"
+#include "tc.cuh"
+
+namespace slab {
+
+namespace {
+
+constexpr int kStages = 4;
+constexpr int kBK = 64;  // K elements per stage (one 128-byte swizzle row of bf16)
+
+template <int BM, int BN>
+struct GemmSmem {
+  static constexpr int kA = BM * kBK * 2;
+  static constexpr int kB = BN * kBK * 2;
+  static constexpr int kStage = kA + kB;
+  static constexpr int kBytes = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+template <int BM, int BN, bool A_MN, bool B_MN, typename OutT>
+__global__ void __launch_bounds__(192, 1)
+    k_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+           OutT* __restrict__ C, int M, int N, int K, long long c_batch, int ldc) {
+  using L = GemmSmem<BM, BN>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * L::kStage);
+  uint64_t* empty = full + kStages;
+  uint64_t* done = empty + kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, b = blockIdx.z;
+  const int nk = K / kBK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::tma_prefetch(&ta);
+      tc::tma_prefetch(&tb);
+      for (int s = 0; s < kStages; ++s) {
+        tc::mbar_init(&full[s], 1);
+        tc::mbar_init(&empty[s], 1);
+      }
+      tc::mbar_init(done, 1);
+      tc::fence_barrier_init();
+    }
+    __syncwarp();
+    tc::tmem_alloc<BN>(tmem_slot);
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % kStages;
+        const uint32_t ph = (kb / kStages) & 1;
+        tc::mbar_wait(&empty[s], ph ^ 1);
+        uint8_t* sa = smem + s * L::kStage;
+        uint8_t* sb = sa + L::kA;
+        tc::mbar_expect_tx(&full[s], L::kStage);
+        const int k0 = kb * kBK;
+        if (A_MN) {
+#pragma unroll
+          for (int c = 0; c < BM / 64; ++c) tc::tma_load_3d(sa + c * 8192, &ta, &full[s], m0 + 64 * c, k0, b);
+        } else {
+          tc::tma_load_3d(sa, &ta, &full[s], k0, m0, b);
+        }
+        if (B_MN) {
+#pragma unroll
+          for (int c = 0; c < BN / 64; ++c) tc::tma_load_3d(sb + c * 8192, &tb, &full[s], n0 + 64 * c, k0, b);
+        } else {
+          tc::tma_load_3d(sb, &tb, &full[s], k0, n0, b);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, A_MN, B_MN);
+    for (int kb = 0; kb < nk; ++kb) {
+      const int s = kb % kStages;
+      const uint32_t ph = (kb / kStages) & 1;
+      tc::mbar_wait(&full[s], ph);
+      tc::tc_fence_after();
+      if (lane == 0) {
+        const uint32_t sa = tc::smem_u32(smem + s * L::kStage);
+        const uint32_t sb = sa + L::kA;
+#pragma unroll
+        for (int kk = 0; kk < kBK / 16; ++kk) {
+          const uint64_t ad = A_MN ? tc::desc_mnmajor(sa + kk * 2048, 8192) : tc::desc_kmajor(sa + kk * 32);
+          const uint64_t bd = B_MN ? tc::desc_mnmajor(sb + kk * 2048, 8192) : tc::desc_kmajor(sb + kk * 32);
+          tc::mma_bf16(tmem, ad, bd, idesc, (kb | kk) != 0);
+        }
+        tc::mma_commit(&empty[s]);
+        if (kb == nk - 1) tc::mma_commit(done);
+      }
+      __syncwarp();
+    }
+  } else {
+    // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
+    const int q = warp & 3;
+    tc::mbar_wait(done, 0);
+    tc::tc_fence_after();
+    const int row = BM == 128 ? 32 * q + lane : 16 * q + lane;
+    const bool live = (BM == 128 || lane < 16) && (m0 + row) < M;
+    OutT* crow = C + (long long)b * c_batch + (long long)(m0 + row) * ldc + n0;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      uint32_t r[32];
+      tc::tmem_ld32(tmem + (uint32_t(32 * q) << 16) + c0, r);
+      tc::tmem_ld_wait();
+      if (live) {
+        if constexpr (sizeof(OutT) == 4) {
+#pragma unroll
+          for (int e = 0; e < 32; e += 4)
+            *reinterpret_cast<float4*>(crow + c0 + e) =
+                make_float4(__uint_as_float(r[e]), __uint_as_float(r[e + 1]),
+                            __uint_as_float(r[e + 2]), __uint_as_float(r[e + 3]));
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; e += 8) {
+            uint4 v;
+            v.x = tc::pack_bf16(__uint_as_float(r[e]), __uint_as_float(r[e + 1]));
+            v.y = tc::pack_bf16(__uint_as_float(r[e + 2]), __uint_as_float(r[e + 3]));
+            v.z = tc::pack_bf16(__uint_as_float(r[e + 4]), __uint_as_float(r[e + 5]));
+            v.w = tc::pack_bf16(__uint_as_float(r[e + 6]), __uint_as_float(r[e + 7]));
+            *reinterpret_cast<uint4*>(crow + c0 + e) = v;
+          }
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<BN>(tmem);
+}
+
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                              CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                              CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    SLAB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) throw CudaError("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<EncodeFn>(p);
+  }
+  return fn;
+}
+
+template <int BM, int BN, bool A_MN, bool B_MN, typename OutT>
+void launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
+  CUtensorMap ta, tb;
+  // A: K-major -> tensor [batch][M][K], box [BM][64]; M-major -> [batch][K][M], box [64][64]
+  if (A_MN)
+    make_tmap_bf16(&ta, g.A, g.M, g.K, g.batch, g.lda, g.a_batch, 64);
+  else
+    make_tmap_bf16(&ta, g.A, g.K, g.M, g.batch, g.lda, g.a_batch, BM);
+  if (B_MN)
+    make_tmap_bf16(&tb, g.B, g.N, g.K, g.batch, g.ldb, g.b_batch, 64);
+  else
+    make_tmap_bf16(&tb, g.B, g.K, g.N, g.batch, g.ldb, g.b_batch, BN);
+  auto kern = k_gemm<BM, BN, A_MN, B_MN, OutT>;
+  constexpr int smem = GemmSmem<BM, BN>::kBytes;
+  SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  dim3 grid(g.N / BN, g.M / BM, g.batch);
+  kern<<<grid, 192, smem, st>>>(ta, tb, static_cast<OutT*>(g.C), g.M, g.N, g.K, g.c_batch, g.ldc);
+  check_launch(g.name ? g.name : "k_gemm", st);
+}
+
+template <int BM, int BN, typename OutT>
+void dispatch_major(const GemmArgs& g, cudaStream_t st) {
+  if (g.a_mn && g.b_mn) launch_gemm_t<BM, BN, true, true, OutT>(g, st);
+  else if (g.a_mn) launch_gemm_t<BM, BN, true, false, OutT>(g, st);
+  else if (g.b_mn) launch_gemm_t<BM, BN, false, true, OutT>(g, st);
+  else launch_gemm_t<BM, BN, false, false, OutT>(g, st);
+}
+
+template <typename OutT>
+void dispatch_tile(const GemmArgs& g, cudaStream_t st) {
+  const int BM = g.M % 128 == 0 ? 128 : 64;
+  const int BN = g.N % 256 == 0 ? 256 : (g.N % 128 == 0 ? 128 : 64);
+  if (BM == 128) {
+    if (BN == 256) dispatch_major<128, 256, OutT>(g, st);
+    else if (BN == 128) dispatch_major<128, 128, OutT>(g, st);
+    else dispatch_major<128, 64, OutT>(g, st);
+  } else {
+    if (BN == 256) dispatch_major<64, 256, OutT>(g, st);
+    else if (BN == 128) dispatch_major<64, 128, OutT>(g, st);
+    else dispatch_major<64, 64, OutT>(g, st);
+  }
+}
+
+}  // namespace
+
+bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t outer,
+                    uint64_t row_stride_elems, uint64_t outer_stride_elems, uint32_t box_rows) {
+  cuuint64_t dims[3] = {cols, rows, outer};
+  cuuint64_t strides[2] = {row_stride_elems * 2, outer_stride_elems * 2};
+  cuuint32_t box[3] = {64, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides,
+                           box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw CudaError("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
+  return true;
+}
+
+void launch_gemm(const GemmArgs& g, cudaStream_t st) {
+  if (g.M % 64 || g.N % 64 || g.K % 64 || g.M <= 0 || g.N <= 0 || g.K <= 0)
+    throw InvalidArgument("sla_b200 gemm: M, N, K must be positive multiples of 64");
+  if (g.out_f32)
+    dispatch_tile<float>(g, st);
+  else
+    dispatch_tile<__nv_bfloat16>(g, st);
+}
+
+}  // namespace slab
+
+extern "C" int sla_b200_diag_gemm(const void* A, const void* B, void* C, int batch, int M, int N,
+                                  int K, int a_mn, int b_mn, int out_f32, void* stream) {
+  try {
+    slab::GemmArgs g{};
+    g.A = A;
+    g.B = B;
+    g.C = C;
+    g.batch = batch;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.a_mn = a_mn;
+    g.b_mn = b_mn;
+    g.out_f32 = out_f32;
+    g.lda = a_mn ? M : K;
+    g.ldb = b_mn ? N : K;
+    g.ldc = N;
+    g.a_batch = (long long)M * K;
+    g.b_batch = (long long)K * N;
+    g.c_batch = (long long)M * N;
+    slab::launch_gemm(g, static_cast<cudaStream_t>(stream));
+    return 0;
+  } catch (const slab::InvalidArgument& e) {
+    std::fprintf(stderr, "%s\n", e.msg.c_str());
+    return 2;
+  } catch (const slab::CudaError& e) {
+    std::fprintf(stderr, "%s\n", e.msg.c_str());
+    return 1;
+  }
+}

@@ -25,6 +25,19 @@ void generic_backward(const Dims& D, int dtype, const void* q, const void* k, co
                       const void* d_out, void* dq, void* dk, void* dv, float* dw,
                       const StateBufs& s, const WorkBufs& wb, cudaStream_t st);
 
+// gemm.cu -- batched tcgen05 GEMM (bf16 in, f32 accumulate)
+struct GemmArgs {
+  const void* A;
+  const void* B;
+  void* C;
+  int batch, M, N, K;
+  bool a_mn, b_mn, out_f32;
+  long long lda, ldb, ldc;          // row strides in elements
+  long long a_batch, b_batch, c_batch;  // batch strides in elements
+  const char* name;
+};
+void launch_gemm(const GemmArgs& g, cudaStream_t st);
+
 // fast path (tcgen05) -- b_q = b_kv = 64, d in {64, 128}, bf16
 bool fast_supported(const Dims& D, int dtype);
 void fast_forward(const Dims& D, const void* q, const void* k, const void* v, const void* w,

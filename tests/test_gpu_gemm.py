@@ -1,0 +1,41 @@
+"""GPU test of the batched tcgen05 GEMM (gemm.cu) behind the linear branch: every operand
+majorness, both M tiles, all N tiles, batched, against an fp32 matmul of the same bf16
+inputs (the numerics reference for a floating-point kernel)."""
+import ctypes as C
+
+import pytest
+import torch
+
+from paper_2509_24006_b200 import _lib as L
+
+pytestmark = pytest.mark.gpu
+
+
+def _gemm(A, B, M, N, K, batch, a_mn, b_mn, out_f32):
+    lib = L.lib()
+    fn = lib.sla_b200_diag_gemm
+    fn.argtypes = [C.c_void_p] * 3 + [C.c_int] * 7 + [C.c_void_p]
+    out = torch.empty((batch, M, N), dtype=torch.float32 if out_f32 else torch.bfloat16, device="cuda")
+    rc = fn(A.data_ptr(), B.data_ptr(), out.data_ptr(), batch, M, N, K, int(a_mn), int(b_mn),
+            int(out_f32), C.c_void_p(torch.cuda.current_stream().cuda_stream))
+    assert rc == 0
+    torch.cuda.synchronize()
+    return out
+
+
+@pytest.mark.parametrize("a_mn", [False, True])
+@pytest.mark.parametrize("b_mn", [False, True])
+@pytest.mark.parametrize("M,N,K,batch", [(128, 256, 512, 2), (64, 128, 64, 3), (256, 64, 192, 1),
+                                         (128, 128, 128, 5)])
+@pytest.mark.parametrize("out_f32", [True, False])
+def test_gemm_matches_fp32_matmul(a_mn, b_mn, M, N, K, batch, out_f32):
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K + batch)
+    A = torch.randn((batch, M, K), device="cuda", generator=g).to(torch.bfloat16)
+    B = torch.randn((batch, K, N), device="cuda", generator=g).to(torch.bfloat16)
+    ref = A.float() @ B.float()
+    A_in = A.transpose(1, 2).contiguous() if a_mn else A.contiguous()   # [K][M] when M-major
+    B_in = B.contiguous() if b_mn else B.transpose(1, 2).contiguous()   # [N][K] when K-major
+    out = _gemm(A_in, B_in, M, N, K, batch, a_mn, b_mn, out_f32).float()
+    tol = 1e-3 if out_f32 else 1e-2
+    err = ((out - ref).abs().max() / ref.abs().max().clamp_min(1.0)).item()
+    assert err <= tol, err

@@ -58,7 +58,7 @@ def _close(got, want, tol, keys=("o", "o_s", "o_l", "dq_total", "dk_total", "dv"
 
 def _lse_close(got, want, tol):
     live = want > -1e29
-    assert np.all(got[~live] == -1e30)
+    assert np.all(got[~live] == np.float32(-1e30))
     if live.any():
         assert np.abs(got[live] - want[live]).max() <= tol
 
@@ -191,7 +191,7 @@ def test_degenerate_masks(fill):  # forward_test.cpp:60-85; all-negligible -> ze
     want = O.step(x["q"], x["k"], x["v"], x["w"], x["do"], lab, 16, 16, "elu1")
     _close(got, want, 1e-4)
     if fill != 1:
-        assert np.abs(got["o_s"]).max() == 0 and (got["lse"] == -1e30).all()
+        assert np.abs(got["o_s"]).max() == 0 and (got["lse"] == np.float32(-1e30)).all()
     if fill != 0:
         assert np.abs(got["o_l"]).max() == 0
 
@@ -204,7 +204,7 @@ def test_rows_without_critical_blocks():  # mask.hpp:21-23
     got, _ = _run_step(x, 16, "softmax", torch.float32, labels=lab, generic=True)
     want = O.step(x["q"], x["k"], x["v"], x["w"], x["do"], lab, 16, 16, "softmax")
     _close(got, want, 1e-4)
-    assert (got["lse"][48:64] == -1e30).all()
+    assert (got["lse"][48:64] == np.float32(-1e30)).all()
 
 
 def test_relu_zero_denominator_rows():  # backward_test.cpp:247-264
