@@ -50,6 +50,7 @@ struct WorkBufs {
   float* dqf = nullptr;      // dQ^phi
   float* dkf = nullptr;      // dK^phi
   __nv_bfloat16* hb = nullptr;   // fast path: h in bf16, [U, Tn, d*d]
+  __nv_bfloat16* kfb = nullptr;  // fast path: phi(K) in bf16, [U, N, d]
 };
 
 // Bump allocator: with base == nullptr it only measures.
@@ -78,7 +79,7 @@ inline void carve_state(const Dims& D, bool fast, void* base, StateBufs& s, size
   s.Z = c.take<float>(U * Tm * d);
   if (fast) {
     s.Hb = c.take<__nv_bfloat16>(U * Tm * d * d);
-    s.M0 = c.take<__nv_bfloat16>(U * Tm * Tn);
+    s.M0 = c.take<__nv_bfloat16>(U * Tm * ((Tn + 7) / 8 * 8));
   } else {
     s.H = c.take<float>(U * Tm * d * d);
   }
@@ -95,22 +96,20 @@ inline void carve_work(const Dims& D, bool fast, void* base, WorkBufs& w, size_t
   w.Ds = c.take<float>(U * N);
   w.Dl = c.take<float>(U * N);
   w.gZ = c.take<float>(U * Tm * d);
+  w.qf = c.take<float>(U * N * d);
+  w.kf = c.take<float>(U * N * d);
+  w.dOl = c.take<float>(U * N * d);
+  w.gH = c.take<float>(U * Tm * d * d);
+  w.dq = c.take<float>(U * N * d);
+  w.dk = c.take<float>(U * N * d);
+  w.dv = c.take<float>(U * N * d);
+  w.dqf = c.take<float>(U * N * d);
+  w.dkf = c.take<float>(U * N * d);
   if (fast) {
     w.hb = c.take<__nv_bfloat16>(U * Tn * d * d);
-    w.dq = c.take<float>(U * N * d);
-    w.dOl = c.take<float>(U * N * d);
-    w.gH = c.take<float>(U * Tm * d * d);
+    w.kfb = c.take<__nv_bfloat16>(U * N * d);
   } else {
-    w.qf = c.take<float>(U * N * d);
-    w.kf = c.take<float>(U * N * d);
     w.h = c.take<float>(U * Tn * d * d);
-    w.dOl = c.take<float>(U * N * d);
-    w.gH = c.take<float>(U * Tm * d * d);
-    w.dq = c.take<float>(U * N * d);
-    w.dk = c.take<float>(U * N * d);
-    w.dv = c.take<float>(U * N * d);
-    w.dqf = c.take<float>(U * N * d);
-    w.dkf = c.take<float>(U * N * d);
   }
   if (bytes) *bytes = c.off + 256;
 }

@@ -221,11 +221,14 @@ __global__ void k_build_csc(const int8_t* __restrict__ labels, int Tm, int Tn,
 }
 
 // Marginal indicator as a bf16 0/1 matrix: the A operand of H = M0 h (fast path).
-__global__ void k_build_m0(const int8_t* __restrict__ labels, long long total,
+__global__ void k_build_m0(const int8_t* __restrict__ labels, long long total, int Tn, int ld,
                            __nv_bfloat16* __restrict__ m0) {
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x)
-    m0[e] = __float2bfloat16_rn(labels[e] == 0 ? 1.f : 0.f);
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long row = e / ld;
+    const int j = int(e % ld);
+    m0[e] = __float2bfloat16_rn(j < Tn && labels[row * Tn + j] == 0 ? 1.f : 0.f);
+  }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -314,9 +317,10 @@ void launch_build_csc(const Dims& D, const StateBufs& s, cudaStream_t st) {
 }
 
 void launch_build_m0(const Dims& D, const StateBufs& s, cudaStream_t st) {
-  const long long total = D.U * (long long)D.Tm * D.Tn;
+  const int ld = int(m0_stride(D));
+  const long long total = D.U * (long long)D.Tm * ld;
   const int blocks = int(std::min<long long>((total + 255) / 256, 148 * 8));
-  k_build_m0<<<blocks, 256, 0, st>>>(s.labels, total, s.M0);
+  k_build_m0<<<blocks, 256, 0, st>>>(s.labels, total, D.Tn, ld, s.M0);
   check_launch("k_build_m0", st);
 }
 

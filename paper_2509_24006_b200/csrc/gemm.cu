@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(192, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, b = blockIdx.z;
-  const int nk = K / kBK;
+  const int nk = (K + kBK - 1) / kBK;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -179,7 +179,7 @@ void launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
   auto kern = k_gemm<BM, BN, A_MN, B_MN, OutT>;
   constexpr int smem = GemmSmem<BM, BN>::kBytes;
   SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  dim3 grid(g.N / BN, g.M / BM, g.batch);
+  dim3 grid(g.N / BN, (g.M + BM - 1) / BM, g.batch);
   kern<<<grid, 192, smem, st>>>(ta, tb, static_cast<OutT*>(g.C), g.M, g.N, g.K, g.c_batch, g.ldc);
   check_launch(g.name ? g.name : "k_gemm", st);
 }
@@ -194,7 +194,7 @@ void dispatch_major(const GemmArgs& g, cudaStream_t st) {
 
 template <typename OutT>
 void dispatch_tile(const GemmArgs& g, cudaStream_t st) {
-  const int BM = g.M % 128 == 0 ? 128 : 64;
+  const int BM = (g.M % 128 == 0 || g.M > 192) ? 128 : 64;
   const int BN = g.N % 256 == 0 ? 256 : (g.N % 128 == 0 ? 128 : 64);
   if (BM == 128) {
     if (BN == 256) dispatch_major<128, 256, OutT>(g, st);
@@ -224,8 +224,9 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t cols, uint64_t 
 }
 
 void launch_gemm(const GemmArgs& g, cudaStream_t st) {
-  if (g.M % 64 || g.N % 64 || g.K % 64 || g.M <= 0 || g.N <= 0 || g.K <= 0)
-    throw InvalidArgument("sla_b200 gemm: M, N, K must be positive multiples of 64");
+  // N must tile exactly; M and K tails are handled by TMA zero fill + masked stores
+  if (g.N % 64 || g.M <= 0 || g.N <= 0 || g.K <= 0)
+    throw InvalidArgument("sla_b200 gemm: N must be a positive multiple of 64");
   if (g.out_f32)
     dispatch_tile<float>(g, st);
   else

@@ -366,9 +366,10 @@ __global__ void k_dw(Dims D, const In* __restrict__ o_l, const In* __restrict__ 
 }
 
 // Row phase, linear branch (backward.cpp:70-95): dH_i, dZ_i, dQ^phi.  grid (Tm, U).
+template <typename HT>
 __global__ void k_bwd_rows_lin(Dims D, const int* __restrict__ marg_cnt,
                                const float* __restrict__ qf, const float* __restrict__ dOl,
-                               const float* __restrict__ Dl, const float* __restrict__ H,
+                               const float* __restrict__ Dl, const HT* __restrict__ H,
                                const float* __restrict__ Z, float* __restrict__ gH,
                                float* __restrict__ gZ, float* __restrict__ dqf) {
   extern __shared__ float sm[];
@@ -390,12 +391,12 @@ __global__ void k_bwd_rows_lin(Dims D, const int* __restrict__ marg_cnt,
     for (int e = threadIdx.x; e < bq * d; e += blockDim.x) dqf[row0 * d + e] = 0.f;
     return;
   }
-  const float* Hi = H + (u * D.Tm + i) * (long long)d * d;
+  const HT* Hi = H + (u * D.Tm + i) * (long long)d * d;
   for (int e = threadIdx.x; e < bq * d; e += blockDim.x) {
     sQF[e] = qf[row0 * d + e];
     sDO[e] = dOl[row0 * d + e];
   }
-  for (int e = threadIdx.x; e < d * d; e += blockDim.x) sH[(e / d) * dp + e % d] = Hi[e];
+  for (int e = threadIdx.x; e < d * d; e += blockDim.x) sH[(e / d) * dp + e % d] = to_f(Hi[e]);
   for (int a = threadIdx.x; a < d; a += blockDim.x) sZ[a] = Z[(u * D.Tm + i) * d + a];
   for (int r = threadIdx.x; r < bq; r += blockDim.x) sDl[r] = Dl[row0 + r];
   __syncthreads();
@@ -757,9 +758,15 @@ void backward_t(const Dims& D, const In* q, const In* k, const In* v, const In* 
   k_dw<In><<<dim3(grid1(D.N, 32), unsigned(D.U)), 256, dws, st>>>(D, o_l, d_out, dw);
   check_launch("k_dw", st);
   const size_t rl = rows_lin_smem(D);
-  set_smem(k_bwd_rows_lin, rl);
-  k_bwd_rows_lin<<<dim3(D.Tm, unsigned(D.U)), kThreads, rl, st>>>(
-      D, s.marg_cnt, wb.qf, wb.dOl, wb.Dl, s.H, s.Z, wb.gH, wb.gZ, wb.dqf);
+  if (s.H) {
+    set_smem(k_bwd_rows_lin<float>, rl);
+    k_bwd_rows_lin<float><<<dim3(D.Tm, unsigned(D.U)), kThreads, rl, st>>>(
+        D, s.marg_cnt, wb.qf, wb.dOl, wb.Dl, s.H, s.Z, wb.gH, wb.gZ, wb.dqf);
+  } else {
+    set_smem(k_bwd_rows_lin<__nv_bfloat16>, rl);
+    k_bwd_rows_lin<__nv_bfloat16><<<dim3(D.Tm, unsigned(D.U)), kThreads, rl, st>>>(
+        D, s.marg_cnt, wb.qf, wb.dOl, wb.Dl, s.Hb, s.Z, wb.gH, wb.gZ, wb.dqf);
+  }
   check_launch("k_bwd_rows_lin", st);
   const size_t rs = rows_sparse_smem(D);
   set_smem(k_bwd_rows_sparse<In>, rs);

@@ -39,6 +39,11 @@ struct GemmArgs {
 void launch_gemm(const GemmArgs& g, cudaStream_t st);
 
 // fast path (tcgen05) -- b_q = b_kv = 64, d in {64, 128}, bf16
+inline long long m0_stride(const Dims& D) { return (D.Tn + 7) / 8 * 8; }  // 16-byte rows for TMA
+void launch_attn_fwd(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
+                     void* o, void* o_s, void* o_l, float* lse, const StateBufs& s, cudaStream_t st);
+void fast_prepare_linear(const Dims& Dm, const void* k, const void* v, const StateBufs& s,
+                         const WorkBufs& wb, cudaStream_t st);
 bool fast_supported(const Dims& D, int dtype);
 void fast_forward(const Dims& D, const void* q, const void* k, const void* v, const void* w,
                   void* o, void* o_s, void* o_l, float* lse, const StateBufs& s,
