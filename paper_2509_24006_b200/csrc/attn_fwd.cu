@@ -126,7 +126,7 @@ __global__ void __launch_bounds__(192, 2)
     if (lane == 0) {
       tc::mbar_expect_tx(q_full, L::kQ);
 #pragma unroll
-      for (int c = 0; c < D / 64; ++c) tc::tma_load_2d(sQ + c * 8192, &tmQ, q_full, 64 * c, row0);
+      for (int c = 0; c < D / 64; ++c) tc::tma_load_3d(sQ + c * 8192, &tmQ, q_full, 64 * c, row0, 0);
       int item = 0;
       auto acquire = [&](int bytes) -> uint8_t* {
         const int s = item & 1;
@@ -138,7 +138,7 @@ __global__ void __launch_bounds__(192, 2)
         uint8_t* dst = acquire(D * D * 2);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c)
-          tc::tma_load_2d(dst + c * D * 128, &tmH, ring_full + (item & 1), 64 * c, int(urow * D));
+          tc::tma_load_3d(dst + c * D * 128, &tmH, ring_full + (item & 1), 64 * c, int(urow * D), 0);
         ++item;
       }
       for (int t = 0; t < cnt; ++t) {
@@ -146,8 +146,8 @@ __global__ void __launch_bounds__(192, 2)
         uint8_t* dst = acquire(2 * L::kTile);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
-          tc::tma_load_2d(dst + c * 8192, &tmK, ring_full + (item & 1), 64 * c, kv_row);
-          tc::tma_load_2d(dst + L::kTile + c * 8192, &tmV, ring_full + (item & 1), 64 * c, kv_row);
+          tc::tma_load_3d(dst + c * 8192, &tmK, ring_full + (item & 1), 64 * c, kv_row, 0);
+          tc::tma_load_3d(dst + L::kTile + c * 8192, &tmV, ring_full + (item & 1), 64 * c, kv_row, 0);
         }
         ++item;
       }
@@ -156,7 +156,7 @@ __global__ void __launch_bounds__(192, 2)
         const int h = int(u % p.H);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c)
-          tc::tma_load_2d(dst + c * D * 128, &tmW, ring_full + (item & 1), 64 * c, h * D);
+          tc::tma_load_3d(dst + c * D * 128, &tmW, ring_full + (item & 1), 64 * c, h * D, 0);
         ++item;
       }
     }
