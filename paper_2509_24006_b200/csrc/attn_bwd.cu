@@ -1,0 +1,911 @@
+// attn_bwd.cu -- the fused SLA backward on tcgen05, two deterministic passes that mirror the
+// reference's row and column phases (backward.cpp:68-120 and 142-199); no atomics.
+//
+// k_bwd_rows<D>: one CTA per (unit, query block i)
+//   dO^l_i = dO_i W^T (MMA), D^s, D^l row dots, x = phi(q)/den,
+//   dH_i = x^T dO^l_i (MMA, written bf16 for the M0^T aggregation GEMM), dZ_i = -x^T D^l,
+//   dQ^phi = (dO^l H_i^T - D^l Z_i^T) / den (MMA + epilogue),
+//   sparse dQ = sum_j dS_ij K_j over the critical list (S, dP recomputed on tcgen05),
+//   dq_total = J_phi(q)^T dQ^phi + dQ written once (backward.cpp:211-214).
+// k_bwd_cols<D>: one CTA per (unit, key block j)
+//   sparse dV_j += P^T dO_i, dK_j += dS^T Q_i over the critical rows (CSC list),
+//   linear dK^phi_j = V_j dH_agg^T + dZ_agg, dV_j += phi(K_j) dH_agg (dH_agg = M0^T dH),
+//   dk_total = J_phi(k)^T dK^phi + dK and dv written once.
+//
+// Warp roles as in the forward: warp 0 TMA, warp 1 MMA (one thread), warps 2-5 compute
+// (row = 16*(warp%4) + lane for M=64 tiles).
+#include "kernels.hpp"
+#include "tc.cuh"
+
+namespace slab {
+
+namespace {
+
+__device__ __forceinline__ float ex2f(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void unpack8(const uint4& v, float (&f)[8]) {
+  const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 t = __bfloat1622float2(h2[e]);
+    f[2 * e] = t.x;
+    f[2 * e + 1] = t.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint4 v;
+  v.x = tc::pack_bf16(f[0], f[1]);
+  v.y = tc::pack_bf16(f[2], f[3]);
+  v.z = tc::pack_bf16(f[4], f[5]);
+  v.w = tc::pack_bf16(f[6], f[7]);
+  return v;
+}
+// byte offset of columns [col, col+8) of row r in a K-major SW128 tile (64-column blocks of
+// 8 KB); col is an element index, a multiple of 8
+__device__ __forceinline__ uint32_t tile_off(int r, int col) {
+  return uint32_t(col >> 6) * 8192u + tc::sw128_off(uint32_t(r), uint32_t((col >> 3) & 7));
+}
+
+// phi VJP of one row held in a K-major smem tile (feature_map.cpp:42-73): g -> J^T g.
+// Pass 1 computes the softmax statistics / <s, g>; callers supply g chunk-wise twice.
+template <int D>
+struct RowPhi {
+  float m = 0.f, inv = 0.f;  // softmax stats
+  __device__ void stats(const uint8_t* tile, int r, int phi) {
+    if (phi != 2) return;
+    float mx = -INFINITY;
+#pragma unroll
+    for (int c = 0; c < D / 8; ++c) {
+      float f[8];
+      unpack8(*reinterpret_cast<const uint4*>(tile + tile_off(r, 8 * c)), f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) mx = fmaxf(mx, f[e]);
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int c = 0; c < D / 8; ++c) {
+      float f[8];
+      unpack8(*reinterpret_cast<const uint4*>(tile + tile_off(r, 8 * c)), f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s += __expf(f[e] - mx);
+    }
+    m = mx;
+    inv = 1.f / s;
+  }
+  __device__ float phi_of(float x, int phi) const {
+    return phi == 2 ? __expf(x - m) * inv : phi_elem(phi, x);
+  }
+};
+
+struct BwdParams {
+  const int* crit_cnt;
+  const int* crit_idx;
+  const int* marg_cnt;
+  const int* ccol_cnt;
+  const int* ccol_idx;
+  const float* Z;      // [U, Tm, D]
+  const float* lse;    // [U, N]
+  const float* Ds;     // [U, N] (rows kernel writes, cols kernel reads)
+  float* Ds_out;
+  const __nv_bfloat16* o_s;
+  const __nv_bfloat16* o_l;
+  __nv_bfloat16* gH;   // [U, Tm, D, D] dH_i (rows kernel out)
+  float* gZ;           // [U, Tm, D] dZ_i
+  const float* gZa;    // [U, Tn, D] dZ_agg (cols kernel in)
+  int* has_lin_col;    // unused
+  __nv_bfloat16* dq;   // outputs
+  __nv_bfloat16* dk;
+  __nv_bfloat16* dv;
+  long long N;
+  int Tm, Tn, H;
+  float scale;         // 1/sqrt(D)
+  float scale_log2;    // scale * log2(e)
+  int phi;
+  const int8_t* labels;
+};
+
+// =========================================================================================
+// rows pass
+// =========================================================================================
+template <int D>
+struct RowsLayout {
+  static constexpr int kT = 64 * D * 2;
+  static constexpr int oQ = 0, oDO = kT, oDOL = 2 * kT;
+  static constexpr int oRing = 3 * kT;
+  static constexpr int kStage = 2 * kT;  // K + V, or W / H_i (D*D*2)
+  static constexpr int oDS = oRing + 2 * kStage;  // 2 x 8 KB dS buffers, X aliases them
+  static constexpr int oDZ = oDS + 16384;          // float dz[D]
+  static constexpr int oBar = oDZ + 4 * D;
+  static constexpr int kBytes = oBar + 256 + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(192, 1)
+    k_bwd_rows(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
+               const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+               const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmH,
+               BwdParams p) {
+  using L = RowsLayout<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem + L::oQ;
+  uint8_t* sDO = smem + L::oDO;
+  uint8_t* sDOL = smem + L::oDOL;
+  uint8_t* sRing = smem + L::oRing;
+  uint8_t* sDS = smem + L::oDS;
+  uint8_t* sX = sDS;
+  float* dz = reinterpret_cast<float*>(smem + L::oDZ);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::oBar);
+  uint64_t* qdo_full = bars + 0;
+  uint64_t* ring_full = bars + 1;   // [2]
+  uint64_t* ring_empty = bars + 3;  // [2]
+  uint64_t* sdp_full = bars + 5;    // [2]
+  uint64_t* ds_full = bars + 7;     // [2]
+  uint64_t* ds_empty = bars + 9;    // [2]
+  uint64_t* dol_done = bars + 11;
+  uint64_t* x_ready = bars + 12;
+  uint64_t* lin_done = bars + 13;
+  uint64_t* dh_read = bars + 14;
+  uint64_t* dq_done = bars + 15;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x;
+  const long long u = blockIdx.y;
+  const long long urow = u * p.Tm + i;
+  const int cnt = p.crit_cnt[urow];
+  const int* list = p.crit_idx + urow * p.Tn;
+  const bool has_lin = p.marg_cnt[urow] > 0;
+  const int row0 = int(u * p.N) + i * 64;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::mbar_init(qdo_full, 1);
+      for (int s = 0; s < 2; ++s) {
+        tc::mbar_init(ring_full + s, 1);
+        tc::mbar_init(ring_empty + s, 1);
+        tc::mbar_init(sdp_full + s, 1);
+        tc::mbar_init(ds_full + s, 4);
+        tc::mbar_init(ds_empty + s, 1);
+      }
+      tc::mbar_init(dol_done, 1);
+      tc::mbar_init(x_ready, 4);
+      tc::mbar_init(lin_done, 1);
+      tc::mbar_init(dh_read, 4);
+      tc::mbar_init(dq_done, 1);
+      tc::fence_barrier_init();
+    }
+    __syncwarp();
+    tc::tmem_alloc<512>(tmem_slot);
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tDQ = tmem, tB0 = tmem + 128, tB1 = tmem + 256, tQPHI = tmem + 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::mbar_expect_tx(qdo_full, 2 * L::kT);
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        tc::tma_load_3d(sQ + c * 8192, &tmQ, qdo_full, 64 * c, row0, 0);
+        tc::tma_load_3d(sDO + c * 8192, &tmDO, qdo_full, 64 * c, row0, 0);
+      }
+      int item = 0;
+      auto acquire = [&](int bytes) -> uint8_t* {
+        const int s = item & 1;
+        tc::mbar_wait(ring_empty + s, ((item >> 1) & 1) ^ 1);
+        tc::mbar_expect_tx(ring_full + s, bytes);
+        return sRing + s * L::kStage;
+      };
+      {
+        uint8_t* dst = acquire(D * D * 2);
+        const int h = int(u % p.H);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) tc::tma_load_3d(dst + c * D * 128, &tmW, ring_full + (item & 1), 64 * c, h * D, 0);
+        ++item;
+      }
+      if (has_lin) {
+        uint8_t* dst = acquire(D * D * 2);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c)
+          tc::tma_load_3d(dst + c * D * 128, &tmH, ring_full + (item & 1), 64 * c, int(urow * D), 0);
+        ++item;
+      }
+      for (int t = 0; t < cnt; ++t) {
+        const int kv_row = int(u * p.N) + list[t] * 64;
+        uint8_t* dst = acquire(2 * L::kT);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) {
+          tc::tma_load_3d(dst + c * 8192, &tmK, ring_full + (item & 1), 64 * c, kv_row, 0);
+          tc::tma_load_3d(dst + L::kT + c * 8192, &tmV, ring_full + (item & 1), 64 * c, kv_row, 0);
+        }
+        ++item;
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t aQ = tc::smem_u32(sQ), aDO = tc::smem_u32(sDO), aDOL = tc::smem_u32(sDOL);
+    const uint32_t aR = tc::smem_u32(sRing), aDS = tc::smem_u32(sDS);
+    constexpr uint32_t id_nd_kk = tc::idesc_bf16(64, D, false, false);   // A K-major, B K-major
+    constexpr uint32_t id_nd_kn = tc::idesc_bf16(64, D, false, true);    // B MN-major
+    constexpr uint32_t id_dh = tc::idesc_bf16(D, D, true, true);         // A, B MN-major
+    constexpr uint32_t id_ss = tc::idesc_bf16(64, 64, false, false);
+    int item = 0;
+    auto wait_item = [&]() -> uint32_t {
+      const int s = item & 1;
+      tc::mbar_wait(ring_full + s, (item >> 1) & 1);
+      tc::tc_fence_after();
+      return aR + s * L::kStage;
+    };
+    auto kdesc = [](uint32_t base, int kk, int rows) {  // K-major tile with `rows` rows/chunk
+      return tc::desc_kmajor(base + (kk >> 2) * rows * 128 + (kk & 3) * 32);
+    };
+    tc::mbar_wait(qdo_full, 0);
+    {  // dO^l = dO W^T  -> B0
+      const uint32_t sw = wait_item();
+      if (lane == 0) {
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) tc::mma_bf16(tB0, kdesc(aDO, kk, 64), kdesc(sw, kk, D), id_nd_kk, kk > 0);
+        tc::mma_commit(ring_empty + (item & 1));
+        tc::mma_commit(dol_done);
+      }
+      __syncwarp();
+      ++item;
+    }
+    tc::mbar_wait(x_ready, 0);
+    tc::tc_fence_after();
+    if (has_lin) {
+      const uint32_t sh = wait_item();
+      if (lane == 0) {
+        // dQ^phi raw = dO^l H_i^T -> QPHI
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) tc::mma_bf16(tQPHI, kdesc(aDOL, kk, 64), kdesc(sh, kk, D), id_nd_kk, kk > 0);
+        // dH_i = x^T dO^l (M = D over a, N = D over b, K = 64 rows) -> B1
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          tc::mma_bf16(tB1, tc::desc_mnmajor(aDS + kk * 2048, 8192), tc::desc_mnmajor(aDOL + kk * 2048, 8192), id_dh,
+                       kk > 0);
+        tc::mma_commit(ring_empty + (item & 1));
+        tc::mma_commit(lin_done);
+      }
+      __syncwarp();
+      ++item;
+      tc::mbar_wait(dh_read, 0);  // B1 and the X (= dS) buffers are free again
+      tc::tc_fence_after();
+    }
+    const int item0 = item;
+    auto issue_dq = [&](int j) {
+      tc::mbar_wait(ds_full + (j & 1), (j >> 1) & 1);
+      tc::tc_fence_after();
+      const int it = item0 + j;
+      const uint32_t sk = aR + (it & 1) * L::kStage;
+      if (lane == 0) {
+        const uint32_t sds = aDS + (j & 1) * 8192;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          tc::mma_bf16(tDQ, tc::desc_kmajor(sds + kk * 32), tc::desc_mnmajor(sk + kk * 2048, 8192), id_nd_kn,
+                       (j | kk) != 0);
+        tc::mma_commit(ring_empty + (it & 1));
+        tc::mma_commit(ds_empty + (j & 1));
+      }
+      __syncwarp();
+    };
+    for (int t = 0; t < cnt; ++t) {
+      const uint32_t skv = wait_item();
+      if (lane == 0) {
+        const uint32_t tb = (t & 1) ? tB1 : tB0;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          tc::mma_bf16(tb, kdesc(aQ, kk, 64), kdesc(skv, kk, 64), id_ss, kk > 0);
+          tc::mma_bf16(tb + 64, kdesc(aDO, kk, 64), kdesc(skv + L::kT, kk, 64), id_ss, kk > 0);
+        }
+        tc::mma_commit(sdp_full + (t & 1));
+      }
+      __syncwarp();
+      ++item;
+      if (t > 0) issue_dq(t - 1);
+    }
+    if (cnt > 0) issue_dq(cnt - 1);
+    if (lane == 0) tc::mma_commit(dq_done);
+    __syncwarp();
+  } else {
+    const int q4 = warp & 3;
+    const int r = 16 * q4 + lane;
+    const bool valid = lane < 16;
+    const uint32_t lane_base = uint32_t(32 * q4) << 16;
+    const long long grow = (long long)row0 + r;
+    const int rr = r & 63;
+    const long long growr = (long long)row0 + rr;  // in-bounds row for the idle lanes' reads
+    for (int a = threadIdx.x - 64; a < D; a += 128) dz[a] = 0.f;
+    named_sync(1, 128);
+    tc::mbar_wait(qdo_full, 0);
+    // D^s = <dO, O^s>
+    float ds_r = 0.f;
+#pragma unroll
+    for (int c = 0; c < D / 8; ++c) {
+      float f[8], g[8];
+      unpack8(*reinterpret_cast<const uint4*>(sDO + tile_off(rr, 8 * c)), f);
+      unpack8(*reinterpret_cast<const uint4*>(p.o_s + growr * D + 8 * c), g);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) ds_r = fmaf(f[e], g[e], ds_r);
+    }
+    if (valid) p.Ds_out[grow] = ds_r;
+    // dO^l from TMEM -> D^l, and bf16 into sDOL
+    tc::mbar_wait(dol_done, 0);
+    tc::tc_fence_after();
+    float dl_r = 0.f;
+#pragma unroll 1
+    for (int c0 = 0; c0 < D; c0 += 32) {
+      uint32_t a[32];
+      tc::tmem_ld32(tB0 + lane_base + c0, a);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float f[8], g[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(a[8 * c + e]);
+        unpack8(*reinterpret_cast<const uint4*>(p.o_l + growr * D + c0 + 8 * c), g);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) dl_r = fmaf(f[e], g[e], dl_r);
+        if (valid) *reinterpret_cast<uint4*>(sDOL + tile_off(r, c0 + 8 * c)) = pack8(f);
+      }
+    }
+    // x = phi(q) / den (zero rows when den == 0 or no marginal block), dZ_i = -sum_r x D^l
+    RowPhi<D> ph;
+    ph.stats(sQ, rr, p.phi);
+    float den = 0.f;
+    const float* Zi = p.Z + urow * D;
+    if (has_lin) {
+#pragma unroll
+      for (int c = 0; c < D / 8; ++c) {
+        float f[8];
+        unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(rr, 8 * c)), f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) den = fmaf(ph.phi_of(f[e], p.phi), __ldg(Zi + 8 * c + e), den);
+      }
+    }
+    const float inv_den = (has_lin && den != 0.f) ? 1.f / den : 0.f;
+#pragma unroll 1
+    for (int c = 0; c < D / 8; ++c) {
+      float f[8];
+      unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(rr, 8 * c)), f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) f[e] = valid ? ph.phi_of(f[e], p.phi) * inv_den : 0.f;
+      if (valid) *reinterpret_cast<uint4*>(sX + tile_off(r, 8 * c)) = pack8(f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        float v = -f[e] * dl_r;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) atomicAdd(dz + 8 * c + e, v);
+      }
+    }
+    tc::fence_proxy_async();
+    tc::tc_fence_before();
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(x_ready);
+    // dH_i -> global bf16 (rows a of the M = D accumulator); dZ_i
+    __nv_bfloat16* gHi = p.gH + urow * D * D;
+    if (has_lin) {
+      tc::mbar_wait(lin_done, 0);
+      tc::tc_fence_after();
+      const int arow = D == 128 ? 32 * q4 + lane : 16 * q4 + lane;
+      const bool avalid = D == 128 || lane < 16;
+#pragma unroll 1
+      for (int c0 = 0; c0 < D; c0 += 32) {
+        uint32_t a[32];
+        tc::tmem_ld32(tB1 + lane_base + c0, a);
+        tc::tmem_ld_wait();
+        if (avalid) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float f[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(a[8 * c + e]);
+            *reinterpret_cast<uint4*>(gHi + arow * D + c0 + 8 * c) = pack8(f);
+          }
+        }
+      }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(dh_read);
+    } else {
+      for (int e = threadIdx.x - 64; e < D * D / 8; e += 128)
+        reinterpret_cast<uint4*>(gHi)[e] = make_uint4(0, 0, 0, 0);
+    }
+    named_sync(1, 128);
+    for (int a = threadIdx.x - 64; a < D; a += 128) p.gZ[urow * D + a] = has_lin ? dz[a] : 0.f;
+    // sparse dQ: dS = P (dP - D^s) / sqrt(d), P = exp(S/sqrt(d) - lse)
+    const float lse2 = valid ? p.lse[grow] * 1.4426950408889634f : 0.f;
+    for (int t = 0; t < cnt; ++t) {
+      tc::mbar_wait(sdp_full + (t & 1), (t >> 1) & 1);
+      tc::tc_fence_after();
+      const uint32_t tb = ((t & 1) ? tB1 : tB0) + lane_base;
+      uint32_t s[32], dp[32];
+      uint32_t pk[32];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        tc::tmem_ld32(tb + 32 * h, s);
+        tc::tmem_ld32(tb + 64 + 32 * h, dp);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const float p0 = ex2f(__uint_as_float(s[e]) * p.scale_log2 - lse2);
+          const float p1 = ex2f(__uint_as_float(s[e + 1]) * p.scale_log2 - lse2);
+          const float d0 = p0 * (__uint_as_float(dp[e]) - ds_r) * p.scale;
+          const float d1 = p1 * (__uint_as_float(dp[e + 1]) - ds_r) * p.scale;
+          pk[16 * h + (e >> 1)] = tc::pack_bf16(d0, d1);
+        }
+      }
+      if (t >= 2) tc::mbar_wait(ds_empty + (t & 1), ((t - 2) >> 1) & 1);
+      if (valid) {
+        uint8_t* drow = sDS + (t & 1) * 8192;
+#pragma unroll
+        for (int c = 0; c < 8; ++c)
+          *reinterpret_cast<uint4*>(drow + tc::sw128_off(r, c)) = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+      }
+      tc::fence_proxy_async();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(ds_full + (t & 1));
+    }
+    // dq_total = J_phi(q)^T dQ^phi + dQ
+    tc::mbar_wait(dq_done, 0);
+    tc::tc_fence_after();
+    float dot = 0.f;  // <phi(q), dQ^phi> for the softmax VJP
+    if (p.phi == 2 && has_lin) {
+#pragma unroll 1
+      for (int c0 = 0; c0 < D; c0 += 32) {
+        uint32_t a[32];
+        tc::tmem_ld32(tQPHI + lane_base + c0, a);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float f[8];
+          unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(rr, c0 + 8 * c)), f);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float g = (__uint_as_float(a[8 * c + e]) - dl_r * __ldg(Zi + c0 + 8 * c + e)) * inv_den;
+            dot = fmaf(ph.phi_of(f[e], 2), g, dot);
+          }
+        }
+      }
+    }
+#pragma unroll 1
+    for (int c0 = 0; c0 < D; c0 += 32) {
+      uint32_t a[32], b[32];
+      if (has_lin) tc::tmem_ld32(tQPHI + lane_base + c0, a);
+      if (cnt > 0) tc::tmem_ld32(tDQ + lane_base + c0, b);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float f[8], o[8];
+        unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(rr, c0 + 8 * c)), f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int col = c0 + 8 * c + e;
+          const float g = has_lin ? (__uint_as_float(a[8 * c + e]) - dl_r * __ldg(Zi + col)) * inv_den : 0.f;
+          float jg;
+          if (p.phi == 2) jg = ph.phi_of(f[e], 2) * (g - dot);
+          else if (p.phi == 0) jg = f[e] >= 0.f ? g : __expf(f[e]) * g;
+          else jg = f[e] > 0.f ? g : 0.f;
+          o[e] = jg + (cnt > 0 ? __uint_as_float(b[8 * c + e]) : 0.f);
+        }
+        if (valid) *reinterpret_cast<uint4*>(p.dq + grow * D + c0 + 8 * c) = pack8(o);
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(tmem);
+}
+
+// =========================================================================================
+// columns pass
+// =========================================================================================
+template <int D>
+struct ColsLayout {
+  static constexpr int kT = 64 * D * 2;
+  static constexpr int oK = 0, oV = kT, oKF = 2 * kT;
+  static constexpr int oRing = 3 * kT;
+  static constexpr int kStage = 2 * kT;  // Q_i + dO_i, or dH_agg (D*D*2)
+  static constexpr int oPD = oRing + 2 * kStage;  // [2 buffers][P^T 8 KB, dS^T 8 KB]
+  static constexpr int oLS = oPD + 32768;          // float [2][128] lse*log2e, D^s
+  static constexpr int oBar = oLS + 2 * 128 * 4;
+  static constexpr int kBytes = oBar + 256 + 1024;
+};
+
+template <int D>
+__global__ void __launch_bounds__(192, 1)
+    k_bwd_cols(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
+               const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+               const __grid_constant__ CUtensorMap tmHa, BwdParams p) {
+  using L = ColsLayout<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = smem + L::oK;
+  uint8_t* sV = smem + L::oV;
+  uint8_t* sKF = smem + L::oKF;
+  uint8_t* sRing = smem + L::oRing;
+  uint8_t* sPD = smem + L::oPD;
+  float* sLS = reinterpret_cast<float*>(smem + L::oLS);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::oBar);
+  uint64_t* kv_full = bars + 0;
+  uint64_t* ring_full = bars + 1;   // [2]
+  uint64_t* ring_empty = bars + 3;  // [2]
+  uint64_t* sdp_full = bars + 5;    // [2]
+  uint64_t* pd_full = bars + 7;     // [2]
+  uint64_t* pd_empty = bars + 9;    // [2]
+  uint64_t* kf_ready = bars + 11;
+  uint64_t* all_done = bars + 12;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int j = blockIdx.x;
+  const long long u = blockIdx.y;
+  const long long ucol = u * p.Tn + j;
+  const int cnt = p.ccol_cnt[ucol];
+  const int* list = p.ccol_idx + ucol * p.Tm;
+  // does any block row see column j as marginal?
+  __shared__ int s_lin;
+  if (threadIdx.x == 0) s_lin = 0;
+  __syncthreads();
+  {
+    const int8_t* lu = p.labels + u * (long long)p.Tm * p.Tn;
+    int any = 0;
+    for (int ii = threadIdx.x; ii < p.Tm; ii += blockDim.x) any |= lu[(long long)ii * p.Tn + j] == 0;
+    if (any) s_lin = 1;
+  }
+  __syncthreads();
+  const bool has_lin = s_lin != 0;
+  const int kv0 = int(u * p.N) + j * 64;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::mbar_init(kv_full, 1);
+      for (int s = 0; s < 2; ++s) {
+        tc::mbar_init(ring_full + s, 1);
+        tc::mbar_init(ring_empty + s, 1);
+        tc::mbar_init(sdp_full + s, 1);
+        tc::mbar_init(pd_full + s, 4);
+        tc::mbar_init(pd_empty + s, 1);
+      }
+      tc::mbar_init(kf_ready, 4);
+      tc::mbar_init(all_done, 1);
+      tc::fence_barrier_init();
+    }
+    __syncwarp();
+    tc::tmem_alloc<512>(tmem_slot);
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tDK = tmem, tDV = tmem + 128, tB0 = tmem + 256, tB1 = tmem + 384;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::mbar_expect_tx(kv_full, 2 * L::kT);
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        tc::tma_load_3d(sK + c * 8192, &tmK, kv_full, 64 * c, kv0, 0);
+        tc::tma_load_3d(sV + c * 8192, &tmV, kv_full, 64 * c, kv0, 0);
+      }
+      int item = 0;
+      auto acquire = [&](int bytes) -> uint8_t* {
+        const int s = item & 1;
+        tc::mbar_wait(ring_empty + s, ((item >> 1) & 1) ^ 1);
+        tc::mbar_expect_tx(ring_full + s, bytes);
+        return sRing + s * L::kStage;
+      };
+      for (int t = 0; t < cnt; ++t) {
+        const int q_row = int(u * p.N) + list[t] * 64;
+        uint8_t* dst = acquire(2 * L::kT);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) {
+          tc::tma_load_3d(dst + c * 8192, &tmQ, ring_full + (item & 1), 64 * c, q_row, 0);
+          tc::tma_load_3d(dst + L::kT + c * 8192, &tmDO, ring_full + (item & 1), 64 * c, q_row, 0);
+        }
+        ++item;
+      }
+      if (has_lin) {
+        uint8_t* dst = acquire(D * D * 2);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c)
+          tc::tma_load_3d(dst + c * D * 128, &tmHa, ring_full + (item & 1), 64 * c, int(ucol * D), 0);
+        ++item;
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t aK = tc::smem_u32(sK), aV = tc::smem_u32(sV), aKF = tc::smem_u32(sKF);
+    const uint32_t aR = tc::smem_u32(sRing), aPD = tc::smem_u32(sPD);
+    constexpr uint32_t id_ss = tc::idesc_bf16(64, 64, false, false);
+    constexpr uint32_t id_nd_kn = tc::idesc_bf16(64, D, false, true);
+    constexpr uint32_t id_nd_kk = tc::idesc_bf16(64, D, false, false);
+    int item = 0;
+    auto wait_item = [&]() -> uint32_t {
+      const int s = item & 1;
+      tc::mbar_wait(ring_full + s, (item >> 1) & 1);
+      tc::tc_fence_after();
+      return aR + s * L::kStage;
+    };
+    auto kdesc = [](uint32_t base, int kk, int rows) {
+      return tc::desc_kmajor(base + (kk >> 2) * rows * 128 + (kk & 3) * 32);
+    };
+    tc::mbar_wait(kv_full, 0);
+    tc::tc_fence_after();
+    auto issue_acc = [&](int t) {  // dV += P^T dO_t, dK += dS^T Q_t
+      tc::mbar_wait(pd_full + (t & 1), (t >> 1) & 1);
+      tc::tc_fence_after();
+      const uint32_t sq = aR + (t & 1) * L::kStage;
+      if (lane == 0) {
+        const uint32_t sp = aPD + (t & 1) * 16384, sd = sp + 8192;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          tc::mma_bf16(tDV, tc::desc_kmajor(sp + kk * 32), tc::desc_mnmajor(sq + L::kT + kk * 2048, 8192), id_nd_kn,
+                       (t | kk) != 0);
+          tc::mma_bf16(tDK, tc::desc_kmajor(sd + kk * 32), tc::desc_mnmajor(sq + kk * 2048, 8192), id_nd_kn,
+                       (t | kk) != 0);
+        }
+        tc::mma_commit(ring_empty + (t & 1));
+        tc::mma_commit(pd_empty + (t & 1));
+      }
+      __syncwarp();
+    };
+    for (int t = 0; t < cnt; ++t) {
+      const uint32_t sq = wait_item();
+      if (lane == 0) {
+        const uint32_t tb = (t & 1) ? tB1 : tB0;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          tc::mma_bf16(tb, kdesc(aK, kk, 64), kdesc(sq, kk, 64), id_ss, kk > 0);            // S^T = K Q^T
+          tc::mma_bf16(tb + 64, kdesc(aV, kk, 64), kdesc(sq + L::kT, kk, 64), id_ss, kk > 0); // dP^T = V dO^T
+        }
+        tc::mma_commit(sdp_full + (t & 1));
+      }
+      __syncwarp();
+      ++item;
+      if (t > 0) issue_acc(t - 1);
+    }
+    if (cnt > 0) issue_acc(cnt - 1);
+    if (has_lin) {
+      const uint32_t sh = wait_item();
+      tc::mbar_wait(kf_ready, 0);
+      tc::tc_fence_after();
+      if (lane == 0) {
+        // dK^phi raw = V dH_agg^T -> B0 ; dV += phi(K) dH_agg
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          tc::mma_bf16(tB0, kdesc(aV, kk, 64), kdesc(sh, kk, D), id_nd_kk, kk > 0);
+          tc::mma_bf16(tDV, kdesc(aKF, kk, 64), tc::desc_mnmajor(sh + kk * 2048, D * 128), id_nd_kn,
+                       (cnt > 0 || kk > 0) ? 1u : 0u);
+        }
+        tc::mma_commit(ring_empty + (item & 1));
+      }
+      __syncwarp();
+      ++item;
+    }
+    if (lane == 0) tc::mma_commit(all_done);
+    __syncwarp();
+  } else {
+    const int q4 = warp & 3;
+    const int c = 16 * q4 + lane;  // key row within the block
+    const bool valid = lane < 16;
+    const int cc = c & 63;
+    const uint32_t lane_base = uint32_t(32 * q4) << 16;
+    const long long grow = (long long)kv0 + c;
+    tc::mbar_wait(kv_full, 0);
+    RowPhi<D> ph;
+    ph.stats(sK, cc, p.phi);
+    if (has_lin) {  // phi(K_j) in bf16, A operand of phi(K) dH_agg
+      if (valid) {
+#pragma unroll
+        for (int ch = 0; ch < D / 8; ++ch) {
+          float f[8];
+          unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, 8 * ch)), f);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) f[e] = ph.phi_of(f[e], p.phi);
+          *reinterpret_cast<uint4*>(sKF + tile_off(c, 8 * ch)) = pack8(f);
+        }
+      }
+      tc::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(kf_ready);
+    }
+    const int ct = threadIdx.x - 64;  // 0..127
+    for (int t = 0; t < cnt; ++t) {
+      const long long qrow0 = u * p.N + (long long)list[t] * 64;
+      float* ls = sLS + (t & 1) * 128;
+      // stage lse*log2e and D^s of the 64 query rows (buffer t&1 is free: its last reader
+      // finished iteration t-2 before the named barrier of iteration t-1)
+      if (ct < 64) ls[ct] = p.lse[qrow0 + ct] * 1.4426950408889634f;
+      else ls[ct] = p.Ds[qrow0 + ct - 64];
+      named_sync(1, 128);
+      tc::mbar_wait(sdp_full + (t & 1), (t >> 1) & 1);
+      tc::tc_fence_after();
+      const uint32_t tb = ((t & 1) ? tB1 : tB0) + lane_base;
+      uint32_t pk[32], dk[32];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t s[32], dp[32];
+        tc::tmem_ld32(tb + 32 * h, s);
+        tc::tmem_ld32(tb + 64 + 32 * h, dp);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const int r0 = 32 * h + e;
+          const float p0 = ex2f(__uint_as_float(s[e]) * p.scale_log2 - ls[r0]);
+          const float p1 = ex2f(__uint_as_float(s[e + 1]) * p.scale_log2 - ls[r0 + 1]);
+          const float d0 = p0 * (__uint_as_float(dp[e]) - ls[64 + r0]) * p.scale;
+          const float d1 = p1 * (__uint_as_float(dp[e + 1]) - ls[64 + r0 + 1]) * p.scale;
+          pk[16 * h + (e >> 1)] = tc::pack_bf16(p0, p1);
+          dk[16 * h + (e >> 1)] = tc::pack_bf16(d0, d1);
+        }
+      }
+      if (t >= 2) tc::mbar_wait(pd_empty + (t & 1), ((t - 2) >> 1) & 1);
+      if (valid) {
+        uint8_t* prow = sPD + (t & 1) * 16384;
+#pragma unroll
+        for (int ch = 0; ch < 8; ++ch) {
+          *reinterpret_cast<uint4*>(prow + tc::sw128_off(c, ch)) =
+              make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+          *reinterpret_cast<uint4*>(prow + 8192 + tc::sw128_off(c, ch)) =
+              make_uint4(dk[4 * ch], dk[4 * ch + 1], dk[4 * ch + 2], dk[4 * ch + 3]);
+        }
+      }
+      tc::fence_proxy_async();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(pd_full + (t & 1));
+    }
+    tc::mbar_wait(all_done, 0);
+    tc::tc_fence_after();
+    // dk_total = J_phi(k)^T dK^phi + dK, dK^phi = raw + dZ_agg (broadcast over the rows)
+    const float* dza = p.gZa + ucol * D;
+    float dot = 0.f;
+    if (p.phi == 2 && has_lin) {
+#pragma unroll 1
+      for (int c0 = 0; c0 < D; c0 += 32) {
+        uint32_t a[32];
+        tc::tmem_ld32(tB0 + lane_base + c0, a);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int ch = 0; ch < 4; ++ch) {
+          float f[8];
+          unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(cc, c0 + 8 * ch)), f);
+#pragma unroll
+          for (int e = 0; e < 8; ++e)
+            dot = fmaf(ph.phi_of(f[e], 2), __uint_as_float(a[8 * ch + e]) + __ldg(dza + c0 + 8 * ch + e), dot);
+        }
+      }
+    }
+#pragma unroll 1
+    for (int c0 = 0; c0 < D; c0 += 32) {
+      uint32_t a[32], b[32], v[32];
+      if (has_lin) tc::tmem_ld32(tB0 + lane_base + c0, a);
+      if (cnt > 0) tc::tmem_ld32(tDK + lane_base + c0, b);
+      if (cnt > 0 || has_lin) tc::tmem_ld32(tDV + lane_base + c0, v);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch) {
+        float f[8], o[8], w8[8];
+        unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(cc, c0 + 8 * ch)), f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int col = c0 + 8 * ch + e;
+          const float g = has_lin ? __uint_as_float(a[8 * ch + e]) + __ldg(dza + col) : 0.f;
+          float jg;
+          if (p.phi == 2) jg = ph.phi_of(f[e], 2) * (g - dot);
+          else if (p.phi == 0) jg = f[e] >= 0.f ? g : __expf(f[e]) * g;
+          else jg = f[e] > 0.f ? g : 0.f;
+          o[e] = jg + (cnt > 0 ? __uint_as_float(b[8 * ch + e]) : 0.f);
+          w8[e] = (cnt > 0 || has_lin) ? __uint_as_float(v[8 * ch + e]) : 0.f;
+        }
+        if (valid) {
+          *reinterpret_cast<uint4*>(p.dk + grow * D + c0 + 8 * ch) = pack8(o);
+          *reinterpret_cast<uint4*>(p.dv + grow * D + c0 + 8 * ch) = pack8(w8);
+        }
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(tmem);
+}
+
+template <int D>
+void launch_rows_t(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
+                   const void* d_out, const __nv_bfloat16* Hb, BwdParams p, cudaStream_t st) {
+  CUtensorMap tq, tdo, tk, tv, tw, th;
+  const uint64_t rows = uint64_t(Dm.U) * Dm.N;
+  make_tmap_bf16(&tq, q, D, rows, 1, D, 0, 64);
+  make_tmap_bf16(&tdo, d_out, D, rows, 1, D, 0, 64);
+  make_tmap_bf16(&tk, k, D, rows, 1, D, 0, 64);
+  make_tmap_bf16(&tv, v, D, rows, 1, D, 0, 64);
+  make_tmap_bf16(&tw, w, D, uint64_t(Dm.H) * D, 1, D, 0, D);
+  make_tmap_bf16(&th, Hb, D, uint64_t(Dm.U) * Dm.Tm * D, 1, D, 0, D);
+  auto kern = k_bwd_rows<D>;
+  SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, RowsLayout<D>::kBytes));
+  kern<<<dim3(Dm.Tm, unsigned(Dm.U)), 192, RowsLayout<D>::kBytes, st>>>(tq, tdo, tk, tv, tw, th, p);
+  check_launch("k_bwd_rows", st);
+}
+
+template <int D>
+void launch_cols_t(const Dims& Dm, const void* q, const void* k, const void* v, const void* d_out,
+                   const __nv_bfloat16* Ha, BwdParams p, cudaStream_t st) {
+  CUtensorMap tq, tdo, tk, tv, th;
+  const uint64_t rows = uint64_t(Dm.U) * Dm.N;
+  make_tmap_bf16(&tq, q, D, rows, 1, D, 0, 64);
+  make_tmap_bf16(&tdo, d_out, D, rows, 1, D, 0, 64);
+  make_tmap_bf16(&tk, k, D, rows, 1, D, 0, 64);
+  make_tmap_bf16(&tv, v, D, rows, 1, D, 0, 64);
+  make_tmap_bf16(&th, Ha, D, uint64_t(Dm.U) * Dm.Tn * D, 1, D, 0, D);
+  auto kern = k_bwd_cols<D>;
+  SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ColsLayout<D>::kBytes));
+  kern<<<dim3(Dm.Tn, unsigned(Dm.U)), 192, ColsLayout<D>::kBytes, st>>>(tq, tdo, tk, tv, th, p);
+  check_launch("k_bwd_cols", st);
+}
+
+}  // namespace
+
+void launch_bwd_rows(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
+                     const void* o_s, const void* o_l, const float* lse, const void* d_out, void* dq,
+                     const StateBufs& s, __nv_bfloat16* gH, float* gZ, float* Ds, cudaStream_t st) {
+  BwdParams p{};
+  p.crit_cnt = s.crit_cnt;
+  p.crit_idx = s.crit_idx;
+  p.marg_cnt = s.marg_cnt;
+  p.Z = s.Z;
+  p.lse = lse;
+  p.Ds_out = Ds;
+  p.o_s = static_cast<const __nv_bfloat16*>(o_s);
+  p.o_l = static_cast<const __nv_bfloat16*>(o_l);
+  p.gH = gH;
+  p.gZ = gZ;
+  p.dq = static_cast<__nv_bfloat16*>(dq);
+  p.N = Dm.N;
+  p.Tm = Dm.Tm;
+  p.Tn = Dm.Tn;
+  p.H = int(Dm.H);
+  p.scale = float(Dm.inv_sqrt_d);
+  p.scale_log2 = float(Dm.inv_sqrt_d * 1.4426950408889634);
+  p.phi = Dm.phi;
+  if (Dm.d == 128)
+    launch_rows_t<128>(Dm, q, k, v, w, d_out, s.Hb, p, st);
+  else
+    launch_rows_t<64>(Dm, q, k, v, w, d_out, s.Hb, p, st);
+}
+
+void launch_bwd_cols(const Dims& Dm, const void* q, const void* k, const void* v, const float* lse,
+                     const void* d_out, void* dk, void* dv, const StateBufs& s,
+                     const __nv_bfloat16* Ha, const float* gZa, const float* Ds, cudaStream_t st) {
+  BwdParams p{};
+  p.ccol_cnt = s.ccol_cnt;
+  p.ccol_idx = s.ccol_idx;
+  p.labels = s.labels;
+  p.lse = lse;
+  p.Ds = Ds;
+  p.gZa = gZa;
+  p.dk = static_cast<__nv_bfloat16*>(dk);
+  p.dv = static_cast<__nv_bfloat16*>(dv);
+  p.N = Dm.N;
+  p.Tm = Dm.Tm;
+  p.Tn = Dm.Tn;
+  p.H = int(Dm.H);
+  p.scale = float(Dm.inv_sqrt_d);
+  p.scale_log2 = float(Dm.inv_sqrt_d * 1.4426950408889634);
+  p.phi = Dm.phi;
+  if (Dm.d == 128)
+    launch_cols_t<128>(Dm, q, k, v, d_out, Ha, p, st);
+  else
+    launch_cols_t<64>(Dm, q, k, v, d_out, Ha, p, st);
+}
+
+}  // namespace slab

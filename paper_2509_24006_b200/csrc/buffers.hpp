@@ -51,7 +51,19 @@ struct WorkBufs {
   float* dkf = nullptr;      // dK^phi
   __nv_bfloat16* hb = nullptr;   // fast path: h in bf16, [U, Tn, d*d]
   __nv_bfloat16* kfb = nullptr;  // fast path: phi(K) in bf16, [U, N, d]
+  __nv_bfloat16* hab = nullptr;  // fast path: dH_agg = M0^T dH in bf16, [U, Tn, d*d]
+  float* gZa = nullptr;          // fast path: dZ_agg [U, Tn, d]
+  float* dwp = nullptr;          // fast path: split-K partials of dW [U * N / 64, d, d]
 };
+
+// split-K factor of the fast path's dW GEMM: row chunks of 64*c rows, c | N/64, c <= 32
+inline int dw_chunk_tiles(const Dims& D) {
+  const long long tiles = D.N / 64;
+  for (int c = 32; c > 1; c >>= 1)
+    if (tiles % c == 0) return c;
+  return 1;
+}
+inline long long dw_chunks(const Dims& D) { return D.N / (64LL * dw_chunk_tiles(D)); }
 
 // Bump allocator: with base == nullptr it only measures.
 struct Carver {
@@ -92,6 +104,7 @@ inline void carve_work(const Dims& D, bool fast, void* base, WorkBufs& w, size_t
   w.err = c.take<long long>(8);
   w.pq = c.take<double>(U * Tm * d);
   w.pk = c.take<double>(U * Tn * d);
+  w.p_c = c.take<double>(U * Tm * Tn);  // pooled scores (f64 or f32 storage)
   w.z = c.take<float>(U * Tn * d);
   w.Ds = c.take<float>(U * N);
   w.Dl = c.take<float>(U * N);
@@ -108,6 +121,9 @@ inline void carve_work(const Dims& D, bool fast, void* base, WorkBufs& w, size_t
   if (fast) {
     w.hb = c.take<__nv_bfloat16>(U * Tn * d * d);
     w.kfb = c.take<__nv_bfloat16>(U * N * d);
+    w.hab = c.take<__nv_bfloat16>(U * Tn * d * d);
+    w.gZa = c.take<float>(U * Tn * d);
+    w.dwp = c.take<float>(U * dw_chunks(D) * d * d);
   } else {
     w.h = c.take<float>(U * Tn * d * d);
   }

@@ -54,38 +54,84 @@ __global__ void k_pool(const In* __restrict__ x, R* __restrict__ out, long long 
 // (weight desc, column asc) -- exactly std::stable_sort's order from an iota start
 // (mask.cpp:105-113) -- and the label / lookup writes (mask.cpp:114-153).
 // ---------------------------------------------------------------------------------------
+// K1b: pooled scores S = pool(Q) pool(K)^T * (1/sqrt(d)) for all block pairs, tiled 64x64
+// per CTA (each thread a 4x4 patch).  Every element is still ONE sequential ascending-c dot
+// with separately rounded mul and add (mat.hpp:83-97), so the values are bit-identical to
+// the reference's; tiling only shares the pooled rows through shared memory.
+template <typename R>
+__global__ void __launch_bounds__(256) k_scores(const R* __restrict__ pq, const R* __restrict__ pk,
+                                                int d, int Tm, int Tn, R inv_sqrt_d,
+                                                R* __restrict__ s) {
+  constexpr int CK = 32;
+  __shared__ R sa[64][CK + 1];
+  __shared__ R sb[64][CK + 1];
+  const long long u = blockIdx.z;
+  const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  R acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) acc[a][b] = R(0);
+  const R* pqu = pq + u * (long long)Tm * d;
+  const R* pku = pk + u * (long long)Tn * d;
+  for (int c0 = 0; c0 < d; c0 += CK) {
+    const int ck = min(CK, d - c0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < 64 * CK; e += 256) {
+      const int r = e / CK, c = e % CK;
+      sa[r][c] = (i0 + r < Tm && c < ck) ? pqu[(long long)(i0 + r) * d + c0 + c] : R(0);
+      sb[r][c] = (j0 + r < Tn && c < ck) ? pku[(long long)(j0 + r) * d + c0 + c] : R(0);
+    }
+    __syncthreads();
+    for (int c = 0; c < ck; ++c) {
+      R av[4], bv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) av[a] = sa[ty * 4 + a][c];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) bv[b] = sb[tx * 4 + b][c];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = add_rn(acc[a][b], mul_rn(av[a], bv[b]));
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 4; ++a) {
+    const int i = i0 + ty * 4 + a;
+    if (i >= Tm) continue;
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      const int j = j0 + tx * 4 + b;
+      if (j < Tn) s[(u * Tm + i) * (long long)Tn + j] = mul_rn(acc[a][b], inv_sqrt_d);
+    }
+  }
+}
+
 template <typename R>
 __device__ __forceinline__ bool before(R ka, int ia, R kb, int ib) {
   return ka > kb || (ka == kb && ia < ib);
 }
 
 template <typename R>
-__global__ void k_classify(const R* __restrict__ pq, const R* __restrict__ pk, int d, int Tm,
-                           int Tn, int P2, int n1, int n_neg, R inv_sqrt_d,
+__global__ void k_classify(const R* __restrict__ scores, int Tm,
+                           int Tn, int P2, int n1, int n_neg,
                            int8_t* __restrict__ labels, int* __restrict__ crit_cnt,
                            int* __restrict__ crit_idx, int* __restrict__ marg_cnt,
                            double* __restrict__ p_c_out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   R* key = reinterpret_cast<R*>(smem_raw);                   // [P2]
-  R* qrow = key + P2;                                         // [d]
-  int* idx = reinterpret_cast<int*>(qrow + d);                // [P2]
+  int* idx = reinterpret_cast<int*>(key + P2);                // [P2]
   int8_t* lab = reinterpret_cast<int8_t*>(idx + P2);          // [Tn]
   __shared__ R red[32];
 
   const long long u = blockIdx.y;
   const int i = blockIdx.x;
   const int tid = threadIdx.x, nt = blockDim.x;
-  const R* pku = pk + u * (long long)Tn * d;
-  for (int c = tid; c < d; c += nt) qrow[c] = pq[(u * Tm + i) * d + c];
-  __syncthreads();
-
-  // scores
+  const R* srow = scores + (u * Tm + i) * (long long)Tn;
   R lmax = -R(INFINITY);
   for (int j = tid; j < Tn; j += nt) {
-    const R* kr = pku + (long long)j * d;
-    R acc = R(0);
-    for (int c = 0; c < d; ++c) acc = add_rn(acc, mul_rn(qrow[c], kr[c]));
-    const R s = mul_rn(acc, inv_sqrt_d);
+    const R s = srow[j];
     key[j] = s;
     lmax = s > lmax ? s : lmax;
   }
@@ -243,7 +289,7 @@ static int next_pow2(int x) {
 size_t classify_smem_bytes(const Dims& D, bool f64) {
   const int P2 = next_pow2(D.Tn);
   const size_t rs = f64 ? 8 : 4;
-  return rs * (P2 + D.d) + 4 * size_t(P2) + size_t(D.Tn) + 16;
+  return rs * P2 + 4 * size_t(P2) + size_t(D.Tn) + 16;
 }
 
 template <typename In>
@@ -276,8 +322,12 @@ static void classify_t(const Dims& D, const In* q, const In* k, const StateBufs&
   if (smem > 48 * 1024)
     SLAB_CUDA(cudaFuncSetAttribute(k_classify<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(smem)));
+  R* scores = reinterpret_cast<R*>(w.p_c);
+  k_scores<R><<<dim3((D.Tn + 63) / 64, (D.Tm + 63) / 64, unsigned(D.U)), 256, 0, st>>>(
+      pq, pk, D.d, D.Tm, D.Tn, R(D.inv_sqrt_d), scores);
+  check_launch("k_scores", st);
   k_classify<R><<<dim3(D.Tm, unsigned(D.U)), 256, smem, st>>>(
-      pq, pk, D.d, D.Tm, D.Tn, next_pow2(D.Tn), D.n1, D.n_neg, R(D.inv_sqrt_d), s.labels,
+      scores, D.Tm, D.Tn, next_pow2(D.Tn), D.n1, D.n_neg, s.labels,
       s.crit_cnt, s.crit_idx, s.marg_cnt, p_c);
   check_launch("k_classify", st);
 }

@@ -69,32 +69,83 @@ __global__ void __launch_bounds__(256) k_phi_kz(const __nv_bfloat16* __restrict_
   }
 }
 
-// Z_i = sum_{j marginal, ascending} z_j (aggregation.cpp:40-56); grid (Tm, U), D threads.
+// Z_i = sum_{j marginal, ascending} z_j (aggregation.cpp:40-56).  grid (ceil(Tm/16), U),
+// d threads; 16 block rows per CTA share every z_j read; labels staged per 1024 columns.
 __global__ void k_aggregate_z(const int8_t* __restrict__ labels, const float* __restrict__ z,
                               int d, int Tm, int Tn, float* __restrict__ Z) {
-  extern __shared__ int slist[];
-  __shared__ int s_cnt;
+  constexpr int R = 16, JC = 1024;
+  __shared__ int8_t lab[R][JC];
   const long long u = blockIdx.y;
-  const int i = blockIdx.x;
-  if (threadIdx.x < 32) {
-    const int8_t* lrow = labels + (u * Tm + i) * (long long)Tn;
-    int base = 0;
-    for (int j0 = 0; j0 < Tn; j0 += 32) {
-      const int j = j0 + threadIdx.x;
-      const bool m = j < Tn && lrow[j] == 0;
-      const unsigned b = __ballot_sync(0xffffffffu, m);
-      if (m) slist[base + __popc(b & ((1u << threadIdx.x) - 1u))] = j;
-      base += __popc(b);
-    }
-    if (threadIdx.x == 0) s_cnt = base;
-  }
-  __syncthreads();
-  const int cnt = s_cnt;
+  const int i0 = blockIdx.x * R;
+  const int a = threadIdx.x;
+  float acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = 0.f;
   const float* zu = z + u * (long long)Tn * d;
-  for (int a = threadIdx.x; a < d; a += blockDim.x) {
+  for (int jc = 0; jc < Tn; jc += JC) {
+    const int jn = min(JC, Tn - jc);
+    __syncthreads();
+    for (int e = threadIdx.x; e < R * JC; e += blockDim.x) {
+      const int r = e / JC, j = e % JC;
+      lab[r][j] = (i0 + r < Tm && j < jn) ? labels[(u * Tm + i0 + r) * (long long)Tn + jc + j] : int8_t(-1);
+    }
+    __syncthreads();
+    for (int j = 0; j < jn; ++j) {
+      const float zj = zu[(long long)(jc + j) * d + a];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (lab[r][j] == 0) acc[r] += zj;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (i0 + r < Tm) Z[(u * Tm + i0 + r) * d + a] = acc[r];
+}
+
+// dZ_agg_j = sum_{i: label(i,j) = 0, ascending} dZ_i (backward.cpp:170-178); grid
+// (ceil(Tn/16), U), d threads; 16 key columns per CTA.
+__global__ void k_aggregate_dz_cols(const int8_t* __restrict__ labels, const float* __restrict__ gz,
+                                    int d, int Tm, int Tn, float* __restrict__ out) {
+  constexpr int R = 16;
+  __shared__ int8_t lab[1024][R];
+  const long long u = blockIdx.y;
+  const int j0 = blockIdx.x * R;
+  const int a = threadIdx.x;
+  float acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = 0.f;
+  const float* gu = gz + u * (long long)Tm * d;
+  for (int ic = 0; ic < Tm; ic += 1024) {
+    const int in = min(1024, Tm - ic);
+    __syncthreads();
+    for (int e = threadIdx.x; e < 1024 * R; e += blockDim.x) {
+      const int i = e / R, r = e % R;
+      lab[i][r] = (i < in && j0 + r < Tn) ? labels[(u * Tm + ic + i) * (long long)Tn + j0 + r] : int8_t(-1);
+    }
+    __syncthreads();
+    for (int i = 0; i < in; ++i) {
+      const float g = gu[(long long)(ic + i) * d + a];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+        if (lab[i][r] == 0) acc[r] += g;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (j0 + r < Tn) out[(u * Tn + j0 + r) * d + a] = acc[r];
+}
+
+// dW[h] = sum over the batch and the split-K chunks of O^l^T dO (backward.cpp:46).
+__global__ void k_reduce_dw(const float* __restrict__ part, int chunks_per_unit, long long B,
+                            long long H, int dd, float* __restrict__ dw) {
+  const int h = blockIdx.y;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < dd; e += gridDim.x * blockDim.x) {
     float acc = 0.f;
-    for (int p = 0; p < cnt; ++p) acc += zu[(long long)slist[p] * d + a];
-    Z[(u * Tm + i) * d + a] = acc;
+    for (long long b = 0; b < B; ++b) {
+      const long long u = b * H + h;
+      for (int c = 0; c < chunks_per_unit; ++c) acc += part[(u * chunks_per_unit + c) * (long long)dd + e];
+    }
+    dw[(long long)h * dd + e] = acc;
   }
 }
 
@@ -155,8 +206,8 @@ void fast_prepare_linear(const Dims& Dm, const void* k, const void* v, const Sta
   a.c_batch = (long long)Dm.Tm * d * d;
   a.name = "gemm_aggregate";
   launch_gemm(a, st);
-  k_aggregate_z<<<dim3(Dm.Tm, unsigned(Dm.U)), d, size_t(Dm.Tn) * 4, st>>>(s.labels, wb.z, d, Dm.Tm,
-                                                                            Dm.Tn, s.Z);
+  k_aggregate_z<<<dim3((Dm.Tm + 15) / 16, unsigned(Dm.U)), d, 0, st>>>(s.labels, wb.z, d, Dm.Tm,
+                                                                        Dm.Tn, s.Z);
   check_launch("k_aggregate_z", st);
 }
 
@@ -171,8 +222,59 @@ void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, 
                    const void* o_s, const void* o_l, const float* lse, const void* d_out,
                    void* dq, void* dk, void* dv, float* dw, const StateBufs& s,
                    const WorkBufs& wb, cudaStream_t st) {
-  // first fast-path revision: the SIMT backward over the fast path's bf16 H state
-  generic_backward(Dm, 0, q, k, v, w, o_s, o_l, lse, d_out, dq, dk, dv, dw, s, wb, st);
+  const int d = Dm.d;
+  launch_build_csc(Dm, s, st);
+  // rows pass: dq_total, dH_i (bf16, reusing the forward's h scratch), dZ_i, D^s
+  launch_bwd_rows(Dm, q, k, v, w, o_s, o_l, lse, d_out, dq, s, wb.hb, wb.gZ, wb.Ds, st);
+  // dH_agg = M0^T dH (A = M0 read M-major), dZ_agg
+  GemmArgs a{};
+  a.A = s.M0;
+  a.B = wb.hb;
+  a.C = wb.hab;
+  a.batch = int(Dm.U);
+  a.M = Dm.Tn;
+  a.N = d * d;
+  a.K = Dm.Tm;
+  a.a_mn = true;
+  a.b_mn = true;
+  a.out_f32 = false;
+  a.lda = m0_stride(Dm);
+  a.ldb = (long long)d * d;
+  a.ldc = (long long)d * d;
+  a.a_batch = (long long)Dm.Tm * m0_stride(Dm);
+  a.b_batch = (long long)Dm.Tm * d * d;
+  a.c_batch = (long long)Dm.Tn * d * d;
+  a.name = "gemm_aggregate_t";
+  launch_gemm(a, st);
+  k_aggregate_dz_cols<<<dim3((Dm.Tn + 15) / 16, unsigned(Dm.U)), d, 0, st>>>(s.labels, wb.gZ, d, Dm.Tm,
+                                                                            Dm.Tn, wb.gZa);
+  check_launch("k_aggregate_dz_cols", st);
+  // columns pass: dk_total, dv
+  launch_bwd_cols(Dm, q, k, v, lse, d_out, dk, dv, s, wb.hab, wb.gZa, wb.Ds, st);
+  // dW = O^l^T dO per head, split-K over row chunks of each unit, then reduced over chunks + batch
+  const long long KC = 64LL * dw_chunk_tiles(Dm);
+  const int chunks = int(dw_chunks(Dm));
+  GemmArgs g{};
+  g.A = o_l;
+  g.B = d_out;
+  g.C = wb.dwp;
+  g.batch = int(Dm.U * chunks);
+  g.M = d;
+  g.N = d;
+  g.K = int(KC);
+  g.a_mn = true;
+  g.b_mn = true;
+  g.out_f32 = true;
+  g.lda = d;
+  g.ldb = d;
+  g.ldc = d;
+  g.a_batch = KC * d;
+  g.b_batch = KC * d;
+  g.c_batch = (long long)d * d;
+  g.name = "gemm_dw";
+  launch_gemm(g, st);
+  k_reduce_dw<<<dim3((d * d + 255) / 256, unsigned(Dm.H)), 256, 0, st>>>(wb.dwp, chunks, Dm.B, Dm.H, d * d, dw);
+  check_launch("k_reduce_dw", st);
 }
 
 }  // namespace slab

@@ -44,6 +44,12 @@ void launch_attn_fwd(const Dims& Dm, const void* q, const void* k, const void* v
                      void* o, void* o_s, void* o_l, float* lse, const StateBufs& s, cudaStream_t st);
 void fast_prepare_linear(const Dims& Dm, const void* k, const void* v, const StateBufs& s,
                          const WorkBufs& wb, cudaStream_t st);
+void launch_bwd_rows(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
+                     const void* o_s, const void* o_l, const float* lse, const void* d_out, void* dq,
+                     const StateBufs& s, __nv_bfloat16* gH, float* gZ, float* Ds, cudaStream_t st);
+void launch_bwd_cols(const Dims& Dm, const void* q, const void* k, const void* v, const float* lse,
+                     const void* d_out, void* dk, void* dv, const StateBufs& s,
+                     const __nv_bfloat16* Ha, const float* gZa, const float* Ds, cudaStream_t st);
 bool fast_supported(const Dims& D, int dtype);
 void fast_forward(const Dims& D, const void* q, const void* k, const void* v, const void* w,
                   void* o, void* o_s, void* o_l, float* lse, const StateBufs& s,
