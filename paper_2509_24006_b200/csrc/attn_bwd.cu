@@ -52,37 +52,6 @@ __device__ __forceinline__ uint32_t tile_off(int r, int col) {
   return uint32_t(col >> 6) * 8192u + tc::sw128_off(uint32_t(r), uint32_t((col >> 3) & 7));
 }
 
-// phi VJP of one row held in a K-major smem tile (feature_map.cpp:42-73): g -> J^T g.
-// Pass 1 computes the softmax statistics / <s, g>; callers supply g chunk-wise twice.
-template <int D>
-struct RowPhi {
-  float m = 0.f, inv = 0.f;  // softmax stats
-  __device__ void stats(const uint8_t* tile, int r, int phi) {
-    if (phi != 2) return;
-    float mx = -INFINITY;
-#pragma unroll
-    for (int c = 0; c < D / 8; ++c) {
-      float f[8];
-      unpack8(*reinterpret_cast<const uint4*>(tile + tile_off(r, 8 * c)), f);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) mx = fmaxf(mx, f[e]);
-    }
-    float s = 0.f;
-#pragma unroll
-    for (int c = 0; c < D / 8; ++c) {
-      float f[8];
-      unpack8(*reinterpret_cast<const uint4*>(tile + tile_off(r, 8 * c)), f);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) s += __expf(f[e] - mx);
-    }
-    m = mx;
-    inv = 1.f / s;
-  }
-  __device__ float phi_of(float x, int phi) const {
-    return phi == 2 ? __expf(x - m) * inv : phi_elem(phi, x);
-  }
-};
-
 struct BwdParams {
   const int* crit_cnt;
   const int* crit_idx;
@@ -117,12 +86,15 @@ template <int D>
 struct RowsLayout {
   static constexpr int kT = 64 * D * 2;
   static constexpr int oQ = 0, oDO = kT, oDOL = 2 * kT;
-  static constexpr int oRing = 3 * kT;
+  static constexpr int oDL = 3 * kT;            // [64][64] bf16: column 0 = D^l/den (N tail of dH)
+  static constexpr int oRing = 3 * kT + 8192;
   static constexpr int kStage = 2 * kT;  // K + V, or W / H_i (D*D*2)
-  static constexpr int oDS = oRing + 2 * kStage;  // 2 x 8 KB dS buffers, X aliases them
+  static constexpr int kStages = 4;
+  static constexpr int oDS = oRing + kStages * kStage;  // 2 x 8 KB dS buffers, X aliases them
   static constexpr int oDZ = oDS + 16384;          // float dz[D]
   static constexpr int oBar = oDZ + 4 * D;
   static constexpr int kBytes = oBar + 256 + 1024;
+  static_assert(kBytes <= 232448, "smem");
 };
 
 template <int D>
@@ -137,14 +109,16 @@ __global__ void __launch_bounds__(192, 1)
   uint8_t* sQ = smem + L::oQ;
   uint8_t* sDO = smem + L::oDO;
   uint8_t* sDOL = smem + L::oDOL;
+  uint8_t* sDL = smem + L::oDL;
   uint8_t* sRing = smem + L::oRing;
   uint8_t* sDS = smem + L::oDS;
-  uint8_t* sX = sDS;
-  float* dz = reinterpret_cast<float*>(smem + L::oDZ);
+  uint8_t* sX = sDS;  // phi(Q) tile (bf16), dead once dH is formed; aliases the dS buffers
+  float* zs = reinterpret_cast<float*>(smem + L::oDZ);  // Z_i staged in smem
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::oBar);
   uint64_t* qdo_full = bars + 0;
-  uint64_t* ring_full = bars + 1;   // [2]
-  uint64_t* ring_empty = bars + 3;  // [2]
+  constexpr int RS = L::kStages;
+  uint64_t* ring_full = bars + 16;        // [RS]
+  uint64_t* ring_empty = bars + 16 + RS;  // [RS]
   uint64_t* sdp_full = bars + 5;    // [2]
   uint64_t* ds_full = bars + 7;     // [2]
   uint64_t* ds_empty = bars + 9;    // [2]
@@ -153,7 +127,7 @@ __global__ void __launch_bounds__(192, 1)
   uint64_t* lin_done = bars + 13;
   uint64_t* dh_read = bars + 14;
   uint64_t* dq_done = bars + 15;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + 2 * RS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x;
@@ -167,9 +141,11 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0) {
     if (lane == 0) {
       tc::mbar_init(qdo_full, 1);
-      for (int s = 0; s < 2; ++s) {
+      for (int s = 0; s < RS; ++s) {
         tc::mbar_init(ring_full + s, 1);
         tc::mbar_init(ring_empty + s, 1);
+      }
+      for (int s = 0; s < 2; ++s) {
         tc::mbar_init(sdp_full + s, 1);
         tc::mbar_init(ds_full + s, 4);
         tc::mbar_init(ds_empty + s, 1);
@@ -200,8 +176,8 @@ __global__ void __launch_bounds__(192, 1)
       }
       int item = 0;
       auto acquire = [&](int bytes) -> uint8_t* {
-        const int s = item & 1;
-        tc::mbar_wait(ring_empty + s, ((item >> 1) & 1) ^ 1);
+        const int s = item % RS;
+        tc::mbar_wait(ring_empty + s, ((item / RS) & 1) ^ 1);
         tc::mbar_expect_tx(ring_full + s, bytes);
         return sRing + s * L::kStage;
       };
@@ -209,14 +185,14 @@ __global__ void __launch_bounds__(192, 1)
         uint8_t* dst = acquire(D * D * 2);
         const int h = int(u % p.H);
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c) tc::tma_load_3d(dst + c * D * 128, &tmW, ring_full + (item & 1), 64 * c, h * D, 0);
+        for (int c = 0; c < D / 64; ++c) tc::tma_load_3d(dst + c * D * 128, &tmW, ring_full + (item % RS), 64 * c, h * D, 0);
         ++item;
       }
       if (has_lin) {
         uint8_t* dst = acquire(D * D * 2);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c)
-          tc::tma_load_3d(dst + c * D * 128, &tmH, ring_full + (item & 1), 64 * c, int(urow * D), 0);
+          tc::tma_load_3d(dst + c * D * 128, &tmH, ring_full + (item % RS), 64 * c, int(urow * D), 0);
         ++item;
       }
       for (int t = 0; t < cnt; ++t) {
@@ -224,8 +200,8 @@ __global__ void __launch_bounds__(192, 1)
         uint8_t* dst = acquire(2 * L::kT);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
-          tc::tma_load_3d(dst + c * 8192, &tmK, ring_full + (item & 1), 64 * c, kv_row, 0);
-          tc::tma_load_3d(dst + L::kT + c * 8192, &tmV, ring_full + (item & 1), 64 * c, kv_row, 0);
+          tc::tma_load_3d(dst + c * 8192, &tmK, ring_full + (item % RS), 64 * c, kv_row, 0);
+          tc::tma_load_3d(dst + L::kT + c * 8192, &tmV, ring_full + (item % RS), 64 * c, kv_row, 0);
         }
         ++item;
       }
@@ -235,12 +211,12 @@ __global__ void __launch_bounds__(192, 1)
     const uint32_t aR = tc::smem_u32(sRing), aDS = tc::smem_u32(sDS);
     constexpr uint32_t id_nd_kk = tc::idesc_bf16(64, D, false, false);   // A K-major, B K-major
     constexpr uint32_t id_nd_kn = tc::idesc_bf16(64, D, false, true);    // B MN-major
-    constexpr uint32_t id_dh = tc::idesc_bf16(D, D, true, true);         // A, B MN-major
+    constexpr uint32_t id_dh = tc::idesc_bf16(D, D + 64, true, true);    // A, B MN-major
     constexpr uint32_t id_ss = tc::idesc_bf16(64, 64, false, false);
     int item = 0;
     auto wait_item = [&]() -> uint32_t {
-      const int s = item & 1;
-      tc::mbar_wait(ring_full + s, (item >> 1) & 1);
+      const int s = item % RS;
+      tc::mbar_wait(ring_full + s, (item / RS) & 1);
       tc::tc_fence_after();
       return aR + s * L::kStage;
     };
@@ -253,7 +229,7 @@ __global__ void __launch_bounds__(192, 1)
       if (lane == 0) {
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) tc::mma_bf16(tB0, kdesc(aDO, kk, 64), kdesc(sw, kk, D), id_nd_kk, kk > 0);
-        tc::mma_commit(ring_empty + (item & 1));
+        tc::mma_commit(ring_empty + (item % RS));
         tc::mma_commit(dol_done);
       }
       __syncwarp();
@@ -267,12 +243,13 @@ __global__ void __launch_bounds__(192, 1)
         // dQ^phi raw = dO^l H_i^T -> QPHI
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) tc::mma_bf16(tQPHI, kdesc(aDOL, kk, 64), kdesc(sh, kk, D), id_nd_kk, kk > 0);
-        // dH_i = x^T dO^l (M = D over a, N = D over b, K = 64 rows) -> B1
+        // [dH_i | -dZ_i] = phi(Q)^T [dO^l/den | D^l/den] (M = D over a, N = D + 64, K = 64
+        // rows) -> columns [128, 128 + D + 64) (B0/B1 are idle until dh_read)
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          tc::mma_bf16(tB1, tc::desc_mnmajor(aDS + kk * 2048, 8192), tc::desc_mnmajor(aDOL + kk * 2048, 8192), id_dh,
+          tc::mma_bf16(tB0, tc::desc_mnmajor(aDS + kk * 2048, 8192), tc::desc_mnmajor(aDOL + kk * 2048, 8192), id_dh,
                        kk > 0);
-        tc::mma_commit(ring_empty + (item & 1));
+        tc::mma_commit(ring_empty + (item % RS));
         tc::mma_commit(lin_done);
       }
       __syncwarp();
@@ -285,14 +262,14 @@ __global__ void __launch_bounds__(192, 1)
       tc::mbar_wait(ds_full + (j & 1), (j >> 1) & 1);
       tc::tc_fence_after();
       const int it = item0 + j;
-      const uint32_t sk = aR + (it & 1) * L::kStage;
+      const uint32_t sk = aR + (it % RS) * L::kStage;
       if (lane == 0) {
         const uint32_t sds = aDS + (j & 1) * 8192;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
           tc::mma_bf16(tDQ, tc::desc_kmajor(sds + kk * 32), tc::desc_mnmajor(sk + kk * 2048, 8192), id_nd_kn,
                        (j | kk) != 0);
-        tc::mma_commit(ring_empty + (it & 1));
+        tc::mma_commit(ring_empty + (it % RS));
         tc::mma_commit(ds_empty + (j & 1));
       }
       __syncwarp();
@@ -316,28 +293,71 @@ __global__ void __launch_bounds__(192, 1)
     if (lane == 0) tc::mma_commit(dq_done);
     __syncwarp();
   } else {
+    // all 128 threads share the SIMT work: row r = 16*q4 + (lane & 15), column half lane>>4;
+    // lanes 0-15 also own TMEM row r (M = 64 accumulator layout)
     const int q4 = warp & 3;
-    const int r = 16 * q4 + lane;
+    const int r = 16 * q4 + (lane & 15);
+    const int h0 = (lane >> 4) * (D / 2);
     const bool valid = lane < 16;
     const uint32_t lane_base = uint32_t(32 * q4) << 16;
     const long long grow = (long long)row0 + r;
-    const int rr = r & 63;
-    const long long growr = (long long)row0 + rr;  // in-bounds row for the idle lanes' reads
-    for (int a = threadIdx.x - 64; a < D; a += 128) dz[a] = 0.f;
+    const int tid = threadIdx.x - 64;
+    for (int a = tid; a < D; a += 128) zs[a] = has_lin ? p.Z[urow * D + a] : 0.f;
+    for (int e = tid; e < 64 * 7; e += 128)  // chunks 1..7 of the D^l/den tile are zero
+      *reinterpret_cast<uint4*>(sDL + tc::sw128_off(e / 7, 1 + e % 7)) = make_uint4(0, 0, 0, 0);
     named_sync(1, 128);
     tc::mbar_wait(qdo_full, 0);
-    // D^s = <dO, O^s>
+    // D^s = <dO, O^s> (backward.cpp:48-58)
     float ds_r = 0.f;
 #pragma unroll
-    for (int c = 0; c < D / 8; ++c) {
+    for (int c = 0; c < D / 2; c += 8) {
       float f[8], g[8];
-      unpack8(*reinterpret_cast<const uint4*>(sDO + tile_off(rr, 8 * c)), f);
-      unpack8(*reinterpret_cast<const uint4*>(p.o_s + growr * D + 8 * c), g);
+      unpack8(*reinterpret_cast<const uint4*>(sDO + tile_off(r, h0 + c)), f);
+      unpack8(*reinterpret_cast<const uint4*>(p.o_s + grow * D + h0 + c), g);
 #pragma unroll
       for (int e = 0; e < 8; ++e) ds_r = fmaf(f[e], g[e], ds_r);
     }
+    ds_r += __shfl_xor_sync(0xffffffffu, ds_r, 16);
     if (valid) p.Ds_out[grow] = ds_r;
-    // dO^l from TMEM -> D^l, and bf16 into sDOL
+    // phi(q) (feature_map.cpp:24-40) over this half row, den = phi(q) . Z_i
+    float mx = 0.f, inv = 1.f;
+    if (p.phi == 2) {
+      mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < D / 2; c += 8) {
+        float f[8];
+        unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(r, h0 + c)), f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) mx = fmaxf(mx, f[e]);
+      }
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+      float se = 0.f;
+#pragma unroll
+      for (int c = 0; c < D / 2; c += 8) {
+        float f[8];
+        unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(r, h0 + c)), f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) se += __expf(f[e] - mx);
+      }
+      se += __shfl_xor_sync(0xffffffffu, se, 16);
+      inv = 1.f / se;
+    }
+    auto phi_of = [&](float x) { return p.phi == 2 ? __expf(x - mx) * inv : phi_elem(p.phi, x); };
+    float den = 0.f;
+#pragma unroll
+    for (int c = 0; c < D / 2; c += 8) {
+      float f[8];
+      unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(r, h0 + c)), f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        f[e] = phi_of(f[e]);
+        den = fmaf(f[e], zs[h0 + c + e], den);
+      }
+      *reinterpret_cast<uint4*>(sX + tile_off(r, h0 + c)) = pack8(f);
+    }
+    den += __shfl_xor_sync(0xffffffffu, den, 16);
+    const float inv_den = (has_lin && den != 0.f) ? 1.f / den : 0.f;  // den == 0 -> zero row
+    // dO^l (TMEM, lanes 0-15) -> D^l = <dO^l, O^l>, sDOL = dO^l / den, sDL = D^l / den
     tc::mbar_wait(dol_done, 0);
     tc::tc_fence_after();
     float dl_r = 0.f;
@@ -346,52 +366,29 @@ __global__ void __launch_bounds__(192, 1)
       uint32_t a[32];
       tc::tmem_ld32(tB0 + lane_base + c0, a);
       tc::tmem_ld_wait();
+      if (valid) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float f[8], g[8];
+        for (int c = 0; c < 4; ++c) {
+          float f[8], g[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(a[8 * c + e]);
-        unpack8(*reinterpret_cast<const uint4*>(p.o_l + growr * D + c0 + 8 * c), g);
+          for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(a[8 * c + e]);
+          unpack8(*reinterpret_cast<const uint4*>(p.o_l + grow * D + c0 + 8 * c), g);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) dl_r = fmaf(f[e], g[e], dl_r);
-        if (valid) *reinterpret_cast<uint4*>(sDOL + tile_off(r, c0 + 8 * c)) = pack8(f);
+          for (int e = 0; e < 8; ++e) {
+            dl_r = fmaf(f[e], g[e], dl_r);
+            f[e] *= inv_den;
+          }
+          *reinterpret_cast<uint4*>(sDOL + tile_off(r, c0 + 8 * c)) = pack8(f);
+        }
       }
     }
-    // x = phi(q) / den (zero rows when den == 0 or no marginal block), dZ_i = -sum_r x D^l
-    RowPhi<D> ph;
-    ph.stats(sQ, rr, p.phi);
-    float den = 0.f;
-    const float* Zi = p.Z + urow * D;
-    if (has_lin) {
-#pragma unroll
-      for (int c = 0; c < D / 8; ++c) {
-        float f[8];
-        unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(rr, 8 * c)), f);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) den = fmaf(ph.phi_of(f[e], p.phi), __ldg(Zi + 8 * c + e), den);
-      }
-    }
-    const float inv_den = (has_lin && den != 0.f) ? 1.f / den : 0.f;
-#pragma unroll 1
-    for (int c = 0; c < D / 8; ++c) {
-      float f[8];
-      unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(rr, 8 * c)), f);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) f[e] = valid ? ph.phi_of(f[e], p.phi) * inv_den : 0.f;
-      if (valid) *reinterpret_cast<uint4*>(sX + tile_off(r, 8 * c)) = pack8(f);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        float v = -f[e] * dl_r;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-        if (lane == 0) atomicAdd(dz + 8 * c + e, v);
-      }
-    }
+    const float dls = dl_r * inv_den;  // D^l / den
+    if (valid) *reinterpret_cast<uint4*>(sDL + tc::sw128_off(r, 0)) = make_uint4(tc::pack_bf16(dls, 0.f), 0, 0, 0);
     tc::fence_proxy_async();
     tc::tc_fence_before();
     __syncwarp();
     if (lane == 0) tc::mbar_arrive(x_ready);
-    // dH_i -> global bf16 (rows a of the M = D accumulator); dZ_i
+    // dH_i (bf16, for the M0^T aggregation GEMM) and dZ_i = -(column D of the product)
     __nv_bfloat16* gHi = p.gH + urow * D * D;
     if (has_lin) {
       tc::mbar_wait(lin_done, 0);
@@ -399,31 +396,32 @@ __global__ void __launch_bounds__(192, 1)
       const int arow = D == 128 ? 32 * q4 + lane : 16 * q4 + lane;
       const bool avalid = D == 128 || lane < 16;
 #pragma unroll 1
-      for (int c0 = 0; c0 < D; c0 += 32) {
+      for (int c0 = 0; c0 < D + 32; c0 += 32) {
         uint32_t a[32];
-        tc::tmem_ld32(tB1 + lane_base + c0, a);
+        tc::tmem_ld32(tB0 + lane_base + c0, a);
         tc::tmem_ld_wait();
-        if (avalid) {
+        if (!avalid) continue;
+        if (c0 == D) {
+          p.gZ[urow * D + arow] = -__uint_as_float(a[0]);
+          continue;
+        }
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            float f[8];
+        for (int c = 0; c < 4; ++c) {
+          float f[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(a[8 * c + e]);
-            *reinterpret_cast<uint4*>(gHi + arow * D + c0 + 8 * c) = pack8(f);
-          }
+          for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(a[8 * c + e]);
+          *reinterpret_cast<uint4*>(gHi + arow * D + c0 + 8 * c) = pack8(f);
         }
       }
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(dh_read);
     } else {
-      for (int e = threadIdx.x - 64; e < D * D / 8; e += 128)
-        reinterpret_cast<uint4*>(gHi)[e] = make_uint4(0, 0, 0, 0);
+      for (int e = tid; e < D * D / 8; e += 128) reinterpret_cast<uint4*>(gHi)[e] = make_uint4(0, 0, 0, 0);
+      for (int a = tid; a < D; a += 128) p.gZ[urow * D + a] = 0.f;
     }
-    named_sync(1, 128);
-    for (int a = threadIdx.x - 64; a < D; a += 128) p.gZ[urow * D + a] = has_lin ? dz[a] : 0.f;
     // sparse dQ: dS = P (dP - D^s) / sqrt(d), P = exp(S/sqrt(d) - lse)
-    const float lse2 = valid ? p.lse[grow] * 1.4426950408889634f : 0.f;
+    const float lse2 = p.lse[grow] * 1.4426950408889634f;
     for (int t = 0; t < cnt; ++t) {
       tc::mbar_wait(sdp_full + (t & 1), (t >> 1) & 1);
       tc::tc_fence_after();
@@ -456,10 +454,10 @@ __global__ void __launch_bounds__(192, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(ds_full + (t & 1));
     }
-    // dq_total = J_phi(q)^T dQ^phi + dQ
+    // dq_total = J_phi(q)^T dQ^phi + dQ, dQ^phi = (dO^l/den) H_i^T - (D^l/den) Z_i
     tc::mbar_wait(dq_done, 0);
     tc::tc_fence_after();
-    float dot = 0.f;  // <phi(q), dQ^phi> for the softmax VJP
+    float dot = 0.f;  // <phi(q), dQ^phi> for the softmax Jacobian
     if (p.phi == 2 && has_lin) {
 #pragma unroll 1
       for (int c0 = 0; c0 < D; c0 += 32) {
@@ -469,12 +467,10 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           float f[8];
-          unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(rr, c0 + 8 * c)), f);
+          unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(r, c0 + 8 * c)), f);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) {
-            const float g = (__uint_as_float(a[8 * c + e]) - dl_r * __ldg(Zi + c0 + 8 * c + e)) * inv_den;
-            dot = fmaf(ph.phi_of(f[e], 2), g, dot);
-          }
+          for (int e = 0; e < 8; ++e)
+            dot = fmaf(phi_of(f[e]), __uint_as_float(a[8 * c + e]) - dls * zs[c0 + 8 * c + e], dot);
         }
       }
     }
@@ -484,21 +480,22 @@ __global__ void __launch_bounds__(192, 1)
       if (has_lin) tc::tmem_ld32(tQPHI + lane_base + c0, a);
       if (cnt > 0) tc::tmem_ld32(tDQ + lane_base + c0, b);
       tc::tmem_ld_wait();
+      if (!valid) continue;
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         float f[8], o[8];
-        unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(rr, c0 + 8 * c)), f);
+        unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(r, c0 + 8 * c)), f);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const int col = c0 + 8 * c + e;
-          const float g = has_lin ? (__uint_as_float(a[8 * c + e]) - dl_r * __ldg(Zi + col)) * inv_den : 0.f;
+          const float g = has_lin ? __uint_as_float(a[8 * c + e]) - dls * zs[col] : 0.f;
           float jg;
-          if (p.phi == 2) jg = ph.phi_of(f[e], 2) * (g - dot);
+          if (p.phi == 2) jg = phi_of(f[e]) * (g - dot);
           else if (p.phi == 0) jg = f[e] >= 0.f ? g : __expf(f[e]) * g;
           else jg = f[e] > 0.f ? g : 0.f;
           o[e] = jg + (cnt > 0 ? __uint_as_float(b[8 * c + e]) : 0.f);
         }
-        if (valid) *reinterpret_cast<uint4*>(p.dq + grow * D + c0 + 8 * c) = pack8(o);
+        *reinterpret_cast<uint4*>(p.dq + grow * D + c0 + 8 * c) = pack8(o);
       }
     }
   }
@@ -516,10 +513,13 @@ struct ColsLayout {
   static constexpr int oK = 0, oV = kT, oKF = 2 * kT;
   static constexpr int oRing = 3 * kT;
   static constexpr int kStage = 2 * kT;  // Q_i + dO_i, or dH_agg (D*D*2)
-  static constexpr int oPD = oRing + 2 * kStage;  // [2 buffers][P^T 8 KB, dS^T 8 KB]
+  static constexpr int kStages = 4;
+  static constexpr int oPD = oRing + kStages * kStage;  // [2 buffers][P^T 8 KB, dS^T 8 KB]
   static constexpr int oLS = oPD + 32768;          // float [2][128] lse*log2e, D^s
-  static constexpr int oBar = oLS + 2 * 128 * 4;
+  static constexpr int oZA = oLS + 2 * 128 * 4;    // float [D] dZ_agg
+  static constexpr int oBar = oZA + 4 * D;
   static constexpr int kBytes = oBar + 256 + 1024;
+  static_assert(kBytes <= 232448, "smem");
 };
 
 template <int D>
@@ -536,16 +536,18 @@ __global__ void __launch_bounds__(192, 1)
   uint8_t* sRing = smem + L::oRing;
   uint8_t* sPD = smem + L::oPD;
   float* sLS = reinterpret_cast<float*>(smem + L::oLS);
+  float* zas = reinterpret_cast<float*>(smem + L::oZA);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::oBar);
   uint64_t* kv_full = bars + 0;
-  uint64_t* ring_full = bars + 1;   // [2]
-  uint64_t* ring_empty = bars + 3;  // [2]
+  constexpr int RS = L::kStages;
+  uint64_t* ring_full = bars + 16;        // [RS]
+  uint64_t* ring_empty = bars + 16 + RS;  // [RS]
   uint64_t* sdp_full = bars + 5;    // [2]
   uint64_t* pd_full = bars + 7;     // [2]
   uint64_t* pd_empty = bars + 9;    // [2]
   uint64_t* kf_ready = bars + 11;
   uint64_t* all_done = bars + 12;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + 2 * RS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = blockIdx.x;
@@ -570,9 +572,11 @@ __global__ void __launch_bounds__(192, 1)
   if (warp == 0) {
     if (lane == 0) {
       tc::mbar_init(kv_full, 1);
-      for (int s = 0; s < 2; ++s) {
+      for (int s = 0; s < RS; ++s) {
         tc::mbar_init(ring_full + s, 1);
         tc::mbar_init(ring_empty + s, 1);
+      }
+      for (int s = 0; s < 2; ++s) {
         tc::mbar_init(sdp_full + s, 1);
         tc::mbar_init(pd_full + s, 4);
         tc::mbar_init(pd_empty + s, 1);
@@ -600,8 +604,8 @@ __global__ void __launch_bounds__(192, 1)
       }
       int item = 0;
       auto acquire = [&](int bytes) -> uint8_t* {
-        const int s = item & 1;
-        tc::mbar_wait(ring_empty + s, ((item >> 1) & 1) ^ 1);
+        const int s = item % RS;
+        tc::mbar_wait(ring_empty + s, ((item / RS) & 1) ^ 1);
         tc::mbar_expect_tx(ring_full + s, bytes);
         return sRing + s * L::kStage;
       };
@@ -610,8 +614,8 @@ __global__ void __launch_bounds__(192, 1)
         uint8_t* dst = acquire(2 * L::kT);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
-          tc::tma_load_3d(dst + c * 8192, &tmQ, ring_full + (item & 1), 64 * c, q_row, 0);
-          tc::tma_load_3d(dst + L::kT + c * 8192, &tmDO, ring_full + (item & 1), 64 * c, q_row, 0);
+          tc::tma_load_3d(dst + c * 8192, &tmQ, ring_full + (item % RS), 64 * c, q_row, 0);
+          tc::tma_load_3d(dst + L::kT + c * 8192, &tmDO, ring_full + (item % RS), 64 * c, q_row, 0);
         }
         ++item;
       }
@@ -619,7 +623,7 @@ __global__ void __launch_bounds__(192, 1)
         uint8_t* dst = acquire(D * D * 2);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c)
-          tc::tma_load_3d(dst + c * D * 128, &tmHa, ring_full + (item & 1), 64 * c, int(ucol * D), 0);
+          tc::tma_load_3d(dst + c * D * 128, &tmHa, ring_full + (item % RS), 64 * c, int(ucol * D), 0);
         ++item;
       }
     }
@@ -631,8 +635,8 @@ __global__ void __launch_bounds__(192, 1)
     constexpr uint32_t id_nd_kk = tc::idesc_bf16(64, D, false, false);
     int item = 0;
     auto wait_item = [&]() -> uint32_t {
-      const int s = item & 1;
-      tc::mbar_wait(ring_full + s, (item >> 1) & 1);
+      const int s = item % RS;
+      tc::mbar_wait(ring_full + s, (item / RS) & 1);
       tc::tc_fence_after();
       return aR + s * L::kStage;
     };
@@ -644,7 +648,7 @@ __global__ void __launch_bounds__(192, 1)
     auto issue_acc = [&](int t) {  // dV += P^T dO_t, dK += dS^T Q_t
       tc::mbar_wait(pd_full + (t & 1), (t >> 1) & 1);
       tc::tc_fence_after();
-      const uint32_t sq = aR + (t & 1) * L::kStage;
+      const uint32_t sq = aR + (t % RS) * L::kStage;
       if (lane == 0) {
         const uint32_t sp = aPD + (t & 1) * 16384, sd = sp + 8192;
 #pragma unroll
@@ -654,7 +658,7 @@ __global__ void __launch_bounds__(192, 1)
           tc::mma_bf16(tDK, tc::desc_kmajor(sd + kk * 32), tc::desc_mnmajor(sq + kk * 2048, 8192), id_nd_kn,
                        (t | kk) != 0);
         }
-        tc::mma_commit(ring_empty + (t & 1));
+        tc::mma_commit(ring_empty + (t % RS));
         tc::mma_commit(pd_empty + (t & 1));
       }
       __syncwarp();
@@ -687,7 +691,7 @@ __global__ void __launch_bounds__(192, 1)
           tc::mma_bf16(tDV, kdesc(aKF, kk, 64), tc::desc_mnmajor(sh + kk * 2048, D * 128), id_nd_kn,
                        (cnt > 0 || kk > 0) ? 1u : 0u);
         }
-        tc::mma_commit(ring_empty + (item & 1));
+        tc::mma_commit(ring_empty + (item % RS));
       }
       __syncwarp();
       ++item;
@@ -696,24 +700,46 @@ __global__ void __launch_bounds__(192, 1)
     __syncwarp();
   } else {
     const int q4 = warp & 3;
-    const int c = 16 * q4 + lane;  // key row within the block
+    const int c = 16 * q4 + (lane & 15);  // key row within the block (lanes 0-15 own its TMEM row)
+    const int h0 = (lane >> 4) * (D / 2);
     const bool valid = lane < 16;
-    const int cc = c & 63;
     const uint32_t lane_base = uint32_t(32 * q4) << 16;
     const long long grow = (long long)kv0 + c;
+    for (int a = threadIdx.x - 64; a < D; a += 128) zas[a] = has_lin ? p.gZa[ucol * D + a] : 0.f;
+    named_sync(1, 128);
     tc::mbar_wait(kv_full, 0);
-    RowPhi<D> ph;
-    ph.stats(sK, cc, p.phi);
+    // phi statistics of the key row (feature_map.cpp:10-20), shared by the two half-row lanes
+    float mx = 0.f, inv = 1.f;
+    if (p.phi == 2) {
+      mx = -INFINITY;
+#pragma unroll
+      for (int ch = 0; ch < D / 2; ch += 8) {
+        float f[8];
+        unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, h0 + ch)), f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) mx = fmaxf(mx, f[e]);
+      }
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+      float se = 0.f;
+#pragma unroll
+      for (int ch = 0; ch < D / 2; ch += 8) {
+        float f[8];
+        unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, h0 + ch)), f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) se += __expf(f[e] - mx);
+      }
+      se += __shfl_xor_sync(0xffffffffu, se, 16);
+      inv = 1.f / se;
+    }
+    auto phi_of = [&](float x) { return p.phi == 2 ? __expf(x - mx) * inv : phi_elem(p.phi, x); };
     if (has_lin) {  // phi(K_j) in bf16, A operand of phi(K) dH_agg
-      if (valid) {
 #pragma unroll
-        for (int ch = 0; ch < D / 8; ++ch) {
-          float f[8];
-          unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, 8 * ch)), f);
+      for (int ch = 0; ch < D / 2; ch += 8) {
+        float f[8];
+        unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, h0 + ch)), f);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) f[e] = ph.phi_of(f[e], p.phi);
-          *reinterpret_cast<uint4*>(sKF + tile_off(c, 8 * ch)) = pack8(f);
-        }
+        for (int e = 0; e < 8; ++e) f[e] = phi_of(f[e]);
+        *reinterpret_cast<uint4*>(sKF + tile_off(c, h0 + ch)) = pack8(f);
       }
       tc::fence_proxy_async();
       __syncwarp();
@@ -768,7 +794,6 @@ __global__ void __launch_bounds__(192, 1)
     tc::mbar_wait(all_done, 0);
     tc::tc_fence_after();
     // dk_total = J_phi(k)^T dK^phi + dK, dK^phi = raw + dZ_agg (broadcast over the rows)
-    const float* dza = p.gZa + ucol * D;
     float dot = 0.f;
     if (p.phi == 2 && has_lin) {
 #pragma unroll 1
@@ -779,10 +804,9 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch) {
           float f[8];
-          unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(cc, c0 + 8 * ch)), f);
+          unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, c0 + 8 * ch)), f);
 #pragma unroll
-          for (int e = 0; e < 8; ++e)
-            dot = fmaf(ph.phi_of(f[e], 2), __uint_as_float(a[8 * ch + e]) + __ldg(dza + c0 + 8 * ch + e), dot);
+          for (int e = 0; e < 8; ++e) dot = fmaf(phi_of(f[e]), __uint_as_float(a[8 * ch + e]) + zas[c0 + 8 * ch + e], dot);
         }
       }
     }
@@ -796,13 +820,13 @@ __global__ void __launch_bounds__(192, 1)
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
         float f[8], o[8], w8[8];
-        unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(cc, c0 + 8 * ch)), f);
+        unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, c0 + 8 * ch)), f);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           const int col = c0 + 8 * ch + e;
-          const float g = has_lin ? __uint_as_float(a[8 * ch + e]) + __ldg(dza + col) : 0.f;
+          const float g = has_lin ? __uint_as_float(a[8 * ch + e]) + zas[col] : 0.f;
           float jg;
-          if (p.phi == 2) jg = ph.phi_of(f[e], 2) * (g - dot);
+          if (p.phi == 2) jg = phi_of(f[e]) * (g - dot);
           else if (p.phi == 0) jg = f[e] >= 0.f ? g : __expf(f[e]) * g;
           else jg = f[e] > 0.f ? g : 0.f;
           o[e] = jg + (cnt > 0 ? __uint_as_float(b[8 * ch + e]) : 0.f);

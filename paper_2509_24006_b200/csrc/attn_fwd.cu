@@ -25,13 +25,14 @@ struct FwdLayout {
   static constexpr int kQ = 64 * D * 2;       // Q tile, K-major SW128 (D/64 chunks of 8 KB)
   static constexpr int kTile = 64 * D * 2;    // one K or V tile
   static constexpr int kStage = 2 * kTile;    // K + V; also holds H_i or W (D*D*2 bytes)
-  static constexpr int kStages = 2;
+  static constexpr int kStages = 2;  // 2 CTAs / SM share the tensor core
   static constexpr int kPX = 16384;           // 2 P buffers (8 KB) == phi(Q) / O^l tile
   static constexpr int oQ = 0;
   static constexpr int oRing = oQ + kQ;
   static constexpr int oPX = oRing + kStages * kStage;
   static constexpr int oBar = oPX + kPX;
   static constexpr int kBytes = oBar + 256 + 1024;
+  static_assert(kBytes <= 232448, "smem");
   static_assert(D * D * 2 <= kStage, "H/W must fit a ring stage");
   static_assert(64 * D * 2 <= kPX, "X tile must fit the P region");
 };
@@ -71,8 +72,9 @@ __global__ void __launch_bounds__(192, 2)
   uint8_t* sPX = smem + L::oPX;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::oBar);
   uint64_t* q_full = bars + 0;
-  uint64_t* ring_full = bars + 1;   // [2]
-  uint64_t* ring_empty = bars + 3;  // [2]
+  constexpr int RS = L::kStages;
+  uint64_t* ring_full = bars + 16;        // [RS]
+  uint64_t* ring_empty = bars + 16 + RS;  // [RS]
   uint64_t* s_full = bars + 5;      // [2]
   uint64_t* p_full = bars + 7;      // [2]
   uint64_t* pv_done = bars + 9;     // [2]
@@ -80,7 +82,7 @@ __global__ void __launch_bounds__(192, 2)
   uint64_t* x_full = bars + 12;
   uint64_t* o_ready = bars + 13;
   uint64_t* proj_done = bars + 14;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + 2 * RS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x;
@@ -98,9 +100,11 @@ __global__ void __launch_bounds__(192, 2)
       tc::tma_prefetch(&tmK);
       tc::tma_prefetch(&tmV);
       tc::mbar_init(q_full, 1);
-      for (int s = 0; s < 2; ++s) {
+      for (int s = 0; s < RS; ++s) {
         tc::mbar_init(ring_full + s, 1);
         tc::mbar_init(ring_empty + s, 1);
+      }
+      for (int s = 0; s < 2; ++s) {
         tc::mbar_init(s_full + s, 1);
         tc::mbar_init(p_full + s, 4);
         tc::mbar_init(pv_done + s, 1);
@@ -129,8 +133,8 @@ __global__ void __launch_bounds__(192, 2)
       for (int c = 0; c < D / 64; ++c) tc::tma_load_3d(sQ + c * 8192, &tmQ, q_full, 64 * c, row0, 0);
       int item = 0;
       auto acquire = [&](int bytes) -> uint8_t* {
-        const int s = item & 1;
-        tc::mbar_wait(ring_empty + s, ((item >> 1) & 1) ^ 1);
+        const int s = item % RS;
+        tc::mbar_wait(ring_empty + s, ((item / RS) & 1) ^ 1);
         tc::mbar_expect_tx(ring_full + s, bytes);
         return sRing + s * L::kStage;
       };
@@ -138,7 +142,7 @@ __global__ void __launch_bounds__(192, 2)
         uint8_t* dst = acquire(D * D * 2);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c)
-          tc::tma_load_3d(dst + c * D * 128, &tmH, ring_full + (item & 1), 64 * c, int(urow * D), 0);
+          tc::tma_load_3d(dst + c * D * 128, &tmH, ring_full + (item % RS), 64 * c, int(urow * D), 0);
         ++item;
       }
       for (int t = 0; t < cnt; ++t) {
@@ -146,8 +150,8 @@ __global__ void __launch_bounds__(192, 2)
         uint8_t* dst = acquire(2 * L::kTile);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
-          tc::tma_load_3d(dst + c * 8192, &tmK, ring_full + (item & 1), 64 * c, kv_row, 0);
-          tc::tma_load_3d(dst + L::kTile + c * 8192, &tmV, ring_full + (item & 1), 64 * c, kv_row, 0);
+          tc::tma_load_3d(dst + c * 8192, &tmK, ring_full + (item % RS), 64 * c, kv_row, 0);
+          tc::tma_load_3d(dst + L::kTile + c * 8192, &tmV, ring_full + (item % RS), 64 * c, kv_row, 0);
         }
         ++item;
       }
@@ -156,7 +160,7 @@ __global__ void __launch_bounds__(192, 2)
         const int h = int(u % p.H);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c)
-          tc::tma_load_3d(dst + c * D * 128, &tmW, ring_full + (item & 1), 64 * c, h * D, 0);
+          tc::tma_load_3d(dst + c * D * 128, &tmW, ring_full + (item % RS), 64 * c, h * D, 0);
         ++item;
       }
     }
@@ -167,8 +171,8 @@ __global__ void __launch_bounds__(192, 2)
     constexpr uint32_t id_o = tc::idesc_bf16(64, D, false, true);
     int item = 0;
     auto wait_item = [&]() -> uint32_t {
-      const int s = item & 1;
-      tc::mbar_wait(ring_full + s, (item >> 1) & 1);
+      const int s = item % RS;
+      tc::mbar_wait(ring_full + s, (item / RS) & 1);
       tc::tc_fence_after();
       return sRa + s * L::kStage;
     };
@@ -181,7 +185,7 @@ __global__ void __launch_bounds__(192, 2)
         for (int kk = 0; kk < D / 16; ++kk)
           tc::mma_bf16(tO, tc::desc_kmajor(sPa + (kk >> 2) * 8192 + (kk & 3) * 32),
                        tc::desc_mnmajor(sh + kk * 2048, D * 128), id_o, kk > 0);
-        tc::mma_commit(ring_empty + (item & 1));
+        tc::mma_commit(ring_empty + (item % RS));
         tc::mma_commit(lin_done);
       }
       __syncwarp();
@@ -192,14 +196,14 @@ __global__ void __launch_bounds__(192, 2)
       tc::mbar_wait(p_full + (j & 1), (j >> 1) & 1);
       tc::tc_fence_after();
       const int it = item0 + j;
-      const uint32_t sv = sRa + (it & 1) * L::kStage + L::kTile;
+      const uint32_t sv = sRa + (it % RS) * L::kStage + L::kTile;
       if (lane == 0) {
         const uint32_t sp = sPa + (j & 1) * 8192;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
           tc::mma_bf16(tO, tc::desc_kmajor(sp + kk * 32), tc::desc_mnmajor(sv + kk * 2048, 8192), id_o,
                        (j | kk) != 0);
-        tc::mma_commit(ring_empty + (it & 1));
+        tc::mma_commit(ring_empty + (it % RS));
         tc::mma_commit(pv_done + (j & 1));
       }
       __syncwarp();
@@ -228,7 +232,7 @@ __global__ void __launch_bounds__(192, 2)
         for (int kk = 0; kk < D / 16; ++kk)
           tc::mma_bf16(tO, tc::desc_kmajor(sPa + (kk >> 2) * 8192 + (kk & 3) * 32),
                        tc::desc_mnmajor(sw + kk * 2048, D * 128), id_o, 1);
-        tc::mma_commit(ring_empty + (item & 1));
+        tc::mma_commit(ring_empty + (item % RS));
         tc::mma_commit(proj_done);
       }
       __syncwarp();

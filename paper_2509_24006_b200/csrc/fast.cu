@@ -69,70 +69,66 @@ __global__ void __launch_bounds__(256) k_phi_kz(const __nv_bfloat16* __restrict_
   }
 }
 
-// Z_i = sum_{j marginal, ascending} z_j (aggregation.cpp:40-56).  grid (ceil(Tm/16), U),
-// d threads; 16 block rows per CTA share every z_j read; labels staged per 1024 columns.
-__global__ void k_aggregate_z(const int8_t* __restrict__ labels, const float* __restrict__ z,
-                              int d, int Tm, int Tn, float* __restrict__ Z) {
-  constexpr int R = 16, JC = 1024;
-  __shared__ int8_t lab[R][JC];
+// Marginal aggregation of the per-block vectors as a tiled fp32 GEMM with the 0/1 marginal
+// indicator: Z = M0 z (forward, aggregation.cpp:40-56) or dZ_agg = M0^T dZ (backward,
+// backward.cpp:170-178).  grid (ceil(T_out/64), U); 256 threads, 64 output rows x d columns
+// per CTA, K (= block index) staged 32 at a time.
+template <bool kTrans>
+__global__ void __launch_bounds__(256) k_aggregate_vec(const int8_t* __restrict__ labels,
+                                                       const float* __restrict__ x, int d, int Tm,
+                                                       int Tn, float* __restrict__ out) {
+  constexpr int BM = 64, BK = 32;
+  __shared__ float sa[BK][BM + 1];   // indicator tile, [k][m]
+  __shared__ float sx[BK][128];      // x tile, [k][a]
   const long long u = blockIdx.y;
-  const int i0 = blockIdx.x * R;
-  const int a = threadIdx.x;
-  float acc[R];
+  const int m0 = blockIdx.x * BM;
+  const int Mo = kTrans ? Tn : Tm, Kd = kTrans ? Tm : Tn;
+  const int8_t* lu = labels + u * (long long)Tm * Tn;
+  const float* xu = x + u * (long long)Kd * d;
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 8 row groups x 32 column lanes
+  float acc[8][4];
 #pragma unroll
-  for (int r = 0; r < R; ++r) acc[r] = 0.f;
-  const float* zu = z + u * (long long)Tn * d;
-  for (int jc = 0; jc < Tn; jc += JC) {
-    const int jn = min(JC, Tn - jc);
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[i][c] = 0.f;
+  for (int k0 = 0; k0 < Kd; k0 += BK) {
     __syncthreads();
-    for (int e = threadIdx.x; e < R * JC; e += blockDim.x) {
-      const int r = e / JC, j = e % JC;
-      lab[r][j] = (i0 + r < Tm && j < jn) ? labels[(u * Tm + i0 + r) * (long long)Tn + jc + j] : int8_t(-1);
+    for (int e = threadIdx.x; e < BK * BM; e += 256) {
+      const int kk = e / BM, m = e % BM;
+      const int gm = m0 + m, gk = k0 + kk;
+      float v = 0.f;
+      if (gm < Mo && gk < Kd) {
+        const int8_t l = kTrans ? lu[(long long)gk * Tn + gm] : lu[(long long)gm * Tn + gk];
+        v = l == 0 ? 1.f : 0.f;
+      }
+      sa[kk][m] = v;
+    }
+    for (int e = threadIdx.x; e < BK * d; e += 256) {
+      const int kk = e / d, a = e % d;
+      sx[kk][a] = (k0 + kk < Kd) ? xu[(long long)(k0 + kk) * d + a] : 0.f;
     }
     __syncthreads();
-    for (int j = 0; j < jn; ++j) {
-      const float zj = zu[(long long)(jc + j) * d + a];
+#pragma unroll 4
+    for (int kk = 0; kk < BK; ++kk) {
+      float xv[4];
 #pragma unroll
-      for (int r = 0; r < R; ++r)
-        if (lab[r][j] == 0) acc[r] += zj;
+      for (int c = 0; c < 4; ++c) xv[c] = (tx + 32 * c < d) ? sx[kk][tx + 32 * c] : 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float w = sa[kk][ty * 8 + i];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[i][c] = fmaf(w, xv[c], acc[i][c]);
+      }
     }
   }
 #pragma unroll
-  for (int r = 0; r < R; ++r)
-    if (i0 + r < Tm) Z[(u * Tm + i0 + r) * d + a] = acc[r];
-}
-
-// dZ_agg_j = sum_{i: label(i,j) = 0, ascending} dZ_i (backward.cpp:170-178); grid
-// (ceil(Tn/16), U), d threads; 16 key columns per CTA.
-__global__ void k_aggregate_dz_cols(const int8_t* __restrict__ labels, const float* __restrict__ gz,
-                                    int d, int Tm, int Tn, float* __restrict__ out) {
-  constexpr int R = 16;
-  __shared__ int8_t lab[1024][R];
-  const long long u = blockIdx.y;
-  const int j0 = blockIdx.x * R;
-  const int a = threadIdx.x;
-  float acc[R];
+  for (int i = 0; i < 8; ++i) {
+    const int gm = m0 + ty * 8 + i;
+    if (gm >= Mo) continue;
 #pragma unroll
-  for (int r = 0; r < R; ++r) acc[r] = 0.f;
-  const float* gu = gz + u * (long long)Tm * d;
-  for (int ic = 0; ic < Tm; ic += 1024) {
-    const int in = min(1024, Tm - ic);
-    __syncthreads();
-    for (int e = threadIdx.x; e < 1024 * R; e += blockDim.x) {
-      const int i = e / R, r = e % R;
-      lab[i][r] = (i < in && j0 + r < Tn) ? labels[(u * Tm + ic + i) * (long long)Tn + j0 + r] : int8_t(-1);
-    }
-    __syncthreads();
-    for (int i = 0; i < in; ++i) {
-      const float g = gu[(long long)(ic + i) * d + a];
-#pragma unroll
-      for (int r = 0; r < R; ++r)
-        if (lab[i][r] == 0) acc[r] += g;
-    }
+    for (int c = 0; c < 4; ++c)
+      if (tx + 32 * c < d) out[(u * Mo + gm) * d + tx + 32 * c] = acc[i][c];
   }
-#pragma unroll
-  for (int r = 0; r < R; ++r)
-    if (j0 + r < Tn) out[(u * Tn + j0 + r) * d + a] = acc[r];
 }
 
 // dW[h] = sum over the batch and the split-K chunks of O^l^T dO (backward.cpp:46).
@@ -206,8 +202,8 @@ void fast_prepare_linear(const Dims& Dm, const void* k, const void* v, const Sta
   a.c_batch = (long long)Dm.Tm * d * d;
   a.name = "gemm_aggregate";
   launch_gemm(a, st);
-  k_aggregate_z<<<dim3((Dm.Tm + 15) / 16, unsigned(Dm.U)), d, 0, st>>>(s.labels, wb.z, d, Dm.Tm,
-                                                                        Dm.Tn, s.Z);
+  k_aggregate_vec<false><<<dim3((Dm.Tm + 63) / 64, unsigned(Dm.U)), 256, 0, st>>>(s.labels, wb.z, d, Dm.Tm,
+                                                                                Dm.Tn, s.Z);
   check_launch("k_aggregate_z", st);
 }
 
@@ -246,9 +242,9 @@ void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, 
   a.c_batch = (long long)Dm.Tn * d * d;
   a.name = "gemm_aggregate_t";
   launch_gemm(a, st);
-  k_aggregate_dz_cols<<<dim3((Dm.Tn + 15) / 16, unsigned(Dm.U)), d, 0, st>>>(s.labels, wb.gZ, d, Dm.Tm,
-                                                                            Dm.Tn, wb.gZa);
-  check_launch("k_aggregate_dz_cols", st);
+  k_aggregate_vec<true><<<dim3((Dm.Tn + 63) / 64, unsigned(Dm.U)), 256, 0, st>>>(s.labels, wb.gZ, d, Dm.Tm,
+                                                                               Dm.Tn, wb.gZa);
+  check_launch("k_aggregate_dz", st);
   // columns pass: dk_total, dv
   launch_bwd_cols(Dm, q, k, v, lse, d_out, dk, dv, s, wb.hab, wb.gZa, wb.Ds, st);
   // dW = O^l^T dO per head, split-K over row chunks of each unit, then reduced over chunks + batch
