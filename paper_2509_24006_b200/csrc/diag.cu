@@ -110,3 +110,25 @@ extern "C" int sla_b200_diag_tmem(void* out_x2, void* out_m64_lo, void* out_m64_
   slab::k_diag_m64_lane<<<1, 128, 20480, st>>>(16u, static_cast<float*>(out_m64_hi));
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
+
+namespace slab {
+namespace {
+// L2 read bandwidth probe: every CTA streams 16-byte loads over an L2-resident buffer.
+__global__ void k_diag_l2bw(const uint4* __restrict__ buf, long long n16, int iters, uint4* sink) {
+  uint4 acc = make_uint4(0, 0, 0, 0);
+  for (int it = 0; it < iters; ++it)
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n16;
+         e += (long long)gridDim.x * blockDim.x) {
+      uint4 v;
+      asm volatile("ld.global.cg.v4.u32 {%0,%1,%2,%3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(buf + e));
+      acc.x ^= v.x; acc.y ^= v.y; acc.z ^= v.z; acc.w ^= v.w;
+    }
+  if (acc.x == 0x12345678u) sink[0] = acc;
+}
+}  // namespace
+}  // namespace slab
+
+extern "C" int sla_b200_diag_l2bw(const void* buf, long long bytes, int iters, void* sink, int blocks, int threads) {
+  slab::k_diag_l2bw<<<blocks, threads>>>(static_cast<const uint4*>(buf), bytes / 16, iters, static_cast<uint4*>(sink));
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
