@@ -573,25 +573,27 @@ __global__ void __launch_bounds__(320, 1)
 }
 
 // =========================================================================================
-// columns pass
+// columns pass: critical query blocks in PAIRS (M = 128 S / dP tiles), dV^T / dK^T accumulated
+// transposed (M = D) at full tensor rate; linear dK^phi^T and dV^T += dH_agg^T phi(K)^T on the
+// tensor core; the epilogue transposes through smem and finishes row-wise.
 // =========================================================================================
 template <int D>
 struct ColsLayout {
-  static constexpr int kT = 64 * D * 2;
-  static constexpr int oK = 0, oV = kT, oKF = 2 * kT;
-  static constexpr int oRing = 3 * kT;
-  static constexpr int kStage = 2 * kT;  // Q_i + dO_i, or dH_agg (D*D*2)
-  static constexpr int kStages = 4;
-  static constexpr int oPD = oRing + kStages * kStage;  // [2 buffers][P^T 8 KB, dS^T 8 KB]
-  static constexpr int oLS = oPD + 32768;          // float [2][128] lse*log2e, D^s
-  static constexpr int oZA = oLS + 2 * 128 * 4;    // float [D] dZ_agg
+  static constexpr int kT = 64 * D * 2;    // 64-row tile
+  static constexpr int kP = 128 * D * 2;   // 128-row pair tile
+  static constexpr int oK = 0, oV = kT;
+  static constexpr int oRing = 2 * kT;
+  static constexpr int kStage = 2 * kP;    // Q pair + dO pair, or dH_agg (D*D*2)
+  static constexpr int kStages = 2;
+  static constexpr int oPD = oRing + kStages * kStage;  // 2 x [P 16 KB | dS 16 KB]; phi(K) aliases
+  static constexpr int oZA = oPD + 65536;               // float [D] dZ_agg
   static constexpr int oBar = oZA + 4 * D;
   static constexpr int kBytes = oBar + 256 + 1024;
   static_assert(kBytes <= 232448, "smem");
 };
 
 template <int D>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(320, 1)
     k_bwd_cols(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
                const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                const __grid_constant__ CUtensorMap tmHa, BwdParams p) {
@@ -600,21 +602,21 @@ __global__ void __launch_bounds__(192, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = smem + L::oK;
   uint8_t* sV = smem + L::oV;
-  uint8_t* sKF = smem + L::oKF;
   uint8_t* sRing = smem + L::oRing;
   uint8_t* sPD = smem + L::oPD;
-  float* sLS = reinterpret_cast<float*>(smem + L::oLS);
+  uint8_t* sKF = sPD;  // phi(K_j), written once the accumulation MMAs have drained the P/dS buffers
   float* zas = reinterpret_cast<float*>(smem + L::oZA);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::oBar);
-  uint64_t* kv_full = bars + 0;
   constexpr int RS = L::kStages;
+  uint64_t* kv_full = bars + 0;
+  uint64_t* sdp_full = bars + 1;   // [2]
+  uint64_t* pd_full = bars + 3;    // [2]
+  uint64_t* pd_empty = bars + 5;   // [2]
+  uint64_t* acc_done = bars + 7;
+  uint64_t* kf_ready = bars + 8;
+  uint64_t* all_done = bars + 9;
   uint64_t* ring_full = bars + 16;        // [RS]
   uint64_t* ring_empty = bars + 16 + RS;  // [RS]
-  uint64_t* sdp_full = bars + 5;    // [2]
-  uint64_t* pd_full = bars + 7;     // [2]
-  uint64_t* pd_empty = bars + 9;    // [2]
-  uint64_t* kf_ready = bars + 11;
-  uint64_t* all_done = bars + 12;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + 2 * RS);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -622,8 +624,8 @@ __global__ void __launch_bounds__(192, 1)
   const long long u = blockIdx.y;
   const long long ucol = u * p.Tn + j;
   const int cnt = p.ccol_cnt[ucol];
+  const int np = (cnt + 1) >> 1;
   const int* list = p.ccol_idx + ucol * p.Tm;
-  // does any block row see column j as marginal?
   __shared__ int s_lin;
   if (threadIdx.x == 0) s_lin = 0;
   __syncthreads();
@@ -646,10 +648,11 @@ __global__ void __launch_bounds__(192, 1)
       }
       for (int s = 0; s < 2; ++s) {
         tc::mbar_init(sdp_full + s, 1);
-        tc::mbar_init(pd_full + s, 4);
+        tc::mbar_init(pd_full + s, 8);
         tc::mbar_init(pd_empty + s, 1);
       }
-      tc::mbar_init(kf_ready, 4);
+      tc::mbar_init(acc_done, 1);
+      tc::mbar_init(kf_ready, 8);
       tc::mbar_init(all_done, 1);
       tc::fence_barrier_init();
     }
@@ -660,7 +663,9 @@ __global__ void __launch_bounds__(192, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t tDK = tmem, tDV = tmem + 128, tB0 = tmem + 256, tB1 = tmem + 384;
+  // dV^T [0,64), dK^T [64,128) (M = D); S|dP pair buffers at 128 and 256 (M = 128);
+  // dK^phi^T at [384, 448) (M = D)
+  const uint32_t tDVT = tmem, tDKT = tmem + 64, tB0 = tmem + 128, tB1 = tmem + 256, tKPT = tmem + 384;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -670,6 +675,14 @@ __global__ void __launch_bounds__(192, 1)
         tc::tma_load_3d(sK + c * 8192, &tmK, kv_full, 64 * c, kv0, 0);
         tc::tma_load_3d(sV + c * 8192, &tmV, kv_full, 64 * c, kv0, 0);
       }
+      for (int t = 0; t < cnt; ++t) {  // warm L2 with every Q / dO tile of this column
+        const int q_row = int(u * p.N) + list[t] * 64;
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) {
+          tc::tma_prefetch_3d(&tmQ, 64 * c, q_row, 0);
+          tc::tma_prefetch_3d(&tmDO, 64 * c, q_row, 0);
+        }
+      }
       int item = 0;
       auto acquire = [&](int bytes) -> uint8_t* {
         const int s = item % RS;
@@ -677,13 +690,17 @@ __global__ void __launch_bounds__(192, 1)
         tc::mbar_expect_tx(ring_full + s, bytes);
         return sRing + s * L::kStage;
       };
-      for (int t = 0; t < cnt; ++t) {
-        const int q_row = int(u * p.N) + list[t] * 64;
-        uint8_t* dst = acquire(2 * L::kT);
+      for (int pp = 0; pp < np; ++pp) {
+        const int r1 = int(u * p.N) + list[2 * pp] * 64;
+        const int r2 = int(u * p.N) + list[min(2 * pp + 1, cnt - 1)] * 64;
+        uint8_t* dst = acquire(2 * L::kP);
+        uint64_t* fb = ring_full + (item % RS);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
-          tc::tma_load_3d(dst + c * 8192, &tmQ, ring_full + (item % RS), 64 * c, q_row, 0);
-          tc::tma_load_3d(dst + L::kT + c * 8192, &tmDO, ring_full + (item % RS), 64 * c, q_row, 0);
+          tc::tma_load_3d(dst + c * 16384, &tmQ, fb, 64 * c, r1, 0);
+          tc::tma_load_3d(dst + c * 16384 + 8192, &tmQ, fb, 64 * c, r2, 0);
+          tc::tma_load_3d(dst + L::kP + c * 16384, &tmDO, fb, 64 * c, r1, 0);
+          tc::tma_load_3d(dst + L::kP + c * 16384 + 8192, &tmDO, fb, 64 * c, r2, 0);
         }
         ++item;
       }
@@ -698,9 +715,10 @@ __global__ void __launch_bounds__(192, 1)
   } else if (warp == 1) {
     const uint32_t aK = tc::smem_u32(sK), aV = tc::smem_u32(sV), aKF = tc::smem_u32(sKF);
     const uint32_t aR = tc::smem_u32(sRing), aPD = tc::smem_u32(sPD);
-    constexpr uint32_t id_ss = tc::idesc_bf16(64, 64, false, false);
-    constexpr uint32_t id_nd_kn = tc::idesc_bf16(64, D, false, true);
-    constexpr uint32_t id_nd_kk = tc::idesc_bf16(64, D, false, false);
+    constexpr uint32_t id_s = tc::idesc_bf16(128, 64, false, false);   // pair x K^T
+    constexpr uint32_t id_acc = tc::idesc_bf16(D, 64, true, true);     // pair^T x P
+    constexpr uint32_t id_kp = tc::idesc_bf16(D, 64, false, false);    // dH_agg x V^T
+    constexpr uint32_t id_vl = tc::idesc_bf16(D, 64, true, false);     // dH_agg^T x phi(K)^T
     int item = 0;
     auto wait_item = [&]() -> uint32_t {
       const int s = item % RS;
@@ -713,32 +731,32 @@ __global__ void __launch_bounds__(192, 1)
     };
     tc::mbar_wait(kv_full, 0);
     tc::tc_fence_after();
-    auto issue_acc = [&](int t) {  // dV += P^T dO_t, dK += dS^T Q_t
+    auto issue_acc = [&](int t) {  // dV^T += dO_pair^T P, dK^T += Q_pair^T dS  (M = D, K = 128)
       tc::mbar_wait(pd_full + (t & 1), (t >> 1) & 1);
       tc::tc_fence_after();
       const uint32_t sq = aR + (t % RS) * L::kStage;
       if (lane == 0) {
-        const uint32_t sp = aPD + (t & 1) * 16384, sd = sp + 8192;
+        const uint32_t sp = aPD + (t & 1) * 32768, sd = sp + 16384;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          tc::mma_bf16(tDV, tc::desc_kmajor(sp + kk * 32), tc::desc_mnmajor(sq + L::kT + kk * 2048, 8192), id_nd_kn,
-                       (t | kk) != 0);
-          tc::mma_bf16(tDK, tc::desc_kmajor(sd + kk * 32), tc::desc_mnmajor(sq + kk * 2048, 8192), id_nd_kn,
-                       (t | kk) != 0);
+        for (int kk = 0; kk < 8; ++kk) {
+          tc::mma_bf16(tDVT, tc::desc_mnmajor(sq + L::kP + kk * 2048, 16384), tc::desc_mnmajor(sp + kk * 2048, 16384),
+                       id_acc, (t | kk) != 0);
+          tc::mma_bf16(tDKT, tc::desc_mnmajor(sq + kk * 2048, 16384), tc::desc_mnmajor(sd + kk * 2048, 16384),
+                       id_acc, (t | kk) != 0);
         }
         tc::mma_commit(ring_empty + (t % RS));
         tc::mma_commit(pd_empty + (t & 1));
       }
       __syncwarp();
     };
-    for (int t = 0; t < cnt; ++t) {
+    for (int t = 0; t < np; ++t) {
       const uint32_t sq = wait_item();
       if (lane == 0) {
         const uint32_t tb = (t & 1) ? tB1 : tB0;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          tc::mma_bf16(tb, kdesc(aK, kk, 64), kdesc(sq, kk, 64), id_ss, kk > 0);            // S^T = K Q^T
-          tc::mma_bf16(tb + 64, kdesc(aV, kk, 64), kdesc(sq + L::kT, kk, 64), id_ss, kk > 0); // dP^T = V dO^T
+          tc::mma_bf16(tb, kdesc(sq, kk, 128), kdesc(aK, kk, 64), id_s, kk > 0);                // S
+          tc::mma_bf16(tb + 64, kdesc(sq + L::kP, kk, 128), kdesc(aV, kk, 64), id_s, kk > 0);   // dP
         }
         tc::mma_commit(sdp_full + (t & 1));
       }
@@ -746,18 +764,21 @@ __global__ void __launch_bounds__(192, 1)
       ++item;
       if (t > 0) issue_acc(t - 1);
     }
-    if (cnt > 0) issue_acc(cnt - 1);
+    if (np > 0) issue_acc(np - 1);
+    if (lane == 0) tc::mma_commit(acc_done);
+    __syncwarp();
     if (has_lin) {
       const uint32_t sh = wait_item();
       tc::mbar_wait(kf_ready, 0);
       tc::tc_fence_after();
       if (lane == 0) {
-        // dK^phi raw = V dH_agg^T -> B0 ; dV += phi(K) dH_agg
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
-          tc::mma_bf16(tB0, kdesc(aV, kk, 64), kdesc(sh, kk, D), id_nd_kk, kk > 0);
-          tc::mma_bf16(tDV, kdesc(aKF, kk, 64), tc::desc_mnmajor(sh + kk * 2048, D * 128), id_nd_kn,
-                       (cnt > 0 || kk > 0) ? 1u : 0u);
+          // dK^phi^T raw = dH_agg V^T (M = D over a, N = 64 keys, K = D over b)
+          tc::mma_bf16(tKPT, kdesc(sh, kk, D), kdesc(aV, kk, 64), id_kp, kk > 0);
+          // dV^T += dH_agg^T phi(K)^T (M = D over b, N = 64 keys, K = D over a)
+          tc::mma_bf16(tDVT, tc::desc_mnmajor(sh + kk * 2048, D * 128), kdesc(aKF, kk, 64), id_vl,
+                       (np > 0 || kk > 0) ? 1u : 0u);
         }
         tc::mma_commit(ring_empty + (item % RS));
       }
@@ -768,143 +789,150 @@ __global__ void __launch_bounds__(192, 1)
     __syncwarp();
   } else {
     const int q4 = warp & 3;
-    const int c = 16 * q4 + (lane & 15);  // key row within the block (lanes 0-15 own its TMEM row)
-    const int h0 = (lane >> 4) * (D / 2);
-    const bool valid = lane < 16;
+    const int grp = (warp - 2) >> 2;
     const uint32_t lane_base = uint32_t(32 * q4) << 16;
-    const long long grow = (long long)kv0 + c;
-    for (int a = threadIdx.x - 64; a < D; a += 128) zas[a] = has_lin ? p.gZa[ucol * D + a] : 0.f;
-    named_sync(1, 128);
-    tc::mbar_wait(kv_full, 0);
-    // phi statistics of the key row (feature_map.cpp:10-20), shared by the two half-row lanes
-    float mx = 0.f, inv = 1.f;
-    if (p.phi == 2) {
-      mx = -INFINITY;
-#pragma unroll
-      for (int ch = 0; ch < D / 2; ch += 8) {
-        float f[8];
-        unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, h0 + ch)), f);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) mx = fmaxf(mx, f[e]);
-      }
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
-      float se = 0.f;
-#pragma unroll
-      for (int ch = 0; ch < D / 2; ch += 8) {
-        float f[8];
-        unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, h0 + ch)), f);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) se += __expf(f[e] - mx);
-      }
-      se += __shfl_xor_sync(0xffffffffu, se, 16);
-      inv = 1.f / se;
-    }
-    auto phi_of = [&](float x) { return p.phi == 2 ? __expf(x - mx) * inv : phi_elem(p.phi, x); };
-    if (has_lin) {  // phi(K_j) in bf16, A operand of phi(K) dH_agg
-#pragma unroll
-      for (int ch = 0; ch < D / 2; ch += 8) {
-        float f[8];
-        unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, h0 + ch)), f);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) f[e] = phi_of(f[e]);
-        *reinterpret_cast<uint4*>(sKF + tile_off(c, h0 + ch)) = pack8(f);
-      }
-      tc::fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(kf_ready);
-    }
-    const int ct = threadIdx.x - 64;  // 0..127
-    for (int t = 0; t < cnt; ++t) {
-      const long long qrow0 = u * p.N + (long long)list[t] * 64;
-      float* ls = sLS + (t & 1) * 128;
-      // stage lse*log2e and D^s of the 64 query rows (buffer t&1 is free: its last reader
-      // finished iteration t-2 before the named barrier of iteration t-1)
-      if (ct < 64) ls[ct] = p.lse[qrow0 + ct] * 1.4426950408889634f;
-      else ls[ct] = p.Ds[qrow0 + ct - 64];
-      named_sync(1, 128);
+    const int tid = threadIdx.x - 64;  // 0..255
+    for (int a = tid; a < D; a += 256) zas[a] = has_lin ? p.gZa[ucol * D + a] : 0.f;
+    // ---- loop: thread = query row rq of the pair (S / dP lanes), 32 key columns per group
+    const int rq = 32 * q4 + lane;
+    for (int t = 0; t < np; ++t) {
+      const bool live = rq < 64 || 2 * t + 1 < cnt;
+      const long long qrow = u * p.N + (long long)list[min(2 * t + (rq >> 6), cnt - 1)] * 64 + (rq & 63);
+      const float lse2 = p.lse[qrow] * 1.4426950408889634f;
+      const float dsr = p.Ds[qrow];
       tc::mbar_wait(sdp_full + (t & 1), (t >> 1) & 1);
       tc::tc_fence_after();
-      const uint32_t tb = ((t & 1) ? tB1 : tB0) + lane_base;
-      uint32_t pk[32], dk[32];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        uint32_t s[32], dp[32];
-        tc::tmem_ld32(tb + 32 * h, s);
-        tc::tmem_ld32(tb + 64 + 32 * h, dp);
+      const uint32_t tb = ((t & 1) ? tB1 : tB0) + lane_base + 32 * grp;
+      uint32_t pp[16], dd[16];
+      {
+        uint32_t sv[32], dp[32];
+        tc::tmem_ld32(tb, sv);
+        tc::tmem_ld32(tb + 64, dp);
         tc::tmem_ld_wait();
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
-          const int r0 = 32 * h + e;
-          const float p0 = ex2f(__uint_as_float(s[e]) * p.scale_log2 - ls[r0]);
-          const float p1 = ex2f(__uint_as_float(s[e + 1]) * p.scale_log2 - ls[r0 + 1]);
-          const float d0 = p0 * (__uint_as_float(dp[e]) - ls[64 + r0]) * p.scale;
-          const float d1 = p1 * (__uint_as_float(dp[e + 1]) - ls[64 + r0 + 1]) * p.scale;
-          pk[16 * h + (e >> 1)] = tc::pack_bf16(p0, p1);
-          dk[16 * h + (e >> 1)] = tc::pack_bf16(d0, d1);
+          float p0 = ex2f(__uint_as_float(sv[e]) * p.scale_log2 - lse2);
+          float p1 = ex2f(__uint_as_float(sv[e + 1]) * p.scale_log2 - lse2);
+          float d0 = p0 * (__uint_as_float(dp[e]) - dsr) * p.scale;
+          float d1 = p1 * (__uint_as_float(dp[e + 1]) - dsr) * p.scale;
+          if (!live) p0 = p1 = d0 = d1 = 0.f;
+          pp[e >> 1] = tc::pack_bf16(p0, p1);
+          dd[e >> 1] = tc::pack_bf16(d0, d1);
         }
       }
       if (t >= 2) tc::mbar_wait(pd_empty + (t & 1), ((t - 2) >> 1) & 1);
-      if (valid) {
-        uint8_t* prow = sPD + (t & 1) * 16384;
+      uint8_t* prow = sPD + (t & 1) * 32768;
 #pragma unroll
-        for (int ch = 0; ch < 8; ++ch) {
-          *reinterpret_cast<uint4*>(prow + tc::sw128_off(c, ch)) =
-              make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
-          *reinterpret_cast<uint4*>(prow + 8192 + tc::sw128_off(c, ch)) =
-              make_uint4(dk[4 * ch], dk[4 * ch + 1], dk[4 * ch + 2], dk[4 * ch + 3]);
-        }
+      for (int ch = 0; ch < 4; ++ch) {
+        *reinterpret_cast<uint4*>(prow + tc::sw128_off(rq, 4 * grp + ch)) =
+            make_uint4(pp[4 * ch], pp[4 * ch + 1], pp[4 * ch + 2], pp[4 * ch + 3]);
+        *reinterpret_cast<uint4*>(prow + 16384 + tc::sw128_off(rq, 4 * grp + ch)) =
+            make_uint4(dd[4 * ch], dd[4 * ch + 1], dd[4 * ch + 2], dd[4 * ch + 3]);
       }
       tc::fence_proxy_async();
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(pd_full + (t & 1));
     }
+    // ---- phi(K_j) rows (4 threads per key row, D/4 columns each): statistics + the bf16 tile
+    tc::mbar_wait(kv_full, 0);  // K_j must have landed even when no critical row came by
+    const int c = tid >> 2, c0 = (tid & 3) * (D / 4);
+    float mx = 0.f, inv = 1.f;
+    if (p.phi == 2) {
+      mx = -INFINITY;
+#pragma unroll
+      for (int cc = 0; cc < D / 4; cc += 8) {
+        float f[8];
+        unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, c0 + cc)), f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) mx = fmaxf(mx, f[e]);
+      }
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      float se = 0.f;
+#pragma unroll
+      for (int cc = 0; cc < D / 4; cc += 8) {
+        float f[8];
+        unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, c0 + cc)), f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) se += __expf(f[e] - mx);
+      }
+      se += __shfl_xor_sync(0xffffffffu, se, 1);
+      se += __shfl_xor_sync(0xffffffffu, se, 2);
+      inv = 1.f / se;
+    }
+    auto phi_of = [&](float x) { return p.phi == 2 ? __expf(x - mx) * inv : phi_elem(p.phi, x); };
+    tc::mbar_wait(acc_done, 0);  // the P / dS buffers are free
+    if (has_lin) {
+#pragma unroll
+      for (int cc = 0; cc < D / 4; cc += 8) {
+        float f[8];
+        unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, c0 + cc)), f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) f[e] = phi_of(f[e]);
+        *reinterpret_cast<uint4*>(sKF + tile_off(c, c0 + cc)) = pack8(f);
+      }
+      tc::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(kf_ready);
+    }
     tc::mbar_wait(all_done, 0);
     tc::tc_fence_after();
-    // dk_total = J_phi(k)^T dK^phi + dK, dK^phi = raw + dZ_agg (broadcast over the rows)
-    float dot = 0.f;
-    if (p.phi == 2 && has_lin) {
-#pragma unroll 1
-      for (int c0 = 0; c0 < D; c0 += 32) {
-        uint32_t a[32];
-        tc::tmem_ld32(tB0 + lane_base + c0, a);
-        tc::tmem_ld_wait();
+    // ---- transpose dK^T, dV^T, dK^phi^T (lane = column a) into smem [key row][a]
+    constexpr int TP = D + 4;
+    float* tk = reinterpret_cast<float*>(sRing);
+    float* tv = tk + 64 * TP;
+    float* tkp = tv + 64 * TP;
+    {
+      const int acol = D == 128 ? 32 * q4 + lane : 16 * q4 + lane;
+      const bool avalid = D == 128 || lane < 16;
+      uint32_t a[32], b[32], e3[32];
+      if (np > 0) tc::tmem_ld32(tDKT + lane_base + 32 * grp, a);
+      if (np > 0 || has_lin) tc::tmem_ld32(tDVT + lane_base + 32 * grp, b);
+      if (has_lin) tc::tmem_ld32(tKPT + lane_base + 32 * grp, e3);
+      tc::tmem_ld_wait();
+      if (avalid) {
 #pragma unroll
-        for (int ch = 0; ch < 4; ++ch) {
-          float f[8];
-          unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, c0 + 8 * ch)), f);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) dot = fmaf(phi_of(f[e]), __uint_as_float(a[8 * ch + e]) + zas[c0 + 8 * ch + e], dot);
+        for (int e = 0; e < 32; ++e) {
+          const int kr = 32 * grp + e;
+          tk[kr * TP + acol] = np > 0 ? __uint_as_float(a[e]) : 0.f;
+          tv[kr * TP + acol] = (np > 0 || has_lin) ? __uint_as_float(b[e]) : 0.f;
+          tkp[kr * TP + acol] = has_lin ? __uint_as_float(e3[e]) : 0.f;
         }
       }
     }
-#pragma unroll 1
-    for (int c0 = 0; c0 < D; c0 += 32) {
-      uint32_t a[32], b[32], v[32];
-      if (has_lin) tc::tmem_ld32(tB0 + lane_base + c0, a);
-      if (cnt > 0) tc::tmem_ld32(tDK + lane_base + c0, b);
-      if (cnt > 0 || has_lin) tc::tmem_ld32(tDV + lane_base + c0, v);
-      tc::tmem_ld_wait();
+    named_sync(1, 256);
+    // ---- dk_total = J_phi(k)^T (dK^phi + dZ_agg) + dK ; dv  (row-wise, 4 threads per row)
+    float dot = 0.f;
+    if (p.phi == 2 && has_lin) {
 #pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
-        float f[8], o[8], w8[8];
-        unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, c0 + 8 * ch)), f);
+      for (int cc = 0; cc < D / 4; cc += 8) {
+        float f[8];
+        unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, c0 + cc)), f);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          const int col = c0 + 8 * ch + e;
-          const float g = has_lin ? __uint_as_float(a[8 * ch + e]) + zas[col] : 0.f;
-          float jg;
-          if (p.phi == 2) jg = phi_of(f[e]) * (g - dot);
-          else if (p.phi == 0) jg = f[e] >= 0.f ? g : __expf(f[e]) * g;
-          else jg = f[e] > 0.f ? g : 0.f;
-          o[e] = jg + (cnt > 0 ? __uint_as_float(b[8 * ch + e]) : 0.f);
-          w8[e] = (cnt > 0 || has_lin) ? __uint_as_float(v[8 * ch + e]) : 0.f;
-        }
-        if (valid) {
-          *reinterpret_cast<uint4*>(p.dk + grow * D + c0 + 8 * ch) = pack8(o);
-          *reinterpret_cast<uint4*>(p.dv + grow * D + c0 + 8 * ch) = pack8(w8);
-        }
+        for (int e = 0; e < 8; ++e) dot = fmaf(phi_of(f[e]), tkp[c * TP + c0 + cc + e] + zas[c0 + cc + e], dot);
       }
+      dot += __shfl_xor_sync(0xffffffffu, dot, 1);
+      dot += __shfl_xor_sync(0xffffffffu, dot, 2);
+    }
+    const long long grow = (long long)kv0 + c;
+#pragma unroll
+    for (int cc = 0; cc < D / 4; cc += 8) {
+      const int col = c0 + cc;
+      float f[8], o[8], w8[8];
+      unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, col)), f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float g = has_lin ? tkp[c * TP + col + e] + zas[col + e] : 0.f;
+        float jg;
+        if (p.phi == 2) jg = phi_of(f[e]) * (g - dot);
+        else if (p.phi == 0) jg = f[e] >= 0.f ? g : __expf(f[e]) * g;
+        else jg = f[e] > 0.f ? g : 0.f;
+        o[e] = jg + tk[c * TP + col + e];
+        w8[e] = tv[c * TP + col + e];
+      }
+      *reinterpret_cast<uint4*>(p.dk + grow * D + col) = pack8(o);
+      *reinterpret_cast<uint4*>(p.dv + grow * D + col) = pack8(w8);
     }
   }
   tc::tc_fence_before();
@@ -941,7 +969,7 @@ void launch_cols_t(const Dims& Dm, const void* q, const void* k, const void* v, 
   make_tmap_bf16(&th, Ha, D, uint64_t(Dm.U) * Dm.Tn * D, 1, D, 0, D);
   auto kern = k_bwd_cols<D>;
   SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ColsLayout<D>::kBytes));
-  kern<<<dim3(Dm.Tn, unsigned(Dm.U)), 192, ColsLayout<D>::kBytes, st>>>(tq, tdo, tk, tv, th, p);
+  kern<<<dim3(Dm.Tn, unsigned(Dm.U)), 320, ColsLayout<D>::kBytes, st>>>(tq, tdo, tk, tv, th, p);
   check_launch("k_bwd_cols", st);
 }
 
