@@ -77,7 +77,7 @@ template <bool kTrans>
 __global__ void __launch_bounds__(256) k_aggregate_vec(const int8_t* __restrict__ labels,
                                                        const float* __restrict__ x, int d, int Tm,
                                                        int Tn, float* __restrict__ out) {
-  constexpr int BM = 64, BK = 32;
+  constexpr int BM = 16, BK = 32;
   __shared__ float sa[BK][BM + 1];   // indicator tile, [k][m]
   __shared__ float sx[BK][128];      // x tile, [k][a]
   const long long u = blockIdx.y;
@@ -86,9 +86,10 @@ __global__ void __launch_bounds__(256) k_aggregate_vec(const int8_t* __restrict_
   const int8_t* lu = labels + u * (long long)Tm * Tn;
   const float* xu = x + u * (long long)Kd * d;
   const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 8 row groups x 32 column lanes
-  float acc[8][4];
+  constexpr int RPT = BM / 8;  // rows per thread group
+  float acc[RPT][4];
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < RPT; ++i)
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[i][c] = 0.f;
   for (int k0 = 0; k0 < Kd; k0 += BK) {
@@ -114,16 +115,16 @@ __global__ void __launch_bounds__(256) k_aggregate_vec(const int8_t* __restrict_
 #pragma unroll
       for (int c = 0; c < 4; ++c) xv[c] = (tx + 32 * c < d) ? sx[kk][tx + 32 * c] : 0.f;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float w = sa[kk][ty * 8 + i];
+      for (int i = 0; i < RPT; ++i) {
+        const float w = sa[kk][ty * RPT + i];
 #pragma unroll
         for (int c = 0; c < 4; ++c) acc[i][c] = fmaf(w, xv[c], acc[i][c]);
       }
     }
   }
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int gm = m0 + ty * 8 + i;
+  for (int i = 0; i < RPT; ++i) {
+    const int gm = m0 + ty * RPT + i;
     if (gm >= Mo) continue;
 #pragma unroll
     for (int c = 0; c < 4; ++c)
@@ -202,7 +203,7 @@ void fast_prepare_linear(const Dims& Dm, const void* k, const void* v, const Sta
   a.c_batch = (long long)Dm.Tm * d * d;
   a.name = "gemm_aggregate";
   launch_gemm(a, st);
-  k_aggregate_vec<false><<<dim3((Dm.Tm + 63) / 64, unsigned(Dm.U)), 256, 0, st>>>(s.labels, wb.z, d, Dm.Tm,
+  k_aggregate_vec<false><<<dim3((Dm.Tm + 15) / 16, unsigned(Dm.U)), 256, 0, st>>>(s.labels, wb.z, d, Dm.Tm,
                                                                                 Dm.Tn, s.Z);
   check_launch("k_aggregate_z", st);
 }
@@ -242,7 +243,7 @@ void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, 
   a.c_batch = (long long)Dm.Tn * d * d;
   a.name = "gemm_aggregate_t";
   launch_gemm(a, st);
-  k_aggregate_vec<true><<<dim3((Dm.Tn + 63) / 64, unsigned(Dm.U)), 256, 0, st>>>(s.labels, wb.gZ, d, Dm.Tm,
+  k_aggregate_vec<true><<<dim3((Dm.Tn + 15) / 16, unsigned(Dm.U)), 256, 0, st>>>(s.labels, wb.gZ, d, Dm.Tm,
                                                                                Dm.Tn, wb.gZa);
   check_launch("k_aggregate_dz", st);
   // columns pass: dk_total, dv

@@ -8,6 +8,7 @@
 // Warp roles (192 threads): warp 0 = TMA producer, warp 1 = MMA issuer (one elected
 // thread), warps 2-5 = epilogue (TMEM -> registers -> global).  4-stage smem ring with
 // full/empty mbarriers; the accumulator lives in TMEM (BN columns).
+#include <algorithm>
 #include <cstdio>
 
 #include "kernels.hpp"
@@ -28,21 +29,26 @@ struct GemmSmem {
   static constexpr int kBytes = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
 };
 
+// Persistent: each CTA walks tiles blockIdx.x, +gridDim.x, ...; the smem ring runs across tile
+// boundaries and the TMEM accumulator is double-buffered (2 x BN columns) so the epilogue of
+// tile t overlaps the main loop of tile t+1.
 template <int BM, int BN, bool A_MN, bool B_MN, typename OutT>
 __global__ void __launch_bounds__(192, 1)
     k_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
-           OutT* __restrict__ C, int M, int N, int K, long long c_batch, int ldc) {
+           OutT* __restrict__ C, int M, int N, int K, int batch, long long c_batch, int ldc) {
   using L = GemmSmem<BM, BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * L::kStage);
   uint64_t* empty = full + kStages;
-  uint64_t* done = empty + kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* tfull = empty + kStages;  // [2]
+  uint64_t* tempty = tfull + 2;       // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM, b = blockIdx.z;
   const int nk = (K + kBK - 1) / kBK;
+  const int tiles_n = N / BN, tiles_m = (M + BM - 1) / BM;
+  const long long total = (long long)tiles_n * tiles_m * batch;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -52,99 +58,127 @@ __global__ void __launch_bounds__(192, 1)
         tc::mbar_init(&full[s], 1);
         tc::mbar_init(&empty[s], 1);
       }
-      tc::mbar_init(done, 1);
+      for (int s = 0; s < 2; ++s) {
+        tc::mbar_init(&tfull[s], 1);
+        tc::mbar_init(&tempty[s], 4);
+      }
       tc::fence_barrier_init();
     }
     __syncwarp();
-    tc::tmem_alloc<BN>(tmem_slot);
+    tc::tmem_alloc<2 * BN>(tmem_slot);
   }
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
+  auto coords = [&](long long t, int& n0, int& m0, int& b) {
+    n0 = int(t % tiles_n) * BN;
+    m0 = int((t / tiles_n) % tiles_m) * BM;
+    b = int(t / ((long long)tiles_n * tiles_m));
+  };
+
   if (warp == 0) {
     if (lane == 0) {
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % kStages;
-        const uint32_t ph = (kb / kStages) & 1;
-        tc::mbar_wait(&empty[s], ph ^ 1);
-        uint8_t* sa = smem + s * L::kStage;
-        uint8_t* sb = sa + L::kA;
-        tc::mbar_expect_tx(&full[s], L::kStage);
-        const int k0 = kb * kBK;
-        if (A_MN) {
+      int kc = 0;  // k-blocks issued by this CTA (ring position)
+      for (long long t = blockIdx.x; t < total; t += gridDim.x) {
+        int n0, m0, b;
+        coords(t, n0, m0, b);
+        for (int kb = 0; kb < nk; ++kb, ++kc) {
+          const int s = kc % kStages;
+          tc::mbar_wait(&empty[s], ((kc / kStages) & 1) ^ 1);
+          uint8_t* sa = smem + s * L::kStage;
+          uint8_t* sb = sa + L::kA;
+          tc::mbar_expect_tx(&full[s], L::kStage);
+          const int k0 = kb * kBK;
+          if (A_MN) {
 #pragma unroll
-          for (int c = 0; c < BM / 64; ++c) tc::tma_load_3d(sa + c * 8192, &ta, &full[s], m0 + 64 * c, k0, b);
-        } else {
-          tc::tma_load_3d(sa, &ta, &full[s], k0, m0, b);
-        }
-        if (B_MN) {
+            for (int c = 0; c < BM / 64; ++c) tc::tma_load_3d(sa + c * 8192, &ta, &full[s], m0 + 64 * c, k0, b);
+          } else {
+            tc::tma_load_3d(sa, &ta, &full[s], k0, m0, b);
+          }
+          if (B_MN) {
 #pragma unroll
-          for (int c = 0; c < BN / 64; ++c) tc::tma_load_3d(sb + c * 8192, &tb, &full[s], n0 + 64 * c, k0, b);
-        } else {
-          tc::tma_load_3d(sb, &tb, &full[s], k0, n0, b);
+            for (int c = 0; c < BN / 64; ++c) tc::tma_load_3d(sb + c * 8192, &tb, &full[s], n0 + 64 * c, k0, b);
+          } else {
+            tc::tma_load_3d(sb, &tb, &full[s], k0, n0, b);
+          }
         }
       }
     }
   } else if (warp == 1) {
     constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, A_MN, B_MN);
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % kStages;
-      const uint32_t ph = (kb / kStages) & 1;
-      tc::mbar_wait(&full[s], ph);
+    int kc = 0, lt = 0;
+    for (long long t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+      const int ab = lt & 1;
+      tc::mbar_wait(&tempty[ab], ((lt >> 1) & 1) ^ 1);
       tc::tc_fence_after();
-      if (lane == 0) {
-        const uint32_t sa = tc::smem_u32(smem + s * L::kStage);
-        const uint32_t sb = sa + L::kA;
+      const uint32_t acc = tmem + ab * BN;
+      for (int kb = 0; kb < nk; ++kb, ++kc) {
+        const int s = kc % kStages;
+        tc::mbar_wait(&full[s], (kc / kStages) & 1);
+        tc::tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sa = tc::smem_u32(smem + s * L::kStage);
+          const uint32_t sb = sa + L::kA;
 #pragma unroll
-        for (int kk = 0; kk < kBK / 16; ++kk) {
-          const uint64_t ad = A_MN ? tc::desc_mnmajor(sa + kk * 2048, 8192) : tc::desc_kmajor(sa + kk * 32);
-          const uint64_t bd = B_MN ? tc::desc_mnmajor(sb + kk * 2048, 8192) : tc::desc_kmajor(sb + kk * 32);
-          tc::mma_bf16(tmem, ad, bd, idesc, (kb | kk) != 0);
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            const uint64_t ad = A_MN ? tc::desc_mnmajor(sa + kk * 2048, 8192) : tc::desc_kmajor(sa + kk * 32);
+            const uint64_t bd = B_MN ? tc::desc_mnmajor(sb + kk * 2048, 8192) : tc::desc_kmajor(sb + kk * 32);
+            tc::mma_bf16(acc, ad, bd, idesc, (kb | kk) != 0);
+          }
+          tc::mma_commit(&empty[s]);
+          if (kb == nk - 1) tc::mma_commit(&tfull[ab]);
         }
-        tc::mma_commit(&empty[s]);
-        if (kb == nk - 1) tc::mma_commit(done);
+        __syncwarp();
       }
-      __syncwarp();
     }
   } else {
     // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
     const int q = warp & 3;
-    tc::mbar_wait(done, 0);
-    tc::tc_fence_after();
-    const int row = BM == 128 ? 32 * q + lane : 16 * q + lane;
-    const bool live = (BM == 128 || lane < 16) && (m0 + row) < M;
-    OutT* crow = C + (long long)b * c_batch + (long long)(m0 + row) * ldc + n0;
+    int lt = 0;
+    for (long long t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+      int n0, m0, b;
+      coords(t, n0, m0, b);
+      const int ab = lt & 1;
+      tc::mbar_wait(&tfull[ab], (lt >> 1) & 1);
+      tc::tc_fence_after();
+      const int row = BM == 128 ? 32 * q + lane : 16 * q + lane;
+      const bool live = (BM == 128 || lane < 16) && (m0 + row) < M;
+      OutT* crow = C + (long long)b * c_batch + (long long)(m0 + row) * ldc + n0;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      uint32_t r[32];
-      tc::tmem_ld32(tmem + (uint32_t(32 * q) << 16) + c0, r);
-      tc::tmem_ld_wait();
-      if (live) {
-        if constexpr (sizeof(OutT) == 4) {
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tc::tmem_ld32(tmem + ab * BN + (uint32_t(32 * q) << 16) + c0, r);
+        tc::tmem_ld_wait();
+        if (live) {
+          if constexpr (sizeof(OutT) == 4) {
 #pragma unroll
-          for (int e = 0; e < 32; e += 4)
-            *reinterpret_cast<float4*>(crow + c0 + e) =
-                make_float4(__uint_as_float(r[e]), __uint_as_float(r[e + 1]),
-                            __uint_as_float(r[e + 2]), __uint_as_float(r[e + 3]));
-        } else {
+            for (int e = 0; e < 32; e += 4)
+              *reinterpret_cast<float4*>(crow + c0 + e) =
+                  make_float4(__uint_as_float(r[e]), __uint_as_float(r[e + 1]),
+                              __uint_as_float(r[e + 2]), __uint_as_float(r[e + 3]));
+          } else {
 #pragma unroll
-          for (int e = 0; e < 32; e += 8) {
-            uint4 v;
-            v.x = tc::pack_bf16(__uint_as_float(r[e]), __uint_as_float(r[e + 1]));
-            v.y = tc::pack_bf16(__uint_as_float(r[e + 2]), __uint_as_float(r[e + 3]));
-            v.z = tc::pack_bf16(__uint_as_float(r[e + 4]), __uint_as_float(r[e + 5]));
-            v.w = tc::pack_bf16(__uint_as_float(r[e + 6]), __uint_as_float(r[e + 7]));
-            *reinterpret_cast<uint4*>(crow + c0 + e) = v;
+            for (int e = 0; e < 32; e += 8) {
+              uint4 v;
+              v.x = tc::pack_bf16(__uint_as_float(r[e]), __uint_as_float(r[e + 1]));
+              v.y = tc::pack_bf16(__uint_as_float(r[e + 2]), __uint_as_float(r[e + 3]));
+              v.z = tc::pack_bf16(__uint_as_float(r[e + 4]), __uint_as_float(r[e + 5]));
+              v.w = tc::pack_bf16(__uint_as_float(r[e + 6]), __uint_as_float(r[e + 7]));
+              *reinterpret_cast<uint4*>(crow + c0 + e) = v;
+            }
           }
         }
       }
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty[ab]);
     }
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc<BN>(tmem);
+  if (warp == 0) tc::tmem_dealloc<2 * BN>(tmem);
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -179,8 +213,11 @@ void launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
   auto kern = k_gemm<BM, BN, A_MN, B_MN, OutT>;
   constexpr int smem = GemmSmem<BM, BN>::kBytes;
   SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  dim3 grid(g.N / BN, (g.M + BM - 1) / BM, g.batch);
-  kern<<<grid, 192, smem, st>>>(ta, tb, static_cast<OutT*>(g.C), g.M, g.N, g.K, g.c_batch, g.ldc);
+  const long long tiles = (long long)(g.N / BN) * ((g.M + BM - 1) / BM) * g.batch;
+  static int sms = 0;
+  if (!sms) SLAB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const int grid = int(std::min<long long>(tiles, sms));
+  kern<<<grid, 192, smem, st>>>(ta, tb, static_cast<OutT*>(g.C), g.M, g.N, g.K, g.batch, g.c_batch, g.ldc);
   check_launch(g.name ? g.name : "k_gemm", st);
 }
 
