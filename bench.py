@@ -202,14 +202,12 @@ def algorithmic_work(name, D, labels_stats):
     B, H, N, d, b = D["B"], D["H"], D["N"], D["d"], D["b"]
     crit = labels_stats["critical_blocks"]  # total over all units
     tile = b * b * d
-    if name in ("k_fwd_generic", "k_fwd_attn"):
+    if name in ("k_fwd_generic", "k_attn_fwd"):       # S = QK^T, O += PV
         return "tensor", 4.0 * tile * crit
-    if name in ("k_bwd_rows_sparse",):
+    if name in ("k_bwd_rows_sparse", "k_bwd_rows"):    # S, dP recomputed, dQ += dS K
         return "tensor", 6.0 * tile * crit
-    if name in ("k_bwd_cols_sparse",):
+    if name in ("k_bwd_cols_sparse", "k_bwd_cols"):    # S, dP recomputed, dV += P^T dO, dK += dS^T Q
         return "tensor", 8.0 * tile * crit
-    if name in ("k_bwd_attn",):
-        return "tensor", 10.0 * tile * crit
     if name in ("k_pool(q)", "k_pool(k)"):
         return "hbm", B * H * N * d * 2.0
     return None, None
@@ -301,6 +299,10 @@ def run_ours(args):
     value = flops_step * world / (ms_max * 1e-3) / 1e12
 
     pk, pk_src = peaks()
+    try:  # DRAM bytes per launch from the committed ncu capture (profiles/traffic.json)
+        traffic_tab = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
+    except Exception:
+        traffic_tab = {}
     roof = None
     if kernels:
         dom = max(kernels.items(), key=lambda kv: kv[1][0])
@@ -311,14 +313,16 @@ def run_ours(args):
             ach = work / (avg * 1e-3) / 1e12
             peak = pk["bf16_tflops_sustained"]
             roof = {"kernel": nm, "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                    "frac": ach / peak, "traffic": None, "peak_source": f"{pk_src} bf16 sustained",
-                    "avg_launch_ms": avg, "share_of_step": tot_ms / args.steps / ms}
+                    "frac": ach / peak, "traffic": traffic_tab.get(nm), "peak_source": f"{pk_src} bf16 sustained",
+                    "algorithmic_flops_per_launch": work, "avg_launch_ms": avg,
+                    "share_of_step": tot_ms / args.steps / ms}
         elif kind == "hbm":
             ach = work / (avg * 1e-3) / 1e9
             peak = pk["hbm_gbs"]
             roof = {"kernel": nm, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                    "frac": ach / peak, "traffic": None, "peak_source": f"{pk_src} hbm copy",
-                    "avg_launch_ms": avg, "share_of_step": tot_ms / args.steps / ms}
+                    "frac": ach / peak, "traffic": traffic_tab.get(nm), "peak_source": f"{pk_src} hbm copy",
+                    "algorithmic_bytes_per_launch": work, "avg_launch_ms": avg,
+                    "share_of_step": tot_ms / args.steps / ms}
         else:
             roof = {"kernel": nm, "bound": None, "avg_launch_ms": avg}
 

@@ -109,22 +109,22 @@ inline void carve_work(const Dims& D, bool fast, void* base, WorkBufs& w, size_t
   w.Ds = c.take<float>(U * N);
   w.Dl = c.take<float>(U * N);
   w.gZ = c.take<float>(U * Tm * d);
-  w.qf = c.take<float>(U * N * d);
-  w.kf = c.take<float>(U * N * d);
-  w.dOl = c.take<float>(U * N * d);
-  w.gH = c.take<float>(U * Tm * d * d);
-  w.dq = c.take<float>(U * N * d);
-  w.dk = c.take<float>(U * N * d);
-  w.dv = c.take<float>(U * N * d);
-  w.dqf = c.take<float>(U * N * d);
-  w.dkf = c.take<float>(U * N * d);
-  if (fast) {
+  if (fast) {  // tcgen05 path: bf16 operands, the backward writes its totals directly
     w.hb = c.take<__nv_bfloat16>(U * Tn * d * d);
     w.kfb = c.take<__nv_bfloat16>(U * N * d);
     w.hab = c.take<__nv_bfloat16>(U * Tn * d * d);
     w.gZa = c.take<float>(U * Tn * d);
     w.dwp = c.take<float>(U * dw_chunks(D) * d * d);
-  } else {
+  } else {  // generic SIMT path: f32 scratch for every intermediate
+    w.qf = c.take<float>(U * N * d);
+    w.kf = c.take<float>(U * N * d);
+    w.dOl = c.take<float>(U * N * d);
+    w.gH = c.take<float>(U * Tm * d * d);
+    w.dq = c.take<float>(U * N * d);
+    w.dk = c.take<float>(U * N * d);
+    w.dv = c.take<float>(U * N * d);
+    w.dqf = c.take<float>(U * N * d);
+    w.dkf = c.take<float>(U * N * d);
     w.h = c.take<float>(U * Tn * d * d);
   }
   if (bytes) *bytes = c.off + 256;

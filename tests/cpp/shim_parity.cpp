@@ -1,0 +1,52 @@
+// Drop-in demonstration: the reference's own training-step call sequence
+// (core/src/finetune.cpp:44-61) run twice -- once through namespace sla (the reference CPU
+// library) and once through namespace sla::gpu (include/sla_b200.hpp over libsla_b200.so) --
+// on identical bf16-representable inputs.  Prints one JSON line of max-norm relative diffs.
+#include <cstdio>
+#include <cmath>
+
+#include "sla/backward.hpp"
+#include "sla/forward.hpp"
+#include "sla/rng.hpp"
+#include "sla_b200.hpp"
+
+using namespace sla;
+
+static MatF bf16_mat(SplitMix64& rng, size_t r, size_t c, double sd) {
+  MatF m(r, c);
+  for (auto& x : m.data) x = __bfloat162float(__float2bfloat16_rn(float(sd * rng.gaussian())));
+  return m;
+}
+
+int main(int argc, char** argv) {
+  const size_t n = argc > 1 ? size_t(atoi(argv[1])) : 1024, d = argc > 2 ? size_t(atoi(argv[2])) : 64;
+  SlaConfig cfg;
+  cfg.k_h = 5;
+  cfg.k_l = 10;
+  cfg.phi = FeatureMapKind::feat_softmax;
+  const auto layout = make_block_layout(n, d, 64, 64);
+  SplitMix64 rng(2024);
+  MatF q = bf16_mat(rng, n, d, 1.0), k = bf16_mat(rng, n, d, 1.0), v = bf16_mat(rng, n, d, 1.0);
+  MatF w = bf16_mat(rng, d, d, 0.1), dout = bf16_mat(rng, n, d, 1.0);
+
+  // reference
+  auto st = sla::sla_forward(q, k, v, cfg, layout, 8);
+  auto o = sla::combine_outputs(st, OutputProjection<float>{w});
+  auto [ds, dl, dw] = sla::proj_backward(dout, st.linear_out, w);
+  auto g = sla::sla_backward(st, q, k, v, ds, dl, cfg, layout, 8);
+
+  // drop-in (same calls, namespace sla::gpu)
+  auto st2 = sla::gpu::sla_forward(q, k, v, cfg, layout);
+  auto o2 = sla::gpu::combine_outputs(st2, OutputProjection<float>{w});
+  auto [ds2, dl2, dw2] = sla::gpu::proj_backward(dout, st2.linear_out, w);
+  auto g2 = sla::gpu::sla_backward(st2, q, k, v, ds2, dl2, cfg, layout);
+
+  const bool labels_equal = st.mask.labels == st2.mask.labels;
+  std::printf(
+      "{\"n\": %zu, \"d\": %zu, \"labels_equal\": %s, \"o\": %.3e, \"o_s\": %.3e, \"o_l\": %.3e, "
+      "\"dq_total\": %.3e, \"dk_total\": %.3e, \"dv\": %.3e, \"dw\": %.3e}\n",
+      n, d, labels_equal ? "true" : "false", rel_diff(o2, o, 1.0), rel_diff(st2.sparse_out, st.sparse_out, 1.0),
+      rel_diff(st2.linear_out, st.linear_out, 1.0), rel_diff(g2.dq_total, g.dq_total, 1.0),
+      rel_diff(g2.dk_total, g.dk_total, 1.0), rel_diff(g2.dv, g.dv, 1.0), rel_diff(g2.dproj, dw, 1.0));
+  return labels_equal ? 0 : 1;
+}
