@@ -1,0 +1,635 @@
+// attn_bwd_rows.cu -- the ROW phase of the SLA backward (backward.cpp:46-120, 211-214) as two
+// tcgen05 kernels:
+//
+// k_bwd_lin<D>: one CTA per (unit, query block i), 2 CTAs / SM -- the linear branch
+//   dO^l_i = dO_i W^T (MMA, backward.cpp:12-22), D^s, D^l (backward.cpp:48-58),
+//   x = phi(q), den = phi(q) . Z_i, [dH_i | -dZ_i] = x^T [dO^l/den | D^l/den] (one MMA),
+//   dQ^phi^T = H_i (dO^l/den)^T (MMA) - (D^l/den) Z_i  (backward.cpp:70-95).
+//   Outputs: D^s, dH_i (bf16, for the M0^T aggregation GEMM), dZ_i, dQ^phi (bf16 rows).
+// k_bwd_rows<D>: one CTA per (unit, query block i), 1 CTA / SM -- the sparse dQ
+//   critical key blocks in PAIRS: S^T = [K_j1; K_j2] Q^T, dP^T = [V_j1; V_j2] dO^T (M = 128),
+//   dS^T = P (dP - D^s) / sqrt(d), dQ^T += [K_j1; K_j2]^T dS^T (M = d) (backward.cpp:98-119),
+//   then dq_total = J_phi(q)^T dQ^phi + dQ (backward.cpp:211-214).
+//   K pairs and V pairs stream through separate rings (3 and 2 slots): V frees as soon as dP
+//   is done, so the tensor pipe keeps S/dP of the next pair queued behind dQ of this one.
+#include "bwd_common.cuh"
+
+namespace slab {
+namespace {
+
+// =========================================================================================
+// linear branch
+// =========================================================================================
+template <int D>
+struct LinLayout {
+  static constexpr int kT = 64 * D * 2;
+  static constexpr int oQ = 0, oDO = kT, oDOL = 2 * kT, oDL = 3 * kT, oX = 3 * kT + 8192;
+  static constexpr int oWH = oX + kT;   // W, then H_i (D*D*2)
+  static constexpr int oZS = oWH + D * D * 2;
+  static constexpr int oBar = oZS + 4 * D + 4 * 64;
+  static constexpr int kBytes = oBar + 128 + 1024;
+  static_assert(kBytes <= 116736, "2 CTAs / SM");
+};
+
+template <int D>
+__global__ void __launch_bounds__(192, 2)
+    k_bwd_lin(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
+              const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmH,
+              BwdParams p) {
+  using L = LinLayout<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem + L::oQ;
+  uint8_t* sDO = smem + L::oDO;
+  uint8_t* sDOL = smem + L::oDOL;
+  uint8_t* sDL = smem + L::oDL;
+  uint8_t* sX = smem + L::oX;
+  uint8_t* sWH = smem + L::oWH;
+  float* zs = reinterpret_cast<float*>(smem + L::oZS);
+  float* s_dls = zs + D;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::oBar);
+  uint64_t* qdo_full = bars + 0;
+  uint64_t* w_full = bars + 1;
+  uint64_t* w_free = bars + 2;
+  uint64_t* h_full = bars + 3;
+  uint64_t* dol_done = bars + 4;
+  uint64_t* x_ready = bars + 5;
+  uint64_t* lin_done = bars + 6;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x;
+  const long long u = blockIdx.y;
+  const long long urow = u * p.Tm + i;
+  const bool has_lin = p.marg_cnt[urow] > 0;
+  const int row0 = int(u * p.N) + i * 64;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::mbar_init(qdo_full, 1);
+      tc::mbar_init(w_full, 1);
+      tc::mbar_init(w_free, 1);
+      tc::mbar_init(h_full, 1);
+      tc::mbar_init(dol_done, 1);
+      tc::mbar_init(x_ready, 4);
+      tc::mbar_init(lin_done, 1);
+      tc::fence_barrier_init();
+    }
+    __syncwarp();
+    tc::tmem_alloc<256>(tmem_slot);
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  // dO^l (M = 64) at [0, D); then [dH | dZ] (M = D) at [0, D + 64) and dQ^phi^T (M = D) at [192, 256)
+  const uint32_t tA = tmem, tQP = tmem + 192;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::mbar_expect_tx(qdo_full, 2 * L::kT);
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        tc::tma_load_3d(sQ + c * 8192, &tmQ, qdo_full, 64 * c, row0, 0);
+        tc::tma_load_3d(sDO + c * 8192, &tmDO, qdo_full, 64 * c, row0, 0);
+      }
+      tc::mbar_expect_tx(w_full, D * D * 2);
+      const int h = int(u % p.H);
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) tc::tma_load_3d(sWH + c * D * 128, &tmW, w_full, 64 * c, h * D, 0);
+      if (has_lin) {
+        tc::mbar_wait(w_free, 0);
+        tc::mbar_expect_tx(h_full, D * D * 2);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) tc::tma_load_3d(sWH + c * D * 128, &tmH, h_full, 64 * c, int(urow * D), 0);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t aDO = tc::smem_u32(sDO), aDOL = tc::smem_u32(sDOL), aX = tc::smem_u32(sX);
+    const uint32_t aWH = tc::smem_u32(sWH);
+    constexpr uint32_t id_dol = tc::idesc_bf16(64, D, false, false);
+    constexpr uint32_t id_dh = tc::idesc_bf16(D, D + 64, true, true);
+    constexpr uint32_t id_qp = tc::idesc_bf16(D, 64, false, false);
+    auto kdesc = [](uint32_t base, int kk, int rows) {
+      return tc::desc_kmajor(base + (kk >> 2) * rows * 128 + (kk & 3) * 32);
+    };
+    tc::mbar_wait(qdo_full, 0);
+    tc::mbar_wait(w_full, 0);
+    tc::tc_fence_after();
+    if (lane == 0) {  // dO^l = dO W^T
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) tc::mma_bf16(tA, kdesc(aDO, kk, 64), kdesc(aWH, kk, D), id_dol, kk > 0);
+      tc::mma_commit(w_free);
+      tc::mma_commit(dol_done);
+    }
+    __syncwarp();
+    if (has_lin) {
+      tc::mbar_wait(x_ready, 0);
+      tc::mbar_wait(h_full, 0);
+      tc::tc_fence_after();
+      if (lane == 0) {
+        // dQ^phi^T raw = H_i (dO^l/den)^T  (M = D over a, N = 64 rows, K = D over b)
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) tc::mma_bf16(tQP, kdesc(aWH, kk, D), kdesc(aDOL, kk, 64), id_qp, kk > 0);
+        // [dH_i | -dZ_i] = phi(Q)^T [dO^l/den | D^l/den]  (M = D, N = D + 64, K = 64 rows)
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          tc::mma_bf16(tA, tc::desc_mnmajor(aX + kk * 2048, 8192), tc::desc_mnmajor(aDOL + kk * 2048, 8192), id_dh, kk > 0);
+        tc::mma_commit(lin_done);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int q4 = warp & 3;
+    const int r = 16 * q4 + (lane & 15);
+    const int h0 = (lane >> 4) * (D / 2);
+    const bool valid = lane < 16;
+    const uint32_t lane_base = uint32_t(32 * q4) << 16;
+    const long long grow = (long long)row0 + r;
+    const int tid = threadIdx.x - 64;
+    for (int a = tid; a < D; a += 128) zs[a] = has_lin ? p.Z[urow * D + a] : 0.f;
+    for (int e = tid; e < 64 * 7; e += 128)
+      *reinterpret_cast<uint4*>(sDL + tc::sw128_off(e / 7, 1 + e % 7)) = make_uint4(0, 0, 0, 0);
+    named_sync(1, 128);
+    tc::mbar_wait(qdo_full, 0);
+    float ds_r = 0.f;
+#pragma unroll
+    for (int c = 0; c < D / 2; c += 8) {
+      float f[8], g[8];
+      unpack8(*reinterpret_cast<const uint4*>(sDO + tile_off(r, h0 + c)), f);
+      unpack8(*reinterpret_cast<const uint4*>(p.o_s + grow * D + h0 + c), g);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) ds_r = fmaf(f[e], g[e], ds_r);
+    }
+    ds_r += __shfl_xor_sync(0xffffffffu, ds_r, 16);
+    if (valid) p.Ds_out[grow] = ds_r;
+    float mx = 0.f, inv = 1.f;
+    if (p.phi == 2) {
+      mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < D / 2; c += 8) {
+        float f[8];
+        unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(r, h0 + c)), f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) mx = fmaxf(mx, f[e]);
+      }
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+      float se = 0.f;
+#pragma unroll
+      for (int c = 0; c < D / 2; c += 8) {
+        float f[8];
+        unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(r, h0 + c)), f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) se += __expf(f[e] - mx);
+      }
+      se += __shfl_xor_sync(0xffffffffu, se, 16);
+      inv = 1.f / se;
+    }
+    float den = 0.f;
+#pragma unroll
+    for (int c = 0; c < D / 2; c += 8) {
+      float f[8];
+      unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(r, h0 + c)), f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        f[e] = p.phi == 2 ? __expf(f[e] - mx) * inv : phi_elem(p.phi, f[e]);
+        den = fmaf(f[e], zs[h0 + c + e], den);
+      }
+      *reinterpret_cast<uint4*>(sX + tile_off(r, h0 + c)) = pack8(f);
+    }
+    den += __shfl_xor_sync(0xffffffffu, den, 16);
+    const float inv_den = (has_lin && den != 0.f) ? 1.f / den : 0.f;  // den == 0 -> zero row
+    tc::mbar_wait(dol_done, 0);
+    tc::tc_fence_after();
+    float dl_r = 0.f;
+#pragma unroll 1
+    for (int c0 = 0; c0 < D; c0 += 32) {
+      uint32_t a[32];
+      tc::tmem_ld32(tA + lane_base + c0, a);
+      tc::tmem_ld_wait();
+      if (valid) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float f[8], g[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(a[8 * c + e]);
+          unpack8(*reinterpret_cast<const uint4*>(p.o_l + grow * D + c0 + 8 * c), g);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            dl_r = fmaf(f[e], g[e], dl_r);
+            f[e] *= inv_den;
+          }
+          *reinterpret_cast<uint4*>(sDOL + tile_off(r, c0 + 8 * c)) = pack8(f);
+        }
+      }
+    }
+    const float dls = dl_r * inv_den;  // D^l / den
+    if (valid) {
+      *reinterpret_cast<uint4*>(sDL + tc::sw128_off(r, 0)) = make_uint4(tc::pack_bf16(dls, 0.f), 0, 0, 0);
+      s_dls[r] = dls;
+    }
+    tc::fence_proxy_async();
+    tc::tc_fence_before();
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(x_ready);
+    named_sync(1, 128);  // s_dls visible
+    __nv_bfloat16* gHi = p.gH + urow * D * D;
+    __nv_bfloat16* dqp = p.dqphi + (long long)row0 * D;
+    if (has_lin) {
+      tc::mbar_wait(lin_done, 0);
+      tc::tc_fence_after();
+      const int arow = D == 128 ? 32 * q4 + lane : 16 * q4 + lane;
+      const bool avalid = D == 128 || lane < 16;
+#pragma unroll 1
+      for (int c0 = 0; c0 < D + 32; c0 += 32) {
+        uint32_t a[32];
+        tc::tmem_ld32(tA + lane_base + c0, a);
+        tc::tmem_ld_wait();
+        if (!avalid) continue;
+        if (c0 == D) {
+          p.gZ[urow * D + arow] = -__uint_as_float(a[0]);
+          continue;
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          float f[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(a[8 * c + e]);
+          *reinterpret_cast<uint4*>(gHi + arow * D + c0 + 8 * c) = pack8(f);
+        }
+      }
+      // dQ^phi[r][a] = raw^T[a][r] - (D^l/den)_r Z[a]; stage as a row-major bf16 tile in sX
+      // (phi(Q) is dead once lin_done fired), then store coalesced rows
+      const float za = avalid ? zs[arow] : 0.f;
+#pragma unroll 1
+      for (int c0 = 0; c0 < 64; c0 += 32) {
+        uint32_t a[32];
+        tc::tmem_ld32(tQP + lane_base + c0, a);
+        tc::tmem_ld_wait();
+        if (!avalid) continue;
+#pragma unroll
+        for (int e = 0; e < 32; ++e) {
+          const int rr = c0 + e;
+          const float v = __uint_as_float(a[e]) - s_dls[rr] * za;
+          *reinterpret_cast<__nv_bfloat16*>(sX + tile_off(rr, arow & ~7) + (arow & 7) * 2) = __float2bfloat16_rn(v);
+        }
+      }
+      named_sync(1, 128);
+      for (int e = tid; e < 64 * D / 8; e += 128) {
+        const int rr = e / (D / 8), cc = (e % (D / 8)) * 8;
+        *reinterpret_cast<uint4*>(dqp + (long long)rr * D + cc) = *reinterpret_cast<const uint4*>(sX + tile_off(rr, cc));
+      }
+    } else {
+      for (int e = tid; e < D * D / 8; e += 128) reinterpret_cast<uint4*>(gHi)[e] = make_uint4(0, 0, 0, 0);
+      for (int a = tid; a < D; a += 128) p.gZ[urow * D + a] = 0.f;
+      for (int e = tid; e < 64 * D / 8; e += 128) reinterpret_cast<uint4*>(dqp)[e] = make_uint4(0, 0, 0, 0);
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<256>(tmem);
+}
+
+// =========================================================================================
+// sparse dQ over pairs of critical key blocks
+// =========================================================================================
+template <int D>
+struct RowsLayout {
+  static constexpr int kT = 64 * D * 2;   // 64-row tile
+  static constexpr int kP = 128 * D * 2;  // 128-row pair tile
+  static constexpr int KS = 3, VS = 2;    // K-pair and V-pair ring slots
+  static constexpr int oQ = 0, oDO = kT, oDS = 2 * kT;  // dS^T [128 kv][64 q] bf16 (16 KB)
+  static constexpr int oK = oDS + 16384;
+  static constexpr int oV = oK + KS * kP;
+  static constexpr int oSM = oV + VS * kP;  // floats: lse2[64], ds[64]
+  static constexpr int oBar = oSM + 512;
+  static constexpr int kBytes = oBar + 256 + 1024;
+  static_assert(kBytes <= 232448, "smem");
+};
+
+template <int D>
+__global__ void __launch_bounds__(320, 1)
+    k_bwd_rows(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
+               const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+               BwdParams p) {
+  using L = RowsLayout<D>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sQ = smem + L::oQ;
+  uint8_t* sDO = smem + L::oDO;
+  uint8_t* sDS = smem + L::oDS;
+  uint8_t* sK = smem + L::oK;
+  uint8_t* sV = smem + L::oV;
+  float* s_lse2 = reinterpret_cast<float*>(smem + L::oSM);
+  float* s_ds = s_lse2 + 64;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::oBar);
+  uint64_t* qdo_full = bars + 0;
+  uint64_t* sdp_full = bars + 1;   // [2]
+  uint64_t* ds_full = bars + 3;
+  uint64_t* ds_empty = bars + 4;
+  uint64_t* dq_done = bars + 5;
+  uint64_t* k_full = bars + 8;     // [KS]
+  uint64_t* k_empty = bars + 11;   // [KS]
+  uint64_t* v_full = bars + 14;    // [VS]
+  uint64_t* v_empty = bars + 16;   // [VS]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x;
+  const long long u = blockIdx.y;
+  const long long urow = u * p.Tm + i;
+  const int cnt = p.crit_cnt[urow];
+  const int* list = p.crit_idx + urow * p.Tn;
+  const int np = (cnt + 1) >> 1;
+  const int row0 = int(u * p.N) + i * 64;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::mbar_init(qdo_full, 1);
+      for (int s = 0; s < 2; ++s) tc::mbar_init(sdp_full + s, 1);
+      tc::mbar_init(ds_full, 8);
+      tc::mbar_init(ds_empty, 1);
+      tc::mbar_init(dq_done, 1);
+      for (int s = 0; s < L::KS; ++s) {
+        tc::mbar_init(k_full + s, 1);
+        tc::mbar_init(k_empty + s, 1);
+      }
+      for (int s = 0; s < L::VS; ++s) {
+        tc::mbar_init(v_full + s, 1);
+        tc::mbar_init(v_empty + s, 1);
+      }
+      tc::fence_barrier_init();
+    }
+    __syncwarp();
+    tc::tmem_alloc<512>(tmem_slot);
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tDQT = tmem, tB0 = tmem + 128, tB1 = tmem + 256;  // dQ^T (M = D); S^T|dP^T pairs
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::mbar_expect_tx(qdo_full, 2 * L::kT);
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        tc::tma_load_3d(sQ + c * 8192, &tmQ, qdo_full, 64 * c, row0, 0);
+        tc::tma_load_3d(sDO + c * 8192, &tmDO, qdo_full, 64 * c, row0, 0);
+      }
+      for (int t = 0; t < np; ++t) {
+        // an odd tail repeats its block (finite data); the compute warps zero its dS rows
+        const int r1 = int(u * p.N) + list[2 * t] * 64;
+        const int r2 = int(u * p.N) + list[min(2 * t + 1, cnt - 1)] * 64;
+        const int ks = t % L::KS, vs = t % L::VS;
+        tc::mbar_wait(k_empty + ks, ((t / L::KS) & 1) ^ 1);
+        tc::mbar_expect_tx(k_full + ks, L::kP);
+        uint8_t* dk = sK + ks * L::kP;
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) {
+          tc::tma_load_3d(dk + c * 16384, &tmK, k_full + ks, 64 * c, r1, 0);
+          tc::tma_load_3d(dk + c * 16384 + 8192, &tmK, k_full + ks, 64 * c, r2, 0);
+        }
+        tc::mbar_wait(v_empty + vs, ((t / L::VS) & 1) ^ 1);
+        tc::mbar_expect_tx(v_full + vs, L::kP);
+        uint8_t* dv = sV + vs * L::kP;
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) {
+          tc::tma_load_3d(dv + c * 16384, &tmV, v_full + vs, 64 * c, r1, 0);
+          tc::tma_load_3d(dv + c * 16384 + 8192, &tmV, v_full + vs, 64 * c, r2, 0);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t aQ = tc::smem_u32(sQ), aDO = tc::smem_u32(sDO), aDS = tc::smem_u32(sDS);
+    const uint32_t aK = tc::smem_u32(sK), aV = tc::smem_u32(sV);
+    constexpr uint32_t id_st = tc::idesc_bf16(128, 64, false, false);  // pair x Q^T
+    constexpr uint32_t id_dqt = tc::idesc_bf16(D, 64, true, true);     // pair^T x dS^T
+    auto kdesc = [](uint32_t base, int kk, int rows) {
+      return tc::desc_kmajor(base + (kk >> 2) * rows * 128 + (kk & 3) * 32);
+    };
+    tc::mbar_wait(qdo_full, 0);
+    auto issue_dq = [&](int j) {  // dQ^T += [K_j1; K_j2]^T dS^T  (M = D, N = 64, K = 128)
+      tc::mbar_wait(ds_full, j & 1);
+      tc::tc_fence_after();
+      if (lane == 0) {
+        const uint32_t sk = aK + (j % L::KS) * L::kP;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          tc::mma_bf16(tDQT, tc::desc_mnmajor(sk + kk * 2048, 16384), tc::desc_mnmajor(aDS + kk * 2048, 16384),
+                       id_dqt, (j | kk) != 0);
+        tc::mma_commit(k_empty + (j % L::KS));
+        tc::mma_commit(ds_empty);
+      }
+      __syncwarp();
+    };
+    for (int t = 0; t < np; ++t) {
+      const int ks = t % L::KS, vs = t % L::VS;
+      tc::mbar_wait(k_full + ks, (t / L::KS) & 1);
+      tc::mbar_wait(v_full + vs, (t / L::VS) & 1);
+      tc::tc_fence_after();
+      if (lane == 0) {
+        const uint32_t tb = (t & 1) ? tB1 : tB0;
+        const uint32_t sk = aK + ks * L::kP, sv = aV + vs * L::kP;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          tc::mma_bf16(tb, kdesc(sk, kk, 128), kdesc(aQ, kk, 64), id_st, kk > 0);        // S^T
+          tc::mma_bf16(tb + 64, kdesc(sv, kk, 128), kdesc(aDO, kk, 64), id_st, kk > 0);  // dP^T
+        }
+        tc::mma_commit(sdp_full + (t & 1));
+        tc::mma_commit(v_empty + vs);
+      }
+      __syncwarp();
+      if (t > 0) issue_dq(t - 1);
+    }
+    if (np > 0) issue_dq(np - 1);
+    if (lane == 0) tc::mma_commit(dq_done);
+    __syncwarp();
+  } else {
+    const int q4 = warp & 3;
+    const int grp = (warp - 2) >> 2;
+    const uint32_t lane_base = uint32_t(32 * q4) << 16;
+    const int tid = threadIdx.x - 64;  // 0..255
+    if (tid < 64) s_lse2[tid] = p.lse[(long long)row0 + tid] * 1.4426950408889634f;
+    else if (tid < 128) s_ds[tid - 64] = p.Ds[(long long)row0 + tid - 64];
+    named_sync(1, 256);
+    const int c = 32 * q4 + lane;  // key row of the pair (c < 64: block j1, else j2)
+#pragma unroll 1
+    for (int t = 0; t < np; ++t) {
+      tc::mbar_wait(sdp_full + (t & 1), (t >> 1) & 1);
+      tc::tc_fence_after();
+      const bool live = c < 64 || 2 * t + 1 < cnt;
+      const uint32_t tb = ((t & 1) ? tB1 : tB0) + lane_base + 32 * grp;
+      uint32_t pk[16];
+      {
+        uint32_t sv[32], dp[32];
+        tc::tmem_ld32(tb, sv);
+        tc::tmem_ld32(tb + 64, dp);
+        tc::tmem_ld_wait();
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) {
+          const int rr = 32 * grp + e;
+          const float p0 = ex2f(__uint_as_float(sv[e]) * p.scale_log2 - s_lse2[rr]);
+          const float p1 = ex2f(__uint_as_float(sv[e + 1]) * p.scale_log2 - s_lse2[rr + 1]);
+          const float d0 = live ? p0 * (__uint_as_float(dp[e]) - s_ds[rr]) * p.scale : 0.f;
+          const float d1 = live ? p1 * (__uint_as_float(dp[e + 1]) - s_ds[rr + 1]) * p.scale : 0.f;
+          pk[e >> 1] = tc::pack_bf16(d0, d1);
+        }
+      }
+      if (t >= 1) tc::mbar_wait(ds_empty, (t - 1) & 1);  // dQ of the previous pair has read dS
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch)
+        *reinterpret_cast<uint4*>(sDS + tc::sw128_off(c, 4 * grp + ch)) =
+            make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+      tc::fence_proxy_async();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(ds_full);
+    }
+    // dq_total = J_phi(q)^T dQ^phi + dQ: transpose dQ^T through smem (the K ring is idle once
+    // dq_done fired), then finish row-wise with 4 threads per query row.  For the softmax
+    // feature map <phi(q), dQ^phi> = D^l - (D^l/den) den = 0 exactly (O^l = phi(q) H / den), so
+    // the Jacobian reduces to phi(q) * dQ^phi.
+    tc::mbar_wait(dq_done, 0);
+    tc::tc_fence_after();
+    constexpr int TP = D + 4;
+    float* tq = reinterpret_cast<float*>(sK);
+    {
+      const int acol = D == 128 ? 32 * q4 + lane : 16 * q4 + lane;
+      const bool avalid = D == 128 || lane < 16;
+      uint32_t b[32];
+      if (np > 0) tc::tmem_ld32(tDQT + lane_base + 32 * grp, b);
+      tc::tmem_ld_wait();
+      if (avalid) {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) tq[(32 * grp + e) * TP + acol] = np > 0 ? __uint_as_float(b[e]) : 0.f;
+      }
+    }
+    named_sync(1, 256);
+    {
+      const int rq = tid >> 2, c0 = (tid & 3) * (D / 4);
+      float mx = 0.f, inv = 1.f;
+      if (p.phi == 2) {
+        mx = -INFINITY;
+#pragma unroll
+        for (int cc = 0; cc < D / 4; cc += 8) {
+          float x[8];
+          unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(rq, c0 + cc)), x);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) mx = fmaxf(mx, x[e]);
+        }
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        float se = 0.f;
+#pragma unroll
+        for (int cc = 0; cc < D / 4; cc += 8) {
+          float x[8];
+          unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(rq, c0 + cc)), x);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) se += __expf(x[e] - mx);
+        }
+        se += __shfl_xor_sync(0xffffffffu, se, 1);
+        se += __shfl_xor_sync(0xffffffffu, se, 2);
+        inv = 1.f / se;
+      }
+      const long long grow = (long long)row0 + rq;
+#pragma unroll
+      for (int cc = 0; cc < D / 4; cc += 8) {
+        const int col = c0 + cc;
+        float x[8], g[8], o[8];
+        unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(rq, col)), x);
+        unpack8(*reinterpret_cast<const uint4*>(p.dqphi + grow * D + col), g);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          float jg;
+          if (p.phi == 2) jg = __expf(x[e] - mx) * inv * g[e];
+          else if (p.phi == 0) jg = x[e] >= 0.f ? g[e] : __expf(x[e]) * g[e];
+          else jg = x[e] > 0.f ? g[e] : 0.f;
+          o[e] = jg + tq[rq * TP + col + e];
+        }
+        *reinterpret_cast<uint4*>(p.dq + grow * D + col) = pack8(o);
+      }
+    }
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(tmem);
+}
+
+}  // namespace
+
+void launch_bwd_lin(const Dims& Dm, const void* q, const void* w, const void* o_s, const void* o_l,
+                    const void* d_out, const StateBufs& s, __nv_bfloat16* gH, float* gZ, float* Ds,
+                    __nv_bfloat16* dqphi, cudaStream_t st) {
+  BwdParams p{};
+  p.marg_cnt = s.marg_cnt;
+  p.Z = s.Z;
+  p.Ds_out = Ds;
+  p.o_s = static_cast<const __nv_bfloat16*>(o_s);
+  p.o_l = static_cast<const __nv_bfloat16*>(o_l);
+  p.gH = gH;
+  p.gZ = gZ;
+  p.dqphi = dqphi;
+  p.N = Dm.N;
+  p.Tm = Dm.Tm;
+  p.Tn = Dm.Tn;
+  p.H = int(Dm.H);
+  p.phi = Dm.phi;
+  const uint64_t rows = uint64_t(Dm.U) * Dm.N;
+  CUtensorMap tq, tdo, tw, th;
+  auto go = [&](auto kern, int bytes, auto dd) {
+    constexpr int D = decltype(dd)::value;
+    make_tmap_bf16(&tq, q, D, rows, 1, D, 0, 64);
+    make_tmap_bf16(&tdo, d_out, D, rows, 1, D, 0, 64);
+    make_tmap_bf16(&tw, w, D, uint64_t(Dm.H) * D, 1, D, 0, D);
+    make_tmap_bf16(&th, s.Hb, D, uint64_t(Dm.U) * Dm.Tm * D, 1, D, 0, D);
+    SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    kern<<<dim3(Dm.Tm, unsigned(Dm.U)), 192, bytes, st>>>(tq, tdo, tw, th, p);
+    check_launch("k_bwd_lin", st);
+  };
+  if (Dm.d == 128)
+    go(k_bwd_lin<128>, LinLayout<128>::kBytes, std::integral_constant<int, 128>{});
+  else
+    go(k_bwd_lin<64>, LinLayout<64>::kBytes, std::integral_constant<int, 64>{});
+}
+
+void launch_bwd_rows(const Dims& Dm, const void* q, const void* k, const void* v, const float* lse,
+                     const void* d_out, void* dq, const StateBufs& s, const float* Ds,
+                     const __nv_bfloat16* dqphi, cudaStream_t st) {
+  BwdParams p{};
+  p.crit_cnt = s.crit_cnt;
+  p.crit_idx = s.crit_idx;
+  p.lse = lse;
+  p.Ds = Ds;
+  p.dqphi = const_cast<__nv_bfloat16*>(dqphi);
+  p.dq = static_cast<__nv_bfloat16*>(dq);
+  p.N = Dm.N;
+  p.Tm = Dm.Tm;
+  p.Tn = Dm.Tn;
+  p.H = int(Dm.H);
+  p.scale = float(Dm.inv_sqrt_d);
+  p.scale_log2 = float(Dm.inv_sqrt_d * 1.4426950408889634);
+  p.phi = Dm.phi;
+  const uint64_t rows = uint64_t(Dm.U) * Dm.N;
+  CUtensorMap tq, tdo, tk, tv;
+  auto go = [&](auto kern, int bytes, auto dd) {
+    constexpr int D = decltype(dd)::value;
+    make_tmap_bf16(&tq, q, D, rows, 1, D, 0, 64);
+    make_tmap_bf16(&tdo, d_out, D, rows, 1, D, 0, 64);
+    make_tmap_bf16(&tk, k, D, rows, 1, D, 0, 64);
+    make_tmap_bf16(&tv, v, D, rows, 1, D, 0, 64);
+    SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    kern<<<dim3(Dm.Tm, unsigned(Dm.U)), 320, bytes, st>>>(tq, tdo, tk, tv, p);
+    check_launch("k_bwd_rows", st);
+  };
+  if (Dm.d == 128)
+    go(k_bwd_rows<128>, RowsLayout<128>::kBytes, std::integral_constant<int, 128>{});
+  else
+    go(k_bwd_rows<64>, RowsLayout<64>::kBytes, std::integral_constant<int, 64>{});
+}
+
+}  // namespace slab
+
+extern "C" int sla_b200_diag_bwd_timeline(long long* host128) {
+  return cudaMemcpyFromSymbol(host128, slab::g_bwd_ts, 128 * sizeof(long long)) == cudaSuccess ? 0 : 1;
+}

@@ -54,6 +54,7 @@ struct WorkBufs {
   __nv_bfloat16* hab = nullptr;  // fast path: dH_agg = M0^T dH in bf16, [U, Tn, d*d]
   float* gZa = nullptr;          // fast path: dZ_agg [U, Tn, d]
   float* dwp = nullptr;          // fast path: split-K partials of dW [U * N / 64, d, d]
+  __nv_bfloat16* dqphi = nullptr;  // fast path: dQ^phi [U, N, d] (linear kernel -> rows kernel)
 };
 
 // split-K factor of the fast path's dW GEMM: row chunks of 64*c rows, c | N/64, c <= 32
@@ -115,6 +116,7 @@ inline void carve_work(const Dims& D, bool fast, void* base, WorkBufs& w, size_t
     w.hab = c.take<__nv_bfloat16>(U * Tn * d * d);
     w.gZa = c.take<float>(U * Tn * d);
     w.dwp = c.take<float>(U * dw_chunks(D) * d * d);
+    w.dqphi = c.take<__nv_bfloat16>(U * N * d);
   } else {  // generic SIMT path: f32 scratch for every intermediate
     w.qf = c.take<float>(U * N * d);
     w.kf = c.take<float>(U * N * d);

@@ -221,8 +221,10 @@ void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, 
                    const WorkBufs& wb, cudaStream_t st) {
   const int d = Dm.d;
   launch_build_csc(Dm, s, st);
-  // rows pass: dq_total, dH_i (bf16, reusing the forward's h scratch), dZ_i, D^s
-  launch_bwd_rows(Dm, q, k, v, w, o_s, o_l, lse, d_out, dq, s, wb.hb, wb.gZ, wb.Ds, st);
+  // row phase: the linear branch (dH_i reusing the forward's h scratch, dZ_i, D^s, dQ^phi),
+  // then the sparse dQ over critical pairs with dq_total = J_phi^T dQ^phi + dQ
+  launch_bwd_lin(Dm, q, w, o_s, o_l, d_out, s, wb.hb, wb.gZ, wb.Ds, wb.dqphi, st);
+  launch_bwd_rows(Dm, q, k, v, lse, d_out, dq, s, wb.Ds, wb.dqphi, st);
   // dH_agg = M0^T dH (A = M0 read M-major), dZ_agg
   GemmArgs a{};
   a.A = s.M0;

@@ -44,9 +44,12 @@ void launch_attn_fwd(const Dims& Dm, const void* q, const void* k, const void* v
                      void* o, void* o_s, void* o_l, float* lse, const StateBufs& s, cudaStream_t st);
 void fast_prepare_linear(const Dims& Dm, const void* k, const void* v, const StateBufs& s,
                          const WorkBufs& wb, cudaStream_t st);
-void launch_bwd_rows(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
-                     const void* o_s, const void* o_l, const float* lse, const void* d_out, void* dq,
-                     const StateBufs& s, __nv_bfloat16* gH, float* gZ, float* Ds, cudaStream_t st);
+void launch_bwd_lin(const Dims& Dm, const void* q, const void* w, const void* o_s, const void* o_l,
+                    const void* d_out, const StateBufs& s, __nv_bfloat16* gH, float* gZ, float* Ds,
+                    __nv_bfloat16* dqphi, cudaStream_t st);
+void launch_bwd_rows(const Dims& Dm, const void* q, const void* k, const void* v, const float* lse,
+                     const void* d_out, void* dq, const StateBufs& s, const float* Ds,
+                     const __nv_bfloat16* dqphi, cudaStream_t st);
 void launch_bwd_cols(const Dims& Dm, const void* q, const void* k, const void* v, const float* lse,
                      const void* d_out, void* dk, void* dv, const StateBufs& s,
                      const __nv_bfloat16* Ha, const float* gZa, const float* Ds, cudaStream_t st);
