@@ -35,6 +35,7 @@ template <int D>
 __global__ void __launch_bounds__(192, 2)
     k_bwd_lin(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
               const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmH,
+              const __grid_constant__ CUtensorMap tmOS, const __grid_constant__ CUtensorMap tmOL,
               BwdParams p) {
   using L = LinLayout<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -55,6 +56,7 @@ __global__ void __launch_bounds__(192, 2)
   uint64_t* dol_done = bars + 4;
   uint64_t* x_ready = bars + 5;
   uint64_t* lin_done = bars + 6;
+  uint64_t* o_full = bars + 7;  // O^s -> sX and O^l -> sDOL (both consumed before being overwritten)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -73,6 +75,7 @@ __global__ void __launch_bounds__(192, 2)
       tc::mbar_init(dol_done, 1);
       tc::mbar_init(x_ready, 4);
       tc::mbar_init(lin_done, 1);
+      tc::mbar_init(o_full, 1);
       tc::fence_barrier_init();
     }
     __syncwarp();
@@ -92,6 +95,12 @@ __global__ void __launch_bounds__(192, 2)
       for (int c = 0; c < D / 64; ++c) {
         tc::tma_load_3d(sQ + c * 8192, &tmQ, qdo_full, 64 * c, row0, 0);
         tc::tma_load_3d(sDO + c * 8192, &tmDO, qdo_full, 64 * c, row0, 0);
+      }
+      tc::mbar_expect_tx(o_full, 2 * L::kT);
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        tc::tma_load_3d(sX + c * 8192, &tmOS, o_full, 64 * c, row0, 0);
+        tc::tma_load_3d(sDOL + c * 8192, &tmOL, o_full, 64 * c, row0, 0);
       }
       tc::mbar_expect_tx(w_full, D * D * 2);
       const int h = int(u % p.H);
@@ -152,17 +161,19 @@ __global__ void __launch_bounds__(192, 2)
       *reinterpret_cast<uint4*>(sDL + tc::sw128_off(e / 7, 1 + e % 7)) = make_uint4(0, 0, 0, 0);
     named_sync(1, 128);
     tc::mbar_wait(qdo_full, 0);
+    tc::mbar_wait(o_full, 0);
     float ds_r = 0.f;
 #pragma unroll
     for (int c = 0; c < D / 2; c += 8) {
       float f[8], g[8];
       unpack8(*reinterpret_cast<const uint4*>(sDO + tile_off(r, h0 + c)), f);
-      unpack8(*reinterpret_cast<const uint4*>(p.o_s + grow * D + h0 + c), g);
+      unpack8(*reinterpret_cast<const uint4*>(sX + tile_off(r, h0 + c)), g);
 #pragma unroll
       for (int e = 0; e < 8; ++e) ds_r = fmaf(f[e], g[e], ds_r);
     }
     ds_r += __shfl_xor_sync(0xffffffffu, ds_r, 16);
     if (valid) p.Ds_out[grow] = ds_r;
+    named_sync(1, 128);  // O^s (in sX) fully consumed before phi(Q) overwrites it
     float mx = 0.f, inv = 1.f;
     if (p.phi == 2) {
       mx = -INFINITY;
@@ -213,13 +224,13 @@ __global__ void __launch_bounds__(192, 2)
           float f[8], g[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(a[8 * c + e]);
-          unpack8(*reinterpret_cast<const uint4*>(p.o_l + grow * D + c0 + 8 * c), g);
+          unpack8(*reinterpret_cast<const uint4*>(sDOL + tile_off(r, c0 + 8 * c)), g);  // O^l row
 #pragma unroll
           for (int e = 0; e < 8; ++e) {
             dl_r = fmaf(f[e], g[e], dl_r);
             f[e] *= inv_den;
           }
-          *reinterpret_cast<uint4*>(sDOL + tile_off(r, c0 + 8 * c)) = pack8(f);
+          *reinterpret_cast<uint4*>(sDOL + tile_off(r, c0 + 8 * c)) = pack8(f);  // same thread, same row
         }
       }
     }
@@ -576,15 +587,17 @@ void launch_bwd_lin(const Dims& Dm, const void* q, const void* w, const void* o_
   p.H = int(Dm.H);
   p.phi = Dm.phi;
   const uint64_t rows = uint64_t(Dm.U) * Dm.N;
-  CUtensorMap tq, tdo, tw, th;
+  CUtensorMap tq, tdo, tw, th, tos, tol;
   auto go = [&](auto kern, int bytes, auto dd) {
     constexpr int D = decltype(dd)::value;
     make_tmap_bf16(&tq, q, D, rows, 1, D, 0, 64);
     make_tmap_bf16(&tdo, d_out, D, rows, 1, D, 0, 64);
     make_tmap_bf16(&tw, w, D, uint64_t(Dm.H) * D, 1, D, 0, D);
     make_tmap_bf16(&th, s.Hb, D, uint64_t(Dm.U) * Dm.Tm * D, 1, D, 0, D);
+    make_tmap_bf16(&tos, o_s, D, rows, 1, D, 0, 64);
+    make_tmap_bf16(&tol, o_l, D, rows, 1, D, 0, 64);
     SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    kern<<<dim3(Dm.Tm, unsigned(Dm.U)), 192, bytes, st>>>(tq, tdo, tw, th, p);
+    kern<<<dim3(Dm.Tm, unsigned(Dm.U)), 192, bytes, st>>>(tq, tdo, tw, th, tos, tol, p);
     check_launch("k_bwd_lin", st);
   };
   if (Dm.d == 128)
