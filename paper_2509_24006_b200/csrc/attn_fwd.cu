@@ -18,22 +18,34 @@
 
 namespace slab {
 
+static __device__ long long g_fwd_ts[128];  // -DSLAB_TIMELINE: timeline of one CTA
+
 namespace {
+
+__device__ __forceinline__ void fts(bool on, int slot) {
+#ifdef SLAB_TIMELINE
+  if (on) g_fwd_ts[slot] = clock64();
+#else
+  (void)on;
+  (void)slot;
+#endif
+}
 
 template <int D>
 struct FwdLayout {
   static constexpr int kQ = 64 * D * 2;       // Q tile, K-major SW128 (D/64 chunks of 8 KB)
-  static constexpr int kTile = 64 * D * 2;    // one K or V tile
-  static constexpr int kStage = 2 * kTile;    // K + V; also holds H_i or W (D*D*2 bytes)
-  static constexpr int kStages = 2;  // 2 CTAs / SM share the tensor core
+  static constexpr int kTile = 64 * D * 2;    // one K or V tile == one 64-column chunk of H / W
+  static constexpr int kSlots = 2;            // per ring; 2 CTAs / SM share the tensor core
   static constexpr int kPX = 16384;           // 2 P buffers (8 KB) == phi(Q) / O^l tile
   static constexpr int oQ = 0;
-  static constexpr int oRing = oQ + kQ;
-  static constexpr int oPX = oRing + kStages * kStage;
+  static constexpr int oK = oQ + kQ;          // K ring; W chunks after the loop
+  static constexpr int oV = oK + kSlots * kTile;  // V ring; H chunks before the loop
+  static constexpr int oPX = oV + kSlots * kTile;
   static constexpr int oBar = oPX + kPX;
-  static constexpr int kBytes = oBar + 256 + 1024;
-  static_assert(kBytes <= 232448, "smem");
-  static_assert(D * D * 2 <= kStage, "H/W must fit a ring stage");
+  static constexpr int oZ = oBar + 256;       // Z_i (f32 [D])
+  static constexpr int kBytes = oZ + D * 4 + 1024;
+  static_assert(kBytes <= 232448 / 2, "smem: 2 CTAs / SM");
+  static_assert(D / 64 <= kSlots, "H/W chunks must fit a ring");
   static_assert(64 * D * 2 <= kPX, "X tile must fit the P region");
 };
 
@@ -65,16 +77,17 @@ __global__ void __launch_bounds__(192, 2)
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmH,
                const __grid_constant__ CUtensorMap tmW, FwdParams p) {
   using L = FwdLayout<D>;
+  constexpr int RS = L::kSlots;
+  constexpr int NC = D / 64;  // 64-column chunks of H / W
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = smem + L::oQ;
-  uint8_t* sRing = smem + L::oRing;
+  uint8_t* sK = smem + L::oK;
+  uint8_t* sV = smem + L::oV;
   uint8_t* sPX = smem + L::oPX;
+  float* sZ = reinterpret_cast<float*>(smem + L::oZ);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::oBar);
   uint64_t* q_full = bars + 0;
-  constexpr int RS = L::kStages;
-  uint64_t* ring_full = bars + 16;        // [RS]
-  uint64_t* ring_empty = bars + 16 + RS;  // [RS]
   uint64_t* s_full = bars + 5;      // [2]
   uint64_t* p_full = bars + 7;      // [2]
   uint64_t* pv_done = bars + 9;     // [2]
@@ -82,7 +95,11 @@ __global__ void __launch_bounds__(192, 2)
   uint64_t* x_full = bars + 12;
   uint64_t* o_ready = bars + 13;
   uint64_t* proj_done = bars + 14;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + 2 * RS);
+  uint64_t* k_full = bars + 16;     // [RS]
+  uint64_t* k_empty = bars + 18;    // [RS]
+  uint64_t* v_full = bars + 20;     // [RS]
+  uint64_t* v_empty = bars + 22;    // [RS]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 24);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x;
@@ -93,6 +110,8 @@ __global__ void __launch_bounds__(192, 2)
   const bool has_lin = p.marg_cnt[urow] > 0;
   const bool has_w = p.has_w != 0;
   const int row0 = int(u * p.N) + i * 64;  // row in the [U*N, D] view
+  const bool dbg = blockIdx.x == 100 && blockIdx.y == 6;
+  fts(dbg && threadIdx.x == 0, 127);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -101,8 +120,10 @@ __global__ void __launch_bounds__(192, 2)
       tc::tma_prefetch(&tmV);
       tc::mbar_init(q_full, 1);
       for (int s = 0; s < RS; ++s) {
-        tc::mbar_init(ring_full + s, 1);
-        tc::mbar_init(ring_empty + s, 1);
+        tc::mbar_init(k_full + s, 1);
+        tc::mbar_init(k_empty + s, 1);
+        tc::mbar_init(v_full + s, 1);
+        tc::mbar_init(v_empty + s, 1);
       }
       for (int s = 0; s < 2; ++s) {
         tc::mbar_init(s_full + s, 1);
@@ -127,217 +148,242 @@ __global__ void __launch_bounds__(192, 2)
 
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer
+    // Two rings: K slots are released by S(t), V slots by PV(t), so K(t+2) is in flight while
+    // PV(t) still waits for P(t).  H_i's chunks go through the V ring (needed before V(0)),
+    // W's chunks through the K ring (needed after the last S).
     if (lane == 0) {
       tc::mbar_expect_tx(q_full, L::kQ);
 #pragma unroll
-      for (int c = 0; c < D / 64; ++c) tc::tma_load_3d(sQ + c * 8192, &tmQ, q_full, 64 * c, row0, 0);
-      int item = 0;
-      auto acquire = [&](int bytes) -> uint8_t* {
-        const int s = item % RS;
-        tc::mbar_wait(ring_empty + s, ((item / RS) & 1) ^ 1);
-        tc::mbar_expect_tx(ring_full + s, bytes);
-        return sRing + s * L::kStage;
+      for (int c = 0; c < NC; ++c) tc::tma_load_3d(sQ + c * 8192, &tmQ, q_full, 64 * c, row0, 0);
+      int kit = 0, vit = 0;
+      auto take = [&](uint64_t* full, uint64_t* empty, uint8_t* base, int& it, int bytes) -> uint8_t* {
+        const int s = it % RS;
+        tc::mbar_wait(empty + s, ((it / RS) & 1) ^ 1);
+        tc::mbar_expect_tx(full + s, bytes);
+        return base + s * L::kTile;
       };
-      if (has_lin) {
-        uint8_t* dst = acquire(D * D * 2);
+      auto load_kv = [&](const CUtensorMap* tm, uint64_t* full, uint64_t* empty, uint8_t* base, int& it, int t) {
+        const int kv_row = int(u * p.N) + list[t] * 64;
+        uint8_t* dst = take(full, empty, base, it, L::kTile);
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c)
-          tc::tma_load_3d(dst + c * D * 128, &tmH, ring_full + (item % RS), 64 * c, int(urow * D), 0);
-        ++item;
+        for (int c = 0; c < NC; ++c) tc::tma_load_3d(dst + c * 8192, tm, full + (it % RS), 64 * c, kv_row, 0);
+        ++it;
+      };
+      if (cnt > 0) load_kv(&tmK, k_full, k_empty, sK, kit, 0);
+      if (has_lin) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+          uint8_t* dst = take(v_full, v_empty, sV, vit, L::kTile);
+          tc::tma_load_3d(dst, &tmH, v_full + (vit % RS), 64 * c, int(urow * D), 0);
+          ++vit;
+        }
       }
       for (int t = 0; t < cnt; ++t) {
-        const int kv_row = int(u * p.N) + list[t] * 64;
-        uint8_t* dst = acquire(2 * L::kTile);
-#pragma unroll
-        for (int c = 0; c < D / 64; ++c) {
-          tc::tma_load_3d(dst + c * 8192, &tmK, ring_full + (item % RS), 64 * c, kv_row, 0);
-          tc::tma_load_3d(dst + L::kTile + c * 8192, &tmV, ring_full + (item % RS), 64 * c, kv_row, 0);
-        }
-        ++item;
+        fts(dbg && t < 24, t);
+        if (t + 1 < cnt) load_kv(&tmK, k_full, k_empty, sK, kit, t + 1);
+        load_kv(&tmV, v_full, v_empty, sV, vit, t);
       }
       if (has_w) {
-        uint8_t* dst = acquire(D * D * 2);
         const int h = int(u % p.H);
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c)
-          tc::tma_load_3d(dst + c * D * 128, &tmW, ring_full + (item % RS), 64 * c, h * D, 0);
-        ++item;
+        for (int c = 0; c < NC; ++c) {
+          uint8_t* dst = take(k_full, k_empty, sK, kit, L::kTile);
+          tc::tma_load_3d(dst, &tmW, k_full + (kit % RS), 64 * c, h * D, 0);
+          ++kit;
+        }
       }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer
-    const uint32_t sQa = tc::smem_u32(sQ), sRa = tc::smem_u32(sRing), sPa = tc::smem_u32(sPX);
+    const uint32_t sQa = tc::smem_u32(sQ), sKa = tc::smem_u32(sK), sVa = tc::smem_u32(sV);
+    const uint32_t sPa = tc::smem_u32(sPX);
     constexpr uint32_t id_s = tc::idesc_bf16(64, 64, false, false);
     constexpr uint32_t id_o = tc::idesc_bf16(64, D, false, true);
-    int item = 0;
-    auto wait_item = [&]() -> uint32_t {
-      const int s = item % RS;
-      tc::mbar_wait(ring_full + s, (item / RS) & 1);
+    constexpr uint32_t id_c = tc::idesc_bf16(64, 64, false, true);  // X . (one 64-col chunk)
+    int kit = 0, vit = 0;
+    auto wait_slot = [&](uint64_t* full, uint32_t base, int it) -> uint32_t {
+      const int s = it % RS;
+      tc::mbar_wait(full + s, (it / RS) & 1);
       tc::tc_fence_after();
-      return sRa + s * L::kStage;
+      return base + s * L::kTile;
     };
-    tc::mbar_wait(q_full, 0);
-    if (has_lin) {  // O-region <- phi(Q_i) H_i
-      tc::mbar_wait(x_full, 0);
-      const uint32_t sh = wait_item();
-      if (lane == 0) {
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          tc::mma_bf16(tO, tc::desc_kmajor(sPa + (kk >> 2) * 8192 + (kk & 3) * 32),
-                       tc::desc_mnmajor(sh + kk * 2048, D * 128), id_o, kk > 0);
-        tc::mma_commit(ring_empty + (item % RS));
-        tc::mma_commit(lin_done);
-      }
-      __syncwarp();
-      ++item;
-    }
-    const int item0 = item;
-    auto issue_pv = [&](int j) {
-      tc::mbar_wait(p_full + (j & 1), (j >> 1) & 1);
-      tc::tc_fence_after();
-      const int it = item0 + j;
-      const uint32_t sv = sRa + (it % RS) * L::kStage + L::kTile;
-      if (lane == 0) {
-        const uint32_t sp = sPa + (j & 1) * 8192;
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          tc::mma_bf16(tO, tc::desc_kmajor(sp + kk * 32), tc::desc_mnmajor(sv + kk * 2048, 8192), id_o,
-                       (j | kk) != 0);
-        tc::mma_commit(ring_empty + (it % RS));
-        tc::mma_commit(pv_done + (j & 1));
-      }
-      __syncwarp();
-    };
-    for (int t = 0; t < cnt; ++t) {
-      const uint32_t sk = wait_item();
+    auto issue_s = [&](int t) {
+      const uint32_t sk = wait_slot(k_full, sKa, kit);
+      fts(dbg && lane == 0 && t < 24, 24 + t);
       if (lane == 0) {
         const uint32_t ts = tS0 + 64 * (t & 1);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
           tc::mma_bf16(ts, tc::desc_kmajor(sQa + (kk >> 2) * 8192 + (kk & 3) * 32),
                        tc::desc_kmajor(sk + (kk >> 2) * 8192 + (kk & 3) * 32), id_s, kk > 0);
+        tc::mma_commit(k_empty + (kit % RS));
         tc::mma_commit(s_full + (t & 1));
       }
       __syncwarp();
-      ++item;
-      if (t > 0) issue_pv(t - 1);
+      ++kit;
+    };
+    // tO[:, 64c:64c+64] (+)= X . chunk_c for the NC chunks at ring items it0.. (H_i or W)
+    auto issue_chunks = [&](uint64_t* full, uint64_t* empty, uint32_t base, int& it, bool acc) {
+      uint32_t sc[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) sc[c] = wait_slot(full, base, it + c);
+      if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+#pragma unroll
+          for (int kk = 0; kk < D / 16; ++kk)
+            tc::mma_bf16(tO + 64 * c, tc::desc_kmajor(sPa + (kk >> 2) * 8192 + (kk & 3) * 32),
+                         tc::desc_mnmajor(sc[c] + kk * 2048, 8192), id_c, acc || kk > 0);
+          tc::mma_commit(empty + ((it + c) % RS));
+        }
+      }
+      it += NC;
+    };
+    auto issue_pv = [&](int j) {
+      tc::mbar_wait(p_full + (j & 1), (j >> 1) & 1);
+      const uint32_t sv = wait_slot(v_full, sVa, vit);
+      if (lane == 0) {
+        const uint32_t sp = sPa + (j & 1) * 8192;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          tc::mma_bf16(tO, tc::desc_kmajor(sp + kk * 32), tc::desc_mnmajor(sv + kk * 2048, 8192), id_o,
+                       (j | kk) != 0);
+        tc::mma_commit(v_empty + (vit % RS));
+        tc::mma_commit(pv_done + (j & 1));
+      }
+      __syncwarp();
+      ++vit;
+    };
+    tc::mbar_wait(q_full, 0);
+    if (cnt > 0) issue_s(0);  // S(0) runs while the softmax warps build phi(Q_i)
+    if (has_lin) {            // O-region <- phi(Q_i) H_i
+      tc::mbar_wait(x_full, 0);
+      fts(dbg && lane == 0, 102);
+      issue_chunks(v_full, v_empty, sVa, vit, false);
+      if (lane == 0) tc::mma_commit(lin_done);
+      __syncwarp();
+    }
+    for (int t = 1; t < cnt; ++t) {
+      issue_s(t);
+      issue_pv(t - 1);
     }
     if (cnt > 0) issue_pv(cnt - 1);
     if (has_w) {  // O-region (normalised O^s) += O^l W
-      const uint32_t sw = wait_item();
       tc::mbar_wait(o_ready, 0);
       tc::tc_fence_after();
-      if (lane == 0) {
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          tc::mma_bf16(tO, tc::desc_kmajor(sPa + (kk >> 2) * 8192 + (kk & 3) * 32),
-                       tc::desc_mnmajor(sw + kk * 2048, D * 128), id_o, 1);
-        tc::mma_commit(ring_empty + (item % RS));
-        tc::mma_commit(proj_done);
-      }
+      issue_chunks(k_full, k_empty, sKa, kit, true);
+      if (lane == 0) tc::mma_commit(proj_done);
       __syncwarp();
-      ++item;
     }
   } else {
     // ------------------------------------------------------------------ softmax / epilogue
+    // Every lane works: row r = 16*q4 + (lane & 15) (the M=64 TMEM layout), and lanes 0-15 /
+    // 16-31 take the two column halves through the 16x32bx2 TMEM shape; row reductions need
+    // one shfl_xor(16).
     const int q4 = warp & 3;
-    const int r = 16 * q4 + lane;           // row within the block (valid for lane < 16)
-    const bool valid = lane < 16;
+    const int r = 16 * q4 + (lane & 15);
+    const int hh = lane >> 4;
     const uint32_t lane_base = uint32_t(32 * q4) << 16;
     const long long grow = (long long)row0 + r;  // global row in [U*N, D]
+    constexpr int DH = D / 2;                    // columns per half row
+    auto dcol = [&](int c0) { return hh * DH + c0; };  // first column of chunk c0 of my half
+    if (has_lin) {  // Z_i -> smem (one coalesced row instead of per-thread dependent loads)
+      const int tid = threadIdx.x - 64;
+      if (tid < D) sZ[tid] = p.Z[urow * D + tid];
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+    }
+    uint32_t olp[DH / 2];  // my half row of O^l (bf16x2), kept for the projection
     tc::mbar_wait(q_full, 0);
+    fts(dbg && threadIdx.x == 64, 96);
 
-    // ---- marginal branch: phi(Q_i) into X, den = phi(q) . Z_i, then O^l
+    // ---- marginal branch: phi(Q_i) into X, den = phi(q) . Z_i, then O^l = phi(q) H_i / den
     float den = 0.f;
     if (has_lin) {
-      const float* Zi = p.Z + urow * D;
-      float x[D];
+      // my half row of Q_i -> f32 registers, then phi in place (feature_map.cpp:10-20)
+      float x[DH];
 #pragma unroll
-      for (int c = 0; c < D / 8; ++c) {
-        const uint4 v = *reinterpret_cast<const uint4*>(sQ + (c >> 3) * 8192 + tc::sw128_off(r & 63, c & 7));
+      for (int c = 0; c < DH; c += 8) {
+        const int col = dcol(c);
+        const uint4 v = *reinterpret_cast<const uint4*>(sQ + (col >> 6) * 8192 + tc::sw128_off(r, (col >> 3) & 7));
         const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const float2 f = __bfloat1622float2(h2[e]);
-          x[8 * c + 2 * e] = f.x;
-          x[8 * c + 2 * e + 1] = f.y;
+          x[c + 2 * e] = f.x;
+          x[c + 2 * e + 1] = f.y;
         }
       }
-      if (p.phi == 2) {  // per-row softmax over d (feature_map.cpp:10-20)
+      if (p.phi == 2) {  // per-row softmax over d: each exp computed once
         float mx = -INFINITY;
 #pragma unroll
-        for (int a = 0; a < D; ++a) mx = fmaxf(mx, x[a]);
-        float sum = 0.f;
+        for (int e = 0; e < DH; ++e) mx = fmaxf(mx, x[e]);
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+        float se = 0.f;
 #pragma unroll
-        for (int a = 0; a < D; ++a) {
-          x[a] = __expf(x[a] - mx);
-          sum += x[a];
+        for (int e = 0; e < DH; ++e) {
+          x[e] = __expf(x[e] - mx);
+          se += x[e];
         }
-        const float inv = 1.f / sum;
+        se += __shfl_xor_sync(0xffffffffu, se, 16);
+        const float inv = 1.f / se;
 #pragma unroll
-        for (int a = 0; a < D; ++a) x[a] *= inv;
+        for (int e = 0; e < DH; ++e) x[e] *= inv;
       } else {
 #pragma unroll
-        for (int a = 0; a < D; ++a) x[a] = phi_elem(p.phi, x[a]);
+        for (int e = 0; e < DH; ++e) x[e] = phi_elem(p.phi, x[e]);
       }
 #pragma unroll
-      for (int a = 0; a < D; ++a) den = fmaf(x[a], __ldg(Zi + a), den);
-      if (valid) {
+      for (int c = 0; c < DH; c += 8) {
+        const int col = dcol(c);
 #pragma unroll
-        for (int c = 0; c < D / 8; ++c) {
-          uint4 v;
-          v.x = tc::pack_bf16(x[8 * c + 0], x[8 * c + 1]);
-          v.y = tc::pack_bf16(x[8 * c + 2], x[8 * c + 3]);
-          v.z = tc::pack_bf16(x[8 * c + 4], x[8 * c + 5]);
-          v.w = tc::pack_bf16(x[8 * c + 6], x[8 * c + 7]);
-          *reinterpret_cast<uint4*>(sPX + (c >> 3) * 8192 + tc::sw128_off(r, c & 7)) = v;
-        }
+        for (int e = 0; e < 8; ++e) den = fmaf(x[c + e], sZ[col + e], den);
+        *reinterpret_cast<uint4*>(sPX + (col >> 6) * 8192 + tc::sw128_off(r, (col >> 3) & 7)) =
+            make_uint4(tc::pack_bf16(x[c], x[c + 1]), tc::pack_bf16(x[c + 2], x[c + 3]),
+                       tc::pack_bf16(x[c + 4], x[c + 5]), tc::pack_bf16(x[c + 6], x[c + 7]));
       }
+      den += __shfl_xor_sync(0xffffffffu, den, 16);
       tc::fence_proxy_async();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(x_full);
+      fts(dbg && threadIdx.x == 64, 97);
       tc::mbar_wait(lin_done, 0);
       tc::tc_fence_after();
+      fts(dbg && threadIdx.x == 64, 98);
       const float inv_den = den != 0.f ? 1.f / den : 0.f;  // den == 0 -> zero row (forward.cpp:136)
-#pragma unroll 1
-      for (int c0 = 0; c0 < D; c0 += 32) {
+#pragma unroll
+      for (int c0 = 0; c0 < DH; c0 += 32) {
         uint32_t a[32];
-        tc::tmem_ld32(tO + lane_base + c0, a);
+        tc::tmem_ld32_x2<DH>(tO + lane_base + c0, a);
         tc::tmem_ld_wait();
-        if (valid) {
 #pragma unroll
-          for (int e = 0; e < 32; e += 8) {
-            uint4 v;
-            v.x = tc::pack_bf16(__uint_as_float(a[e]) * inv_den, __uint_as_float(a[e + 1]) * inv_den);
-            v.y = tc::pack_bf16(__uint_as_float(a[e + 2]) * inv_den, __uint_as_float(a[e + 3]) * inv_den);
-            v.z = tc::pack_bf16(__uint_as_float(a[e + 4]) * inv_den, __uint_as_float(a[e + 5]) * inv_den);
-            v.w = tc::pack_bf16(__uint_as_float(a[e + 6]) * inv_den, __uint_as_float(a[e + 7]) * inv_den);
-            *reinterpret_cast<uint4*>(p.o_l + grow * D + c0 + e) = v;
-          }
-        }
+        for (int e = 0; e < 32; e += 2)
+          olp[(c0 + e) >> 1] = tc::pack_bf16(__uint_as_float(a[e]) * inv_den, __uint_as_float(a[e + 1]) * inv_den);
       }
-    } else if (valid) {
+    } else {
 #pragma unroll
-      for (int c = 0; c < D; c += 8)
-        *reinterpret_cast<uint4*>(p.o_l + grow * D + c) = make_uint4(0, 0, 0, 0);
+      for (int e = 0; e < DH / 2; ++e) olp[e] = 0u;
     }
+#pragma unroll
+    for (int c = 0; c < DH; c += 8)
+      *reinterpret_cast<uint4*>(p.o_l + grow * D + dcol(c)) =
+          make_uint4(olp[c >> 1], olp[(c >> 1) + 1], olp[(c >> 1) + 2], olp[(c >> 1) + 3]);
 
+    fts(dbg && threadIdx.x == 64, 99);
     // ---- critical branch: online softmax over the ascending critical list
     float m_used = -INFINITY, l = 0.f;
     for (int t = 0; t < cnt; ++t) {
       tc::mbar_wait(s_full + (t & 1), (t >> 1) & 1);
       tc::tc_fence_after();
-      uint32_t sa[32], sb[32];
-      const uint32_t ts = tS0 + 64 * (t & 1) + lane_base;
-      tc::tmem_ld32(ts, sa);
-      tc::tmem_ld32(ts + 32, sb);
+      fts(dbg && threadIdx.x == 64 && t < 24, 48 + t);
+      uint32_t sa[32];
+      tc::tmem_ld32_x2<32>(tS0 + 64 * (t & 1) + lane_base, sa);  // my 32 of the 64 scores
       tc::tmem_ld_wait();
       float mx = -INFINITY;
 #pragma unroll
-      for (int e = 0; e < 32; ++e) mx = fmaxf(mx, fmaxf(__uint_as_float(sa[e]), __uint_as_float(sb[e])));
-      mx *= p.scale_log2;
+      for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sa[e]));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16)) * p.scale_log2;
       const float m_new = fmaxf(m_used, mx);
-      const bool need = valid && t > 0 && m_new > m_used + 8.f;
+      const bool need = t > 0 && m_new > m_used + 8.f;
       if (t == 0) m_used = m_new;
       if (__any_sync(0xffffffffu, need)) {  // rescale O and l (all previous PVs must be done)
         tc::mbar_wait(pv_done + ((t - 1) & 1), ((t - 1) >> 1) & 1);
@@ -348,20 +394,20 @@ __global__ void __launch_bounds__(192, 2)
           m_used = m_new;
         }
 #pragma unroll 1
-        for (int c0 = 0; c0 < D; c0 += 32) {
+        for (int c0 = 0; c0 < DH; c0 += 32) {
           uint32_t o[32];
-          tc::tmem_ld32(tO + lane_base + c0, o);
+          tc::tmem_ld32_x2<DH>(tO + lane_base + c0, o);
           tc::tmem_ld_wait();
 #pragma unroll
           for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * alpha);
-          tc::tmem_st32(tO + lane_base + c0, o);
+          tc::tmem_st32_x2<DH>(tO + lane_base + c0, o);
         }
         tc::tmem_st_wait();
       }
       if (t >= 2) tc::mbar_wait(pv_done + (t & 1), ((t - 2) >> 1) & 1);  // P buffer free
       const float sc = p.scale_log2;
       float ps = 0.f;
-      uint32_t pk[32];
+      uint32_t pk[16];
 #pragma unroll
       for (int e = 0; e < 32; e += 2) {
         const float p0 = ex2(__uint_as_float(sa[e]) * sc - m_used);
@@ -369,38 +415,32 @@ __global__ void __launch_bounds__(192, 2)
         ps += p0 + p1;
         pk[e >> 1] = tc::pack_bf16(p0, p1);
       }
+      l += ps + __shfl_xor_sync(0xffffffffu, ps, 16);
+      uint8_t* prow = sPX + (t & 1) * 8192;
 #pragma unroll
-      for (int e = 0; e < 32; e += 2) {
-        const float p0 = ex2(__uint_as_float(sb[e]) * sc - m_used);
-        const float p1 = ex2(__uint_as_float(sb[e + 1]) * sc - m_used);
-        ps += p0 + p1;
-        pk[16 + (e >> 1)] = tc::pack_bf16(p0, p1);
-      }
-      l += ps;
-      if (valid) {
-        uint8_t* prow = sPX + (t & 1) * 8192;
-#pragma unroll
-        for (int c = 0; c < 8; ++c)
-          *reinterpret_cast<uint4*>(prow + tc::sw128_off(r, c)) =
-              make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-      }
+      for (int c = 0; c < 4; ++c)
+        *reinterpret_cast<uint4*>(prow + tc::sw128_off(r, 4 * hh + c)) =
+            make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
       tc::fence_proxy_async();
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(p_full + (t & 1));
+      fts(dbg && threadIdx.x == 64 && t < 24, 72 + t);
     }
 
+    fts(dbg && threadIdx.x == 64, 100);
     // ---- finalize O^s, lse (forward.cpp:68-78); stage O^s / O^l for the projection
     if (cnt > 0) {
       tc::mbar_wait(pv_done + ((cnt - 1) & 1), ((cnt - 1) >> 1) & 1);
       tc::tc_fence_after();
     }
+    fts(dbg && threadIdx.x == 64, 103);
     const float inv_l = l > 0.f ? 1.f / l : 0.f;
 #pragma unroll 1
-    for (int c0 = 0; c0 < D; c0 += 32) {
+    for (int c0 = 0; c0 < DH; c0 += 32) {
       uint32_t o[32];
       if (cnt > 0) {
-        tc::tmem_ld32(tO + lane_base + c0, o);
+        tc::tmem_ld32_x2<DH>(tO + lane_base + c0, o);
         tc::tmem_ld_wait();
       } else {
 #pragma unroll
@@ -408,7 +448,40 @@ __global__ void __launch_bounds__(192, 2)
       }
 #pragma unroll
       for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * inv_l);
-      if (valid) {
+#pragma unroll
+      for (int e = 0; e < 32; e += 8) {
+        uint4 v;
+        v.x = tc::pack_bf16(__uint_as_float(o[e]), __uint_as_float(o[e + 1]));
+        v.y = tc::pack_bf16(__uint_as_float(o[e + 2]), __uint_as_float(o[e + 3]));
+        v.z = tc::pack_bf16(__uint_as_float(o[e + 4]), __uint_as_float(o[e + 5]));
+        v.w = tc::pack_bf16(__uint_as_float(o[e + 6]), __uint_as_float(o[e + 7]));
+        *reinterpret_cast<uint4*>(p.o_s + grow * D + dcol(c0) + e) = v;
+      }
+      if (has_w) tc::tmem_st32_x2<DH>(tO + lane_base + c0, o);
+    }
+    if (hh == 0) p.lse[grow] = l > 0.f ? (m_used + __log2f(l)) * 0.69314718055994531f : kLseSentinel;
+    if (has_w) {
+      tc::tmem_st_wait();
+      // X <- O^l (bf16), the A operand of O^l W: my half row, from registers
+#pragma unroll
+      for (int c = 0; c < DH; c += 8) {
+        const int col = dcol(c);
+        *reinterpret_cast<uint4*>(sPX + (col >> 6) * 8192 + tc::sw128_off(r, (col >> 3) & 7)) =
+            make_uint4(olp[c >> 1], olp[(c >> 1) + 1], olp[(c >> 1) + 2], olp[(c >> 1) + 3]);
+      }
+      tc::fence_proxy_async();
+      tc::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(o_ready);
+      fts(dbg && threadIdx.x == 64, 104);
+      tc::mbar_wait(proj_done, 0);
+      tc::tc_fence_after();
+      fts(dbg && threadIdx.x == 64, 105);
+#pragma unroll 1
+      for (int c0 = 0; c0 < DH; c0 += 32) {
+        uint32_t o[32];
+        tc::tmem_ld32_x2<DH>(tO + lane_base + c0, o);
+        tc::tmem_ld_wait();
 #pragma unroll
         for (int e = 0; e < 32; e += 8) {
           uint4 v;
@@ -416,46 +489,12 @@ __global__ void __launch_bounds__(192, 2)
           v.y = tc::pack_bf16(__uint_as_float(o[e + 2]), __uint_as_float(o[e + 3]));
           v.z = tc::pack_bf16(__uint_as_float(o[e + 4]), __uint_as_float(o[e + 5]));
           v.w = tc::pack_bf16(__uint_as_float(o[e + 6]), __uint_as_float(o[e + 7]));
-          *reinterpret_cast<uint4*>(p.o_s + grow * D + c0 + e) = v;
-        }
-      }
-      if (has_w) tc::tmem_st32(tO + lane_base + c0, o);
-    }
-    if (valid) p.lse[grow] = l > 0.f ? (m_used + __log2f(l)) * 0.69314718055994531f : kLseSentinel;
-    if (has_w) {
-      tc::tmem_st_wait();
-      if (valid) {  // X <- O^l (bf16), the A operand of O^l W
-#pragma unroll
-        for (int c = 0; c < D / 8; ++c) {
-          const uint4 v = *reinterpret_cast<const uint4*>(p.o_l + grow * D + 8 * c);
-          *reinterpret_cast<uint4*>(sPX + (c >> 3) * 8192 + tc::sw128_off(r, c & 7)) = v;
-        }
-      }
-      tc::fence_proxy_async();
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(o_ready);
-      tc::mbar_wait(proj_done, 0);
-      tc::tc_fence_after();
-#pragma unroll 1
-      for (int c0 = 0; c0 < D; c0 += 32) {
-        uint32_t o[32];
-        tc::tmem_ld32(tO + lane_base + c0, o);
-        tc::tmem_ld_wait();
-        if (valid) {
-#pragma unroll
-          for (int e = 0; e < 32; e += 8) {
-            uint4 v;
-            v.x = tc::pack_bf16(__uint_as_float(o[e]), __uint_as_float(o[e + 1]));
-            v.y = tc::pack_bf16(__uint_as_float(o[e + 2]), __uint_as_float(o[e + 3]));
-            v.z = tc::pack_bf16(__uint_as_float(o[e + 4]), __uint_as_float(o[e + 5]));
-            v.w = tc::pack_bf16(__uint_as_float(o[e + 6]), __uint_as_float(o[e + 7]));
-            *reinterpret_cast<uint4*>(p.o + grow * D + c0 + e) = v;
-          }
+          *reinterpret_cast<uint4*>(p.o + grow * D + dcol(c0) + e) = v;
         }
       }
     }
   }
+  fts(dbg && threadIdx.x == 64, 101);
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<256>(tmem);
@@ -507,3 +546,7 @@ void launch_attn_fwd(const Dims& Dm, const void* q, const void* k, const void* v
 }
 
 }  // namespace slab
+
+extern "C" int sla_b200_diag_fwd_timeline(long long* host128) {
+  return cudaMemcpyFromSymbol(host128, slab::g_fwd_ts, 128 * sizeof(long long)) == cudaSuccess ? 0 : 1;
+}
