@@ -68,6 +68,8 @@ __global__ void __launch_bounds__(320, 1)
   const int cnt = p.ccol_cnt[ucol];
   const int np = (cnt + 1) >> 1;
   const int* list = p.ccol_idx + ucol * p.Tm;
+  const bool dbg = blockIdx.x == 100 && blockIdx.y == 6;
+  ts_mark(dbg && threadIdx.x == 0, 127);
   __shared__ int s_lin;
   if (threadIdx.x == 0) s_lin = 0;
   __syncthreads();
@@ -79,6 +81,7 @@ __global__ void __launch_bounds__(320, 1)
   }
   __syncthreads();
   const bool has_lin = s_lin != 0;
+  ts_mark(dbg && threadIdx.x == 0, 126);
   const int kv0 = int(u * p.N) + j * 64;
 
   if (warp == 0) {
@@ -110,20 +113,14 @@ __global__ void __launch_bounds__(320, 1)
   const uint32_t tDVT = tmem, tDKT = tmem + 64, tB0 = tmem + 128, tB1 = tmem + 256, tKPT = tmem + 384;
 
   if (warp == 0) {
+    // No L2 prefetch of the column's Q / dO tiles: prefetches queue in the TMA unit ahead of
+    // the ring loads, and a wave's columns share one unit's Q / dO, which stays L2-resident.
     if (lane == 0) {
       tc::mbar_expect_tx(kv_full, 2 * L::kT);
 #pragma unroll
       for (int c = 0; c < D / 64; ++c) {
         tc::tma_load_3d(sK + c * 8192, &tmK, kv_full, 64 * c, kv0, 0);
         tc::tma_load_3d(sV + c * 8192, &tmV, kv_full, 64 * c, kv0, 0);
-      }
-      for (int t = 0; t < cnt; ++t) {  // warm L2 with every Q / dO tile of this column
-        const int q_row = int(u * p.N) + list[t] * 64;
-#pragma unroll
-        for (int c = 0; c < D / 64; ++c) {
-          tc::tma_prefetch_3d(&tmQ, 64 * c, q_row, 0);
-          tc::tma_prefetch_3d(&tmDO, 64 * c, q_row, 0);
-        }
       }
       int item = 0;
       auto acquire = [&](int bytes) -> uint8_t* {
@@ -136,6 +133,7 @@ __global__ void __launch_bounds__(320, 1)
         const int r1 = int(u * p.N) + list[2 * pp] * 64;
         const int r2 = int(u * p.N) + list[min(2 * pp + 1, cnt - 1)] * 64;
         uint8_t* dst = acquire(2 * L::kP);
+        ts_mark(dbg && pp < 16, pp);
         uint64_t* fb = ring_full + (item % RS);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
@@ -173,11 +171,11 @@ __global__ void __launch_bounds__(320, 1)
     };
     tc::mbar_wait(kv_full, 0);
     tc::tc_fence_after();
+    ts_mark(dbg && lane == 0, 125);
     auto issue_acc = [&](int t) {  // dV^T += dO_pair^T P, dK^T += Q_pair^T dS  (M = D, K = 128)
-      tc::mbar_wait(pd_full + (t & 1), (t >> 1) & 1);
       tc::tc_fence_after();
       const uint32_t sq = aR + (t % RS) * L::kStage;
-      if (lane == 0) {
+      {
         const uint32_t sp = aPD + (t & 1) * 32768, sd = sp + 16384;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
@@ -189,25 +187,34 @@ __global__ void __launch_bounds__(320, 1)
         tc::mma_commit(ring_empty + (t % RS));
         tc::mma_commit(pd_empty + (t & 1));
       }
-      __syncwarp();
     };
-    for (int t = 0; t < np; ++t) {
-      const uint32_t sq = wait_item();
-      if (lane == 0) {
-        const uint32_t tb = (t & 1) ? tB1 : tB0;
+    // The tensor pipe executes in issue order, so S/dP(t+1) and acc(t) are issued in whichever
+    // order their inputs become ready: acc(t) releases a ring stage, S/dP(t+1) feeds the compute
+    // warps.  S/dP(t) reuses TMEM buffer t&1, free once acc(t-2) was issued (pd_full(t-2) seen).
+    if (lane == 0) {
+      int ts = 0, ta = 0;
+      while (ta < np) {
+        if (ts < np && ts <= ta + 1 && tc::mbar_test(ring_full + ts % RS, (ts / RS) & 1)) {
+          tc::tc_fence_after();
+          ts_mark(dbg && ts < 16, 16 + ts);
+          const uint32_t sq = aR + (ts % RS) * L::kStage;
+          const uint32_t tb = (ts & 1) ? tB1 : tB0;
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          tc::mma_bf16(tb, kdesc(sq, kk, 128), kdesc(aK, kk, 64), id_s, kk > 0);                // S
-          tc::mma_bf16(tb + 64, kdesc(sq + L::kP, kk, 128), kdesc(aV, kk, 64), id_s, kk > 0);   // dP
+          for (int kk = 0; kk < D / 16; ++kk) {
+            tc::mma_bf16(tb, kdesc(sq, kk, 128), kdesc(aK, kk, 64), id_s, kk > 0);               // S
+            tc::mma_bf16(tb + 64, kdesc(sq + L::kP, kk, 128), kdesc(aV, kk, 64), id_s, kk > 0);  // dP
+          }
+          tc::mma_commit(sdp_full + (ts & 1));
+          ++ts;
         }
-        tc::mma_commit(sdp_full + (t & 1));
+        if (ta < ts && tc::mbar_test(pd_full + (ta & 1), (ta >> 1) & 1)) {
+          issue_acc(ta);
+          ++ta;
+        }
       }
-      __syncwarp();
-      ++item;
-      if (t > 0) issue_acc(t - 1);
+      tc::mma_commit(acc_done);
     }
-    if (np > 0) issue_acc(np - 1);
-    if (lane == 0) tc::mma_commit(acc_done);
+    item = np;
     __syncwarp();
     if (has_lin) {
       const uint32_t sh = wait_item();
@@ -244,6 +251,7 @@ __global__ void __launch_bounds__(320, 1)
       const float dsr = p.Ds[qrow];
       tc::mbar_wait(sdp_full + (t & 1), (t >> 1) & 1);
       tc::tc_fence_after();
+      ts_mark(dbg && threadIdx.x == 64 && t < 16, 32 + t);
       const uint32_t tb = ((t & 1) ? tB1 : tB0) + lane_base + 32 * grp;
       uint32_t pp[16], dd[16];
       {
@@ -275,6 +283,7 @@ __global__ void __launch_bounds__(320, 1)
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(pd_full + (t & 1));
+      ts_mark(dbg && threadIdx.x == 64 && t < 16, 48 + t);
     }
     // ---- phi(K_j) rows (4 threads per key row, D/4 columns each): statistics + the bf16 tile
     tc::mbar_wait(kv_full, 0);  // K_j must have landed even when no critical row came by
@@ -305,6 +314,7 @@ __global__ void __launch_bounds__(320, 1)
     }
     auto phi_of = [&](float x) { return p.phi == 2 ? __expf(x - mx) * inv : phi_elem(p.phi, x); };
     tc::mbar_wait(acc_done, 0);  // the P / dS buffers are free
+    ts_mark(dbg && threadIdx.x == 64, 120);
     if (has_lin) {
 #pragma unroll
       for (int cc = 0; cc < D / 4; cc += 8) {
@@ -318,10 +328,12 @@ __global__ void __launch_bounds__(320, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(kf_ready);
     }
+    ts_mark(dbg && threadIdx.x == 64, 121);
     tc::mbar_wait(all_done, 0);
     tc::tc_fence_after();
+    ts_mark(dbg && threadIdx.x == 64, 122);
     // ---- transpose dK^T, dV^T, dK^phi^T (lane = column a) into smem [key row][a]
-    constexpr int TP = D + 4;
+    constexpr int TP = D + 1;  // with the chunk rotation below: conflict-free row-wise reads
     float* tk = reinterpret_cast<float*>(sRing);
     float* tv = tk + 64 * TP;
     float* tkp = tv + 64 * TP;
@@ -344,11 +356,15 @@ __global__ void __launch_bounds__(320, 1)
       }
     }
     named_sync(1, 256);
+    ts_mark(dbg && threadIdx.x == 64, 123);
     // ---- dk_total = J_phi(k)^T (dK^phi + dZ_agg) + dK ; dv  (row-wise, 4 threads per row)
+    const int sub = tid & 3;
+    auto rot = [&](int cc) { return (cc + 8 * sub) & (D / 4 - 1); };  // chunk order per thread
     float dot = 0.f;
     if (p.phi == 2 && has_lin) {
 #pragma unroll
-      for (int cc = 0; cc < D / 4; cc += 8) {
+      for (int cc0 = 0; cc0 < D / 4; cc0 += 8) {
+        const int cc = rot(cc0);
         float f[8];
         unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, c0 + cc)), f);
 #pragma unroll
@@ -359,8 +375,8 @@ __global__ void __launch_bounds__(320, 1)
     }
     const long long grow = (long long)kv0 + c;
 #pragma unroll
-    for (int cc = 0; cc < D / 4; cc += 8) {
-      const int col = c0 + cc;
+    for (int cc0 = 0; cc0 < D / 4; cc0 += 8) {
+      const int col = c0 + rot(cc0);
       float f[8], o[8], w8[8];
       unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, col)), f);
 #pragma unroll
@@ -377,6 +393,7 @@ __global__ void __launch_bounds__(320, 1)
       *reinterpret_cast<uint4*>(p.dv + grow * D + col) = pack8(w8);
     }
   }
+  ts_mark(dbg && threadIdx.x == 64, 124);
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
@@ -427,3 +444,6 @@ void launch_bwd_cols(const Dims& Dm, const void* q, const void* k, const void* v
 
 }  // namespace slab
 
+extern "C" int sla_b200_diag_cols_timeline(long long* host128) {
+  return cudaMemcpyFromSymbol(host128, slab::g_bwd_ts, 128 * sizeof(long long)) == cudaSuccess ? 0 : 1;
+}
