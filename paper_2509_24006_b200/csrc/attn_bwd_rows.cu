@@ -353,6 +353,8 @@ __global__ void __launch_bounds__(320, 1)
   const int* list = p.crit_idx + urow * p.Tn;
   const int np = (cnt + 1) >> 1;
   const int row0 = int(u * p.N) + i * 64;
+  const bool dbg = blockIdx.x == 100 && blockIdx.y == 6;
+  ts_mark(dbg && threadIdx.x == 0, 127);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -395,6 +397,7 @@ __global__ void __launch_bounds__(320, 1)
         const int ks = t % L::KS, vs = t % L::VS;
         tc::mbar_wait(k_empty + ks, ((t / L::KS) & 1) ^ 1);
         tc::mbar_expect_tx(k_full + ks, L::kP);
+        ts_mark(dbg && t < 16, t);
         uint8_t* dk = sK + ks * L::kP;
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
@@ -420,41 +423,46 @@ __global__ void __launch_bounds__(320, 1)
       return tc::desc_kmajor(base + (kk >> 2) * rows * 128 + (kk & 3) * 32);
     };
     tc::mbar_wait(qdo_full, 0);
-    auto issue_dq = [&](int j) {  // dQ^T += [K_j1; K_j2]^T dS^T  (M = D, N = 64, K = 128)
-      tc::mbar_wait(ds_full, j & 1);
-      tc::tc_fence_after();
-      if (lane == 0) {
-        const uint32_t sk = aK + (j % L::KS) * L::kP;
+    // dQ^T += [K_j1; K_j2]^T dS^T  (M = D, N = 64, K = 128)
+    auto issue_dq = [&](int j) {
+      const uint32_t sk = aK + (j % L::KS) * L::kP;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          tc::mma_bf16(tDQT, tc::desc_mnmajor(sk + kk * 2048, 16384), tc::desc_mnmajor(aDS + kk * 2048, 16384),
-                       id_dqt, (j | kk) != 0);
-        tc::mma_commit(k_empty + (j % L::KS));
-        tc::mma_commit(ds_empty);
-      }
-      __syncwarp();
+      for (int kk = 0; kk < 8; ++kk)
+        tc::mma_bf16(tDQT, tc::desc_mnmajor(sk + kk * 2048, 16384), tc::desc_mnmajor(aDS + kk * 2048, 16384),
+                     id_dqt, (j | kk) != 0);
+      tc::mma_commit(k_empty + (j % L::KS));
+      tc::mma_commit(ds_empty);
     };
-    for (int t = 0; t < np; ++t) {
-      const int ks = t % L::KS, vs = t % L::VS;
-      tc::mbar_wait(k_full + ks, (t / L::KS) & 1);
-      tc::mbar_wait(v_full + vs, (t / L::VS) & 1);
-      tc::tc_fence_after();
-      if (lane == 0) {
-        const uint32_t tb = (t & 1) ? tB1 : tB0;
-        const uint32_t sk = aK + ks * L::kP, sv = aV + vs * L::kP;
+    // In-order tensor pipe: issue S^T/dP^T(t) and dQ(t-1) in whichever order their inputs
+    // arrive (dQ releases a K slot).  S/dP(t) reuses TMEM buffer t&1: free once dQ(t-2) issued.
+    if (lane == 0) {
+      int ts = 0, ta = 0;
+      while (ta < np) {
+        if (ts < np && ts <= ta + 1 && tc::mbar_test(k_full + ts % L::KS, (ts / L::KS) & 1) &&
+            tc::mbar_test(v_full + ts % L::VS, (ts / L::VS) & 1)) {
+          tc::tc_fence_after();
+          ts_mark(dbg && ts < 16, 16 + ts);
+          const int ks = ts % L::KS, vs = ts % L::VS;
+          const uint32_t tb = (ts & 1) ? tB1 : tB0;
+          const uint32_t sk = aK + ks * L::kP, sv = aV + vs * L::kP;
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          tc::mma_bf16(tb, kdesc(sk, kk, 128), kdesc(aQ, kk, 64), id_st, kk > 0);        // S^T
-          tc::mma_bf16(tb + 64, kdesc(sv, kk, 128), kdesc(aDO, kk, 64), id_st, kk > 0);  // dP^T
+          for (int kk = 0; kk < D / 16; ++kk) {
+            tc::mma_bf16(tb, kdesc(sk, kk, 128), kdesc(aQ, kk, 64), id_st, kk > 0);        // S^T
+            tc::mma_bf16(tb + 64, kdesc(sv, kk, 128), kdesc(aDO, kk, 64), id_st, kk > 0);  // dP^T
+          }
+          tc::mma_commit(sdp_full + (ts & 1));
+          tc::mma_commit(v_empty + vs);
+          ++ts;
         }
-        tc::mma_commit(sdp_full + (t & 1));
-        tc::mma_commit(v_empty + vs);
+        if (ta < ts && tc::mbar_test(ds_full, ta & 1)) {
+          tc::tc_fence_after();
+          ts_mark(dbg && ta < 16, 64 + ta);
+          issue_dq(ta);
+          ++ta;
+        }
       }
-      __syncwarp();
-      if (t > 0) issue_dq(t - 1);
+      tc::mma_commit(dq_done);
     }
-    if (np > 0) issue_dq(np - 1);
-    if (lane == 0) tc::mma_commit(dq_done);
     __syncwarp();
   } else {
     const int q4 = warp & 3;
@@ -469,6 +477,7 @@ __global__ void __launch_bounds__(320, 1)
     for (int t = 0; t < np; ++t) {
       tc::mbar_wait(sdp_full + (t & 1), (t >> 1) & 1);
       tc::tc_fence_after();
+      ts_mark(dbg && threadIdx.x == 64 && t < 16, 32 + t);
       const bool live = c < 64 || 2 * t + 1 < cnt;
       const uint32_t tb = ((t & 1) ? tB1 : tB0) + lane_base + 32 * grp;
       uint32_t pk[16];
@@ -496,6 +505,7 @@ __global__ void __launch_bounds__(320, 1)
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(ds_full);
+      ts_mark(dbg && threadIdx.x == 64 && t < 16, 48 + t);
     }
     // dq_total = J_phi(q)^T dQ^phi + dQ: transpose dQ^T through smem (the K ring is idle once
     // dq_done fired), then finish row-wise with 4 threads per query row.  For the softmax
@@ -503,7 +513,8 @@ __global__ void __launch_bounds__(320, 1)
     // the Jacobian reduces to phi(q) * dQ^phi.
     tc::mbar_wait(dq_done, 0);
     tc::tc_fence_after();
-    constexpr int TP = D + 4;
+    ts_mark(dbg && threadIdx.x == 64, 120);
+    constexpr int TP = D + 1;  // with the chunk rotation below: conflict-free row-wise reads
     float* tq = reinterpret_cast<float*>(sK);
     {
       const int acol = D == 128 ? 32 * q4 + lane : 16 * q4 + lane;
@@ -518,49 +529,57 @@ __global__ void __launch_bounds__(320, 1)
     }
     named_sync(1, 256);
     {
-      const int rq = tid >> 2, c0 = (tid & 3) * (D / 4);
-      float mx = 0.f, inv = 1.f;
-      if (p.phi == 2) {
-        mx = -INFINITY;
+      constexpr int DQ = D / 4;
+      const int rq = tid >> 2, sub = tid & 3, c0 = sub * DQ;
+      const long long grow = (long long)row0 + rq;
+      float x[DQ];
 #pragma unroll
-        for (int cc = 0; cc < D / 4; cc += 8) {
-          float x[8];
-          unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(rq, c0 + cc)), x);
+      for (int cc = 0; cc < DQ; cc += 8) {
+        float t8[8];
+        unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(rq, c0 + cc)), t8);
 #pragma unroll
-          for (int e = 0; e < 8; ++e) mx = fmaxf(mx, x[e]);
-        }
+        for (int e = 0; e < 8; ++e) x[cc + e] = t8[e];
+      }
+      if (p.phi == 2) {  // phi(q) in place, one exp per element
+        float mx = -INFINITY;
+#pragma unroll
+        for (int e = 0; e < DQ; ++e) mx = fmaxf(mx, x[e]);
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
         float se = 0.f;
 #pragma unroll
-        for (int cc = 0; cc < D / 4; cc += 8) {
-          float x[8];
-          unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(rq, c0 + cc)), x);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) se += __expf(x[e] - mx);
+        for (int e = 0; e < DQ; ++e) {
+          x[e] = __expf(x[e] - mx);
+          se += x[e];
         }
         se += __shfl_xor_sync(0xffffffffu, se, 1);
         se += __shfl_xor_sync(0xffffffffu, se, 2);
-        inv = 1.f / se;
-      }
-      const long long grow = (long long)row0 + rq;
+        const float inv = 1.f / se;
 #pragma unroll
-      for (int cc = 0; cc < D / 4; cc += 8) {
+        for (int e = 0; e < DQ; ++e) x[e] *= inv;
+      }
+#pragma unroll
+      for (int cc0 = 0; cc0 < DQ; cc0 += 8) {
+        const int cc = (cc0 + 8 * sub) & (DQ - 1);  // rotated chunk order (bank spread)
         const int col = c0 + cc;
-        float x[8], g[8], o[8];
-        unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(rq, col)), x);
+        float g[8], o[8];
         unpack8(*reinterpret_cast<const uint4*>(p.dqphi + grow * D + col), g);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
+          float xe = x[0];
+#pragma unroll
+          for (int k = 0; k < DQ; k += 8)  // x[cc + e] with cc dynamic: select among chunks
+            if (k == cc) xe = x[k + e];
           float jg;
-          if (p.phi == 2) jg = __expf(x[e] - mx) * inv * g[e];
-          else if (p.phi == 0) jg = x[e] >= 0.f ? g[e] : __expf(x[e]) * g[e];
-          else jg = x[e] > 0.f ? g[e] : 0.f;
+          if (p.phi == 2) jg = xe * g[e];
+          else if (p.phi == 0) jg = xe >= 0.f ? g[e] : __expf(xe) * g[e];
+          else jg = xe > 0.f ? g[e] : 0.f;
           o[e] = jg + tq[rq * TP + col + e];
         }
         *reinterpret_cast<uint4*>(p.dq + grow * D + col) = pack8(o);
       }
     }
+    ts_mark(dbg && threadIdx.x == 64, 124);
   }
   tc::tc_fence_before();
   __syncthreads();

@@ -169,27 +169,30 @@ __global__ void k_classify(const R* __restrict__ scores, int Tm,
   }
   __syncthreads();
 
-  // bitonic sort into before-order
+  // bitonic sort into before-order; pass (k, jj) compares t and t ^ jj for the P2/2 pairs
+  // with bit jj of t clear -- indexed by pair so every thread does one exchange per pass
+  int lj = 0;
   for (int k = 2; k <= P2; k <<= 1) {
     for (int jj = k >> 1; jj > 0; jj >>= 1) {
-      for (int t = tid; t < P2; t += nt) {
-        const int x = t ^ jj;
-        if (x > t) {
-          const R ka = key[t], kb = key[x];
-          const int ia = idx[t], ib = idx[x];
-          const bool t_first = before(ka, ia, kb, ib);
-          const bool up = (t & k) == 0;
-          if (up ? !t_first : t_first) {
-            key[t] = kb;
-            key[x] = ka;
-            idx[t] = ib;
-            idx[x] = ia;
-          }
+      lj = __ffs(jj) - 1;
+      for (int pr = tid; pr < (P2 >> 1); pr += nt) {
+        const int t = ((pr >> lj) << (lj + 1)) | (pr & (jj - 1));
+        const int x = t | jj;
+        const R ka = key[t], kb = key[x];
+        const int ia = idx[t], ib = idx[x];
+        const bool t_first = before(ka, ia, kb, ib);
+        const bool up = (t & k) == 0;
+        if (up != t_first) {
+          key[t] = kb;
+          key[x] = ka;
+          idx[t] = ib;
+          idx[x] = ia;
         }
       }
       __syncthreads();
     }
   }
+  (void)lj;
   for (int r = tid; r < Tn; r += nt) {
     const int j = idx[r];
     lab[j] = r < n1 ? int8_t(1) : (r >= Tn - n_neg ? int8_t(-1) : int8_t(0));

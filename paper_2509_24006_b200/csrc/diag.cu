@@ -132,3 +132,57 @@ extern "C" int sla_b200_diag_l2bw(const void* buf, long long bytes, int iters, v
   slab::k_diag_l2bw<<<blocks, threads>>>(static_cast<const uint4*>(buf), bytes / 16, iters, static_cast<uint4*>(sink));
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
+
+// (3) tcgen05.mma issue-to-completion cost per shape: one CTA, one thread issues `reps`
+// back-to-back M x N x 16 bf16 MMAs (SS operands, K-major or MN-major SW128) into one TMEM
+// accumulator; cycles between the first issue and the commit's mbarrier completing.
+namespace slab {
+namespace {
+__global__ void k_diag_mma_rate(int m, int n, int a_mn, int b_mn, int reps, long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint32_t slot;
+  __shared__ uint64_t bar;
+  const int warp = threadIdx.x >> 5;
+  for (int e = threadIdx.x; e < (128 + 256) * 64 / 8; e += blockDim.x)
+    reinterpret_cast<uint4*>(sm)[e] = make_uint4(0x3c003c00u, 0, 0x3c003c00u, 0);
+  tc::fence_proxy_async();
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 0) tc::tmem_alloc<512>(&slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (threadIdx.x == 0) {
+    const uint32_t a = tc::smem_u32(sm), b = a + 128 * 128;
+    const uint32_t id = tc::idesc_bf16(m, n, a_mn != 0, b_mn != 0);
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      const int kk = r & 3;
+      const uint64_t da = a_mn ? tc::desc_mnmajor(a + kk * 2048, 8192) : tc::desc_kmajor(a + kk * 32);
+      const uint64_t db = b_mn ? tc::desc_mnmajor(b + kk * 2048, 8192) : tc::desc_kmajor(b + kk * 32);
+      tc::mma_bf16(slot, da, db, id, r > 0);
+    }
+    tc::mma_commit(&bar);
+    tc::mbar_wait(&bar, 0);
+    out[0] = clock64() - t0;
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(slot);
+}
+}  // namespace
+}  // namespace slab
+
+extern "C" int sla_b200_diag_mma_rate(int m, int n, int a_mn, int b_mn, int reps, long long* host_cycles) {
+  long long* d = nullptr;
+  if (cudaMalloc(&d, sizeof(long long)) != cudaSuccess) return 1;
+  const int bytes = (128 + 256) * 128 + 1024;
+  cudaFuncSetAttribute(slab::k_diag_mma_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  slab::k_diag_mma_rate<<<1, 128, bytes>>>(m, n, a_mn, b_mn, reps, d);
+  int rc = cudaMemcpy(host_cycles, d, sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 1;
+  cudaFree(d);
+  return rc;
+}

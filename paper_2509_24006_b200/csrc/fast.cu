@@ -70,65 +70,99 @@ __global__ void __launch_bounds__(256) k_phi_kz(const __nv_bfloat16* __restrict_
 }
 
 // Marginal aggregation of the per-block vectors as a tiled fp32 GEMM with the 0/1 marginal
-// indicator: Z = M0 z (forward, aggregation.cpp:40-56) or dZ_agg = M0^T dZ (backward,
-// backward.cpp:170-178).  grid (ceil(T_out/64), U); 256 threads, 64 output rows x d columns
-// per CTA, K (= block index) staged 32 at a time.
+// indicator M0 (bf16, the A operand of the H GEMM): Z = M0 z (forward, aggregation.cpp:40-56)
+// or dZ_agg = M0^T dZ (backward, backward.cpp:170-178).  grid (ceil(T_out/32), U); 256
+// threads, 32 output rows x d (<= 128) columns per CTA, 2 rows x 8 columns per thread; K (the
+// block index) staged 64 at a time with coalesced 16-byte loads of M0 and x.
 template <bool kTrans>
-__global__ void __launch_bounds__(256) k_aggregate_vec(const int8_t* __restrict__ labels,
+__global__ void __launch_bounds__(256) k_aggregate_vec(const __nv_bfloat16* __restrict__ m0, int ld,
                                                        const float* __restrict__ x, int d, int Tm,
                                                        int Tn, float* __restrict__ out) {
-  constexpr int BM = 16, BK = 32;
-  __shared__ float sa[BK][BM + 1];   // indicator tile, [k][m]
-  __shared__ float sx[BK][128];      // x tile, [k][a]
+  constexpr int BM = 32, BK = 64;
+  __shared__ __align__(16) float sa[BK][BM];   // indicator tile, [k][m]
+  __shared__ __align__(16) float sx[BK][128];  // x tile, [k][a]
   const long long u = blockIdx.y;
-  const int m0 = blockIdx.x * BM;
+  const int m0r = blockIdx.x * BM;
   const int Mo = kTrans ? Tn : Tm, Kd = kTrans ? Tm : Tn;
-  const int8_t* lu = labels + u * (long long)Tm * Tn;
+  const __nv_bfloat16* mu = m0 + u * (long long)Tm * ld;
   const float* xu = x + u * (long long)Kd * d;
-  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;  // 8 row groups x 32 column lanes
-  constexpr int RPT = BM / 8;  // rows per thread group
-  float acc[RPT][4];
+  const int tid = threadIdx.x;
+  const int ty = tid >> 4, tx = tid & 15;  // rows 2*ty, 2*ty+1; columns 4*tx.. and 64+4*tx..
+  float acc[2][8];
 #pragma unroll
-  for (int i = 0; i < RPT; ++i)
+  for (int i = 0; i < 2; ++i)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc[i][c] = 0.f;
+    for (int c = 0; c < 8; ++c) acc[i][c] = 0.f;
+  // chunk k0 is staged from registers loaded during chunk k0 - BK (software pipelining)
+  uint4 ra;
+  float4 rx[8];
+  auto load = [&](int k0) {
+    ra = make_uint4(0, 0, 0, 0);
+    if (!kTrans) {  // A[m][k] = M0[m][k]: row m = tid/8, k chunk 8*(tid%8)
+      const int gm = m0r + (tid >> 3), gk = k0 + 8 * (tid & 7);
+      if (gm < Mo && gk < ld) ra = *reinterpret_cast<const uint4*>(mu + (long long)gm * ld + gk);
+    } else {  // A[m][k] = M0[k][m]: row k = tid/4, m chunk 8*(tid%4)
+      const int gk = k0 + (tid >> 2), gm = m0r + 8 * (tid & 3);
+      if (gk < Kd && gm < ld) ra = *reinterpret_cast<const uint4*>(mu + (long long)gk * ld + gm);
+    }
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {  // x: 64 rows x 128 columns as float4, 8 per thread
+      const int e = tid + 256 * r;
+      const int kk = e >> 5, a4 = 4 * (e & 31);
+      rx[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (k0 + kk < Kd && a4 < d) rx[r] = *reinterpret_cast<const float4*>(xu + (long long)(k0 + kk) * d + a4);
+    }
+  };
+  load(0);
   for (int k0 = 0; k0 < Kd; k0 += BK) {
     __syncthreads();
-    for (int e = threadIdx.x; e < BK * BM; e += 256) {
-      const int kk = e / BM, m = e % BM;
-      const int gm = m0 + m, gk = k0 + kk;
-      float v = 0.f;
-      if (gm < Mo && gk < Kd) {
-        const int8_t l = kTrans ? lu[(long long)gk * Tn + gm] : lu[(long long)gm * Tn + gk];
-        v = l == 0 ? 1.f : 0.f;
+    {
+      float v[8];
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&ra);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(h2[e]);
+        v[2 * e] = f.x;
+        v[2 * e + 1] = f.y;
       }
-      sa[kk][m] = v;
-    }
-    for (int e = threadIdx.x; e < BK * d; e += 256) {
-      const int kk = e / d, a = e % d;
-      sx[kk][a] = (k0 + kk < Kd) ? xu[(long long)(k0 + kk) * d + a] : 0.f;
+      if (!kTrans) {
+        const int m = tid >> 3, kc = 8 * (tid & 7);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) sa[kc + e][m] = k0 + kc + e < Kd ? v[e] : 0.f;
+      } else {
+        const int kk = tid >> 2, mc = 8 * (tid & 3);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) sa[kk][mc + e] = m0r + mc + e < Mo ? v[e] : 0.f;
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        const int e = tid + 256 * r;
+        *reinterpret_cast<float4*>(&sx[e >> 5][4 * (e & 31)]) = rx[r];
+      }
     }
     __syncthreads();
-#pragma unroll 4
+    if (k0 + BK < Kd) load(k0 + BK);
+#pragma unroll 8
     for (int kk = 0; kk < BK; ++kk) {
-      float xv[4];
+      const float2 w = *reinterpret_cast<const float2*>(&sa[kk][2 * ty]);
+      const float4 x0 = *reinterpret_cast<const float4*>(&sx[kk][4 * tx]);
+      const float4 x1 = *reinterpret_cast<const float4*>(&sx[kk][64 + 4 * tx]);
+      const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
 #pragma unroll
-      for (int c = 0; c < 4; ++c) xv[c] = (tx + 32 * c < d) ? sx[kk][tx + 32 * c] : 0.f;
-#pragma unroll
-      for (int i = 0; i < RPT; ++i) {
-        const float w = sa[kk][ty * RPT + i];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[i][c] = fmaf(w, xv[c], acc[i][c]);
+      for (int c = 0; c < 8; ++c) {
+        acc[0][c] = fmaf(w.x, xv[c], acc[0][c]);
+        acc[1][c] = fmaf(w.y, xv[c], acc[1][c]);
       }
     }
   }
 #pragma unroll
-  for (int i = 0; i < RPT; ++i) {
-    const int gm = m0 + ty * RPT + i;
+  for (int i = 0; i < 2; ++i) {
+    const int gm = m0r + 2 * ty + i;
     if (gm >= Mo) continue;
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-      if (tx + 32 * c < d) out[(u * Mo + gm) * d + tx + 32 * c] = acc[i][c];
+    float* orow = out + (u * Mo + gm) * d;
+    if (4 * tx < d) *reinterpret_cast<float4*>(orow + 4 * tx) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
+    if (64 + 4 * tx < d)
+      *reinterpret_cast<float4*>(orow + 64 + 4 * tx) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
   }
 }
 
@@ -203,8 +237,8 @@ void fast_prepare_linear(const Dims& Dm, const void* k, const void* v, const Sta
   a.c_batch = (long long)Dm.Tm * d * d;
   a.name = "gemm_aggregate";
   launch_gemm(a, st);
-  k_aggregate_vec<false><<<dim3((Dm.Tm + 15) / 16, unsigned(Dm.U)), 256, 0, st>>>(s.labels, wb.z, d, Dm.Tm,
-                                                                                Dm.Tn, s.Z);
+  k_aggregate_vec<false><<<dim3((Dm.Tm + 31) / 32, unsigned(Dm.U)), 256, 0, st>>>(s.M0, int(m0_stride(Dm)), wb.z, d,
+                                                                                Dm.Tm, Dm.Tn, s.Z);
   check_launch("k_aggregate_z", st);
 }
 
@@ -245,8 +279,8 @@ void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, 
   a.c_batch = (long long)Dm.Tn * d * d;
   a.name = "gemm_aggregate_t";
   launch_gemm(a, st);
-  k_aggregate_vec<true><<<dim3((Dm.Tn + 15) / 16, unsigned(Dm.U)), 256, 0, st>>>(s.labels, wb.gZ, d, Dm.Tm,
-                                                                               Dm.Tn, wb.gZa);
+  k_aggregate_vec<true><<<dim3((Dm.Tn + 31) / 32, unsigned(Dm.U)), 256, 0, st>>>(s.M0, int(m0_stride(Dm)), wb.gZ, d,
+                                                                               Dm.Tm, Dm.Tn, wb.gZa);
   check_launch("k_aggregate_dz", st);
   // columns pass: dk_total, dv
   launch_bwd_cols(Dm, q, k, v, lse, d_out, dk, dv, s, wb.hab, wb.gZa, wb.Ds, st);
