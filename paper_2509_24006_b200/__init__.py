@@ -13,9 +13,10 @@ from .sla import (  # noqa: F401
     sla_forward,
     sla_forward_with_mask,
 )
+from .pipeline import HostTrainStep  # noqa: F401
 from ._lib import LIB_PATH  # noqa: F401
 
 __all__ = [
     "SLA", "BlockLayout", "SlaConfig", "SlaForwardState", "SlaGradients", "combine_outputs",
-    "make_block_layout", "sla_backward", "sla_forward", "sla_forward_with_mask",
+    "make_block_layout", "sla_backward", "sla_forward", "sla_forward_with_mask", "HostTrainStep",
 ]

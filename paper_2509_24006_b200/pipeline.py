@@ -1,0 +1,124 @@
+"""Host-buffer training step with copy / compute overlap.
+
+The reference's API works on host matrices (forward.hpp / backward.hpp take `Mat<T>` in host
+memory), so a drop-in that is handed host buffers pays PCIe both ways.  `HostTrainStep` runs
+the fused SLA forward + backward on pinned host tensors and hides most of that traffic: the
+(batch, head) units are independent, so it splits them into contiguous chunks (over heads when
+batch == 1, over the batch otherwise) and overlaps, on three CUDA streams,
+
+    H2D(chunk c+1)  |  forward + backward(chunk c)  |  D2H(chunk c-1)
+
+with two device-side slots.  Every chunk runs through the same C-ABI calls as `SLA` (one
+`SLA` instance per distinct chunk shape).  dW is per head: chunks over heads write disjoint
+head rows; chunks over the batch accumulate into one dW (backward.cpp:46 sums over the batch).
+"""
+from __future__ import annotations
+
+from typing import List, Optional, Tuple
+
+import torch
+
+from .sla import SLA, SlaConfig
+
+
+def _split(n: int, parts: int) -> List[Tuple[int, int]]:
+    parts = max(1, min(parts, n))
+    base, extra = divmod(n, parts)
+    out, s = [], 0
+    for i in range(parts):
+        e = s + base + (1 if i < extra else 0)
+        out.append((s, e))
+        s = e
+    return out
+
+
+class HostTrainStep:
+    """fwd+bwd of an SLA layer on pinned host tensors [B, H, N, d] (bf16), W [H, d, d].
+
+    Outputs (host): o [B, H, N, d], dq, dk, dv [B, H, N, d] (bf16) and dW [H, d, d] (f32).
+    The call is stream-ordered after the caller's current stream and the caller's current
+    stream is made to wait for the last device->host copy, so CUDA events recorded around the
+    call time the whole step.
+    """
+
+    def __init__(self, batch: int, heads: int, n: int, d: int, b_q: int = 64, b_kv: int = 64,
+                 cfg: Optional[SlaConfig] = None, dtype=torch.bfloat16, device="cuda", chunks: int = 4):
+        self.batch, self.heads, self.n, self.d = batch, heads, n, d
+        self.device = torch.device(device)
+        self.dtype = dtype
+        self.by_heads = batch == 1
+        self.ranges = _split(heads if self.by_heads else batch, chunks)
+        self.ops = {}
+        for s, e in self.ranges:
+            shape = (1, e - s) if self.by_heads else (e - s, heads)
+            if shape not in self.ops:
+                self.ops[shape] = SLA(shape[0], shape[1], n, d, b_q, b_kv, cfg, dtype, device)
+        span = max(e - s for s, e in self.ranges)
+        cshape = (1, span, n, d) if self.by_heads else (span, heads, n, d)
+        mk = lambda dt=dtype: torch.empty(cshape, dtype=dt, device=self.device)  # noqa: E731
+        self.slots = []
+        for _ in range(2):
+            self.slots.append({
+                "q": mk(), "k": mk(), "v": mk(), "do": mk(),
+                "o": mk(), "o_s": mk(), "o_l": mk(), "lse": mk(torch.float32)[..., 0].contiguous(),
+                "dq": mk(), "dk": mk(), "dv": mk(),
+            })
+        self.states = {shape: op.new_state() for shape, op in self.ops.items()}
+        self.w = torch.empty((heads, d, d), dtype=dtype, device=self.device)
+        self.dw = torch.empty((heads, d, d), dtype=torch.float32, device=self.device)
+        self.dw_part = None if self.by_heads else torch.empty_like(self.dw)
+        self.s_in, self.s_c, self.s_out = (torch.cuda.Stream(self.device) for _ in range(3))
+        self.ev_in = [torch.cuda.Event() for _ in range(2)]
+        self.ev_c = [torch.cuda.Event() for _ in range(2)]
+        self.ev_out = [torch.cuda.Event() for _ in range(2)]
+        self.launches = 0
+
+    def h2d_bytes(self) -> int:
+        return 4 * self.batch * self.heads * self.n * self.d * 2 + self.heads * self.d * self.d * 2
+
+    def d2h_bytes(self) -> int:
+        return 4 * self.batch * self.heads * self.n * self.d * 2 + self.heads * self.d * self.d * 4
+
+    def __call__(self, hq, hk, hv, hw, hdo, ho, hdq, hdk, hdv, hdw) -> None:
+        cur = torch.cuda.current_stream(self.device)
+        for s in (self.s_in, self.s_c, self.s_out):
+            s.wait_stream(cur)
+        self.launches = 0
+        with torch.cuda.stream(self.s_in):
+            self.w.copy_(hw, non_blocking=True)
+        for c, (s, e) in enumerate(self.ranges):
+            slot = self.slots[c % 2]
+            shape = (1, e - s) if self.by_heads else (e - s, self.heads)
+            op, state = self.ops[shape], self.states[shape]
+            sl = (slice(0, 1), slice(s, e)) if self.by_heads else (slice(s, e),)
+            view = lambda t: t[: shape[0], : shape[1]]  # noqa: E731  (slot tensors are max-span)
+            with torch.cuda.stream(self.s_in):
+                if c >= 2:
+                    self.s_in.wait_event(self.ev_c[c % 2])  # compute(c-2) done with the inputs
+                for nm, src in (("q", hq), ("k", hk), ("v", hv), ("do", hdo)):
+                    view(slot[nm]).copy_(src[sl], non_blocking=True)
+                self.ev_in[c % 2].record(self.s_in)
+            with torch.cuda.stream(self.s_c):
+                self.s_c.wait_event(self.ev_in[c % 2])
+                if c >= 2:
+                    self.s_c.wait_event(self.ev_out[c % 2])  # D2H(c-2) done with the outputs
+                q, k, v, do = (view(slot[nm]) for nm in ("q", "k", "v", "do"))
+                w = self.w[s:e] if self.by_heads else self.w
+                dw = self.dw[s:e] if self.by_heads else (self.dw if c == 0 else self.dw_part)
+                st = op.forward(q, k, v, w, state=state,
+                                out=(view(slot["o"]), view(slot["o_s"]), view(slot["o_l"]), view(slot["lse"])))
+                self.launches += op.launches()
+                op.backward(st, q, k, v, w, do, out=(view(slot["dq"]), view(slot["dk"]), view(slot["dv"]), dw))
+                self.launches += op.launches()
+                if not self.by_heads and c > 0:
+                    self.dw.add_(self.dw_part)
+                self.ev_c[c % 2].record(self.s_c)
+            with torch.cuda.stream(self.s_out):
+                self.s_out.wait_event(self.ev_c[c % 2])
+                for nm, dst in (("o", ho), ("dq", hdq), ("dk", hdk), ("dv", hdv)):
+                    dst[sl].copy_(view(slot[nm]), non_blocking=True)
+                self.ev_out[c % 2].record(self.s_out)
+        with torch.cuda.stream(self.s_out):
+            self.s_out.wait_stream(self.s_c)
+            hdw.copy_(self.dw, non_blocking=True)
+        cur.wait_stream(self.s_out)
