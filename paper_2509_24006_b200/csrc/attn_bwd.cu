@@ -7,7 +7,8 @@
 //   linear dK^phi_j = V_j dH_agg^T + dZ_agg, dV_j += phi(K_j) dH_agg (dH_agg = M0^T dH),
 //   dk_total = J_phi(k)^T dK^phi + dK and dv written once.
 //
-// Warp roles: warp 0 TMA, warp 1 MMA (one thread), warps 2-9 compute.
+// Warp roles: warps 0 and 10 TMA (each ring stage is filled by both -- Q pair / dO pair -- since
+// one issuing warp's TMA stream caps at ~40 B/cycle), warp 1 MMA (one thread), warps 2-9 compute.
 #include "bwd_common.cuh"
 
 namespace slab {
@@ -35,7 +36,7 @@ struct ColsLayout {
 };
 
 template <int D>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(352, 1)
     k_bwd_cols(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
                const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                const __grid_constant__ CUtensorMap tmHa, BwdParams p) {
@@ -88,7 +89,7 @@ __global__ void __launch_bounds__(320, 1)
     if (lane == 0) {
       tc::mbar_init(kv_full, 1);
       for (int s = 0; s < RS; ++s) {
-        tc::mbar_init(ring_full + s, 1);
+        tc::mbar_init(ring_full + s, 2);  // one arrive.expect_tx per producer warp
         tc::mbar_init(ring_empty + s, 1);
       }
       for (int s = 0; s < 2; ++s) {
@@ -112,15 +113,18 @@ __global__ void __launch_bounds__(320, 1)
   // dK^phi^T at [384, 448) (M = D)
   const uint32_t tDVT = tmem, tDKT = tmem + 64, tB0 = tmem + 128, tB1 = tmem + 256, tKPT = tmem + 384;
 
-  if (warp == 0) {
+  if (warp == 0 || warp == 10) {
     // No L2 prefetch of the column's Q / dO tiles: prefetches queue in the TMA unit ahead of
     // the ring loads, and a wave's columns share one unit's Q / dO, which stays L2-resident.
     if (lane == 0) {
-      tc::mbar_expect_tx(kv_full, 2 * L::kT);
+      const int pid = warp == 0 ? 0 : 1;  // 0: K/V + Q pairs + even dH_agg chunks; 1: dO pairs + odd chunks
+      if (pid == 0) {
+        tc::mbar_expect_tx(kv_full, 2 * L::kT);
 #pragma unroll
-      for (int c = 0; c < D / 64; ++c) {
-        tc::tma_load_3d(sK + c * 8192, &tmK, kv_full, 64 * c, kv0, 0);
-        tc::tma_load_3d(sV + c * 8192, &tmV, kv_full, 64 * c, kv0, 0);
+        for (int c = 0; c < D / 64; ++c) {
+          tc::tma_load_3d(sK + c * 8192, &tmK, kv_full, 64 * c, kv0, 0);
+          tc::tma_load_3d(sV + c * 8192, &tmV, kv_full, 64 * c, kv0, 0);
+        }
       }
       int item = 0;
       auto acquire = [&](int bytes) -> uint8_t* {
@@ -129,25 +133,25 @@ __global__ void __launch_bounds__(320, 1)
         tc::mbar_expect_tx(ring_full + s, bytes);
         return sRing + s * L::kStage;
       };
+      const CUtensorMap* tm = pid == 0 ? &tmQ : &tmDO;
       for (int pp = 0; pp < np; ++pp) {
         const int r1 = int(u * p.N) + list[2 * pp] * 64;
         const int r2 = int(u * p.N) + list[min(2 * pp + 1, cnt - 1)] * 64;
-        uint8_t* dst = acquire(2 * L::kP);
-        ts_mark(dbg && pp < 16, pp);
+        uint8_t* dst = acquire(L::kP) + pid * L::kP;
+        ts_mark(dbg && pid == 0 && pp < 16, pp);
         uint64_t* fb = ring_full + (item % RS);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
-          tc::tma_load_3d(dst + c * 16384, &tmQ, fb, 64 * c, r1, 0);
-          tc::tma_load_3d(dst + c * 16384 + 8192, &tmQ, fb, 64 * c, r2, 0);
-          tc::tma_load_3d(dst + L::kP + c * 16384, &tmDO, fb, 64 * c, r1, 0);
-          tc::tma_load_3d(dst + L::kP + c * 16384 + 8192, &tmDO, fb, 64 * c, r2, 0);
+          tc::tma_load_3d(dst + c * 16384, tm, fb, 64 * c, r1, 0);
+          tc::tma_load_3d(dst + c * 16384 + 8192, tm, fb, 64 * c, r2, 0);
         }
         ++item;
       }
       if (has_lin) {
-        uint8_t* dst = acquire(D * D * 2);
-#pragma unroll
-        for (int c = 0; c < D / 64; ++c)
+        constexpr int NC = D / 64;
+        const int mine = pid == 0 ? (NC + 1) / 2 : NC / 2;  // chunks c with c % 2 == pid
+        uint8_t* dst = acquire(mine * D * 128);
+        for (int c = pid; c < NC; c += 2)
           tc::tma_load_3d(dst + c * D * 128, &tmHa, ring_full + (item % RS), 64 * c, int(ucol * D), 0);
         ++item;
       }
@@ -411,7 +415,7 @@ void launch_cols_t(const Dims& Dm, const void* q, const void* k, const void* v, 
   make_tmap_bf16(&th, Ha, D, uint64_t(Dm.U) * Dm.Tn * D, 1, D, 0, D);
   auto kern = k_bwd_cols<D>;
   SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ColsLayout<D>::kBytes));
-  kern<<<dim3(Dm.Tn, unsigned(Dm.U)), 320, ColsLayout<D>::kBytes, st>>>(tq, tdo, tk, tv, th, p);
+  kern<<<dim3(Dm.Tn, unsigned(Dm.U)), 352, ColsLayout<D>::kBytes, st>>>(tq, tdo, tk, tv, th, p);
   check_launch("k_bwd_cols", st);
 }
 

@@ -319,7 +319,7 @@ struct RowsLayout {
 };
 
 template <int D>
-__global__ void __launch_bounds__(320, 1)
+__global__ void __launch_bounds__(352, 1)
     k_bwd_rows(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
                const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                BwdParams p) {
@@ -382,35 +382,42 @@ __global__ void __launch_bounds__(320, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t tDQT = tmem, tB0 = tmem + 128, tB1 = tmem + 256;  // dQ^T (M = D); S^T|dP^T pairs
 
-  if (warp == 0) {
+  if (warp == 0 || warp == 10) {
+    // two producer warps (Q/dO + K ring, V ring): one issuing warp's TMA stream caps at ~40 B/cycle
     if (lane == 0) {
-      tc::mbar_expect_tx(qdo_full, 2 * L::kT);
+      const int pid = warp == 0 ? 0 : 1;
+      if (pid == 0) {
+        tc::mbar_expect_tx(qdo_full, 2 * L::kT);
 #pragma unroll
-      for (int c = 0; c < D / 64; ++c) {
-        tc::tma_load_3d(sQ + c * 8192, &tmQ, qdo_full, 64 * c, row0, 0);
-        tc::tma_load_3d(sDO + c * 8192, &tmDO, qdo_full, 64 * c, row0, 0);
+        for (int c = 0; c < D / 64; ++c) {
+          tc::tma_load_3d(sQ + c * 8192, &tmQ, qdo_full, 64 * c, row0, 0);
+          tc::tma_load_3d(sDO + c * 8192, &tmDO, qdo_full, 64 * c, row0, 0);
+        }
       }
       for (int t = 0; t < np; ++t) {
         // an odd tail repeats its block (finite data); the compute warps zero its dS rows
         const int r1 = int(u * p.N) + list[2 * t] * 64;
         const int r2 = int(u * p.N) + list[min(2 * t + 1, cnt - 1)] * 64;
         const int ks = t % L::KS, vs = t % L::VS;
-        tc::mbar_wait(k_empty + ks, ((t / L::KS) & 1) ^ 1);
-        tc::mbar_expect_tx(k_full + ks, L::kP);
-        ts_mark(dbg && t < 16, t);
-        uint8_t* dk = sK + ks * L::kP;
+        if (pid == 0) {
+          tc::mbar_wait(k_empty + ks, ((t / L::KS) & 1) ^ 1);
+          tc::mbar_expect_tx(k_full + ks, L::kP);
+          ts_mark(dbg && t < 16, t);
+          uint8_t* dk = sK + ks * L::kP;
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c) {
-          tc::tma_load_3d(dk + c * 16384, &tmK, k_full + ks, 64 * c, r1, 0);
-          tc::tma_load_3d(dk + c * 16384 + 8192, &tmK, k_full + ks, 64 * c, r2, 0);
-        }
-        tc::mbar_wait(v_empty + vs, ((t / L::VS) & 1) ^ 1);
-        tc::mbar_expect_tx(v_full + vs, L::kP);
-        uint8_t* dv = sV + vs * L::kP;
+          for (int c = 0; c < D / 64; ++c) {
+            tc::tma_load_3d(dk + c * 16384, &tmK, k_full + ks, 64 * c, r1, 0);
+            tc::tma_load_3d(dk + c * 16384 + 8192, &tmK, k_full + ks, 64 * c, r2, 0);
+          }
+        } else {
+          tc::mbar_wait(v_empty + vs, ((t / L::VS) & 1) ^ 1);
+          tc::mbar_expect_tx(v_full + vs, L::kP);
+          uint8_t* dv = sV + vs * L::kP;
 #pragma unroll
-        for (int c = 0; c < D / 64; ++c) {
-          tc::tma_load_3d(dv + c * 16384, &tmV, v_full + vs, 64 * c, r1, 0);
-          tc::tma_load_3d(dv + c * 16384 + 8192, &tmV, v_full + vs, 64 * c, r2, 0);
+          for (int c = 0; c < D / 64; ++c) {
+            tc::tma_load_3d(dv + c * 16384, &tmV, v_full + vs, 64 * c, r1, 0);
+            tc::tma_load_3d(dv + c * 16384 + 8192, &tmV, v_full + vs, 64 * c, r2, 0);
+          }
         }
       }
     }
@@ -651,7 +658,7 @@ void launch_bwd_rows(const Dims& Dm, const void* q, const void* k, const void* v
     make_tmap_bf16(&tk, k, D, rows, 1, D, 0, 64);
     make_tmap_bf16(&tv, v, D, rows, 1, D, 0, 64);
     SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    kern<<<dim3(Dm.Tm, unsigned(Dm.U)), 320, bytes, st>>>(tq, tdo, tk, tv, p);
+    kern<<<dim3(Dm.Tm, unsigned(Dm.U)), 352, bytes, st>>>(tq, tdo, tk, tv, p);
     check_launch("k_bwd_rows", st);
   };
   if (Dm.d == 128)

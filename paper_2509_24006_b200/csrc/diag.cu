@@ -186,3 +186,145 @@ extern "C" int sla_b200_diag_mma_rate(int m, int n, int a_mn, int b_mn, int reps
   cudaFree(d);
   return rc;
 }
+
+// (4) TMA throughput per SM vs bytes in flight: each CTA streams `iters` random 64x128 bf16
+// tiles (16 KB, two SW128 boxes) from an L2-resident buffer through a ring of `slots` tiles.
+namespace slab {
+namespace {
+__global__ void k_diag_tma_bw(const __grid_constant__ CUtensorMap tm, int rows, int slots, int iters,
+                              int producers, long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bars[16];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < slots; ++s) tc::mbar_init(bars + s, 1);
+    tc::fence_barrier_init();
+  }
+  __syncthreads();
+  // producer p (lane 0 of warp p) runs its own ring of slots/producers tiles
+  const int pw = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0 && pw < producers) {
+    const int ps = slots / producers, s0 = pw * ps, my_iters = iters / producers;
+    uint32_t x = 12345u + 7919u * blockIdx.x + 104729u * pw;
+    const int tiles = rows / 64;
+    const long long t0 = clock64();
+    for (int it = 0; it < my_iters + ps; ++it) {
+      const int s = s0 + it % ps;
+      if (it >= ps) tc::mbar_wait(bars + s, ((it / ps) - 1) & 1);
+      if (it < my_iters) {
+        x = x * 1664525u + 1013904223u;
+        const int row = int((x >> 8) % uint32_t(tiles)) * 64;
+        tc::mbar_expect_tx(bars + s, 16384);
+        tc::tma_load_3d(sm + s * 16384, &tm, bars + s, 0, row, 0);
+        tc::tma_load_3d(sm + s * 16384 + 8192, &tm, bars + s, 64, row, 0);
+      }
+    }
+    const long long dt = clock64() - t0;
+    if (pw == 0) out[blockIdx.x] = dt;
+  }
+}
+}  // namespace
+}  // namespace slab
+
+extern "C" int sla_b200_diag_tma_bw(const void* buf, int rows, int ctas, int slots, int iters,
+                                    int producers, long long* host_cycles) {
+  try {
+    CUtensorMap tm;
+    slab::make_tmap_bf16(&tm, buf, 128, uint64_t(rows), 1, 128, 0, 64);
+    long long* d = nullptr;
+    if (cudaMalloc(&d, sizeof(long long) * ctas) != cudaSuccess) return 1;
+    const int bytes = slots * 16384 + 1024;
+    cudaFuncSetAttribute(slab::k_diag_tma_bw, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    slab::k_diag_tma_bw<<<ctas, 32 * producers, bytes>>>(tm, rows, slots, iters, producers, d);
+    int rc = cudaMemcpy(host_cycles, d, sizeof(long long) * ctas, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 1;
+    cudaFree(d);
+    return rc;
+  } catch (...) {
+    return 1;
+  }
+}
+
+// (5) contention: the MMA stream of (3) while warp 1 streams TMA tile loads (16 KB each, ring
+// of 4) into a separate smem region of the same CTA (tma_on = 0: MMAs alone).
+namespace slab {
+namespace {
+__global__ void k_diag_mma_tma(const __grid_constant__ CUtensorMap tm, int rows, int m, int n, int reps,
+                               int tma_on, long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* ring = sm + (128 + 256) * 128;
+  __shared__ uint32_t slot;
+  __shared__ uint64_t bar, rb[4];
+  __shared__ volatile int stop;
+  const int warp = threadIdx.x >> 5;
+  for (int e = threadIdx.x; e < (128 + 256) * 64 / 8; e += blockDim.x)
+    reinterpret_cast<uint4*>(sm)[e] = make_uint4(0x3c003c00u, 0, 0x3c003c00u, 0);
+  tc::fence_proxy_async();
+  if (threadIdx.x == 0) {
+    stop = 0;
+    tc::mbar_init(&bar, 1);
+    for (int s = 0; s < 4; ++s) tc::mbar_init(rb + s, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 0) tc::tmem_alloc<512>(&slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (threadIdx.x == 0) {
+    const uint32_t a = tc::smem_u32(sm), b = a + 128 * 128;
+    const uint32_t id = tc::idesc_bf16(m, n, false, false);
+    const long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      const int kk = r & 3;
+      tc::mma_bf16(slot, tc::desc_kmajor(a + kk * 32), tc::desc_kmajor(b + kk * 32), id, r > 0);
+    }
+    tc::mma_commit(&bar);
+    tc::mbar_wait(&bar, 0);
+    out[2 * blockIdx.x] = clock64() - t0;
+    stop = 1;
+  } else if (threadIdx.x == 32 && tma_on) {
+    uint32_t x = 777u + blockIdx.x;
+    const int tiles = rows / 64;
+    long long loads = 0;
+    for (int it = 0;; ++it) {
+      const int s = it & 3;
+      if (it >= 4) tc::mbar_wait(rb + s, ((it >> 2) - 1) & 1);
+      if (stop) {
+        for (int k = it + 1; k < it + 4; ++k)
+          if (k >= 4 && k - 4 < it) tc::mbar_wait(rb + (k & 3), ((k >> 2) - 1) & 1);
+        break;
+      }
+      x = x * 1664525u + 1013904223u;
+      const int row = int((x >> 8) % uint32_t(tiles)) * 64;
+      tc::mbar_expect_tx(rb + s, 16384);
+      tc::tma_load_3d(ring + s * 16384, &tm, rb + s, 0, row, 0);
+      tc::tma_load_3d(ring + s * 16384 + 8192, &tm, rb + s, 64, row, 0);
+      ++loads;
+    }
+    out[2 * blockIdx.x + 1] = loads;
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc<512>(slot);
+}
+}  // namespace
+}  // namespace slab
+
+extern "C" int sla_b200_diag_mma_tma(const void* buf, int rows, int ctas, int m, int n, int reps, int tma_on,
+                                     long long* host2) {
+  try {
+    CUtensorMap tm;
+    slab::make_tmap_bf16(&tm, buf, 128, uint64_t(rows), 1, 128, 0, 64);
+    long long* d = nullptr;
+    if (cudaMalloc(&d, sizeof(long long) * 2 * ctas) != cudaSuccess) return 1;
+    cudaMemset(d, 0, sizeof(long long) * 2 * ctas);
+    const int bytes = (128 + 256) * 128 + 4 * 16384 + 1024;
+    cudaFuncSetAttribute(slab::k_diag_mma_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    slab::k_diag_mma_tma<<<ctas, 64, bytes>>>(tm, rows, m, n, reps, tma_on, d);
+    int rc = cudaMemcpy(host2, d, sizeof(long long) * 2 * ctas, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 1;
+    cudaFree(d);
+    return rc;
+  } catch (...) {
+    return 1;
+  }
+}

@@ -5,9 +5,11 @@
 // C[b] = A[b] . B[b] with A either K-major ([M][K] rows) or M-major ([K][M] rows) and
 // B either N-major ([K][N] rows) or K-major ([N][K] rows); fp32 accumulate in TMEM.
 //
-// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = MMA issuer (one elected
-// thread), warps 2-5 = epilogue (TMEM -> registers -> global).  4-stage smem ring with
-// full/empty mbarriers; the accumulator lives in TMEM (BN columns).
+// Warp roles (224 threads): warp 0 = TMA producer of A, warp 6 = TMA producer of B (one issuing
+// warp's TMA stream saturates at ~40 B/cycle, two reach ~70 B/cycle per SM -- csrc/diag.cu
+// sla_b200_diag_tma_bw -- so each stage is filled by both), warp 1 = MMA issuer (one elected thread), warps 2-5 = epilogue
+// (TMEM -> registers -> global).  4-stage smem ring with full/empty mbarriers; the
+// accumulator lives in TMEM (BN columns).
 #include <algorithm>
 #include <cstdio>
 
@@ -33,7 +35,7 @@ struct GemmSmem {
 // boundaries and the TMEM accumulator is double-buffered (2 x BN columns) so the epilogue of
 // tile t overlaps the main loop of tile t+1.
 template <int BM, int BN, bool A_MN, bool B_MN, typename OutT>
-__global__ void __launch_bounds__(192, 1)
+__global__ void __launch_bounds__(224, 1)
     k_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
            OutT* __restrict__ C, int M, int N, int K, int batch, long long c_batch, int ldc) {
   using L = GemmSmem<BM, BN>;
@@ -55,7 +57,7 @@ __global__ void __launch_bounds__(192, 1)
       tc::tma_prefetch(&ta);
       tc::tma_prefetch(&tb);
       for (int s = 0; s < kStages; ++s) {
-        tc::mbar_init(&full[s], 1);
+        tc::mbar_init(&full[s], 2);  // one arrive.expect_tx per producer
         tc::mbar_init(&empty[s], 1);
       }
       for (int s = 0; s < 2; ++s) {
@@ -78,8 +80,9 @@ __global__ void __launch_bounds__(192, 1)
     b = int(t / ((long long)tiles_n * tiles_m));
   };
 
-  if (warp == 0) {
+  if (warp == 0 || warp == 6) {
     if (lane == 0) {
+      const bool loads_a = warp == 0;
       int kc = 0;  // k-blocks issued by this CTA (ring position)
       for (long long t = blockIdx.x; t < total; t += gridDim.x) {
         int n0, m0, b;
@@ -89,19 +92,23 @@ __global__ void __launch_bounds__(192, 1)
           tc::mbar_wait(&empty[s], ((kc / kStages) & 1) ^ 1);
           uint8_t* sa = smem + s * L::kStage;
           uint8_t* sb = sa + L::kA;
-          tc::mbar_expect_tx(&full[s], L::kStage);
           const int k0 = kb * kBK;
-          if (A_MN) {
+          if (loads_a) {
+            tc::mbar_expect_tx(&full[s], L::kA);
+            if (A_MN) {
 #pragma unroll
-            for (int c = 0; c < BM / 64; ++c) tc::tma_load_3d(sa + c * 8192, &ta, &full[s], m0 + 64 * c, k0, b);
+              for (int c = 0; c < BM / 64; ++c) tc::tma_load_3d(sa + c * 8192, &ta, &full[s], m0 + 64 * c, k0, b);
+            } else {
+              tc::tma_load_3d(sa, &ta, &full[s], k0, m0, b);
+            }
           } else {
-            tc::tma_load_3d(sa, &ta, &full[s], k0, m0, b);
-          }
-          if (B_MN) {
+            tc::mbar_expect_tx(&full[s], L::kB);
+            if (B_MN) {
 #pragma unroll
-            for (int c = 0; c < BN / 64; ++c) tc::tma_load_3d(sb + c * 8192, &tb, &full[s], n0 + 64 * c, k0, b);
-          } else {
-            tc::tma_load_3d(sb, &tb, &full[s], k0, n0, b);
+              for (int c = 0; c < BN / 64; ++c) tc::tma_load_3d(sb + c * 8192, &tb, &full[s], n0 + 64 * c, k0, b);
+            } else {
+              tc::tma_load_3d(sb, &tb, &full[s], k0, n0, b);
+            }
           }
         }
       }
@@ -133,7 +140,7 @@ __global__ void __launch_bounds__(192, 1)
         __syncwarp();
       }
     }
-  } else {
+  } else if (warp <= 5) {
     // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
     const int q = warp & 3;
     int lt = 0;
@@ -217,7 +224,7 @@ void launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
   static int sms = 0;
   if (!sms) SLAB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   const int grid = int(std::min<long long>(tiles, sms));
-  kern<<<grid, 192, smem, st>>>(ta, tb, static_cast<OutT*>(g.C), g.M, g.N, g.K, g.batch, g.c_batch, g.ldc);
+  kern<<<grid, 224, smem, st>>>(ta, tb, static_cast<OutT*>(g.C), g.M, g.N, g.K, g.batch, g.c_batch, g.ldc);
   check_launch(g.name ? g.name : "k_gemm", st);
 }
 
