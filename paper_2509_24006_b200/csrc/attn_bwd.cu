@@ -69,8 +69,9 @@ __global__ void __launch_bounds__(352, 1)
   const int cnt = p.ccol_cnt[ucol];
   const int np = (cnt + 1) >> 1;
   const int* list = p.ccol_idx + ucol * p.Tm;
-  const bool dbg = blockIdx.x == 100 && blockIdx.y == 6;
+  const bool dbg = blockIdx.x == SLAB_DBG_X && blockIdx.y == 6;
   ts_mark(dbg && threadIdx.x == 0, 127);
+  cta_mark(threadIdx.x == 0, 0);
   __shared__ int s_lin;
   if (threadIdx.x == 0) s_lin = 0;
   __syncthreads();
@@ -118,6 +119,9 @@ __global__ void __launch_bounds__(352, 1)
     // the ring loads, and a wave's columns share one unit's Q / dO, which stays L2-resident.
     if (lane == 0) {
       const int pid = warp == 0 ? 0 : 1;  // 0: K/V + Q pairs + even dH_agg chunks; 1: dO pairs + odd chunks
+#ifndef SLAB_NO_TMAP_PREFETCH
+      tc::tma_prefetch(pid == 0 ? &tmQ : &tmDO);
+#endif
       if (pid == 0) {
         tc::mbar_expect_tx(kv_full, 2 * L::kT);
 #pragma unroll
@@ -176,6 +180,7 @@ __global__ void __launch_bounds__(352, 1)
     tc::mbar_wait(kv_full, 0);
     tc::tc_fence_after();
     ts_mark(dbg && lane == 0, 125);
+    cta_mark(lane == 0, 1);
     auto issue_acc = [&](int t) {  // dV^T += dO_pair^T P, dK^T += Q_pair^T dS  (M = D, K = 128)
       tc::tc_fence_after();
       const uint32_t sq = aR + (t % RS) * L::kStage;
@@ -197,7 +202,22 @@ __global__ void __launch_bounds__(352, 1)
     // warps.  S/dP(t) reuses TMEM buffer t&1, free once acc(t-2) was issued (pd_full(t-2) seen).
     if (lane == 0) {
       int ts = 0, ta = 0;
+      uint32_t seen_k = 0, seen_v = 0;
+      (void)seen_k;
+      (void)seen_v;
       while (ta < np) {
+        bool progressed = false;
+        (void)progressed;
+#ifdef SLAB_TIMELINE
+        if (dbg && ts < 16 && ts < np && !(seen_k >> ts & 1) && tc::mbar_test(ring_full + ts % RS, (ts / RS) & 1)) {
+          g_bwd_ts[80 + ts] = clock64();
+          seen_k |= 1u << ts;
+        }
+        if (dbg && ta < 16 && ta < ts && !(seen_v >> ta & 1) && tc::mbar_test(pd_full + (ta & 1), (ta >> 1) & 1)) {
+          g_bwd_ts[96 + ta] = clock64();
+          seen_v |= 1u << ta;
+        }
+#endif
         if (ts < np && ts <= ta + 1 && tc::mbar_test(ring_full + ts % RS, (ts / RS) & 1)) {
           tc::tc_fence_after();
           ts_mark(dbg && ts < 16, 16 + ts);
@@ -210,11 +230,15 @@ __global__ void __launch_bounds__(352, 1)
           }
           tc::mma_commit(sdp_full + (ts & 1));
           ++ts;
+          progressed = true;
         }
         if (ta < ts && tc::mbar_test(pd_full + (ta & 1), (ta >> 1) & 1)) {
           issue_acc(ta);
           ++ta;
         }
+#if SLAB_POLL_NS > 0
+        else if (!progressed) __nanosleep(SLAB_POLL_NS);
+#endif
       }
       tc::mma_commit(acc_done);
     }
@@ -274,7 +298,9 @@ __global__ void __launch_bounds__(352, 1)
           dd[e >> 1] = tc::pack_bf16(d0, d1);
         }
       }
+      ts_mark(dbg && threadIdx.x == 64 && t < 16, 128 + t);
       if (t >= 2) tc::mbar_wait(pd_empty + (t & 1), ((t - 2) >> 1) & 1);
+      ts_mark(dbg && threadIdx.x == 64 && t < 16, 144 + t);
       uint8_t* prow = sPD + (t & 1) * 32768;
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
@@ -319,6 +345,7 @@ __global__ void __launch_bounds__(352, 1)
     auto phi_of = [&](float x) { return p.phi == 2 ? __expf(x - mx) * inv : phi_elem(p.phi, x); };
     tc::mbar_wait(acc_done, 0);  // the P / dS buffers are free
     ts_mark(dbg && threadIdx.x == 64, 120);
+    cta_mark(threadIdx.x == 64, 2);
     if (has_lin) {
 #pragma unroll
       for (int cc = 0; cc < D / 4; cc += 8) {
@@ -398,6 +425,7 @@ __global__ void __launch_bounds__(352, 1)
     }
   }
   ts_mark(dbg && threadIdx.x == 64, 124);
+  cta_mark(threadIdx.x == 64, 3);
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
@@ -448,6 +476,10 @@ void launch_bwd_cols(const Dims& Dm, const void* q, const void* k, const void* v
 
 }  // namespace slab
 
+extern "C" int sla_b200_diag_cols_ctaprof(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, slab::g_cta_prof, sizeof(slab::g_cta_prof)) == cudaSuccess ? 0 : 1;
+}
+
 extern "C" int sla_b200_diag_cols_timeline(long long* host128) {
-  return cudaMemcpyFromSymbol(host128, slab::g_bwd_ts, 128 * sizeof(long long)) == cudaSuccess ? 0 : 1;
+  return cudaMemcpyFromSymbol(host128, slab::g_bwd_ts, 256 * sizeof(long long)) == cudaSuccess ? 0 : 1;
 }

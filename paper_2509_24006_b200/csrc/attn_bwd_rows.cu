@@ -353,8 +353,9 @@ __global__ void __launch_bounds__(352, 1)
   const int* list = p.crit_idx + urow * p.Tn;
   const int np = (cnt + 1) >> 1;
   const int row0 = int(u * p.N) + i * 64;
-  const bool dbg = blockIdx.x == 100 && blockIdx.y == 6;
+  const bool dbg = blockIdx.x == SLAB_DBG_X && blockIdx.y == 6;
   ts_mark(dbg && threadIdx.x == 0, 127);
+  cta_mark(threadIdx.x == 0, 0);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -383,9 +384,22 @@ __global__ void __launch_bounds__(352, 1)
   const uint32_t tDQT = tmem, tB0 = tmem + 128, tB1 = tmem + 256;  // dQ^T (M = D); S^T|dP^T pairs
 
   if (warp == 0 || warp == 10) {
+#ifdef SLAB_TIMELINE
+    if (dbg && warp == 0 && lane == 1) {  // observer: true K / V pair arrival times
+      for (int t = 0; t < np && t < 16; ++t) {
+        tc::mbar_wait(k_full + t % L::KS, (t / L::KS) & 1);
+        g_bwd_ts[80 + t] = clock64();
+        tc::mbar_wait(v_full + t % L::VS, (t / L::VS) & 1);
+        g_bwd_ts[96 + t] = clock64();
+      }
+    }
+#endif
     // two producer warps (Q/dO + K ring, V ring): one issuing warp's TMA stream caps at ~40 B/cycle
     if (lane == 0) {
       const int pid = warp == 0 ? 0 : 1;
+#ifndef SLAB_NO_TMAP_PREFETCH
+      tc::tma_prefetch(pid == 0 ? &tmK : &tmV);
+#endif
       if (pid == 0) {
         tc::mbar_expect_tx(qdo_full, 2 * L::kT);
 #pragma unroll
@@ -412,6 +426,7 @@ __global__ void __launch_bounds__(352, 1)
         } else {
           tc::mbar_wait(v_empty + vs, ((t / L::VS) & 1) ^ 1);
           tc::mbar_expect_tx(v_full + vs, L::kP);
+          ts_mark(dbg && t < 8, 112 + t);
           uint8_t* dv = sV + vs * L::kP;
 #pragma unroll
           for (int c = 0; c < D / 64; ++c) {
@@ -422,54 +437,57 @@ __global__ void __launch_bounds__(352, 1)
       }
     }
   } else if (warp == 1) {
-    const uint32_t aQ = tc::smem_u32(sQ), aDO = tc::smem_u32(sDO), aDS = tc::smem_u32(sDS);
-    const uint32_t aK = tc::smem_u32(sK), aV = tc::smem_u32(sV);
+    // Static issue order, whole warp converged (see tc::mma_bf16_w): S^T/dP^T(0), S^T/dP^T(1),
+    // then per pair t: dQ^T(t) as soon as dS(t) is in smem (it releases K slot t), then
+    // S^T/dP^T(t+2) into the TMEM buffer the compute warps just finished with.  The tensor pipe
+    // is in order, so S/dP(t+1) runs during the softmax-gradient of t and dQ(t) right after it.
+    const uint64_t dQk = tc::desc_kmajor(tc::smem_u32(sQ)), dDOk = tc::desc_kmajor(tc::smem_u32(sDO));
+    const uint64_t dKk = tc::desc_kmajor(tc::smem_u32(sK)), dVk = tc::desc_kmajor(tc::smem_u32(sV));
+    const uint64_t dKm = tc::desc_mnmajor(tc::smem_u32(sK), 16384);
+    const uint64_t dDSm = tc::desc_mnmajor(tc::smem_u32(sDS), 16384);
     constexpr uint32_t id_st = tc::idesc_bf16(128, 64, false, false);  // pair x Q^T
     constexpr uint32_t id_dqt = tc::idesc_bf16(D, 64, true, true);     // pair^T x dS^T
-    auto kdesc = [](uint32_t base, int kk, int rows) {
-      return tc::desc_kmajor(base + (kk >> 2) * rows * 128 + (kk & 3) * 32);
-    };
+    // K-major SW128 tile of `rows` rows: k-step kk (16 elements) starts at chunk kk/4, +32 B
+    auto koff = [](int kk, int rows) { return uint32_t((kk >> 2) * rows * 128 + (kk & 3) * 32); };
     tc::mbar_wait(qdo_full, 0);
-    // dQ^T += [K_j1; K_j2]^T dS^T  (M = D, N = 64, K = 128)
-    auto issue_dq = [&](int j) {
-      const uint32_t sk = aK + (j % L::KS) * L::kP;
+    cta_mark(lane == 0, 1);
+    auto issue_sdp = [&](int t) {
+      const int ks = t % L::KS, vs = t % L::VS;
+      tc::mbar_wait(k_full + ks, (t / L::KS) & 1);
+      tc::mbar_wait(v_full + vs, (t / L::VS) & 1);
+      tc::tc_fence_after();
+      ts_mark(dbg && lane == 0 && t < 16, 16 + t);
+      const uint32_t tb = (t & 1) ? tB1 : tB0;
+      const uint64_t dk = tc::desc_add(dKk, ks * L::kP), dv = tc::desc_add(dVk, vs * L::kP);
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk)
-        tc::mma_bf16(tDQT, tc::desc_mnmajor(sk + kk * 2048, 16384), tc::desc_mnmajor(aDS + kk * 2048, 16384),
-                     id_dqt, (j | kk) != 0);
-      tc::mma_commit(k_empty + (j % L::KS));
-      tc::mma_commit(ds_empty);
-    };
-    // In-order tensor pipe: issue S^T/dP^T(t) and dQ(t-1) in whichever order their inputs
-    // arrive (dQ releases a K slot).  S/dP(t) reuses TMEM buffer t&1: free once dQ(t-2) issued.
-    if (lane == 0) {
-      int ts = 0, ta = 0;
-      while (ta < np) {
-        if (ts < np && ts <= ta + 1 && tc::mbar_test(k_full + ts % L::KS, (ts / L::KS) & 1) &&
-            tc::mbar_test(v_full + ts % L::VS, (ts / L::VS) & 1)) {
-          tc::tc_fence_after();
-          ts_mark(dbg && ts < 16, 16 + ts);
-          const int ks = ts % L::KS, vs = ts % L::VS;
-          const uint32_t tb = (ts & 1) ? tB1 : tB0;
-          const uint32_t sk = aK + ks * L::kP, sv = aV + vs * L::kP;
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            tc::mma_bf16(tb, kdesc(sk, kk, 128), kdesc(aQ, kk, 64), id_st, kk > 0);        // S^T
-            tc::mma_bf16(tb + 64, kdesc(sv, kk, 128), kdesc(aDO, kk, 64), id_st, kk > 0);  // dP^T
-          }
-          tc::mma_commit(sdp_full + (ts & 1));
-          tc::mma_commit(v_empty + vs);
-          ++ts;
-        }
-        if (ta < ts && tc::mbar_test(ds_full, ta & 1)) {
-          tc::tc_fence_after();
-          ts_mark(dbg && ta < 16, 64 + ta);
-          issue_dq(ta);
-          ++ta;
-        }
+      for (int kk = 0; kk < D / 16; ++kk) {
+        if (SLAB_DIAG_NOMMA == 1 || SLAB_DIAG_NOMMA == 2) continue;
+        tc::mma_bf16_w(tb, tc::desc_add(dk, koff(kk, 128)), tc::desc_add(dQk, koff(kk, 64)), id_st, kk > 0);
+        tc::mma_bf16_w(tb + 64, tc::desc_add(dv, koff(kk, 128)), tc::desc_add(dDOk, koff(kk, 64)), id_st, kk > 0);
       }
-      tc::mma_commit(dq_done);
+      tc::mma_commit_w(sdp_full + (t & 1));
+      tc::mma_commit_w(v_empty + vs);
+      ts_mark(dbg && lane == 0 && t < 16, 208 + t);
+    };
+    if (np > 0) issue_sdp(0);
+    if (np > 1) issue_sdp(1);
+    for (int t = 0; t < np; ++t) {
+      // dQ^T += [K_j1; K_j2]^T dS^T  (M = D, N = 64, K = 128)
+      tc::mbar_wait(ds_full, t & 1);
+      tc::tc_fence_after();
+      ts_mark(dbg && lane == 0 && t < 16, 64 + t);
+      const uint64_t dk = tc::desc_add(dKm, (t % L::KS) * L::kP);
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk) {
+        if (SLAB_DIAG_NOMMA == 1 || SLAB_DIAG_NOMMA == 3) continue;
+        tc::mma_bf16_w(tDQT, tc::desc_add(dk, kk * 2048), tc::desc_add(dDSm, kk * 2048), id_dqt, (t | kk) != 0);
+      }
+      tc::mma_commit_w(k_empty + (t % L::KS));
+      tc::mma_commit_w(ds_empty);
+      ts_mark(dbg && lane == 0 && t < 16, 224 + t);
+      if (t + 2 < np) issue_sdp(t + 2);
     }
+    tc::mma_commit_w(dq_done);
     __syncwarp();
   } else {
     const int q4 = warp & 3;
@@ -485,6 +503,7 @@ __global__ void __launch_bounds__(352, 1)
       tc::mbar_wait(sdp_full + (t & 1), (t >> 1) & 1);
       tc::tc_fence_after();
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 32 + t);
+      ts_mark(dbg && lane == 0 && t >= 4 && t < 8, 192 + 8 * (t - 4) + (warp - 2));
       const bool live = c < 64 || 2 * t + 1 < cnt;
       const uint32_t tb = ((t & 1) ? tB1 : tB0) + lane_base + 32 * grp;
       uint32_t pk[16];
@@ -495,6 +514,10 @@ __global__ void __launch_bounds__(352, 1)
         tc::tmem_ld_wait();
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
+          if (SLAB_DIAG_NOMMA == 4) {
+            pk[e >> 1] = sv[e] ^ dp[e];
+            continue;
+          }
           const int rr = 32 * grp + e;
           const float p0 = ex2f(__uint_as_float(sv[e]) * p.scale_log2 - s_lse2[rr]);
           const float p1 = ex2f(__uint_as_float(sv[e + 1]) * p.scale_log2 - s_lse2[rr + 1]);
@@ -503,7 +526,9 @@ __global__ void __launch_bounds__(352, 1)
           pk[e >> 1] = tc::pack_bf16(d0, d1);
         }
       }
+      ts_mark(dbg && threadIdx.x == 64 && t < 16, 128 + t);
       if (t >= 1) tc::mbar_wait(ds_empty, (t - 1) & 1);  // dQ of the previous pair has read dS
+      ts_mark(dbg && threadIdx.x == 64 && t < 16, 144 + t);
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch)
         *reinterpret_cast<uint4*>(sDS + tc::sw128_off(c, 4 * grp + ch)) =
@@ -513,6 +538,7 @@ __global__ void __launch_bounds__(352, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(ds_full);
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 48 + t);
+      ts_mark(dbg && lane == 0 && t >= 4 && t < 8, 160 + 8 * (t - 4) + (warp - 2));
     }
     // dq_total = J_phi(q)^T dQ^phi + dQ: transpose dQ^T through smem (the K ring is idle once
     // dq_done fired), then finish row-wise with 4 threads per query row.  For the softmax
@@ -521,6 +547,7 @@ __global__ void __launch_bounds__(352, 1)
     tc::mbar_wait(dq_done, 0);
     tc::tc_fence_after();
     ts_mark(dbg && threadIdx.x == 64, 120);
+    cta_mark(threadIdx.x == 64, 2);
     constexpr int TP = D + 1;  // with the chunk rotation below: conflict-free row-wise reads
     float* tq = reinterpret_cast<float*>(sK);
     {
@@ -587,6 +614,7 @@ __global__ void __launch_bounds__(352, 1)
       }
     }
     ts_mark(dbg && threadIdx.x == 64, 124);
+    cta_mark(threadIdx.x == 64, 3);
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -669,6 +697,10 @@ void launch_bwd_rows(const Dims& Dm, const void* q, const void* k, const void* v
 
 }  // namespace slab
 
+extern "C" int sla_b200_diag_rows_ctaprof(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, slab::g_cta_prof, sizeof(slab::g_cta_prof)) == cudaSuccess ? 0 : 1;
+}
+
 extern "C" int sla_b200_diag_bwd_timeline(long long* host128) {
-  return cudaMemcpyFromSymbol(host128, slab::g_bwd_ts, 128 * sizeof(long long)) == cudaSuccess ? 0 : 1;
+  return cudaMemcpyFromSymbol(host128, slab::g_bwd_ts, 256 * sizeof(long long)) == cudaSuccess ? 0 : 1;
 }

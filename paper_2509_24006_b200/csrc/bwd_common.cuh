@@ -4,16 +4,45 @@
 #include "kernels.hpp"
 #include "tc.cuh"
 
+#ifndef SLAB_DIAG_NOMMA
+#define SLAB_DIAG_NOMMA 0  // timing experiment only: skip the rows-pass MMAs
+#endif
+#ifndef SLAB_DBG_X
+#define SLAB_DBG_X 100  // -DSLAB_TIMELINE: key/query block of the traced CTA (unit 6)
+#endif
+#ifndef SLAB_POLL_NS
+#define SLAB_POLL_NS 0  // MMA-issuer back-off between idle barrier polls (ns)
+#endif
+
 namespace slab {
 
 // debug timeline of one CTA (-DSLAB_TIMELINE; read by sla_b200_diag_bwd_timeline in attn_bwd_rows.cu)
-static __device__ long long g_bwd_ts[128];
+static __device__ long long g_bwd_ts[256];
+// -DSLAB_TIMELINE: per-CTA phase clocks [cta][start, loop start, loop end, end | smid << 56]
+static __device__ unsigned long long g_cta_prof[8192][4];
 
 namespace {
 
 __device__ __forceinline__ void ts_mark(bool on, int slot) {  // -DSLAB_TIMELINE builds only
 #ifdef SLAB_TIMELINE
   if (on) g_bwd_ts[slot] = clock64();
+#else
+  (void)on;
+  (void)slot;
+#endif
+}
+
+__device__ __forceinline__ void cta_mark(bool on, int slot) {  // -DSLAB_TIMELINE builds only
+#ifdef SLAB_TIMELINE
+  if (on) {
+    unsigned long long v = clock64();
+    if (slot == 3) {
+      uint32_t sm;
+      asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
+      v |= (unsigned long long)sm << 56;
+    }
+    g_cta_prof[(blockIdx.y * gridDim.x + blockIdx.x) & 8191][slot] = v;
+  }
 #else
   (void)on;
   (void)slot;

@@ -1,3 +1,4 @@
+#include <type_traits>
 // diag.cu -- diagnostics used by tests/test_gpu_tmem.py to pin TMEM data-path layouts that the
 // kernels rely on: (1) the thread <-> (lane, column) map of tcgen05.ld.16x32bx2, and (2) that
 // an M=64 MMA whose D address carries lane offset 16 fills lanes 16-31 of each quarter.
@@ -157,13 +158,40 @@ __global__ void k_diag_mma_rate(int m, int n, int a_mn, int b_mn, int reps, long
   tc::tc_fence_after();
   if (threadIdx.x == 0) {
     const uint32_t a = tc::smem_u32(sm), b = a + 128 * 128;
-    const uint32_t id = tc::idesc_bf16(m, n, a_mn != 0, b_mn != 0);
+    const uint32_t id = tc::idesc_bf16(m, n, a_mn == 1, b_mn != 0 && a_mn < 3);
     const long long t0 = clock64();
-    for (int r = 0; r < reps; ++r) {
-      const int kk = r & 3;
-      const uint64_t da = a_mn ? tc::desc_mnmajor(a + kk * 2048, 8192) : tc::desc_kmajor(a + kk * 32);
-      const uint64_t db = b_mn ? tc::desc_mnmajor(b + kk * 2048, 8192) : tc::desc_kmajor(b + kk * 32);
-      tc::mma_bf16(slot, da, db, id, r > 0);
+    if (a_mn == 2) {  // A from TMEM (ts form): M lanes x 16 bf16 (8 columns) at column 256 + 8 kk
+      for (int r = 0; r < reps; ++r) {
+        const int kk = r & 3;
+        const uint64_t db = b_mn ? tc::desc_mnmajor(b + kk * 2048, 8192) : tc::desc_kmajor(b + kk * 32);
+        tc::mma_bf16_ts(slot, slot + 256 + 8 * kk, db, id, r > 0);
+      }
+    } else if (a_mn >= 3) {  // SS, K-major, round-robin over (a_mn - 2) accumulators 128 columns apart
+      uint64_t da[4], db[4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        da[kk] = tc::desc_kmajor(a + kk * 32);
+        db[kk] = tc::desc_kmajor(b + kk * 32);
+      }
+      auto run = [&](auto nacc_c) {
+        constexpr int NA = decltype(nacc_c)::value;
+        for (int r = 0; r < reps; r += 4 * NA) {
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+#pragma unroll
+            for (int q = 0; q < NA; ++q) tc::mma_bf16(slot + 128 * q, da[kk], db[kk], id, (r | kk) != 0);
+        }
+      };
+      if (a_mn == 3) run(std::integral_constant<int, 1>{});
+      else if (a_mn == 4) run(std::integral_constant<int, 2>{});
+      else run(std::integral_constant<int, 4>{});
+    } else {
+      for (int r = 0; r < reps; ++r) {
+        const int kk = r & 3;
+        const uint64_t db = b_mn ? tc::desc_mnmajor(b + kk * 2048, 8192) : tc::desc_kmajor(b + kk * 32);
+        const uint64_t da = a_mn ? tc::desc_mnmajor(a + kk * 2048, 8192) : tc::desc_kmajor(a + kk * 32);
+        tc::mma_bf16(slot, da, db, id, r > 0);
+      }
     }
     tc::mma_commit(&bar);
     tc::mbar_wait(&bar, 0);
@@ -321,6 +349,195 @@ extern "C" int sla_b200_diag_mma_tma(const void* buf, int rows, int ctas, int m,
     const int bytes = (128 + 256) * 128 + 4 * 16384 + 1024;
     cudaFuncSetAttribute(slab::k_diag_mma_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     slab::k_diag_mma_tma<<<ctas, 64, bytes>>>(tm, rows, m, n, reps, tma_on, d);
+    int rc = cudaMemcpy(host2, d, sizeof(long long) * 2 * ctas, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 1;
+    cudaFree(d);
+    return rc;
+  } catch (...) {
+    return 1;
+  }
+}
+
+// (6) TMA load latency: each producer warp (lane 0) loads one item of `boxes` 8 KB SW128 boxes
+// (random 64-row blocks, both 64-column halves) and waits for it before issuing the next, so
+// cycles / item is the issue-to-complete latency of a ring slot of that size.
+namespace slab {
+namespace {
+__global__ void k_diag_tma_lat(const __grid_constant__ CUtensorMap tm, int rows, int boxes, int iters,
+                               int producers, long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bars[8];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < 8; ++s) tc::mbar_init(bars + s, 1);
+    tc::fence_barrier_init();
+  }
+  __syncthreads();
+  const int pw = threadIdx.x >> 5;
+  if ((threadIdx.x & 31) == 0 && pw < producers) {
+    uint8_t* dst = sm + pw * boxes * 8192;
+    uint32_t x = 12345u + 7919u * blockIdx.x + 104729u * pw;
+    const int tiles = rows / 64;
+    const long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+      tc::mbar_expect_tx(bars + pw, boxes * 8192);
+      for (int b = 0; b < boxes; b += 2) {
+        x = x * 1664525u + 1013904223u;
+        const int row = int((x >> 8) % uint32_t(tiles)) * 64;
+        tc::tma_load_3d(dst + b * 8192, &tm, bars + pw, 0, row, 0);
+        tc::tma_load_3d(dst + (b + 1) * 8192, &tm, bars + pw, 64, row, 0);
+      }
+      tc::mbar_wait(bars + pw, it & 1);
+    }
+    out[blockIdx.x * 8 + pw] = clock64() - t0;
+  }
+}
+}  // namespace
+}  // namespace slab
+
+extern "C" int sla_b200_diag_tma_lat(const void* buf, int rows, int ctas, int boxes, int iters,
+                                     int producers, long long* host_cycles) {
+  try {
+    CUtensorMap tm;
+    slab::make_tmap_bf16(&tm, buf, 128, uint64_t(rows), 1, 128, 0, 64);
+    long long* d = nullptr;
+    if (cudaMalloc(&d, sizeof(long long) * 8 * ctas) != cudaSuccess) return 1;
+    const int bytes = producers * boxes * 8192 + 1024;
+    cudaFuncSetAttribute(slab::k_diag_tma_lat, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    slab::k_diag_tma_lat<<<ctas, 32 * producers, bytes>>>(tm, rows, boxes, iters, producers, d);
+    int rc = cudaMemcpy(host_cycles, d, sizeof(long long) * 8 * ctas, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 1;
+    cudaFree(d);
+    return rc;
+  } catch (...) {
+    return 1;
+  }
+}
+
+// (7) what slows TMA inside the backward kernels: two producer warps each load 32 KB items
+// (one in flight, so cycles / item = latency) while, per `mode` bit, (1) one thread streams
+// M=128 N=64 SS MMAs over distinct smem tiles, (2) 8 warps loop tcgen05.ld + exp + st.shared +
+// fence.proxy.async (the softmax-gradient phase), (4) those warps skip the proxy fence.
+namespace slab {
+namespace {
+__global__ void __launch_bounds__(352, 1)
+    k_diag_contention(const __grid_constant__ CUtensorMap tm, int rows, int iters, int mode, long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* ld = sm;                 // 2 x 32 KB TMA destinations
+  uint8_t* ops = sm + 65536;        // 96 KB MMA operand tiles
+  uint8_t* pd = sm + 65536 + 98304; // 32 KB generic-proxy stores
+  __shared__ uint64_t bars[2], mbar, mb2[2];
+  __shared__ uint32_t slot;
+  __shared__ volatile int stop;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    stop = 0;
+    tc::mbar_init(bars, 1);
+    tc::mbar_init(bars + 1, 1);
+    tc::mbar_init(&mbar, 1);
+    tc::mbar_init(mb2, 1);
+    tc::mbar_init(mb2 + 1, 1);
+    tc::fence_barrier_init();
+  }
+  if (warp == 2) tc::tmem_alloc<512>(&slot);
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  if (warp < 2) {
+    if (lane == 0) {
+      uint32_t x = 12345u + 7919u * blockIdx.x + 104729u * warp;
+      const int tiles = rows / 64;
+      const long long t0 = clock64();
+      for (int it = 0; it < iters; ++it) {
+        tc::mbar_expect_tx(bars + warp, 32768);
+        for (int b = 0; b < 4; b += 2) {
+          x = x * 1664525u + 1013904223u;
+          const int row = int((x >> 8) % uint32_t(tiles)) * 64;
+          tc::tma_load_3d(ld + warp * 32768 + b * 8192, &tm, bars + warp, 0, row, 0);
+          tc::tma_load_3d(ld + warp * 32768 + (b + 1) * 8192, &tm, bars + warp, 64, row, 0);
+        }
+        tc::mbar_wait(bars + warp, it & 1);
+      }
+      out[blockIdx.x * 2 + warp] = clock64() - t0;
+    }
+    __syncwarp();
+  } else if (warp == 2) {
+    if (lane == 0 && (mode & 1)) {
+      const uint32_t a = tc::smem_u32(ops);
+      constexpr uint32_t id = tc::idesc_bf16(128, 64, false, false);
+      constexpr uint32_t id_mn = tc::idesc_bf16(128, 64, true, true);
+      int r = 0;
+      while (!stop) {
+        if (mode & 16) {  // dQ^T-like: both operands MN-major
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            tc::mma_bf16(slot + 128 * (kk & 1), tc::desc_mnmajor(a + (r % 3) * 32768 + kk * 2048, 16384),
+                         tc::desc_mnmajor(a + ((r + 1) % 3) * 32768 + kk * 2048, 16384), id_mn, kk > 1);
+        } else {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t base = a + ((r + kk) % 3) * 32768;
+            tc::mma_bf16(slot + 128 * (kk & 1), tc::desc_kmajor(base + (kk >> 2) * 16384 + (kk & 3) * 32),
+                         tc::desc_kmajor(base + 24576 + (kk & 3) * 32), id, kk > 1);
+          }
+        }
+        if (mode & 8) {  // keep the pipe full: wait for the group before the previous one
+          tc::mma_commit(mb2 + (r & 1));
+          if (r >= 1) tc::mbar_wait(mb2 + ((r - 1) & 1), ((r - 1) >> 1) & 1);
+        } else {
+          tc::mma_commit(&mbar);
+          tc::mbar_wait(&mbar, r & 1);
+        }
+        ++r;
+      }
+      if (mode & 8) tc::mbar_wait(mb2 + ((r - 1) & 1), ((r - 1) >> 1) & 1);
+    }
+  } else if (mode & 2) {
+    const int q4 = warp & 3, grp = (warp - 3) >> 2;
+    const uint32_t lane_base = uint32_t(32 * q4) << 16;
+    const int rq = 32 * q4 + lane;
+    while (!stop) {
+      uint32_t sv[32], pp[16];
+      tc::tmem_ld32(slot + 256 + lane_base + 32 * (grp & 1), sv);
+      tc::tmem_ld_wait();
+#pragma unroll
+      for (int e = 0; e < 32; e += 2) {
+        float p0, p1;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p0) : "f"(__uint_as_float(sv[e]) * 0.01f - 1.f));
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(p1) : "f"(__uint_as_float(sv[e + 1]) * 0.01f - 1.f));
+        pp[e >> 1] = tc::pack_bf16(p0, p1);
+      }
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch)
+        *reinterpret_cast<uint4*>(pd + (grp & 1) * 16384 + tc::sw128_off(rq, 4 * (grp >> 1) + ch)) =
+            make_uint4(pp[4 * ch], pp[4 * ch + 1], pp[4 * ch + 2], pp[4 * ch + 3]);
+      if (!(mode & 4)) tc::fence_proxy_async();
+      __syncwarp();
+    }
+  }
+  if (threadIdx.x == 0) {
+    // producers finished (thread 0 is producer 0); wait for producer 1 via its output slot
+    while (out[blockIdx.x * 2 + 1] == 0) {
+    }
+    stop = 1;
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) tc::tmem_dealloc<512>(slot);
+}
+}  // namespace
+}  // namespace slab
+
+extern "C" int sla_b200_diag_contention(const void* buf, int rows, int ctas, int iters, int mode,
+                                        long long* host2) {
+  try {
+    CUtensorMap tm;
+    slab::make_tmap_bf16(&tm, buf, 128, uint64_t(rows), 1, 128, 0, 64);
+    long long* d = nullptr;
+    if (cudaMalloc(&d, sizeof(long long) * 2 * ctas) != cudaSuccess) return 1;
+    cudaMemset(d, 0, sizeof(long long) * 2 * ctas);
+    const int bytes = 65536 + 98304 + 32768 + 1024;
+    cudaFuncSetAttribute(slab::k_diag_contention, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    slab::k_diag_contention<<<ctas, 352, bytes>>>(tm, rows, iters, mode, d);
     int rc = cudaMemcpy(host2, d, sizeof(long long) * 2 * ctas, cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 1;
     cudaFree(d);
     return rc;

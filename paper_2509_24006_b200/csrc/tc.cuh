@@ -173,6 +173,32 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
       : "memory");
 }
 
+// Warp-converged issue: every lane of the MMA warp runs the schedule, so descriptors and TMEM
+// addresses are warp-uniform and stay in uniform registers (no per-MMA R2UR); one elected lane
+// (always lane 0 with a full mask, so commits track the same thread's MMAs) executes the op.
+// A lane-0-only issue loop costs ~70-80 cycles per MMA in R2UR round trips, more than the
+// 50-cycle M=128/N=64 MMA itself.
+__device__ __forceinline__ void mma_bf16_w(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                           uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p, e;\n .reg .b32 rx;\n setp.ne.b32 p, %4, 0;\n"
+      " elect.sync rx|e, 0xffffffff;\n"
+      " @e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_w(uint64_t* bar) {
+  asm volatile(
+      "{\n .reg .pred e;\n .reg .b32 rx;\n elect.sync rx|e, 0xffffffff;\n"
+      " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+// descriptor of the same tile `bytes` further on (start address field, no carry: smem < 256 KB)
+__device__ __forceinline__ uint64_t desc_add(uint64_t desc, uint32_t bytes) {
+  return desc + uint64_t(bytes >> 4);
+}
+
 // ---- TMEM <-> registers (32 lanes x 32 bit, 32 / 16 consecutive columns) ----------------
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
