@@ -35,8 +35,14 @@ struct ColsLayout {
   static_assert(kBytes <= 232448, "smem");
 };
 
+#ifndef SLAB_COLS_PROD
+#define SLAB_COLS_PROD 2
+#endif
+constexpr int kColsProd = SLAB_COLS_PROD;  // TMA producer warps (2 or 4)
+constexpr int kColsThreads = 32 * (10 + kColsProd - 1);
+
 template <int D>
-__global__ void __launch_bounds__(352, 1)
+__global__ void __launch_bounds__(kColsThreads, 1)
     k_bwd_cols(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
                const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                const __grid_constant__ CUtensorMap tmHa, BwdParams p) {
@@ -90,7 +96,7 @@ __global__ void __launch_bounds__(352, 1)
     if (lane == 0) {
       tc::mbar_init(kv_full, 1);
       for (int s = 0; s < RS; ++s) {
-        tc::mbar_init(ring_full + s, 2);  // one arrive.expect_tx per producer warp
+        tc::mbar_init(ring_full + s, kColsProd);  // one arrive.expect_tx per producer warp
         tc::mbar_init(ring_empty + s, 1);
       }
       for (int s = 0; s < 2; ++s) {
@@ -114,11 +120,13 @@ __global__ void __launch_bounds__(352, 1)
   // dK^phi^T at [384, 448) (M = D)
   const uint32_t tDVT = tmem, tDKT = tmem + 64, tB0 = tmem + 128, tB1 = tmem + 256, tKPT = tmem + 384;
 
-  if (warp == 0 || warp == 10) {
+  if (warp == 0 || warp >= 10) {
     // No L2 prefetch of the column's Q / dO tiles: prefetches queue in the TMA unit ahead of
     // the ring loads, and a wave's columns share one unit's Q / dO, which stays L2-resident.
+    // kColsProd producer warps fill each stage (TMA issue from one warp caps at ~40 B/cycle):
+    // pid&1 selects Q / dO, with 4 producers pid>>1 selects the pair's first / second block.
     if (lane == 0) {
-      const int pid = warp == 0 ? 0 : 1;  // 0: K/V + Q pairs + even dH_agg chunks; 1: dO pairs + odd chunks
+      const int pid = warp == 0 ? 0 : warp - 9;  // pid 0 also loads K_j / V_j
 #ifndef SLAB_NO_TMAP_PREFETCH
       tc::tma_prefetch(pid == 0 ? &tmQ : &tmDO);
 #endif
@@ -137,26 +145,25 @@ __global__ void __launch_bounds__(352, 1)
         tc::mbar_expect_tx(ring_full + s, bytes);
         return sRing + s * L::kStage;
       };
-      const CUtensorMap* tm = pid == 0 ? &tmQ : &tmDO;
+      const CUtensorMap* tm = (pid & 1) ? &tmDO : &tmQ;
       for (int pp = 0; pp < np; ++pp) {
         const int r1 = int(u * p.N) + list[2 * pp] * 64;
         const int r2 = int(u * p.N) + list[min(2 * pp + 1, cnt - 1)] * 64;
-        uint8_t* dst = acquire(L::kP) + pid * L::kP;
+        uint8_t* dst = acquire(kColsProd == 2 ? L::kP : L::kP / 2) + (pid & 1) * L::kP;
         ts_mark(dbg && pid == 0 && pp < 16, pp);
         uint64_t* fb = ring_full + (item % RS);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
-          tc::tma_load_3d(dst + c * 16384, tm, fb, 64 * c, r1, 0);
-          tc::tma_load_3d(dst + c * 16384 + 8192, tm, fb, 64 * c, r2, 0);
+          if (kColsProd == 2 || pid < 2) tc::tma_load_3d(dst + c * 16384, tm, fb, 64 * c, r1, 0);
+          if (kColsProd == 2 || pid >= 2) tc::tma_load_3d(dst + c * 16384 + 8192, tm, fb, 64 * c, r2, 0);
         }
         ++item;
       }
-      if (has_lin) {
+      if (has_lin) {  // dH_agg chunk c by producer c (D / 64 <= 2 chunks)
         constexpr int NC = D / 64;
-        const int mine = pid == 0 ? (NC + 1) / 2 : NC / 2;  // chunks c with c % 2 == pid
-        uint8_t* dst = acquire(mine * D * 128);
-        for (int c = pid; c < NC; c += 2)
-          tc::tma_load_3d(dst + c * D * 128, &tmHa, ring_full + (item % RS), 64 * c, int(ucol * D), 0);
+        uint8_t* dst = acquire(pid < NC ? D * 128 : 0);
+        if (pid < NC)
+          tc::tma_load_3d(dst + pid * D * 128, &tmHa, ring_full + (item % RS), 64 * pid, int(ucol * D), 0);
         ++item;
       }
     }
@@ -181,66 +188,49 @@ __global__ void __launch_bounds__(352, 1)
     tc::tc_fence_after();
     ts_mark(dbg && lane == 0, 125);
     cta_mark(lane == 0, 1);
+    // Whole warp runs the issue loop (warp-uniform operands, one elected lane issues; see
+    // tc::mma_bf16_w).  Descriptors: ring stage s at +s*kStage, k-step kk at +koff / +kk*2048.
+    const uint64_t dRk = tc::desc_kmajor(aR), dKk = tc::desc_kmajor(aK), dVk = tc::desc_kmajor(aV);
+    const uint64_t dRm = tc::desc_mnmajor(aR, 16384), dPDm = tc::desc_mnmajor(aPD, 16384);
+    auto koff = [](int kk, int rows) { return uint32_t((kk >> 2) * rows * 128 + (kk & 3) * 32); };
     auto issue_acc = [&](int t) {  // dV^T += dO_pair^T P, dK^T += Q_pair^T dS  (M = D, K = 128)
       tc::tc_fence_after();
-      const uint32_t sq = aR + (t % RS) * L::kStage;
-      {
-        const uint32_t sp = aPD + (t & 1) * 32768, sd = sp + 16384;
+      const uint64_t dq = tc::desc_add(dRm, (t % RS) * L::kStage), ddo = tc::desc_add(dq, L::kP);
+      const uint64_t dp = tc::desc_add(dPDm, (t & 1) * 32768), dd = tc::desc_add(dp, 16384);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          tc::mma_bf16(tDVT, tc::desc_mnmajor(sq + L::kP + kk * 2048, 16384), tc::desc_mnmajor(sp + kk * 2048, 16384),
-                       id_acc, (t | kk) != 0);
-          tc::mma_bf16(tDKT, tc::desc_mnmajor(sq + kk * 2048, 16384), tc::desc_mnmajor(sd + kk * 2048, 16384),
-                       id_acc, (t | kk) != 0);
-        }
-        tc::mma_commit(ring_empty + (t % RS));
-        tc::mma_commit(pd_empty + (t & 1));
+      for (int kk = 0; kk < 8; ++kk) {
+        tc::mma_bf16_w(tDVT, tc::desc_add(ddo, kk * 2048), tc::desc_add(dp, kk * 2048), id_acc, (t | kk) != 0);
+        tc::mma_bf16_w(tDKT, tc::desc_add(dq, kk * 2048), tc::desc_add(dd, kk * 2048), id_acc, (t | kk) != 0);
       }
+      tc::mma_commit_w(ring_empty + (t % RS));
+      tc::mma_commit_w(pd_empty + (t & 1));
     };
     // The tensor pipe executes in issue order, so S/dP(t+1) and acc(t) are issued in whichever
     // order their inputs become ready: acc(t) releases a ring stage, S/dP(t+1) feeds the compute
     // warps.  S/dP(t) reuses TMEM buffer t&1, free once acc(t-2) was issued (pd_full(t-2) seen).
-    if (lane == 0) {
+    // Barrier probes are warp votes so every lane takes the same branch.
+    {
       int ts = 0, ta = 0;
-      uint32_t seen_k = 0, seen_v = 0;
-      (void)seen_k;
-      (void)seen_v;
       while (ta < np) {
-        bool progressed = false;
-        (void)progressed;
-#ifdef SLAB_TIMELINE
-        if (dbg && ts < 16 && ts < np && !(seen_k >> ts & 1) && tc::mbar_test(ring_full + ts % RS, (ts / RS) & 1)) {
-          g_bwd_ts[80 + ts] = clock64();
-          seen_k |= 1u << ts;
-        }
-        if (dbg && ta < 16 && ta < ts && !(seen_v >> ta & 1) && tc::mbar_test(pd_full + (ta & 1), (ta >> 1) & 1)) {
-          g_bwd_ts[96 + ta] = clock64();
-          seen_v |= 1u << ta;
-        }
-#endif
-        if (ts < np && ts <= ta + 1 && tc::mbar_test(ring_full + ts % RS, (ts / RS) & 1)) {
+        if (ts < np && ts <= ta + 1 && __all_sync(0xffffffffu, tc::mbar_test(ring_full + ts % RS, (ts / RS) & 1))) {
           tc::tc_fence_after();
-          ts_mark(dbg && ts < 16, 16 + ts);
-          const uint32_t sq = aR + (ts % RS) * L::kStage;
+          ts_mark(dbg && lane == 0 && ts < 16, 16 + ts);
+          const uint64_t dq = tc::desc_add(dRk, (ts % RS) * L::kStage), ddo = tc::desc_add(dq, L::kP);
           const uint32_t tb = (ts & 1) ? tB1 : tB0;
 #pragma unroll
           for (int kk = 0; kk < D / 16; ++kk) {
-            tc::mma_bf16(tb, kdesc(sq, kk, 128), kdesc(aK, kk, 64), id_s, kk > 0);               // S
-            tc::mma_bf16(tb + 64, kdesc(sq + L::kP, kk, 128), kdesc(aV, kk, 64), id_s, kk > 0);  // dP
+            tc::mma_bf16_w(tb, tc::desc_add(dq, koff(kk, 128)), tc::desc_add(dKk, koff(kk, 64)), id_s, kk > 0);        // S
+            tc::mma_bf16_w(tb + 64, tc::desc_add(ddo, koff(kk, 128)), tc::desc_add(dVk, koff(kk, 64)), id_s, kk > 0);  // dP
           }
-          tc::mma_commit(sdp_full + (ts & 1));
+          tc::mma_commit_w(sdp_full + (ts & 1));
           ++ts;
-          progressed = true;
         }
-        if (ta < ts && tc::mbar_test(pd_full + (ta & 1), (ta >> 1) & 1)) {
+        if (ta < ts && __all_sync(0xffffffffu, tc::mbar_test(pd_full + (ta & 1), (ta >> 1) & 1))) {
           issue_acc(ta);
           ++ta;
         }
-#if SLAB_POLL_NS > 0
-        else if (!progressed) __nanosleep(SLAB_POLL_NS);
-#endif
       }
-      tc::mma_commit(acc_done);
+      tc::mma_commit_w(acc_done);
     }
     item = np;
     __syncwarp();
@@ -248,17 +238,15 @@ __global__ void __launch_bounds__(352, 1)
       const uint32_t sh = wait_item();
       tc::mbar_wait(kf_ready, 0);
       tc::tc_fence_after();
-      if (lane == 0) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          // dK^phi^T raw = dH_agg V^T (M = D over a, N = 64 keys, K = D over b)
-          tc::mma_bf16(tKPT, kdesc(sh, kk, D), kdesc(aV, kk, 64), id_kp, kk > 0);
-          // dV^T += dH_agg^T phi(K)^T (M = D over b, N = 64 keys, K = D over a)
-          tc::mma_bf16(tDVT, tc::desc_mnmajor(sh + kk * 2048, D * 128), kdesc(aKF, kk, 64), id_vl,
+      for (int kk = 0; kk < D / 16; ++kk) {
+        // dK^phi^T raw = dH_agg V^T (M = D over a, N = 64 keys, K = D over b)
+        tc::mma_bf16_w(tKPT, kdesc(sh, kk, D), kdesc(aV, kk, 64), id_kp, kk > 0);
+        // dV^T += dH_agg^T phi(K)^T (M = D over b, N = 64 keys, K = D over a)
+        tc::mma_bf16_w(tDVT, tc::desc_mnmajor(sh + kk * 2048, D * 128), kdesc(aKF, kk, 64), id_vl,
                        (np > 0 || kk > 0) ? 1u : 0u);
-        }
-        tc::mma_commit(ring_empty + (item % RS));
       }
+      tc::mma_commit_w(ring_empty + (item % RS));
       __syncwarp();
       ++item;
     }
@@ -389,35 +377,51 @@ __global__ void __launch_bounds__(352, 1)
     named_sync(1, 256);
     ts_mark(dbg && threadIdx.x == 64, 123);
     // ---- dk_total = J_phi(k)^T (dK^phi + dZ_agg) + dK ; dv  (row-wise, 4 threads per row)
+    // Thread (c, sub) owns 32 columns, visited in a per-sub rotated chunk order (conflict-free
+    // reads of the transposed tiles); K, phi(K) and g = dK^phi + dZ_agg stay in registers.
     const int sub = tid & 3;
-    auto rot = [&](int cc) { return (cc + 8 * sub) & (D / 4 - 1); };  // chunk order per thread
-    float dot = 0.f;
-    if (p.phi == 2 && has_lin) {
+    auto rot = [&](int cc) { return (cc + 8 * sub) & (D / 4 - 1); };
+    constexpr int DQ = D / 4;
+    float kx[DQ], g[DQ];
 #pragma unroll
-      for (int cc0 = 0; cc0 < D / 4; cc0 += 8) {
-        const int cc = rot(cc0);
-        float f[8];
-        unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, c0 + cc)), f);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) dot = fmaf(phi_of(f[e]), tkp[c * TP + c0 + cc + e] + zas[c0 + cc + e], dot);
-      }
-      dot += __shfl_xor_sync(0xffffffffu, dot, 1);
-      dot += __shfl_xor_sync(0xffffffffu, dot, 2);
-    }
-    const long long grow = (long long)kv0 + c;
-#pragma unroll
-    for (int cc0 = 0; cc0 < D / 4; cc0 += 8) {
+    for (int cc0 = 0; cc0 < DQ; cc0 += 8) {
       const int col = c0 + rot(cc0);
-      float f[8], o[8], w8[8];
+      float f[8];
       unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, col)), f);
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const float g = has_lin ? tkp[c * TP + col + e] + zas[col + e] : 0.f;
-        float jg;
-        if (p.phi == 2) jg = phi_of(f[e]) * (g - dot);
-        else if (p.phi == 0) jg = f[e] >= 0.f ? g : __expf(f[e]) * g;
-        else jg = f[e] > 0.f ? g : 0.f;
-        o[e] = jg + tk[c * TP + col + e];
+        kx[cc0 + e] = f[e];
+        g[cc0 + e] = has_lin ? tkp[c * TP + col + e] + zas[col + e] : 0.f;
+      }
+    }
+    const long long grow = (long long)kv0 + c;
+    float jg[DQ];
+    if (p.phi == 2) {  // J^T g = phi * (g - <phi, g>)
+      float dot = 0.f;
+#pragma unroll
+      for (int e = 0; e < DQ; ++e) {
+        kx[e] = __expf(kx[e] - mx) * inv;
+        dot = fmaf(kx[e], g[e], dot);
+      }
+      dot += __shfl_xor_sync(0xffffffffu, dot, 1);
+      dot += __shfl_xor_sync(0xffffffffu, dot, 2);
+#pragma unroll
+      for (int e = 0; e < DQ; ++e) jg[e] = kx[e] * (g[e] - dot);
+    } else if (p.phi == 0) {
+#pragma unroll
+      for (int e = 0; e < DQ; ++e) jg[e] = kx[e] >= 0.f ? g[e] : __expf(kx[e]) * g[e];
+    } else {
+#pragma unroll
+      for (int e = 0; e < DQ; ++e) jg[e] = kx[e] > 0.f ? g[e] : 0.f;
+    }
+    ts_mark(dbg && threadIdx.x == 64, 118);
+#pragma unroll
+    for (int cc0 = 0; cc0 < DQ; cc0 += 8) {
+      const int col = c0 + rot(cc0);
+      float o[8], w8[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        o[e] = jg[cc0 + e] + tk[c * TP + col + e];
         w8[e] = tv[c * TP + col + e];
       }
       *reinterpret_cast<uint4*>(p.dk + grow * D + col) = pack8(o);
@@ -443,7 +447,7 @@ void launch_cols_t(const Dims& Dm, const void* q, const void* k, const void* v, 
   make_tmap_bf16(&th, Ha, D, uint64_t(Dm.U) * Dm.Tn * D, 1, D, 0, D);
   auto kern = k_bwd_cols<D>;
   SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ColsLayout<D>::kBytes));
-  kern<<<dim3(Dm.Tn, unsigned(Dm.U)), 352, ColsLayout<D>::kBytes, st>>>(tq, tdo, tk, tv, th, p);
+  kern<<<dim3(Dm.Tn, unsigned(Dm.U)), kColsThreads, ColsLayout<D>::kBytes, st>>>(tq, tdo, tk, tv, th, p);
   check_launch("k_bwd_cols", st);
 }
 

@@ -59,6 +59,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
   }
 }
 
+// warp-converged wait: the exit condition is a warp vote, so the compiler can keep values
+// computed after it (descriptors, TMEM addresses) in uniform registers
+__device__ __forceinline__ void mbar_wait_w(uint64_t* bar, uint32_t phase) {
+  const uint32_t a = smem_u32(bar);
+  while (!__all_sync(0xffffffffu, mbar_try_wait(a, phase))) {
+  }
+}
+
 // generic-proxy smem writes -> visible to the async proxy (tensor core / TMA)
 __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");

@@ -39,7 +39,7 @@ for name, fn, cols in (("rows", L.sla_b200_diag_bwd_timeline, [("ldK", 0), ("ldV
     assert fn(buf) == 0
     t = np.frombuffer(buf, dtype=np.int64).copy(); t0 = t[127]
     rel = lambda s: (t[s] - t0) if t[s] else -1
-    print(f"== {name} CTA(100,6) timeline (cycles from entry); marks 120-126:", [rel(s) for s in range(120, 127)])
+    print(f"== {name} CTA timeline (cycles from entry); marks 118-126:", [rel(s) for s in range(118, 127)])
     print("   t  " + "  ".join(f"{c:>6}" for c, _ in cols))
     for i in range(16):
         print(f"  {i:2d}  " + "  ".join(f"{rel(o + i) if o != 112 or i < 8 else -1:6d}" for _, o in cols))
