@@ -125,28 +125,23 @@ __global__ void __launch_bounds__(192, 2)
     tc::mbar_wait(qdo_full, 0);
     tc::mbar_wait(w_full, 0);
     tc::tc_fence_after();
-    if (lane == 0) {  // dO^l = dO W^T
+    // dO^l = dO W^T  (whole warp, one elected lane issues; see tc::mma_bf16_w)
 #pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) tc::mma_bf16(tA, kdesc(aDO, kk, 64), kdesc(aWH, kk, D), id_dol, kk > 0);
-      tc::mma_commit(w_free);
-      tc::mma_commit(dol_done);
-    }
-    __syncwarp();
+    for (int kk = 0; kk < D / 16; ++kk) tc::mma_bf16_w(tA, kdesc(aDO, kk, 64), kdesc(aWH, kk, D), id_dol, kk > 0);
+    tc::mma_commit_w(w_free);
+    tc::mma_commit_w(dol_done);
     if (has_lin) {
       tc::mbar_wait(x_ready, 0);
       tc::mbar_wait(h_full, 0);
       tc::tc_fence_after();
-      if (lane == 0) {
-        // dQ^phi^T raw = H_i (dO^l/den)^T  (M = D over a, N = 64 rows, K = D over b)
+      // dQ^phi^T raw = H_i (dO^l/den)^T  (M = D over a, N = 64 rows, K = D over b)
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) tc::mma_bf16(tQP, kdesc(aWH, kk, D), kdesc(aDOL, kk, 64), id_qp, kk > 0);
-        // [dH_i | -dZ_i] = phi(Q)^T [dO^l/den | D^l/den]  (M = D, N = D + 64, K = 64 rows)
+      for (int kk = 0; kk < D / 16; ++kk) tc::mma_bf16_w(tQP, kdesc(aWH, kk, D), kdesc(aDOL, kk, 64), id_qp, kk > 0);
+      // [dH_i | -dZ_i] = phi(Q)^T [dO^l/den | D^l/den]  (M = D, N = D + 64, K = 64 rows)
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          tc::mma_bf16(tA, tc::desc_mnmajor(aX + kk * 2048, 8192), tc::desc_mnmajor(aDOL + kk * 2048, 8192), id_dh, kk > 0);
-        tc::mma_commit(lin_done);
-      }
-      __syncwarp();
+      for (int kk = 0; kk < 4; ++kk)
+        tc::mma_bf16_w(tA, tc::desc_mnmajor(aX + kk * 2048, 8192), tc::desc_mnmajor(aDOL + kk * 2048, 8192), id_dh, kk > 0);
+      tc::mma_commit_w(lin_done);
     }
   } else {
     const int q4 = warp & 3;

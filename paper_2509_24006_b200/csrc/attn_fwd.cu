@@ -207,19 +207,19 @@ __global__ void __launch_bounds__(192, 2)
       tc::tc_fence_after();
       return base + s * L::kTile;
     };
+    // every lane runs the issue code (warp-uniform operands); one elected lane issues
+    const uint64_t dQk = tc::desc_kmajor(sQa), dPk = tc::desc_kmajor(sPa);
+    auto koff = [](int kk) { return uint32_t((kk >> 2) * 8192 + (kk & 3) * 32); };
     auto issue_s = [&](int t) {
       const uint32_t sk = wait_slot(k_full, sKa, kit);
       fts(dbg && lane == 0 && t < 24, 24 + t);
-      if (lane == 0) {
-        const uint32_t ts = tS0 + 64 * (t & 1);
+      const uint32_t ts = tS0 + 64 * (t & 1);
+      const uint64_t dk = tc::desc_kmajor(sk);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          tc::mma_bf16(ts, tc::desc_kmajor(sQa + (kk >> 2) * 8192 + (kk & 3) * 32),
-                       tc::desc_kmajor(sk + (kk >> 2) * 8192 + (kk & 3) * 32), id_s, kk > 0);
-        tc::mma_commit(k_empty + (kit % RS));
-        tc::mma_commit(s_full + (t & 1));
-      }
-      __syncwarp();
+      for (int kk = 0; kk < D / 16; ++kk)
+        tc::mma_bf16_w(ts, tc::desc_add(dQk, koff(kk)), tc::desc_add(dk, koff(kk)), id_s, kk > 0);
+      tc::mma_commit_w(k_empty + (kit % RS));
+      tc::mma_commit_w(s_full + (t & 1));
       ++kit;
     };
     // tO[:, 64c:64c+64] (+)= X . chunk_c for the NC chunks at ring items it0.. (H_i or W)
@@ -227,31 +227,25 @@ __global__ void __launch_bounds__(192, 2)
       uint32_t sc[NC];
 #pragma unroll
       for (int c = 0; c < NC; ++c) sc[c] = wait_slot(full, base, it + c);
-      if (lane == 0) {
 #pragma unroll
-        for (int c = 0; c < NC; ++c) {
+      for (int c = 0; c < NC; ++c) {
+        const uint64_t dc = tc::desc_mnmajor(sc[c], 8192);
 #pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk)
-            tc::mma_bf16(tO + 64 * c, tc::desc_kmajor(sPa + (kk >> 2) * 8192 + (kk & 3) * 32),
-                         tc::desc_mnmajor(sc[c] + kk * 2048, 8192), id_c, acc || kk > 0);
-          tc::mma_commit(empty + ((it + c) % RS));
-        }
+        for (int kk = 0; kk < D / 16; ++kk)
+          tc::mma_bf16_w(tO + 64 * c, tc::desc_add(dPk, koff(kk)), tc::desc_add(dc, kk * 2048), id_c, acc || kk > 0);
+        tc::mma_commit_w(empty + ((it + c) % RS));
       }
       it += NC;
     };
     auto issue_pv = [&](int j) {
       tc::mbar_wait(p_full + (j & 1), (j >> 1) & 1);
       const uint32_t sv = wait_slot(v_full, sVa, vit);
-      if (lane == 0) {
-        const uint32_t sp = sPa + (j & 1) * 8192;
+      const uint64_t dp = tc::desc_add(dPk, (j & 1) * 8192), dv = tc::desc_mnmajor(sv, 8192);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          tc::mma_bf16(tO, tc::desc_kmajor(sp + kk * 32), tc::desc_mnmajor(sv + kk * 2048, 8192), id_o,
-                       (j | kk) != 0);
-        tc::mma_commit(v_empty + (vit % RS));
-        tc::mma_commit(pv_done + (j & 1));
-      }
-      __syncwarp();
+      for (int kk = 0; kk < 4; ++kk)
+        tc::mma_bf16_w(tO, tc::desc_add(dp, kk * 32), tc::desc_add(dv, kk * 2048), id_o, (j | kk) != 0);
+      tc::mma_commit_w(v_empty + (vit % RS));
+      tc::mma_commit_w(pv_done + (j & 1));
       ++vit;
     };
     tc::mbar_wait(q_full, 0);
@@ -260,8 +254,7 @@ __global__ void __launch_bounds__(192, 2)
       tc::mbar_wait(x_full, 0);
       fts(dbg && lane == 0, 102);
       issue_chunks(v_full, v_empty, sVa, vit, false);
-      if (lane == 0) tc::mma_commit(lin_done);
-      __syncwarp();
+      tc::mma_commit_w(lin_done);
     }
     for (int t = 1; t < cnt; ++t) {
       issue_s(t);
@@ -272,8 +265,7 @@ __global__ void __launch_bounds__(192, 2)
       tc::mbar_wait(o_ready, 0);
       tc::tc_fence_after();
       issue_chunks(k_full, k_empty, sKa, kit, true);
-      if (lane == 0) tc::mma_commit(proj_done);
-      __syncwarp();
+      tc::mma_commit_w(proj_done);
     }
   } else {
     // ------------------------------------------------------------------ softmax / epilogue

@@ -125,19 +125,18 @@ __global__ void __launch_bounds__(224, 1)
         const int s = kc % kStages;
         tc::mbar_wait(&full[s], (kc / kStages) & 1);
         tc::tc_fence_after();
-        if (lane == 0) {
+        {  // whole warp, one elected lane issues (warp-uniform descriptors, see tc::mma_bf16_w)
           const uint32_t sa = tc::smem_u32(smem + s * L::kStage);
           const uint32_t sb = sa + L::kA;
+          const uint64_t a0 = A_MN ? tc::desc_mnmajor(sa, 8192) : tc::desc_kmajor(sa);
+          const uint64_t b0 = B_MN ? tc::desc_mnmajor(sb, 8192) : tc::desc_kmajor(sb);
 #pragma unroll
-          for (int kk = 0; kk < kBK / 16; ++kk) {
-            const uint64_t ad = A_MN ? tc::desc_mnmajor(sa + kk * 2048, 8192) : tc::desc_kmajor(sa + kk * 32);
-            const uint64_t bd = B_MN ? tc::desc_mnmajor(sb + kk * 2048, 8192) : tc::desc_kmajor(sb + kk * 32);
-            tc::mma_bf16(acc, ad, bd, idesc, (kb | kk) != 0);
-          }
-          tc::mma_commit(&empty[s]);
-          if (kb == nk - 1) tc::mma_commit(&tfull[ab]);
+          for (int kk = 0; kk < kBK / 16; ++kk)
+            tc::mma_bf16_w(acc, tc::desc_add(a0, A_MN ? kk * 2048 : kk * 32), tc::desc_add(b0, B_MN ? kk * 2048 : kk * 32),
+                           idesc, (kb | kk) != 0);
+          tc::mma_commit_w(&empty[s]);
+          if (kb == nk - 1) tc::mma_commit_w(&tfull[ab]);
         }
-        __syncwarp();
       }
     }
   } else if (warp <= 5) {
