@@ -7,6 +7,7 @@
 // HBM-bound: Q and K are each read once (vectorised over d, coalesced across threads);
 // everything after pooling works on T x d / T x T data that lives in L2.
 #include <cfloat>
+#include <type_traits>
 
 #include "buffers.hpp"
 #include "kernels.hpp"
@@ -221,6 +222,126 @@ __global__ void k_classify(const R* __restrict__ scores, int Tm,
 }
 
 // ---------------------------------------------------------------------------------------
+// K2, warp-per-row variant for 32 <= P2 <= 512 (the Wan2.1 shape has T = 512): one warp owns
+// a block row, EPL = P2/32 consecutive entries per lane in registers.  Same arithmetic as
+// k_classify -- exact max, exp, the reference's sequential ascending normaliser (the running
+// sum is handed lane to lane), one rounded division -- and the same bitonic network over
+// (weight desc, column asc), with the distance >= EPL passes done by shuffles.  No block
+// barriers: a whole row is one warp's registers.
+// ---------------------------------------------------------------------------------------
+template <typename R, int EPL>
+__global__ void __launch_bounds__(256) k_classify_warp(const R* __restrict__ scores, long long rows,
+                                                       int Tn, int n1, int n_neg,
+                                                       int8_t* __restrict__ labels, int* __restrict__ crit_cnt,
+                                                       int* __restrict__ crit_idx, int* __restrict__ marg_cnt,
+                                                       double* __restrict__ p_c_out) {
+  constexpr int P2 = 32 * EPL;
+  __shared__ int8_t slab[8][P2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const long long row = (long long)blockIdx.x * 8 + warp;
+  if (row >= rows) return;
+  const R* srow = scores + row * Tn;
+  R key[EPL];
+  int idx[EPL];
+  R m = -R(INFINITY);
+#pragma unroll
+  for (int r = 0; r < EPL; ++r) {
+    const int j = lane * EPL + r;
+    key[r] = j < Tn ? srow[j] : -R(INFINITY);
+    m = key[r] > m ? key[r] : m;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const R other = __shfl_xor_sync(0xffffffffu, m, o);
+    m = other > m ? other : m;
+  }
+#pragma unroll
+  for (int r = 0; r < EPL; ++r) key[r] = lane * EPL + r < Tn ? exp_r(key[r] - m) : R(0);
+  // sequential ascending-j normaliser (mask.cpp:73-77): lane L continues lane L-1's sum
+  R sum = R(0);
+  for (int L = 0; L < 32; ++L) {
+    if (lane == L) {
+#pragma unroll
+      for (int r = 0; r < EPL; ++r)
+        if (lane * EPL + r < Tn) sum = add_rn(sum, key[r]);
+    }
+    sum = __shfl_sync(0xffffffffu, sum, L);
+  }
+#pragma unroll
+  for (int r = 0; r < EPL; ++r) {
+    const int j = lane * EPL + r;
+    idx[r] = j;
+    if (j < Tn) {
+      key[r] = div_rn(key[r], sum);
+      if (p_c_out) p_c_out[row * Tn + j] = double(key[r]);
+    } else {
+      key[r] = -R(1);  // pads sort after every weight (weights are >= 0)
+    }
+  }
+#pragma unroll
+  for (int k = 2; k <= P2; k <<= 1) {
+#pragma unroll
+    for (int jj = k >> 1; jj > 0; jj >>= 1) {
+      if (jj >= EPL) {  // partner in lane ^ (jj / EPL), same register
+        const int lm = jj / EPL;
+        const bool lower = (lane & lm) == 0;
+#pragma unroll
+        for (int r = 0; r < EPL; ++r) {
+          const R ok = __shfl_xor_sync(0xffffffffu, key[r], lm);
+          const int oi = __shfl_xor_sync(0xffffffffu, idx[r], lm);
+          const int t = (lane * EPL + r) & ~jj;  // lower position of the pair
+          const bool up = (t & k) == 0;
+          const bool mine_first = before(key[r], idx[r], ok, oi);
+          if ((lower == up) != mine_first) {
+            key[r] = ok;
+            idx[r] = oi;
+          }
+        }
+      } else {  // partner in the same lane
+#pragma unroll
+        for (int r = 0; r < EPL; ++r) {
+          if (r & jj) continue;
+          const int x = r | jj;
+          const bool up = ((lane * EPL + r) & k) == 0;
+          if (up != before(key[r], idx[r], key[x], idx[x])) {
+            const R tk = key[r];
+            key[r] = key[x];
+            key[x] = tk;
+            const int ti = idx[r];
+            idx[r] = idx[x];
+            idx[x] = ti;
+          }
+        }
+      }
+    }
+  }
+  int8_t* lab = slab[warp];
+#pragma unroll
+  for (int r = 0; r < EPL; ++r) {
+    const int e = lane * EPL + r;  // rank
+    if (idx[r] < Tn) lab[idx[r]] = e < n1 ? int8_t(1) : (e >= Tn - n_neg ? int8_t(-1) : int8_t(0));
+  }
+  __syncwarp();
+  int8_t* lrow = labels + row * Tn;
+  for (int j = lane; j < Tn; j += 32) lrow[j] = lab[j];
+  int base = 0, marg = 0;
+  int* crow = crit_idx + row * Tn;
+  for (int j0 = 0; j0 < Tn; j0 += 32) {
+    const int j = j0 + lane;
+    const int l = j < Tn ? lab[j] : -1;
+    const unsigned bc = __ballot_sync(0xffffffffu, l == 1);
+    const unsigned bm = __ballot_sync(0xffffffffu, l == 0);
+    if (l == 1) crow[base + __popc(bc & ((1u << lane) - 1u))] = j;
+    base += __popc(bc);
+    marg += __popc(bm);
+  }
+  if (lane == 0) {
+    crit_cnt[row] = base;
+    marg_cnt[row] = marg;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
 // build_lookup for an injected label grid (mask.cpp:121-153); flags invalid labels.
 // ---------------------------------------------------------------------------------------
 __global__ void k_build_lut(const int8_t* __restrict__ labels, int Tm, int Tn,
@@ -329,8 +450,24 @@ static void classify_t(const Dims& D, const In* q, const In* k, const StateBufs&
   k_scores<R><<<dim3((D.Tn + 63) / 64, (D.Tm + 63) / 64, unsigned(D.U)), 256, 0, st>>>(
       pq, pk, D.d, D.Tm, D.Tn, R(D.inv_sqrt_d), scores);
   check_launch("k_scores", st);
+  const int P2 = next_pow2(D.Tn);
+  const long long rows = D.U * (long long)D.Tm;
+  const unsigned wblocks = unsigned((rows + 7) / 8);
+  auto warp_rows = [&](auto kern) {
+    kern<<<wblocks, 256, 0, st>>>(scores, rows, D.Tn, D.n1, D.n_neg, s.labels, s.crit_cnt, s.crit_idx,
+                                  s.marg_cnt, p_c);
+    check_launch("k_classify", st);
+  };
+  switch (P2) {  // one warp per block row while a row fits 16 registers per lane
+    case 32: warp_rows(k_classify_warp<R, 1>); return;
+    case 64: warp_rows(k_classify_warp<R, 2>); return;
+    case 128: warp_rows(k_classify_warp<R, 4>); return;
+    case 256: warp_rows(k_classify_warp<R, 8>); return;
+    case 512: warp_rows(k_classify_warp<R, 16>); return;
+    default: break;
+  }
   k_classify<R><<<dim3(D.Tm, unsigned(D.U)), 256, smem, st>>>(
-      scores, D.Tm, D.Tn, next_pow2(D.Tn), D.n1, D.n_neg, s.labels,
+      scores, D.Tm, D.Tn, P2, D.n1, D.n_neg, s.labels,
       s.crit_cnt, s.crit_idx, s.marg_cnt, p_c);
   check_launch("k_classify", st);
 }
