@@ -78,17 +78,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
   const bool dbg = blockIdx.x == SLAB_DBG_X && blockIdx.y == 6;
   ts_mark(dbg && threadIdx.x == 0, 127);
   cta_mark(threadIdx.x == 0, 0);
-  __shared__ int s_lin;
-  if (threadIdx.x == 0) s_lin = 0;
-  __syncthreads();
-  {
-    const int8_t* lu = p.labels + u * (long long)p.Tm * p.Tn;
-    int any = 0;
-    for (int ii = threadIdx.x; ii < p.Tm; ii += blockDim.x) any |= lu[(long long)ii * p.Tn + j] == 0;
-    if (any) s_lin = 1;
-  }
-  __syncthreads();
-  const bool has_lin = s_lin != 0;
+  const bool has_lin = p.ccol_marg[ucol] > 0;  // some marginal row in this column (k_build_csc)
   ts_mark(dbg && threadIdx.x == 0, 126);
   const int kv0 = int(u * p.N) + j * 64;
 
@@ -459,6 +449,7 @@ void launch_bwd_cols(const Dims& Dm, const void* q, const void* k, const void* v
   BwdParams p{};
   p.ccol_cnt = s.ccol_cnt;
   p.ccol_idx = s.ccol_idx;
+  p.ccol_marg = s.ccol_marg;
   p.labels = s.labels;
   p.lse = lse;
   p.Ds = Ds;

@@ -490,7 +490,7 @@ __global__ void __launch_bounds__(352, 1)
     const uint32_t lane_base = uint32_t(32 * q4) << 16;
     const int tid = threadIdx.x - 64;  // 0..255
     if (tid < 64) s_lse2[tid] = p.lse[(long long)row0 + tid] * 1.4426950408889634f;
-    else if (tid < 128) s_ds[tid - 64] = p.Ds[(long long)row0 + tid - 64];
+    else if (tid < 128) s_ds[tid - 64] = p.Ds[(long long)row0 + tid - 64] * p.scale;  // D^s / sqrt(d)
     named_sync(1, 256);
     const int c = 32 * q4 + lane;  // key row of the pair (c < 64: block j1, else j2)
 #pragma unroll 1
@@ -507,27 +507,32 @@ __global__ void __launch_bounds__(352, 1)
         tc::tmem_ld32(tb, sv);
         tc::tmem_ld32(tb + 64, dp);
         tc::tmem_ld_wait();
+        // dS = P (dP - D^s) / sqrt(d) with P = exp2(S log2e / sqrt(d) - lse log2e); the
+        // per-query constants (lse log2e, D^s / sqrt(d)) are shared-space vector loads
+        const float sc = live ? p.scale : 0.f;
+        const uint32_t a_l = tc::smem_u32(s_lse2) + 4u * uint32_t(32 * grp);
+        const uint32_t a_d = tc::smem_u32(s_ds) + 4u * uint32_t(32 * grp);
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          if (SLAB_DIAG_NOMMA == 4) {
-            pk[e >> 1] = sv[e] ^ dp[e];
-            continue;
+        for (int e = 0; e < 32; e += 4) {
+          const float4 l4 = tc::lds_f4(a_l + 4u * e), d4 = tc::lds_f4(a_d + 4u * e);
+          const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
+          float dsv[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float pq = ex2f(__uint_as_float(sv[e + q]) * p.scale_log2 - lv[q]);
+            dsv[q] = pq * fmaf(__uint_as_float(dp[e + q]), sc, -dv4[q] * (live ? 1.f : 0.f));
           }
-          const int rr = 32 * grp + e;
-          const float p0 = ex2f(__uint_as_float(sv[e]) * p.scale_log2 - s_lse2[rr]);
-          const float p1 = ex2f(__uint_as_float(sv[e + 1]) * p.scale_log2 - s_lse2[rr + 1]);
-          const float d0 = live ? p0 * (__uint_as_float(dp[e]) - s_ds[rr]) * p.scale : 0.f;
-          const float d1 = live ? p1 * (__uint_as_float(dp[e + 1]) - s_ds[rr + 1]) * p.scale : 0.f;
-          pk[e >> 1] = tc::pack_bf16(d0, d1);
+          pk[e >> 1] = tc::pack_bf16(dsv[0], dsv[1]);
+          pk[(e >> 1) + 1] = tc::pack_bf16(dsv[2], dsv[3]);
         }
       }
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 128 + t);
       if (t >= 1) tc::mbar_wait(ds_empty, (t - 1) & 1);  // dQ of the previous pair has read dS
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 144 + t);
+      const uint32_t a_ds_tile = tc::smem_u32(sDS);
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch)
-        *reinterpret_cast<uint4*>(sDS + tc::sw128_off(c, 4 * grp + ch)) =
-            make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]);
+        tc::sts_u4(a_ds_tile + tc::sw128_off(c, 4 * grp + ch), make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]));
       tc::fence_proxy_async();
       tc::tc_fence_before();
       __syncwarp();

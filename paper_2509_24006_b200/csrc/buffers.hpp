@@ -24,6 +24,7 @@ struct StateBufs {
   int* marg_cnt = nullptr;
   int* ccol_cnt = nullptr;   // [U, Tn] critical rows per column (CSC, backward)
   int* ccol_idx = nullptr;   // [U, Tn, Tm] ascending critical rows per column
+  int* ccol_marg = nullptr;  // [U, Tn] marginal rows per column (backward linear branch)
   float* H = nullptr;
   float* Z = nullptr;
   __nv_bfloat16* Hb = nullptr;   // fast path: H in bf16 [U, Tm, d, d]
@@ -89,6 +90,7 @@ inline void carve_state(const Dims& D, bool fast, void* base, StateBufs& s, size
   s.marg_cnt = c.take<int>(U * Tm);
   s.ccol_cnt = c.take<int>(U * Tn);
   s.ccol_idx = c.take<int>(U * Tn * Tm);
+  s.ccol_marg = c.take<int>(U * Tn);
   s.Z = c.take<float>(U * Tm * d);
   if (fast) {
     s.Hb = c.take<__nv_bfloat16>(U * Tm * d * d);

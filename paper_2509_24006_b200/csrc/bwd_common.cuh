@@ -86,6 +86,7 @@ struct BwdParams {
   const int* marg_cnt;
   const int* ccol_cnt;
   const int* ccol_idx;
+  const int* ccol_marg;
   const float* Z;      // [U, Tm, D]
   const float* lse;    // [U, N]
   const float* Ds;     // [U, N] (rows kernel writes, cols kernel reads)

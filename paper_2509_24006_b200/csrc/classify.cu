@@ -372,22 +372,27 @@ __global__ void k_build_lut(const int8_t* __restrict__ labels, int Tm, int Tn,
 
 // Transposed critical lists (backward.cpp:133-137): per column, ascending rows.
 __global__ void k_build_csc(const int8_t* __restrict__ labels, int Tm, int Tn,
-                            int* __restrict__ ccol_cnt, int* __restrict__ ccol_idx) {
+                            int* __restrict__ ccol_cnt, int* __restrict__ ccol_idx,
+                            int* __restrict__ ccol_marg) {
   const long long u = blockIdx.y;
   const int j = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (j >= Tn) return;
   const int8_t* lu = labels + u * (long long)Tm * Tn;
   int* out = ccol_idx + (u * Tn + j) * (long long)Tm;
-  int base = 0;
+  int base = 0, marg = 0;
   for (int i0 = 0; i0 < Tm; i0 += 32) {
     const int i = i0 + lane;
-    const bool c = i < Tm && lu[(long long)i * Tn + j] == 1;
-    const unsigned b = __ballot_sync(0xffffffffu, c);
-    if (c) out[base + __popc(b & ((1u << lane) - 1u))] = i;
+    const int l = i < Tm ? lu[(long long)i * Tn + j] : -1;
+    const unsigned b = __ballot_sync(0xffffffffu, l == 1);
+    if (l == 1) out[base + __popc(b & ((1u << lane) - 1u))] = i;
     base += __popc(b);
+    marg += __popc(__ballot_sync(0xffffffffu, l == 0));
   }
-  if (lane == 0) ccol_cnt[u * Tn + j] = base;
+  if (lane == 0) {
+    ccol_cnt[u * Tn + j] = base;
+    ccol_marg[u * Tn + j] = marg;
+  }
 }
 
 // Marginal indicator as a bf16 0/1 matrix: the A operand of H = M0 h (fast path).
@@ -502,7 +507,7 @@ void launch_build_lut(const Dims& D, const StateBufs& s, long long* bad, cudaStr
 void launch_build_csc(const Dims& D, const StateBufs& s, cudaStream_t st) {
   const int warps = 8;
   k_build_csc<<<dim3((D.Tn + warps - 1) / warps, unsigned(D.U)), 32 * warps, 0, st>>>(
-      s.labels, D.Tm, D.Tn, s.ccol_cnt, s.ccol_idx);
+      s.labels, D.Tm, D.Tn, s.ccol_cnt, s.ccol_idx, s.ccol_marg);
   check_launch("k_build_csc", st);
 }
 
