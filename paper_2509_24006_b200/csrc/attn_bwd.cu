@@ -35,6 +35,9 @@ struct ColsLayout {
   static_assert(kBytes <= 232448, "smem");
 };
 
+#ifndef SLAB_COLS_ACC_FIRST
+#define SLAB_COLS_ACC_FIRST 0  // issue the ready acc(t) before a ready S/dP(t+1)
+#endif
 #ifndef SLAB_COLS_PROD
 #define SLAB_COLS_PROD 2
 #endif
@@ -202,6 +205,11 @@ __global__ void __launch_bounds__(kColsThreads, 1)
     {
       int ts = 0, ta = 0;
       while (ta < np) {
+        if (SLAB_COLS_ACC_FIRST && ta < ts && __all_sync(0xffffffffu, tc::mbar_test(pd_full + (ta & 1), (ta >> 1) & 1))) {
+          issue_acc(ta);  // release the ring stage first
+          ++ta;
+          continue;
+        }
         if (ts < np && ts <= ta + 1 && __all_sync(0xffffffffu, tc::mbar_test(ring_full + ts % RS, (ts / RS) & 1))) {
           tc::tc_fence_after();
           ts_mark(dbg && lane == 0 && ts < 16, 16 + ts);
@@ -254,7 +262,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
       const bool live = rq < 64 || 2 * t + 1 < cnt;
       const long long qrow = u * p.N + (long long)list[min(2 * t + (rq >> 6), cnt - 1)] * 64 + (rq & 63);
       const float lse2 = p.lse[qrow] * 1.4426950408889634f;
-      const float dsr = p.Ds[qrow];
+      const float dss = p.Ds[qrow] * p.scale;  // D^s / sqrt(d)
       tc::mbar_wait(sdp_full + (t & 1), (t >> 1) & 1);
       tc::tc_fence_after();
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 32 + t);
@@ -267,25 +275,26 @@ __global__ void __launch_bounds__(kColsThreads, 1)
         tc::tmem_ld_wait();
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
-          float p0 = ex2f(__uint_as_float(sv[e]) * p.scale_log2 - lse2);
-          float p1 = ex2f(__uint_as_float(sv[e + 1]) * p.scale_log2 - lse2);
-          float d0 = p0 * (__uint_as_float(dp[e]) - dsr) * p.scale;
-          float d1 = p1 * (__uint_as_float(dp[e + 1]) - dsr) * p.scale;
-          if (!live) p0 = p1 = d0 = d1 = 0.f;
+          const float p0 = ex2f(__uint_as_float(sv[e]) * p.scale_log2 - lse2);
+          const float p1 = ex2f(__uint_as_float(sv[e + 1]) * p.scale_log2 - lse2);
+          const float d0 = p0 * fmaf(__uint_as_float(dp[e]), p.scale, -dss);
+          const float d1 = p1 * fmaf(__uint_as_float(dp[e + 1]), p.scale, -dss);
           pp[e >> 1] = tc::pack_bf16(p0, p1);
           dd[e >> 1] = tc::pack_bf16(d0, d1);
+        }
+        if (!live) {  // the repeated block of an odd tail contributes nothing
+#pragma unroll
+          for (int e = 0; e < 16; ++e) pp[e] = dd[e] = 0u;
         }
       }
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 128 + t);
       if (t >= 2) tc::mbar_wait(pd_empty + (t & 1), ((t - 2) >> 1) & 1);
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 144 + t);
-      uint8_t* prow = sPD + (t & 1) * 32768;
+      const uint32_t prow = tc::smem_u32(sPD) + (t & 1) * 32768;
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
-        *reinterpret_cast<uint4*>(prow + tc::sw128_off(rq, 4 * grp + ch)) =
-            make_uint4(pp[4 * ch], pp[4 * ch + 1], pp[4 * ch + 2], pp[4 * ch + 3]);
-        *reinterpret_cast<uint4*>(prow + 16384 + tc::sw128_off(rq, 4 * grp + ch)) =
-            make_uint4(dd[4 * ch], dd[4 * ch + 1], dd[4 * ch + 2], dd[4 * ch + 3]);
+        tc::sts_u4(prow + tc::sw128_off(rq, 4 * grp + ch), make_uint4(pp[4 * ch], pp[4 * ch + 1], pp[4 * ch + 2], pp[4 * ch + 3]));
+        tc::sts_u4(prow + 16384 + tc::sw128_off(rq, 4 * grp + ch), make_uint4(dd[4 * ch], dd[4 * ch + 1], dd[4 * ch + 2], dd[4 * ch + 3]));
       }
       tc::fence_proxy_async();
       tc::tc_fence_before();

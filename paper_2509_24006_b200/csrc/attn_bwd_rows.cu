@@ -509,7 +509,8 @@ __global__ void __launch_bounds__(352, 1)
         tc::tmem_ld_wait();
         // dS = P (dP - D^s) / sqrt(d) with P = exp2(S log2e / sqrt(d) - lse log2e); the
         // per-query constants (lse log2e, D^s / sqrt(d)) are shared-space vector loads
-        const float sc = live ? p.scale : 0.f;
+        ts_mark(dbg && threadIdx.x == 64 && t < 16, 240 + t);
+        const float sc = p.scale;
         const uint32_t a_l = tc::smem_u32(s_lse2) + 4u * uint32_t(32 * grp);
         const uint32_t a_d = tc::smem_u32(s_ds) + 4u * uint32_t(32 * grp);
 #pragma unroll
@@ -520,10 +521,14 @@ __global__ void __launch_bounds__(352, 1)
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const float pq = ex2f(__uint_as_float(sv[e + q]) * p.scale_log2 - lv[q]);
-            dsv[q] = pq * fmaf(__uint_as_float(dp[e + q]), sc, -dv4[q] * (live ? 1.f : 0.f));
+            dsv[q] = pq * fmaf(__uint_as_float(dp[e + q]), sc, -dv4[q]);
           }
           pk[e >> 1] = tc::pack_bf16(dsv[0], dsv[1]);
           pk[(e >> 1) + 1] = tc::pack_bf16(dsv[2], dsv[3]);
+        }
+        if (!live) {  // the repeated block of an odd tail contributes nothing
+#pragma unroll
+          for (int e = 0; e < 16; ++e) pk[e] = 0u;
         }
       }
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 128 + t);
