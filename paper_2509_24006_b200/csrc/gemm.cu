@@ -28,7 +28,10 @@ struct GemmSmem {
   static constexpr int kA = BM * kBK * 2;
   static constexpr int kB = BN * kBK * 2;
   static constexpr int kStage = kA + kB;
-  static constexpr int kBytes = kStages * kStage + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int kOut = BM * 64 * 2;  // one [BM][64] bf16 output box (TMA-store staging)
+  static constexpr int oOut = kStages * kStage;
+  static constexpr int kBytes = oOut + 2 * kOut + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(kBytes <= 232448, "smem");
 };
 
 // Persistent: each CTA walks tiles blockIdx.x, +gridDim.x, ...; the smem ring runs across tile
@@ -37,11 +40,12 @@ struct GemmSmem {
 template <int BM, int BN, bool A_MN, bool B_MN, typename OutT>
 __global__ void __launch_bounds__(224, 1)
     k_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
+           const __grid_constant__ CUtensorMap tc_out,
            OutT* __restrict__ C, int M, int N, int K, int batch, long long c_batch, int ldc) {
   using L = GemmSmem<BM, BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * L::kStage);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::oOut + 2 * L::kOut);
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;  // [2]
   uint64_t* tempty = tfull + 2;       // [2]
@@ -151,6 +155,45 @@ __global__ void __launch_bounds__(224, 1)
       tc::tc_fence_after();
       const int row = BM == 128 ? 32 * q + lane : 16 * q + lane;
       const bool live = (BM == 128 || lane < 16) && (m0 + row) < M;
+      if constexpr (sizeof(OutT) == 2) {
+        // bf16: each 64-column chunk goes TMEM -> registers -> SW128 smem box -> one TMA store
+        // (coalesced; row-per-thread global stores were as slow as the MMAs of the tile)
+        const uint32_t ob = tc::smem_u32(smem + L::oOut);
+#pragma unroll 1
+        for (int c = 0; c < BN / 64; ++c) {
+          uint32_t r0[32], r1[32];
+          const uint32_t ta0 = tmem + ab * BN + (uint32_t(32 * q) << 16) + 64 * c;
+          tc::tmem_ld32(ta0, r0);
+          tc::tmem_ld32(ta0 + 32, r1);
+          tc::tmem_ld_wait();
+          // staging buffer (c & 1) is free once the store issued two chunks ago has read it
+          if (threadIdx.x == 64) tc::bulk_wait_read<1>();
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          const uint32_t buf = ob + (c & 1) * L::kOut;
+          if (BM == 128 || lane < 16) {
+#pragma unroll
+            for (int ch = 0; ch < 8; ++ch) {
+              const uint32_t* src = ch < 4 ? r0 + 8 * ch : r1 + 8 * (ch - 4);
+              uint4 v;
+              v.x = tc::pack_bf16(__uint_as_float(src[0]), __uint_as_float(src[1]));
+              v.y = tc::pack_bf16(__uint_as_float(src[2]), __uint_as_float(src[3]));
+              v.z = tc::pack_bf16(__uint_as_float(src[4]), __uint_as_float(src[5]));
+              v.w = tc::pack_bf16(__uint_as_float(src[6]), __uint_as_float(src[7]));
+              tc::sts_u4(buf + tc::sw128_off(row, ch), v);
+            }
+          }
+          tc::fence_proxy_async();
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          if (threadIdx.x == 64) {
+            tc::tma_store_3d(&tc_out, smem + L::oOut + (c & 1) * L::kOut, n0 + 64 * c, m0, b);
+            tc::bulk_commit();
+          }
+        }
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&tempty[ab]);
+        continue;
+      }
       OutT* crow = C + (long long)b * c_batch + (long long)(m0 + row) * ldc + n0;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 32) {
@@ -182,6 +225,7 @@ __global__ void __launch_bounds__(224, 1)
       if (lane == 0) tc::mbar_arrive(&tempty[ab]);
     }
   }
+  if (threadIdx.x == 64) tc::bulk_wait<0>();
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<2 * BN>(tmem);
@@ -216,6 +260,9 @@ void launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
     make_tmap_bf16(&tb, g.B, g.N, g.K, g.batch, g.ldb, g.b_batch, 64);
   else
     make_tmap_bf16(&tb, g.B, g.K, g.N, g.batch, g.ldb, g.b_batch, BN);
+  CUtensorMap tcm{};
+  if (sizeof(OutT) == 2)  // output boxes [BM rows][64 cols] of C [batch][M][ldc]
+    make_tmap_bf16(&tcm, g.C, g.N, g.M, g.batch, g.ldc, g.c_batch, BM);
   auto kern = k_gemm<BM, BN, A_MN, B_MN, OutT>;
   constexpr int smem = GemmSmem<BM, BN>::kBytes;
   SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -223,7 +270,7 @@ void launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
   static int sms = 0;
   if (!sms) SLAB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   const int grid = int(std::min<long long>(tiles, sms));
-  kern<<<grid, 224, smem, st>>>(ta, tb, static_cast<OutT*>(g.C), g.M, g.N, g.K, g.batch, g.c_batch, g.ldc);
+  kern<<<grid, 224, smem, st>>>(ta, tb, tcm, static_cast<OutT*>(g.C), g.M, g.N, g.K, g.batch, g.c_batch, g.ldc);
   check_launch(g.name ? g.name : "k_gemm", st);
 }
 

@@ -26,7 +26,10 @@ def _gemm(A, B, M, N, K, batch, a_mn, b_mn, out_f32):
 @pytest.mark.parametrize("a_mn", [False, True])
 @pytest.mark.parametrize("b_mn", [False, True])
 @pytest.mark.parametrize("M,N,K,batch", [(128, 256, 512, 2), (64, 128, 64, 3), (256, 64, 192, 1),
-                                         (128, 128, 128, 5)])
+                                         (128, 128, 128, 5),
+                                         # A-resident aggregation kernel: CTA tile ranges that
+                                         # cross (batch, m) blocks, and a K tail
+                                         (512, 4096, 512, 3), (384, 512, 200, 2)])
 @pytest.mark.parametrize("out_f32", [True, False])
 def test_gemm_matches_fp32_matmul(a_mn, b_mn, M, N, K, batch, out_f32):
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K + batch)
