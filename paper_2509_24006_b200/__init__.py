@@ -14,9 +14,11 @@ from .sla import (  # noqa: F401
     sla_forward_with_mask,
 )
 from .pipeline import HostTrainStep  # noqa: F401
+from .autograd import SparseLinearAttention, sparse_linear_attention  # noqa: F401
 from ._lib import LIB_PATH  # noqa: F401
 
 __all__ = [
     "SLA", "BlockLayout", "SlaConfig", "SlaForwardState", "SlaGradients", "combine_outputs",
     "make_block_layout", "sla_backward", "sla_forward", "sla_forward_with_mask", "HostTrainStep",
+    "SparseLinearAttention", "sparse_linear_attention",
 ]

@@ -53,3 +53,12 @@ for i in range(4):
 
 lat_k = [t[80 + i] - t[i] for i in range(3, 12)]; lat_v = [t[96 + i] - t[112 + i] for i in range(3, 8)]
 print(f"rows TMA latency (t>=3): K pair {np.mean(lat_k):.0f} cyc, V pair {np.mean(lat_v):.0f} cyc; loop/pair {(t[64+11]-t[64+3])/8:.0f}")
+
+# forward CTA (100, 6) timeline (attn_fwd.cu fts marks)
+buf = (C.c_longlong * 128)(); L.sla_b200_diag_fwd_timeline(buf)
+t = np.frombuffer(buf, dtype=np.int64).copy(); t0 = t[127]
+rel = lambda s: int(t[s] - t0) if t[s] else -1
+print("fwd marks 96-105:", [rel(s) for s in range(96, 106)])
+print("   t   ldK     S   got     P")
+for i in range(24):
+    print(f"  {i:2d} " + " ".join(f"{rel(o + i):6d}" for o in (0, 24, 48, 72)))

@@ -83,3 +83,15 @@ def test_generic_shape_limits_are_reported():
     p.flags = L.FLAG_GENERIC
     assert L.lib().sla_b200_validate(C.byref(p)) == L.ERR_INVALID
     assert "shared memory" in L.lib().sla_b200_last_error().decode()
+
+
+def test_autograd_caller_validates_shapes_before_any_launch():
+    import torch
+    from paper_2509_24006_b200 import sparse_linear_attention
+    q = torch.zeros(1, 2, 128, 64)
+    with pytest.raises(ValueError):
+        sparse_linear_attention(q, q[:, :1], q, torch.zeros(64, 64))
+    with pytest.raises(ValueError):
+        sparse_linear_attention(q, q, q, torch.zeros(3, 64, 64))
+    with pytest.raises(ValueError):
+        sparse_linear_attention(q, q, q, torch.zeros(64, 64), layout="nhd")
