@@ -65,11 +65,17 @@ extern "C" {
 #define SLA_B200_FLAG_CHECK_FINITE 1u /* reject non-finite q/k/v with "(r, c)" (forward.cpp:15-25)
                                          and non-finite outputs (forward.cpp:164-170); syncs  */
 #define SLA_B200_FLAG_GENERIC 2u      /* force the shape-generic SIMT kernels                 */
+/* Ragged N (an extension; the reference rejects N % b != 0, layout.cpp:12-17, and so does this
+ * library without the flag).  With it, T = ceil(N / b) and the last block holds r = N - (T-1) b
+ * rows: its pooled mean is over those r rows, keys >= N take no part in either branch (no
+ * softmax weight, no phi(K) summary), and only rows < N are read or written.  For N % b == 0
+ * the results are identical to the unflagged call.  tcgen05 path only (bf16, b_q = b_kv = 64). */
+#define SLA_B200_FLAG_RAGGED 4u
 
 typedef struct sla_b200_problem {
   int64_t batch;    /* B                                  */
   int64_t heads;    /* H                                  */
-  int64_t n;        /* sequence length N (multiple of b_q and b_kv) */
+  int64_t n;        /* sequence length N (multiple of b_q and b_kv unless FLAG_RAGGED) */
   int64_t d;        /* head dimension                     */
   int64_t b_q;      /* rows per query block               */
   int64_t b_kv;     /* rows per key/value block           */

@@ -75,6 +75,7 @@ class Oracle:
             lib.orc_validate.argtypes = [_sz, _sz, _sz, _sz, C.c_double, C.c_double, C.c_char_p, _sz]
             lib.orc_pool_mean.argtypes = [_dp, _sz, _sz, _sz, _dp]
             lib.orc_predict.argtypes = [_dp, _dp, _sz, _sz, _sz, _sz, _dp]
+            lib.orc_predict_ragged.argtypes = [_dp, _dp, _sz, _sz, _sz, _dp]
             lib.orc_scores.argtypes = [_dp, _dp, _sz, _sz, _sz, _sz, _dp]
             lib.orc_counts.argtypes = [_sz, C.c_double, C.c_double, C.POINTER(_sz), C.POINTER(_sz)]
             lib.orc_classify.argtypes = [_dp, _sz, _sz, C.c_double, C.c_double, _i8]
@@ -167,6 +168,23 @@ def predict(q, k, b_q, b_kv):
     if Oracle.lib().orc_predict(q, k, n, d, b_q, b_kv, out):
         raise ValueError("predict: bad layout")
     return out
+
+
+def predict_ragged(q, k, b):
+    """Ragged-N extension of predict (sla_oracle.c orc_predict_ragged): T = ceil(N / b), the
+    last block's pooled mean over its valid rows.  No reference counterpart (layout.cpp:12-17
+    rejects ragged N)."""
+    q, k = _f64(q), _f64(k)
+    n, d = q.shape
+    t = (n + b - 1) // b
+    out = np.empty((t, t))
+    if Oracle.lib().orc_predict_ragged(q, k, n, d, b, out):
+        raise ValueError("predict_ragged: bad layout")
+    return out
+
+
+def dynamic_labels_ragged(q, k, b, k_h, k_l):
+    return classify(predict_ragged(q, k, b), k_h, k_l)
 
 
 def classify(p_c, k_h, k_l):

@@ -146,6 +146,49 @@ int orc_predict(const double* q, const double* k, size_t n, size_t d, size_t b_q
   return 0;
 }
 
+/* Ragged-N extension (SLA_B200_FLAG_RAGGED; the reference has no counterpart -- it rejects
+ * N % b != 0, layout.cpp:12-17): T = ceil(n / b) blocks, the last one averaging its r valid
+ * rows; otherwise mask.cpp:40-81 operation for operation (ascending row sums, ascending-k dot,
+ * max-shifted softmax with the ascending normaliser). */
+int orc_predict_ragged(const double* q, const double* k, size_t n, size_t d, size_t b, double* p_c) {
+  if (b == 0 || n == 0) return 2;
+  const size_t t = (n + b - 1) / b;
+  double* pq = (double*)calloc(t * d, sizeof(double));
+  double* pk = (double*)calloc(t * d, sizeof(double));
+  for (size_t g = 0; g < t; ++g) {
+    const size_t rows = (g + 1) * b <= n ? b : n - g * b;
+    for (size_t r = 0; r < rows; ++r)
+      for (size_t c = 0; c < d; ++c) {
+        pq[g * d + c] += q[(g * b + r) * d + c];
+        pk[g * d + c] += k[(g * b + r) * d + c];
+      }
+    for (size_t c = 0; c < d; ++c) {
+      pq[g * d + c] /= (double)rows;
+      pk[g * d + c] /= (double)rows;
+    }
+  }
+  const double inv_sqrt_d = 1.0 / sqrt((double)d);
+  for (size_t i = 0; i < t; ++i) {
+    double* row = p_c + i * t;
+    for (size_t j = 0; j < t; ++j) {
+      double acc = 0;
+      for (size_t c = 0; c < d; ++c) acc += pq[i * d + c] * pk[j * d + c];
+      row[j] = acc * inv_sqrt_d;
+    }
+    double m = row[0];
+    for (size_t j = 1; j < t; ++j) m = row[j] > m ? row[j] : m;
+    double sum = 0;
+    for (size_t j = 0; j < t; ++j) {
+      row[j] = exp(row[j] - m);
+      sum += row[j];
+    }
+    for (size_t j = 0; j < t; ++j) row[j] /= sum;
+  }
+  free(pq);
+  free(pk);
+  return 0;
+}
+
 /* mask.cpp:85-101 */
 static size_t round_half_up(double x) { return (size_t)floor(x + 0.5); }
 

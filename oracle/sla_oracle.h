@@ -42,6 +42,7 @@ int orc_validate(size_t n, size_t d, size_t b_q, size_t b_kv, double k_h, double
 int orc_pool_mean(const double* x, size_t rows, size_t cols, size_t b, double* out);
 int orc_predict(const double* q, const double* k, size_t n, size_t d, size_t b_q,
                 size_t b_kv, double* p_c /* T_m x T_n */);
+int orc_predict_ragged(const double* q, const double* k, size_t n, size_t d, size_t b, double* p_c);
 /* pooled, scaled scores before the softmax (same op order as predict) */
 int orc_scores(const double* q, const double* k, size_t n, size_t d, size_t b_q,
                size_t b_kv, double* s /* T_m x T_n */);

@@ -29,7 +29,7 @@ _OPS: Dict[Tuple, SLA] = {}
 def _op(batch: int, heads: int, n: int, d: int, b_q: int, b_kv: int, cfg: SlaConfig,
         dtype: torch.dtype, device: torch.device) -> SLA:
     key = (batch, heads, n, d, b_q, b_kv, cfg.k_h, cfg.k_l, cfg.phi, cfg.mask_precision,
-           cfg.check_finite, cfg.force_generic, dtype, device)
+           cfg.check_finite, cfg.force_generic, cfg.ragged, dtype, device)
     op = _OPS.get(key)
     if op is None:
         op = SLA(batch, heads, n, d, b_q, b_kv, cfg, dtype, device)

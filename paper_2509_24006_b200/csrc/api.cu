@@ -25,12 +25,18 @@ Dims resolve(const sla_b200_problem* p) {
   if (p->batch < 1 || p->heads < 1) throw InvalidArgument("sla_b200: batch and heads must be >= 1");
   if (p->n <= 0 || p->d <= 0 || p->b_q <= 0 || p->b_kv <= 0)
     throw InvalidArgument("make_block_layout: all sizes must be positive");
-  if (p->n % p->b_q != 0)
-    throw InvalidArgument("make_block_layout: b_q=" + std::to_string(p->b_q) +
-                          " does not divide N=" + std::to_string(p->n));
-  if (p->n % p->b_kv != 0)
-    throw InvalidArgument("make_block_layout: b_kv=" + std::to_string(p->b_kv) +
-                          " does not divide N=" + std::to_string(p->n));
+  const bool ragged = (p->flags & SLA_B200_FLAG_RAGGED) && (p->n % p->b_q != 0 || p->n % p->b_kv != 0);
+  if (ragged) {
+    if (p->b_q != 64 || p->b_kv != 64 || p->dtype != SLA_B200_BF16 || (p->flags & SLA_B200_FLAG_GENERIC))
+      throw InvalidArgument("sla_b200: ragged N needs the tcgen05 path (bf16, b_q = b_kv = 64)");
+  } else {
+    if (p->n % p->b_q != 0)
+      throw InvalidArgument("make_block_layout: b_q=" + std::to_string(p->b_q) +
+                            " does not divide N=" + std::to_string(p->n));
+    if (p->n % p->b_kv != 0)
+      throw InvalidArgument("make_block_layout: b_kv=" + std::to_string(p->b_kv) +
+                            " does not divide N=" + std::to_string(p->n));
+  }
   if (!(p->k_h > 0.0 && p->k_h <= 100.0)) throw InvalidArgument("config: k_h must be in (0, 100]");
   if (!(p->k_l >= 0.0 && p->k_l < 100.0)) throw InvalidArgument("config: k_l must be in [0, 100)");
   if (p->k_h + p->k_l > 100.0) throw InvalidArgument("config: k_h + k_l must be <= 100");
@@ -43,12 +49,13 @@ Dims resolve(const sla_b200_problem* p) {
   D.B = p->batch;
   D.H = p->heads;
   D.U = p->batch * p->heads;
-  D.N = p->n;
+  D.N_valid = p->n;
+  D.N = ragged ? (p->n + 63) / 64 * 64 : p->n;
   D.d = int(p->d);
   D.bq = int(p->b_q);
   D.bkv = int(p->b_kv);
-  D.Tm = int(p->n / p->b_q);
-  D.Tn = int(p->n / p->b_kv);
+  D.Tm = int(D.N / p->b_q);
+  D.Tn = int(D.N / p->b_kv);
   D.phi = p->phi;
   if (D.Tn > 8192 || D.Tm > 65535)
     throw InvalidArgument("sla_b200: at most 8192 key blocks per row are supported");
@@ -137,6 +144,17 @@ void check_inputs(const sla_b200_problem* p, const Dims& D, const WorkBufs& w,
   }
 }
 
+// ragged N: [U, N_valid, rows] <-> [U, N, rows] (zero tail rows), `esz`-byte elements
+void pad_rows(const Dims& D, void* dst, const void* src, size_t row_bytes, cudaStream_t st) {
+  const size_t sp = size_t(D.N_valid) * row_bytes, dp = size_t(D.N) * row_bytes;
+  SLAB_CUDA(cudaMemcpy2DAsync(dst, dp, src, sp, sp, size_t(D.U), cudaMemcpyDeviceToDevice, st));
+  SLAB_CUDA(cudaMemset2DAsync(static_cast<char*>(dst) + sp, dp, 0, dp - sp, size_t(D.U), st));
+}
+void unpad_rows(const Dims& D, void* dst, const void* src, size_t row_bytes, cudaStream_t st) {
+  const size_t sp = size_t(D.N) * row_bytes, dp = size_t(D.N_valid) * row_bytes;
+  SLAB_CUDA(cudaMemcpy2DAsync(dst, dp, src, sp, dp, size_t(D.U), cudaMemcpyDeviceToDevice, st));
+}
+
 void classify_into_state(const sla_b200_problem* p, const Dims& D, const void* q, const void* k,
                          const int8_t* mask_in, double* p_c, const StateBufs& s,
                          const WorkBufs& w, cudaStream_t st) {
@@ -208,6 +226,13 @@ int sla_b200_classify(const sla_b200_problem* p, const void* q, const void* k, i
     StateBufs s;
     WorkBufs w;
     buffers(p, D, state, workspace, s, w);
+    if (D.N_valid != D.N) {
+      const size_t rb = size_t(D.d) * 2;
+      pad_rows(D, w.pad[kPQ], q, rb, st);
+      pad_rows(D, w.pad[kPK], k, rb, st);
+      q = w.pad[kPQ];
+      k = w.pad[kPK];
+    }
     if (p->flags & SLA_B200_FLAG_CHECK_FINITE) check_inputs(p, D, w, {{"Q", q}, {"K", k}}, st);
     launch_classify(D, p->dtype, p->mask_precision, q, k, s, w, p_c, st);
     if (labels && labels != s.labels)
@@ -228,6 +253,22 @@ int sla_b200_forward(const sla_b200_problem* p, const void* q, const void* k, co
     StateBufs s;
     WorkBufs wb;
     buffers(p, D, state, workspace, s, wb);
+    const bool ragged = D.N_valid != D.N;
+    void *o_u = o, *o_s_u = o_s, *o_l_u = o_l;
+    float* lse_u = lse;
+    if (ragged) {  // run on zero-padded copies; only rows < N_valid go back
+      const size_t rb = size_t(D.d) * 2;
+      pad_rows(D, wb.pad[kPQ], q, rb, st);
+      pad_rows(D, wb.pad[kPK], k, rb, st);
+      pad_rows(D, wb.pad[kPV], v, rb, st);
+      q = wb.pad[kPQ];
+      k = wb.pad[kPK];
+      v = wb.pad[kPV];
+      o = o ? wb.pad[kPO] : nullptr;
+      o_s = wb.pad[kPOs];
+      o_l = wb.pad[kPOl];
+      lse = wb.pad_lse;
+    }
     const bool check = p->flags & SLA_B200_FLAG_CHECK_FINITE;
     if (check) check_inputs(p, D, wb, {{"Q", q}, {"K", k}, {"V", v}}, st);
     classify_into_state(p, D, q, k, mask_in, nullptr, s, wb, st);
@@ -250,6 +291,13 @@ int sla_b200_forward(const sla_b200_problem* p, const void* q, const void* k, co
         }
       }
     }
+    if (ragged) {
+      const size_t rb = size_t(D.d) * 2;
+      if (o_u) unpad_rows(D, o_u, o, rb, st);
+      if (o_s_u) unpad_rows(D, o_s_u, o_s, rb, st);
+      if (o_l_u) unpad_rows(D, o_l_u, o_l, rb, st);
+      unpad_rows(D, lse_u, lse, sizeof(float), st);
+    }
   });
 }
 
@@ -269,6 +317,29 @@ int sla_b200_backward_ex(const sla_b200_problem* p, const void* q, const void* k
     WorkBufs wb;
     buffers(p, D, state, workspace, s, wb);
     const bool fast = use_fast(p, D);
+    const bool ragged = D.N_valid != D.N;
+    void *dq_u = dq, *dk_u = dk, *dv_u = dv;
+    if (ragged) {
+      if (parts) throw InvalidArgument("sla_backward: gradient parts are not available with ragged N");
+      const size_t rb = size_t(D.d) * 2;
+      pad_rows(D, wb.pad[kPQ], q, rb, st);
+      pad_rows(D, wb.pad[kPK], k, rb, st);
+      pad_rows(D, wb.pad[kPV], v, rb, st);
+      pad_rows(D, wb.pad[kPOs], o_s, rb, st);
+      pad_rows(D, wb.pad[kPOl], o_l, rb, st);
+      pad_rows(D, wb.pad[kPdO], d_out, rb, st);  // zero cotangent rows: padded queries are inert
+      pad_rows(D, wb.pad_lse, lse, sizeof(float), st);
+      q = wb.pad[kPQ];
+      k = wb.pad[kPK];
+      v = wb.pad[kPV];
+      o_s = wb.pad[kPOs];
+      o_l = wb.pad[kPOl];
+      d_out = wb.pad[kPdO];
+      lse = wb.pad_lse;
+      dq = wb.pad[kPdQ];
+      dk = wb.pad[kPdK];
+      dv = wb.pad[kPdV];
+    }
     if (fast)
       fast_backward(D, q, k, v, w, o_s, o_l, lse, d_out, dq, dk, dv, dw, s, wb, st);
     else
@@ -284,6 +355,12 @@ int sla_b200_backward_ex(const sla_b200_problem* p, const void* q, const void* k
       cp(parts->dk_sparse, wb.dk);
       cp(parts->dq_feat, wb.dqf);
       cp(parts->dk_feat, wb.dkf);
+    }
+    if (ragged) {
+      const size_t rb = size_t(D.d) * 2;
+      unpad_rows(D, dq_u, dq, rb, st);
+      unpad_rows(D, dk_u, dk, rb, st);
+      unpad_rows(D, dv_u, dv, rb, st);
     }
   });
 }

@@ -63,6 +63,7 @@ struct FwdParams {
   float scale_log2;
   int has_w;
   int phi;
+  int kv_last;  // valid keys in the last key block (64 unless ragged N)
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -370,6 +371,11 @@ __global__ void __launch_bounds__(192, 2)
       uint32_t sa[32];
       tc::tmem_ld32_x2<32>(tS0 + 64 * (t & 1) + lane_base, sa);  // my 32 of the 64 scores
       tc::tmem_ld_wait();
+      if (p.kv_last < 64 && list[t] == p.Tn - 1) {  // ragged N: keys past N get no weight
+#pragma unroll
+        for (int e = 0; e < 32; ++e)
+          if (32 * hh + e >= p.kv_last) sa[e] = __float_as_uint(-INFINITY);
+      }
       float mx = -INFINITY;
 #pragma unroll
       for (int e = 0; e < 32; ++e) mx = fmaxf(mx, __uint_as_float(sa[e]));
@@ -531,6 +537,7 @@ void launch_attn_fwd(const Dims& Dm, const void* q, const void* k, const void* v
   p.scale_log2 = float(Dm.inv_sqrt_d * 1.4426950408889634);
   p.has_w = (w != nullptr && o != nullptr) ? 1 : 0;
   p.phi = Dm.phi;
+  p.kv_last = int(Dm.N_valid - (long long)(Dm.Tn - 1) * 64);
   if (Dm.d == 128)
     launch_t<128>(Dm, q, k, v, w, s.Hb, p, st);
   else

@@ -56,7 +56,11 @@ struct WorkBufs {
   float* gZa = nullptr;          // fast path: dZ_agg [U, Tn, d]
   float* dwp = nullptr;          // fast path: split-K partials of dW [U * N / 64, d, d]
   __nv_bfloat16* dqphi = nullptr;  // fast path: dQ^phi [U, N, d] (linear kernel -> rows kernel)
+  // ragged N: the caller's [U, N_valid, d] tensors padded to [U, N, d] (zero tail rows)
+  __nv_bfloat16* pad[11] = {};     // q k v o o_s o_l dO dq dk dv (bf16), see RaggedSlot
+  float* pad_lse = nullptr;        // [U, N]
 };
+enum RaggedSlot { kPQ, kPK, kPV, kPO, kPOs, kPOl, kPdO, kPdQ, kPdK, kPdV };
 
 // split-K factor of the fast path's dW GEMM: row chunks of 64*c rows, c | N/64, c <= 32
 inline int dw_chunk_tiles(const Dims& D) {
@@ -119,6 +123,10 @@ inline void carve_work(const Dims& D, bool fast, void* base, WorkBufs& w, size_t
     w.gZa = c.take<float>(U * Tn * d);
     w.dwp = c.take<float>(U * dw_chunks(D) * d * d);
     w.dqphi = c.take<__nv_bfloat16>(U * N * d);
+    if (D.N_valid != D.N) {
+      for (int i = kPQ; i <= kPdV; ++i) w.pad[i] = c.take<__nv_bfloat16>(U * N * d);
+      w.pad_lse = c.take<float>(U * N);
+    }
   } else {  // generic SIMT path: f32 scratch for every intermediate
     w.qf = c.take<float>(U * N * d);
     w.kf = c.take<float>(U * N * d);

@@ -37,14 +37,17 @@ __global__ void k_check_finite(const In* __restrict__ x, long long total,
 // ---------------------------------------------------------------------------------------
 template <typename R, typename In>
 __global__ void k_pool(const In* __restrict__ x, R* __restrict__ out, long long N, int d, int b,
-                       int T) {
+                       int T, long long n_valid) {
   const long long u = blockIdx.y;
   const int g = blockIdx.x;
   const In* base = x + (u * N + (long long)g * b) * d;
+  // ragged N (SLA_B200_FLAG_RAGGED): the last block's mean is over its valid rows only
+  const long long left = n_valid - (long long)g * b;
+  const int rows = left < b ? int(left) : b;
   for (int c = threadIdx.x; c < d; c += blockDim.x) {
     R acc = R(0);
-    for (int r = 0; r < b; ++r) acc = add_rn(acc, R(to_f(base[(long long)r * d + c])));
-    out[(u * T + g) * d + c] = div_rn(acc, R(b));
+    for (int r = 0; r < rows; ++r) acc = add_rn(acc, R(to_f(base[(long long)r * d + c])));
+    out[(u * T + g) * d + c] = div_rn(acc, R(rows));
   }
 }
 
@@ -443,9 +446,9 @@ static void classify_t(const Dims& D, const In* q, const In* k, const StateBufs&
   R* pq = reinterpret_cast<R*>(w.pq);
   R* pk = reinterpret_cast<R*>(w.pk);
   const int pt = D.d < 256 ? ((D.d + 31) / 32) * 32 : 256;
-  k_pool<R, In><<<dim3(D.Tm, unsigned(D.U)), pt, 0, st>>>(q, pq, D.N, D.d, D.bq, D.Tm);
+  k_pool<R, In><<<dim3(D.Tm, unsigned(D.U)), pt, 0, st>>>(q, pq, D.N, D.d, D.bq, D.Tm, D.N_valid);
   check_launch("k_pool(q)", st);
-  k_pool<R, In><<<dim3(D.Tn, unsigned(D.U)), pt, 0, st>>>(k, pk, D.N, D.d, D.bkv, D.Tn);
+  k_pool<R, In><<<dim3(D.Tn, unsigned(D.U)), pt, 0, st>>>(k, pk, D.N, D.d, D.bkv, D.Tn, D.N_valid);
   check_launch("k_pool(k)", st);
   const size_t smem = classify_smem_bytes(D, sizeof(R) == 8);
   if (smem > 48 * 1024)

@@ -13,7 +13,8 @@ namespace slab {
 struct Dims {
   int64_t U;     // units = batch * heads
   int64_t B, H;  // batch, heads
-  int64_t N;     // sequence length
+  int64_t N;     // sequence length (rows per unit in the kernels' buffers; padded if ragged)
+  int64_t N_valid;  // rows per unit in the caller's tensors (== N unless SLA_B200_FLAG_RAGGED)
   int d, bq, bkv;
   int Tm, Tn;    // query / key-value block counts (layout.hpp:10-20)
   int phi;       // 0 elu1, 1 relu, 2 softmax

@@ -17,7 +17,8 @@ namespace {
 template <int D>
 __global__ void __launch_bounds__(256) k_phi_kz(const __nv_bfloat16* __restrict__ k,
                                                 __nv_bfloat16* __restrict__ kfb,
-                                                float* __restrict__ z, long long N, int Tn, int phi) {
+                                                float* __restrict__ z, long long N, int Tn, int phi,
+                                                long long n_valid) {
   constexpr int C = D / 32;
   __shared__ float zpart[8][D];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -27,11 +28,18 @@ __global__ void __launch_bounds__(256) k_phi_kz(const __nv_bfloat16* __restrict_
 #pragma unroll
   for (int c = 0; c < C; ++c) zacc[c] = 0.f;
   for (int rr = 0; rr < 8; ++rr) {
-    const long long row = u * N + (long long)j * 64 + warp * 8 + rr;
+    const long long rin = (long long)j * 64 + warp * 8 + rr;  // row within the unit
+    const long long row = u * N + rin;
     const __nv_bfloat16* src = k + row * D + lane * C;
     float x[C];
 #pragma unroll
     for (int c = 0; c < C; ++c) x[c] = __bfloat162float(src[c]);
+    if (rin >= n_valid) {  // ragged N: padded keys have no feature map (no summary weight)
+      __nv_bfloat16* dst = kfb + row * D + lane * C;
+#pragma unroll
+      for (int c = 0; c < C; ++c) dst[c] = __float2bfloat16_rn(0.f);
+      continue;
+    }
     if (phi == 2) {
       float m = -INFINITY;
 #pragma unroll
@@ -191,10 +199,10 @@ void fast_prepare_linear(const Dims& Dm, const void* k, const void* v, const Sta
   const int d = Dm.d;
   if (d == 128)
     k_phi_kz<128><<<dim3(Dm.Tn, unsigned(Dm.U)), 256, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(k), wb.kfb, wb.z, Dm.N, Dm.Tn, Dm.phi);
+        static_cast<const __nv_bfloat16*>(k), wb.kfb, wb.z, Dm.N, Dm.Tn, Dm.phi, Dm.N_valid);
   else
     k_phi_kz<64><<<dim3(Dm.Tn, unsigned(Dm.U)), 256, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(k), wb.kfb, wb.z, Dm.N, Dm.Tn, Dm.phi);
+        static_cast<const __nv_bfloat16*>(k), wb.kfb, wb.z, Dm.N, Dm.Tn, Dm.phi, Dm.N_valid);
   check_launch("k_phi_kz", st);
   // h_j = phi(K_j)^T V_j: batch = every key block, M = N = d, K = 64 tokens
   GemmArgs g{};

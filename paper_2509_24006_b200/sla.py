@@ -37,6 +37,7 @@ class SlaConfig:
     mask_precision: str = "f64"   # "f64" (reference-exact) | "f32" (north-star fp32 variant)
     check_finite: bool = False    # reproduce the reference's non-finite input/output errors
     force_generic: bool = False   # run the shape-generic SIMT kernels
+    ragged: bool = False          # allow N % 64 != 0 (SLA_B200_FLAG_RAGGED; not in the reference)
 
 
 @dataclass
@@ -63,7 +64,8 @@ def _problem(batch, heads, n, d, b_q, b_kv, cfg: SlaConfig, dtype) -> L.Problem:
     else:
         raise ValueError(f"unsupported dtype {dtype}")
     p.mask_precision = {"f64": L.MASK_F64, "f32": L.MASK_F32}[cfg.mask_precision]
-    p.flags = (L.FLAG_CHECK_FINITE if cfg.check_finite else 0) | (L.FLAG_GENERIC if cfg.force_generic else 0)
+    p.flags = ((L.FLAG_CHECK_FINITE if cfg.check_finite else 0) | (L.FLAG_GENERIC if cfg.force_generic else 0)
+               | (L.FLAG_RAGGED if cfg.ragged else 0))
     return p
 
 

@@ -209,3 +209,18 @@ def test_oracle_matches_reference_live():
         orc = O.step(q, k, v, w, do, lab, b, b, phi)
         for key in ("o_s", "o_l", "o", "dq_total", "dk_total", "dv", "dw", "dq", "dk", "dq_feat", "dk_feat"):
             assert (orc[key] == ref[key]).all(), key
+
+
+def test_ragged_predict_restatement():
+    """orc_predict_ragged (the SLA_B200_FLAG_RAGGED extension) equals predict bit for bit when
+    b divides N, and pools the partial last block over its valid rows only."""
+    rng = O.Rng(4242)
+    q, k = O.to_bf16_exact(rng.gaussian(512, 16)), O.to_bf16_exact(rng.gaussian(512, 16))
+    assert np.array_equal(O.predict_ragged(q, k, 64), O.predict(q, k, 64, 64))
+    qr, kr = q[:500], k[:500]
+    p = O.predict_ragged(qr, kr, 64)
+    pool = lambda x: np.array([x[i * 64:min(500, (i + 1) * 64)].mean(0) for i in range(8)])  # noqa: E731
+    s_ = pool(qr) @ pool(kr).T / 4.0
+    want = np.exp(s_ - s_.max(1, keepdims=True))
+    want /= want.sum(1, keepdims=True)
+    assert p.shape == (8, 8) and np.allclose(p, want, rtol=1e-12, atol=0)
