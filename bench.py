@@ -66,32 +66,60 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region.
+
+    NVML (nvidia_ml_py) is polled every ~2 ms from a thread, so even a ~70 ms timed region
+    yields dozens of samples; `nvidia-smi -lms 100` (the fallback) needs >100 ms to emit its
+    first line and missed short regions entirely."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
 
     def __init__(self, gpu_index: int):
         self.idx = gpu_index
+        self.samples = []
+        self.stop = threading.Event()
+        self.t = None
+        self.mx = None
         self.proc = None
         self.lines = []
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap,utilization.gpu")
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100",
-                 "-i", str(self.idx)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as N
+
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.idx)
+            self.mx = float(N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        self.samples.append((float(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)),
+                                             int(N.nvmlDeviceGetCurrentClocksEventReasons(h))))
+                    except Exception:
+                        pass
+                    time.sleep(0.002)
+
+            self.t = threading.Thread(target=poll, daemon=True)
             self.t.start()
         except Exception:
-            self.proc = None
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap,utilization.gpu")
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits", "-lms", "100",
+                     "-i", str(self.idx)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.t = threading.Thread(target=lambda: self.lines.extend(l.strip() for l in self.proc.stdout),
+                                          daemon=True)
+                self.t.start()
+            except Exception:
+                self.proc = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
     def __exit__(self, *a):
+        self.stop.set()
         if self.proc:
             time.sleep(0.15)
             self.proc.terminate()
@@ -99,26 +127,34 @@ class Clocks:
                 self.proc.wait(timeout=2)
             except Exception:
                 self.proc.kill()
+        elif self.t:
+            self.t.join(timeout=1)
 
     def summary(self):
-        sm, mx, reasons = [], 0.0, set()
-        for ln in self.lines:
+        sm, reasons = [], set()
+        mx = self.mx or 0.0
+        for f, bits in self.samples:
+            sm.append(f)
+            for name, bit in self.REASONS.items():
+                if bits & bit:
+                    reasons.add(name)
+        for ln in self.lines:  # nvidia-smi fallback
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 8:
                 continue
             try:
-                f, m, util = float(parts[0]), float(parts[1]), float(parts[7])
+                f, m = float(parts[0]), float(parts[1])
             except ValueError:
                 continue
             mx = max(mx, m)
-            if util > 0:
-                sm.append(f)
+            sm.append(f)
             for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"),
                                  parts[3:7]):
                 if val.lower() == "active":
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
-                "reasons": sorted(reasons), "samples": len(self.lines)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "source": "nvml" if self.samples else "nvidia-smi"}
 
 
 # ---------------------------------------------------------------------------------------

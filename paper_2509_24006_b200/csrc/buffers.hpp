@@ -56,6 +56,8 @@ struct WorkBufs {
   float* gZa = nullptr;          // fast path: dZ_agg [U, Tn, d]
   float* dwp = nullptr;          // fast path: split-K partials of dW [U * N / 64, d, d]
   __nv_bfloat16* dqphi = nullptr;  // fast path: dQ^phi [U, N, d] (linear kernel -> rows kernel)
+  __nv_bfloat16* z3b = nullptr;    // fast path: z / dZ split into 3 bf16 parts [U, T, 3d]
+  float* z3f = nullptr;            // fast path: M0 (or M0^T) times those parts, f32 [U, T, 3d]
   // ragged N: the caller's [U, N_valid, d] tensors padded to [U, N, d] (zero tail rows)
   __nv_bfloat16* pad[11] = {};     // q k v o o_s o_l dO dq dk dv (bf16), see RaggedSlot
   float* pad_lse = nullptr;        // [U, N]
@@ -123,6 +125,9 @@ inline void carve_work(const Dims& D, bool fast, void* base, WorkBufs& w, size_t
     w.gZa = c.take<float>(U * Tn * d);
     w.dwp = c.take<float>(U * dw_chunks(D) * d * d);
     w.dqphi = c.take<__nv_bfloat16>(U * N * d);
+    const size_t T = Tm > Tn ? Tm : Tn;
+    w.z3b = c.take<__nv_bfloat16>(U * T * 3 * d);
+    w.z3f = c.take<float>(U * T * 3 * d);
     if (D.N_valid != D.N) {
       for (int i = kPQ; i <= kPdV; ++i) w.pad[i] = c.take<__nv_bfloat16>(U * N * d);
       w.pad_lse = c.take<float>(U * N);

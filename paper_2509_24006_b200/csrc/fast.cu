@@ -188,6 +188,69 @@ __global__ void k_reduce_dw(const float* __restrict__ part, int chunks_per_unit,
   }
 }
 
+// Z = M0 z (and dZ_agg = M0^T dZ) on the tensor core without losing f32: z = hi + mid + lo in
+// three bf16 parts (8 + 8 + 8 significant bits cover f32's 24), M0 is an exact 0/1 bf16
+// matrix, so the GEMM's products are exact and its f32 accumulation matches an f32 sum.
+__global__ void k_split3(const float* __restrict__ x, long long rows, int d, __nv_bfloat16* __restrict__ out) {
+  const long long total = rows * d;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / d;
+    const int a = int(e % d);
+    const float v = x[e];
+    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
+    const float r1 = v - __bfloat162float(hi);
+    const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+    __nv_bfloat16* o = out + r * 3 * d + a;
+    o[0] = hi;
+    o[d] = mid;
+    o[2 * d] = lo;
+  }
+}
+__global__ void k_sum3(const float* __restrict__ x3, long long rows, int d, float* __restrict__ out) {
+  const long long total = rows * d;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long r = e / d;
+    const int a = int(e % d);
+    const float* x = x3 + r * 3 * d + a;
+    out[e] = (x[0] + x[d]) + x[2 * d];
+  }
+}
+
+// out[u] = A[u] x[u] with A = M0 (trans = false, [Tm x Tn]) or M0^T; x, out f32 [rows][d]
+void aggregate_vec_tc(const Dims& Dm, const StateBufs& s, const WorkBufs& wb, bool trans, const float* x,
+                      float* out, const char* name, cudaStream_t st) {
+  const int d = Dm.d;
+  const int Mo = trans ? Dm.Tn : Dm.Tm, Kd = trans ? Dm.Tm : Dm.Tn;
+  const long long xrows = Dm.U * (long long)Kd, orows = Dm.U * (long long)Mo;
+  const int grid = 148 * 4;
+  k_split3<<<grid, 256, 0, st>>>(x, xrows, d, wb.z3b);
+  check_launch("k_split3", st);
+  GemmArgs a{};
+  a.A = s.M0;
+  a.B = wb.z3b;
+  a.C = wb.z3f;
+  a.batch = int(Dm.U);
+  a.M = Mo;
+  a.N = 3 * d;
+  a.K = Kd;
+  a.a_mn = trans;
+  a.b_mn = true;
+  a.out_f32 = true;
+  a.lda = m0_stride(Dm);
+  a.ldb = 3LL * d;
+  a.ldc = 3LL * d;
+  a.a_batch = (long long)Dm.Tm * m0_stride(Dm);
+  a.b_batch = (long long)Kd * 3 * d;
+  a.c_batch = (long long)Mo * 3 * d;
+  a.name = name;
+  launch_gemm(a, st);
+  k_sum3<<<grid, 256, 0, st>>>(wb.z3f, orows, d, out);
+  check_launch("k_sum3", st);
+}
+
 }  // namespace
 
 bool fast_supported(const Dims& D, int dtype) {
@@ -245,9 +308,13 @@ void fast_prepare_linear(const Dims& Dm, const void* k, const void* v, const Sta
   a.c_batch = (long long)Dm.Tm * d * d;
   a.name = "gemm_aggregate";
   launch_gemm(a, st);
+#ifdef SLAB_SIMT_AGG
   k_aggregate_vec<false><<<dim3((Dm.Tm + 31) / 32, unsigned(Dm.U)), 256, 0, st>>>(s.M0, int(m0_stride(Dm)), wb.z, d,
                                                                                 Dm.Tm, Dm.Tn, s.Z);
   check_launch("k_aggregate_z", st);
+#else
+  aggregate_vec_tc(Dm, s, wb, false, wb.z, s.Z, "gemm_aggregate_z", st);
+#endif
 }
 
 void fast_forward(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
@@ -287,9 +354,13 @@ void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, 
   a.c_batch = (long long)Dm.Tn * d * d;
   a.name = "gemm_aggregate_t";
   launch_gemm(a, st);
+#ifdef SLAB_SIMT_AGG
   k_aggregate_vec<true><<<dim3((Dm.Tn + 31) / 32, unsigned(Dm.U)), 256, 0, st>>>(s.M0, int(m0_stride(Dm)), wb.gZ, d,
                                                                                Dm.Tm, Dm.Tn, wb.gZa);
   check_launch("k_aggregate_dz", st);
+#else
+  aggregate_vec_tc(Dm, s, wb, true, wb.gZ, wb.gZa, "gemm_aggregate_dz", st);
+#endif
   // columns pass: dk_total, dv
   launch_bwd_cols(Dm, q, k, v, lse, d_out, dk, dv, s, wb.hab, wb.gZa, wb.Ds, st);
   // dW = O^l^T dO per head, split-K over row chunks of each unit, then reduced over chunks + batch
