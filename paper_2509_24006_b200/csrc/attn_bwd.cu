@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
     const int grp = (warp - 2) >> 2;
     const uint32_t lane_base = uint32_t(32 * q4) << 16;
     const int tid = threadIdx.x - 64;  // 0..255
-    for (int a = tid; a < D; a += 256) zas[a] = has_lin ? p.gZa[ucol * D + a] : 0.f;
+    for (int a = tid; a < D; a += 256) zas[a] = has_lin ? tc::load_sum3(p.gZa + ucol * 3 * D + a, D) : 0.f;
     // ---- loop: thread = query row rq of the pair (S / dP lanes), 32 key columns per group
     const int rq = 32 * q4 + lane;
     for (int t = 0; t < np; ++t) {

@@ -151,7 +151,7 @@ __global__ void __launch_bounds__(192, 2)
     const uint32_t lane_base = uint32_t(32 * q4) << 16;
     const long long grow = (long long)row0 + r;
     const int tid = threadIdx.x - 64;
-    for (int a = tid; a < D; a += 128) zs[a] = has_lin ? p.Z[urow * D + a] : 0.f;
+    for (int a = tid; a < D; a += 128) zs[a] = has_lin ? tc::load_sum3(p.Z + urow * 3 * D + a, D) : 0.f;
     for (int e = tid; e < 64 * 7; e += 128)
       *reinterpret_cast<uint4*>(sDL + tc::sw128_off(e / 7, 1 + e % 7)) = make_uint4(0, 0, 0, 0);
     named_sync(1, 128);
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(192, 2)
         tc::tmem_ld_wait();
         if (!avalid) continue;
         if (c0 == D) {
-          p.gZ[urow * D + arow] = -__uint_as_float(a[0]);
+          tc::store_split3(p.z3 + urow * 3 * D + arow, D, -__uint_as_float(a[0]));
           continue;
         }
 #pragma unroll
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(192, 2)
       }
     } else {
       for (int e = tid; e < D * D / 8; e += 128) reinterpret_cast<uint4*>(gHi)[e] = make_uint4(0, 0, 0, 0);
-      for (int a = tid; a < D; a += 128) p.gZ[urow * D + a] = 0.f;
+      for (int a = tid; a < D; a += 128) tc::store_split3(p.z3 + urow * 3 * D + a, D, 0.f);
       for (int e = tid; e < 64 * D / 8; e += 128) reinterpret_cast<uint4*>(dqp)[e] = make_uint4(0, 0, 0, 0);
     }
   }
@@ -629,7 +629,7 @@ __global__ void __launch_bounds__(352, 1)
 }  // namespace
 
 void launch_bwd_lin(const Dims& Dm, const void* q, const void* w, const void* o_s, const void* o_l,
-                    const void* d_out, const StateBufs& s, __nv_bfloat16* gH, float* gZ, float* Ds,
+                    const void* d_out, const StateBufs& s, __nv_bfloat16* gH, __nv_bfloat16* z3, float* Ds,
                     __nv_bfloat16* dqphi, cudaStream_t st) {
   BwdParams p{};
   p.marg_cnt = s.marg_cnt;
@@ -638,7 +638,7 @@ void launch_bwd_lin(const Dims& Dm, const void* q, const void* w, const void* o_
   p.o_s = static_cast<const __nv_bfloat16*>(o_s);
   p.o_l = static_cast<const __nv_bfloat16*>(o_l);
   p.gH = gH;
-  p.gZ = gZ;
+  p.z3 = z3;
   p.dqphi = dqphi;
   p.N = Dm.N;
   p.Tm = Dm.Tm;

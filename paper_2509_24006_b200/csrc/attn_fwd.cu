@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(192, 2)
     auto dcol = [&](int c0) { return hh * DH + c0; };  // first column of chunk c0 of my half
     if (has_lin) {  // Z_i -> smem (one coalesced row instead of per-thread dependent loads)
       const int tid = threadIdx.x - 64;
-      if (tid < D) sZ[tid] = p.Z[urow * D + tid];
+      if (tid < D) sZ[tid] = tc::load_sum3(p.Z + urow * 3 * D + tid, D);
       asm volatile("bar.sync 1, 128;" ::: "memory");
     }
     uint32_t olp[DH / 2];  // my half row of O^l (bf16x2), kept for the projection

@@ -53,11 +53,10 @@ struct WorkBufs {
   __nv_bfloat16* hb = nullptr;   // fast path: h in bf16, [U, Tn, d*d]
   __nv_bfloat16* kfb = nullptr;  // fast path: phi(K) in bf16, [U, N, d]
   __nv_bfloat16* hab = nullptr;  // fast path: dH_agg = M0^T dH in bf16, [U, Tn, d*d]
-  float* gZa = nullptr;          // fast path: dZ_agg [U, Tn, d]
+  float* gZa = nullptr;          // fast path: dZ_agg as three partial columns [U, Tn, 3d]
   float* dwp = nullptr;          // fast path: split-K partials of dW [U * N / 64, d, d]
   __nv_bfloat16* dqphi = nullptr;  // fast path: dQ^phi [U, N, d] (linear kernel -> rows kernel)
-  __nv_bfloat16* z3b = nullptr;    // fast path: z / dZ split into 3 bf16 parts [U, T, 3d]
-  float* z3f = nullptr;            // fast path: M0 (or M0^T) times those parts, f32 [U, T, 3d]
+  __nv_bfloat16* z3b = nullptr;    // fast path: z_j / dZ_i split into 3 bf16 parts [U, T, 3d]
   // ragged N: the caller's [U, N_valid, d] tensors padded to [U, N, d] (zero tail rows)
   __nv_bfloat16* pad[11] = {};     // q k v o o_s o_l dO dq dk dv (bf16), see RaggedSlot
   float* pad_lse = nullptr;        // [U, N]
@@ -97,7 +96,7 @@ inline void carve_state(const Dims& D, bool fast, void* base, StateBufs& s, size
   s.ccol_cnt = c.take<int>(U * Tn);
   s.ccol_idx = c.take<int>(U * Tn * Tm);
   s.ccol_marg = c.take<int>(U * Tn);
-  s.Z = c.take<float>(U * Tm * d);
+  s.Z = c.take<float>(U * Tm * d * (fast ? 3 : 1));  // fast path: three partial columns
   if (fast) {
     s.Hb = c.take<__nv_bfloat16>(U * Tm * d * d);
     s.M0 = c.take<__nv_bfloat16>(U * Tm * ((Tn + 7) / 8 * 8));
@@ -122,12 +121,11 @@ inline void carve_work(const Dims& D, bool fast, void* base, WorkBufs& w, size_t
     w.hb = c.take<__nv_bfloat16>(U * Tn * d * d);
     w.kfb = c.take<__nv_bfloat16>(U * N * d);
     w.hab = c.take<__nv_bfloat16>(U * Tn * d * d);
-    w.gZa = c.take<float>(U * Tn * d);
+    w.gZa = c.take<float>(U * Tn * 3 * d);
     w.dwp = c.take<float>(U * dw_chunks(D) * d * d);
     w.dqphi = c.take<__nv_bfloat16>(U * N * d);
     const size_t T = Tm > Tn ? Tm : Tn;
     w.z3b = c.take<__nv_bfloat16>(U * T * 3 * d);
-    w.z3f = c.take<float>(U * T * 3 * d);
     if (D.N_valid != D.N) {
       for (int i = kPQ; i <= kPdV; ++i) w.pad[i] = c.take<__nv_bfloat16>(U * N * d);
       w.pad_lse = c.take<float>(U * N);

@@ -95,8 +95,8 @@ struct BwdParams {
   const __nv_bfloat16* o_l;
   __nv_bfloat16* gH;   // [U, Tm, D, D] dH_i (linear kernel out)
   __nv_bfloat16* dqphi;  // [U, N, D] dQ^phi (linear kernel out, rows kernel in)
-  float* gZ;           // [U, Tm, D] dZ_i
-  const float* gZa;    // [U, Tn, D] dZ_agg (cols kernel in)
+  __nv_bfloat16* z3;   // [U, Tm, 3D] dZ_i in 3 bf16 parts (B operand of dZ_agg = M0^T dZ)
+  const float* gZa;    // [U, Tn, 3D] dZ_agg as three partial columns (cols kernel in)
   int* has_lin_col;    // unused
   __nv_bfloat16* dq;   // outputs
   __nv_bfloat16* dk;

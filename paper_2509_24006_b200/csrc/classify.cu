@@ -63,52 +63,50 @@ __global__ void k_pool(const In* __restrict__ x, R* __restrict__ out, long long 
 // with separately rounded mul and add (mat.hpp:83-97), so the values are bit-identical to
 // the reference's; tiling only shares the pooled rows through shared memory.
 template <typename R>
-__global__ void __launch_bounds__(64) k_scores(const R* __restrict__ pq, const R* __restrict__ pk,
-                                               int d, int Tm, int Tn, R inv_sqrt_d,
-                                               R* __restrict__ s) {
-  // 64 threads, each an 8 x 8 patch; chunks of CK pooled columns staged transposed
-  // ([c][row]) so a thread's 8 rows / 8 columns are 4 vector loads each.
+__global__ void __launch_bounds__(256) k_scores(const R* __restrict__ pq, const R* __restrict__ pk,
+                                                int d, int Tm, int Tn, R inv_sqrt_d,
+                                                R* __restrict__ s) {
   constexpr int CK = 32;
-  __shared__ __align__(16) R sa[CK][64];
-  __shared__ __align__(16) R sb[CK][64];
+  __shared__ R sa[64][CK + 1];
+  __shared__ R sb[64][CK + 1];
   const long long u = blockIdx.z;
   const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
-  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;
-  R acc[8][8];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  R acc[4][4];
 #pragma unroll
-  for (int a = 0; a < 8; ++a)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 8; ++b) acc[a][b] = R(0);
+    for (int b = 0; b < 4; ++b) acc[a][b] = R(0);
   const R* pqu = pq + u * (long long)Tm * d;
   const R* pku = pk + u * (long long)Tn * d;
   for (int c0 = 0; c0 < d; c0 += CK) {
     const int ck = min(CK, d - c0);
     __syncthreads();
-    for (int e = threadIdx.x; e < 64 * CK; e += 64) {
+    for (int e = threadIdx.x; e < 64 * CK; e += 256) {
       const int r = e / CK, c = e % CK;
-      sa[c][r] = (i0 + r < Tm && c < ck) ? pqu[(long long)(i0 + r) * d + c0 + c] : R(0);
-      sb[c][r] = (j0 + r < Tn && c < ck) ? pku[(long long)(j0 + r) * d + c0 + c] : R(0);
+      sa[r][c] = (i0 + r < Tm && c < ck) ? pqu[(long long)(i0 + r) * d + c0 + c] : R(0);
+      sb[r][c] = (j0 + r < Tn && c < ck) ? pku[(long long)(j0 + r) * d + c0 + c] : R(0);
     }
     __syncthreads();
     for (int c = 0; c < ck; ++c) {
-      R av[8], bv[8];
+      R av[4], bv[4];
 #pragma unroll
-      for (int a = 0; a < 8; ++a) av[a] = sa[c][ty * 8 + a];
+      for (int a = 0; a < 4; ++a) av[a] = sa[ty * 4 + a][c];
 #pragma unroll
-      for (int b = 0; b < 8; ++b) bv[b] = sb[c][tx * 8 + b];
+      for (int b = 0; b < 4; ++b) bv[b] = sb[tx * 4 + b][c];
 #pragma unroll
-      for (int a = 0; a < 8; ++a)
+      for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 8; ++b) acc[a][b] = add_rn(acc[a][b], mul_rn(av[a], bv[b]));
+        for (int b = 0; b < 4; ++b) acc[a][b] = add_rn(acc[a][b], mul_rn(av[a], bv[b]));
     }
   }
 #pragma unroll
-  for (int a = 0; a < 8; ++a) {
-    const int i = i0 + ty * 8 + a;
+  for (int a = 0; a < 4; ++a) {
+    const int i = i0 + ty * 4 + a;
     if (i >= Tm) continue;
 #pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const int j = j0 + tx * 8 + b;
+    for (int b = 0; b < 4; ++b) {
+      const int j = j0 + tx * 4 + b;
       if (j < Tn) s[(u * Tm + i) * (long long)Tn + j] = mul_rn(acc[a][b], inv_sqrt_d);
     }
   }
@@ -457,7 +455,7 @@ static void classify_t(const Dims& D, const In* q, const In* k, const StateBufs&
     SLAB_CUDA(cudaFuncSetAttribute(k_classify<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(smem)));
   R* scores = reinterpret_cast<R*>(w.p_c);
-  k_scores<R><<<dim3((D.Tn + 63) / 64, (D.Tm + 63) / 64, unsigned(D.U)), 64, 0, st>>>(
+  k_scores<R><<<dim3((D.Tn + 63) / 64, (D.Tm + 63) / 64, unsigned(D.U)), 256, 0, st>>>(
       pq, pk, D.d, D.Tm, D.Tn, R(D.inv_sqrt_d), scores);
   check_launch("k_scores", st);
   const int P2 = next_pow2(D.Tn);

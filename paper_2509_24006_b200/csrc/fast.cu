@@ -17,7 +17,7 @@ namespace {
 template <int D>
 __global__ void __launch_bounds__(256) k_phi_kz(const __nv_bfloat16* __restrict__ k,
                                                 __nv_bfloat16* __restrict__ kfb,
-                                                float* __restrict__ z, long long N, int Tn, int phi,
+                                                __nv_bfloat16* __restrict__ z3b, long long N, int Tn, int phi,
                                                 long long n_valid) {
   constexpr int C = D / 32;
   __shared__ float zpart[8][D];
@@ -73,104 +73,7 @@ __global__ void __launch_bounds__(256) k_phi_kz(const __nv_bfloat16* __restrict_
     float s = 0.f;
 #pragma unroll
     for (int w = 0; w < 8; ++w) s += zpart[w][a];
-    z[(u * Tn + j) * D + a] = s;
-  }
-}
-
-// Marginal aggregation of the per-block vectors as a tiled fp32 GEMM with the 0/1 marginal
-// indicator M0 (bf16, the A operand of the H GEMM): Z = M0 z (forward, aggregation.cpp:40-56)
-// or dZ_agg = M0^T dZ (backward, backward.cpp:170-178).  grid (ceil(T_out/32), U); 256
-// threads, 32 output rows x d (<= 128) columns per CTA, 2 rows x 8 columns per thread; K (the
-// block index) staged 64 at a time with coalesced 16-byte loads of M0 and x.
-template <bool kTrans>
-__global__ void __launch_bounds__(256) k_aggregate_vec(const __nv_bfloat16* __restrict__ m0, int ld,
-                                                       const float* __restrict__ x, int d, int Tm,
-                                                       int Tn, float* __restrict__ out) {
-  constexpr int BM = 32, BK = 64;
-  __shared__ __align__(16) float sa[BK][BM];   // indicator tile, [k][m]
-  __shared__ __align__(16) float sx[BK][128];  // x tile, [k][a]
-  const long long u = blockIdx.y;
-  const int m0r = blockIdx.x * BM;
-  const int Mo = kTrans ? Tn : Tm, Kd = kTrans ? Tm : Tn;
-  const __nv_bfloat16* mu = m0 + u * (long long)Tm * ld;
-  const float* xu = x + u * (long long)Kd * d;
-  const int tid = threadIdx.x;
-  const int ty = tid >> 4, tx = tid & 15;  // rows 2*ty, 2*ty+1; columns 4*tx.. and 64+4*tx..
-  float acc[2][8];
-#pragma unroll
-  for (int i = 0; i < 2; ++i)
-#pragma unroll
-    for (int c = 0; c < 8; ++c) acc[i][c] = 0.f;
-  // chunk k0 is staged from registers loaded during chunk k0 - BK (software pipelining)
-  uint4 ra;
-  float4 rx[8];
-  auto load = [&](int k0) {
-    ra = make_uint4(0, 0, 0, 0);
-    if (!kTrans) {  // A[m][k] = M0[m][k]: row m = tid/8, k chunk 8*(tid%8)
-      const int gm = m0r + (tid >> 3), gk = k0 + 8 * (tid & 7);
-      if (gm < Mo && gk < ld) ra = *reinterpret_cast<const uint4*>(mu + (long long)gm * ld + gk);
-    } else {  // A[m][k] = M0[k][m]: row k = tid/4, m chunk 8*(tid%4)
-      const int gk = k0 + (tid >> 2), gm = m0r + 8 * (tid & 3);
-      if (gk < Kd && gm < ld) ra = *reinterpret_cast<const uint4*>(mu + (long long)gk * ld + gm);
-    }
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {  // x: 64 rows x 128 columns as float4, 8 per thread
-      const int e = tid + 256 * r;
-      const int kk = e >> 5, a4 = 4 * (e & 31);
-      rx[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (k0 + kk < Kd && a4 < d) rx[r] = *reinterpret_cast<const float4*>(xu + (long long)(k0 + kk) * d + a4);
-    }
-  };
-  load(0);
-  for (int k0 = 0; k0 < Kd; k0 += BK) {
-    __syncthreads();
-    {
-      float v[8];
-      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&ra);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = __bfloat1622float2(h2[e]);
-        v[2 * e] = f.x;
-        v[2 * e + 1] = f.y;
-      }
-      if (!kTrans) {
-        const int m = tid >> 3, kc = 8 * (tid & 7);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) sa[kc + e][m] = k0 + kc + e < Kd ? v[e] : 0.f;
-      } else {
-        const int kk = tid >> 2, mc = 8 * (tid & 3);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) sa[kk][mc + e] = m0r + mc + e < Mo ? v[e] : 0.f;
-      }
-#pragma unroll
-      for (int r = 0; r < 8; ++r) {
-        const int e = tid + 256 * r;
-        *reinterpret_cast<float4*>(&sx[e >> 5][4 * (e & 31)]) = rx[r];
-      }
-    }
-    __syncthreads();
-    if (k0 + BK < Kd) load(k0 + BK);
-#pragma unroll 8
-    for (int kk = 0; kk < BK; ++kk) {
-      const float2 w = *reinterpret_cast<const float2*>(&sa[kk][2 * ty]);
-      const float4 x0 = *reinterpret_cast<const float4*>(&sx[kk][4 * tx]);
-      const float4 x1 = *reinterpret_cast<const float4*>(&sx[kk][64 + 4 * tx]);
-      const float xv[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
-#pragma unroll
-      for (int c = 0; c < 8; ++c) {
-        acc[0][c] = fmaf(w.x, xv[c], acc[0][c]);
-        acc[1][c] = fmaf(w.y, xv[c], acc[1][c]);
-      }
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const int gm = m0r + 2 * ty + i;
-    if (gm >= Mo) continue;
-    float* orow = out + (u * Mo + gm) * d;
-    if (4 * tx < d) *reinterpret_cast<float4*>(orow + 4 * tx) = make_float4(acc[i][0], acc[i][1], acc[i][2], acc[i][3]);
-    if (64 + 4 * tx < d)
-      *reinterpret_cast<float4*>(orow + 64 + 4 * tx) = make_float4(acc[i][4], acc[i][5], acc[i][6], acc[i][7]);
+    tc::store_split3(z3b + (u * Tn + j) * 3 * D + a, D, s);  // z_j in 3 bf16 parts
   }
 }
 
@@ -188,50 +91,18 @@ __global__ void k_reduce_dw(const float* __restrict__ part, int chunks_per_unit,
   }
 }
 
-// Z = M0 z (and dZ_agg = M0^T dZ) on the tensor core without losing f32: z = hi + mid + lo in
-// three bf16 parts (8 + 8 + 8 significant bits cover f32's 24), M0 is an exact 0/1 bf16
-// matrix, so the GEMM's products are exact and its f32 accumulation matches an f32 sum.
-__global__ void k_split3(const float* __restrict__ x, long long rows, int d, __nv_bfloat16* __restrict__ out) {
-  const long long total = rows * d;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long r = e / d;
-    const int a = int(e % d);
-    const float v = x[e];
-    const __nv_bfloat16 hi = __float2bfloat16_rn(v);
-    const float r1 = v - __bfloat162float(hi);
-    const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
-    const __nv_bfloat16 lo = __float2bfloat16_rn(r1 - __bfloat162float(mid));
-    __nv_bfloat16* o = out + r * 3 * d + a;
-    o[0] = hi;
-    o[d] = mid;
-    o[2 * d] = lo;
-  }
-}
-__global__ void k_sum3(const float* __restrict__ x3, long long rows, int d, float* __restrict__ out) {
-  const long long total = rows * d;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const long long r = e / d;
-    const int a = int(e % d);
-    const float* x = x3 + r * 3 * d + a;
-    out[e] = (x[0] + x[d]) + x[2 * d];
-  }
-}
-
-// out[u] = A[u] x[u] with A = M0 (trans = false, [Tm x Tn]) or M0^T; x, out f32 [rows][d]
-void aggregate_vec_tc(const Dims& Dm, const StateBufs& s, const WorkBufs& wb, bool trans, const float* x,
-                      float* out, const char* name, cudaStream_t st) {
+// Z3 = M0 [z_hi | z_mid | z_lo] (trans: M0^T [dZ parts]) on the tensor core: the z parts are
+// written by their producers (k_phi_kz, k_bwd_lin) with tc::store_split3, M0 is an exact 0/1
+// bf16 matrix, so products are exact and the f32 accumulation matches an f32 sum; consumers
+// add the three output columns back (tc::load_sum3).
+void aggregate_vec_tc(const Dims& Dm, const StateBufs& s, const WorkBufs& wb, bool trans, float* out3,
+                      const char* name, cudaStream_t st) {
   const int d = Dm.d;
   const int Mo = trans ? Dm.Tn : Dm.Tm, Kd = trans ? Dm.Tm : Dm.Tn;
-  const long long xrows = Dm.U * (long long)Kd, orows = Dm.U * (long long)Mo;
-  const int grid = 148 * 4;
-  k_split3<<<grid, 256, 0, st>>>(x, xrows, d, wb.z3b);
-  check_launch("k_split3", st);
   GemmArgs a{};
   a.A = s.M0;
   a.B = wb.z3b;
-  a.C = wb.z3f;
+  a.C = out3;
   a.batch = int(Dm.U);
   a.M = Mo;
   a.N = 3 * d;
@@ -247,8 +118,6 @@ void aggregate_vec_tc(const Dims& Dm, const StateBufs& s, const WorkBufs& wb, bo
   a.c_batch = (long long)Mo * 3 * d;
   a.name = name;
   launch_gemm(a, st);
-  k_sum3<<<grid, 256, 0, st>>>(wb.z3f, orows, d, out);
-  check_launch("k_sum3", st);
 }
 
 }  // namespace
@@ -262,10 +131,10 @@ void fast_prepare_linear(const Dims& Dm, const void* k, const void* v, const Sta
   const int d = Dm.d;
   if (d == 128)
     k_phi_kz<128><<<dim3(Dm.Tn, unsigned(Dm.U)), 256, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(k), wb.kfb, wb.z, Dm.N, Dm.Tn, Dm.phi, Dm.N_valid);
+        static_cast<const __nv_bfloat16*>(k), wb.kfb, wb.z3b, Dm.N, Dm.Tn, Dm.phi, Dm.N_valid);
   else
     k_phi_kz<64><<<dim3(Dm.Tn, unsigned(Dm.U)), 256, 0, st>>>(
-        static_cast<const __nv_bfloat16*>(k), wb.kfb, wb.z, Dm.N, Dm.Tn, Dm.phi, Dm.N_valid);
+        static_cast<const __nv_bfloat16*>(k), wb.kfb, wb.z3b, Dm.N, Dm.Tn, Dm.phi, Dm.N_valid);
   check_launch("k_phi_kz", st);
   // h_j = phi(K_j)^T V_j: batch = every key block, M = N = d, K = 64 tokens
   GemmArgs g{};
@@ -308,13 +177,7 @@ void fast_prepare_linear(const Dims& Dm, const void* k, const void* v, const Sta
   a.c_batch = (long long)Dm.Tm * d * d;
   a.name = "gemm_aggregate";
   launch_gemm(a, st);
-#ifdef SLAB_SIMT_AGG
-  k_aggregate_vec<false><<<dim3((Dm.Tm + 31) / 32, unsigned(Dm.U)), 256, 0, st>>>(s.M0, int(m0_stride(Dm)), wb.z, d,
-                                                                                Dm.Tm, Dm.Tn, s.Z);
-  check_launch("k_aggregate_z", st);
-#else
-  aggregate_vec_tc(Dm, s, wb, false, wb.z, s.Z, "gemm_aggregate_z", st);
-#endif
+  aggregate_vec_tc(Dm, s, wb, false, s.Z, "gemm_aggregate_z", st);  // s.Z: [U, Tm, 3d]
 }
 
 void fast_forward(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
@@ -332,7 +195,7 @@ void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, 
   launch_build_csc(Dm, s, st);
   // row phase: the linear branch (dH_i reusing the forward's h scratch, dZ_i, D^s, dQ^phi),
   // then the sparse dQ over critical pairs with dq_total = J_phi^T dQ^phi + dQ
-  launch_bwd_lin(Dm, q, w, o_s, o_l, d_out, s, wb.hb, wb.gZ, wb.Ds, wb.dqphi, st);
+  launch_bwd_lin(Dm, q, w, o_s, o_l, d_out, s, wb.hb, wb.z3b, wb.Ds, wb.dqphi, st);
   launch_bwd_rows(Dm, q, k, v, lse, d_out, dq, s, wb.Ds, wb.dqphi, st);
   // dH_agg = M0^T dH (A = M0 read M-major), dZ_agg
   GemmArgs a{};
@@ -354,13 +217,7 @@ void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, 
   a.c_batch = (long long)Dm.Tn * d * d;
   a.name = "gemm_aggregate_t";
   launch_gemm(a, st);
-#ifdef SLAB_SIMT_AGG
-  k_aggregate_vec<true><<<dim3((Dm.Tn + 31) / 32, unsigned(Dm.U)), 256, 0, st>>>(s.M0, int(m0_stride(Dm)), wb.gZ, d,
-                                                                               Dm.Tm, Dm.Tn, wb.gZa);
-  check_launch("k_aggregate_dz", st);
-#else
-  aggregate_vec_tc(Dm, s, wb, true, wb.gZ, wb.gZa, "gemm_aggregate_dz", st);
-#endif
+  aggregate_vec_tc(Dm, s, wb, true, wb.gZa, "gemm_aggregate_dz", st);  // gZa: [U, Tn, 3d]
   // columns pass: dk_total, dv
   launch_bwd_cols(Dm, q, k, v, lse, d_out, dk, dv, s, wb.hab, wb.gZa, wb.Ds, st);
   // dW = O^l^T dO per head, split-K over row chunks of each unit, then reduced over chunks + batch

@@ -45,7 +45,7 @@ void launch_attn_fwd(const Dims& Dm, const void* q, const void* k, const void* v
 void fast_prepare_linear(const Dims& Dm, const void* k, const void* v, const StateBufs& s,
                          const WorkBufs& wb, cudaStream_t st);
 void launch_bwd_lin(const Dims& Dm, const void* q, const void* w, const void* o_s, const void* o_l,
-                    const void* d_out, const StateBufs& s, __nv_bfloat16* gH, float* gZ, float* Ds,
+                    const void* d_out, const StateBufs& s, __nv_bfloat16* gH, __nv_bfloat16* z3, float* Ds,
                     __nv_bfloat16* dqphi, cudaStream_t st);
 void launch_bwd_rows(const Dims& Dm, const void* q, const void* k, const void* v, const float* lse,
                      const void* d_out, void* dq, const StateBufs& s, const float* Ds,

@@ -311,6 +311,19 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
+// f32 x as three bf16 parts hi + mid + lo (24 significant bits, = f32 for normal x): the B
+// operand of the exact 0/1 aggregation GEMMs Z = M0 z, dZ_agg = M0^T dZ; parts land d apart
+__device__ __forceinline__ void store_split3(__nv_bfloat16* dst, int d, float x) {
+  const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+  const float r1 = x - __bfloat162float(hi);
+  const __nv_bfloat16 mid = __float2bfloat16_rn(r1);
+  dst[0] = hi;
+  dst[d] = mid;
+  dst[2 * d] = __float2bfloat16_rn(r1 - __bfloat162float(mid));
+}
+// the f32 aggregate back from the GEMM's three partial columns
+__device__ __forceinline__ float load_sum3(const float* src, int d) { return (src[0] + src[d]) + src[2 * d]; }
+
 // Byte offset of 16-byte chunk `c` (0..7) of row `r` inside a SW128 atom-tiled buffer whose
 // rows are 128 B: the hardware XORs the chunk index with (row % 8).
 __device__ __forceinline__ uint32_t sw128_off(uint32_t r, uint32_t c) {
