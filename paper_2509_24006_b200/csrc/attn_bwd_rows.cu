@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(192, 2)
     k_bwd_lin(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
               const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmH,
               const __grid_constant__ CUtensorMap tmOS, const __grid_constant__ CUtensorMap tmOL,
-              BwdParams p) {
+              const __grid_constant__ CUtensorMap tmGH, BwdParams p) {
   using L = LinLayout<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -256,13 +256,22 @@ __global__ void __launch_bounds__(192, 2)
           tc::store_split3(p.z3 + urow * 3 * D + arow, D, -__uint_as_float(a[0]));
           continue;
         }
+        // dH_i row arow -> SW128 staging boxes [D rows][64 cols] in the dead Q / dO tiles
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           float f[8];
 #pragma unroll
           for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(a[8 * c + e]);
-          *reinterpret_cast<uint4*>(gHi + arow * D + c0 + 8 * c) = pack8(f);
+          const int col = c0 + 8 * c;
+          tc::sts_u4(tc::smem_u32(sQ) + (col >> 6) * (D * 128) + tc::sw128_off(arow, (col >> 3) & 7), pack8(f));
         }
+      }
+      tc::fence_proxy_async();
+      named_sync(1, 128);
+      if (tid == 0) {  // coalesced: one TMA store per 64-column box
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) tc::tma_store_3d(&tmGH, sQ + c * (D * 128), 64 * c, int(urow * D), 0);
+        tc::bulk_commit();
       }
       // dQ^phi[r][a] = raw^T[a][r] - (D^l/den)_r Z[a]; stage as a row-major bf16 tile in sX
       // (phi(Q) is dead once lin_done fired), then store coalesced rows
@@ -285,6 +294,7 @@ __global__ void __launch_bounds__(192, 2)
         const int rr = e / (D / 8), cc = (e % (D / 8)) * 8;
         *reinterpret_cast<uint4*>(dqp + (long long)rr * D + cc) = *reinterpret_cast<const uint4*>(sX + tile_off(rr, cc));
       }
+      if (tid == 0) tc::bulk_wait<0>();  // dH_i stores have read the staging smem
     } else {
       for (int e = tid; e < D * D / 8; e += 128) reinterpret_cast<uint4*>(gHi)[e] = make_uint4(0, 0, 0, 0);
       for (int a = tid; a < D; a += 128) tc::store_split3(p.z3 + urow * 3 * D + a, D, 0.f);
@@ -646,7 +656,7 @@ void launch_bwd_lin(const Dims& Dm, const void* q, const void* w, const void* o_
   p.H = int(Dm.H);
   p.phi = Dm.phi;
   const uint64_t rows = uint64_t(Dm.U) * Dm.N;
-  CUtensorMap tq, tdo, tw, th, tos, tol;
+  CUtensorMap tq, tdo, tw, th, tos, tol, tgh;
   auto go = [&](auto kern, int bytes, auto dd) {
     constexpr int D = decltype(dd)::value;
     make_tmap_bf16(&tq, q, D, rows, 1, D, 0, 64);
@@ -655,8 +665,9 @@ void launch_bwd_lin(const Dims& Dm, const void* q, const void* w, const void* o_
     make_tmap_bf16(&th, s.Hb, D, uint64_t(Dm.U) * Dm.Tm * D, 1, D, 0, D);
     make_tmap_bf16(&tos, o_s, D, rows, 1, D, 0, 64);
     make_tmap_bf16(&tol, o_l, D, rows, 1, D, 0, 64);
+    make_tmap_bf16(&tgh, gH, D, uint64_t(Dm.U) * Dm.Tm * D, 1, D, 0, D);  // dH_i boxes [D rows][64]
     SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    kern<<<dim3(Dm.Tm, unsigned(Dm.U)), 192, bytes, st>>>(tq, tdo, tw, th, tos, tol, p);
+    kern<<<dim3(Dm.Tm, unsigned(Dm.U)), 192, bytes, st>>>(tq, tdo, tw, th, tos, tol, tgh, p);
     check_launch("k_bwd_lin", st);
   };
   if (Dm.d == 128)
