@@ -323,8 +323,13 @@ struct RowsLayout {
   static_assert(kBytes <= 232448, "smem");
 };
 
+#ifndef SLAB_ROWS_2ISSUE
+#define SLAB_ROWS_2ISSUE 1  // S/dP and dQ issued by two MMA warps (1, 11)
+#endif
+constexpr int kRowsThreads = SLAB_ROWS_2ISSUE ? 384 : 352;
+
 template <int D>
-__global__ void __launch_bounds__(352, 1)
+__global__ void __launch_bounds__(kRowsThreads, 1)
     k_bwd_rows(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
                const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                BwdParams p) {
@@ -344,6 +349,7 @@ __global__ void __launch_bounds__(352, 1)
   uint64_t* ds_full = bars + 3;
   uint64_t* ds_empty = bars + 4;
   uint64_t* dq_done = bars + 5;
+  uint64_t* sdp_free = bars + 6;   // [2] compute warps have read S^T|dP^T buffer t&1 (2-issuer mode)
   uint64_t* k_full = bars + 8;     // [KS]
   uint64_t* k_empty = bars + 11;   // [KS]
   uint64_t* v_full = bars + 14;    // [VS]
@@ -365,7 +371,10 @@ __global__ void __launch_bounds__(352, 1)
   if (warp == 0) {
     if (lane == 0) {
       tc::mbar_init(qdo_full, 1);
-      for (int s = 0; s < 2; ++s) tc::mbar_init(sdp_full + s, 1);
+      for (int s = 0; s < 2; ++s) {
+        tc::mbar_init(sdp_full + s, 1);
+        tc::mbar_init(sdp_free + s, 8);
+      }
       tc::mbar_init(ds_full, 8);
       tc::mbar_init(ds_empty, 1);
       tc::mbar_init(dq_done, 1);
@@ -474,6 +483,15 @@ __global__ void __launch_bounds__(352, 1)
       tc::mma_commit_w(v_empty + vs);
       ts_mark(dbg && lane == 0 && t < 16, 208 + t);
     };
+    if (SLAB_ROWS_2ISSUE) {
+      // S^T/dP^T(t) as soon as its K / V pair landed and the softmax-gradient warps have read
+      // TMEM buffer t&1 (sdp_free of t-2); dQ is issued by warp 11 independently
+      for (int t = 0; t < np; ++t) {
+        if (t >= 2) tc::mbar_wait(sdp_free + (t & 1), ((t - 2) >> 1) & 1);
+        issue_sdp(t);
+      }
+      __syncwarp();
+    } else {
     if (np > 0) issue_sdp(0);
     if (np > 1) issue_sdp(1);
     for (int t = 0; t < np; ++t) {
@@ -491,6 +509,27 @@ __global__ void __launch_bounds__(352, 1)
       tc::mma_commit_w(ds_empty);
       ts_mark(dbg && lane == 0 && t < 16, 224 + t);
       if (t + 2 < np) issue_sdp(t + 2);
+    }
+    tc::mma_commit_w(dq_done);
+    __syncwarp();
+    }
+  } else if (SLAB_ROWS_2ISSUE && warp == 11) {
+    // dQ^T += [K_j1; K_j2]^T dS^T  (M = D, N = 64, K = 128) as soon as dS(t) is in smem
+    tc::mbar_wait(qdo_full, 0);
+    const uint64_t dKm = tc::desc_mnmajor(tc::smem_u32(sK), 16384);
+    const uint64_t dDSm = tc::desc_mnmajor(tc::smem_u32(sDS), 16384);
+    constexpr uint32_t id_dqt = tc::idesc_bf16(D, 64, true, true);
+    for (int t = 0; t < np; ++t) {
+      tc::mbar_wait(ds_full, t & 1);
+      tc::tc_fence_after();
+      ts_mark(dbg && lane == 0 && t < 16, 64 + t);
+      const uint64_t dk = tc::desc_add(dKm, (t % L::KS) * L::kP);
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        tc::mma_bf16_w(tDQT, tc::desc_add(dk, kk * 2048), tc::desc_add(dDSm, kk * 2048), id_dqt, (t | kk) != 0);
+      tc::mma_commit_w(k_empty + (t % L::KS));
+      tc::mma_commit_w(ds_empty);
+      ts_mark(dbg && lane == 0 && t < 16, 224 + t);
     }
     tc::mma_commit_w(dq_done);
     __syncwarp();
@@ -517,6 +556,11 @@ __global__ void __launch_bounds__(352, 1)
         tc::tmem_ld32(tb, sv);
         tc::tmem_ld32(tb + 64, dp);
         tc::tmem_ld_wait();
+        if (SLAB_ROWS_2ISSUE) {  // TMEM buffer t&1 may take S/dP(t+2)
+          tc::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(sdp_free + (t & 1));
+        }
         // dS = P (dP - D^s) / sqrt(d) with P = exp2(S log2e / sqrt(d) - lse log2e); the
         // per-query constants (lse log2e, D^s / sqrt(d)) are shared-space vector loads
         ts_mark(dbg && threadIdx.x == 64 && t < 16, 240 + t);
@@ -702,7 +746,7 @@ void launch_bwd_rows(const Dims& Dm, const void* q, const void* k, const void* v
     make_tmap_bf16(&tk, k, D, rows, 1, D, 0, 64);
     make_tmap_bf16(&tv, v, D, rows, 1, D, 0, 64);
     SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    kern<<<dim3(Dm.Tm, unsigned(Dm.U)), 352, bytes, st>>>(tq, tdo, tk, tv, p);
+    kern<<<dim3(Dm.Tm, unsigned(Dm.U)), kRowsThreads, bytes, st>>>(tq, tdo, tk, tv, p);
     check_launch("k_bwd_rows", st);
   };
   if (Dm.d == 128)
