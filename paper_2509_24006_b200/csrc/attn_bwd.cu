@@ -41,8 +41,12 @@ struct ColsLayout {
 #ifndef SLAB_COLS_PROD
 #define SLAB_COLS_PROD 2
 #endif
+#ifndef SLAB_COLS_2ISSUE
+#define SLAB_COLS_2ISSUE 1  // S/dP (warp 1) and the dV/dK accumulation (last warp) issued separately
+#endif
 constexpr int kColsProd = SLAB_COLS_PROD;  // TMA producer warps (2 or 4)
-constexpr int kColsThreads = 32 * (10 + kColsProd - 1);
+constexpr int kAccWarp = 10 + kColsProd - 1;  // accumulation issuer in 2-issuer mode
+constexpr int kColsThreads = 32 * (kAccWarp + (SLAB_COLS_2ISSUE ? 1 : 0));
 
 template <int D>
 __global__ void __launch_bounds__(kColsThreads, 1)
@@ -67,6 +71,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
   uint64_t* acc_done = bars + 7;
   uint64_t* kf_ready = bars + 8;
   uint64_t* all_done = bars + 9;
+  uint64_t* sdp_free = bars + 10;  // [2] (2-issuer mode) compute warps have read S|dP buffer t&1
   uint64_t* ring_full = bars + 16;        // [RS]
   uint64_t* ring_empty = bars + 16 + RS;  // [RS]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + 2 * RS);
@@ -98,6 +103,8 @@ __global__ void __launch_bounds__(kColsThreads, 1)
         tc::mbar_init(pd_empty + s, 1);
       }
       tc::mbar_init(acc_done, 1);
+      tc::mbar_init(sdp_free, 8);
+      tc::mbar_init(sdp_free + 1, 8);
       tc::mbar_init(kf_ready, 8);
       tc::mbar_init(all_done, 1);
       tc::fence_barrier_init();
@@ -113,7 +120,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
   // dK^phi^T at [384, 448) (M = D)
   const uint32_t tDVT = tmem, tDKT = tmem + 64, tB0 = tmem + 128, tB1 = tmem + 256, tKPT = tmem + 384;
 
-  if (warp == 0 || warp >= 10) {
+  if (warp == 0 || (warp >= 10 && warp < kAccWarp)) {
     // No L2 prefetch of the column's Q / dO tiles: prefetches queue in the TMA unit ahead of
     // the ring loads, and a wave's columns share one unit's Q / dO, which stays L2-resident.
     // kColsProd producer warps fill each stage (TMA issue from one warp caps at ~40 B/cycle):
@@ -160,7 +167,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
         ++item;
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 || (SLAB_COLS_2ISSUE && warp == kAccWarp)) {
     const uint32_t aK = tc::smem_u32(sK), aV = tc::smem_u32(sV), aKF = tc::smem_u32(sKF);
     const uint32_t aR = tc::smem_u32(sRing), aPD = tc::smem_u32(sPD);
     constexpr uint32_t id_s = tc::idesc_bf16(128, 64, false, false);   // pair x K^T
@@ -202,7 +209,30 @@ __global__ void __launch_bounds__(kColsThreads, 1)
     // order their inputs become ready: acc(t) releases a ring stage, S/dP(t+1) feeds the compute
     // warps.  S/dP(t) reuses TMEM buffer t&1, free once acc(t-2) was issued (pd_full(t-2) seen).
     // Barrier probes are warp votes so every lane takes the same branch.
-    {
+    if (SLAB_COLS_2ISSUE && warp == 1) {
+      // S/dP(t) once its ring stage landed and the compute warps have read TMEM buffer t&1
+      for (int ts = 0; ts < np; ++ts) {
+        tc::mbar_wait(ring_full + ts % RS, (ts / RS) & 1);
+        if (ts >= 2) tc::mbar_wait(sdp_free + (ts & 1), ((ts - 2) >> 1) & 1);
+        tc::tc_fence_after();
+        ts_mark(dbg && lane == 0 && ts < 16, 16 + ts);
+        const uint64_t dq = tc::desc_add(dRk, (ts % RS) * L::kStage), ddo = tc::desc_add(dq, L::kP);
+        const uint32_t tb = (ts & 1) ? tB1 : tB0;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          tc::mma_bf16_w(tb, tc::desc_add(dq, koff(kk, 128)), tc::desc_add(dKk, koff(kk, 64)), id_s, kk > 0);        // S
+          tc::mma_bf16_w(tb + 64, tc::desc_add(ddo, koff(kk, 128)), tc::desc_add(dVk, koff(kk, 64)), id_s, kk > 0);  // dP
+        }
+        tc::mma_commit_w(sdp_full + (ts & 1));
+      }
+      __syncwarp();
+    } else if (SLAB_COLS_2ISSUE) {  // accumulation warp: acc(t) as soon as P / dS(t) are in smem
+      for (int ta = 0; ta < np; ++ta) {
+        tc::mbar_wait(pd_full + (ta & 1), (ta >> 1) & 1);
+        issue_acc(ta);
+      }
+      tc::mma_commit_w(acc_done);
+    } else {
       int ts = 0, ta = 0;
       while (ta < np) {
         if (SLAB_COLS_ACC_FIRST && ta < ts && __all_sync(0xffffffffu, tc::mbar_test(pd_full + (ta & 1), (ta >> 1) & 1))) {
@@ -232,6 +262,9 @@ __global__ void __launch_bounds__(kColsThreads, 1)
     }
     item = np;
     __syncwarp();
+    if (SLAB_COLS_2ISSUE && warp == 1) {
+      // linear part and all_done come from the accumulation warp (same issuing thread as acc)
+    } else {
     if (has_lin) {
       const uint32_t sh = wait_item();
       tc::mbar_wait(kf_ready, 0);
@@ -250,6 +283,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
     }
     if (lane == 0) tc::mma_commit(all_done);
     __syncwarp();
+    }
   } else {
     const int q4 = warp & 3;
     const int grp = (warp - 2) >> 2;
@@ -273,6 +307,11 @@ __global__ void __launch_bounds__(kColsThreads, 1)
         tc::tmem_ld32(tb, sv);
         tc::tmem_ld32(tb + 64, dp);
         tc::tmem_ld_wait();
+        if (SLAB_COLS_2ISSUE) {  // TMEM buffer t&1 may take S/dP(t+2)
+          tc::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(sdp_free + (t & 1));
+        }
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
           const float p0 = ex2f(__uint_as_float(sv[e]) * p.scale_log2 - lse2);
