@@ -538,6 +538,17 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     const int grp = (warp - 2) >> 2;
     const uint32_t lane_base = uint32_t(32 * q4) << 16;
     const int tid = threadIdx.x - 64;  // 0..255
+    // this thread's dQ^phi chunks for the epilogue (written by k_bwd_lin): issued now so their
+    // latency hides behind the main loop instead of stalling the final row-wise pass
+    constexpr int DQ = D / 4;
+    uint4 gq[DQ / 8];
+    {
+      const int rq = tid >> 2, sub = tid & 3;
+      const __nv_bfloat16* src = p.dqphi + ((long long)row0 + rq) * D + sub * DQ;
+#pragma unroll
+      for (int i = 0; i < DQ / 8; ++i)
+        gq[i] = *reinterpret_cast<const uint4*>(src + ((8 * i + 8 * sub) & (DQ - 1)));
+    }
     if (tid < 64) s_lse2[tid] = p.lse[(long long)row0 + tid] * 1.4426950408889634f;
     else if (tid < 128) s_ds[tid - 64] = p.Ds[(long long)row0 + tid - 64] * p.scale;  // D^s / sqrt(d)
     named_sync(1, 256);
@@ -622,7 +633,6 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     }
     named_sync(1, 256);
     {
-      constexpr int DQ = D / 4;
       const int rq = tid >> 2, sub = tid & 3, c0 = sub * DQ;
       const long long grow = (long long)row0 + rq;
       float x[DQ];
@@ -656,7 +666,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         const int cc = (cc0 + 8 * sub) & (DQ - 1);  // rotated chunk order (bank spread)
         const int col = c0 + cc;
         float g[8], o[8];
-        unpack8(*reinterpret_cast<const uint4*>(p.dqphi + grow * D + col), g);
+        unpack8(gq[cc0 / 8], g);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           float xe = x[0];
