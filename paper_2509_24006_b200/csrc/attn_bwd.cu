@@ -292,11 +292,26 @@ __global__ void __launch_bounds__(kColsThreads, 1)
     for (int a = tid; a < D; a += 256) zas[a] = has_lin ? tc::load_sum3(p.gZa + ucol * 3 * D + a, D) : 0.f;
     // ---- loop: thread = query row rq of the pair (S / dP lanes), 32 key columns per group
     const int rq = 32 * q4 + lane;
+    // per-query-row lse / D^s of pair t+1 are fetched during pair t (two dependent global
+    // loads -- list entry, then the row values -- would otherwise stall every iteration)
+    auto row_of = [&](int t) {
+      return u * p.N + (long long)list[min(2 * t + (rq >> 6), cnt - 1)] * 64 + (rq & 63);
+    };
+    float lse_n = 0.f, ds_n = 0.f;
+    if (np > 0) {
+      const long long r0 = row_of(0);
+      lse_n = p.lse[r0];
+      ds_n = p.Ds[r0];
+    }
     for (int t = 0; t < np; ++t) {
       const bool live = rq < 64 || 2 * t + 1 < cnt;
-      const long long qrow = u * p.N + (long long)list[min(2 * t + (rq >> 6), cnt - 1)] * 64 + (rq & 63);
-      const float lse2 = p.lse[qrow] * 1.4426950408889634f;
-      const float dss = p.Ds[qrow] * p.scale;  // D^s / sqrt(d)
+      const float lse2 = lse_n * 1.4426950408889634f;
+      const float dss = ds_n * p.scale;  // D^s / sqrt(d)
+      if (t + 1 < np) {
+        const long long r1 = row_of(t + 1);
+        lse_n = p.lse[r1];
+        ds_n = p.Ds[r1];
+      }
       tc::mbar_wait(sdp_full + (t & 1), (t >> 1) & 1);
       tc::tc_fence_after();
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 32 + t);
