@@ -51,6 +51,40 @@ __global__ void k_pool(const In* __restrict__ x, R* __restrict__ out, long long 
   }
 }
 
+// K1a for bf16 inputs with d % 4 == 0: Q and K in one launch (blockIdx.z), one warp per block,
+// each lane four adjacent columns (8-byte loads, four independent ascending sums), the same
+// per-column operation order as k_pool.
+template <typename R>
+__global__ void __launch_bounds__(32) k_pool2_bf16(const __nv_bfloat16* __restrict__ q,
+                                                   const __nv_bfloat16* __restrict__ k,
+                                                   R* __restrict__ pq, R* __restrict__ pk, long long N,
+                                                   int d, int b, int T, long long n_valid) {
+  const long long u = blockIdx.y;
+  const int g = blockIdx.x;
+  const __nv_bfloat16* x = blockIdx.z ? k : q;
+  R* out = blockIdx.z ? pk : pq;
+  const __nv_bfloat16* base = x + (u * N + (long long)g * b) * d;
+  const long long left = n_valid - (long long)g * b;
+  const int rows = left < b ? int(left) : b;
+  for (int c = 4 * threadIdx.x; c < d; c += 128) {
+    R a0 = R(0), a1 = R(0), a2 = R(0), a3 = R(0);
+    for (int r = 0; r < rows; ++r) {
+      const uint2 v = *reinterpret_cast<const uint2*>(base + (long long)r * d + c);
+      const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
+      const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
+      a0 = add_rn(a0, R(f0.x));
+      a1 = add_rn(a1, R(f0.y));
+      a2 = add_rn(a2, R(f1.x));
+      a3 = add_rn(a3, R(f1.y));
+    }
+    R* o = out + (u * T + g) * d + c;
+    o[0] = div_rn(a0, R(rows));
+    o[1] = div_rn(a1, R(rows));
+    o[2] = div_rn(a2, R(rows));
+    o[3] = div_rn(a3, R(rows));
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // K1b+K2: one CTA per (unit, block row).  Scores in R with the reference's operation order
 // (matmul_nt ascending-k dot, mat.hpp:83-97; then * 1/sqrt(d)), max-shifted softmax with
@@ -446,10 +480,20 @@ static void classify_t(const Dims& D, const In* q, const In* k, const StateBufs&
   R* pq = reinterpret_cast<R*>(w.pq);
   R* pk = reinterpret_cast<R*>(w.pk);
   const int pt = D.d < 256 ? ((D.d + 31) / 32) * 32 : 256;
-  k_pool<R, In><<<dim3(D.Tm, unsigned(D.U)), pt, 0, st>>>(q, pq, D.N, D.d, D.bq, D.Tm, D.N_valid);
-  check_launch("k_pool(q)", st);
-  k_pool<R, In><<<dim3(D.Tn, unsigned(D.U)), pt, 0, st>>>(k, pk, D.N, D.d, D.bkv, D.Tn, D.N_valid);
-  check_launch("k_pool(k)", st);
+  bool pooled = false;
+  if constexpr (std::is_same<In, __nv_bfloat16>::value) {
+    if (D.d % 4 == 0 && D.bq == D.bkv) {
+      k_pool2_bf16<R><<<dim3(D.Tm, unsigned(D.U), 2), 32, 0, st>>>(q, k, pq, pk, D.N, D.d, D.bq, D.Tm, D.N_valid);
+      check_launch("k_pool", st);
+      pooled = true;
+    }
+  }
+  if (!pooled) {
+    k_pool<R, In><<<dim3(D.Tm, unsigned(D.U)), pt, 0, st>>>(q, pq, D.N, D.d, D.bq, D.Tm, D.N_valid);
+    check_launch("k_pool(q)", st);
+    k_pool<R, In><<<dim3(D.Tn, unsigned(D.U)), pt, 0, st>>>(k, pk, D.N, D.d, D.bkv, D.Tn, D.N_valid);
+    check_launch("k_pool(k)", st);
+  }
   const size_t smem = classify_smem_bytes(D, sizeof(R) == 8);
   if (smem > 48 * 1024)
     SLAB_CUDA(cudaFuncSetAttribute(k_classify<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
