@@ -5,6 +5,8 @@
 //       Z = sum over marginal z_j (ascending, f32)              k_aggregate_z
 //   K5  fused sparse + linear + projection forward              attn_fwd.cu
 // References: summaries.cpp:17-42, aggregation.cpp:40-56, forward.cpp:81-195.
+#include <type_traits>
+
 #include "kernels.hpp"
 #include "tc.cuh"
 
@@ -27,18 +29,29 @@ __global__ void __launch_bounds__(256) k_phi_kz(const __nv_bfloat16* __restrict_
   float zacc[C];
 #pragma unroll
   for (int c = 0; c < C; ++c) zacc[c] = 0.f;
+  // all 8 rows' loads in flight before any reduction (C bf16 = 2C bytes per lane and row)
+  using V = typename std::conditional<C == 4, uint2, uint32_t>::type;
+  static_assert(C == 2 || C == 4, "d in {64, 128}");
+  const long long rin0 = (long long)j * 64 + warp * 8;
+  const V* src = reinterpret_cast<const V*>(k + (u * N + rin0) * D) + lane;
+  V raw[8];
+#pragma unroll
+  for (int rr = 0; rr < 8; ++rr) raw[rr] = src[rr * (D / C)];
+#pragma unroll
   for (int rr = 0; rr < 8; ++rr) {
-    const long long rin = (long long)j * 64 + warp * 8 + rr;  // row within the unit
-    const long long row = u * N + rin;
-    const __nv_bfloat16* src = k + row * D + lane * C;
-    float x[C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) x[c] = __bfloat162float(src[c]);
+    const long long rin = rin0 + rr;  // row within the unit
+    V* dst = reinterpret_cast<V*>(kfb + (u * N + rin) * D) + lane;
     if (rin >= n_valid) {  // ragged N: padded keys have no feature map (no summary weight)
-      __nv_bfloat16* dst = kfb + row * D + lane * C;
-#pragma unroll
-      for (int c = 0; c < C; ++c) dst[c] = __float2bfloat16_rn(0.f);
+      *dst = V{};
       continue;
+    }
+    float x[C];
+    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw[rr]);
+#pragma unroll
+    for (int c = 0; c < C; c += 2) {
+      const float2 f = __bfloat1622float2(h2[c / 2]);
+      x[c] = f.x;
+      x[c + 1] = f.y;
     }
     if (phi == 2) {
       float m = -INFINITY;
@@ -59,12 +72,15 @@ __global__ void __launch_bounds__(256) k_phi_kz(const __nv_bfloat16* __restrict_
 #pragma unroll
       for (int c = 0; c < C; ++c) x[c] = phi_elem(phi, x[c]);
     }
-    __nv_bfloat16* dst = kfb + row * D + lane * C;
+    V out;
+    uint32_t* o32 = reinterpret_cast<uint32_t*>(&out);
 #pragma unroll
-    for (int c = 0; c < C; ++c) {
-      dst[c] = __float2bfloat16_rn(x[c]);
+    for (int c = 0; c < C; c += 2) {
+      o32[c / 2] = tc::pack_bf16(x[c], x[c + 1]);
       zacc[c] += x[c];
+      zacc[c + 1] += x[c + 1];
     }
+    *dst = out;
   }
 #pragma unroll
   for (int c = 0; c < C; ++c) zpart[warp][lane * C + c] = zacc[c];
