@@ -383,18 +383,30 @@ __global__ void __launch_bounds__(kColsThreads, 1)
       se += __shfl_xor_sync(0xffffffffu, se, 2);
       inv = 1.f / se;
     }
-    auto phi_of = [&](float x) { return p.phi == 2 ? __expf(x - mx) * inv : phi_elem(p.phi, x); };
+    // phi(K_j) of this thread's D/4 columns, in the per-sub rotated chunk order the final
+    // row-wise pass reads (conflict-free transposed tiles), computed while the last
+    // accumulation MMAs still run; kept in registers for the Jacobian at the end
+    const int sub = tid & 3;
+    auto rot = [&](int cc) { return (cc + 8 * sub) & (D / 4 - 1); };
+    constexpr int DQ = D / 4;
+    float kf[DQ];
+#pragma unroll
+    for (int cc0 = 0; cc0 < DQ; cc0 += 8) {
+      float f[8];
+      unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, c0 + rot(cc0))), f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) kf[cc0 + e] = p.phi == 2 ? __expf(f[e] - mx) * inv : phi_elem(p.phi, f[e]);
+    }
     tc::mbar_wait(acc_done, 0);  // the P / dS buffers are free
     ts_mark(dbg && threadIdx.x == 64, 120);
     cta_mark(threadIdx.x == 64, 2);
     if (has_lin) {
 #pragma unroll
-      for (int cc = 0; cc < D / 4; cc += 8) {
+      for (int cc0 = 0; cc0 < DQ; cc0 += 8) {
         float f[8];
-        unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, c0 + cc)), f);
 #pragma unroll
-        for (int e = 0; e < 8; ++e) f[e] = phi_of(f[e]);
-        *reinterpret_cast<uint4*>(sKF + tile_off(c, c0 + cc)) = pack8(f);
+        for (int e = 0; e < 8; ++e) f[e] = kf[cc0 + e];
+        *reinterpret_cast<uint4*>(sKF + tile_off(c, c0 + rot(cc0))) = pack8(f);
       }
       tc::fence_proxy_async();
       __syncwarp();
@@ -430,42 +442,31 @@ __global__ void __launch_bounds__(kColsThreads, 1)
     named_sync(1, 256);
     ts_mark(dbg && threadIdx.x == 64, 123);
     // ---- dk_total = J_phi(k)^T (dK^phi + dZ_agg) + dK ; dv  (row-wise, 4 threads per row)
-    // Thread (c, sub) owns 32 columns, visited in a per-sub rotated chunk order (conflict-free
-    // reads of the transposed tiles); K, phi(K) and g = dK^phi + dZ_agg stay in registers.
-    const int sub = tid & 3;
-    auto rot = [&](int cc) { return (cc + 8 * sub) & (D / 4 - 1); };
-    constexpr int DQ = D / 4;
-    float kx[DQ], g[DQ];
+    // The Jacobian needs only phi(k): softmax J^T g = phi (g - <phi, g>); elu1 J = 1 where
+    // k >= 0 (phi >= 1) else phi; relu J = 1 where phi > 0.
+    float g[DQ];
 #pragma unroll
     for (int cc0 = 0; cc0 < DQ; cc0 += 8) {
       const int col = c0 + rot(cc0);
-      float f[8];
-      unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, col)), f);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        kx[cc0 + e] = f[e];
-        g[cc0 + e] = has_lin ? tkp[c * TP + col + e] + zas[col + e] : 0.f;
-      }
+      for (int e = 0; e < 8; ++e) g[cc0 + e] = has_lin ? tkp[c * TP + col + e] + zas[col + e] : 0.f;
     }
     const long long grow = (long long)kv0 + c;
     float jg[DQ];
-    if (p.phi == 2) {  // J^T g = phi * (g - <phi, g>)
+    if (p.phi == 2) {
       float dot = 0.f;
 #pragma unroll
-      for (int e = 0; e < DQ; ++e) {
-        kx[e] = __expf(kx[e] - mx) * inv;
-        dot = fmaf(kx[e], g[e], dot);
-      }
+      for (int e = 0; e < DQ; ++e) dot = fmaf(kf[e], g[e], dot);
       dot += __shfl_xor_sync(0xffffffffu, dot, 1);
       dot += __shfl_xor_sync(0xffffffffu, dot, 2);
 #pragma unroll
-      for (int e = 0; e < DQ; ++e) jg[e] = kx[e] * (g[e] - dot);
+      for (int e = 0; e < DQ; ++e) jg[e] = kf[e] * (g[e] - dot);
     } else if (p.phi == 0) {
 #pragma unroll
-      for (int e = 0; e < DQ; ++e) jg[e] = kx[e] >= 0.f ? g[e] : __expf(kx[e]) * g[e];
+      for (int e = 0; e < DQ; ++e) jg[e] = kf[e] >= 1.f ? g[e] : kf[e] * g[e];
     } else {
 #pragma unroll
-      for (int e = 0; e < DQ; ++e) jg[e] = kx[e] > 0.f ? g[e] : 0.f;
+      for (int e = 0; e < DQ; ++e) jg[e] = kf[e] > 0.f ? g[e] : 0.f;
     }
     ts_mark(dbg && threadIdx.x == 64, 118);
 #pragma unroll
