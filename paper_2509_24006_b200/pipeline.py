@@ -8,7 +8,8 @@ batch == 1, over the batch otherwise) and overlaps, on three CUDA streams,
 
     H2D(chunk c+1)  |  forward + backward(chunk c)  |  D2H(chunk c-1)
 
-with two device-side slots.  Every chunk runs through the same C-ABI calls as `SLA` (one
+with `slots` device-side buffers (3 by default: a chunk's inputs can land while the previous
+two chunks still compute and drain).  Every chunk runs through the same C-ABI calls as `SLA` (one
 `SLA` instance per distinct chunk shape).  dW is per head: chunks over heads write disjoint
 head rows; chunks over the batch accumulate into one dW (backward.cpp:46 sums over the batch).
 """
@@ -42,7 +43,8 @@ class HostTrainStep:
     """
 
     def __init__(self, batch: int, heads: int, n: int, d: int, b_q: int = 64, b_kv: int = 64,
-                 cfg: Optional[SlaConfig] = None, dtype=torch.bfloat16, device="cuda", chunks: int = 4):
+                 cfg: Optional[SlaConfig] = None, dtype=torch.bfloat16, device="cuda", chunks: int = 4,
+                 slots: int = 3):
         self.batch, self.heads, self.n, self.d = batch, heads, n, d
         self.device = torch.device(device)
         self.dtype = dtype
@@ -56,8 +58,9 @@ class HostTrainStep:
         span = max(e - s for s, e in self.ranges)
         cshape = (1, span, n, d) if self.by_heads else (span, heads, n, d)
         mk = lambda dt=dtype: torch.empty(cshape, dtype=dt, device=self.device)  # noqa: E731
+        self.nslots = max(2, slots)
         self.slots = []
-        for _ in range(2):
+        for _ in range(self.nslots):
             self.slots.append({
                 "q": mk(), "k": mk(), "v": mk(), "do": mk(),
                 "o": mk(), "o_s": mk(), "o_l": mk(), "lse": mk(torch.float32)[..., 0].contiguous(),
@@ -68,9 +71,9 @@ class HostTrainStep:
         self.dw = torch.empty((heads, d, d), dtype=torch.float32, device=self.device)
         self.dw_part = None if self.by_heads else torch.empty_like(self.dw)
         self.s_in, self.s_c, self.s_out = (torch.cuda.Stream(self.device) for _ in range(3))
-        self.ev_in = [torch.cuda.Event() for _ in range(2)]
-        self.ev_c = [torch.cuda.Event() for _ in range(2)]
-        self.ev_out = [torch.cuda.Event() for _ in range(2)]
+        self.ev_in = [torch.cuda.Event() for _ in range(self.nslots)]
+        self.ev_c = [torch.cuda.Event() for _ in range(self.nslots)]
+        self.ev_out = [torch.cuda.Event() for _ in range(self.nslots)]
         self.launches = 0
 
     def h2d_bytes(self) -> int:
@@ -87,21 +90,22 @@ class HostTrainStep:
         with torch.cuda.stream(self.s_in):
             self.w.copy_(hw, non_blocking=True)
         for c, (s, e) in enumerate(self.ranges):
-            slot = self.slots[c % 2]
+            S = self.nslots
+            slot = self.slots[c % S]
             shape = (1, e - s) if self.by_heads else (e - s, self.heads)
             op, state = self.ops[shape], self.states[shape]
             sl = (slice(0, 1), slice(s, e)) if self.by_heads else (slice(s, e),)
             view = lambda t: t[: shape[0], : shape[1]]  # noqa: E731  (slot tensors are max-span)
             with torch.cuda.stream(self.s_in):
-                if c >= 2:
-                    self.s_in.wait_event(self.ev_c[c % 2])  # compute(c-2) done with the inputs
+                if c >= S:
+                    self.s_in.wait_event(self.ev_c[c % S])  # compute(c-S) done with the inputs
                 for nm, src in (("q", hq), ("k", hk), ("v", hv), ("do", hdo)):
                     view(slot[nm]).copy_(src[sl], non_blocking=True)
-                self.ev_in[c % 2].record(self.s_in)
+                self.ev_in[c % S].record(self.s_in)
             with torch.cuda.stream(self.s_c):
-                self.s_c.wait_event(self.ev_in[c % 2])
-                if c >= 2:
-                    self.s_c.wait_event(self.ev_out[c % 2])  # D2H(c-2) done with the outputs
+                self.s_c.wait_event(self.ev_in[c % S])
+                if c >= S:
+                    self.s_c.wait_event(self.ev_out[c % S])  # D2H(c-S) done with the outputs
                 q, k, v, do = (view(slot[nm]) for nm in ("q", "k", "v", "do"))
                 w = self.w[s:e] if self.by_heads else self.w
                 dw = self.dw[s:e] if self.by_heads else (self.dw if c == 0 else self.dw_part)
@@ -112,12 +116,12 @@ class HostTrainStep:
                 self.launches += op.launches()
                 if not self.by_heads and c > 0:
                     self.dw.add_(self.dw_part)
-                self.ev_c[c % 2].record(self.s_c)
+                self.ev_c[c % S].record(self.s_c)
             with torch.cuda.stream(self.s_out):
-                self.s_out.wait_event(self.ev_c[c % 2])
+                self.s_out.wait_event(self.ev_c[c % S])
                 for nm, dst in (("o", ho), ("dq", hdq), ("dk", hdk), ("dv", hdv)):
                     dst[sl].copy_(view(slot[nm]), non_blocking=True)
-                self.ev_out[c % 2].record(self.s_out)
+                self.ev_out[c % S].record(self.s_out)
         with torch.cuda.stream(self.s_out):
             self.s_out.wait_stream(self.s_c)
             hdw.copy_(self.dw, non_blocking=True)
