@@ -36,6 +36,8 @@ CONFIGS = {
     "c3": (1, 12, 32768, 128, 64, 5.0, 10.0, "softmax"),
     "c1": (1, 2, 1024, 64, 64, 5.0, 10.0, "softmax"),
     "c5": (8, 40, 75648, 128, 64, 5.0, 10.0, "softmax"),
+    # the literal Wan2.1-1.3B length through SLA_B200_FLAG_RAGGED (the reference rejects it)
+    "c3r": (1, 12, 32760, 128, 64, 5.0, 10.0, "softmax"),
 }
 
 
@@ -194,6 +196,9 @@ def run_reference(args):
         return
     cfg = CONFIGS[args.config]
     B, H, N, d, b, k_h, k_l, phi = cfg
+    if N % b:  # the reference rejects ragged N (layout.cpp:12-17): time the padded length
+        N = (N + b - 1) // b * b
+        cfg = (B, H, N, d, b, k_h, k_l, phi)
     threads = os.cpu_count() or 1
     x = reference_step_inputs(N, d)
     for _ in range(args.warmup):
@@ -225,7 +230,9 @@ def config_json(name):
     B, H, N, d, b, k_h, k_l, phi = CONFIGS[name]
     return {"workload": f"{name}: SLA fwd+bwd, B={B} H={H} N={N} d={d} b_q=b_kv={b} k_h={k_h}% k_l={k_l}% phi={phi}",
             "batch": B, "heads": H, "n": N, "d": d, "block": b, "k_h": k_h, "k_l": k_l, "phi": phi,
-            "n_note": "N padded from 32760/75600 to a multiple of 64 (make_block_layout rejects ragged N)",
+            "n_note": ("N = 32760 as-is through SLA_B200_FLAG_RAGGED (zero-padded unit copies inside the "
+                       "timed region); the reference arm times N = 32768") if N % b else
+                      "N padded from 32760/75600 to a multiple of 64 (make_block_layout rejects ragged N)",
             "l2": "inputs (Q,K,V,dO = 4 x B*H*N*d*2 bytes) exceed the 126 MB L2; no flush needed",
             "parallelism": "(batch x head) units sharded over ranks, no collective"}
 
@@ -265,7 +272,7 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     B, H, N, d, b, k_h, k_l, phi = CONFIGS[args.config]
-    cfg = SlaConfig(k_h=k_h, k_l=k_l, phi=phi)
+    cfg = SlaConfig(k_h=k_h, k_l=k_l, phi=phi, ragged=N % b != 0)
     op = SLA(B, H, N, d, b, b, cfg, torch.bfloat16, dev)
     g = torch.Generator(device=dev)
     g.manual_seed(1234 + rank)
@@ -440,7 +447,10 @@ def run_ours(args):
     if not args.no_cpu_baseline and rank == 0 and world == 1:
         try:
             threads = os.cpu_count() or 1
-            tsec, kind, threads = time_reference_head(CONFIGS[args.config], threads)
+            rcfg = CONFIGS[args.config]
+            if rcfg[2] % rcfg[4]:  # the reference needs b | N: time the padded length
+                rcfg = rcfg[:2] + ((rcfg[2] + rcfg[4] - 1) // rcfg[4] * rcfg[4],) + rcfg[3:]
+            tsec, kind, threads = time_reference_head(rcfg, threads)
             out["cpu_baseline"] = {"value": dense_equiv_flops(1, 1, N, d) / tsec / 1e12, "unit": "TFLOPS",
                                    "cores": threads, "kind": kind,
                                    "sample": f"one (batch, head) unit of {B * H}: fwd+bwd f32 in {tsec:.2f} s"}

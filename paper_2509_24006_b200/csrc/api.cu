@@ -1,6 +1,7 @@
 // api.cu -- the extern "C" boundary (include/sla_b200.h): validation with the reference's
 // messages, buffer carving, path dispatch, error mapping to the reference's exception
 // classes (status 2 = std::invalid_argument, 1 = std::runtime_error).
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <string>
@@ -144,15 +145,35 @@ void check_inputs(const sla_b200_problem* p, const Dims& D, const WorkBufs& w,
   }
 }
 
-// ragged N: [U, N_valid, rows] <-> [U, N, rows] (zero tail rows), `esz`-byte elements
+// ragged N: [U, N_valid, rows] <-> [U, N, rows] (zero tail rows).  An SM copy kernel: the
+// copy engines behind cudaMemcpy2DAsync moved these ~1 GB per step at a fraction of HBM speed.
+__global__ void k_copy_units(uint4* __restrict__ dst, const uint4* __restrict__ src, long long units,
+                             long long dst_per_unit, long long src_per_unit) {
+  const long long total = units * dst_per_unit;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long u = e / dst_per_unit, r = e % dst_per_unit;
+    dst[e] = r < src_per_unit ? src[u * src_per_unit + r] : make_uint4(0, 0, 0, 0);
+  }
+}
+void copy_units(void* dst, const void* src, long long units, size_t dst_bytes, size_t src_bytes,
+                cudaStream_t st) {
+  if (dst_bytes % 16 || src_bytes % 16) {  // f32 lse rows of an odd length: copy engines
+    const size_t w = std::min(dst_bytes, src_bytes);
+    SLAB_CUDA(cudaMemcpy2DAsync(dst, dst_bytes, src, src_bytes, w, size_t(units), cudaMemcpyDeviceToDevice, st));
+    if (dst_bytes > w)
+      SLAB_CUDA(cudaMemset2DAsync(static_cast<char*>(dst) + w, dst_bytes, 0, dst_bytes - w, size_t(units), st));
+    return;
+  }
+  k_copy_units<<<148 * 8, 256, 0, st>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), units,
+                                        (long long)(dst_bytes / 16), (long long)(src_bytes / 16));
+  check_launch("k_copy_units", st);
+}
 void pad_rows(const Dims& D, void* dst, const void* src, size_t row_bytes, cudaStream_t st) {
-  const size_t sp = size_t(D.N_valid) * row_bytes, dp = size_t(D.N) * row_bytes;
-  SLAB_CUDA(cudaMemcpy2DAsync(dst, dp, src, sp, sp, size_t(D.U), cudaMemcpyDeviceToDevice, st));
-  SLAB_CUDA(cudaMemset2DAsync(static_cast<char*>(dst) + sp, dp, 0, dp - sp, size_t(D.U), st));
+  copy_units(dst, src, D.U, size_t(D.N) * row_bytes, size_t(D.N_valid) * row_bytes, st);
 }
 void unpad_rows(const Dims& D, void* dst, const void* src, size_t row_bytes, cudaStream_t st) {
-  const size_t sp = size_t(D.N) * row_bytes, dp = size_t(D.N_valid) * row_bytes;
-  SLAB_CUDA(cudaMemcpy2DAsync(dst, dp, src, sp, dp, size_t(D.U), cudaMemcpyDeviceToDevice, st));
+  copy_units(dst, src, D.U, size_t(D.N_valid) * row_bytes, size_t(D.N) * row_bytes, st);
 }
 
 void classify_into_state(const sla_b200_problem* p, const Dims& D, const void* q, const void* k,
