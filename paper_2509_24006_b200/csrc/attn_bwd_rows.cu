@@ -313,7 +313,11 @@ template <int D>
 struct RowsLayout {
   static constexpr int kT = 64 * D * 2;   // 64-row tile
   static constexpr int kP = 128 * D * 2;  // 128-row pair tile
-  static constexpr int KS = 3, VS = 2;    // K-pair and V-pair ring slots
+#ifndef SLAB_ROWS_KS
+#define SLAB_ROWS_KS 3
+#define SLAB_ROWS_VS 2
+#endif
+  static constexpr int KS = SLAB_ROWS_KS, VS = SLAB_ROWS_VS;  // K-pair and V-pair ring slots
   static constexpr int oQ = 0, oDO = kT, oDS = 2 * kT;  // dS^T [128 kv][64 q] bf16 (16 KB)
   static constexpr int oK = oDS + 16384;
   static constexpr int oV = oK + KS * kP;
@@ -350,11 +354,12 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   uint64_t* ds_empty = bars + 4;
   uint64_t* dq_done = bars + 5;
   uint64_t* sdp_free = bars + 6;   // [2] compute warps have read S^T|dP^T buffer t&1 (2-issuer mode)
-  uint64_t* k_full = bars + 8;     // [KS]
-  uint64_t* k_empty = bars + 11;   // [KS]
-  uint64_t* v_full = bars + 14;    // [VS]
-  uint64_t* v_empty = bars + 16;   // [VS]
+  uint64_t* k_full = bars + 8;               // [KS]
+  uint64_t* k_empty = k_full + L::KS;        // [KS]
+  uint64_t* v_full = k_empty + L::KS;        // [VS]
+  uint64_t* v_empty = v_full + L::VS;        // [VS]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
+  static_assert(8 + 2 * (L::KS + L::VS) <= 20, "barrier slots");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x;
