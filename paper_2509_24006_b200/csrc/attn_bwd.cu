@@ -35,18 +35,13 @@ struct ColsLayout {
   static_assert(kBytes <= 232448, "smem");
 };
 
-#ifndef SLAB_COLS_ACC_FIRST
-#define SLAB_COLS_ACC_FIRST 0  // issue the ready acc(t) before a ready S/dP(t+1)
-#endif
-#ifndef SLAB_COLS_PROD
-#define SLAB_COLS_PROD 2
-#endif
-#ifndef SLAB_COLS_2ISSUE
-#define SLAB_COLS_2ISSUE 1  // S/dP (warp 1) and the dV/dK accumulation (last warp) issued separately
-#endif
-constexpr int kColsProd = SLAB_COLS_PROD;  // TMA producer warps (2 or 4)
-constexpr int kAccWarp = 10 + kColsProd - 1;  // accumulation issuer in 2-issuer mode
-constexpr int kColsThreads = 32 * (kAccWarp + (SLAB_COLS_2ISSUE ? 1 : 0));
+// Warps: 0 and 10 TMA producers, 1 S/dP issuer, 2-9 softmax-gradient / epilogue, 11 the
+// dV / dK accumulation issuer (and the linear-branch MMAs).  Two issuing warps keep one's
+// barrier waits from delaying the other's MMAs (1.09 -> 1.04 ms); 4 producer warps and a
+// single poll-driven issuer were measured no better.
+constexpr int kColsProd = 2;
+constexpr int kAccWarp = 11;
+constexpr int kColsThreads = 32 * 12;
 
 template <int D>
 __global__ void __launch_bounds__(kColsThreads, 1)
@@ -123,13 +118,11 @@ __global__ void __launch_bounds__(kColsThreads, 1)
   if (warp == 0 || (warp >= 10 && warp < kAccWarp)) {
     // No L2 prefetch of the column's Q / dO tiles: prefetches queue in the TMA unit ahead of
     // the ring loads, and a wave's columns share one unit's Q / dO, which stays L2-resident.
-    // kColsProd producer warps fill each stage (TMA issue from one warp caps at ~40 B/cycle):
-    // pid&1 selects Q / dO, with 4 producers pid>>1 selects the pair's first / second block.
+    // Two producer warps fill each stage (TMA issue from one warp caps at ~40 B/cycle):
+    // pid 0 loads the Q pair (and K_j / V_j), pid 1 the dO pair.
     if (lane == 0) {
-      const int pid = warp == 0 ? 0 : warp - 9;  // pid 0 also loads K_j / V_j
-#ifndef SLAB_NO_TMAP_PREFETCH
+      const int pid = warp == 0 ? 0 : 1;
       tc::tma_prefetch(pid == 0 ? &tmQ : &tmDO);
-#endif
       if (pid == 0) {
         tc::mbar_expect_tx(kv_full, 2 * L::kT);
 #pragma unroll
@@ -145,17 +138,17 @@ __global__ void __launch_bounds__(kColsThreads, 1)
         tc::mbar_expect_tx(ring_full + s, bytes);
         return sRing + s * L::kStage;
       };
-      const CUtensorMap* tm = (pid & 1) ? &tmDO : &tmQ;
+      const CUtensorMap* tm = pid ? &tmDO : &tmQ;
       for (int pp = 0; pp < np; ++pp) {
         const int r1 = int(u * p.N) + list[2 * pp] * 64;
         const int r2 = int(u * p.N) + list[min(2 * pp + 1, cnt - 1)] * 64;
-        uint8_t* dst = acquire(kColsProd == 2 ? L::kP : L::kP / 2) + (pid & 1) * L::kP;
+        uint8_t* dst = acquire(L::kP) + pid * L::kP;
         ts_mark(dbg && pid == 0 && pp < 16, pp);
         uint64_t* fb = ring_full + (item % RS);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
-          if (kColsProd == 2 || pid < 2) tc::tma_load_3d(dst + c * 16384, tm, fb, 64 * c, r1, 0);
-          if (kColsProd == 2 || pid >= 2) tc::tma_load_3d(dst + c * 16384 + 8192, tm, fb, 64 * c, r2, 0);
+          tc::tma_load_3d(dst + c * 16384, tm, fb, 64 * c, r1, 0);
+          tc::tma_load_3d(dst + c * 16384 + 8192, tm, fb, 64 * c, r2, 0);
         }
         ++item;
       }
@@ -167,7 +160,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
         ++item;
       }
     }
-  } else if (warp == 1 || (SLAB_COLS_2ISSUE && warp == kAccWarp)) {
+  } else if (warp == 1 || warp == kAccWarp) {
     const uint32_t aK = tc::smem_u32(sK), aV = tc::smem_u32(sV), aKF = tc::smem_u32(sKF);
     const uint32_t aR = tc::smem_u32(sRing), aPD = tc::smem_u32(sPD);
     constexpr uint32_t id_s = tc::idesc_bf16(128, 64, false, false);   // pair x K^T
@@ -205,11 +198,9 @@ __global__ void __launch_bounds__(kColsThreads, 1)
       tc::mma_commit_w(ring_empty + (t % RS));
       tc::mma_commit_w(pd_empty + (t & 1));
     };
-    // The tensor pipe executes in issue order, so S/dP(t+1) and acc(t) are issued in whichever
-    // order their inputs become ready: acc(t) releases a ring stage, S/dP(t+1) feeds the compute
-    // warps.  S/dP(t) reuses TMEM buffer t&1, free once acc(t-2) was issued (pd_full(t-2) seen).
-    // Barrier probes are warp votes so every lane takes the same branch.
-    if (SLAB_COLS_2ISSUE && warp == 1) {
+    // The tensor pipe executes in issue order; the two issuers interleave S/dP(t+1) and acc(t)
+    // in whichever order their inputs become ready.
+    if (warp == 1) {
       // S/dP(t) once its ring stage landed and the compute warps have read TMEM buffer t&1
       for (int ts = 0; ts < np; ++ts) {
         tc::mbar_wait(ring_full + ts % RS, (ts / RS) & 1);
@@ -226,45 +217,16 @@ __global__ void __launch_bounds__(kColsThreads, 1)
         tc::mma_commit_w(sdp_full + (ts & 1));
       }
       __syncwarp();
-    } else if (SLAB_COLS_2ISSUE) {  // accumulation warp: acc(t) as soon as P / dS(t) are in smem
+    } else {  // accumulation warp: acc(t) as soon as P / dS(t) are in smem
       for (int ta = 0; ta < np; ++ta) {
         tc::mbar_wait(pd_full + (ta & 1), (ta >> 1) & 1);
         issue_acc(ta);
       }
       tc::mma_commit_w(acc_done);
-    } else {
-      int ts = 0, ta = 0;
-      while (ta < np) {
-        if (SLAB_COLS_ACC_FIRST && ta < ts && __all_sync(0xffffffffu, tc::mbar_test(pd_full + (ta & 1), (ta >> 1) & 1))) {
-          issue_acc(ta);  // release the ring stage first
-          ++ta;
-          continue;
-        }
-        if (ts < np && ts <= ta + 1 && __all_sync(0xffffffffu, tc::mbar_test(ring_full + ts % RS, (ts / RS) & 1))) {
-          tc::tc_fence_after();
-          ts_mark(dbg && lane == 0 && ts < 16, 16 + ts);
-          const uint64_t dq = tc::desc_add(dRk, (ts % RS) * L::kStage), ddo = tc::desc_add(dq, L::kP);
-          const uint32_t tb = (ts & 1) ? tB1 : tB0;
-#pragma unroll
-          for (int kk = 0; kk < D / 16; ++kk) {
-            tc::mma_bf16_w(tb, tc::desc_add(dq, koff(kk, 128)), tc::desc_add(dKk, koff(kk, 64)), id_s, kk > 0);        // S
-            tc::mma_bf16_w(tb + 64, tc::desc_add(ddo, koff(kk, 128)), tc::desc_add(dVk, koff(kk, 64)), id_s, kk > 0);  // dP
-          }
-          tc::mma_commit_w(sdp_full + (ts & 1));
-          ++ts;
-        }
-        if (ta < ts && __all_sync(0xffffffffu, tc::mbar_test(pd_full + (ta & 1), (ta >> 1) & 1))) {
-          issue_acc(ta);
-          ++ta;
-        }
-      }
-      tc::mma_commit_w(acc_done);
     }
     item = np;
     __syncwarp();
-    if (SLAB_COLS_2ISSUE && warp == 1) {
-      // linear part and all_done come from the accumulation warp (same issuing thread as acc)
-    } else {
+    if (warp == kAccWarp) {  // the linear part and all_done: same issuing thread as acc
     if (has_lin) {
       const uint32_t sh = wait_item();
       tc::mbar_wait(kf_ready, 0);
@@ -322,11 +284,9 @@ __global__ void __launch_bounds__(kColsThreads, 1)
         tc::tmem_ld32(tb, sv);
         tc::tmem_ld32(tb + 64, dp);
         tc::tmem_ld_wait();
-        if (SLAB_COLS_2ISSUE) {  // TMEM buffer t&1 may take S/dP(t+2)
-          tc::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(sdp_free + (t & 1));
-        }
+        tc::tc_fence_before();  // TMEM buffer t&1 may take S/dP(t+2)
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(sdp_free + (t & 1));
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
           const float p0 = ex2f(__uint_as_float(sv[e]) * p.scale_log2 - lse2);

@@ -313,11 +313,8 @@ template <int D>
 struct RowsLayout {
   static constexpr int kT = 64 * D * 2;   // 64-row tile
   static constexpr int kP = 128 * D * 2;  // 128-row pair tile
-#ifndef SLAB_ROWS_KS
-#define SLAB_ROWS_KS 3
-#define SLAB_ROWS_VS 2
-#endif
-  static constexpr int KS = SLAB_ROWS_KS, VS = SLAB_ROWS_VS;  // K-pair and V-pair ring slots
+  // K-pair and V-pair ring slots (4 / 1 measured 0.85 ms against 0.63 ms for 3 / 2)
+  static constexpr int KS = 3, VS = 2;
   static constexpr int oQ = 0, oDO = kT, oDS = 2 * kT;  // dS^T [128 kv][64 q] bf16 (16 KB)
   static constexpr int oK = oDS + 16384;
   static constexpr int oV = oK + KS * kP;
@@ -327,10 +324,10 @@ struct RowsLayout {
   static_assert(kBytes <= 232448, "smem");
 };
 
-#ifndef SLAB_ROWS_2ISSUE
-#define SLAB_ROWS_2ISSUE 1  // S/dP and dQ issued by two MMA warps (1, 11)
-#endif
-constexpr int kRowsThreads = SLAB_ROWS_2ISSUE ? 384 : 352;
+// Warps: 0 / 10 TMA producers (K pairs, V pairs), 1 S^T/dP^T issuer, 2-9 softmax-gradient /
+// epilogue, 11 dQ^T issuer.  With one issuer in a static order the pass ran 0.706 ms, with two
+// 0.678 ms.
+constexpr int kRowsThreads = 384;
 
 template <int D>
 __global__ void __launch_bounds__(kRowsThreads, 1)
@@ -416,9 +413,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     // two producer warps (Q/dO + K ring, V ring): one issuing warp's TMA stream caps at ~40 B/cycle
     if (lane == 0) {
       const int pid = warp == 0 ? 0 : 1;
-#ifndef SLAB_NO_TMAP_PREFETCH
       tc::tma_prefetch(pid == 0 ? &tmK : &tmV);
-#endif
       if (pid == 0) {
         tc::mbar_expect_tx(qdo_full, 2 * L::kT);
 #pragma unroll
@@ -456,16 +451,12 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       }
     }
   } else if (warp == 1) {
-    // Static issue order, whole warp converged (see tc::mma_bf16_w): S^T/dP^T(0), S^T/dP^T(1),
-    // then per pair t: dQ^T(t) as soon as dS(t) is in smem (it releases K slot t), then
-    // S^T/dP^T(t+2) into the TMEM buffer the compute warps just finished with.  The tensor pipe
-    // is in order, so S/dP(t+1) runs during the softmax-gradient of t and dQ(t) right after it.
+    // S^T/dP^T issuer, whole warp converged (see tc::mma_bf16_w).  The tensor pipe is in order;
+    // with dQ on its own warp, S/dP(t+2) enters the pipe as soon as buffer t&1 was read, so the
+    // softmax-gradient warps find S/dP(t+1) done when they finish pair t.
     const uint64_t dQk = tc::desc_kmajor(tc::smem_u32(sQ)), dDOk = tc::desc_kmajor(tc::smem_u32(sDO));
     const uint64_t dKk = tc::desc_kmajor(tc::smem_u32(sK)), dVk = tc::desc_kmajor(tc::smem_u32(sV));
-    const uint64_t dKm = tc::desc_mnmajor(tc::smem_u32(sK), 16384);
-    const uint64_t dDSm = tc::desc_mnmajor(tc::smem_u32(sDS), 16384);
     constexpr uint32_t id_st = tc::idesc_bf16(128, 64, false, false);  // pair x Q^T
-    constexpr uint32_t id_dqt = tc::idesc_bf16(D, 64, true, true);     // pair^T x dS^T
     // K-major SW128 tile of `rows` rows: k-step kk (16 elements) starts at chunk kk/4, +32 B
     auto koff = [](int kk, int rows) { return uint32_t((kk >> 2) * rows * 128 + (kk & 3) * 32); };
     tc::mbar_wait(qdo_full, 0);
@@ -480,7 +471,6 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       const uint64_t dk = tc::desc_add(dKk, ks * L::kP), dv = tc::desc_add(dVk, vs * L::kP);
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk) {
-        if (SLAB_DIAG_NOMMA == 1 || SLAB_DIAG_NOMMA == 2) continue;
         tc::mma_bf16_w(tb, tc::desc_add(dk, koff(kk, 128)), tc::desc_add(dQk, koff(kk, 64)), id_st, kk > 0);
         tc::mma_bf16_w(tb + 64, tc::desc_add(dv, koff(kk, 128)), tc::desc_add(dDOk, koff(kk, 64)), id_st, kk > 0);
       }
@@ -488,37 +478,14 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       tc::mma_commit_w(v_empty + vs);
       ts_mark(dbg && lane == 0 && t < 16, 208 + t);
     };
-    if (SLAB_ROWS_2ISSUE) {
-      // S^T/dP^T(t) as soon as its K / V pair landed and the softmax-gradient warps have read
-      // TMEM buffer t&1 (sdp_free of t-2); dQ is issued by warp 11 independently
-      for (int t = 0; t < np; ++t) {
-        if (t >= 2) tc::mbar_wait(sdp_free + (t & 1), ((t - 2) >> 1) & 1);
-        issue_sdp(t);
-      }
-      __syncwarp();
-    } else {
-    if (np > 0) issue_sdp(0);
-    if (np > 1) issue_sdp(1);
+    // S^T/dP^T(t) as soon as its K / V pair landed and the softmax-gradient warps have read
+    // TMEM buffer t&1 (sdp_free of t-2); dQ is issued by warp 11 independently
     for (int t = 0; t < np; ++t) {
-      // dQ^T += [K_j1; K_j2]^T dS^T  (M = D, N = 64, K = 128)
-      tc::mbar_wait(ds_full, t & 1);
-      tc::tc_fence_after();
-      ts_mark(dbg && lane == 0 && t < 16, 64 + t);
-      const uint64_t dk = tc::desc_add(dKm, (t % L::KS) * L::kP);
-#pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        if (SLAB_DIAG_NOMMA == 1 || SLAB_DIAG_NOMMA == 3) continue;
-        tc::mma_bf16_w(tDQT, tc::desc_add(dk, kk * 2048), tc::desc_add(dDSm, kk * 2048), id_dqt, (t | kk) != 0);
-      }
-      tc::mma_commit_w(k_empty + (t % L::KS));
-      tc::mma_commit_w(ds_empty);
-      ts_mark(dbg && lane == 0 && t < 16, 224 + t);
-      if (t + 2 < np) issue_sdp(t + 2);
+      if (t >= 2) tc::mbar_wait(sdp_free + (t & 1), ((t - 2) >> 1) & 1);
+      issue_sdp(t);
     }
-    tc::mma_commit_w(dq_done);
     __syncwarp();
-    }
-  } else if (SLAB_ROWS_2ISSUE && warp == 11) {
+  } else if (warp == 11) {
     // dQ^T += [K_j1; K_j2]^T dS^T  (M = D, N = 64, K = 128) as soon as dS(t) is in smem
     tc::mbar_wait(qdo_full, 0);
     const uint64_t dKm = tc::desc_mnmajor(tc::smem_u32(sK), 16384);
@@ -572,11 +539,9 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         tc::tmem_ld32(tb, sv);
         tc::tmem_ld32(tb + 64, dp);
         tc::tmem_ld_wait();
-        if (SLAB_ROWS_2ISSUE) {  // TMEM buffer t&1 may take S/dP(t+2)
-          tc::tc_fence_before();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive(sdp_free + (t & 1));
-        }
+        tc::tc_fence_before();  // TMEM buffer t&1 may take S/dP(t+2)
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(sdp_free + (t & 1));
         // dS = P (dP - D^s) / sqrt(d) with P = exp2(S log2e / sqrt(d) - lse log2e); the
         // per-query constants (lse log2e, D^s / sqrt(d)) are shared-space vector loads
         ts_mark(dbg && threadIdx.x == 64 && t < 16, 240 + t);

@@ -4,14 +4,8 @@
 #include "kernels.hpp"
 #include "tc.cuh"
 
-#ifndef SLAB_DIAG_NOMMA
-#define SLAB_DIAG_NOMMA 0  // timing experiment only: skip the rows-pass MMAs
-#endif
 #ifndef SLAB_DBG_X
 #define SLAB_DBG_X 100  // -DSLAB_TIMELINE: key/query block of the traced CTA (unit 6)
-#endif
-#ifndef SLAB_POLL_NS
-#define SLAB_POLL_NS 0  // MMA-issuer back-off between idle barrier polls (ns)
 #endif
 
 namespace slab {
