@@ -76,7 +76,8 @@ template <int D>
 __global__ void __launch_bounds__(192, 2)
     k_attn_fwd(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmK,
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmH,
-               const __grid_constant__ CUtensorMap tmW, FwdParams p) {
+               const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmO,
+               const __grid_constant__ CUtensorMap tmOs, const __grid_constant__ CUtensorMap tmOl, FwdParams p) {
   using L = FwdLayout<D>;
   constexpr int RS = L::kSlots;
   constexpr int NC = D / 64;  // 64-column chunks of H / W
@@ -356,10 +357,6 @@ __global__ void __launch_bounds__(192, 2)
 #pragma unroll
       for (int e = 0; e < DH / 2; ++e) olp[e] = 0u;
     }
-#pragma unroll
-    for (int c = 0; c < DH; c += 8)
-      *reinterpret_cast<uint4*>(p.o_l + grow * D + dcol(c)) =
-          make_uint4(olp[c >> 1], olp[(c >> 1) + 1], olp[(c >> 1) + 2], olp[(c >> 1) + 3]);
 
     fts(dbg && threadIdx.x == 64, 99);
     // ---- critical branch: online softmax over the ascending critical list
@@ -453,7 +450,8 @@ __global__ void __launch_bounds__(192, 2)
         v.y = tc::pack_bf16(__uint_as_float(o[e + 2]), __uint_as_float(o[e + 3]));
         v.z = tc::pack_bf16(__uint_as_float(o[e + 4]), __uint_as_float(o[e + 5]));
         v.w = tc::pack_bf16(__uint_as_float(o[e + 6]), __uint_as_float(o[e + 7]));
-        *reinterpret_cast<uint4*>(p.o_s + grow * D + dcol(c0) + e) = v;
+        const int col = dcol(c0) + e;  // staged in the dead Q tile, written by TMA below
+        tc::sts_u4(tc::smem_u32(sQ) + (col >> 6) * 8192 + tc::sw128_off(r, (col >> 3) & 7), v);
       }
       if (has_w) tc::tmem_st32_x2<DH>(tO + lane_base + c0, o);
     }
@@ -487,9 +485,31 @@ __global__ void __launch_bounds__(192, 2)
           v.y = tc::pack_bf16(__uint_as_float(o[e + 2]), __uint_as_float(o[e + 3]));
           v.z = tc::pack_bf16(__uint_as_float(o[e + 4]), __uint_as_float(o[e + 5]));
           v.w = tc::pack_bf16(__uint_as_float(o[e + 6]), __uint_as_float(o[e + 7]));
-          *reinterpret_cast<uint4*>(p.o + grow * D + dcol(c0) + e) = v;
+          const int col = dcol(c0) + e;  // staged in the idle V ring, written by TMA below
+          tc::sts_u4(tc::smem_u32(sV) + (col >> 6) * 8192 + tc::sw128_off(r, (col >> 3) & 7), v);
         }
       }
+    } else {  // no projection: O^l goes to its staging tile (the P buffers, idle after the last PV)
+#pragma unroll
+      for (int c = 0; c < DH; c += 8) {
+        const int col = dcol(c);
+        tc::sts_u4(tc::smem_u32(sPX) + (col >> 6) * 8192 + tc::sw128_off(r, (col >> 3) & 7),
+                   make_uint4(olp[c >> 1], olp[(c >> 1) + 1], olp[(c >> 1) + 2], olp[(c >> 1) + 3]));
+      }
+    }
+    // O^s (Q tile), O^l (X tile) and O (V ring) leave as whole [64 x 64] boxes: coalesced, where
+    // row-per-thread 16-byte stores cost 0.075 ms of the kernel's 0.57
+    tc::fence_proxy_async();
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    if (threadIdx.x == 64) {
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        tc::tma_store_3d(&tmOs, sQ + c * 8192, 64 * c, row0, 0);
+        tc::tma_store_3d(&tmOl, sPX + c * 8192, 64 * c, row0, 0);
+        if (has_w) tc::tma_store_3d(&tmO, sV + c * 8192, 64 * c, row0, 0);
+      }
+      tc::bulk_commit();
+      tc::bulk_wait<0>();
     }
   }
   fts(dbg && threadIdx.x == 64, 101);
@@ -511,9 +531,16 @@ void launch_t(const Dims& Dm, const void* q, const void* k, const void* v, const
     make_tmap_bf16(&tw, w, D, uint64_t(Dm.H) * D, 1, D, 0, D);
   else
     tw = th;
+  CUtensorMap to, tos, tol;  // output boxes [64 rows][64 cols]
+  make_tmap_bf16(&tos, p.o_s, D, rows, 1, D, 0, 64);
+  make_tmap_bf16(&tol, p.o_l, D, rows, 1, D, 0, 64);
+  if (p.o)
+    make_tmap_bf16(&to, p.o, D, rows, 1, D, 0, 64);
+  else
+    to = tos;
   auto kern = k_attn_fwd<D>;
   SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdLayout<D>::kBytes));
-  kern<<<dim3(Dm.Tm, unsigned(Dm.U)), 192, FwdLayout<D>::kBytes, st>>>(tq, tk, tv, th, tw, p);
+  kern<<<dim3(Dm.Tm, unsigned(Dm.U)), 192, FwdLayout<D>::kBytes, st>>>(tq, tk, tv, th, tw, to, tos, tol, p);
   check_launch("k_attn_fwd", st);
 }
 
