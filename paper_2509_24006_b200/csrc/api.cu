@@ -176,7 +176,8 @@ void unpad_rows(const Dims& D, void* dst, const void* src, size_t row_bytes, cud
   copy_units(dst, src, D.U, size_t(D.N_valid) * row_bytes, size_t(D.N) * row_bytes, st);
 }
 
-void classify_into_state(const sla_b200_problem* p, const Dims& D, const void* q, const void* k,
+// returns true when the fast path's marginal indicator M0 was written along with the labels
+bool classify_into_state(const sla_b200_problem* p, const Dims& D, const void* q, const void* k,
                          const int8_t* mask_in, double* p_c, const StateBufs& s,
                          const WorkBufs& w, cudaStream_t st) {
   if (mask_in) {
@@ -188,9 +189,9 @@ void classify_into_state(const sla_b200_problem* p, const Dims& D, const void* q
     launch_build_lut(D, s, check ? w.err + 1 : nullptr, st);
     if (check && read_slot(w.err + 1, st) != LLONG_MAX)
       throw InvalidArgument("build_lookup: label must be -1, 0 or 1");
-  } else {
-    launch_classify(D, p->dtype, p->mask_precision, q, k, s, w, p_c, st);
+    return false;
   }
+  return launch_classify(D, p->dtype, p->mask_precision, q, k, s, w, p_c, st);
 }
 
 }  // namespace
@@ -292,9 +293,9 @@ int sla_b200_forward(const sla_b200_problem* p, const void* q, const void* k, co
     }
     const bool check = p->flags & SLA_B200_FLAG_CHECK_FINITE;
     if (check) check_inputs(p, D, wb, {{"Q", q}, {"K", k}, {"V", v}}, st);
-    classify_into_state(p, D, q, k, mask_in, nullptr, s, wb, st);
+    const bool m0_ready = classify_into_state(p, D, q, k, mask_in, nullptr, s, wb, st);
     if (use_fast(p, D))
-      fast_forward(D, q, k, v, w, o, o_s, o_l, lse, s, wb, st);
+      fast_forward(D, q, k, v, w, o, o_s, o_l, lse, s, wb, m0_ready, st);
     else
       generic_forward(D, p->dtype, q, k, v, w, o, o_s, o_l, lse, s, wb, st);
     if (check) {  // forward.cpp:164-170

@@ -271,7 +271,8 @@ __global__ void __launch_bounds__(256) k_classify_warp(const R* __restrict__ sco
                                                        int Tn, int n1, int n_neg,
                                                        int8_t* __restrict__ labels, int* __restrict__ crit_cnt,
                                                        int* __restrict__ crit_idx, int* __restrict__ marg_cnt,
-                                                       double* __restrict__ p_c_out) {
+                                                       double* __restrict__ p_c_out,
+                                                       __nv_bfloat16* __restrict__ m0, int m0_ld) {
   constexpr int P2 = 32 * EPL;
   __shared__ int8_t slab[8][P2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -361,6 +362,14 @@ __global__ void __launch_bounds__(256) k_classify_warp(const R* __restrict__ sco
   __syncwarp();
   int8_t* lrow = labels + row * Tn;
   for (int j = lane; j < Tn; j += 32) lrow[j] = lab[j];
+  if (m0) {  // fast path: the marginal indicator row (A operand of H = M0 h), bf16 pairs
+    __nv_bfloat162* mrow = reinterpret_cast<__nv_bfloat162*>(m0 + row * m0_ld);
+    for (int j2 = lane; j2 < m0_ld / 2; j2 += 32) {
+      const int j = 2 * j2;
+      mrow[j2] = __floats2bfloat162_rn(j < Tn && lab[j] == 0 ? 1.f : 0.f,
+                                       j + 1 < Tn && lab[j + 1] == 0 ? 1.f : 0.f);
+    }
+  }
   int base = 0, marg = 0;
   int* crow = crit_idx + row * Tn;
   for (int j0 = 0; j0 < Tn; j0 += 32) {
@@ -475,7 +484,7 @@ void launch_check_finite(const Dims& D, int dtype, const void* x, long long* slo
 }
 
 template <typename R, typename In>
-static void classify_t(const Dims& D, const In* q, const In* k, const StateBufs& s,
+static bool classify_t(const Dims& D, const In* q, const In* k, const StateBufs& s,
                        const WorkBufs& w, double* p_c, cudaStream_t st) {
   R* pq = reinterpret_cast<R*>(w.pq);
   R* pk = reinterpret_cast<R*>(w.pk);
@@ -507,40 +516,39 @@ static void classify_t(const Dims& D, const In* q, const In* k, const StateBufs&
   const unsigned wblocks = unsigned((rows + 7) / 8);
   auto warp_rows = [&](auto kern) {
     kern<<<wblocks, 256, 0, st>>>(scores, rows, D.Tn, D.n1, D.n_neg, s.labels, s.crit_cnt, s.crit_idx,
-                                  s.marg_cnt, p_c);
+                                  s.marg_cnt, p_c, s.M0, int(m0_stride(D)));
     check_launch("k_classify", st);
   };
   switch (P2) {  // one warp per block row while a row fits 16 registers per lane
-    case 32: warp_rows(k_classify_warp<R, 1>); return;
-    case 64: warp_rows(k_classify_warp<R, 2>); return;
-    case 128: warp_rows(k_classify_warp<R, 4>); return;
-    case 256: warp_rows(k_classify_warp<R, 8>); return;
-    case 512: warp_rows(k_classify_warp<R, 16>); return;
+    case 32: warp_rows(k_classify_warp<R, 1>); return true;
+    case 64: warp_rows(k_classify_warp<R, 2>); return true;
+    case 128: warp_rows(k_classify_warp<R, 4>); return true;
+    case 256: warp_rows(k_classify_warp<R, 8>); return true;
+    case 512: warp_rows(k_classify_warp<R, 16>); return true;
     default: break;
   }
   k_classify<R><<<dim3(D.Tm, unsigned(D.U)), 256, smem, st>>>(
       scores, D.Tm, D.Tn, P2, D.n1, D.n_neg, s.labels,
       s.crit_cnt, s.crit_idx, s.marg_cnt, p_c);
   check_launch("k_classify", st);
+  return false;
 }
 
-void launch_classify(const Dims& D, int dtype, int mask_precision, const void* q, const void* k,
+bool launch_classify(const Dims& D, int dtype, int mask_precision, const void* q, const void* k,
                      const StateBufs& s, const WorkBufs& w, double* p_c, cudaStream_t st) {
   // the f32 variant computes 1/sqrt(d) in f32 as well
   if (dtype == 0) {
     auto qb = static_cast<const __nv_bfloat16*>(q);
     auto kb = static_cast<const __nv_bfloat16*>(k);
     if (mask_precision == 0)
-      classify_t<double>(D, qb, kb, s, w, p_c, st);
-    else
-      classify_t<float>(D, qb, kb, s, w, p_c, st);
+      return classify_t<double>(D, qb, kb, s, w, p_c, st);
+    return classify_t<float>(D, qb, kb, s, w, p_c, st);
   } else {
     auto qf = static_cast<const float*>(q);
     auto kf = static_cast<const float*>(k);
     if (mask_precision == 0)
-      classify_t<double>(D, qf, kf, s, w, p_c, st);
-    else
-      classify_t<float>(D, qf, kf, s, w, p_c, st);
+      return classify_t<double>(D, qf, kf, s, w, p_c, st);
+    return classify_t<float>(D, qf, kf, s, w, p_c, st);
   }
 }
 

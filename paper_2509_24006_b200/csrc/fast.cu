@@ -143,7 +143,7 @@ bool fast_supported(const Dims& D, int dtype) {
 }
 
 void fast_prepare_linear(const Dims& Dm, const void* k, const void* v, const StateBufs& s,
-                         const WorkBufs& wb, cudaStream_t st) {
+                         const WorkBufs& wb, bool m0_ready, cudaStream_t st) {
   const int d = Dm.d;
   if (d == 128)
     k_phi_kz<128><<<dim3(Dm.Tn, unsigned(Dm.U)), 256, 0, st>>>(
@@ -173,7 +173,7 @@ void fast_prepare_linear(const Dims& Dm, const void* k, const void* v, const Sta
   g.name = "gemm_summaries";
   launch_gemm(g, st);
   // H = M0 . h per unit: M = Tm, N = d*d, K = Tn
-  launch_build_m0(Dm, s, st);
+  if (!m0_ready) launch_build_m0(Dm, s, st);  // the warp classifier writes M0 itself
   GemmArgs a{};
   a.A = s.M0;
   a.B = wb.hb;
@@ -198,8 +198,8 @@ void fast_prepare_linear(const Dims& Dm, const void* k, const void* v, const Sta
 
 void fast_forward(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
                   void* o, void* o_s, void* o_l, float* lse, const StateBufs& s,
-                  const WorkBufs& wb, cudaStream_t st) {
-  fast_prepare_linear(Dm, k, v, s, wb, st);
+                  const WorkBufs& wb, bool m0_ready, cudaStream_t st) {
+  fast_prepare_linear(Dm, k, v, s, wb, m0_ready, st);
   launch_attn_fwd(Dm, q, k, v, w, o, o_s, o_l, lse, s, st);
 }
 

@@ -9,7 +9,8 @@ namespace slab {
 size_t classify_smem_bytes(const Dims& D, bool f64);
 void launch_check_finite(const Dims& D, int dtype, const void* x, long long* slot,
                          cudaStream_t st);
-void launch_classify(const Dims& D, int dtype, int mask_precision, const void* q, const void* k,
+// returns true when it also wrote the fast path's marginal indicator M0 (s.M0 non-null)
+bool launch_classify(const Dims& D, int dtype, int mask_precision, const void* q, const void* k,
                      const StateBufs& s, const WorkBufs& w, double* p_c, cudaStream_t st);
 void launch_build_lut(const Dims& D, const StateBufs& s, long long* bad, cudaStream_t st);
 void launch_build_csc(const Dims& D, const StateBufs& s, cudaStream_t st);
@@ -43,7 +44,7 @@ inline long long m0_stride(const Dims& D) { return (D.Tn + 7) / 8 * 8; }  // 16-
 void launch_attn_fwd(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
                      void* o, void* o_s, void* o_l, float* lse, const StateBufs& s, cudaStream_t st);
 void fast_prepare_linear(const Dims& Dm, const void* k, const void* v, const StateBufs& s,
-                         const WorkBufs& wb, cudaStream_t st);
+                         const WorkBufs& wb, bool m0_ready, cudaStream_t st);
 void launch_bwd_lin(const Dims& Dm, const void* q, const void* w, const void* o_s, const void* o_l,
                     const void* d_out, const StateBufs& s, __nv_bfloat16* gH, __nv_bfloat16* z3, float* Ds,
                     __nv_bfloat16* dqphi, cudaStream_t st);
@@ -56,7 +57,7 @@ void launch_bwd_cols(const Dims& Dm, const void* q, const void* k, const void* v
 bool fast_supported(const Dims& D, int dtype);
 void fast_forward(const Dims& D, const void* q, const void* k, const void* v, const void* w,
                   void* o, void* o_s, void* o_l, float* lse, const StateBufs& s,
-                  const WorkBufs& wb, cudaStream_t st);
+                  const WorkBufs& wb, bool m0_ready, cudaStream_t st);
 void fast_backward(const Dims& D, const void* q, const void* k, const void* v, const void* w,
                    const void* o_s, const void* o_l, const float* lse, const void* d_out,
                    void* dq, void* dk, void* dv, float* dw, const StateBufs& s,
