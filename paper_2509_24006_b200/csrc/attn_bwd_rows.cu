@@ -294,7 +294,7 @@ __global__ void __launch_bounds__(192, 2)
         const int rr = e / (D / 8), cc = (e % (D / 8)) * 8;
         *reinterpret_cast<uint4*>(dqp + (long long)rr * D + cc) = *reinterpret_cast<const uint4*>(sX + tile_off(rr, cc));
       }
-      if (tid == 0) tc::bulk_wait<0>();  // dH_i stores have read the staging smem
+      if (tid == 0) tc::bulk_wait_read<0>();  // dH_i stores have read the staging smem
     } else {
       for (int e = tid; e < D * D / 8; e += 128) reinterpret_cast<uint4*>(gHi)[e] = make_uint4(0, 0, 0, 0);
       for (int a = tid; a < D; a += 128) tc::store_split3(p.z3 + urow * 3 * D + a, D, 0.f);

@@ -329,8 +329,17 @@ __global__ void __launch_bounds__(192, 2)
 #pragma unroll
       for (int c = 0; c < DH; c += 8) {
         const int col = dcol(c);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) den = fmaf(x[c + e], sZ[col + e], den);
+        {  // Z_i from smem as two 16-byte loads per 8 columns
+          const float4 z0 = *reinterpret_cast<const float4*>(sZ + col), z1 = *reinterpret_cast<const float4*>(sZ + col + 4);
+          den = fmaf(x[c], z0.x, den);
+          den = fmaf(x[c + 1], z0.y, den);
+          den = fmaf(x[c + 2], z0.z, den);
+          den = fmaf(x[c + 3], z0.w, den);
+          den = fmaf(x[c + 4], z1.x, den);
+          den = fmaf(x[c + 5], z1.y, den);
+          den = fmaf(x[c + 6], z1.z, den);
+          den = fmaf(x[c + 7], z1.w, den);
+        }
         *reinterpret_cast<uint4*>(sPX + (col >> 6) * 8192 + tc::sw128_off(r, (col >> 3) & 7)) =
             make_uint4(tc::pack_bf16(x[c], x[c + 1]), tc::pack_bf16(x[c + 2], x[c + 3]),
                        tc::pack_bf16(x[c + 4], x[c + 5]), tc::pack_bf16(x[c + 6], x[c + 7]));
@@ -509,7 +518,7 @@ __global__ void __launch_bounds__(192, 2)
         if (has_w) tc::tma_store_3d(&tmO, sV + c * 8192, 64 * c, row0, 0);
       }
       tc::bulk_commit();
-      tc::bulk_wait<0>();
+      tc::bulk_wait_read<0>();  // smem may be released; the writes complete with the grid
     }
   }
   fts(dbg && threadIdx.x == 64, 101);

@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(224, 1)
       if (lane == 0) tc::mbar_arrive(&tempty[ab]);
     }
   }
-  if (threadIdx.x == 64) tc::bulk_wait<0>();
+  if (threadIdx.x == 64) tc::bulk_wait_read<0>();
   tc::tc_fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc<2 * BN>(tmem);
