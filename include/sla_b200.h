@@ -71,6 +71,10 @@ extern "C" {
  * softmax weight, no phi(K) summary), and only rows < N are read or written.  For N % b == 0
  * the results are identical to the unflagged call.  tcgen05 path only (bf16, b_q = b_kv = 64). */
 #define SLA_B200_FLAG_RAGGED 4u
+/* Token-major tensors: q, k, v, o, o_s, o_l, dO, dq, dk, dv are [B, N, H, d] and lse is [B, N, H]
+ * (the layout a DiT's fused QKV projection produces) instead of the unit-major [B, H, N, d].
+ * Staged through unit-major copies in the workspace; tcgen05 path only. */
+#define SLA_B200_FLAG_BNHD 8u
 
 typedef struct sla_b200_problem {
   int64_t batch;    /* B                                  */

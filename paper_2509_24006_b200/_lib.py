@@ -16,7 +16,7 @@ OK, ERR_RUNTIME, ERR_INVALID = 0, 1, 2
 PHI = {"elu1": 0, "relu": 1, "softmax": 2}
 DTYPE_BF16, DTYPE_F32 = 0, 1
 MASK_F64, MASK_F32 = 0, 1
-FLAG_CHECK_FINITE, FLAG_GENERIC, FLAG_RAGGED = 1, 2, 4
+FLAG_CHECK_FINITE, FLAG_GENERIC, FLAG_RAGGED, FLAG_BNHD = 1, 2, 4, 8
 
 
 class Problem(C.Structure):

@@ -9,14 +9,14 @@ same through libsla_b200.so:
   forward : mask prediction, fused sparse + linear forward, O = O^s + O^l W  (one C-ABI call)
   backward: dQ_total, dK_total, dV and dW                                   (one C-ABI call)
 
-Layouts: "bhnd" ([B, H, N, d], the library's native unit-major layout, zero-copy) or "bnhd"
-([B, N, H, d], the usual DiT projection output, transposed to unit-major on the way in and
-back on the way out).  W is the per-head projection [H, d, d] (indexed [in][out]) or one
+Layouts: "bhnd" ([B, H, N, d], the library's native unit-major layout) or "bnhd" ([B, N, H, d],
+the usual DiT projection output, passed as-is with SLA_B200_FLAG_BNHD).  W is the per-head projection [H, d, d] (indexed [in][out]) or one
 shared [d, d] matrix; its gradient comes back in the same shape (a shared W receives the
 sum over heads).  Operators are cached per (shape, config, dtype, device).
 """
 from __future__ import annotations
 
+import dataclasses
 from typing import Dict, Optional, Tuple
 
 import torch
@@ -29,7 +29,7 @@ _OPS: Dict[Tuple, SLA] = {}
 def _op(batch: int, heads: int, n: int, d: int, b_q: int, b_kv: int, cfg: SlaConfig,
         dtype: torch.dtype, device: torch.device) -> SLA:
     key = (batch, heads, n, d, b_q, b_kv, cfg.k_h, cfg.k_l, cfg.phi, cfg.mask_precision,
-           cfg.check_finite, cfg.force_generic, cfg.ragged, dtype, device)
+           cfg.check_finite, cfg.force_generic, cfg.ragged, cfg.bnhd, dtype, device)
     op = _OPS.get(key)
     if op is None:
         op = SLA(batch, heads, n, d, b_q, b_kv, cfg, dtype, device)
@@ -62,10 +62,12 @@ def sparse_linear_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, w
         raise ValueError(f"sparse_linear_attention: unknown layout {layout!r}")
     if q.dim() != 4 or k.shape != q.shape or v.shape != q.shape:
         raise ValueError("sparse_linear_attention: q, k, v must share one 4-D shape")
-    if layout == "bnhd":
-        q, k, v = (t.transpose(1, 2) for t in (q, k, v))
     q, k, v = (t.contiguous() for t in (q, k, v))
-    batch, heads, n, d = q.shape
+    if layout == "bnhd":  # token-major tensors go to the library as they are (SLA_B200_FLAG_BNHD)
+        cfg = dataclasses.replace(cfg, bnhd=True)
+        batch, n, heads, d = q.shape
+    else:
+        batch, heads, n, d = q.shape
     shared_w = w.dim() == 2
     if shared_w:
         if w.shape != (d, d):
@@ -77,8 +79,7 @@ def sparse_linear_attention(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, w
         w_h = w
     w_h = w_h.to(q.dtype).contiguous()
     op = _op(batch, heads, n, d, b_q, b_kv, cfg, q.dtype, q.device)
-    o = _SlaFn.apply(q, k, v, w_h, op)
-    return o.transpose(1, 2) if layout == "bnhd" else o
+    return _SlaFn.apply(q, k, v, w_h, op)
 
 
 class SparseLinearAttention(torch.nn.Module):

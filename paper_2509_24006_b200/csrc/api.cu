@@ -27,10 +27,13 @@ Dims resolve(const sla_b200_problem* p) {
   if (p->n <= 0 || p->d <= 0 || p->b_q <= 0 || p->b_kv <= 0)
     throw InvalidArgument("make_block_layout: all sizes must be positive");
   const bool ragged = (p->flags & SLA_B200_FLAG_RAGGED) && (p->n % p->b_q != 0 || p->n % p->b_kv != 0);
-  if (ragged) {
-    if (p->b_q != 64 || p->b_kv != 64 || p->dtype != SLA_B200_BF16 || (p->flags & SLA_B200_FLAG_GENERIC))
-      throw InvalidArgument("sla_b200: ragged N needs the tcgen05 path (bf16, b_q = b_kv = 64)");
-  } else {
+  const bool bnhd = p->flags & SLA_B200_FLAG_BNHD;
+  if ((ragged || bnhd) &&
+      (p->b_q != 64 || p->b_kv != 64 || p->dtype != SLA_B200_BF16 || (p->flags & SLA_B200_FLAG_GENERIC) ||
+       (p->d != 64 && p->d != 128)))
+    throw InvalidArgument(std::string("sla_b200: ") + (ragged ? "ragged N" : "the [B, N, H, d] layout") +
+                          " needs the tcgen05 path (bf16, b_q = b_kv = 64, d in {64, 128})");
+  if (!ragged) {
     if (p->n % p->b_q != 0)
       throw InvalidArgument("make_block_layout: b_q=" + std::to_string(p->b_q) +
                             " does not divide N=" + std::to_string(p->n));
@@ -51,6 +54,8 @@ Dims resolve(const sla_b200_problem* p) {
   D.H = p->heads;
   D.U = p->batch * p->heads;
   D.N_valid = p->n;
+  D.bnhd = bnhd;
+  D.staged = ragged || bnhd;
   D.N = ragged ? (p->n + 63) / 64 * 64 : p->n;
   D.d = int(p->d);
   D.bq = int(p->b_q);
@@ -145,35 +150,41 @@ void check_inputs(const sla_b200_problem* p, const Dims& D, const WorkBufs& w,
   }
 }
 
-// ragged N: [U, N_valid, rows] <-> [U, N, rows] (zero tail rows).  An SM copy kernel: the
-// copy engines behind cudaMemcpy2DAsync moved these ~1 GB per step at a fraction of HBM speed.
-__global__ void k_copy_units(uint4* __restrict__ dst, const uint4* __restrict__ src, long long units,
-                             long long dst_per_unit, long long src_per_unit) {
-  const long long total = units * dst_per_unit;
+// Staged problems (ragged N and/or [B, N, H, d] callers): the kernels run on unit-major
+// [U, N, row] copies with zero tail rows.  An SM gather / scatter kernel (the copy engines
+// behind cudaMemcpy2DAsync moved these ~1 GB per step at a fraction of HBM speed).
+template <typename T>
+__global__ void k_stage_rows(T* __restrict__ dst, const T* __restrict__ src, long long U, long long H,
+                             long long n_pad, long long n_valid, int row_elems, bool bnhd, bool to_unit) {
+  const long long rows = to_unit ? n_pad : n_valid;
+  const long long total = U * rows * row_elems;
   for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
        e += (long long)gridDim.x * blockDim.x) {
-    const long long u = e / dst_per_unit, r = e % dst_per_unit;
-    dst[e] = r < src_per_unit ? src[u * src_per_unit + r] : make_uint4(0, 0, 0, 0);
+    const int ce = int(e % row_elems);
+    const long long rr = e / row_elems, r = rr % rows, u = rr / rows;
+    const long long caller = bnhd ? ((u / H) * n_valid + r) * H + (u % H) : u * n_valid + r;
+    const long long unit = u * n_pad + r;
+    if (to_unit)
+      dst[unit * row_elems + ce] = r < n_valid ? src[caller * row_elems + ce] : T{};
+    else
+      dst[caller * row_elems + ce] = src[unit * row_elems + ce];
   }
 }
-void copy_units(void* dst, const void* src, long long units, size_t dst_bytes, size_t src_bytes,
-                cudaStream_t st) {
-  if (dst_bytes % 16 || src_bytes % 16) {  // f32 lse rows of an odd length: copy engines
-    const size_t w = std::min(dst_bytes, src_bytes);
-    SLAB_CUDA(cudaMemcpy2DAsync(dst, dst_bytes, src, src_bytes, w, size_t(units), cudaMemcpyDeviceToDevice, st));
-    if (dst_bytes > w)
-      SLAB_CUDA(cudaMemset2DAsync(static_cast<char*>(dst) + w, dst_bytes, 0, dst_bytes - w, size_t(units), st));
-    return;
+void stage_rows(const Dims& D, void* dst, const void* src, size_t row_bytes, bool to_unit, cudaStream_t st) {
+  if (row_bytes % 16 == 0) {
+    k_stage_rows<uint4><<<148 * 8, 256, 0, st>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), D.U, D.H,
+                                                 D.N, D.N_valid, int(row_bytes / 16), D.bnhd, to_unit);
+  } else {
+    k_stage_rows<uint32_t><<<148 * 8, 256, 0, st>>>(static_cast<uint32_t*>(dst), static_cast<const uint32_t*>(src),
+                                                    D.U, D.H, D.N, D.N_valid, int(row_bytes / 4), D.bnhd, to_unit);
   }
-  k_copy_units<<<148 * 8, 256, 0, st>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), units,
-                                        (long long)(dst_bytes / 16), (long long)(src_bytes / 16));
-  check_launch("k_copy_units", st);
+  check_launch("k_stage_rows", st);
 }
 void pad_rows(const Dims& D, void* dst, const void* src, size_t row_bytes, cudaStream_t st) {
-  copy_units(dst, src, D.U, size_t(D.N) * row_bytes, size_t(D.N_valid) * row_bytes, st);
+  stage_rows(D, dst, src, row_bytes, true, st);
 }
 void unpad_rows(const Dims& D, void* dst, const void* src, size_t row_bytes, cudaStream_t st) {
-  copy_units(dst, src, D.U, size_t(D.N_valid) * row_bytes, size_t(D.N) * row_bytes, st);
+  stage_rows(D, dst, src, row_bytes, false, st);
 }
 
 // returns true when the fast path's marginal indicator M0 was written along with the labels
@@ -248,7 +259,7 @@ int sla_b200_classify(const sla_b200_problem* p, const void* q, const void* k, i
     StateBufs s;
     WorkBufs w;
     buffers(p, D, state, workspace, s, w);
-    if (D.N_valid != D.N) {
+    if (D.staged) {
       const size_t rb = size_t(D.d) * 2;
       pad_rows(D, w.pad[kPQ], q, rb, st);
       pad_rows(D, w.pad[kPK], k, rb, st);
@@ -275,7 +286,7 @@ int sla_b200_forward(const sla_b200_problem* p, const void* q, const void* k, co
     StateBufs s;
     WorkBufs wb;
     buffers(p, D, state, workspace, s, wb);
-    const bool ragged = D.N_valid != D.N;
+    const bool ragged = D.staged;  // ragged N and/or the [B, N, H, d] layout
     void *o_u = o, *o_s_u = o_s, *o_l_u = o_l;
     float* lse_u = lse;
     if (ragged) {  // run on zero-padded copies; only rows < N_valid go back
@@ -339,10 +350,10 @@ int sla_b200_backward_ex(const sla_b200_problem* p, const void* q, const void* k
     WorkBufs wb;
     buffers(p, D, state, workspace, s, wb);
     const bool fast = use_fast(p, D);
-    const bool ragged = D.N_valid != D.N;
+    const bool ragged = D.staged;  // ragged N and/or the [B, N, H, d] layout
     void *dq_u = dq, *dk_u = dk, *dv_u = dv;
     if (ragged) {
-      if (parts) throw InvalidArgument("sla_backward: gradient parts are not available with ragged N");
+      if (parts) throw InvalidArgument("sla_backward: gradient parts are not available for staged layouts");
       const size_t rb = size_t(D.d) * 2;
       pad_rows(D, wb.pad[kPQ], q, rb, st);
       pad_rows(D, wb.pad[kPK], k, rb, st);

@@ -126,7 +126,7 @@ inline void carve_work(const Dims& D, bool fast, void* base, WorkBufs& w, size_t
     w.dqphi = c.take<__nv_bfloat16>(U * N * d);
     const size_t T = Tm > Tn ? Tm : Tn;
     w.z3b = c.take<__nv_bfloat16>(U * T * 3 * d);
-    if (D.N_valid != D.N) {
+    if (D.staged) {
       for (int i = kPQ; i <= kPdV; ++i) w.pad[i] = c.take<__nv_bfloat16>(U * N * d);
       w.pad_lse = c.take<float>(U * N);
     }

@@ -15,6 +15,8 @@ struct Dims {
   int64_t B, H;  // batch, heads
   int64_t N;     // sequence length (rows per unit in the kernels' buffers; padded if ragged)
   int64_t N_valid;  // rows per unit in the caller's tensors (== N unless SLA_B200_FLAG_RAGGED)
+  bool bnhd;        // caller tensors are [B, N, H, d] (SLA_B200_FLAG_BNHD)
+  bool staged;      // ragged or bnhd: kernels run on unit-major zero-padded workspace copies
   int d, bq, bkv;
   int Tm, Tn;    // query / key-value block counts (layout.hpp:10-20)
   int phi;       // 0 elu1, 1 relu, 2 softmax

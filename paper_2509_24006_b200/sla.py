@@ -38,6 +38,7 @@ class SlaConfig:
     check_finite: bool = False    # reproduce the reference's non-finite input/output errors
     force_generic: bool = False   # run the shape-generic SIMT kernels
     ragged: bool = False          # allow N % 64 != 0 (SLA_B200_FLAG_RAGGED; not in the reference)
+    bnhd: bool = False            # tensors are [B, N, H, d], lse [B, N, H] (SLA_B200_FLAG_BNHD)
 
 
 @dataclass
@@ -65,7 +66,7 @@ def _problem(batch, heads, n, d, b_q, b_kv, cfg: SlaConfig, dtype) -> L.Problem:
         raise ValueError(f"unsupported dtype {dtype}")
     p.mask_precision = {"f64": L.MASK_F64, "f32": L.MASK_F32}[cfg.mask_precision]
     p.flags = ((L.FLAG_CHECK_FINITE if cfg.check_finite else 0) | (L.FLAG_GENERIC if cfg.force_generic else 0)
-               | (L.FLAG_RAGGED if cfg.ragged else 0))
+               | (L.FLAG_RAGGED if cfg.ragged else 0) | (L.FLAG_BNHD if cfg.bnhd else 0))
     return p
 
 
@@ -137,6 +138,8 @@ class SLA:
 
     # -- helpers ----------------------------------------------------------------------
     def _unit_shape(self):
+        if self.cfg.bnhd:
+            return (self.batch, self.n, self.heads, self.d)
         return (self.batch, self.heads, self.n, self.d)
 
     def _check(self, name, t, shape=None, dtype=None):

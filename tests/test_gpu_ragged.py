@@ -1,4 +1,5 @@
-"""Ragged N (SLA_B200_FLAG_RAGGED).
+"""Ragged N (SLA_B200_FLAG_RAGGED) and the token-major
+[B, N, H, d] layout (SLA_B200_FLAG_BNHD).
 
 The reference rejects N % b != 0 (layout.cpp:12-17), so there is no reference output to match.
 The semantics are pinned three ways:
@@ -81,7 +82,6 @@ def test_ragged_matches_dense_reference(n, d, phi):
         for got, ref in pairs:
             err = O.rel_diff(got.double().cpu().numpy(), ref.detach().double().cpu().numpy(), 1.0)
             assert err <= 2e-2, err
-    dw_ref = torch.zeros(d, d, device="cuda")
     for h in range(heads):  # per-head dW against the dense reference (summed W gradient per head)
         x = xs[h]
         leaves = [T(x[nm]) for nm in ("q", "k", "v")]
@@ -115,3 +115,28 @@ def test_ragged_needs_the_flag_and_the_fast_path():
         SLA(1, 1, 1000, 64, B, B, SlaConfig(ragged=True), torch.float32)
     with pytest.raises(ValueError, match="ragged"):
         SLA(1, 1, 1000, 64, 32, 32, SlaConfig(ragged=True), torch.bfloat16)
+
+
+@pytest.mark.parametrize("n", [1024, 1000])
+def test_token_major_layout_matches_unit_major(n):
+    """SLA_B200_FLAG_BNHD: [B, N, H, d] tensors (lse [B, N, H]) give the unit-major results bit
+    for bit, with and without a ragged tail."""
+    B, H, d = 2, 3, 64
+    g = torch.Generator(device="cuda").manual_seed(11)
+    q, k, v, do = (torch.randn((B, H, n, d), generator=g, device="cuda").bfloat16() for _ in range(4))
+    w = (torch.randn((H, d, d), generator=g, device="cuda") * 0.1).bfloat16()
+    ragged = n % 64 != 0
+    op1 = SLA(B, H, n, d, 64, 64, SlaConfig(k_h=10.0, k_l=20.0, phi="softmax", ragged=ragged))
+    op2 = SLA(B, H, n, d, 64, 64, SlaConfig(k_h=10.0, k_l=20.0, phi="softmax", ragged=ragged, bnhd=True))
+    t = lambda x: x.transpose(1, 2).contiguous()  # noqa: E731
+    st1 = op1.forward(q, k, v, w)
+    g1 = op1.backward(st1, q, k, v, w, do)
+    st2 = op2.forward(t(q), t(k), t(v), w)
+    g2 = op2.backward(st2, t(q), t(k), t(v), w, t(do))
+    torch.cuda.synchronize()
+    assert torch.equal(st1.labels, st2.labels)
+    for x1, x2 in ((st1.o, st2.o), (st1.o_s, st2.o_s), (st1.o_l, st2.o_l), (g1.dq_total, g2.dq_total),
+                   (g1.dk_total, g2.dk_total), (g1.dv, g2.dv)):
+        assert torch.equal(x1, x2.transpose(1, 2))
+    assert torch.equal(st1.lse, st2.lse.transpose(1, 2))
+    assert torch.equal(g1.dproj, g2.dproj)
