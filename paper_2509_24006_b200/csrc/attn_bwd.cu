@@ -229,16 +229,17 @@ __global__ void __launch_bounds__(kColsThreads, 1)
     if (warp == kAccWarp) {  // the linear part and all_done: same issuing thread as acc
     if (has_lin) {
       const uint32_t sh = wait_item();
+      // dK^phi^T raw = dH_agg V^T (M = D over a, N = 64 keys, K = D over b): needs only dH_agg
+      // and V_j, so it runs while the compute warps still write the phi(K_j) tile
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk) tc::mma_bf16_w(tKPT, kdesc(sh, kk, D), kdesc(aV, kk, 64), id_kp, kk > 0);
       tc::mbar_wait(kf_ready, 0);
       tc::tc_fence_after();
+      // dV^T += dH_agg^T phi(K)^T (M = D over b, N = 64 keys, K = D over a)
 #pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {
-        // dK^phi^T raw = dH_agg V^T (M = D over a, N = 64 keys, K = D over b)
-        tc::mma_bf16_w(tKPT, kdesc(sh, kk, D), kdesc(aV, kk, 64), id_kp, kk > 0);
-        // dV^T += dH_agg^T phi(K)^T (M = D over b, N = 64 keys, K = D over a)
+      for (int kk = 0; kk < D / 16; ++kk)
         tc::mma_bf16_w(tDVT, tc::desc_mnmajor(sh + kk * 2048, D * 128), kdesc(aKF, kk, 64), id_vl,
                        (np > 0 || kk > 0) ? 1u : 0u);
-      }
       tc::mma_commit_w(ring_empty + (item % RS));
       __syncwarp();
       ++item;
