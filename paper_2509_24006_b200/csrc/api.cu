@@ -188,6 +188,27 @@ void unpad_rows(const Dims& D, void* dst, const void* src, size_t row_bytes, cud
 }
 
 // returns true when the fast path's marginal indicator M0 was written along with the labels
+// A non-blocking side stream (and fork / join events) per device and host thread.  The forward
+// runs the mask-independent key summaries there while the classification chain, which is
+// latency- and FP64-bound and leaves most of each SM idle, runs on the caller's stream.
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+SideStream& side_stream() {
+  thread_local SideStream per_dev[16];
+  int dev = 0;
+  SLAB_CUDA(cudaGetDevice(&dev));
+  SideStream& x = per_dev[dev & 15];
+  if (!x.s) {
+    SLAB_CUDA(cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking));
+    SLAB_CUDA(cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming));
+    SLAB_CUDA(cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming));
+  }
+  return x;
+}
+
 bool classify_into_state(const sla_b200_problem* p, const Dims& D, const void* q, const void* k,
                          const int8_t* mask_in, double* p_c, const StateBufs& s,
                          const WorkBufs& w, cudaStream_t st) {
@@ -304,9 +325,22 @@ int sla_b200_forward(const sla_b200_problem* p, const void* q, const void* k, co
     }
     const bool check = p->flags & SLA_B200_FLAG_CHECK_FINITE;
     if (check) check_inputs(p, D, wb, {{"Q", q}, {"K", k}, {"V", v}}, st);
+    const bool fast = use_fast(p, D);
+    // fork: phi(K), z and h = phi(K)^T V on the side stream, concurrent with classification.
+    // Not under the per-kernel profiler (one event sequence) nor with the finiteness checks
+    // (host syncs that may throw between fork and join).
+    const bool fork = fast && !check && !prof_enabled();
+    SideStream* ss = fork ? &side_stream() : nullptr;
+    if (fork) {
+      SLAB_CUDA(cudaEventRecord(ss->fork, st));
+      SLAB_CUDA(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+      fast_summaries(D, k, v, wb, ss->s);
+      SLAB_CUDA(cudaEventRecord(ss->join, ss->s));
+    }
     const bool m0_ready = classify_into_state(p, D, q, k, mask_in, nullptr, s, wb, st);
-    if (use_fast(p, D))
-      fast_forward(D, q, k, v, w, o, o_s, o_l, lse, s, wb, m0_ready, st);
+    if (fork) SLAB_CUDA(cudaStreamWaitEvent(st, ss->join, 0));
+    if (fast)
+      fast_forward(D, q, k, v, w, o, o_s, o_l, lse, s, wb, m0_ready, fork, st);
     else
       generic_forward(D, p->dtype, q, k, v, w, o, o_s, o_l, lse, s, wb, st);
     if (check) {  // forward.cpp:164-170

@@ -69,6 +69,7 @@ __device__ __forceinline__ float phi_elem(int phi, float x) {
 // per-kernel event profiler (profiler.cu)
 void count_launch(int n = 1);
 void prof_mark(const char* name, cudaStream_t st);
+bool prof_enabled();  // per-kernel event profiling on (bench.py's breakdown pass)
 
 #define SLAB_CUDA(call)                                                             \
   do {                                                                              \

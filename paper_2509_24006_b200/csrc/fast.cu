@@ -142,8 +142,9 @@ bool fast_supported(const Dims& D, int dtype) {
   return dtype == 0 && D.bq == 64 && D.bkv == 64 && (D.d == 64 || D.d == 128);
 }
 
-void fast_prepare_linear(const Dims& Dm, const void* k, const void* v, const StateBufs& s,
-                         const WorkBufs& wb, bool m0_ready, cudaStream_t st) {
+// phi(K), z_j and h_j = phi(K_j)^T V_j: independent of the mask, so the C-ABI forward runs them
+// on a side stream while the classification kernels (latency / FP64 bound) run
+void fast_summaries(const Dims& Dm, const void* k, const void* v, const WorkBufs& wb, cudaStream_t st) {
   const int d = Dm.d;
   if (d == 128)
     k_phi_kz<128><<<dim3(Dm.Tn, unsigned(Dm.U)), 256, 0, st>>>(
@@ -172,6 +173,11 @@ void fast_prepare_linear(const Dims& Dm, const void* k, const void* v, const Sta
   g.c_batch = (long long)d * d;
   g.name = "gemm_summaries";
   launch_gemm(g, st);
+}
+
+// H = M0 h, Z = M0 z (needs the mask); M0 itself unless the warp classifier wrote it
+void fast_aggregate(const Dims& Dm, const StateBufs& s, const WorkBufs& wb, bool m0_ready, cudaStream_t st) {
+  const int d = Dm.d;
   // H = M0 . h per unit: M = Tm, N = d*d, K = Tn
   if (!m0_ready) launch_build_m0(Dm, s, st);  // the warp classifier writes M0 itself
   GemmArgs a{};
@@ -198,8 +204,9 @@ void fast_prepare_linear(const Dims& Dm, const void* k, const void* v, const Sta
 
 void fast_forward(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
                   void* o, void* o_s, void* o_l, float* lse, const StateBufs& s,
-                  const WorkBufs& wb, bool m0_ready, cudaStream_t st) {
-  fast_prepare_linear(Dm, k, v, s, wb, m0_ready, st);
+                  const WorkBufs& wb, bool m0_ready, bool summaries_done, cudaStream_t st) {
+  if (!summaries_done) fast_summaries(Dm, k, v, wb, st);
+  fast_aggregate(Dm, s, wb, m0_ready, st);
   launch_attn_fwd(Dm, q, k, v, w, o, o_s, o_l, lse, s, st);
 }
 

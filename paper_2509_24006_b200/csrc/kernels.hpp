@@ -43,8 +43,8 @@ void launch_gemm(const GemmArgs& g, cudaStream_t st);
 inline long long m0_stride(const Dims& D) { return (D.Tn + 7) / 8 * 8; }  // 16-byte rows for TMA
 void launch_attn_fwd(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
                      void* o, void* o_s, void* o_l, float* lse, const StateBufs& s, cudaStream_t st);
-void fast_prepare_linear(const Dims& Dm, const void* k, const void* v, const StateBufs& s,
-                         const WorkBufs& wb, bool m0_ready, cudaStream_t st);
+void fast_summaries(const Dims& Dm, const void* k, const void* v, const WorkBufs& wb, cudaStream_t st);
+void fast_aggregate(const Dims& Dm, const StateBufs& s, const WorkBufs& wb, bool m0_ready, cudaStream_t st);
 void launch_bwd_lin(const Dims& Dm, const void* q, const void* w, const void* o_s, const void* o_l,
                     const void* d_out, const StateBufs& s, __nv_bfloat16* gH, __nv_bfloat16* z3, float* Ds,
                     __nv_bfloat16* dqphi, cudaStream_t st);
@@ -57,7 +57,7 @@ void launch_bwd_cols(const Dims& Dm, const void* q, const void* k, const void* v
 bool fast_supported(const Dims& D, int dtype);
 void fast_forward(const Dims& D, const void* q, const void* k, const void* v, const void* w,
                   void* o, void* o_s, void* o_l, float* lse, const StateBufs& s,
-                  const WorkBufs& wb, bool m0_ready, cudaStream_t st);
+                  const WorkBufs& wb, bool m0_ready, bool summaries_done, cudaStream_t st);
 void fast_backward(const Dims& D, const void* q, const void* k, const void* v, const void* w,
                    const void* o_s, const void* o_l, const float* lse, const void* d_out,
                    void* dq, void* dk, void* dv, float* dw, const StateBufs& s,

@@ -55,6 +55,8 @@ void flush() {
 }
 }  // namespace
 
+bool prof_enabled() { return prof().on; }
+
 void prof_mark(const char* name, cudaStream_t st) {
   Prof& p = prof();
   if (!p.on) return;
