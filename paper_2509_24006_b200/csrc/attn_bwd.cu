@@ -7,8 +7,8 @@
 //   linear dK^phi_j = V_j dH_agg^T + dZ_agg, dV_j += phi(K_j) dH_agg (dH_agg = M0^T dH),
 //   dk_total = J_phi(k)^T dK^phi + dK and dv written once.
 //
-// Warp roles: warps 0 and 10 TMA (each ring stage is filled by both -- Q pair / dO pair -- since
-// one issuing warp's TMA stream caps at ~40 B/cycle), warp 1 MMA (one thread), warps 2-9 compute.
+// Warp roles: warps 0 and 10 TMA (Q pairs / dO pairs, since one issuing warp's TMA stream caps
+// at ~40 B/cycle), warps 1 and 11 MMA, warps 2-9 compute.
 #include "bwd_common.cuh"
 
 namespace slab {
@@ -20,26 +20,45 @@ namespace {
 // transposed (M = D) at full tensor rate; linear dK^phi^T and dV^T += dH_agg^T phi(K)^T on the
 // tensor core; the epilogue transposes through smem and finishes row-wise.
 // =========================================================================================
+// The ring holds slots of one pair tile each: pair t's Q pair is item 2t, its dO pair item 2t+1
+// (item n in slot n % kSlots), and dH_agg the last item.  S(t) waits only for the Q pair, dP(t)
+// for the dO pair; acc(t) runs dK^T first and releases the Q pair's slot halfway, which is the
+// slot dO(t+2) refills (5 slots).  A single P / dS buffer makes room for the fifth slot.
+// Measured (C3, k_bwd_cols ms): 4 slots + 2 P/dS buffers 1.008; 5 + 1 + dK-first 0.890; making
+// acc(t) wait until S/dP(t+1) is queued (SLAB_COLS_PRIO) 0.925 / 1.055 -- slower either way.
+#ifndef SLAB_COLS_SLOTS
+#define SLAB_COLS_SLOTS 5
+#endif
+#ifndef SLAB_COLS_PD
+#define SLAB_COLS_PD 1
+#endif
+#ifndef SLAB_COLS_DKFIRST  // acc(t) issues dK^T (frees the Q pair slot) before dV^T
+#define SLAB_COLS_DKFIRST 1
+#endif
+#ifndef SLAB_COLS_PRIO  // acc(t) enters the tensor queue only after S/dP(t+1) has
+#define SLAB_COLS_PRIO 0
+#endif
 template <int D>
 struct ColsLayout {
   static constexpr int kT = 64 * D * 2;    // 64-row tile
   static constexpr int kP = 128 * D * 2;   // 128-row pair tile
   static constexpr int oK = 0, oV = kT;
   static constexpr int oRing = 2 * kT;
-  static constexpr int kStage = 2 * kP;    // Q pair + dO pair, or dH_agg (D*D*2)
-  static constexpr int kStages = 2;
-  static constexpr int oPD = oRing + kStages * kStage;  // 2 x [P 16 KB | dS 16 KB]; phi(K) aliases
-  static constexpr int oZA = oPD + 65536;               // float [D] dZ_agg
+  static constexpr int kSlot = kP;         // Q pair, dO pair, or dH_agg (D*D*2 <= kP)
+  static constexpr int kSlots = SLAB_COLS_SLOTS;
+  static constexpr int kPD = SLAB_COLS_PD;  // P / dS buffers of [P 16 KB | dS 16 KB]
+  static constexpr int oPD = oRing + kSlots * kSlot;  // phi(K) aliases the P / dS buffer
+  static constexpr int oZA = oPD + kPD * 32768;       // float [D] dZ_agg
   static constexpr int oBar = oZA + 4 * D;
   static constexpr int kBytes = oBar + 256 + 1024;
   static_assert(kBytes <= 232448, "smem");
+  static_assert(D * D * 2 <= kSlot && 3 * 64 * (D + 1) * 4 <= kSlots * kSlot, "ring reuse");
 };
 
 // Warps: 0 and 10 TMA producers, 1 S/dP issuer, 2-9 softmax-gradient / epilogue, 11 the
 // dV / dK accumulation issuer (and the linear-branch MMAs).  Two issuing warps keep one's
 // barrier waits from delaying the other's MMAs (1.09 -> 1.04 ms); 4 producer warps and a
 // single poll-driven issuer were measured no better.
-constexpr int kColsProd = 2;
 constexpr int kAccWarp = 11;
 constexpr int kColsThreads = 32 * 12;
 
@@ -58,11 +77,12 @@ __global__ void __launch_bounds__(kColsThreads, 1)
   uint8_t* sKF = sPD;  // phi(K_j), written once the accumulation MMAs have drained the P/dS buffers
   float* zas = reinterpret_cast<float*>(smem + L::oZA);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::oBar);
-  constexpr int RS = L::kStages;
+  constexpr int RS = L::kSlots;
+  constexpr int PDN = L::kPD;
   uint64_t* kv_full = bars + 0;
   uint64_t* sdp_full = bars + 1;   // [2]
-  uint64_t* pd_full = bars + 3;    // [2]
-  uint64_t* pd_empty = bars + 5;   // [2]
+  uint64_t* pd_full = bars + 3;    // [PDN <= 2]
+  uint64_t* pd_empty = bars + 5;   // [PDN <= 2]
   uint64_t* acc_done = bars + 7;
   uint64_t* kf_ready = bars + 8;
   uint64_t* all_done = bars + 9;
@@ -70,6 +90,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
   uint64_t* ring_full = bars + 16;        // [RS]
   uint64_t* ring_empty = bars + 16 + RS;  // [RS]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + 2 * RS);
+  volatile int* sdp_issued = reinterpret_cast<volatile int*>(tmem_slot + 1);  // S/dP pairs queued
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = blockIdx.x;
@@ -89,7 +110,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
     if (lane == 0) {
       tc::mbar_init(kv_full, 1);
       for (int s = 0; s < RS; ++s) {
-        tc::mbar_init(ring_full + s, kColsProd);  // one arrive.expect_tx per producer warp
+        tc::mbar_init(ring_full + s, 1);  // one arrive.expect_tx: the item's producer warp
         tc::mbar_init(ring_empty + s, 1);
       }
       for (int s = 0; s < 2; ++s) {
@@ -102,6 +123,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
       tc::mbar_init(sdp_free + 1, 8);
       tc::mbar_init(kf_ready, 8);
       tc::mbar_init(all_done, 1);
+      *sdp_issued = 0;
       tc::fence_barrier_init();
     }
     __syncwarp();
@@ -131,18 +153,18 @@ __global__ void __launch_bounds__(kColsThreads, 1)
           tc::tma_load_3d(sV + c * 8192, &tmV, kv_full, 64 * c, kv0, 0);
         }
       }
-      int item = 0;
-      auto acquire = [&](int bytes) -> uint8_t* {
+      auto acquire = [&](int item, int bytes) -> uint8_t* {
         const int s = item % RS;
         tc::mbar_wait(ring_empty + s, ((item / RS) & 1) ^ 1);
         tc::mbar_expect_tx(ring_full + s, bytes);
-        return sRing + s * L::kStage;
+        return sRing + s * L::kSlot;
       };
       const CUtensorMap* tm = pid ? &tmDO : &tmQ;
       for (int pp = 0; pp < np; ++pp) {
         const int r1 = int(u * p.N) + list[2 * pp] * 64;
         const int r2 = int(u * p.N) + list[min(2 * pp + 1, cnt - 1)] * 64;
-        uint8_t* dst = acquire(L::kP) + pid * L::kP;
+        const int item = 2 * pp + pid;
+        uint8_t* dst = acquire(item, L::kP);
         ts_mark(dbg && pid == 0 && pp < 16, pp);
         uint64_t* fb = ring_full + (item % RS);
 #pragma unroll
@@ -150,14 +172,13 @@ __global__ void __launch_bounds__(kColsThreads, 1)
           tc::tma_load_3d(dst + c * 16384, tm, fb, 64 * c, r1, 0);
           tc::tma_load_3d(dst + c * 16384 + 8192, tm, fb, 64 * c, r2, 0);
         }
-        ++item;
       }
-      if (has_lin) {  // dH_agg chunk c by producer c (D / 64 <= 2 chunks)
-        constexpr int NC = D / 64;
-        uint8_t* dst = acquire(pid < NC ? D * 128 : 0);
-        if (pid < NC)
-          tc::tma_load_3d(dst + pid * D * 128, &tmHa, ring_full + (item % RS), 64 * pid, int(ucol * D), 0);
-        ++item;
+      if (has_lin && pid == 0) {  // dH_agg: the last item, D / 64 chunks of [D rows x 64]
+        const int item = 2 * np;
+        uint8_t* dst = acquire(item, D * D * 2);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c)
+          tc::tma_load_3d(dst + c * D * 128, &tmHa, ring_full + (item % RS), 64 * c, int(ucol * D), 0);
       }
     }
   } else if (warp == 1 || warp == kAccWarp) {
@@ -167,12 +188,11 @@ __global__ void __launch_bounds__(kColsThreads, 1)
     constexpr uint32_t id_acc = tc::idesc_bf16(D, 64, true, true);     // pair^T x P
     constexpr uint32_t id_kp = tc::idesc_bf16(D, 64, false, false);    // dH_agg x V^T
     constexpr uint32_t id_vl = tc::idesc_bf16(D, 64, true, false);     // dH_agg^T x phi(K)^T
-    int item = 0;
-    auto wait_item = [&]() -> uint32_t {
+    auto wait_item = [&](int item) -> uint32_t {
       const int s = item % RS;
       tc::mbar_wait(ring_full + s, (item / RS) & 1);
       tc::tc_fence_after();
-      return aR + s * L::kStage;
+      return aR + s * L::kSlot;
     };
     auto kdesc = [](uint32_t base, int kk, int rows) {
       return tc::desc_kmajor(base + (kk >> 2) * rows * 128 + (kk & 3) * 32);
@@ -182,53 +202,78 @@ __global__ void __launch_bounds__(kColsThreads, 1)
     ts_mark(dbg && lane == 0, 125);
     cta_mark(lane == 0, 1);
     // Whole warp runs the issue loop (warp-uniform operands, one elected lane issues; see
-    // tc::mma_bf16_w).  Descriptors: ring stage s at +s*kStage, k-step kk at +koff / +kk*2048.
+    // tc::mma_bf16_w).  Descriptors: ring slot s at +s*kSlot, k-step kk at +koff / +kk*2048.
     const uint64_t dRk = tc::desc_kmajor(aR), dKk = tc::desc_kmajor(aK), dVk = tc::desc_kmajor(aV);
     const uint64_t dRm = tc::desc_mnmajor(aR, 16384), dPDm = tc::desc_mnmajor(aPD, 16384);
     auto koff = [](int kk, int rows) { return uint32_t((kk >> 2) * rows * 128 + (kk & 3) * 32); };
     auto issue_acc = [&](int t) {  // dV^T += dO_pair^T P, dK^T += Q_pair^T dS  (M = D, K = 128)
       tc::tc_fence_after();
-      const uint64_t dq = tc::desc_add(dRm, (t % RS) * L::kStage), ddo = tc::desc_add(dq, L::kP);
-      const uint64_t dp = tc::desc_add(dPDm, (t & 1) * 32768), dd = tc::desc_add(dp, 16384);
+      const int sq = (2 * t) % RS, sdo = (2 * t + 1) % RS;
+      const uint64_t dq = tc::desc_add(dRm, sq * L::kSlot), ddo = tc::desc_add(dRm, sdo * L::kSlot);
+      const uint64_t dp = tc::desc_add(dPDm, (t % PDN) * 32768), dd = tc::desc_add(dp, 16384);
+      auto dv = [&] {
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk) {
-        tc::mma_bf16_w(tDVT, tc::desc_add(ddo, kk * 2048), tc::desc_add(dp, kk * 2048), id_acc, (t | kk) != 0);
-        tc::mma_bf16_w(tDKT, tc::desc_add(dq, kk * 2048), tc::desc_add(dd, kk * 2048), id_acc, (t | kk) != 0);
+        for (int kk = 0; kk < 8; ++kk)
+          tc::mma_bf16_w(tDVT, tc::desc_add(ddo, kk * 2048), tc::desc_add(dp, kk * 2048), id_acc, (t | kk) != 0);
+        tc::mma_commit_w(ring_empty + sdo);  // the slot refills while the other half runs
+      };
+      auto dk = [&] {
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          tc::mma_bf16_w(tDKT, tc::desc_add(dq, kk * 2048), tc::desc_add(dd, kk * 2048), id_acc, (t | kk) != 0);
+        tc::mma_commit_w(ring_empty + sq);
+      };
+      if (SLAB_COLS_DKFIRST) {
+        dk();
+        dv();
+      } else {
+        dv();
+        dk();
       }
-      tc::mma_commit_w(ring_empty + (t % RS));
-      tc::mma_commit_w(pd_empty + (t & 1));
+      tc::mma_commit_w(pd_empty + (t % PDN));
     };
     // The tensor pipe executes in issue order; the two issuers interleave S/dP(t+1) and acc(t)
     // in whichever order their inputs become ready.
     if (warp == 1) {
       // S/dP(t) once its ring stage landed and the compute warps have read TMEM buffer t&1
       for (int ts = 0; ts < np; ++ts) {
-        tc::mbar_wait(ring_full + ts % RS, (ts / RS) & 1);
+        const int iq = 2 * ts, ido = 2 * ts + 1;
         if (ts >= 2) tc::mbar_wait(sdp_free + (ts & 1), ((ts - 2) >> 1) & 1);
+        tc::mbar_wait(ring_full + iq % RS, (iq / RS) & 1);
         tc::tc_fence_after();
         ts_mark(dbg && lane == 0 && ts < 16, 16 + ts);
-        const uint64_t dq = tc::desc_add(dRk, (ts % RS) * L::kStage), ddo = tc::desc_add(dq, L::kP);
+        const uint64_t dq = tc::desc_add(dRk, (iq % RS) * L::kSlot), ddo = tc::desc_add(dRk, (ido % RS) * L::kSlot);
         const uint32_t tb = (ts & 1) ? tB1 : tB0;
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          tc::mma_bf16_w(tb, tc::desc_add(dq, koff(kk, 128)), tc::desc_add(dKk, koff(kk, 64)), id_s, kk > 0);        // S
-          tc::mma_bf16_w(tb + 64, tc::desc_add(ddo, koff(kk, 128)), tc::desc_add(dVk, koff(kk, 64)), id_s, kk > 0);  // dP
-        }
+        for (int kk = 0; kk < D / 16; ++kk)  // S = Q_pair K_j^T as soon as the Q pair landed
+          tc::mma_bf16_w(tb, tc::desc_add(dq, koff(kk, 128)), tc::desc_add(dKk, koff(kk, 64)), id_s, kk > 0);
+        tc::mbar_wait(ring_full + ido % RS, (ido / RS) & 1);
+        tc::tc_fence_after();
+        ts_mark(dbg && lane == 0 && ts < 16, 80 + ts);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)  // dP = dO_pair V_j^T
+          tc::mma_bf16_w(tb + 64, tc::desc_add(ddo, koff(kk, 128)), tc::desc_add(dVk, koff(kk, 64)), id_s, kk > 0);
         tc::mma_commit_w(sdp_full + (ts & 1));
+        __syncwarp();
+        if (lane == 0) *sdp_issued = ts + 1;
       }
       __syncwarp();
     } else {  // accumulation warp: acc(t) as soon as P / dS(t) are in smem
       for (int ta = 0; ta < np; ++ta) {
-        tc::mbar_wait(pd_full + (ta & 1), (ta >> 1) & 1);
+        tc::mbar_wait(pd_full + (ta % PDN), (ta / PDN) & 1);
+        if (SLAB_COLS_PRIO && ta + 1 < np)
+          while (*sdp_issued < ta + 2) {
+          }
+        ts_mark(dbg && lane == 0 && ta < 16, 96 + ta);
         issue_acc(ta);
       }
       tc::mma_commit_w(acc_done);
     }
-    item = np;
     __syncwarp();
     if (warp == kAccWarp) {  // the linear part and all_done: same issuing thread as acc
     if (has_lin) {
-      const uint32_t sh = wait_item();
+      const int item = 2 * np;
+      const uint32_t sh = wait_item(item);
       // dK^phi^T raw = dH_agg V^T (M = D over a, N = 64 keys, K = D over b): needs only dH_agg
       // and V_j, so it runs while the compute warps still write the phi(K_j) tile
 #pragma unroll
@@ -242,7 +287,6 @@ __global__ void __launch_bounds__(kColsThreads, 1)
                        (np > 0 || kk > 0) ? 1u : 0u);
       tc::mma_commit_w(ring_empty + (item % RS));
       __syncwarp();
-      ++item;
     }
     if (lane == 0) tc::mma_commit(all_done);
     __syncwarp();
@@ -303,9 +347,9 @@ __global__ void __launch_bounds__(kColsThreads, 1)
         }
       }
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 128 + t);
-      if (t >= 2) tc::mbar_wait(pd_empty + (t & 1), ((t - 2) >> 1) & 1);
+      if (t >= PDN) tc::mbar_wait(pd_empty + (t % PDN), ((t - PDN) / PDN) & 1);
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 144 + t);
-      const uint32_t prow = tc::smem_u32(sPD) + (t & 1) * 32768;
+      const uint32_t prow = tc::smem_u32(sPD) + (t % PDN) * 32768;
 #pragma unroll
       for (int ch = 0; ch < 4; ++ch) {
         tc::sts_u4(prow + tc::sw128_off(rq, 4 * grp + ch), make_uint4(pp[4 * ch], pp[4 * ch + 1], pp[4 * ch + 2], pp[4 * ch + 3]));
@@ -314,7 +358,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
       tc::fence_proxy_async();
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(pd_full + (t & 1));
+      if (lane == 0) tc::mbar_arrive(pd_full + (t % PDN));
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 48 + t);
     }
     // ---- phi(K_j) rows (4 threads per key row, D/4 columns each): statistics + the bf16 tile
