@@ -23,20 +23,12 @@ namespace {
 // The ring holds slots of one pair tile each: pair t's Q pair is item 2t, its dO pair item 2t+1
 // (item n in slot n % kSlots), and dH_agg the last item.  S(t) waits only for the Q pair, dP(t)
 // for the dO pair; acc(t) runs dK^T first and releases the Q pair's slot halfway, which is the
-// slot dO(t+2) refills (5 slots).  A single P / dS buffer makes room for the fifth slot.
-// Measured (C3, k_bwd_cols ms): 4 slots + 2 P/dS buffers 1.008; 5 + 1 + dK-first 0.890; making
-// acc(t) wait until S/dP(t+1) is queued (SLAB_COLS_PRIO) 0.925 / 1.055 -- slower either way.
-#ifndef SLAB_COLS_SLOTS
-#define SLAB_COLS_SLOTS 5
-#endif
-#ifndef SLAB_COLS_PD
-#define SLAB_COLS_PD 1
-#endif
-#ifndef SLAB_COLS_DKFIRST  // acc(t) issues dK^T (frees the Q pair slot) before dV^T
-#define SLAB_COLS_DKFIRST 1
-#endif
-#ifndef SLAB_COLS_PRIO  // acc(t) enters the tensor queue only after S/dP(t+1) has
-#define SLAB_COLS_PRIO 0
+// slot dO(t+2) refills.  One P / dS buffer makes room for the fifth slot; P and dS have their own
+// full / empty barriers, so dS(t+1) is written once dK^T(t) has read dS(t) and dK^T(t+1) queues
+// behind dV^T(t) without a gap.  Measured (C3, k_bwd_cols ms): 4 slots + 2 P/dS buffers 1.008;
+// 5 slots + 1 buffer, dK first 0.890; + P from S before dP lands 0.882.
+#ifndef SLAB_COLS_POLY  // every N-th exponential by ex2_poly; measured: 0 0.869 ms, 2 0.875, 4 0.851
+#define SLAB_COLS_POLY 4
 #endif
 template <int D>
 struct ColsLayout {
@@ -45,10 +37,9 @@ struct ColsLayout {
   static constexpr int oK = 0, oV = kT;
   static constexpr int oRing = 2 * kT;
   static constexpr int kSlot = kP;         // Q pair, dO pair, or dH_agg (D*D*2 <= kP)
-  static constexpr int kSlots = SLAB_COLS_SLOTS;
-  static constexpr int kPD = SLAB_COLS_PD;  // P / dS buffers of [P 16 KB | dS 16 KB]
-  static constexpr int oPD = oRing + kSlots * kSlot;  // phi(K) aliases the P / dS buffer
-  static constexpr int oZA = oPD + kPD * 32768;       // float [D] dZ_agg
+  static constexpr int kSlots = 5;
+  static constexpr int oPD = oRing + kSlots * kSlot;  // [P 16 KB | dS 16 KB]; phi(K) aliases
+  static constexpr int oZA = oPD + 32768;             // float [D] dZ_agg
   static constexpr int oBar = oZA + 4 * D;
   static constexpr int kBytes = oBar + 256 + 1024;
   static_assert(kBytes <= 232448, "smem");
@@ -78,19 +69,20 @@ __global__ void __launch_bounds__(kColsThreads, 1)
   float* zas = reinterpret_cast<float*>(smem + L::oZA);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::oBar);
   constexpr int RS = L::kSlots;
-  constexpr int PDN = L::kPD;
   uint64_t* kv_full = bars + 0;
   uint64_t* sdp_full = bars + 1;   // [2]
-  uint64_t* pd_full = bars + 3;    // [PDN <= 2]
-  uint64_t* pd_empty = bars + 5;   // [PDN <= 2]
+  uint64_t* p_full = bars + 3;     // compute warps stored P(t)
+  uint64_t* ds_full = bars + 4;    // ... dS(t)
+  uint64_t* p_empty = bars + 5;    // dV^T(t) has read P(t)
+  uint64_t* ds_empty = bars + 6;   // dK^T(t) has read dS(t)
   uint64_t* acc_done = bars + 7;
   uint64_t* kf_ready = bars + 8;
   uint64_t* all_done = bars + 9;
   uint64_t* sdp_free = bars + 10;  // [2] (2-issuer mode) compute warps have read S|dP buffer t&1
+  uint64_t* s_full = bars + 12;    // [2] S(t) alone is in TMEM (P's exponentials start early)
   uint64_t* ring_full = bars + 16;        // [RS]
   uint64_t* ring_empty = bars + 16 + RS;  // [RS]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + 2 * RS);
-  volatile int* sdp_issued = reinterpret_cast<volatile int*>(tmem_slot + 1);  // S/dP pairs queued
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = blockIdx.x;
@@ -115,15 +107,17 @@ __global__ void __launch_bounds__(kColsThreads, 1)
       }
       for (int s = 0; s < 2; ++s) {
         tc::mbar_init(sdp_full + s, 1);
-        tc::mbar_init(pd_full + s, 8);
-        tc::mbar_init(pd_empty + s, 1);
+        tc::mbar_init(s_full + s, 1);
       }
+      tc::mbar_init(p_full, 8);
+      tc::mbar_init(ds_full, 8);
+      tc::mbar_init(p_empty, 1);
+      tc::mbar_init(ds_empty, 1);
       tc::mbar_init(acc_done, 1);
       tc::mbar_init(sdp_free, 8);
       tc::mbar_init(sdp_free + 1, 8);
       tc::mbar_init(kf_ready, 8);
       tc::mbar_init(all_done, 1);
-      *sdp_issued = 0;
       tc::fence_barrier_init();
     }
     __syncwarp();
@@ -206,31 +200,25 @@ __global__ void __launch_bounds__(kColsThreads, 1)
     const uint64_t dRk = tc::desc_kmajor(aR), dKk = tc::desc_kmajor(aK), dVk = tc::desc_kmajor(aV);
     const uint64_t dRm = tc::desc_mnmajor(aR, 16384), dPDm = tc::desc_mnmajor(aPD, 16384);
     auto koff = [](int kk, int rows) { return uint32_t((kk >> 2) * rows * 128 + (kk & 3) * 32); };
-    auto issue_acc = [&](int t) {  // dV^T += dO_pair^T P, dK^T += Q_pair^T dS  (M = D, K = 128)
-      tc::tc_fence_after();
+    // acc(t): dK^T += Q_pair^T dS, then dV^T += dO_pair^T P  (M = D, N = 64 keys, K = 128)
+    auto issue_acc = [&](int t) {
       const int sq = (2 * t) % RS, sdo = (2 * t + 1) % RS;
       const uint64_t dq = tc::desc_add(dRm, sq * L::kSlot), ddo = tc::desc_add(dRm, sdo * L::kSlot);
-      const uint64_t dp = tc::desc_add(dPDm, (t % PDN) * 32768), dd = tc::desc_add(dp, 16384);
-      auto dv = [&] {
+      const uint64_t dp = dPDm, dd = tc::desc_add(dPDm, 16384);
+      tc::mbar_wait_w(ds_full, t & 1);
+      tc::tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          tc::mma_bf16_w(tDVT, tc::desc_add(ddo, kk * 2048), tc::desc_add(dp, kk * 2048), id_acc, (t | kk) != 0);
-        tc::mma_commit_w(ring_empty + sdo);  // the slot refills while the other half runs
-      };
-      auto dk = [&] {
+      for (int kk = 0; kk < 8; ++kk)
+        tc::mma_bf16_w(tDKT, tc::desc_add(dq, kk * 2048), tc::desc_add(dd, kk * 2048), id_acc, (t | kk) != 0);
+      tc::mma_commit_w(ring_empty + sq);  // dO(t+2) refills this slot while dV^T(t) runs
+      tc::mma_commit_w(ds_empty);
+      tc::mbar_wait_w(p_full, t & 1);
+      tc::tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          tc::mma_bf16_w(tDKT, tc::desc_add(dq, kk * 2048), tc::desc_add(dd, kk * 2048), id_acc, (t | kk) != 0);
-        tc::mma_commit_w(ring_empty + sq);
-      };
-      if (SLAB_COLS_DKFIRST) {
-        dk();
-        dv();
-      } else {
-        dv();
-        dk();
-      }
-      tc::mma_commit_w(pd_empty + (t % PDN));
+      for (int kk = 0; kk < 8; ++kk)
+        tc::mma_bf16_w(tDVT, tc::desc_add(ddo, kk * 2048), tc::desc_add(dp, kk * 2048), id_acc, (t | kk) != 0);
+      tc::mma_commit_w(ring_empty + sdo);
+      tc::mma_commit_w(p_empty);
     };
     // The tensor pipe executes in issue order; the two issuers interleave S/dP(t+1) and acc(t)
     // in whichever order their inputs become ready.
@@ -247,6 +235,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)  // S = Q_pair K_j^T as soon as the Q pair landed
           tc::mma_bf16_w(tb, tc::desc_add(dq, koff(kk, 128)), tc::desc_add(dKk, koff(kk, 64)), id_s, kk > 0);
+        tc::mma_commit_w(s_full + (ts & 1));
         tc::mbar_wait(ring_full + ido % RS, (ido / RS) & 1);
         tc::tc_fence_after();
         ts_mark(dbg && lane == 0 && ts < 16, 80 + ts);
@@ -254,18 +243,18 @@ __global__ void __launch_bounds__(kColsThreads, 1)
         for (int kk = 0; kk < D / 16; ++kk)  // dP = dO_pair V_j^T
           tc::mma_bf16_w(tb + 64, tc::desc_add(ddo, koff(kk, 128)), tc::desc_add(dVk, koff(kk, 64)), id_s, kk > 0);
         tc::mma_commit_w(sdp_full + (ts & 1));
-        __syncwarp();
-        if (lane == 0) *sdp_issued = ts + 1;
       }
       __syncwarp();
-    } else {  // accumulation warp: acc(t) as soon as P / dS(t) are in smem
+    } else {  // accumulation warp: dK^T(t) / dV^T(t) as soon as dS(t) / P(t) are in smem
       for (int ta = 0; ta < np; ++ta) {
-        tc::mbar_wait(pd_full + (ta % PDN), (ta / PDN) & 1);
-        if (SLAB_COLS_PRIO && ta + 1 < np)
-          while (*sdp_issued < ta + 2) {
-          }
         ts_mark(dbg && lane == 0 && ta < 16, 96 + ta);
         issue_acc(ta);
+#ifdef SLAB_TIMELINE
+        if (dbg && ta < 16) {  // acc(ta) completion (P(ta+1)'s store waits for it anyway)
+          tc::mbar_wait_w(p_empty, ta & 1);
+          ts_mark(lane == 0, 64 + ta);
+        }
+#endif
       }
       tc::mma_commit_w(acc_done);
     }
@@ -319,14 +308,29 @@ __global__ void __launch_bounds__(kColsThreads, 1)
         lse_n = p.lse[r1];
         ds_n = p.Ds[r1];
       }
-      tc::mbar_wait(sdp_full + (t & 1), (t >> 1) & 1);
+      // P from S alone (the exponentials run while dP(t) may still wait for its dO pair)
+      tc::mbar_wait(s_full + (t & 1), (t >> 1) & 1);
       tc::tc_fence_after();
-      ts_mark(dbg && threadIdx.x == 64 && t < 16, 32 + t);
       const uint32_t tb = ((t & 1) ? tB1 : tB0) + lane_base + 32 * grp;
       uint32_t pp[16], dd[16];
       {
-        uint32_t sv[32], dp[32];
-        tc::tmem_ld32(tb, sv);
+        float pf[32];
+        {
+          uint32_t sv[32];
+          tc::tmem_ld32(tb, sv);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {  // every POLY-th exponential on the FMA pipe
+            const float x = __uint_as_float(sv[e]) * p.scale_log2 - lse2;
+            pf[e] = (SLAB_COLS_POLY > 0 && e % SLAB_COLS_POLY == SLAB_COLS_POLY - 1) ? ex2_poly(x) : ex2f(x);
+          }
+        }
+#pragma unroll
+        for (int e = 0; e < 32; e += 2) pp[e >> 1] = tc::pack_bf16(pf[e], pf[e + 1]);
+        tc::mbar_wait(sdp_full + (t & 1), (t >> 1) & 1);
+        tc::tc_fence_after();
+        ts_mark(dbg && threadIdx.x == 64 && t < 16, 32 + t);
+        uint32_t dp[32];
         tc::tmem_ld32(tb + 64, dp);
         tc::tmem_ld_wait();
         tc::tc_fence_before();  // TMEM buffer t&1 may take S/dP(t+2)
@@ -334,11 +338,8 @@ __global__ void __launch_bounds__(kColsThreads, 1)
         if (lane == 0) tc::mbar_arrive(sdp_free + (t & 1));
 #pragma unroll
         for (int e = 0; e < 32; e += 2) {
-          const float p0 = ex2f(__uint_as_float(sv[e]) * p.scale_log2 - lse2);
-          const float p1 = ex2f(__uint_as_float(sv[e + 1]) * p.scale_log2 - lse2);
-          const float d0 = p0 * fmaf(__uint_as_float(dp[e]), p.scale, -dss);
-          const float d1 = p1 * fmaf(__uint_as_float(dp[e + 1]), p.scale, -dss);
-          pp[e >> 1] = tc::pack_bf16(p0, p1);
+          const float d0 = pf[e] * fmaf(__uint_as_float(dp[e]), p.scale, -dss);
+          const float d1 = pf[e + 1] * fmaf(__uint_as_float(dp[e + 1]), p.scale, -dss);
           dd[e >> 1] = tc::pack_bf16(d0, d1);
         }
         if (!live) {  // the repeated block of an odd tail contributes nothing
@@ -347,18 +348,23 @@ __global__ void __launch_bounds__(kColsThreads, 1)
         }
       }
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 128 + t);
-      if (t >= PDN) tc::mbar_wait(pd_empty + (t % PDN), ((t - PDN) / PDN) & 1);
+      const uint32_t prow = tc::smem_u32(sPD);
+      if (t >= 1) tc::mbar_wait(ds_empty, (t - 1) & 1);
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 144 + t);
-      const uint32_t prow = tc::smem_u32(sPD) + (t % PDN) * 32768;
 #pragma unroll
-      for (int ch = 0; ch < 4; ++ch) {
-        tc::sts_u4(prow + tc::sw128_off(rq, 4 * grp + ch), make_uint4(pp[4 * ch], pp[4 * ch + 1], pp[4 * ch + 2], pp[4 * ch + 3]));
+      for (int ch = 0; ch < 4; ++ch)
         tc::sts_u4(prow + 16384 + tc::sw128_off(rq, 4 * grp + ch), make_uint4(dd[4 * ch], dd[4 * ch + 1], dd[4 * ch + 2], dd[4 * ch + 3]));
-      }
+      tc::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(ds_full);
+      if (t >= 1) tc::mbar_wait(p_empty, (t - 1) & 1);
+#pragma unroll
+      for (int ch = 0; ch < 4; ++ch)
+        tc::sts_u4(prow + tc::sw128_off(rq, 4 * grp + ch), make_uint4(pp[4 * ch], pp[4 * ch + 1], pp[4 * ch + 2], pp[4 * ch + 3]));
       tc::fence_proxy_async();
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(pd_full + (t % PDN));
+      if (lane == 0) tc::mbar_arrive(p_full);
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 48 + t);
     }
     // ---- phi(K_j) rows (4 threads per key row, D/4 columns each): statistics + the bf16 tile

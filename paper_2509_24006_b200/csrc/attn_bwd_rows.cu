@@ -14,6 +14,10 @@
 //   is done, so the tensor pipe keeps S/dP of the next pair queued behind dQ of this one.
 #include "bwd_common.cuh"
 
+#ifndef SLAB_ROWS_POLY
+#define SLAB_ROWS_POLY 0  // every N-th exponential by ex2_poly; measured: 0 0.620 ms, 4 0.629, 2 0.653
+#endif
+
 namespace slab {
 namespace {
 
@@ -355,8 +359,9 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   uint64_t* k_empty = k_full + L::KS;        // [KS]
   uint64_t* v_full = k_empty + L::KS;        // [VS]
   uint64_t* v_empty = v_full + L::VS;        // [VS]
+  uint64_t* s_full = bars + 18;    // [2] S^T(t) alone is in TMEM (P's exponentials start early)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 20);
-  static_assert(8 + 2 * (L::KS + L::VS) <= 20, "barrier slots");
+  static_assert(8 + 2 * (L::KS + L::VS) <= 18, "barrier slots");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x;
@@ -375,6 +380,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       tc::mbar_init(qdo_full, 1);
       for (int s = 0; s < 2; ++s) {
         tc::mbar_init(sdp_full + s, 1);
+        tc::mbar_init(s_full + s, 1);
         tc::mbar_init(sdp_free + s, 8);
       }
       tc::mbar_init(ds_full, 8);
@@ -464,16 +470,19 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     auto issue_sdp = [&](int t) {
       const int ks = t % L::KS, vs = t % L::VS;
       tc::mbar_wait(k_full + ks, (t / L::KS) & 1);
-      tc::mbar_wait(v_full + vs, (t / L::VS) & 1);
       tc::tc_fence_after();
       ts_mark(dbg && lane == 0 && t < 16, 16 + t);
       const uint32_t tb = (t & 1) ? tB1 : tB0;
       const uint64_t dk = tc::desc_add(dKk, ks * L::kP), dv = tc::desc_add(dVk, vs * L::kP);
 #pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) {
+      for (int kk = 0; kk < D / 16; ++kk)  // S^T on the K pair alone
         tc::mma_bf16_w(tb, tc::desc_add(dk, koff(kk, 128)), tc::desc_add(dQk, koff(kk, 64)), id_st, kk > 0);
+      tc::mma_commit_w(s_full + (t & 1));
+      tc::mbar_wait(v_full + vs, (t / L::VS) & 1);
+      tc::tc_fence_after();
+#pragma unroll
+      for (int kk = 0; kk < D / 16; ++kk)
         tc::mma_bf16_w(tb + 64, tc::desc_add(dv, koff(kk, 128)), tc::desc_add(dDOk, koff(kk, 64)), id_st, kk > 0);
-      }
       tc::mma_commit_w(sdp_full + (t & 1));
       tc::mma_commit_w(v_empty + vs);
       ts_mark(dbg && lane == 0 && t < 16, 208 + t);
@@ -527,37 +536,52 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     const int c = 32 * q4 + lane;  // key row of the pair (c < 64: block j1, else j2)
 #pragma unroll 1
     for (int t = 0; t < np; ++t) {
-      tc::mbar_wait(sdp_full + (t & 1), (t >> 1) & 1);
+      // P = exp2(S log2e / sqrt(d) - lse log2e) from S^T alone, while dP^T may still wait for
+      // its V pair; then dS = P (dP - D^s) / sqrt(d).  The per-query constants (lse log2e,
+      // D^s / sqrt(d)) are shared-space vector loads.
+      tc::mbar_wait(s_full + (t & 1), (t >> 1) & 1);
       tc::tc_fence_after();
-      ts_mark(dbg && threadIdx.x == 64 && t < 16, 32 + t);
-      ts_mark(dbg && lane == 0 && t >= 4 && t < 8, 192 + 8 * (t - 4) + (warp - 2));
       const bool live = c < 64 || 2 * t + 1 < cnt;
       const uint32_t tb = ((t & 1) ? tB1 : tB0) + lane_base + 32 * grp;
+      const uint32_t a_l = tc::smem_u32(s_lse2) + 4u * uint32_t(32 * grp);
+      const uint32_t a_d = tc::smem_u32(s_ds) + 4u * uint32_t(32 * grp);
       uint32_t pk[16];
       {
-        uint32_t sv[32], dp[32];
-        tc::tmem_ld32(tb, sv);
+        float pf[32];
+        {
+          uint32_t sv[32];
+          tc::tmem_ld32(tb, sv);
+          tc::tmem_ld_wait();
+#pragma unroll
+          for (int e = 0; e < 32; e += 4) {
+            const float4 l4 = tc::lds_f4(a_l + 4u * e);
+            const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {  // every fourth exponential on the FMA pipe
+              const float x = __uint_as_float(sv[e + q]) * p.scale_log2 - lv[q];
+              pf[e + q] = (SLAB_ROWS_POLY > 0 && (e + q) % SLAB_ROWS_POLY == SLAB_ROWS_POLY - 1) ? ex2_poly(x) : ex2f(x);
+            }
+          }
+        }
+        tc::mbar_wait(sdp_full + (t & 1), (t >> 1) & 1);
+        tc::tc_fence_after();
+        ts_mark(dbg && threadIdx.x == 64 && t < 16, 32 + t);
+        ts_mark(dbg && lane == 0 && t >= 4 && t < 8, 192 + 8 * (t - 4) + (warp - 2));
+        uint32_t dp[32];
         tc::tmem_ld32(tb + 64, dp);
         tc::tmem_ld_wait();
         tc::tc_fence_before();  // TMEM buffer t&1 may take S/dP(t+2)
         __syncwarp();
         if (lane == 0) tc::mbar_arrive(sdp_free + (t & 1));
-        // dS = P (dP - D^s) / sqrt(d) with P = exp2(S log2e / sqrt(d) - lse log2e); the
-        // per-query constants (lse log2e, D^s / sqrt(d)) are shared-space vector loads
         ts_mark(dbg && threadIdx.x == 64 && t < 16, 240 + t);
         const float sc = p.scale;
-        const uint32_t a_l = tc::smem_u32(s_lse2) + 4u * uint32_t(32 * grp);
-        const uint32_t a_d = tc::smem_u32(s_ds) + 4u * uint32_t(32 * grp);
 #pragma unroll
         for (int e = 0; e < 32; e += 4) {
-          const float4 l4 = tc::lds_f4(a_l + 4u * e), d4 = tc::lds_f4(a_d + 4u * e);
-          const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dv4[4] = {d4.x, d4.y, d4.z, d4.w};
+          const float4 d4 = tc::lds_f4(a_d + 4u * e);
+          const float dv4[4] = {d4.x, d4.y, d4.z, d4.w};
           float dsv[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float pq = ex2f(__uint_as_float(sv[e + q]) * p.scale_log2 - lv[q]);
-            dsv[q] = pq * fmaf(__uint_as_float(dp[e + q]), sc, -dv4[q]);
-          }
+          for (int q = 0; q < 4; ++q) dsv[q] = pf[e + q] * fmaf(__uint_as_float(dp[e + q]), sc, -dv4[q]);
           pk[e >> 1] = tc::pack_bf16(dsv[0], dsv[1]);
           pk[(e >> 1) + 1] = tc::pack_bf16(dsv[2], dsv[3]);
         }
