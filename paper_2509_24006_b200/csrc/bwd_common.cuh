@@ -62,6 +62,8 @@ __device__ __forceinline__ float ex2_poly(float x) {
   p = fmaf(f, p, 1.f);
   return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
 }
+// element e of an unrolled exponential loop goes to ex2_poly when every n-th (n = 0: never)
+__host__ __device__ constexpr bool poly_slot(int e, int n) { return n > 0 && e % n == n - 1; }
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
