@@ -93,11 +93,14 @@ __global__ void __launch_bounds__(32) k_pool2_bf16(const __nv_bfloat16* __restri
 // (mask.cpp:105-113) -- and the label / lookup writes (mask.cpp:114-153).
 // ---------------------------------------------------------------------------------------
 // K1b: pooled scores S = pool(Q) pool(K)^T * (1/sqrt(d)) for all block pairs, tiled 64x64
-// per CTA (each thread a 4x4 patch).  Every element is still ONE sequential ascending-c dot
+// per CTA (each thread a 4x4 patch, strided by 16 rows / columns).  Every element is still ONE sequential ascending-c dot
 // with separately rounded mul and add (mat.hpp:83-97), so the values are bit-identical to
 // the reference's; tiling only shares the pooled rows through shared memory.
+#ifndef SLAB_SCORES_REGS
+#define SLAB_SCORES_REGS 96  // 64 spills; 80-128 all 0.083 ms (was 0.116 with the 4-way-conflicted tiling)
+#endif
 template <typename R>
-__global__ void __launch_bounds__(256) k_scores(const R* __restrict__ pq, const R* __restrict__ pk,
+__global__ void __maxnreg__(SLAB_SCORES_REGS) k_scores(const R* __restrict__ pq, const R* __restrict__ pk,
                                                 int d, int Tm, int Tn, R inv_sqrt_d,
                                                 R* __restrict__ s) {
   constexpr int CK = 32;
@@ -123,11 +126,13 @@ __global__ void __launch_bounds__(256) k_scores(const R* __restrict__ pq, const 
     }
     __syncthreads();
     for (int c = 0; c < ck; ++c) {
+      // rows ty + 16a / columns tx + 16b: with the 33-element row pitch the 16 column reads of a
+      // warp hit 16 distinct 8-byte bank pairs (rows 4 apart collided 4-way)
       R av[4], bv[4];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) av[a] = sa[ty * 4 + a][c];
+      for (int a = 0; a < 4; ++a) av[a] = sa[ty + 16 * a][c];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) bv[b] = sb[tx * 4 + b][c];
+      for (int b = 0; b < 4; ++b) bv[b] = sb[tx + 16 * b][c];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -136,11 +141,11 @@ __global__ void __launch_bounds__(256) k_scores(const R* __restrict__ pq, const 
   }
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
-    const int i = i0 + ty * 4 + a;
+    const int i = i0 + ty + 16 * a;
     if (i >= Tm) continue;
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int j = j0 + tx * 4 + b;
+      const int j = j0 + tx + 16 * b;
       if (j < Tn) s[(u * Tm + i) * (long long)Tn + j] = mul_rn(acc[a][b], inv_sqrt_d);
     }
   }
