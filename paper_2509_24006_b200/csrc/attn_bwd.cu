@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
 #pragma unroll
           for (int e = 0; e < 32; ++e) {  // every POLY-th exponential on the FMA pipe
             const float x = __uint_as_float(sv[e]) * p.scale_log2 - lse2;
-            pf[e] = poly_slot(e, SLAB_COLS_POLY) ? ex2_poly(x) : ex2f(x);
+            pf[e] = tc::poly_slot(e, SLAB_COLS_POLY) ? tc::ex2_poly(x) : ex2f(x);
           }
         }
 #pragma unroll

@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
 #pragma unroll
             for (int q = 0; q < 4; ++q) {  // every fourth exponential on the FMA pipe
               const float x = __uint_as_float(sv[e + q]) * p.scale_log2 - lv[q];
-              pf[e + q] = poly_slot(e + q, SLAB_ROWS_POLY) ? ex2_poly(x) : ex2f(x);
+              pf[e + q] = tc::poly_slot(e + q, SLAB_ROWS_POLY) ? tc::ex2_poly(x) : ex2f(x);
             }
           }
         }

@@ -16,6 +16,10 @@
 #include "kernels.hpp"
 #include "tc.cuh"
 
+#ifndef SLAB_FWD_POLY
+#define SLAB_FWD_POLY 0  // every N-th exponential by tc::ex2_poly; measured: 0 best, 4 +0.003 ms, 2 +0.027
+#endif
+
 namespace slab {
 
 static __device__ long long g_fwd_ts[128];  // -DSLAB_TIMELINE: timeline of one CTA
@@ -414,8 +418,9 @@ __global__ void __launch_bounds__(192, 2)
       uint32_t pk[16];
 #pragma unroll
       for (int e = 0; e < 32; e += 2) {
-        const float p0 = ex2(__uint_as_float(sa[e]) * sc - m_used);
-        const float p1 = ex2(__uint_as_float(sa[e + 1]) * sc - m_used);
+        const float x0 = __uint_as_float(sa[e]) * sc - m_used, x1 = __uint_as_float(sa[e + 1]) * sc - m_used;
+        const float p0 = tc::poly_slot(e, SLAB_FWD_POLY) ? tc::ex2_poly(x0) : ex2(x0);
+        const float p1 = tc::poly_slot(e + 1, SLAB_FWD_POLY) ? tc::ex2_poly(x1) : ex2(x1);
         ps += p0 + p1;
         pk[e >> 1] = tc::pack_bf16(p0, p1);
       }

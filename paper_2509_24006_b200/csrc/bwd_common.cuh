@@ -48,22 +48,6 @@ __device__ __forceinline__ float ex2f(float x) {
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-// 2^x on the FMA pipe: Cody-Waite split x = j + f (floor by a round-down add of 1.5 * 2^23),
-// 2^f by a degree-3 fit on [0, 1) with p(0) = 1 (max rel. error 8.6e-5, far below the bf16
-// rounding every consumer applies), 2^j added into the exponent field.  Exponential-heavy
-// loops run part of their exponentials here so the MUFU pipe (4 lanes / clk / SMSP) stops
-// being the bottleneck; x >= -126 keeps the result normal (smaller x gives ~2^-126, i.e. 0).
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -126.f);
-  const float t = __fadd_rd(x, 12582912.f);
-  const float f = x - (t - 12582912.f);
-  float p = fmaf(f, 0.07706641f, 0.2276457f);
-  p = fmaf(f, p, 0.69511662f);
-  p = fmaf(f, p, 1.f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
-}
-// element e of an unrolled exponential loop goes to ex2_poly when every n-th (n = 0: never)
-__host__ __device__ constexpr bool poly_slot(int e, int n) { return n > 0 && e % n == n - 1; }
 __device__ __forceinline__ void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
