@@ -99,6 +99,49 @@ typedef struct sla_b200_info {
   int64_t gpu_launches;      /* kernels launched by the last call on this thread        */
 } sla_b200_info;
 
+/* flops_report (flops.cpp:7-33) of one (batch, head) unit, computed from the device LUT. */
+typedef struct sla_b200_flops {
+  uint64_t full_flops;   /* 4 N^2 d                                              */
+  uint64_t sparse_flops; /* 4 b_q b_kv d x critical blocks                       */
+  uint64_t linear_flops; /* 2 d^2 per row of a block row with a marginal block, + N d */
+  uint64_t proj_flops;   /* 2 N d^2                                              */
+  uint64_t mask_flops;   /* 2 N d + 2 T_m T_n d                                  */
+  uint64_t sla_total;    /* sparse + linear + proj + mask                        */
+  double ratio;          /* sla_total / full_flops                               */
+  double sparsity;       /* 1 - critical block fraction                          */
+} sla_b200_flops;
+
+/* ExecCounters (forward.hpp:46-50) of a forward, summed over units, as the reference's
+ * sla_forward_with_mask counts them for the given aggregation strategy. */
+typedef struct sla_b200_exec_counters {
+  uint64_t sparse_block_matmuls;   /* 2 per critical block (score + weight-value)        */
+  uint64_t linear_row_products;    /* rows with a marginal block and phi(q) . Z_i != 0    */
+  uint64_t additions;              /* AggCounters (aggregation.hpp:14-19)                 */
+  uint64_t subtractions;
+  uint64_t lookups;
+  uint64_t table_build_additions;
+} sla_b200_counters;
+
+/* Aggregation strategies of the counting (config.hpp:19-31).  The device always computes
+ * H = M0 h as one tensor-core GEMM -- arithmetic-equivalent to every strategy -- so the strategy
+ * only selects which of the reference's counts are reported. */
+#define SLA_B200_AGG_DIRECT 0
+#define SLA_B200_AGG_COMPLEMENT 1
+#define SLA_B200_AGG_FOUR_RUSSIANS 2
+#define SLA_B200_AGG_AUTO 3 /* resolve_strategy with thresholds 0.25 / 0.75, per unit */
+
+/* flops_report of every unit (per_unit: [B*H]) from the LUT in `state` (after
+ * sla_b200_classify or sla_b200_forward).  Synchronises `stream`.  Ragged N counts the N
+ * valid rows (full / proj / mask flops, and the valid rows of each covered block row). */
+int sla_b200_flops_report(const sla_b200_problem* p, const void* state, sla_b200_flops* per_unit,
+                          void* workspace, void* stream);
+
+/* ExecCounters of the forward that filled `state` (q: that forward's Q, for the linear-row
+ * denominators; group_size: the Four-Russians g, 1..20).  Synchronises `stream`. */
+int sla_b200_exec_counters(const sla_b200_problem* p, const void* q, const void* state,
+                           int aggregation, int group_size, sla_b200_counters* out,
+                           void* workspace, void* stream);
+
 /* Thread-local message of the last non-OK status; carries the reference's fragments. */
 const char* sla_b200_last_error(void);
 int sla_b200_abi_version(void);

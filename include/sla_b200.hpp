@@ -151,6 +151,20 @@ struct Forward {
                                   nullptr, o_s.p, o_l.p, static_cast<float*>(lse.p), state.p, work.p, nullptr));
     cuda_check(cudaDeviceSynchronize());
   }
+  // ExecCounters of this forward as the reference counts them for cfg's strategy, added to c
+  // (forward.cpp:152-161), from the device LUT (sla_b200_exec_counters)
+  void count(const SlaConfig& cfg, ExecCounters* c) const {
+    if (!c) return;
+    sla_b200_counters e{};
+    throw_status(sla_b200_exec_counters(&p, q.p, state.p, static_cast<int>(cfg.aggregation),
+                                        static_cast<int>(cfg.group_size), &e, work.p, nullptr));
+    c->sparse_block_matmuls += e.sparse_block_matmuls;
+    c->linear_row_products += e.linear_row_products;
+    c->aggregation.additions += e.additions;
+    c->aggregation.subtractions += e.subtractions;
+    c->aggregation.lookups += e.lookups;
+    c->aggregation.table_build_additions += e.table_build_additions;
+  }
   SlaForwardState<float> state_of() const {
     SlaForwardState<float> st;
     const size_t n = size_t(p.n), d = size_t(p.d);
@@ -173,10 +187,11 @@ struct Forward {
 // forward.cpp:174-185 -- the mask is re-predicted from the live q, k.
 inline SlaForwardState<float> sla_forward(const Mat<float>& q, const Mat<float>& k, const Mat<float>& v,
                                           const SlaConfig& cfg, const BlockLayout& layout, unsigned = 1,
-                                          ExecCounters* = nullptr) {
+                                          ExecCounters* counters = nullptr) {
   validate_config(cfg);
   detail::Forward f(detail::problem(cfg, layout), q, k, v);
   f.run(nullptr);
+  f.count(cfg, counters);
   return f.state_of();
 }
 
@@ -184,11 +199,12 @@ inline SlaForwardState<float> sla_forward(const Mat<float>& q, const Mat<float>&
 inline SlaForwardState<float> sla_forward_with_mask(const Mat<float>& q, const Mat<float>& k,
                                                     const Mat<float>& v, const CompressedMask& mask,
                                                     const SlaConfig& cfg, const BlockLayout& layout,
-                                                    unsigned = 1, ExecCounters* = nullptr) {
+                                                    unsigned = 1, ExecCounters* counters = nullptr) {
   if (mask.t_m != layout.t_m || mask.t_n != layout.t_n)
     throw std::invalid_argument("sla_forward: mask does not match layout");
   detail::Forward f(detail::problem(cfg, layout), q, k, v);
   f.run(mask.labels.data());
+  f.count(cfg, counters);
   return f.state_of();
 }
 

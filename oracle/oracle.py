@@ -307,6 +307,61 @@ def flops(n, d, b_q, b_kv, labels):
     return dict(zip(["full", "sparse", "linear", "proj", "mask", "total"], [int(x) for x in out]))
 
 
+AGG = {"direct": 0, "complement": 1, "four_russians": 2, "auto": 3}
+
+
+def resolve_strategy(kind, marginal_fraction, direct_max=0.25, complement_min=0.75):
+    """aggregation.cpp:147-156 with the config.hpp:30-31 default thresholds."""
+    if kind != AGG["auto"]:
+        return kind
+    if marginal_fraction <= direct_max:
+        return AGG["direct"]
+    if marginal_fraction >= complement_min:
+        return AGG["complement"]
+    return AGG["four_russians"]
+
+
+def exec_counters(q, k, labels, b_q, b_kv, phi_kind="elu1", aggregation="direct", group_size=4):
+    """ExecCounters of sla_forward_with_mask (forward.hpp:46-50) restated from the label grid:
+    2 block matmuls per critical block (forward.cpp:46, 123-124); one linear row product per
+    row of a block row with a marginal block whose den = phi(q) . Z_i is non-zero
+    (forward.cpp:130-146; phi >= 0 and z >= 0, so den == 0 iff every product is 0); the
+    aggregation counts of the resolved strategy: direct = marginal - 1 additions per non-empty
+    row (aggregation.cpp:40-56), complement = one subtraction per excluded block
+    (aggregation.cpp:58-70), Four-Russians = one lookup per group holding a marginal block and
+    lookups - 1 additions per row, plus 2^size - 1 table additions per group
+    (aggregation.cpp:72-145).  Returns [sparse, linear_rows, additions, subtractions, lookups,
+    table_build_additions]."""
+    lab = np.asarray(labels)
+    t_m, t_n = lab.shape
+    qf, kf = phi(np.asarray(q, np.float64), phi_kind), phi(np.asarray(k, np.float64), phi_kind)
+    z = kf.reshape(t_n, b_kv, -1).sum(axis=1)
+    marg = lab == 0
+    strat = resolve_strategy(AGG[aggregation] if isinstance(aggregation, str) else aggregation,
+                             marg.sum() / (t_m * t_n))
+    out = [2 * int((lab == 1).sum()), 0, 0, 0, 0, 0]
+    g = group_size
+    groups = [(b, min(b + g, t_n)) for b in range(0, t_n, g)]
+    if strat == AGG["four_russians"]:
+        out[5] = sum((1 << (e - b)) - 1 for b, e in groups)
+    for i in range(t_m):
+        m = marg[i]
+        cnt = int(m.sum())
+        if strat == AGG["direct"]:
+            out[2] += max(cnt - 1, 0)
+        elif strat == AGG["complement"]:
+            out[3] += t_n - cnt
+        else:
+            hit = sum(1 for b, e in groups if m[b:e].any())
+            out[4] += hit
+            out[2] += max(hit - 1, 0)
+        if cnt:
+            zi = z[m].sum(axis=0)
+            rows = qf[i * b_q:(i + 1) * b_q]
+            out[1] += int(((rows * zi) != 0).any(axis=1).sum())
+    return out
+
+
 def rel_diff(a, b, floor=1e-300):
     """mat.hpp:169-178 max-norm relative difference."""
     a = np.asarray(a, np.float64)
@@ -337,6 +392,9 @@ class Reference:
                 f.restype = C.c_int
             lib.ref_predict.argtypes = [_sz, _sz, _sz, _sz, _dp, _dp, _dp, C.c_char_p, _sz]
             lib.ref_classify.argtypes = [_sz, _sz, _dp, C.c_double, C.c_double, _i8, C.c_char_p, _sz]
+            lib.ref_exec_counters.argtypes = [_sz, _sz, _sz, _sz, C.c_int, C.c_int, _sz] + \
+                                             [C.c_void_p] * 5 + [C.c_char_p, _sz]
+            lib.ref_flops_report.argtypes = [_sz, _sz, _sz, _sz] + [C.c_void_p] * 3 + [C.c_char_p, _sz]
             cls._lib = lib
         return cls._lib
 
@@ -387,6 +445,31 @@ class Reference:
         if cls.lib().ref_predict(n, d, b_q, b_kv, q, k, out, err, 300):
             raise ValueError(err.value.decode())
         return out
+
+    @classmethod
+    def exec_counters(cls, q, k, v, labels, b_q, b_kv, phi_kind="elu1", aggregation="direct", group_size=4):
+        """ExecCounters of the reference's sla_forward_with_mask<float> on this label grid."""
+        q, k, v = (np.ascontiguousarray(x, np.float32) for x in (q, k, v))
+        lab = np.ascontiguousarray(labels, np.int8)
+        out = np.zeros(6, np.uint64)
+        err = C.create_string_buffer(300)
+        agg = AGG[aggregation] if isinstance(aggregation, str) else aggregation
+        rc = cls.lib().ref_exec_counters(q.shape[0], q.shape[1], b_q, b_kv, PHI[phi_kind], agg, group_size,
+                                         q.ctypes.data, k.ctypes.data, v.ctypes.data, lab.ctypes.data,
+                                         out.ctypes.data, err, 300)
+        if rc:
+            raise ValueError(err.value.decode())
+        return [int(x) for x in out]
+
+    @classmethod
+    def flops_report(cls, n, d, b_q, b_kv, labels):
+        """flops.cpp:7-33: ([full, sparse, linear, proj, mask, total], ratio, sparsity)."""
+        lab = np.ascontiguousarray(labels, np.int8)
+        u, f = np.zeros(6, np.uint64), np.zeros(2)
+        err = C.create_string_buffer(300)
+        if cls.lib().ref_flops_report(n, d, b_q, b_kv, lab.ctypes.data, u.ctypes.data, f.ctypes.data, err, 300):
+            raise ValueError(err.value.decode())
+        return [int(x) for x in u], float(f[0]), float(f[1])
 
     @classmethod
     def classify(cls, p_c, k_h, k_l):

@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "sla/backward.hpp"
+#include "sla/flops.hpp"
 #include "sla/forward.hpp"
 #include "sla/mask.hpp"
 
@@ -137,6 +138,63 @@ int ref_classify(std::size_t t_m, std::size_t t_n, const double* p_c, double kh,
     sla::CompressedWeights w{load(p_c, t_m, t_n)};
     auto m = sla::classify_mask(w, kh, kl);
     std::memcpy(labels, m.labels.data(), m.labels.size());
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    put_err(e.what(), err, errlen);
+    return 2;
+  } catch (const std::exception& e) {
+    put_err(e.what(), err, errlen);
+    return 1;
+  }
+}
+
+// forward.cpp:81-172 with ExecCounters (forward.hpp:46-50) on an injected label grid, one
+// aggregation strategy (config.hpp:19-31: 0 direct, 1 complement, 2 Four-Russians, 3 auto).
+// out: sparse_block_matmuls, linear_row_products, additions, subtractions, lookups,
+// table_build_additions.
+int ref_exec_counters(std::size_t n, std::size_t d, std::size_t bq, std::size_t bkv, int phi,
+                      int aggregation, std::size_t group_size, const float* q, const float* k,
+                      const float* v, const std::int8_t* labels, std::uint64_t* out, char* err,
+                      std::size_t errlen) {
+  try {
+    sla::SlaConfig cfg;
+    cfg.phi = static_cast<sla::FeatureMapKind>(phi);
+    cfg.dtype = sla::Dtype::f32;
+    cfg.aggregation = static_cast<sla::AggregationKind>(aggregation);
+    cfg.group_size = group_size;
+    const auto layout = sla::make_block_layout(n, d, bq, bkv);
+    auto mask = sla::build_lookup(layout.t_m, layout.t_n,
+                                  std::vector<std::int8_t>(labels, labels + layout.t_m * layout.t_n));
+    sla::ExecCounters c;
+    sla::sla_forward_with_mask(load(q, n, d), load(k, n, d), load(v, n, d), mask, cfg, layout, 1, &c);
+    const std::uint64_t r[6] = {c.sparse_block_matmuls, c.linear_row_products,
+                                c.aggregation.additions, c.aggregation.subtractions,
+                                c.aggregation.lookups, c.aggregation.table_build_additions};
+    std::memcpy(out, r, sizeof(r));
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    put_err(e.what(), err, errlen);
+    return 2;
+  } catch (const std::exception& e) {
+    put_err(e.what(), err, errlen);
+    return 1;
+  }
+}
+
+// flops.cpp:7-33.  out: full, sparse, linear, proj, mask, sla_total; out_f: ratio, sparsity.
+int ref_flops_report(std::size_t n, std::size_t d, std::size_t bq, std::size_t bkv,
+                     const std::int8_t* labels, std::uint64_t* out, double* out_f, char* err,
+                     std::size_t errlen) {
+  try {
+    const auto layout = sla::make_block_layout(n, d, bq, bkv);
+    auto mask = sla::build_lookup(layout.t_m, layout.t_n,
+                                  std::vector<std::int8_t>(labels, labels + layout.t_m * layout.t_n));
+    const auto r = sla::flops_report(layout, mask);
+    const std::uint64_t u[6] = {r.full_flops, r.sparse_flops, r.linear_flops, r.proj_flops,
+                                r.mask_flops, r.sla_total};
+    std::memcpy(out, u, sizeof(u));
+    out_f[0] = r.ratio;
+    out_f[1] = r.sparsity;
     return 0;
   } catch (const std::invalid_argument& e) {
     put_err(e.what(), err, errlen);

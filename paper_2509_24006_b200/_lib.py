@@ -33,6 +33,23 @@ class Info(C.Structure):
                 ("t_m", C.c_int32), ("t_n", C.c_int32), ("gpu_launches", C.c_int64)]
 
 
+class Flops(C.Structure):
+    """sla_b200_flops: flops_report (flops.cpp:7-33) of one unit."""
+    _fields_ = [("full_flops", C.c_uint64), ("sparse_flops", C.c_uint64), ("linear_flops", C.c_uint64),
+                ("proj_flops", C.c_uint64), ("mask_flops", C.c_uint64), ("sla_total", C.c_uint64),
+                ("ratio", C.c_double), ("sparsity", C.c_double)]
+
+
+class Counters(C.Structure):
+    """sla_b200_counters: ExecCounters (forward.hpp:46-50) with its AggCounters."""
+    _fields_ = [("sparse_block_matmuls", C.c_uint64), ("linear_row_products", C.c_uint64),
+                ("additions", C.c_uint64), ("subtractions", C.c_uint64), ("lookups", C.c_uint64),
+                ("table_build_additions", C.c_uint64)]
+
+
+AGG = {"direct": 0, "complement": 1, "four_russians": 2, "auto": 3}
+
+
 class GradParts(C.Structure):
     _fields_ = [("dq_sparse", C.c_void_p), ("dk_sparse", C.c_void_p),
                 ("dq_feat", C.c_void_p), ("dk_feat", C.c_void_p)]
@@ -44,6 +61,7 @@ EXPORTS = [
     "sla_b200_last_error", "sla_b200_abi_version", "sla_b200_validate", "sla_b200_sizes",
     "sla_b200_query", "sla_b200_last_launch_count", "sla_b200_classify", "sla_b200_forward",
     "sla_b200_backward", "sla_b200_backward_ex", "sla_b200_state_labels",
+    "sla_b200_flops_report", "sla_b200_exec_counters",
 ]
 
 
@@ -67,6 +85,8 @@ def lib():
     L.sla_b200_backward.argtypes = [P] + [vp] * 15
     L.sla_b200_backward_ex.argtypes = [P] + [vp] * 12 + [C.POINTER(GradParts)] + [vp] * 3
     L.sla_b200_state_labels.argtypes = [P, vp, C.POINTER(C.c_void_p)]
+    L.sla_b200_flops_report.argtypes = [P, vp, C.POINTER(Flops), vp, vp]
+    L.sla_b200_exec_counters.argtypes = [P, vp, vp, C.c_int, C.c_int, C.POINTER(Counters), vp, vp]
     for name in EXPORTS:
         getattr(L, name)
     _lib = L

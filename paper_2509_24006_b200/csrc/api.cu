@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdio>
 #include <string>
+#include <vector>
 
 #include "../../include/sla_b200.h"
 #include "buffers.hpp"
@@ -438,6 +439,116 @@ int sla_b200_backward(const sla_b200_problem* p, const void* q, const void* k, c
                       const void* state, void* workspace, void* stream) {
   return sla_b200_backward_ex(p, q, k, v, w, o_s, o_l, lse, d_out, dq, dk, dv, dw, nullptr,
                               state, workspace, stream);
+}
+
+// Per-row LUT statistics (critical, marginal, Four-Russians groups hit) and, when q is given,
+// per-block-row linear row products, copied to the host.  Scratch: the pooled-Q area of the
+// workspace (U * Tm * d doubles >= 20 bytes per block row), idle outside classification.
+struct RowStats {
+  std::vector<int4> rows;
+  std::vector<int> lin;
+};
+
+RowStats row_stats(const sla_b200_problem* p, const Dims& D, const void* q, const void* state,
+                   void* workspace, int g, cudaStream_t st) {
+  StateBufs s;
+  WorkBufs w;
+  buffers(p, D, state, workspace, s, w);
+  const size_t rows = size_t(D.U) * D.Tm;
+  int4* dstats = reinterpret_cast<int4*>(w.pq);
+  int* dlin = reinterpret_cast<int*>(dstats + rows);
+  launch_row_stats(D, s.labels, g, dstats, st);
+  RowStats r;
+  r.rows.resize(rows);
+  if (q) {
+    if (D.staged) {
+      pad_rows(D, w.pad[kPQ], q, size_t(D.d) * 2, st);
+      q = w.pad[kPQ];
+    }
+    launch_lin_rows(D, p->dtype, q, s.Z, use_fast(p, D), dstats, dlin, st);
+    r.lin.resize(rows);
+    SLAB_CUDA(cudaMemcpyAsync(r.lin.data(), dlin, rows * sizeof(int), cudaMemcpyDeviceToHost, st));
+  }
+  SLAB_CUDA(cudaMemcpyAsync(r.rows.data(), dstats, rows * sizeof(int4), cudaMemcpyDeviceToHost, st));
+  SLAB_CUDA(cudaStreamSynchronize(st));
+  return r;
+}
+
+int sla_b200_flops_report(const sla_b200_problem* p, const void* state, sla_b200_flops* per_unit,
+                          void* workspace, void* stream) {
+  return guarded([&] {
+    const Dims D = resolve(p);
+    require_supported(p, D);
+    if (!per_unit) throw InvalidArgument("flops_report: per_unit is required");
+    const RowStats r = row_stats(p, D, nullptr, state, workspace, 1, static_cast<cudaStream_t>(stream));
+    const uint64_t n = uint64_t(D.N_valid), d = uint64_t(D.d);
+    for (long long u = 0; u < D.U; ++u) {  // flops.cpp:10-32
+      uint64_t crit = 0, marg = 0, covered = 0;
+      for (int i = 0; i < D.Tm; ++i) {
+        const int4 x = r.rows[size_t(u) * D.Tm + i];
+        crit += uint64_t(x.x);
+        marg += uint64_t(x.y);
+        if (x.y > 0) covered += uint64_t(std::min<long long>(D.bq, D.N_valid - (long long)i * D.bq));
+      }
+      sla_b200_flops& f = per_unit[u];
+      f.full_flops = 4 * n * n * d;
+      f.sparse_flops = 4 * uint64_t(D.bq) * uint64_t(D.bkv) * d * crit;
+      f.linear_flops = 2 * covered * d * d + (marg > 0 ? n * d : 0);
+      f.proj_flops = 2 * n * d * d;
+      f.mask_flops = 2 * n * d + 2 * uint64_t(D.Tm) * uint64_t(D.Tn) * d;
+      f.sla_total = f.sparse_flops + f.linear_flops + f.proj_flops + f.mask_flops;
+      f.ratio = double(f.sla_total) / double(f.full_flops);
+      f.sparsity = 1.0 - double(crit) / (double(D.Tm) * double(D.Tn));
+    }
+  });
+}
+
+int sla_b200_exec_counters(const sla_b200_problem* p, const void* q, const void* state,
+                           int aggregation, int group_size, sla_b200_counters* out,
+                           void* workspace, void* stream) {
+  return guarded([&] {
+    const Dims D = resolve(p);
+    require_supported(p, D);
+    if (!q || !out) throw InvalidArgument("exec_counters: q and out are required");
+    if (aggregation < SLA_B200_AGG_DIRECT || aggregation > SLA_B200_AGG_AUTO)
+      throw InvalidArgument("exec_counters: unknown aggregation strategy");
+    const int g = group_size >= 1 && group_size <= 20 ? group_size : 1;
+    const RowStats r = row_stats(p, D, q, state, workspace, g, static_cast<cudaStream_t>(stream));
+    *out = sla_b200_counters{};
+    for (long long u = 0; u < D.U; ++u) {
+      uint64_t crit = 0, marg = 0;
+      for (int i = 0; i < D.Tm; ++i) {
+        crit += uint64_t(r.rows[size_t(u) * D.Tm + i].x);
+        marg += uint64_t(r.rows[size_t(u) * D.Tm + i].y);
+      }
+      int kind = aggregation;  // resolve_strategy (aggregation.cpp:147-156), config.hpp:30-31
+      if (kind == SLA_B200_AGG_AUTO) {
+        const double frac = double(marg) / (double(D.Tm) * double(D.Tn));
+        kind = frac <= 0.25 ? SLA_B200_AGG_DIRECT
+                            : (frac >= 0.75 ? SLA_B200_AGG_COMPLEMENT : SLA_B200_AGG_FOUR_RUSSIANS);
+      }
+      if (kind == SLA_B200_AGG_FOUR_RUSSIANS) {
+        if (group_size < 1) throw InvalidArgument("four russians: g must be >= 1");
+        if (group_size > 20) throw InvalidArgument("four russians: g > 20 would need a 2^g table");
+        for (int b = 0; b < D.Tn; b += g)  // Gray-code table walk (aggregation.cpp:95-108)
+          out->table_build_additions += (uint64_t(1) << std::min(g, D.Tn - b)) - 1;
+      }
+      out->sparse_block_matmuls += 2 * crit;  // forward.cpp:46 + 123-124
+      for (int i = 0; i < D.Tm; ++i) {
+        const size_t row = size_t(u) * D.Tm + i;
+        const int4 x = r.rows[row];
+        out->linear_row_products += uint64_t(r.lin[row]);
+        if (kind == SLA_B200_AGG_DIRECT) {  // aggregation.cpp:40-56: the first term is a copy
+          out->additions += x.y > 0 ? uint64_t(x.y - 1) : 0;
+        } else if (kind == SLA_B200_AGG_COMPLEMENT) {  // aggregation.cpp:58-70
+          out->subtractions += uint64_t(D.Tn - x.y);
+        } else {  // aggregation.cpp:118-145
+          out->lookups += uint64_t(x.z);
+          out->additions += x.z > 0 ? uint64_t(x.z - 1) : 0;
+        }
+      }
+    }
+  });
 }
 
 int sla_b200_state_labels(const sla_b200_problem* p, const void* state, const int8_t** labels) {

@@ -15,6 +15,10 @@ bool launch_classify(const Dims& D, int dtype, int mask_precision, const void* q
 void launch_build_lut(const Dims& D, const StateBufs& s, long long* bad, cudaStream_t st);
 void launch_build_csc(const Dims& D, const StateBufs& s, cudaStream_t st);
 void launch_build_m0(const Dims& D, const StateBufs& s, cudaStream_t st);
+// counters.cu: device accounting from the LUT (flops_report, ExecCounters)
+void launch_row_stats(const Dims& D, const int8_t* labels, int g, int4* out, cudaStream_t st);
+void launch_lin_rows(const Dims& D, int dtype, const void* q, const float* Z, bool z3,
+                     const int4* stats, int* lin_rows, cudaStream_t st);
 
 // generic.cu -- shape-generic SIMT kernels (fp32 math, any b_q, b_kv, d within smem limits)
 bool generic_supported(const Dims& D, std::string* why);

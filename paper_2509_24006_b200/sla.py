@@ -231,6 +231,26 @@ class SLA:
             None if gp is None else C.byref(gp), _ptr(st.state), _ptr(self._workspace), _stream()))
         return SlaGradients(dq, dk, dv, dw, **extra)
 
+    def flops_report(self, st) -> list:
+        """flops_report (flops.cpp:7-33) of every (batch, head) unit, from the device LUT of a
+        forward state (SlaForwardState or its state tensor).  Synchronises the stream."""
+        state = st.state if isinstance(st, SlaForwardState) else st
+        arr = (L.Flops * (self.batch * self.heads))()
+        L.check(L.lib().sla_b200_flops_report(C.byref(self.p), _ptr(state), arr, _ptr(self._workspace),
+                                              _stream()))
+        return [{f: getattr(x, f) for f, _ in L.Flops._fields_} for x in arr]
+
+    def exec_counters(self, st: SlaForwardState, q, aggregation: str = "direct", group_size: int = 4) -> dict:
+        """ExecCounters of the forward that produced `st` (forward.hpp:46-50), as the reference
+        counts them for `aggregation` (config.hpp:19-31), summed over units."""
+        self._check("Q", q)
+        if aggregation not in L.AGG:
+            raise ValueError(f"unknown aggregation strategy '{aggregation}'")
+        c = L.Counters()
+        L.check(L.lib().sla_b200_exec_counters(C.byref(self.p), _ptr(q), _ptr(st.state), L.AGG[aggregation],
+                                               group_size, C.byref(c), _ptr(self._workspace), _stream()))
+        return {f: int(getattr(c, f)) for f, _ in L.Counters._fields_}
+
     def launches(self) -> int:
         """Kernels launched by the last C-ABI call on this thread."""
         return int(L.lib().sla_b200_last_launch_count())

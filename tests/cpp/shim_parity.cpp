@@ -30,23 +30,32 @@ int main(int argc, char** argv) {
   MatF w = bf16_mat(rng, d, d, 0.1), dout = bf16_mat(rng, n, d, 1.0);
 
   // reference
-  auto st = sla::sla_forward(q, k, v, cfg, layout, 8);
+  cfg.aggregation = argc > 3 ? static_cast<AggregationKind>(atoi(argv[3])) : AggregationKind::direct;
+  ExecCounters c_ref, c_gpu;
+  auto st = sla::sla_forward(q, k, v, cfg, layout, 8, &c_ref);
   auto o = sla::combine_outputs(st, OutputProjection<float>{w});
   auto [ds, dl, dw] = sla::proj_backward(dout, st.linear_out, w);
   auto g = sla::sla_backward(st, q, k, v, ds, dl, cfg, layout, 8);
 
   // drop-in (same calls, namespace sla::gpu)
-  auto st2 = sla::gpu::sla_forward(q, k, v, cfg, layout);
+  auto st2 = sla::gpu::sla_forward(q, k, v, cfg, layout, 1, &c_gpu);
   auto o2 = sla::gpu::combine_outputs(st2, OutputProjection<float>{w});
   auto [ds2, dl2, dw2] = sla::gpu::proj_backward(dout, st2.linear_out, w);
   auto g2 = sla::gpu::sla_backward(st2, q, k, v, ds2, dl2, cfg, layout);
 
   const bool labels_equal = st.mask.labels == st2.mask.labels;
+  const bool counters_equal =
+      c_ref.sparse_block_matmuls == c_gpu.sparse_block_matmuls &&
+      c_ref.linear_row_products == c_gpu.linear_row_products &&
+      c_ref.aggregation.additions == c_gpu.aggregation.additions &&
+      c_ref.aggregation.subtractions == c_gpu.aggregation.subtractions &&
+      c_ref.aggregation.lookups == c_gpu.aggregation.lookups &&
+      c_ref.aggregation.table_build_additions == c_gpu.aggregation.table_build_additions;
   std::printf(
-      "{\"n\": %zu, \"d\": %zu, \"labels_equal\": %s, \"o\": %.3e, \"o_s\": %.3e, \"o_l\": %.3e, "
+      "{\"n\": %zu, \"d\": %zu, \"labels_equal\": %s, \"counters_equal\": %s, \"o\": %.3e, \"o_s\": %.3e, \"o_l\": %.3e, "
       "\"dq_total\": %.3e, \"dk_total\": %.3e, \"dv\": %.3e, \"dw\": %.3e}\n",
-      n, d, labels_equal ? "true" : "false", rel_diff(o2, o, 1.0), rel_diff(st2.sparse_out, st.sparse_out, 1.0),
+      n, d, labels_equal ? "true" : "false", counters_equal ? "true" : "false", rel_diff(o2, o, 1.0), rel_diff(st2.sparse_out, st.sparse_out, 1.0),
       rel_diff(st2.linear_out, st.linear_out, 1.0), rel_diff(g2.dq_total, g.dq_total, 1.0),
       rel_diff(g2.dk_total, g.dk_total, 1.0), rel_diff(g2.dv, g.dv, 1.0), rel_diff(g2.dproj, dw, 1.0));
-  return labels_equal ? 0 : 1;
+  return labels_equal && counters_equal ? 0 : 1;
 }
