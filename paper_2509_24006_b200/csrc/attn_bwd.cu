@@ -97,6 +97,13 @@ __global__ void __launch_bounds__(kColsThreads, 1)
   const bool has_lin = p.ccol_marg[ucol] > 0;  // some marginal row in this column (k_build_csc)
   ts_mark(dbg && threadIdx.x == 0, 126);
   const int kv0 = int(u * p.N) + j * 64;
+  // pair 0's query blocks, loaded alongside cnt so its loads can leave before the TMEM
+  // allocation and the block barrier
+  int l0 = 0, l1 = 0;
+  if (threadIdx.x == 0) {
+    l0 = list[0];
+    l1 = list[min(1, p.Tm - 1)];
+  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -119,6 +126,28 @@ __global__ void __launch_bounds__(kColsThreads, 1)
       tc::mbar_init(kf_ready, 8);
       tc::mbar_init(all_done, 1);
       tc::fence_barrier_init();
+      // K_j / V_j and pair 0 (items 0 and 1) now; the producer loops start at pair 1
+      tc::tma_prefetch(&tmQ);
+      tc::tma_prefetch(&tmDO);
+      tc::mbar_expect_tx(kv_full, 2 * L::kT);
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        tc::tma_load_3d(sK + c * 8192, &tmK, kv_full, 64 * c, kv0, 0);
+        tc::tma_load_3d(sV + c * 8192, &tmV, kv_full, 64 * c, kv0, 0);
+      }
+      if (np > 0) {
+        const int r1 = int(u * p.N) + l0 * 64, r2 = int(u * p.N) + (cnt > 1 ? l1 : l0) * 64;
+        ts_mark(dbg, 0);
+#pragma unroll
+        for (int it = 0; it < 2; ++it) {
+          tc::mbar_expect_tx(ring_full + it, L::kP);
+#pragma unroll
+          for (int c = 0; c < D / 64; ++c) {
+            tc::tma_load_3d(sRing + it * L::kSlot + c * 16384, it ? &tmDO : &tmQ, ring_full + it, 64 * c, r1, 0);
+            tc::tma_load_3d(sRing + it * L::kSlot + c * 16384 + 8192, it ? &tmDO : &tmQ, ring_full + it, 64 * c, r2, 0);
+          }
+        }
+      }
     }
     __syncwarp();
     tc::tmem_alloc<512>(tmem_slot);
@@ -138,15 +167,6 @@ __global__ void __launch_bounds__(kColsThreads, 1)
     // pid 0 loads the Q pair (and K_j / V_j), pid 1 the dO pair.
     if (lane == 0) {
       const int pid = warp == 0 ? 0 : 1;
-      tc::tma_prefetch(pid == 0 ? &tmQ : &tmDO);
-      if (pid == 0) {
-        tc::mbar_expect_tx(kv_full, 2 * L::kT);
-#pragma unroll
-        for (int c = 0; c < D / 64; ++c) {
-          tc::tma_load_3d(sK + c * 8192, &tmK, kv_full, 64 * c, kv0, 0);
-          tc::tma_load_3d(sV + c * 8192, &tmV, kv_full, 64 * c, kv0, 0);
-        }
-      }
       auto acquire = [&](int item, int bytes) -> uint8_t* {
         const int s = item % RS;
         tc::mbar_wait(ring_empty + s, ((item / RS) & 1) ^ 1);
@@ -154,7 +174,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
         return sRing + s * L::kSlot;
       };
       const CUtensorMap* tm = pid ? &tmDO : &tmQ;
-      for (int pp = 0; pp < np; ++pp) {
+      for (int pp = 1; pp < np; ++pp) {  // pair 0 left before the block barrier
         const int r1 = int(u * p.N) + list[2 * pp] * 64;
         const int r2 = int(u * p.N) + list[min(2 * pp + 1, cnt - 1)] * 64;
         const int item = 2 * pp + pid;

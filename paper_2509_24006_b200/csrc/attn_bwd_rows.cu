@@ -374,6 +374,13 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   const bool dbg = blockIdx.x == SLAB_DBG_X && blockIdx.y == 6;
   ts_mark(dbg && threadIdx.x == 0, 127);
   cta_mark(threadIdx.x == 0, 0);
+  // the first pair's key blocks, loaded alongside cnt (not after it) so the first K / V pair
+  // can leave before the TMEM allocation and the block barrier
+  int l0 = 0, l1 = 0;
+  if (threadIdx.x == 0) {
+    l0 = list[0];
+    l1 = list[min(1, p.Tn - 1)];
+  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -395,6 +402,32 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         tc::mbar_init(v_empty + s, 1);
       }
       tc::fence_barrier_init();
+      // Q_i / dO_i and pair 0 (K and V) now; the producer loops start at pair 1
+      tc::tma_prefetch(&tmK);
+      tc::tma_prefetch(&tmV);
+      tc::mbar_expect_tx(qdo_full, 2 * L::kT);
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        tc::tma_load_3d(sQ + c * 8192, &tmQ, qdo_full, 64 * c, row0, 0);
+        tc::tma_load_3d(sDO + c * 8192, &tmDO, qdo_full, 64 * c, row0, 0);
+      }
+      if (np > 0) {
+        const int r1 = int(u * p.N) + l0 * 64, r2 = int(u * p.N) + (cnt > 1 ? l1 : l0) * 64;
+        ts_mark(dbg, 0);
+        ts_mark(dbg, 112);
+        tc::mbar_expect_tx(k_full, L::kP);
+        tc::mbar_expect_tx(v_full, L::kP);
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) {
+          tc::tma_load_3d(sK + c * 16384, &tmK, k_full, 64 * c, r1, 0);
+          tc::tma_load_3d(sK + c * 16384 + 8192, &tmK, k_full, 64 * c, r2, 0);
+        }
+#pragma unroll
+        for (int c = 0; c < D / 64; ++c) {
+          tc::tma_load_3d(sV + c * 16384, &tmV, v_full, 64 * c, r1, 0);
+          tc::tma_load_3d(sV + c * 16384 + 8192, &tmV, v_full, 64 * c, r2, 0);
+        }
+      }
     }
     __syncwarp();
     tc::tmem_alloc<512>(tmem_slot);
@@ -419,16 +452,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     // two producer warps (Q/dO + K ring, V ring): one issuing warp's TMA stream caps at ~40 B/cycle
     if (lane == 0) {
       const int pid = warp == 0 ? 0 : 1;
-      tc::tma_prefetch(pid == 0 ? &tmK : &tmV);
-      if (pid == 0) {
-        tc::mbar_expect_tx(qdo_full, 2 * L::kT);
-#pragma unroll
-        for (int c = 0; c < D / 64; ++c) {
-          tc::tma_load_3d(sQ + c * 8192, &tmQ, qdo_full, 64 * c, row0, 0);
-          tc::tma_load_3d(sDO + c * 8192, &tmDO, qdo_full, 64 * c, row0, 0);
-        }
-      }
-      for (int t = 0; t < np; ++t) {
+      for (int t = 1; t < np; ++t) {  // pair 0 left before the block barrier
         // an odd tail repeats its block (finite data); the compute warps zero its dS rows
         const int r1 = int(u * p.N) + list[2 * t] * 64;
         const int r2 = int(u * p.N) + list[min(2 * t + 1, cnt - 1)] * 64;
