@@ -408,8 +408,16 @@ int sla_b200_backward_ex(const sla_b200_problem* p, const void* q, const void* k
       dk = wb.pad[kPdK];
       dv = wb.pad[kPdV];
     }
-    if (fast)
-      fast_backward(D, q, k, v, w, o_s, o_l, lse, d_out, dq, dk, dv, dw, s, wb, st);
+    if (fast) {
+      SideFork side;
+      if (!prof_enabled()) {  // the per-kernel profiler times one event sequence
+        SideStream& ss = side_stream();
+        side.s = ss.s;
+        side.fork = ss.fork;
+        side.join = ss.join;
+      }
+      fast_backward(D, q, k, v, w, o_s, o_l, lse, d_out, dq, dk, dv, dw, s, wb, st, side);
+    }
     else
       generic_backward(D, p->dtype, q, k, v, w, o_s, o_l, lse, d_out, dq, dk, dv, dw, s, wb, st);
     if (parts) {

@@ -213,9 +213,18 @@ void fast_forward(const Dims& Dm, const void* q, const void* k, const void* v, c
 void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
                    const void* o_s, const void* o_l, const float* lse, const void* d_out,
                    void* dq, void* dk, void* dv, float* dw, const StateBufs& s,
-                   const WorkBufs& wb, cudaStream_t st) {
+                   const WorkBufs& wb, cudaStream_t st, const SideFork& side) {
   const int d = Dm.d;
-  launch_build_csc(Dm, s, st);
+  // the column lists (labels only) build on the side stream while k_bwd_lin, a latency-bound
+  // kernel with registers and threads to spare on every SM, runs; joined before the columns pass
+  if (side.s) {
+    SLAB_CUDA(cudaEventRecord(side.fork, st));
+    SLAB_CUDA(cudaStreamWaitEvent(side.s, side.fork, 0));
+    launch_build_csc(Dm, s, side.s);
+    SLAB_CUDA(cudaEventRecord(side.join, side.s));
+  } else {
+    launch_build_csc(Dm, s, st);
+  }
   // row phase: the linear branch (dH_i reusing the forward's h scratch, dZ_i, D^s, dQ^phi),
   // then the sparse dQ over critical pairs with dq_total = J_phi^T dQ^phi + dQ
   launch_bwd_lin(Dm, q, w, o_s, o_l, d_out, s, wb.hb, wb.z3b, wb.Ds, wb.dqphi, st);
@@ -242,6 +251,7 @@ void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, 
   launch_gemm(a, st);
   aggregate_vec_tc(Dm, s, wb, true, wb.gZa, "gemm_aggregate_dz", st);  // gZa: [U, Tn, 3d]
   // columns pass: dk_total, dv
+  if (side.s) SLAB_CUDA(cudaStreamWaitEvent(st, side.join, 0));
   launch_bwd_cols(Dm, q, k, v, lse, d_out, dk, dv, s, wb.hab, wb.gZa, wb.Ds, st);
   // dW = O^l^T dO per head, split-K over row chunks of each unit, then reduced over chunks + batch
   const long long KC = 64LL * dw_chunk_tiles(Dm);

@@ -62,9 +62,15 @@ bool fast_supported(const Dims& D, int dtype);
 void fast_forward(const Dims& D, const void* q, const void* k, const void* v, const void* w,
                   void* o, void* o_s, void* o_l, float* lse, const StateBufs& s,
                   const WorkBufs& wb, bool m0_ready, bool summaries_done, cudaStream_t st);
+// A side stream with fork / join events: work that only depends on the call's inputs runs
+// there, concurrent with latency-bound kernels on the caller's stream (s == nullptr: none).
+struct SideFork {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
 void fast_backward(const Dims& D, const void* q, const void* k, const void* v, const void* w,
                    const void* o_s, const void* o_l, const float* lse, const void* d_out,
                    void* dq, void* dk, void* dv, float* dw, const StateBufs& s,
-                   const WorkBufs& wb, cudaStream_t st);
+                   const WorkBufs& wb, cudaStream_t st, const SideFork& side);
 
 }  // namespace slab
