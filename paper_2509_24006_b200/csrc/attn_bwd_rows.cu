@@ -1,7 +1,7 @@
 // attn_bwd_rows.cu -- the ROW phase of the SLA backward (backward.cpp:46-120, 211-214) as two
 // tcgen05 kernels:
 //
-// k_bwd_lin<D>: one CTA per (unit, query block i), 2 CTAs / SM -- the linear branch
+// k_bwd_lin<D>: one CTA per (unit, query block i), 2 CTAs / SM, 8 compute warps -- the linear branch
 //   dO^l_i = dO_i W^T (MMA, backward.cpp:12-22), D^s, D^l (backward.cpp:48-58),
 //   x = phi(q), den = phi(q) . Z_i, [dH_i | -dZ_i] = x^T [dO^l/den | D^l/den] (one MMA),
 //   dQ^phi^T = H_i (dO^l/den)^T (MMA) - (D^l/den) Z_i  (backward.cpp:70-95).
@@ -30,13 +30,16 @@ struct LinLayout {
   static constexpr int oQ = 0, oDO = kT, oDOL = 2 * kT, oDL = 3 * kT, oX = 3 * kT + 8192;
   static constexpr int oWH = oX + kT;   // W, then H_i (D*D*2)
   static constexpr int oZS = oWH + D * D * 2;
-  static constexpr int oBar = oZS + 4 * D + 4 * 64;
+  static constexpr int oRed = oZS + 4 * D + 4 * 64;  // float [5][2][64] row-sum halves
+  static constexpr int oBar = oRed + 5 * 128 * 4;
   static constexpr int kBytes = oBar + 128 + 1024;
   static_assert(kBytes <= 116736, "2 CTAs / SM");
 };
 
+constexpr int kLinThreads = 64 + 256;  // TMA warp, MMA warp, 8 compute warps
+
 template <int D>
-__global__ void __launch_bounds__(192, 2)
+__global__ void __launch_bounds__(kLinThreads, 2)
     k_bwd_lin(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
               const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmH,
               const __grid_constant__ CUtensorMap tmOS, const __grid_constant__ CUtensorMap tmOL,
@@ -52,6 +55,7 @@ __global__ void __launch_bounds__(192, 2)
   uint8_t* sWH = smem + L::oWH;
   float* zs = reinterpret_cast<float*>(smem + L::oZS);
   float* s_dls = zs + D;
+  float* s_red = reinterpret_cast<float*>(smem + L::oRed);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::oBar);
   uint64_t* qdo_full = bars + 0;
   uint64_t* w_full = bars + 1;
@@ -77,7 +81,7 @@ __global__ void __launch_bounds__(192, 2)
       tc::mbar_init(w_free, 1);
       tc::mbar_init(h_full, 1);
       tc::mbar_init(dol_done, 1);
-      tc::mbar_init(x_ready, 4);
+      tc::mbar_init(x_ready, 8);
       tc::mbar_init(lin_done, 1);
       tc::mbar_init(o_full, 1);
       tc::fence_barrier_init();
@@ -148,56 +152,72 @@ __global__ void __launch_bounds__(192, 2)
       tc::mma_commit_w(lin_done);
     }
   } else {
+    // 8 compute warps: warps w and w + 4 share TMEM lane quarter q4 (rows 16 q4 .. +15 of the
+    // M = 64 layout) and split the columns; 4 threads per row, D/4 columns each
+    // (quarter cq = 2 half + lane / 16).  Row sums combine lanes l / l+16 by shuffle and the two
+    // warps of a pair through s_red with a 64-thread named barrier per pair.
     const int q4 = warp & 3;
+    const int half = (warp - 2) >> 2;
     const int r = 16 * q4 + (lane & 15);
-    const int h0 = (lane >> 4) * (D / 2);
+    const int h0 = (2 * half + (lane >> 4)) * (D / 4);
     const bool valid = lane < 16;
     const uint32_t lane_base = uint32_t(32 * q4) << 16;
     const long long grow = (long long)row0 + r;
-    const int tid = threadIdx.x - 64;
-    for (int a = tid; a < D; a += 128) zs[a] = has_lin ? tc::load_sum3(p.Z + urow * 3 * D + a, D) : 0.f;
-    for (int e = tid; e < 64 * 7; e += 128)
+    const int tid = threadIdx.x - 64;  // 0..255
+    auto pair_sum = [&](float x, int slot) {  // full-row sum of a per-thread partial
+      x += __shfl_xor_sync(0xffffffffu, x, 16);
+      if (valid) s_red[slot * 128 + half * 64 + r] = x;
+      named_sync(2 + q4, 64);
+      return s_red[slot * 128 + r] + s_red[slot * 128 + 64 + r];
+    };
+    auto pair_max = [&](float x, int slot) {
+      x = fmaxf(x, __shfl_xor_sync(0xffffffffu, x, 16));
+      if (valid) s_red[slot * 128 + half * 64 + r] = x;
+      named_sync(2 + q4, 64);
+      return fmaxf(s_red[slot * 128 + r], s_red[slot * 128 + 64 + r]);
+    };
+    for (int a = tid; a < D; a += 256) zs[a] = has_lin ? tc::load_sum3(p.Z + urow * 3 * D + a, D) : 0.f;
+    for (int e = tid; e < 64 * 7; e += 256)
       *reinterpret_cast<uint4*>(sDL + tc::sw128_off(e / 7, 1 + e % 7)) = make_uint4(0, 0, 0, 0);
-    named_sync(1, 128);
+    named_sync(1, 256);
     tc::mbar_wait(qdo_full, 0);
     tc::mbar_wait(o_full, 0);
     float ds_r = 0.f;
 #pragma unroll
-    for (int c = 0; c < D / 2; c += 8) {
+    for (int c = 0; c < D / 4; c += 8) {
       float f[8], g[8];
       unpack8(*reinterpret_cast<const uint4*>(sDO + tile_off(r, h0 + c)), f);
       unpack8(*reinterpret_cast<const uint4*>(sX + tile_off(r, h0 + c)), g);
 #pragma unroll
       for (int e = 0; e < 8; ++e) ds_r = fmaf(f[e], g[e], ds_r);
     }
-    ds_r += __shfl_xor_sync(0xffffffffu, ds_r, 16);
-    if (valid) p.Ds_out[grow] = ds_r;
-    named_sync(1, 128);  // O^s (in sX) fully consumed before phi(Q) overwrites it
+    ds_r = pair_sum(ds_r, 0);
+    if (valid && half == 0) p.Ds_out[grow] = ds_r;
+    named_sync(1, 256);  // O^s (in sX) fully consumed before phi(Q) overwrites it
     float mx = 0.f, inv = 1.f;
     if (p.phi == 2) {
       mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < D / 2; c += 8) {
+      for (int c = 0; c < D / 4; c += 8) {
         float f[8];
         unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(r, h0 + c)), f);
 #pragma unroll
         for (int e = 0; e < 8; ++e) mx = fmaxf(mx, f[e]);
       }
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
+      mx = pair_max(mx, 1);
       float se = 0.f;
 #pragma unroll
-      for (int c = 0; c < D / 2; c += 8) {
+      for (int c = 0; c < D / 4; c += 8) {
         float f[8];
         unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(r, h0 + c)), f);
 #pragma unroll
         for (int e = 0; e < 8; ++e) se += __expf(f[e] - mx);
       }
-      se += __shfl_xor_sync(0xffffffffu, se, 16);
-      inv = 1.f / se;
+      inv = 1.f / pair_sum(se, 2);
     }
     float den = 0.f;
 #pragma unroll
-    for (int c = 0; c < D / 2; c += 8) {
+    for (int c = 0; c < D / 4; c += 8) {
       float f[8];
       unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(r, h0 + c)), f);
 #pragma unroll
@@ -207,13 +227,13 @@ __global__ void __launch_bounds__(192, 2)
       }
       *reinterpret_cast<uint4*>(sX + tile_off(r, h0 + c)) = pack8(f);
     }
-    den += __shfl_xor_sync(0xffffffffu, den, 16);
+    den = pair_sum(den, 3);
     const float inv_den = (has_lin && den != 0.f) ? 1.f / den : 0.f;  // den == 0 -> zero row
     tc::mbar_wait(dol_done, 0);
     tc::tc_fence_after();
     float dl_r = 0.f;
 #pragma unroll 1
-    for (int c0 = 0; c0 < D; c0 += 32) {
+    for (int c0 = 32 * half; c0 < D; c0 += 64) {  // this warp's TMEM column blocks of dO^l
       uint32_t a[32];
       tc::tmem_ld32(tA + lane_base + c0, a);
       tc::tmem_ld_wait();
@@ -233,8 +253,8 @@ __global__ void __launch_bounds__(192, 2)
         }
       }
     }
-    const float dls = dl_r * inv_den;  // D^l / den
-    if (valid) {
+    const float dls = pair_sum(dl_r, 4) * inv_den;  // D^l / den (lanes >= 16 contribute 0)
+    if (valid && half == 0) {
       *reinterpret_cast<uint4*>(sDL + tc::sw128_off(r, 0)) = make_uint4(tc::pack_bf16(dls, 0.f), 0, 0, 0);
       s_dls[r] = dls;
     }
@@ -242,7 +262,7 @@ __global__ void __launch_bounds__(192, 2)
     tc::tc_fence_before();
     __syncwarp();
     if (lane == 0) tc::mbar_arrive(x_ready);
-    named_sync(1, 128);  // s_dls visible
+    named_sync(1, 256);  // s_dls visible
     __nv_bfloat16* gHi = p.gH + urow * D * D;
     __nv_bfloat16* dqp = p.dqphi + (long long)row0 * D;
     if (has_lin) {
@@ -251,7 +271,7 @@ __global__ void __launch_bounds__(192, 2)
       const int arow = D == 128 ? 32 * q4 + lane : 16 * q4 + lane;
       const bool avalid = D == 128 || lane < 16;
 #pragma unroll 1
-      for (int c0 = 0; c0 < D + 32; c0 += 32) {
+      for (int c0 = 32 * half; c0 < D + 32; c0 += 64) {  // [dH | -dZ] column blocks of this warp
         uint32_t a[32];
         tc::tmem_ld32(tA + lane_base + c0, a);
         tc::tmem_ld_wait();
@@ -271,7 +291,7 @@ __global__ void __launch_bounds__(192, 2)
         }
       }
       tc::fence_proxy_async();
-      named_sync(1, 128);
+      named_sync(1, 256);
       if (tid == 0) {  // coalesced: one TMA store per 64-column box
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) tc::tma_store_3d(&tmGH, sQ + c * (D * 128), 64 * c, int(urow * D), 0);
@@ -280,29 +300,30 @@ __global__ void __launch_bounds__(192, 2)
       // dQ^phi[r][a] = raw^T[a][r] - (D^l/den)_r Z[a]; stage as a row-major bf16 tile in sX
       // (phi(Q) is dead once lin_done fired), then store coalesced rows
       const float za = avalid ? zs[arow] : 0.f;
-#pragma unroll 1
-      for (int c0 = 0; c0 < 64; c0 += 32) {
+      {
+        const int c0 = 32 * half;  // this warp's 32 query rows
         uint32_t a[32];
         tc::tmem_ld32(tQP + lane_base + c0, a);
         tc::tmem_ld_wait();
-        if (!avalid) continue;
+        if (avalid) {
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const int rr = c0 + e;
-          const float v = __uint_as_float(a[e]) - s_dls[rr] * za;
-          *reinterpret_cast<__nv_bfloat16*>(sX + tile_off(rr, arow & ~7) + (arow & 7) * 2) = __float2bfloat16_rn(v);
+          for (int e = 0; e < 32; ++e) {
+            const int rr = c0 + e;
+            const float v = __uint_as_float(a[e]) - s_dls[rr] * za;
+            *reinterpret_cast<__nv_bfloat16*>(sX + tile_off(rr, arow & ~7) + (arow & 7) * 2) = __float2bfloat16_rn(v);
+          }
         }
       }
-      named_sync(1, 128);
-      for (int e = tid; e < 64 * D / 8; e += 128) {
+      named_sync(1, 256);
+      for (int e = tid; e < 64 * D / 8; e += 256) {
         const int rr = e / (D / 8), cc = (e % (D / 8)) * 8;
         *reinterpret_cast<uint4*>(dqp + (long long)rr * D + cc) = *reinterpret_cast<const uint4*>(sX + tile_off(rr, cc));
       }
       if (tid == 0) tc::bulk_wait_read<0>();  // dH_i stores have read the staging smem
     } else {
-      for (int e = tid; e < D * D / 8; e += 128) reinterpret_cast<uint4*>(gHi)[e] = make_uint4(0, 0, 0, 0);
-      for (int a = tid; a < D; a += 128) tc::store_split3(p.z3 + urow * 3 * D + a, D, 0.f);
-      for (int e = tid; e < 64 * D / 8; e += 128) reinterpret_cast<uint4*>(dqp)[e] = make_uint4(0, 0, 0, 0);
+      for (int e = tid; e < D * D / 8; e += 256) reinterpret_cast<uint4*>(gHi)[e] = make_uint4(0, 0, 0, 0);
+      for (int a = tid; a < D; a += 256) tc::store_split3(p.z3 + urow * 3 * D + a, D, 0.f);
+      for (int e = tid; e < 64 * D / 8; e += 256) reinterpret_cast<uint4*>(dqp)[e] = make_uint4(0, 0, 0, 0);
     }
   }
   tc::tc_fence_before();
@@ -739,7 +760,7 @@ void launch_bwd_lin(const Dims& Dm, const void* q, const void* w, const void* o_
     make_tmap_bf16(&tol, o_l, D, rows, 1, D, 0, 64);
     make_tmap_bf16(&tgh, gH, D, uint64_t(Dm.U) * Dm.Tm * D, 1, D, 0, D);  // dH_i boxes [D rows][64]
     SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    kern<<<dim3(Dm.Tm, unsigned(Dm.U)), 192, bytes, st>>>(tq, tdo, tw, th, tos, tol, tgh, p);
+    kern<<<dim3(Dm.Tm, unsigned(Dm.U)), kLinThreads, bytes, st>>>(tq, tdo, tw, th, tos, tol, tgh, p);
     check_launch("k_bwd_lin", st);
   };
   if (Dm.d == 128)
