@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
     k_bwd_cols(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
                const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                const __grid_constant__ CUtensorMap tmHa, BwdParams p) {
+  pdl_entry();  // launched by launch_pdl
   using L = ColsLayout<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -532,7 +533,7 @@ void launch_cols_t(const Dims& Dm, const void* q, const void* k, const void* v, 
   make_tmap_bf16(&th, Ha, D, uint64_t(Dm.U) * Dm.Tn * D, 1, D, 0, D);
   auto kern = k_bwd_cols<D>;
   SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ColsLayout<D>::kBytes));
-  kern<<<dim3(Dm.Tn, unsigned(Dm.U)), kColsThreads, ColsLayout<D>::kBytes, st>>>(tq, tdo, tk, tv, th, p);
+  launch_pdl(kern, dim3(Dm.Tn, unsigned(Dm.U)), kColsThreads, ColsLayout<D>::kBytes, st, tq, tdo, tk, tv, th, p);
   check_launch("k_bwd_cols", st);
 }
 

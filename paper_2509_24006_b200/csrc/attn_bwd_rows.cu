@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(kLinThreads, 2)
               const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmH,
               const __grid_constant__ CUtensorMap tmOS, const __grid_constant__ CUtensorMap tmOL,
               const __grid_constant__ CUtensorMap tmGH, BwdParams p) {
+  pdl_entry();  // launched by launch_pdl
   using L = LinLayout<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -359,6 +360,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     k_bwd_rows(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
                const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                BwdParams p) {
+  pdl_entry();  // launched by launch_pdl
   using L = RowsLayout<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -760,7 +762,7 @@ void launch_bwd_lin(const Dims& Dm, const void* q, const void* w, const void* o_
     make_tmap_bf16(&tol, o_l, D, rows, 1, D, 0, 64);
     make_tmap_bf16(&tgh, gH, D, uint64_t(Dm.U) * Dm.Tm * D, 1, D, 0, D);  // dH_i boxes [D rows][64]
     SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    kern<<<dim3(Dm.Tm, unsigned(Dm.U)), kLinThreads, bytes, st>>>(tq, tdo, tw, th, tos, tol, tgh, p);
+    launch_pdl(kern, dim3(Dm.Tm, unsigned(Dm.U)), kLinThreads, bytes, st, tq, tdo, tw, th, tos, tol, tgh, p);
     check_launch("k_bwd_lin", st);
   };
   if (Dm.d == 128)
@@ -795,7 +797,7 @@ void launch_bwd_rows(const Dims& Dm, const void* q, const void* k, const void* v
     make_tmap_bf16(&tk, k, D, rows, 1, D, 0, 64);
     make_tmap_bf16(&tv, v, D, rows, 1, D, 0, 64);
     SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    kern<<<dim3(Dm.Tm, unsigned(Dm.U)), kRowsThreads, bytes, st>>>(tq, tdo, tk, tv, p);
+    launch_pdl(kern, dim3(Dm.Tm, unsigned(Dm.U)), kRowsThreads, bytes, st, tq, tdo, tk, tv, p);
     check_launch("k_bwd_rows", st);
   };
   if (Dm.d == 128)

@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(192, 2)
                const __grid_constant__ CUtensorMap tmV, const __grid_constant__ CUtensorMap tmH,
                const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmO,
                const __grid_constant__ CUtensorMap tmOs, const __grid_constant__ CUtensorMap tmOl, FwdParams p) {
+  pdl_entry();  // launched by launch_pdl
   using L = FwdLayout<D>;
   constexpr int RS = L::kSlots;
   constexpr int NC = D / 64;  // 64-column chunks of H / W
@@ -554,7 +555,7 @@ void launch_t(const Dims& Dm, const void* q, const void* k, const void* v, const
     to = tos;
   auto kern = k_attn_fwd<D>;
   SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, FwdLayout<D>::kBytes));
-  kern<<<dim3(Dm.Tm, unsigned(Dm.U)), 192, FwdLayout<D>::kBytes, st>>>(tq, tk, tv, th, tw, to, tos, tol, p);
+  launch_pdl(kern, dim3(Dm.Tm, unsigned(Dm.U)), 192, FwdLayout<D>::kBytes, st, tq, tk, tv, th, tw, to, tos, tol, p);
   check_launch("k_attn_fwd", st);
 }
 

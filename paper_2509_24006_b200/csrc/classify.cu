@@ -59,6 +59,7 @@ __global__ void __launch_bounds__(32) k_pool2_bf16(const __nv_bfloat16* __restri
                                                    const __nv_bfloat16* __restrict__ k,
                                                    R* __restrict__ pq, R* __restrict__ pk, long long N,
                                                    int d, int b, int T, long long n_valid) {
+  pdl_entry();  // launched by launch_pdl
   const long long u = blockIdx.y;
   const int g = blockIdx.x;
   const __nv_bfloat16* x = blockIdx.z ? k : q;
@@ -103,6 +104,7 @@ template <typename R>
 __global__ void __maxnreg__(SLAB_SCORES_REGS) k_scores(const R* __restrict__ pq, const R* __restrict__ pk,
                                                 int d, int Tm, int Tn, R inv_sqrt_d,
                                                 R* __restrict__ s) {
+  pdl_entry();  // launched by launch_pdl
   constexpr int CK = 32;
   __shared__ R sa[64][CK + 1];
   __shared__ R sb[64][CK + 1];
@@ -278,6 +280,7 @@ __global__ void __launch_bounds__(256) k_classify_warp(const R* __restrict__ sco
                                                        int* __restrict__ crit_idx, int* __restrict__ marg_cnt,
                                                        double* __restrict__ p_c_out,
                                                        __nv_bfloat16* __restrict__ m0, int m0_ld) {
+  pdl_entry();  // launched by launch_pdl
   constexpr int P2 = 32 * EPL;
   __shared__ int8_t slab[8][P2];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -425,6 +428,7 @@ __global__ void k_build_lut(const int8_t* __restrict__ labels, int Tm, int Tn,
 __global__ void k_build_csc(const int8_t* __restrict__ labels, int Tm, int Tn,
                             int* __restrict__ ccol_cnt, int* __restrict__ ccol_idx,
                             int* __restrict__ ccol_marg) {
+  pdl_entry();  // launched by launch_pdl
   const long long u = blockIdx.y;
   const int j = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
@@ -497,7 +501,7 @@ static bool classify_t(const Dims& D, const In* q, const In* k, const StateBufs&
   bool pooled = false;
   if constexpr (std::is_same<In, __nv_bfloat16>::value) {
     if (D.d % 4 == 0 && D.bq == D.bkv) {
-      k_pool2_bf16<R><<<dim3(D.Tm, unsigned(D.U), 2), 32, 0, st>>>(q, k, pq, pk, D.N, D.d, D.bq, D.Tm, D.N_valid);
+      launch_pdl(k_pool2_bf16<R>, dim3(D.Tm, unsigned(D.U), 2), 32, 0, st, q, k, pq, pk, D.N, D.d, D.bq, D.Tm, D.N_valid);
       check_launch("k_pool", st);
       pooled = true;
     }
@@ -513,15 +517,15 @@ static bool classify_t(const Dims& D, const In* q, const In* k, const StateBufs&
     SLAB_CUDA(cudaFuncSetAttribute(k_classify<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(smem)));
   R* scores = reinterpret_cast<R*>(w.p_c);
-  k_scores<R><<<dim3((D.Tn + 63) / 64, (D.Tm + 63) / 64, unsigned(D.U)), 256, 0, st>>>(
-      pq, pk, D.d, D.Tm, D.Tn, R(D.inv_sqrt_d), scores);
+  launch_pdl(k_scores<R>, dim3((D.Tn + 63) / 64, (D.Tm + 63) / 64, unsigned(D.U)), 256, 0, st,
+             (const R*)pq, (const R*)pk, D.d, D.Tm, D.Tn, R(D.inv_sqrt_d), scores);
   check_launch("k_scores", st);
   const int P2 = next_pow2(D.Tn);
   const long long rows = D.U * (long long)D.Tm;
   const unsigned wblocks = unsigned((rows + 7) / 8);
   auto warp_rows = [&](auto kern) {
-    kern<<<wblocks, 256, 0, st>>>(scores, rows, D.Tn, D.n1, D.n_neg, s.labels, s.crit_cnt, s.crit_idx,
-                                  s.marg_cnt, p_c, s.M0, int(m0_stride(D)));
+    launch_pdl(kern, wblocks, 256, 0, st, (const R*)scores, rows, D.Tn, D.n1, D.n_neg, s.labels, s.crit_cnt,
+               s.crit_idx, s.marg_cnt, p_c, s.M0, int(m0_stride(D)));
     check_launch("k_classify", st);
   };
   switch (P2) {  // one warp per block row while a row fits 16 registers per lane
@@ -566,8 +570,8 @@ void launch_build_lut(const Dims& D, const StateBufs& s, long long* bad, cudaStr
 
 void launch_build_csc(const Dims& D, const StateBufs& s, cudaStream_t st) {
   const int warps = 8;
-  k_build_csc<<<dim3((D.Tn + warps - 1) / warps, unsigned(D.U)), 32 * warps, 0, st>>>(
-      s.labels, D.Tm, D.Tn, s.ccol_cnt, s.ccol_idx, s.ccol_marg);
+  launch_pdl(k_build_csc, dim3((D.Tn + warps - 1) / warps, unsigned(D.U)), 32 * warps, 0, st,
+             (const int8_t*)s.labels, D.Tm, D.Tn, s.ccol_cnt, s.ccol_idx, s.ccol_marg);
   check_launch("k_build_csc", st);
 }
 

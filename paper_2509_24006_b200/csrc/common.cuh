@@ -6,6 +6,7 @@
 
 #include <cstdint>
 #include <string>
+#include <utility>
 
 namespace slab {
 
@@ -90,6 +91,45 @@ struct RuntimeFailure {
   std::string msg;
   explicit RuntimeFailure(std::string m) : msg(std::move(m)) {}
 };
+
+// Programmatic dependent launch: the next kernel of the chain is launched while this one's
+// last CTAs still run, and every kernel launched this way starts with griddep_wait() (returns
+// once the preceding grid has completed and its writes are visible), so only the launch
+// latency and block rasterisation overlap -- never a read of an unfinished result.
+#ifndef SLAB_PDL
+#define SLAB_PDL 1
+#endif
+__device__ __forceinline__ void griddep_wait() {
+#if SLAB_PDL
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
+__device__ __forceinline__ void griddep_launch() {
+#if SLAB_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
+}
+// prologue of every kernel launched by launch_pdl
+__device__ __forceinline__ void pdl_entry() {
+  griddep_wait();
+  griddep_launch();
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = SLAB_PDL;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);  // errors surface in check_launch
+}
 
 inline void check_launch(const char* what, cudaStream_t st) {
   cudaError_t e = cudaGetLastError();

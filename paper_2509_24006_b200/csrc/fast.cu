@@ -21,6 +21,7 @@ __global__ void __launch_bounds__(256) k_phi_kz(const __nv_bfloat16* __restrict_
                                                 __nv_bfloat16* __restrict__ kfb,
                                                 __nv_bfloat16* __restrict__ z3b, long long N, int Tn, int phi,
                                                 long long n_valid) {
+  pdl_entry();  // launched by launch_pdl
   constexpr int C = D / 32;
   __shared__ float zpart[8][D];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -96,6 +97,7 @@ __global__ void __launch_bounds__(256) k_phi_kz(const __nv_bfloat16* __restrict_
 // dW[h] = sum over the batch and the split-K chunks of O^l^T dO (backward.cpp:46).
 __global__ void k_reduce_dw(const float* __restrict__ part, int chunks_per_unit, long long B,
                             long long H, int dd, float* __restrict__ dw) {
+  pdl_entry();  // launched by launch_pdl
   const int h = blockIdx.y;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < dd; e += gridDim.x * blockDim.x) {
     float acc = 0.f;
@@ -147,10 +149,10 @@ bool fast_supported(const Dims& D, int dtype) {
 void fast_summaries(const Dims& Dm, const void* k, const void* v, const WorkBufs& wb, cudaStream_t st) {
   const int d = Dm.d;
   if (d == 128)
-    k_phi_kz<128><<<dim3(Dm.Tn, unsigned(Dm.U)), 256, 0, st>>>(
+    launch_pdl(k_phi_kz<128>, dim3(Dm.Tn, unsigned(Dm.U)), 256, 0, st,
         static_cast<const __nv_bfloat16*>(k), wb.kfb, wb.z3b, Dm.N, Dm.Tn, Dm.phi, Dm.N_valid);
   else
-    k_phi_kz<64><<<dim3(Dm.Tn, unsigned(Dm.U)), 256, 0, st>>>(
+    launch_pdl(k_phi_kz<64>, dim3(Dm.Tn, unsigned(Dm.U)), 256, 0, st,
         static_cast<const __nv_bfloat16*>(k), wb.kfb, wb.z3b, Dm.N, Dm.Tn, Dm.phi, Dm.N_valid);
   check_launch("k_phi_kz", st);
   // h_j = phi(K_j)^T V_j: batch = every key block, M = N = d, K = 64 tokens
@@ -275,7 +277,8 @@ void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, 
   g.c_batch = (long long)d * d;
   g.name = "gemm_dw";
   launch_gemm(g, st);
-  k_reduce_dw<<<dim3((d * d + 255) / 256, unsigned(Dm.H)), 256, 0, st>>>(wb.dwp, chunks, Dm.B, Dm.H, d * d, dw);
+  launch_pdl(k_reduce_dw, dim3((d * d + 255) / 256, unsigned(Dm.H)), 256, 0, st, (const float*)wb.dwp, chunks,
+             (long long)Dm.B, (long long)Dm.H, d * d, dw);
   check_launch("k_reduce_dw", st);
 }
 

@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(224, 1)
     k_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
            const __grid_constant__ CUtensorMap tc_out,
            OutT* __restrict__ C, int M, int N, int K, int batch, long long c_batch, int ldc) {
+  pdl_entry();  // launched by launch_pdl
   using L = GemmSmem<BM, BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -270,7 +271,7 @@ void launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
   static int sms = 0;
   if (!sms) SLAB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
   const int grid = int(std::min<long long>(tiles, sms));
-  kern<<<grid, 224, smem, st>>>(ta, tb, tcm, static_cast<OutT*>(g.C), g.M, g.N, g.K, g.batch, g.c_batch, g.ldc);
+  launch_pdl(kern, grid, 224, smem, st, ta, tb, tcm, static_cast<OutT*>(g.C), g.M, g.N, g.K, g.batch, g.c_batch, g.ldc);
   check_launch(g.name ? g.name : "k_gemm", st);
 }
 
