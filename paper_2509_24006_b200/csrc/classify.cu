@@ -273,6 +273,9 @@ __global__ void k_classify(const R* __restrict__ scores, int Tm,
 // (weight desc, column asc), with the distance >= EPL passes done by shuffles.  No block
 // barriers: a whole row is one warp's registers.
 // ---------------------------------------------------------------------------------------
+#ifndef SLAB_CLASSIFY_SELECT
+#define SLAB_CLASSIFY_SELECT 1  // 1: quickselect of the two rank thresholds; 0: full bitonic sort
+#endif
 template <typename R, int EPL>
 __global__ void __launch_bounds__(256) k_classify_warp(const R* __restrict__ scores, long long rows,
                                                        int Tn, int n1, int n_neg,
@@ -283,10 +286,13 @@ __global__ void __launch_bounds__(256) k_classify_warp(const R* __restrict__ sco
   pdl_entry();  // launched by launch_pdl
   constexpr int P2 = 32 * EPL;
   __shared__ int8_t slab[8][P2];
+  __shared__ R ebuf[8][P2 + 1];  // the 8 rows' exponentials for the sequential normaliser
+  __shared__ R rsum[8];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const long long row = (long long)blockIdx.x * 8 + warp;
-  if (row >= rows) return;
-  const R* srow = scores + row * Tn;
+  const long long row0 = (long long)blockIdx.x * 8;
+  const long long row = row0 + warp;
+  const bool active = row < rows;
+  const R* srow = scores + (active ? row : 0) * Tn;
   R key[EPL];
   int idx[EPL];
   R m = -R(INFINITY);
@@ -303,16 +309,21 @@ __global__ void __launch_bounds__(256) k_classify_warp(const R* __restrict__ sco
   }
 #pragma unroll
   for (int r = 0; r < EPL; ++r) key[r] = lane * EPL + r < Tn ? exp_r(key[r] - m) : R(0);
-  // sequential ascending-j normaliser (mask.cpp:73-77): lane L continues lane L-1's sum
-  R sum = R(0);
-  for (int L = 0; L < 32; ++L) {
-    if (lane == L) {
+  // sequential ascending-j normaliser (mask.cpp:73-77).  The chain of Tn dependent adds is
+  // inherent (bit-exact order); lanes 0-7 of warp 0 run the block's 8 chains side by side
+  // from shared memory instead of every warp predicating its chain through all 32 lanes.
 #pragma unroll
-      for (int r = 0; r < EPL; ++r)
-        if (lane * EPL + r < Tn) sum = add_rn(sum, key[r]);
-    }
-    sum = __shfl_sync(0xffffffffu, sum, L);
+  for (int r = 0; r < EPL; ++r) ebuf[warp][lane * EPL + r] = key[r];
+  __syncthreads();
+  if (warp == 0 && lane < 8) {
+    R acc = R(0);
+    if (row0 + lane < rows)
+      for (int j = 0; j < Tn; ++j) acc = add_rn(acc, ebuf[lane][j]);
+    rsum[lane] = acc;
   }
+  __syncthreads();
+  if (!active) return;
+  const R sum = rsum[warp];
 #pragma unroll
   for (int r = 0; r < EPL; ++r) {
     const int j = lane * EPL + r;
@@ -324,6 +335,98 @@ __global__ void __launch_bounds__(256) k_classify_warp(const R* __restrict__ sco
       key[r] = -R(1);  // pads sort after every weight (weights are >= 0)
     }
   }
+#if SLAB_CLASSIFY_SELECT
+  // Ranks by selection instead of a full sort.  rank(e) = #(w > w_e) + #(w == w_e, j < j_e) is
+  // the position in stable_sort's (weight desc, column asc) order (mask.cpp:91-119), so with
+  // v1 = the weight at rank n1 - 1 and v2 = the weight at rank Tn - n_neg,
+  //   critical   <=> w > v1, or w == v1 and #(w > v1) + (ties of v1 before e) < n1,
+  //   negligible <=> w < v2, or w == v2 and #(w > v2) + (ties of v2 before e) >= Tn - n_neg.
+  // Each threshold is a quickselect over exact comparisons (pads carry -1 and never qualify).
+  (void)idx;
+  constexpr unsigned FULL = 0xffffffffu;
+  auto select_desc = [&](int K) -> R {  // the weight at 0-based rank K
+    R lo = R(-1), hi = R(INFINITY);     // candidates: lo < w < hi
+    int k = K;
+    for (int it = 0;; ++it) {
+      int mine = -1;
+      R mv = R(0);
+#pragma unroll
+      for (int r = EPL - 1; r >= 0; --r)
+        if (key[r] > lo && key[r] < hi) {
+          mine = r;
+          mv = key[r];
+        }
+      const unsigned has = __ballot_sync(FULL, mine >= 0);
+      if (has == 0u) return R(-1);  // no candidate left (only with non-finite weights): never hang
+      const int rot = (it * 11) & 31;
+      const unsigned rm = rot ? (has >> rot) | (has << (32 - rot)) : has;
+      const R pivot = __shfl_sync(FULL, mv, (__ffs(rm) - 1 + rot) & 31);
+      int g = 0, e = 0;
+#pragma unroll
+      for (int r = 0; r < EPL; ++r) {
+        const bool c = key[r] > lo && key[r] < hi;
+        g += c && key[r] > pivot;
+        e += c && key[r] == pivot;
+      }
+      g = __reduce_add_sync(FULL, g);
+      e = __reduce_add_sync(FULL, e);
+      if (k < g) {
+        lo = pivot;
+      } else if (k < g + e) {
+        return pivot;
+      } else {
+        k -= g + e;
+        hi = pivot;
+      }
+    }
+  };
+  // #(w > v) over the row, and this lane's count of ties w == v before its first element
+  auto ties_before = [&](R v, int& gt) -> int {
+    int g = 0, t = 0;
+#pragma unroll
+    for (int r = 0; r < EPL; ++r) {
+      g += key[r] > v;
+      t += key[r] == v;
+    }
+    gt = __reduce_add_sync(FULL, g);
+    int x = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(FULL, x, o);
+      if (lane >= o) x += y;
+    }
+    return x - t;
+  };
+  int8_t* lab = slab[warp];
+  bool crit[EPL], negl[EPL];
+#pragma unroll
+  for (int r = 0; r < EPL; ++r) crit[r] = negl[r] = false;
+  if (n1 > 0) {
+    const R v1 = select_desc(n1 - 1);
+    int gt1;
+    int run = ties_before(v1, gt1);
+#pragma unroll
+    for (int r = 0; r < EPL; ++r) {
+      if (key[r] == v1) crit[r] = gt1 + run++ < n1;
+      else crit[r] = key[r] > v1;
+    }
+  }
+  if (n_neg > 0) {
+    const R v2 = select_desc(Tn - n_neg);
+    int gt2;
+    int run = ties_before(v2, gt2);
+#pragma unroll
+    for (int r = 0; r < EPL; ++r) {
+      if (key[r] == v2) negl[r] = gt2 + run++ >= Tn - n_neg;
+      else negl[r] = key[r] < v2;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < EPL; ++r) {
+    const int j = lane * EPL + r;
+    if (j < Tn) lab[j] = crit[r] ? int8_t(1) : (negl[r] ? int8_t(-1) : int8_t(0));
+  }
+#else
 #pragma unroll
   for (int k = 2; k <= P2; k <<= 1) {
 #pragma unroll
@@ -367,6 +470,7 @@ __global__ void __launch_bounds__(256) k_classify_warp(const R* __restrict__ sco
     const int e = lane * EPL + r;  // rank
     if (idx[r] < Tn) lab[idx[r]] = e < n1 ? int8_t(1) : (e >= Tn - n_neg ? int8_t(-1) : int8_t(0));
   }
+#endif
   __syncwarp();
   int8_t* lrow = labels + row * Tn;
   for (int j = lane; j < Tn; j += 32) lrow[j] = lab[j];
