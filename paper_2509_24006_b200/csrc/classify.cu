@@ -344,39 +344,43 @@ __global__ void __launch_bounds__(256) k_classify_warp(const R* __restrict__ sco
   // Each threshold is a quickselect over exact comparisons (pads carry -1 and never qualify).
   (void)idx;
   constexpr unsigned FULL = 0xffffffffu;
+  // candidates are a per-lane bit mask over the lane's EPL weights; pivots come from shared memory
+#pragma unroll
+  for (int r = 0; r < EPL; ++r) ebuf[warp][lane * EPL + r] = key[r];
+  __syncwarp();
+  const R* prow = &ebuf[warp][lane * EPL];
+  unsigned vmask = 0u;
+#pragma unroll
+  for (int r = 0; r < EPL; ++r) vmask |= (lane * EPL + r < Tn ? 1u : 0u) << r;
   auto select_desc = [&](int K) -> R {  // the weight at 0-based rank K
-    R lo = R(-1), hi = R(INFINITY);     // candidates: lo < w < hi
+    unsigned cm = vmask;
     int k = K;
     for (int it = 0;; ++it) {
-      int mine = -1;
-      R mv = R(0);
-#pragma unroll
-      for (int r = EPL - 1; r >= 0; --r)
-        if (key[r] > lo && key[r] < hi) {
-          mine = r;
-          mv = key[r];
-        }
-      const unsigned has = __ballot_sync(FULL, mine >= 0);
+      const unsigned has = __ballot_sync(FULL, cm != 0u);
       if (has == 0u) return R(-1);  // no candidate left (only with non-finite weights): never hang
       const int rot = (it * 11) & 31;
       const unsigned rm = rot ? (has >> rot) | (has << (32 - rot)) : has;
-      const R pivot = __shfl_sync(FULL, mv, (__ffs(rm) - 1 + rot) & 31);
-      int g = 0, e = 0;
+      const int src = (__ffs(rm) - 1 + rot) & 31;
+      R mv = R(0);
+      if (lane == src) mv = prow[__ffs(cm) - 1];
+      const R pivot = __shfl_sync(FULL, mv, src);
+      unsigned gm = 0u, em = 0u;
 #pragma unroll
       for (int r = 0; r < EPL; ++r) {
-        const bool c = key[r] > lo && key[r] < hi;
-        g += c && key[r] > pivot;
-        e += c && key[r] == pivot;
+        gm |= (key[r] > pivot ? 1u : 0u) << r;
+        em |= (key[r] == pivot ? 1u : 0u) << r;
       }
-      g = __reduce_add_sync(FULL, g);
-      e = __reduce_add_sync(FULL, e);
+      gm &= cm;
+      em &= cm;
+      const int g = __reduce_add_sync(FULL, __popc(gm));
+      const int e = __reduce_add_sync(FULL, __popc(em));
       if (k < g) {
-        lo = pivot;
+        cm = gm;
       } else if (k < g + e) {
         return pivot;
       } else {
         k -= g + e;
-        hi = pivot;
+        cm &= ~(gm | em);
       }
     }
   };
