@@ -194,7 +194,7 @@ void unpad_rows(const Dims& D, void* dst, const void* src, size_t row_bytes, cud
 // latency- and FP64-bound and leaves most of each SM idle, runs on the caller's stream.
 struct SideStream {
   cudaStream_t s = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr;
 };
 
 SideStream& side_stream() {
@@ -206,6 +206,7 @@ SideStream& side_stream() {
     SLAB_CUDA(cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking));
     SLAB_CUDA(cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming));
     SLAB_CUDA(cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming));
+    SLAB_CUDA(cudaEventCreateWithFlags(&x.join2, cudaEventDisableTiming));
   }
   return x;
 }
@@ -415,6 +416,7 @@ int sla_b200_backward_ex(const sla_b200_problem* p, const void* q, const void* k
         side.s = ss.s;
         side.fork = ss.fork;
         side.join = ss.join;
+        side.join2 = ss.join2;
       }
       fast_backward(D, q, k, v, w, o_s, o_l, lse, d_out, dq, dk, dv, dw, s, wb, st, side);
     }
