@@ -194,7 +194,7 @@ void unpad_rows(const Dims& D, void* dst, const void* src, size_t row_bytes, cud
 // latency- and FP64-bound and leaves most of each SM idle, runs on the caller's stream.
 struct SideStream {
   cudaStream_t s = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr, mid = nullptr, join3 = nullptr;
 };
 
 SideStream& side_stream() {
@@ -207,6 +207,8 @@ SideStream& side_stream() {
     SLAB_CUDA(cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming));
     SLAB_CUDA(cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming));
     SLAB_CUDA(cudaEventCreateWithFlags(&x.join2, cudaEventDisableTiming));
+    SLAB_CUDA(cudaEventCreateWithFlags(&x.mid, cudaEventDisableTiming));
+    SLAB_CUDA(cudaEventCreateWithFlags(&x.join3, cudaEventDisableTiming));
   }
   return x;
 }
@@ -417,6 +419,8 @@ int sla_b200_backward_ex(const sla_b200_problem* p, const void* q, const void* k
         side.fork = ss.fork;
         side.join = ss.join;
         side.join2 = ss.join2;
+        side.mid = ss.mid;
+        side.join3 = ss.join3;
       }
       fast_backward(D, q, k, v, w, o_s, o_l, lse, d_out, dq, dk, dv, dw, s, wb, st, side);
     }

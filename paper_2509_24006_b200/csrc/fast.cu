@@ -212,6 +212,9 @@ void fast_forward(const Dims& Dm, const void* q, const void* k, const void* v, c
   launch_attn_fwd(Dm, q, k, v, w, o, o_s, o_l, lse, s, st);
 }
 
+#ifndef SLAB_AGG_SIDE
+#define SLAB_AGG_SIDE 0  // measured slower: 2.81 ms per step against 2.73-2.78 (rows loses SMs, cols waits)
+#endif
 #ifndef SLAB_DW_SIDE
 #define SLAB_DW_SIDE 1  // measured: 2.72-2.75 ms per step against 2.76-2.78 with dW on the main stream
 #endif
@@ -220,6 +223,29 @@ void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, 
                    void* dq, void* dk, void* dv, float* dw, const StateBufs& s,
                    const WorkBufs& wb, cudaStream_t st, const SideFork& side) {
   const int d = Dm.d;
+  auto launch_agg = [&](cudaStream_t as) {
+    // dH_agg = M0^T dH (A = M0 read M-major), dZ_agg
+    GemmArgs a{};
+    a.A = s.M0;
+    a.B = wb.hb;
+    a.C = wb.hab;
+    a.batch = int(Dm.U);
+    a.M = Dm.Tn;
+    a.N = d * d;
+    a.K = Dm.Tm;
+    a.a_mn = true;
+    a.b_mn = true;
+    a.out_f32 = false;
+    a.lda = m0_stride(Dm);
+    a.ldb = (long long)d * d;
+    a.ldc = (long long)d * d;
+    a.a_batch = (long long)Dm.Tm * m0_stride(Dm);
+    a.b_batch = (long long)Dm.Tm * d * d;
+    a.c_batch = (long long)Dm.Tn * d * d;
+    a.name = "gemm_aggregate_t";
+    launch_gemm(a, as);
+    aggregate_vec_tc(Dm, s, wb, true, wb.gZa, "gemm_aggregate_dz", as);  // gZa: [U, Tn, 3d]
+  };
   // dW = O^l^T dO per head, split-K over row chunks of each unit, then reduced over chunks + batch
   auto launch_dw = [&](cudaStream_t ds) {
     const long long KC = 64LL * dw_chunk_tiles(Dm);
@@ -264,28 +290,20 @@ void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, 
   // row phase: the linear branch (dH_i reusing the forward's h scratch, dZ_i, D^s, dQ^phi),
   // then the sparse dQ over critical pairs with dq_total = J_phi^T dQ^phi + dQ
   launch_bwd_lin(Dm, q, w, o_s, o_l, d_out, s, wb.hb, wb.z3b, wb.Ds, wb.dqphi, st);
+  // dH_agg = M0^T dH and dZ_agg need only k_bwd_lin's dH / dZ: with a side stream they run
+  // beside the rows pass (joined before the columns pass)
+  const bool agg_side = SLAB_AGG_SIDE && side.s;
+  if (agg_side) {
+    SLAB_CUDA(cudaEventRecord(side.mid, st));
+    SLAB_CUDA(cudaStreamWaitEvent(side.s, side.mid, 0));
+    launch_agg(side.s);
+    SLAB_CUDA(cudaEventRecord(side.join3, side.s));
+  }
   launch_bwd_rows(Dm, q, k, v, lse, d_out, dq, s, wb.Ds, wb.dqphi, st);
-  // dH_agg = M0^T dH (A = M0 read M-major), dZ_agg
-  GemmArgs a{};
-  a.A = s.M0;
-  a.B = wb.hb;
-  a.C = wb.hab;
-  a.batch = int(Dm.U);
-  a.M = Dm.Tn;
-  a.N = d * d;
-  a.K = Dm.Tm;
-  a.a_mn = true;
-  a.b_mn = true;
-  a.out_f32 = false;
-  a.lda = m0_stride(Dm);
-  a.ldb = (long long)d * d;
-  a.ldc = (long long)d * d;
-  a.a_batch = (long long)Dm.Tm * m0_stride(Dm);
-  a.b_batch = (long long)Dm.Tm * d * d;
-  a.c_batch = (long long)Dm.Tn * d * d;
-  a.name = "gemm_aggregate_t";
-  launch_gemm(a, st);
-  aggregate_vec_tc(Dm, s, wb, true, wb.gZa, "gemm_aggregate_dz", st);  // gZa: [U, Tn, 3d]
+  if (agg_side)
+    SLAB_CUDA(cudaStreamWaitEvent(st, side.join3, 0));
+  else
+    launch_agg(st);
   // columns pass: dk_total, dv
   if (side.s) SLAB_CUDA(cudaStreamWaitEvent(st, side.join, 0));
   launch_bwd_cols(Dm, q, k, v, lse, d_out, dk, dv, s, wb.hab, wb.gZa, wb.Ds, st);

@@ -66,7 +66,7 @@ void fast_forward(const Dims& D, const void* q, const void* k, const void* v, co
 // there, concurrent with latency-bound kernels on the caller's stream (s == nullptr: none).
 struct SideFork {
   cudaStream_t s = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr, mid = nullptr, join3 = nullptr;
 };
 void fast_backward(const Dims& D, const void* q, const void* k, const void* v, const void* w,
                    const void* o_s, const void* o_l, const float* lse, const void* d_out,
