@@ -37,7 +37,11 @@ struct GemmSmem {
 // Persistent: each CTA walks tiles blockIdx.x, +gridDim.x, ...; the smem ring runs across tile
 // boundaries and the TMEM accumulator is double-buffered (2 x BN columns) so the epilogue of
 // tile t overlaps the main loop of tile t+1.
-template <int BM, int BN, bool A_MN, bool B_MN, typename OutT>
+// MC: 2-CTA clusters whose CTAs take the two M-halves of a 2*BM x BN tile pair; each CTA
+// loads half of the pair's B k-block and multicasts it to both, so B crosses L2 -> SM once per
+// pair (the aggregation GEMMs are L2-bandwidth-bound).  A stage is refilled only after BOTH
+// CTAs' MMAs released it (every MMA commit arrives on the empty barrier of both CTAs).
+template <int BM, int BN, bool A_MN, bool B_MN, typename OutT, bool MC = false>
 __global__ void __launch_bounds__(224, 1)
     k_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
            const __grid_constant__ CUtensorMap tc_out,
@@ -55,15 +59,20 @@ __global__ void __launch_bounds__(224, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = (K + kBK - 1) / kBK;
   const int tiles_n = N / BN, tiles_m = (M + BM - 1) / BM;
-  const long long total = (long long)tiles_n * tiles_m * batch;
+  // work units: tiles, or (MC) pairs of M-adjacent tiles, one per CTA of the cluster
+  const int rank = MC ? int(tc::cluster_rank()) : 0;
+  const long long unit0 = MC ? blockIdx.x / 2 : blockIdx.x;
+  const long long ustep = MC ? gridDim.x / 2 : gridDim.x;
+  const int units_m = MC ? tiles_m / 2 : tiles_m;
+  const long long total = (long long)tiles_n * units_m * batch;
 
   if (warp == 0) {
     if (lane == 0) {
       tc::tma_prefetch(&ta);
       tc::tma_prefetch(&tb);
       for (int s = 0; s < kStages; ++s) {
-        tc::mbar_init(&full[s], 2);  // one arrive.expect_tx per producer
-        tc::mbar_init(&empty[s], 1);
+        tc::mbar_init(&full[s], 2);              // one arrive.expect_tx per producer
+        tc::mbar_init(&empty[s], MC ? 2 : 1);    // (MC) both CTAs' MMA commits
       }
       for (int s = 0; s < 2; ++s) {
         tc::mbar_init(&tfull[s], 1);
@@ -76,20 +85,21 @@ __global__ void __launch_bounds__(224, 1)
   }
   tc::tc_fence_before();
   __syncthreads();
+  if (MC) tc::cluster_sync();  // the peer's barriers are initialised before any multicast / remote arrive
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   auto coords = [&](long long t, int& n0, int& m0, int& b) {
     n0 = int(t % tiles_n) * BN;
-    m0 = int((t / tiles_n) % tiles_m) * BM;
-    b = int(t / ((long long)tiles_n * tiles_m));
+    m0 = (MC ? 2 * int((t / tiles_n) % units_m) + rank : int((t / tiles_n) % units_m)) * BM;
+    b = int(t / ((long long)tiles_n * units_m));
   };
 
   if (warp == 0 || warp == 6) {
     if (lane == 0) {
       const bool loads_a = warp == 0;
       int kc = 0;  // k-blocks issued by this CTA (ring position)
-      for (long long t = blockIdx.x; t < total; t += gridDim.x) {
+      for (long long t = unit0; t < total; t += ustep) {
         int n0, m0, b;
         coords(t, n0, m0, b);
         for (int kb = 0; kb < nk; ++kb, ++kc) {
@@ -108,7 +118,12 @@ __global__ void __launch_bounds__(224, 1)
             }
           } else {
             tc::mbar_expect_tx(&full[s], L::kB);
-            if (B_MN) {
+            if (MC) {  // my half of the pair's B chunks, to both CTAs
+              static_assert(!MC || (B_MN && BN % 128 == 0), "MC: N-major B, even chunk count");
+#pragma unroll
+              for (int c = rank * (BN / 128); c < (rank + 1) * (BN / 128); ++c)
+                tc::tma_load_3d_mc(sb + c * 8192, &tb, &full[s], n0 + 64 * c, k0, b, uint16_t(3));
+            } else if (B_MN) {
 #pragma unroll
               for (int c = 0; c < BN / 64; ++c) tc::tma_load_3d(sb + c * 8192, &tb, &full[s], n0 + 64 * c, k0, b);
             } else {
@@ -121,7 +136,7 @@ __global__ void __launch_bounds__(224, 1)
   } else if (warp == 1) {
     constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, A_MN, B_MN);
     int kc = 0, lt = 0;
-    for (long long t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+    for (long long t = unit0; t < total; t += ustep, ++lt) {
       const int ab = lt & 1;
       tc::mbar_wait(&tempty[ab], ((lt >> 1) & 1) ^ 1);
       tc::tc_fence_after();
@@ -139,7 +154,10 @@ __global__ void __launch_bounds__(224, 1)
           for (int kk = 0; kk < kBK / 16; ++kk)
             tc::mma_bf16_w(acc, tc::desc_add(a0, A_MN ? kk * 2048 : kk * 32), tc::desc_add(b0, B_MN ? kk * 2048 : kk * 32),
                            idesc, (kb | kk) != 0);
-          tc::mma_commit_w(&empty[s]);
+          if (MC)
+            tc::mma_commit_mc_w(&empty[s], uint16_t(3));
+          else
+            tc::mma_commit_w(&empty[s]);
           if (kb == nk - 1) tc::mma_commit_w(&tfull[ab]);
         }
       }
@@ -148,7 +166,7 @@ __global__ void __launch_bounds__(224, 1)
     // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
     const int q = warp & 3;
     int lt = 0;
-    for (long long t = blockIdx.x; t < total; t += gridDim.x, ++lt) {
+    for (long long t = unit0; t < total; t += ustep, ++lt) {
       int n0, m0, b;
       coords(t, n0, m0, b);
       const int ab = lt & 1;
@@ -229,6 +247,7 @@ __global__ void __launch_bounds__(224, 1)
   if (threadIdx.x == 64) tc::bulk_wait_read<0>();
   tc::tc_fence_before();
   __syncthreads();
+  if (MC) tc::cluster_sync();  // no remote arrive may target a CTA that has exited
   if (warp == 0) tc::tmem_dealloc<2 * BN>(tmem);
 }
 
@@ -249,7 +268,7 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-template <int BM, int BN, bool A_MN, bool B_MN, typename OutT>
+template <int BM, int BN, bool A_MN, bool B_MN, typename OutT, bool MC = false>
 void launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
   CUtensorMap ta, tb;
   // A: K-major -> tensor [batch][M][K], box [BM][64]; M-major -> [batch][K][M], box [64][64]
@@ -264,19 +283,50 @@ void launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
   CUtensorMap tcm{};
   if (sizeof(OutT) == 2)  // output boxes [BM rows][64 cols] of C [batch][M][ldc]
     make_tmap_bf16(&tcm, g.C, g.N, g.M, g.batch, g.ldc, g.c_batch, BM);
-  auto kern = k_gemm<BM, BN, A_MN, B_MN, OutT>;
+  auto kern = k_gemm<BM, BN, A_MN, B_MN, OutT, MC>;
   constexpr int smem = GemmSmem<BM, BN>::kBytes;
   SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const long long tiles = (long long)(g.N / BN) * ((g.M + BM - 1) / BM) * g.batch;
   static int sms = 0;
   if (!sms) SLAB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-  const int grid = int(std::min<long long>(tiles, sms));
-  launch_pdl(kern, grid, 224, smem, st, ta, tb, tcm, static_cast<OutT*>(g.C), g.M, g.N, g.K, g.batch, g.c_batch, g.ldc);
+  if (MC) {  // 2-CTA clusters, one tile pair per cluster at a time
+    const int grid = int(std::min<long long>(tiles, sms)) & ~1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(224);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = SLAB_PDL;
+    cfg.attrs = attr;
+    cfg.numAttrs = 2;
+    cudaLaunchKernelEx(&cfg, kern, ta, tb, tcm, static_cast<OutT*>(g.C), g.M, g.N, g.K, g.batch, g.c_batch, g.ldc);
+  } else {
+    const int grid = int(std::min<long long>(tiles, sms));
+    launch_pdl(kern, grid, 224, smem, st, ta, tb, tcm, static_cast<OutT*>(g.C), g.M, g.N, g.K, g.batch, g.c_batch, g.ldc);
+  }
   check_launch(g.name ? g.name : "k_gemm", st);
 }
 
+#ifndef SLAB_GEMM_MC
+#define SLAB_GEMM_MC 1  // measured: gemm_aggregate_t 0.098 -> 0.093 ms, gemm_aggregate 0.098 -> 0.097
+#endif
 template <int BM, int BN, typename OutT>
 void dispatch_major(const GemmArgs& g, cudaStream_t st) {
+  // B multicast across 2-CTA clusters where the tile grid pairs up (the aggregation GEMMs)
+  if constexpr (BM == 128 && BN == 256 && sizeof(OutT) == 2) {
+    const int tiles_m = (g.M + BM - 1) / BM;
+    if (SLAB_GEMM_MC && g.b_mn && tiles_m % 2 == 0 && g.M % BM == 0) {
+      if (g.a_mn) launch_gemm_t<BM, BN, true, true, OutT, true>(g, st);
+      else launch_gemm_t<BM, BN, false, true, OutT, true>(g, st);
+      return;
+    }
+  }
   if (g.a_mn && g.b_mn) launch_gemm_t<BM, BN, true, true, OutT>(g, st);
   else if (g.a_mn) launch_gemm_t<BM, BN, true, false, OutT>(g, st);
   else if (g.b_mn) launch_gemm_t<BM, BN, false, true, OutT>(g, st);
