@@ -655,11 +655,43 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     // dq_done fired), then finish row-wise with 4 threads per query row.  For the softmax
     // feature map <phi(q), dQ^phi> = D^l - (D^l/den) den = 0 exactly (O^l = phi(q) H / den), so
     // the Jacobian reduces to phi(q) * dQ^phi.
+    // phi(q) of this thread's quarter row first: it needs only Q_i, so it runs while the last
+    // dQ^T MMAs drain.  Chunks are held in the rotated order the row-wise pass walks
+    // (slot cc0 <-> columns c0 + ((cc0 + 8 sub) & (DQ - 1))), which spreads its reads of the
+    // transposed tile over the banks.
+    const int rq = tid >> 2, sub = tid & 3, c0 = sub * DQ;
+    auto rot = [&](int cc0) { return (cc0 + 8 * sub) & (DQ - 1); };
+    float x[DQ];
+#pragma unroll
+    for (int cc0 = 0; cc0 < DQ; cc0 += 8) {
+      float t8[8];
+      unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(rq, c0 + rot(cc0))), t8);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) x[cc0 + e] = t8[e];
+    }
+    if (p.phi == 2) {  // phi(q) in place, one exp per element
+      float mx = -INFINITY;
+#pragma unroll
+      for (int e = 0; e < DQ; ++e) mx = fmaxf(mx, x[e]);
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      float se = 0.f;
+#pragma unroll
+      for (int e = 0; e < DQ; ++e) {
+        x[e] = __expf(x[e] - mx);
+        se += x[e];
+      }
+      se += __shfl_xor_sync(0xffffffffu, se, 1);
+      se += __shfl_xor_sync(0xffffffffu, se, 2);
+      const float inv = 1.f / se;
+#pragma unroll
+      for (int e = 0; e < DQ; ++e) x[e] *= inv;
+    }
     tc::mbar_wait(dq_done, 0);
     tc::tc_fence_after();
     ts_mark(dbg && threadIdx.x == 64, 120);
     cta_mark(threadIdx.x == 64, 2);
-    constexpr int TP = D + 1;  // with the chunk rotation below: conflict-free row-wise reads
+    constexpr int TP = D + 1;  // with the chunk rotation: conflict-free row-wise reads
     float* tq = reinterpret_cast<float*>(sK);
     {
       const int acol = D == 128 ? 32 * q4 + lane : 16 * q4 + lane;
@@ -674,46 +706,15 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     }
     named_sync(1, 256);
     {
-      const int rq = tid >> 2, sub = tid & 3, c0 = sub * DQ;
       const long long grow = (long long)row0 + rq;
-      float x[DQ];
-#pragma unroll
-      for (int cc = 0; cc < DQ; cc += 8) {
-        float t8[8];
-        unpack8(*reinterpret_cast<const uint4*>(sQ + tile_off(rq, c0 + cc)), t8);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) x[cc + e] = t8[e];
-      }
-      if (p.phi == 2) {  // phi(q) in place, one exp per element
-        float mx = -INFINITY;
-#pragma unroll
-        for (int e = 0; e < DQ; ++e) mx = fmaxf(mx, x[e]);
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        float se = 0.f;
-#pragma unroll
-        for (int e = 0; e < DQ; ++e) {
-          x[e] = __expf(x[e] - mx);
-          se += x[e];
-        }
-        se += __shfl_xor_sync(0xffffffffu, se, 1);
-        se += __shfl_xor_sync(0xffffffffu, se, 2);
-        const float inv = 1.f / se;
-#pragma unroll
-        for (int e = 0; e < DQ; ++e) x[e] *= inv;
-      }
 #pragma unroll
       for (int cc0 = 0; cc0 < DQ; cc0 += 8) {
-        const int cc = (cc0 + 8 * sub) & (DQ - 1);  // rotated chunk order (bank spread)
-        const int col = c0 + cc;
+        const int col = c0 + rot(cc0);
         float g[8], o[8];
         unpack8(gq[cc0 / 8], g);
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
-          float xe = x[0];
-#pragma unroll
-          for (int k = 0; k < DQ; k += 8)  // x[cc + e] with cc dynamic: select among chunks
-            if (k == cc) xe = x[k + e];
+          const float xe = x[cc0 + e];
           float jg;
           if (p.phi == 2) jg = xe * g[e];
           else if (p.phi == 0) jg = xe >= 0.f ? g[e] : __expf(xe) * g[e];
