@@ -444,20 +444,34 @@ __global__ void __launch_bounds__(kColsThreads, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(kf_ready);
     }
+    // ---- transpose dK^T, dV^T, dK^phi^T (lane = column a) into smem [key row][a].  dK^T is final
+    // at acc_done, so it goes first, while the linear MMAs still run; its region avoids the ring
+    // slot holding dH_agg (item 2 np), which those MMAs read until all_done.
+    constexpr int TP = D + 1;  // with the chunk rotation below: conflict-free row-wise reads
+    const int hs = (2 * np) % RS;
+    const bool tk_low = has_lin && (hs == 2 || hs == 3);
+    float* tbase = reinterpret_cast<float*>(sRing);
+    float* tk = tk_low ? tbase : tbase + 2 * 64 * TP;
+    float* tv = tk_low ? tbase + 64 * TP : tbase;
+    float* tkp = tk_low ? tbase + 2 * 64 * TP : tbase + 64 * TP;
+    const int acol = D == 128 ? 32 * q4 + lane : 16 * q4 + lane;
+    const bool avalid = D == 128 || lane < 16;
+    {
+      tc::tc_fence_after();
+      uint32_t a[32];
+      if (np > 0) tc::tmem_ld32(tDKT + lane_base + 32 * grp, a);
+      tc::tmem_ld_wait();
+      if (avalid) {
+#pragma unroll
+        for (int e = 0; e < 32; ++e) tk[(32 * grp + e) * TP + acol] = np > 0 ? __uint_as_float(a[e]) : 0.f;
+      }
+    }
     ts_mark(dbg && threadIdx.x == 64, 121);
     tc::mbar_wait(all_done, 0);
     tc::tc_fence_after();
     ts_mark(dbg && threadIdx.x == 64, 122);
-    // ---- transpose dK^T, dV^T, dK^phi^T (lane = column a) into smem [key row][a]
-    constexpr int TP = D + 1;  // with the chunk rotation below: conflict-free row-wise reads
-    float* tk = reinterpret_cast<float*>(sRing);
-    float* tv = tk + 64 * TP;
-    float* tkp = tv + 64 * TP;
     {
-      const int acol = D == 128 ? 32 * q4 + lane : 16 * q4 + lane;
-      const bool avalid = D == 128 || lane < 16;
-      uint32_t a[32], b[32], e3[32];
-      if (np > 0) tc::tmem_ld32(tDKT + lane_base + 32 * grp, a);
+      uint32_t b[32], e3[32];
       if (np > 0 || has_lin) tc::tmem_ld32(tDVT + lane_base + 32 * grp, b);
       if (has_lin) tc::tmem_ld32(tKPT + lane_base + 32 * grp, e3);
       tc::tmem_ld_wait();
@@ -465,7 +479,6 @@ __global__ void __launch_bounds__(kColsThreads, 1)
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
           const int kr = 32 * grp + e;
-          tk[kr * TP + acol] = np > 0 ? __uint_as_float(a[e]) : 0.f;
           tv[kr * TP + acol] = (np > 0 || has_lin) ? __uint_as_float(b[e]) : 0.f;
           tkp[kr * TP + acol] = has_lin ? __uint_as_float(e3[e]) : 0.f;
         }
