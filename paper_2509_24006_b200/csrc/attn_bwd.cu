@@ -27,8 +27,10 @@ namespace {
 // full / empty barriers, so dS(t+1) is written once dK^T(t) has read dS(t) and dK^T(t+1) queues
 // behind dV^T(t) without a gap.  Measured (C3, k_bwd_cols ms): 4 slots + 2 P/dS buffers 1.008;
 // 5 slots + 1 buffer, dK first 0.890; + P from S before dP lands 0.882.
-#ifndef SLAB_COLS_POLY  // every N-th exponential by ex2_poly; measured: 0 0.869 ms, 2 0.875, 4 0.851
-#define SLAB_COLS_POLY 4
+// every N-th exponential by tc::ex2_poly.  Measured before the P / dS barrier split: 0 0.869 ms,
+// 2 0.875, 4 0.851; after it: 0 0.840, 3 0.838, 4 0.842, 8 0.847 -- no gain, so off
+#ifndef SLAB_COLS_POLY
+#define SLAB_COLS_POLY 0
 #endif
 template <int D>
 struct ColsLayout {
