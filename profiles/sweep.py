@@ -4,12 +4,13 @@ same shape, plus the configs[4] shape (B=8, H=40, N=75648) for SLA alone.
 
     python profiles/sweep.py [out.md]
 
-Every number is a device time from CUDA events around `iters` back-to-back steps after warm-up,
+Every number is a device time from CUDA events around `iters` (10) back-to-back steps after warm-up,
 inputs resident (> L2 for every N here).  Critical-tile TFLOP/s counts 14 * 64 * 64 * d per
 critical tile (fwd 4 + bwd 10 block matmul-equivalents); dense-equivalent counts 14 N^2 d.
 """
 import os
 import sys
+import time
 
 import torch
 
@@ -69,9 +70,12 @@ def main():
     rows = []
     d = 128
     for N, B, H in ((8192, 1, 12), (32768, 1, 12), (75648, 1, 4)):
+        # SLA first, the (power-hungry) dense run after: a dense run right before the first SLA
+        # case left it up to 25 % slow on some boxes
+        time.sleep(3)  # let the board power average settle after the previous dense run
+        cases = [(kh, *sla_case(B, H, N, d, kh, iters=10)) for kh in (2.5, 5.0, 10.0, 20.0)]
         dense = dense_case(B, H, N, d)
-        for kh in (2.5, 5.0, 10.0, 20.0):
-            ms, crit = sla_case(B, H, N, d, kh)
+        for kh, ms, crit in cases:
             dense_eq = 14.0 * N * N * d * B * H / (ms * 1e-3) / 1e12
             tile_tf = 14.0 * 64 * 64 * d * crit / (ms * 1e-3) / 1e12
             rows.append((N, B * H, kh, ms, dense, dense / ms, dense_eq, tile_tf))
