@@ -142,6 +142,11 @@ __global__ void __launch_bounds__(192, 2)
       tc::mbar_init(o_ready, 4);
       tc::mbar_init(proj_done, 1);
       tc::fence_barrier_init();
+      // Q_i leaves before the TMEM allocation and the block barrier (the producer below
+      // continues with K(0), H_i, ...)
+      tc::mbar_expect_tx(q_full, L::kQ);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) tc::tma_load_3d(sQ + c * 8192, &tmQ, q_full, 64 * c, row0, 0);
     }
     __syncwarp();
     tc::tmem_alloc<256>(tmem_slot);
@@ -159,9 +164,6 @@ __global__ void __launch_bounds__(192, 2)
     // PV(t) still waits for P(t).  H_i's chunks go through the V ring (needed before V(0)),
     // W's chunks through the K ring (needed after the last S).
     if (lane == 0) {
-      tc::mbar_expect_tx(q_full, L::kQ);
-#pragma unroll
-      for (int c = 0; c < NC; ++c) tc::tma_load_3d(sQ + c * 8192, &tmQ, q_full, 64 * c, row0, 0);
       int kit = 0, vit = 0;
       auto take = [&](uint64_t* full, uint64_t* empty, uint8_t* base, int& it, int bytes) -> uint8_t* {
         const int s = it % RS;
