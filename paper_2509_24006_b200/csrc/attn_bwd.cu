@@ -32,6 +32,9 @@ namespace {
 #ifndef SLAB_COLS_POLY
 #define SLAB_COLS_POLY 0
 #endif
+#ifndef SLAB_COLS_DVFIRST  // 1: acc(t) issues dV^T first, P stored first (measured 0.881 vs 0.838 ms)
+#define SLAB_COLS_DVFIRST 0
+#endif
 template <int D>
 struct ColsLayout {
   static constexpr int kT = 64 * D * 2;    // 64-row tile
@@ -228,20 +231,31 @@ __global__ void __launch_bounds__(kColsThreads, 1)
       const int sq = (2 * t) % RS, sdo = (2 * t + 1) % RS;
       const uint64_t dq = tc::desc_add(dRm, sq * L::kSlot), ddo = tc::desc_add(dRm, sdo * L::kSlot);
       const uint64_t dp = dPDm, dd = tc::desc_add(dPDm, 16384);
-      tc::mbar_wait_w(ds_full, t & 1);
-      tc::tc_fence_after();
+      auto dk = [&] {
+        tc::mbar_wait_w(ds_full, t & 1);
+        tc::tc_fence_after();
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk)
-        tc::mma_bf16_w(tDKT, tc::desc_add(dq, kk * 2048), tc::desc_add(dd, kk * 2048), id_acc, (t | kk) != 0);
-      tc::mma_commit_w(ring_empty + sq);  // dO(t+2) refills this slot while dV^T(t) runs
-      tc::mma_commit_w(ds_empty);
-      tc::mbar_wait_w(p_full, t & 1);
-      tc::tc_fence_after();
+        for (int kk = 0; kk < 8; ++kk)
+          tc::mma_bf16_w(tDKT, tc::desc_add(dq, kk * 2048), tc::desc_add(dd, kk * 2048), id_acc, (t | kk) != 0);
+        tc::mma_commit_w(ring_empty + sq);  // dO(t+2) refills this slot
+        tc::mma_commit_w(ds_empty);
+      };
+      auto dv = [&] {
+        tc::mbar_wait_w(p_full, t & 1);
+        tc::tc_fence_after();
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk)
-        tc::mma_bf16_w(tDVT, tc::desc_add(ddo, kk * 2048), tc::desc_add(dp, kk * 2048), id_acc, (t | kk) != 0);
-      tc::mma_commit_w(ring_empty + sdo);
-      tc::mma_commit_w(p_empty);
+        for (int kk = 0; kk < 8; ++kk)
+          tc::mma_bf16_w(tDVT, tc::desc_add(ddo, kk * 2048), tc::desc_add(dp, kk * 2048), id_acc, (t | kk) != 0);
+        tc::mma_commit_w(ring_empty + sdo);
+        tc::mma_commit_w(p_empty);
+      };
+      if (SLAB_COLS_DVFIRST) {
+        dv();
+        dk();
+      } else {
+        dk();
+        dv();
+      }
     };
     // The tensor pipe executes in issue order; the two issuers interleave S/dP(t+1) and acc(t)
     // in whichever order their inputs become ready.
@@ -372,22 +386,34 @@ __global__ void __launch_bounds__(kColsThreads, 1)
       }
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 128 + t);
       const uint32_t prow = tc::smem_u32(sPD);
-      if (t >= 1) tc::mbar_wait(ds_empty, (t - 1) & 1);
-      ts_mark(dbg && threadIdx.x == 64 && t < 16, 144 + t);
+      auto store_ds = [&] {
+        if (t >= 1) tc::mbar_wait(ds_empty, (t - 1) & 1);
+        ts_mark(dbg && threadIdx.x == 64 && t < 16, 144 + t);
 #pragma unroll
-      for (int ch = 0; ch < 4; ++ch)
-        tc::sts_u4(prow + 16384 + tc::sw128_off(rq, 4 * grp + ch), make_uint4(dd[4 * ch], dd[4 * ch + 1], dd[4 * ch + 2], dd[4 * ch + 3]));
-      tc::fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(ds_full);
-      if (t >= 1) tc::mbar_wait(p_empty, (t - 1) & 1);
+        for (int ch = 0; ch < 4; ++ch)
+          tc::sts_u4(prow + 16384 + tc::sw128_off(rq, 4 * grp + ch), make_uint4(dd[4 * ch], dd[4 * ch + 1], dd[4 * ch + 2], dd[4 * ch + 3]));
+        tc::fence_proxy_async();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(ds_full);
+      };
+      auto store_p = [&] {
+        if (t >= 1) tc::mbar_wait(p_empty, (t - 1) & 1);
 #pragma unroll
-      for (int ch = 0; ch < 4; ++ch)
-        tc::sts_u4(prow + tc::sw128_off(rq, 4 * grp + ch), make_uint4(pp[4 * ch], pp[4 * ch + 1], pp[4 * ch + 2], pp[4 * ch + 3]));
-      tc::fence_proxy_async();
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(p_full);
+        for (int ch = 0; ch < 4; ++ch)
+          tc::sts_u4(prow + tc::sw128_off(rq, 4 * grp + ch), make_uint4(pp[4 * ch], pp[4 * ch + 1], pp[4 * ch + 2], pp[4 * ch + 3]));
+        tc::fence_proxy_async();
+        tc::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(p_full);
+      };
+      if (SLAB_COLS_DVFIRST) {
+        store_p();
+        store_ds();
+      } else {
+        store_ds();
+        store_p();
+      }
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 48 + t);
     }
     // ---- phi(K_j) rows (4 threads per key row, D/4 columns each): statistics + the bf16 tile
