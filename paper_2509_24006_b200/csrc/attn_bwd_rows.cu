@@ -21,6 +21,14 @@
 namespace slab {
 namespace {
 
+// CW consecutive TMEM columns of this warp's lane quarter (32x32b shape)
+template <int N>
+__device__ __forceinline__ void tmem_ld_cw(uint32_t taddr, uint32_t (&r)[N]) {
+  static_assert(N == 16 || N == 32, "16 or 32 columns");
+  if constexpr (N == 32) tc::tmem_ld32(taddr, r);
+  else tc::tmem_ld16(taddr, r);
+}
+
 // =========================================================================================
 // linear branch
 // =========================================================================================
@@ -353,7 +361,14 @@ struct RowsLayout {
 // Warps: 0 / 10 TMA producers (K pairs, V pairs), 1 S^T/dP^T issuer, 2-9 softmax-gradient /
 // epilogue, 11 dQ^T issuer.  With one issuer in a static order the pass ran 0.706 ms, with two
 // 0.678 ms.
-constexpr int kRowsThreads = 384;
+// softmax-gradient warps: 8 (32 query columns each per lane quarter) or 16 (16 columns each);
+// (16 warps, for latency hiding, measured slower: TMEM-load and barrier traffic grow with them)
+#ifndef SLAB_ROWS_CW
+#define SLAB_ROWS_CW 8  // measured: 8 warps 0.600 ms, 16 warps 0.613
+#endif
+constexpr int kRowsCW = SLAB_ROWS_CW;
+constexpr int kRowsVWarp = 2 + kRowsCW, kRowsDQWarp = 3 + kRowsCW;  // V producer, dQ issuer
+constexpr int kRowsThreads = 32 * (kRowsCW + 4);
 
 template <int D>
 __global__ void __launch_bounds__(kRowsThreads, 1)
@@ -411,9 +426,9 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       for (int s = 0; s < 2; ++s) {
         tc::mbar_init(sdp_full + s, 1);
         tc::mbar_init(s_full + s, 1);
-        tc::mbar_init(sdp_free + s, 8);
+        tc::mbar_init(sdp_free + s, kRowsCW);
       }
-      tc::mbar_init(ds_full, 8);
+      tc::mbar_init(ds_full, kRowsCW);
       tc::mbar_init(ds_empty, 1);
       tc::mbar_init(dq_done, 1);
       for (int s = 0; s < L::KS; ++s) {
@@ -461,7 +476,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   const uint32_t tmem = *tmem_slot;
   const uint32_t tDQT = tmem, tB0 = tmem + 128, tB1 = tmem + 256;  // dQ^T (M = D); S^T|dP^T pairs
 
-  if (warp == 0 || warp == 10) {
+  if (warp == 0 || warp == kRowsVWarp) {
 #ifdef SLAB_TIMELINE
     if (dbg && warp == 0 && lane == 1) {  // observer: true K / V pair arrival times
       for (int t = 0; t < np && t < 16; ++t) {
@@ -541,7 +556,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       issue_sdp(t);
     }
     __syncwarp();
-  } else if (warp == 11) {
+  } else if (warp == kRowsDQWarp) {
     // dQ^T += [K_j1; K_j2]^T dS^T  (M = D, N = 64, K = 128) as soon as dS(t) is in smem
     tc::mbar_wait(qdo_full, 0);
     const uint64_t dKm = tc::desc_mnmajor(tc::smem_u32(sK), 16384);
@@ -562,16 +577,19 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     tc::mma_commit_w(dq_done);
     __syncwarp();
   } else {
+    constexpr int NCT = 32 * kRowsCW;   // compute threads
+    constexpr int CW = 256 / kRowsCW;   // query columns per thread in the loop (32 or 16)
+    constexpr int TPR = NCT / 64;       // threads per query row in the epilogue (4 or 8)
     const int q4 = warp & 3;
     const int grp = (warp - 2) >> 2;
     const uint32_t lane_base = uint32_t(32 * q4) << 16;
-    const int tid = threadIdx.x - 64;  // 0..255
+    const int tid = threadIdx.x - 64;  // 0 .. NCT-1
     // this thread's dQ^phi chunks for the epilogue (written by k_bwd_lin): issued now so their
     // latency hides behind the main loop instead of stalling the final row-wise pass
-    constexpr int DQ = D / 4;
+    constexpr int DQ = D / TPR;
     uint4 gq[DQ / 8];
     {
-      const int rq = tid >> 2, sub = tid & 3;
+      const int rq = tid / TPR, sub = tid % TPR;
       const __nv_bfloat16* src = p.dqphi + ((long long)row0 + rq) * D + sub * DQ;
 #pragma unroll
       for (int i = 0; i < DQ / 8; ++i)
@@ -579,7 +597,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     }
     if (tid < 64) s_lse2[tid] = p.lse[(long long)row0 + tid] * 1.4426950408889634f;
     else if (tid < 128) s_ds[tid - 64] = p.Ds[(long long)row0 + tid - 64] * p.scale;  // D^s / sqrt(d)
-    named_sync(1, 256);
+    named_sync(1, NCT);
     const int c = 32 * q4 + lane;  // key row of the pair (c < 64: block j1, else j2)
 #pragma unroll 1
     for (int t = 0; t < np; ++t) {
@@ -589,18 +607,18 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       tc::mbar_wait(s_full + (t & 1), (t >> 1) & 1);
       tc::tc_fence_after();
       const bool live = c < 64 || 2 * t + 1 < cnt;
-      const uint32_t tb = ((t & 1) ? tB1 : tB0) + lane_base + 32 * grp;
-      const uint32_t a_l = tc::smem_u32(s_lse2) + 4u * uint32_t(32 * grp);
-      const uint32_t a_d = tc::smem_u32(s_ds) + 4u * uint32_t(32 * grp);
-      uint32_t pk[16];
+      const uint32_t tb = ((t & 1) ? tB1 : tB0) + lane_base + CW * grp;
+      const uint32_t a_l = tc::smem_u32(s_lse2) + 4u * uint32_t(CW * grp);
+      const uint32_t a_d = tc::smem_u32(s_ds) + 4u * uint32_t(CW * grp);
+      uint32_t pk[CW / 2];
       {
-        float pf[32];
+        float pf[CW];
         {
-          uint32_t sv[32];
-          tc::tmem_ld32(tb, sv);
+          uint32_t sv[CW];
+          tmem_ld_cw(tb, sv);
           tc::tmem_ld_wait();
 #pragma unroll
-          for (int e = 0; e < 32; e += 4) {
+          for (int e = 0; e < CW; e += 4) {
             const float4 l4 = tc::lds_f4(a_l + 4u * e);
             const float lv[4] = {l4.x, l4.y, l4.z, l4.w};
 #pragma unroll
@@ -613,9 +631,9 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         tc::mbar_wait(sdp_full + (t & 1), (t >> 1) & 1);
         tc::tc_fence_after();
         ts_mark(dbg && threadIdx.x == 64 && t < 16, 32 + t);
-        ts_mark(dbg && lane == 0 && t >= 4 && t < 8, 192 + 8 * (t - 4) + (warp - 2));
-        uint32_t dp[32];
-        tc::tmem_ld32(tb + 64, dp);
+        ts_mark(dbg && lane == 0 && t >= 4 && t < 8 && warp < 10, 192 + 8 * (t - 4) + (warp - 2));
+        uint32_t dp[CW];
+        tmem_ld_cw(tb + 64, dp);
         tc::tmem_ld_wait();
         tc::tc_fence_before();  // TMEM buffer t&1 may take S/dP(t+2)
         __syncwarp();
@@ -623,7 +641,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         ts_mark(dbg && threadIdx.x == 64 && t < 16, 240 + t);
         const float sc = p.scale;
 #pragma unroll
-        for (int e = 0; e < 32; e += 4) {
+        for (int e = 0; e < CW; e += 4) {
           const float4 d4 = tc::lds_f4(a_d + 4u * e);
           const float dv4[4] = {d4.x, d4.y, d4.z, d4.w};
           float dsv[4];
@@ -634,7 +652,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         }
         if (!live) {  // the repeated block of an odd tail contributes nothing
 #pragma unroll
-          for (int e = 0; e < 16; ++e) pk[e] = 0u;
+          for (int e = 0; e < CW / 2; ++e) pk[e] = 0u;
         }
       }
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 128 + t);
@@ -642,14 +660,14 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 144 + t);
       const uint32_t a_ds_tile = tc::smem_u32(sDS);
 #pragma unroll
-      for (int ch = 0; ch < 4; ++ch)
-        tc::sts_u4(a_ds_tile + tc::sw128_off(c, 4 * grp + ch), make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]));
+      for (int ch = 0; ch < CW / 8; ++ch)
+        tc::sts_u4(a_ds_tile + tc::sw128_off(c, (CW / 8) * grp + ch), make_uint4(pk[4 * ch], pk[4 * ch + 1], pk[4 * ch + 2], pk[4 * ch + 3]));
       tc::fence_proxy_async();
       tc::tc_fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(ds_full);
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 48 + t);
-      ts_mark(dbg && lane == 0 && t >= 4 && t < 8, 160 + 8 * (t - 4) + (warp - 2));
+      ts_mark(dbg && lane == 0 && t >= 4 && t < 8 && warp < 10, 160 + 8 * (t - 4) + (warp - 2));
     }
     // dq_total = J_phi(q)^T dQ^phi + dQ: transpose dQ^T through smem (the K ring is idle once
     // dq_done fired), then finish row-wise with 4 threads per query row.  For the softmax
@@ -659,7 +677,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     // dQ^T MMAs drain.  Chunks are held in the rotated order the row-wise pass walks
     // (slot cc0 <-> columns c0 + ((cc0 + 8 sub) & (DQ - 1))), which spreads its reads of the
     // transposed tile over the banks.
-    const int rq = tid >> 2, sub = tid & 3, c0 = sub * DQ;
+    const int rq = tid / TPR, sub = tid % TPR, c0 = sub * DQ;
     auto rot = [&](int cc0) { return (cc0 + 8 * sub) & (DQ - 1); };
     float x[DQ];
 #pragma unroll
@@ -673,16 +691,16 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       float mx = -INFINITY;
 #pragma unroll
       for (int e = 0; e < DQ; ++e) mx = fmaxf(mx, x[e]);
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+#pragma unroll
+      for (int o = 1; o < TPR; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
       float se = 0.f;
 #pragma unroll
       for (int e = 0; e < DQ; ++e) {
         x[e] = __expf(x[e] - mx);
         se += x[e];
       }
-      se += __shfl_xor_sync(0xffffffffu, se, 1);
-      se += __shfl_xor_sync(0xffffffffu, se, 2);
+#pragma unroll
+      for (int o = 1; o < TPR; o <<= 1) se += __shfl_xor_sync(0xffffffffu, se, o);
       const float inv = 1.f / se;
 #pragma unroll
       for (int e = 0; e < DQ; ++e) x[e] *= inv;
@@ -696,15 +714,15 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     {
       const int acol = D == 128 ? 32 * q4 + lane : 16 * q4 + lane;
       const bool avalid = D == 128 || lane < 16;
-      uint32_t b[32];
-      if (np > 0) tc::tmem_ld32(tDQT + lane_base + 32 * grp, b);
+      uint32_t b[CW];
+      if (np > 0) tmem_ld_cw(tDQT + lane_base + CW * grp, b);
       tc::tmem_ld_wait();
       if (avalid) {
 #pragma unroll
-        for (int e = 0; e < 32; ++e) tq[(32 * grp + e) * TP + acol] = np > 0 ? __uint_as_float(b[e]) : 0.f;
+        for (int e = 0; e < CW; ++e) tq[(CW * grp + e) * TP + acol] = np > 0 ? __uint_as_float(b[e]) : 0.f;
       }
     }
-    named_sync(1, 256);
+    named_sync(1, NCT);
     {
       const long long grow = (long long)row0 + rq;
 #pragma unroll
