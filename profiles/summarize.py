@@ -20,18 +20,20 @@ from collections import defaultdict
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 # ncu kernel (template instance) -> bench.py / profiler name
-GEMM_NAMES = {
+GEMM_NAMES = {  # template arguments BM, BN, A_MN, B_MN, OutT (the trailing multicast flag dropped)
     "k_gemm<128, 128, 1, 1, __nv_bfloat16>": "gemm_summaries",
     "k_gemm<128, 256, 0, 1, __nv_bfloat16>": "gemm_aggregate",
     "k_gemm<128, 256, 1, 1, __nv_bfloat16>": "gemm_aggregate_t",
-    "k_gemm<128, 128, 1, 1, float>": "gemm_dw",
+    "k_gemm<128, 128, 1, 1, float>": "gemm_dw / gemm_aggregate_dz",
+    "k_gemm<128, 128, 0, 1, float>": "gemm_aggregate_z",
 }
 
 
 def short(name: str) -> str:
     m = re.search(r"(k_gemm<[^>]*>)", name)
     if m:
-        return GEMM_NAMES.get(m.group(1), m.group(1))
+        key = re.sub(r", [01]>$", ">", m.group(1))
+        return GEMM_NAMES.get(key, m.group(1))
     m = re.search(r"(k_aggregate_vec)<(\d)>", name)
     if m:
         return "k_aggregate_z" if m.group(2) == "0" else "k_aggregate_dz"
