@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdio>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/sla_b200.h"
@@ -198,10 +199,10 @@ struct SideStream {
 };
 
 SideStream& side_stream() {
-  thread_local SideStream per_dev[16];
+  thread_local std::unordered_map<int, SideStream> per_dev;  // created on first use per device
   int dev = 0;
   SLAB_CUDA(cudaGetDevice(&dev));
-  SideStream& x = per_dev[dev & 15];
+  SideStream& x = per_dev[dev];
   if (!x.s) {
     SLAB_CUDA(cudaStreamCreateWithFlags(&x.s, cudaStreamNonBlocking));
     SLAB_CUDA(cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming));
