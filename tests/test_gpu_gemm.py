@@ -29,7 +29,10 @@ def _gemm(A, B, M, N, K, batch, a_mn, b_mn, out_f32):
                                          (128, 128, 128, 5),
                                          # A-resident aggregation kernel: CTA tile ranges that
                                          # cross (batch, m) blocks, and a K tail
-                                         (512, 4096, 512, 3), (384, 512, 200, 2)])
+                                         (512, 4096, 512, 3), (384, 512, 200, 2),
+                                         # 2-CTA multicast-B path (N-major B, bf16 out, even
+                                         # M-tile count) with a K tail and an odd tile-pair count
+                                         (256, 768, 200, 3)])
 @pytest.mark.parametrize("out_f32", [True, False])
 def test_gemm_matches_fp32_matmul(a_mn, b_mn, M, N, K, batch, out_f32):
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K + batch)
