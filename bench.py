@@ -10,9 +10,16 @@ b_q=b_kv=64, k_h=5 %, k_l=10 %, phi=softmax, bf16 inputs with fp32 accumulation.
   python bench.py [--gpus N --steps K --warmup W]            our CUDA path (1 JSON line)
   python bench.py --impl reference [...]                      the reference's CPU path
 
-Multi-GPU: one process per GPU (torchrun); the (batch x head) units shard with no
-collective on the data path -- every rank runs its own C3 batch element (weak scaling);
-timing is the max over ranks of CUDA-event time.
+Multi-GPU (paper_2509_24006_b200/runner.py): one process per GPU.  `--gpus N` without a
+torchrun environment re-launches itself under torch.distributed.run with N ranks.  The B*H
+(batch, head) units of ONE global problem are partitioned over ranks with
+shard.partition_units; the data path has no collective, the step ends with the one real
+exchange (the per-head dW all-reduce when a head's batch is split), and a validation gather of
+per-unit checksums runs after the timed region.
+  c3 (default): weak scaling -- the global problem is B = N batch elements of the C3 shape
+                (12 heads each), so every rank owns 12 units at any N.
+  c5:           strong scaling -- the fixed B=8 x H=40 problem (configs[4]) split over N ranks.
+Timing is the max over ranks of CUDA-event time.
 """
 from __future__ import annotations
 
@@ -39,6 +46,15 @@ CONFIGS = {
     # the literal Wan2.1-1.3B length through SLA_B200_FLAG_RAGGED (the reference rejects it)
     "c3r": (1, 12, 32760, 128, 64, 5.0, 10.0, "softmax"),
 }
+
+
+SCALING = {"c3": "weak", "c1": "weak", "c3r": "weak", "c5": "strong"}
+
+
+def global_batch(name, world):
+    """Batch of the global problem: weak-scaling configs grow it with the world size."""
+    B = CONFIGS[name][0]
+    return B * world if SCALING[name] == "weak" else B
 
 
 def parse():
@@ -162,22 +178,22 @@ class Clocks:
 # ---------------------------------------------------------------------------------------
 # reference arm / cpu baseline: the reference's own CPU path (oracle/_ref)
 # ---------------------------------------------------------------------------------------
-def reference_step_inputs(N, d, seed=1234):
+def reference_unit_inputs(N, d, unit, seed=1234):
+    """bf16-exact SplitMix64 inputs of one (batch, head) unit (rng.hpp:22-57), f32 storage."""
     from oracle import oracle as O
 
-    rng = O.Rng(seed)
-    bf = O.to_bf16_exact
+    rng = O.Rng(seed + 7919 * unit)
+    bf = lambda a: O.to_bf16_exact(a).astype(np.float32)  # noqa: E731
     return dict(q=bf(rng.gaussian(N, d)), k=bf(rng.gaussian(N, d)), v=bf(rng.gaussian(N, d)),
                 w=bf(rng.gaussian(d, d, 0.1)), do=bf(rng.gaussian(N, d)))
 
 
-def time_reference_head(cfg, threads, x=None):
-    """One (batch, head) unit of the workload through the reference's public API:
-    sla_forward -> combine_outputs -> proj_backward -> sla_backward (f32)."""
+def time_reference_unit(cfg, threads, x):
+    """One (batch, head) unit through the reference's public API:
+    sla_forward -> combine_outputs -> proj_backward -> sla_backward (f32, `threads`)."""
     from oracle import oracle as O
 
     B, H, N, d, b, k_h, k_l, phi = cfg
-    x = x or reference_step_inputs(N, d)
     t0 = time.perf_counter()
     if O.Reference.available():
         O.Reference.run(x["q"], x["k"], x["v"], b, b, k_h, k_l, phi, threads=threads, w=x["w"],
@@ -190,79 +206,227 @@ def time_reference_head(cfg, threads, x=None):
     return time.perf_counter() - t0, kind, threads
 
 
+def reference_cfg(name):
+    cfg = CONFIGS[name]
+    B, H, N, d, b, k_h, k_l, phi = cfg
+    if N % b:  # the reference rejects ragged N (layout.cpp:12-17): time the padded length
+        N = (N + b - 1) // b * b
+    return (B, H, N, d, b, k_h, k_l, phi)
+
+
+# units of one reference step that are actually run (~2 s per C3 unit on 16 cores): the 12 units
+# of one C3 batch element (all of them at N = 1; weak scaling grows the global batch with N, and
+# the step time is scaled by units / 12), or 2 units of c5 (~11 s each) scaled to its 320
+REF_UNITS = {"c5": 2}
+REF_UNITS_DEFAULT = 12
+
+
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    cfg = CONFIGS[args.config]
+    cfg = reference_cfg(args.config)
     B, H, N, d, b, k_h, k_l, phi = cfg
-    if N % b:  # the reference rejects ragged N (layout.cpp:12-17): time the padded length
-        N = (N + b - 1) // b * b
-        cfg = (B, H, N, d, b, k_h, k_l, phi)
+    world = max(1, int(os.environ.get("WORLD_SIZE", "1")))
+    units_total = global_batch(args.config, world) * H
+    run_units = min(units_total, REF_UNITS.get(args.config, REF_UNITS_DEFAULT))
     threads = os.cpu_count() or 1
-    x = reference_step_inputs(N, d)
-    for _ in range(args.warmup):
-        time_reference_head(cfg, threads, x)
-    times = []
+    xs = [reference_unit_inputs(N, d, u) for u in range(run_units)]
+    for i in range(args.warmup):  # a CPU path has nothing to warm beyond its pages: one unit each
+        time_reference_unit(cfg, threads, xs[i % run_units])
     kind = "reference"
+    steps = []
     for _ in range(args.steps):
-        t, kind, threads = time_reference_head(cfg, threads, x)
-        times.append(t)
-    per_head = sum(times) / len(times)
-    flops = dense_equiv_flops(1, 1, N, d)
-    value = flops / per_head / 1e12
-    sample = f"one (batch, head) unit of {B * H} per step, fwd+bwd, f32, threads={threads}"
+        t = 0.0
+        for x in xs:
+            dt, kind, threads = time_reference_unit(cfg, threads, x)
+            t += dt
+        steps.append(t * units_total / run_units)
+    step_s = sum(steps) / len(steps)
+    flops = dense_equiv_flops(1, units_total, N, d)
+    value = flops / step_s / 1e12
+    sample = (f"every step runs all {units_total} (batch, head) units, fwd+bwd, f32, threads={threads}"
+              if run_units == units_total else
+              f"every step runs {run_units} of the {units_total} (batch, head) units (fwd+bwd, f32, "
+              f"threads={threads}) and scales the time by {units_total}/{run_units}")
     out = {
-        "impl": "reference", "metric": "SLA fwd+bwd dense-equiv TFLOPS (Wan2.1-1.3B shape)",
-        "value": value, "unit": "TFLOPS", "n_gpus": args.gpus, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": per_head * 1e3 * B * H, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": config_json(args.config),
-        "cpu_baseline": {"value": value, "unit": "TFLOPS", "cores": threads, "kind": kind,
-                         "sample": sample},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True,
+        "scaling": SCALING[args.config], "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": config_json(args.config, world),
+        "cpu_baseline": {"value": value, "unit": "TFLOPS", "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "ms_per_head": per_head * 1e3,
+        "ms_per_unit": step_s * 1e3 / units_total,
+        "warmup_note": "warm-up steps run one unit each",
     }
     print(json.dumps(out), flush=True)
 
 
-def config_json(name):
+METRIC = "SLA fwd+bwd dense-equiv TFLOPS (Wan2.1-1.3B shape)"
+
+
+def config_json(name, world=1):
     B, H, N, d, b, k_h, k_l, phi = CONFIGS[name]
-    return {"workload": f"{name}: SLA fwd+bwd, B={B} H={H} N={N} d={d} b_q=b_kv={b} k_h={k_h}% k_l={k_l}% phi={phi}",
-            "batch": B, "heads": H, "n": N, "d": d, "block": b, "k_h": k_h, "k_l": k_l, "phi": phi,
+    Bg = global_batch(name, world)
+    return {"workload": f"{name}: SLA fwd+bwd, B={Bg} H={H} N={N} d={d} b_q=b_kv={b} k_h={k_h}% k_l={k_l}% phi={phi}",
+            "batch": Bg, "heads": H, "n": N, "d": d, "block": b, "k_h": k_h, "k_l": k_l, "phi": phi,
+            "units": Bg * H, "units_per_rank": -(-Bg * H // world),
             "n_note": ("N = 32760 as-is through SLA_B200_FLAG_RAGGED (zero-padded unit copies inside the "
                        "timed region); the reference arm times N = 32768") if N % b else
                       "N padded from 32760/75600 to a multiple of 64 (make_block_layout rejects ragged N)",
             "l2": "inputs (Q,K,V,dO = 4 x B*H*N*d*2 bytes) exceed the 126 MB L2; no flush needed",
-            "parallelism": "(batch x head) units sharded over ranks, no collective"}
+            "parallelism": (f"{Bg * H} (batch x head) units partitioned over {world} rank(s) "
+                            f"(shard.partition_units), no data-path collective; dW all-reduce at step end"
+                            + (" when world > 1" if world == 1 else "")),
+            "scaling_rule": ("weak: the global batch is 1 x world (12 units per rank)" if SCALING[name] == "weak"
+                             else "strong: fixed B x H units split over the ranks")}
+
+
+# ---------------------------------------------------------------------------------------
+# roofline bookkeeping
+# ---------------------------------------------------------------------------------------
+def kernel_work(name, D, crit):
+    """Algorithmic work of one step's launches of a kernel: (bound, amount)
+    with amount in FLOPs for tensor-bound kernels and bytes for HBM-bound ones.  D: U (units of
+    this rank), N, d, T.  crit: critical blocks over all units."""
+    U, N, d, T = D["U"], D["N"], D["d"], D["T"]
+    tile = 64 * 64 * d
+    nd2 = U * N * d * 2  # one [U, N, d] bf16 tensor
+    h2 = U * T * d * d * 2  # one [U, T, d, d] bf16 summary tensor
+    m0 = U * T * ((T + 7) // 8 * 8) * 2
+    return {
+        "k_attn_fwd": ("tensor", 4.0 * tile * crit),   # S = QK^T, O += PV
+        "k_bwd_rows": ("tensor", 6.0 * tile * crit),   # S, dP recomputed, dQ += dS K
+        "k_bwd_cols": ("tensor", 8.0 * tile * crit),   # S, dP recomputed, dV += P^T dO, dK += dS^T Q
+        "gemm_aggregate": ("tensor", 2.0 * U * T * T * d * d),
+        "gemm_aggregate_t": ("tensor", 2.0 * U * T * T * d * d),
+        "gemm_dw": ("tensor", 2.0 * U * N * d * d),
+        # HBM: bytes read + written
+        "k_pool": ("hbm", 2.0 * nd2 + 2 * U * T * d * 8),                      # Q, K -> pooled f64
+        "k_scores": ("hbm", 2.0 * U * T * d * 8 + U * T * T * 8),              # pooled -> f64 scores
+        "k_classify": ("hbm", U * T * T * 8 + U * T * T + m0 + U * T * 4 * 2),  # scores -> labels, M0, counts
+        "k_phi_kz": ("hbm", 2.0 * nd2 + U * T * 3 * d * 2),                    # K -> phi(K), z parts
+        "gemm_summaries": ("hbm", 2.0 * nd2 + h2),                             # phi(K), V -> h
+        "k_bwd_lin": ("hbm", 5.0 * nd2 + 2 * h2 + U * N * 4),                  # Q dO O^s O^l H -> dH dQ^phi D^s
+    }.get(name, (None, None))
+
+
+def roofline_table(kernels, steps, D, crit, pk, peak_key):
+    rows = []
+    for nm, (tot_ms, cnt) in sorted(kernels.items(), key=lambda kv: -kv[1][0]):
+        kind, work = kernel_work(nm, D, crit)
+        ms = tot_ms / steps
+        row = {"kernel": nm, "ms_per_step": round(ms, 4), "launches_per_step": cnt / steps}
+        if kind == "tensor":
+            ach = work / (ms * 1e-3) / 1e12
+            row.update(bound="tensor", achieved=round(ach, 1), unit="TFLOP/s", peak=pk[peak_key],
+                       frac=round(ach / pk[peak_key], 3))
+        elif kind == "hbm":
+            ach = work / (ms * 1e-3) / 1e9
+            row.update(bound="hbm", achieved=round(ach, 1), unit="GB/s", peak=pk["hbm_gbs"],
+                       frac=round(ach / pk["hbm_gbs"], 3))
+        rows.append(row)
+    return rows
 
 
 # ---------------------------------------------------------------------------------------
 # our CUDA path
 # ---------------------------------------------------------------------------------------
-def algorithmic_work(name, D, labels_stats):
-    """(kind, units per launch) of a kernel's algorithmic work for the roofline:
-    critical-tile FLOPs for attention kernels, bytes for the HBM-bound ones."""
-    B, H, N, d, b = D["B"], D["H"], D["N"], D["d"], D["b"]
-    crit = labels_stats["critical_blocks"]  # total over all units
-    tile = b * b * d
-    if name in ("k_fwd_generic", "k_attn_fwd"):       # S = QK^T, O += PV
-        return "tensor", 4.0 * tile * crit
-    if name in ("k_bwd_rows_sparse", "k_bwd_rows"):    # S, dP recomputed, dQ += dS K
-        return "tensor", 6.0 * tile * crit
-    if name in ("k_bwd_cols_sparse", "k_bwd_cols"):    # S, dP recomputed, dV += P^T dO, dK += dS^T Q
-        return "tensor", 8.0 * tile * crit
-    if name in ("k_pool(q)", "k_pool(k)"):
-        return "hbm", B * H * N * d * 2.0
-    return None, None
+def relaunch_under_torchrun(args):
+    """`--gpus N` outside torchrun: one process per GPU via torch.distributed.run."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd))
+
+
+def dense_comparators(units_q, units_k, units_v, units_do, stream, flops_per_unit, n_units, cfg_tuple, dev):
+    """Dense attention of the same shape: torch SDPA (library kernel, name recorded) and this
+    repo's own tcgen05 kernels with every block critical (k_h = 100 %: a FlashAttention loop)."""
+    import torch
+    import torch.nn.functional as F
+
+    out = {}
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    qd_, kd_, vd_ = (t.clone().requires_grad_(True) for t in (units_q, units_k, units_v))
+
+    def dense_step():
+        o_ = F.scaled_dot_product_attention(qd_, kd_, vd_)
+        o_.backward(units_do)
+
+    try:
+        for _ in range(2):
+            dense_step()
+        torch.cuda.synchronize()
+        names = []
+        try:
+            from torch.profiler import ProfilerActivity, profile
+
+            with profile(activities=[ProfilerActivity.CUDA]) as prof:
+                dense_step()
+                torch.cuda.synchronize()
+            ka = sorted(prof.key_averages(), key=lambda e: -getattr(e, "device_time_total", 0))
+            names = [e.key for e in ka[:4]]
+        except Exception as e:  # pragma: no cover
+            names = [f"profiler unavailable: {str(e)[:80]}"]
+        ev0.record(stream)
+        for _ in range(3):
+            dense_step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        dms = ev0.elapsed_time(ev1) / 3
+        out["sdpa"] = {"kind": "torch SDPA fwd+bwd (library dense kernel, same shape, bf16)",
+                       "kernels": names, "ms_per_step": dms * n_units / units_q.shape[1],
+                       "tflops": flops_per_unit * units_q.shape[1] / (dms * 1e-3) / 1e12}
+    except Exception as e:  # pragma: no cover
+        out["sdpa"] = {"error": str(e)[:200]}
+    del qd_, kd_, vd_
+    try:  # the repo's own dense kernel: the same fused tcgen05 kernels with an all-critical mask
+        from paper_2509_24006_b200 import SLA, SlaConfig
+
+        B_, H_, N_, d_, b_, _, _, phi_ = cfg_tuple
+        cnt = units_q.shape[1]
+        op = SLA(1, cnt, N_, d_, b_, b_, SlaConfig(k_h=100.0, k_l=0.0, phi=phi_), torch.bfloat16, dev)
+        w = torch.zeros((cnt, d_, d_), dtype=torch.bfloat16, device=dev)
+        st_buf = op.new_state()
+
+        def rd_step():
+            st = op.forward(units_q, units_k, units_v, w, state=st_buf)
+            op.backward(st, units_q, units_k, units_v, w, units_do)
+
+        rd_step()
+        torch.cuda.synchronize()
+        ev0.record(stream)
+        for _ in range(2):
+            rd_step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        rms = ev0.elapsed_time(ev1) / 2
+        out["repo_dense"] = {"kind": "this repo's tcgen05 attention kernels, all blocks critical (k_h = 100 %)",
+                             "ms_per_step": rms * n_units / cnt,
+                             "tflops": flops_per_unit * cnt / (rms * 1e-3) / 1e12}
+        del op, st_buf
+    except Exception as e:  # pragma: no cover
+        out["repo_dense"] = {"error": str(e)[:200]}
+    return out
+
+
+E2E_MAX_UNITS = 24  # pinned host footprint: 8 [N, d] bf16 tensors per unit
 
 
 def run_ours(args):
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(args)
     import torch
     import torch.distributed as dist
 
-    from paper_2509_24006_b200 import SLA, HostTrainStep, SlaConfig
+    from paper_2509_24006_b200 import HostTrainStep, SlaConfig
     from paper_2509_24006_b200 import _lib as L
+    from paper_2509_24006_b200.runner import CudaUnits, ShardedStep
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -272,50 +436,41 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
     B, H, N, d, b, k_h, k_l, phi = CONFIGS[args.config]
+    Bg = global_batch(args.config, world)
     cfg = SlaConfig(k_h=k_h, k_l=k_l, phi=phi, ragged=N % b != 0)
-    op = SLA(B, H, N, d, b, b, cfg, torch.bfloat16, dev)
-    g = torch.Generator(device=dev)
-    g.manual_seed(1234 + rank)
-    shape = (B, H, N, d)
-    mk = lambda s=1.0: (torch.randn(shape, generator=g, device=dev) * s).to(torch.bfloat16)  # noqa: E731
-    q, k, v, do = mk(), mk(), mk(), mk()
-    w = (torch.randn((H, d, d), generator=g, device=dev) * 0.1).to(torch.bfloat16)
-    st_buf = op.new_state()
-    o, o_s, o_l = (torch.empty(shape, dtype=torch.bfloat16, device=dev) for _ in range(3))
-    lse = torch.empty(shape[:-1], dtype=torch.float32, device=dev)
-    dq, dk, dv = (torch.empty(shape, dtype=torch.bfloat16, device=dev) for _ in range(3))
-    dw = torch.empty((H, d, d), dtype=torch.float32, device=dev)
-    launches = [0]
-
-    def step():
-        st = op.forward(q, k, v, w, state=st_buf, out=(o, o_s, o_l, lse))
-        n1 = op.launches()
-        op.backward(st, q, k, v, w, do, out=(dq, dk, dv, dw))
-        launches[0] += n1 + op.launches()
-        return st
+    runner = ShardedStep(Bg, H, d, world, rank)
+    comp = CudaUnits(runner.shard, H, N, d, b, cfg, dev)
+    runner.attach(comp)
+    U = runner.shard.count
 
     for _ in range(args.warmup):
-        st = step()
+        runner.step()
     torch.cuda.synchronize()
-    labels = st.labels.cpu()
-    lab_stats = {"critical_blocks": int((labels == 1).sum()), "marginal_blocks": int((labels == 0).sum())}
+    labels = comp.last_state.labels
+    crit = int((labels == 1).sum())
+    lab_stats = {"critical_blocks": crit, "marginal_blocks": int((labels == 0).sum())}
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    launches[0] = 0
-    L.lib().sla_b200_profiler(1)
-    with Clocks(local) as clk:  # clocks sampled over both timed passes
+
+    def timed(n):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
         ev0.record(stream)
-        for _ in range(args.steps):
-            step()
+        for _ in range(n):
+            runner.step()
         ev1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
-        ms = ev0.elapsed_time(ev1) / args.steps
+        return ev0.elapsed_time(ev1) / n
+
+    with Clocks(local) as clk:  # clocks sampled over both timed passes
+        L.lib().sla_b200_profiler(1)
+        comp.launches = 0
+        ms_prof = timed(args.steps)
+        launches = comp.launches // args.steps
         buf = C.create_string_buffer(1 << 16)
         L.lib().sla_b200_profiler_report(buf, 1 << 16)
         L.lib().sla_b200_profiler(0)
@@ -323,78 +478,90 @@ def run_ours(args):
         for ln in buf.value.decode().splitlines():
             nm, t, cnt = ln.rsplit(" ", 2)
             kernels[nm] = (float(t), int(cnt))
-        # clean timing pass without profiler events (the headline number; the library's side
-        # streams run only when its per-kernel profiler is off)
-        if world > 1:
-            dist.barrier()
-        torch.cuda.synchronize()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step()
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        ms_clean = ev0.elapsed_time(ev1) / args.steps
-    ms = min(ms, ms_clean) if ms_clean > 0 else ms
+        # clean pass without profiler events: the headline number (the library's side streams
+        # run only when its per-kernel profiler is off)
+        ms_clean = timed(args.steps)
+    ms = ms_clean
     t = torch.tensor([ms], device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        dist.barrier()
     ms_max = float(t.item())
-    flops_step = dense_equiv_flops(B, H, N, d)
-    value = flops_step * world / (ms_max * 1e-3) / 1e12
+    flops_unit = dense_equiv_flops(1, 1, N, d)
+    value = flops_unit * runner.n_units / (ms_max * 1e-3) / 1e12
 
+    # ---- roofline: the dominant kernel and every kernel with a stated algorithmic work
     pk, pk_src = peaks()
+    cl = clk.summary()
+    at_max = cl["sm_mhz"] is not None and cl["sm_max_mhz"] and cl["sm_mhz"] >= 0.97 * cl["sm_max_mhz"]
+    peak_key = "bf16_tflops" if at_max else "bf16_tflops_sustained"
+    peak_note = (f"{pk_src} bf16 {'burst' if at_max else 'sustained'}: median SM clock {cl['sm_mhz']} MHz "
+                 f"{'at' if at_max else 'below'} max {cl['sm_max_mhz']} MHz over the timed region")
     try:  # DRAM bytes per launch from the committed ncu capture (profiles/traffic.json)
         traffic_tab = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))
     except Exception:
         traffic_tab = {}
+    D = dict(U=U, N=N if N % b == 0 else (N + b - 1) // b * b, d=d, T=-(-N // b))
+    table = roofline_table(kernels, args.steps, D, crit, pk, peak_key)
     roof = None
-    if kernels:
-        dom = max(kernels.items(), key=lambda kv: kv[1][0])
-        nm, (tot_ms, cnt) = dom
-        kind, work = algorithmic_work(nm, dict(B=B, H=H, N=N, d=d, b=b), lab_stats)
-        avg = tot_ms / max(cnt, 1)
-        if kind == "tensor":
-            ach = work / (avg * 1e-3) / 1e12
-            peak = pk["bf16_tflops_sustained"]
-            roof = {"kernel": nm, "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                    "frac": ach / peak, "traffic": traffic_tab.get(nm), "peak_source": f"{pk_src} bf16 sustained",
-                    "algorithmic_flops_per_launch": work, "avg_launch_ms": avg,
-                    "share_of_step": tot_ms / args.steps / ms}
-        elif kind == "hbm":
-            ach = work / (avg * 1e-3) / 1e9
-            peak = pk["hbm_gbs"]
-            roof = {"kernel": nm, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
-                    "frac": ach / peak, "traffic": traffic_tab.get(nm), "peak_source": f"{pk_src} hbm copy",
-                    "algorithmic_bytes_per_launch": work, "avg_launch_ms": avg,
-                    "share_of_step": tot_ms / args.steps / ms}
-        else:
-            roof = {"kernel": nm, "bound": None, "avg_launch_ms": avg}
+    if table:
+        dom = table[0]
+        nm = dom["kernel"]
+        tot_ms, cnt = kernels[nm]
+        roof = {"kernel": nm, "bound": dom.get("bound"), "achieved": dom.get("achieved"), "peak": dom.get("peak"),
+                "unit": dom.get("unit"), "frac": dom.get("frac"), "traffic": traffic_tab.get(nm),
+                "peak_source": peak_note if dom.get("bound") == "tensor" else f"{pk_src} hbm copy",
+                "algorithmic_per_launch": kernel_work(nm, D, crit)[1] / max(1, cnt / args.steps),
+                "avg_launch_ms": tot_ms / cnt, "share_of_step": tot_ms / args.steps / ms_prof}
+        att = [r for r in table if r["kernel"] in ("k_attn_fwd", "k_bwd_rows", "k_bwd_cols")]
+        if att:
+            w_sum = sum(kernel_work(r["kernel"], D, crit)[1] for r in att)
+            t_sum = sum(r["ms_per_step"] for r in att)
+            roof["critical_tiles_combined"] = {"achieved": round(w_sum / (t_sum * 1e-3) / 1e12, 1),
+                                               "frac": round(w_sum / (t_sum * 1e-3) / 1e12 / pk[peak_key], 3)}
 
     out = {
-        "metric": "SLA fwd+bwd dense-equiv TFLOPS (Wan2.1-1.3B shape)", "value": value,
-        "unit": "TFLOPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "bf16", "data": "synthetic (randn Q,K,V,dO; W ~ 0.1 randn)",
-        "config": config_json(args.config), "path": op.path,
-        "gpu_launches": launches[0],
-        "roofline": roof,
-        "kernels_ms_per_step": {k2: round(v2[0] / args.steps, 4) for k2, v2 in sorted(kernels.items(), key=lambda kv: -kv[1][0])},
-        "mask": lab_stats,
+        "metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+        "scaling": SCALING[args.config], "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (randn Q,K,V,dO per unit seed; W ~ 0.1 randn per head)",
+        "config": config_json(args.config, world), "path": comp.op.path,
+        "gpu_launches": launches * args.steps, "gpu_launches_per_step": launches,
+        "roofline": roof, "kernels": table, "mask": lab_stats,
+        "ms_per_step_profiled": ms_prof,
     }
     if rank == 0:
-        out["clocks"] = clk.summary()
-    # --- e2e through the public host-buffer API (HostTrainStep: every chunk's H2D, fwd+bwd
+        out["clocks"] = cl
+    # ---- validation gather (after the timed region): per-unit checksums to rank 0 over NCCL
+    sums = runner.gather_checksums(device=dev)
+    if rank == 0 and sums is not None:
+        s = sums.double().cpu()
+        out["validation"] = {"units": int(s.shape[0]), "checksum_first_unit": [float(x) for x in s[0]],
+                             "checksum_all": [float(x) for x in s.sum(0)]}
+    # ---- dense attention of the same shape (rank 0): torch SDPA and the repo's own kernels
+    if not args.no_dense and rank == 0:
+        nd = min(U, 12)
+        out["dense"] = dense_comparators(comp.q[:, :nd], comp.k[:, :nd], comp.v[:, :nd], comp.do[:, :nd], stream,
+                                         flops_unit, U, CONFIGS[args.config], dev)
+        if "ms_per_step" in out["dense"].get("sdpa", {}):
+            out["dense"]["speedup_sla_vs_sdpa"] = out["dense"]["sdpa"]["ms_per_step"] / ms
+        if "ms_per_step" in out["dense"].get("repo_dense", {}):
+            out["dense"]["speedup_sla_vs_repo_dense"] = out["dense"]["repo_dense"]["ms_per_step"] / ms
+    # ---- e2e through the public host-buffer API (HostTrainStep: every chunk's H2D, fwd+bwd
     # through the C-ABI and D2H inside the timed region; copies overlap compute across chunks)
     if not args.no_e2e:
+        ne = min(U, E2E_MAX_UNITS)
+        shape = (1, ne, N, d)
         hs = [torch.empty(shape, dtype=torch.bfloat16, pin_memory=True) for _ in range(4)]
-        hw = torch.empty((H, d, d), dtype=torch.bfloat16, pin_memory=True)
-        for hsrc, dsrc in zip(hs + [hw], (q, k, v, do, w)):
+        hw = torch.empty((ne, d, d), dtype=torch.bfloat16, pin_memory=True)
+        for hsrc, dsrc in zip(hs + [hw], (comp.q[:, :ne], comp.k[:, :ne], comp.v[:, :ne], comp.do[:, :ne],
+                                          comp.w[:ne])):
             hsrc.copy_(dsrc.cpu())
         ho = [torch.empty(shape, dtype=torch.bfloat16, pin_memory=True) for _ in range(4)]
-        hdw = torch.empty((H, d, d), dtype=torch.float32, pin_memory=True)
-        del st_buf, o, o_s, o_l, lse, dq, dk, dv  # device-resident step buffers are not used here
-        hts = HostTrainStep(B, H, N, d, b, b, cfg, torch.bfloat16, dev, chunks=args.e2e_chunks)
+        hdw = torch.empty((ne, d, d), dtype=torch.float32, pin_memory=True)
+        runner.compute = None
+        del comp
+        torch.cuda.empty_cache()
+        hts = HostTrainStep(1, ne, N, d, b, b, cfg, torch.bfloat16, dev, chunks=min(args.e2e_chunks, ne))
 
         def e2e_step():
             hts(hs[0], hs[1], hs[2], hw, hs[3], ho[0], ho[1], ho[2], ho[3], hdw)
@@ -413,48 +580,22 @@ def run_ours(args):
         if world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
-        out["e2e"] = {"value": flops_step * world / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOPS",
-                      "ms_per_step": e2e_ms, "h2d_bytes_per_step": hts.h2d_bytes(),
-                      "d2h_bytes_per_step": hts.d2h_bytes(), "chunks": len(hts.ranges),
-                      "api": "paper_2509_24006_b200.HostTrainStep (pinned host buffers)"}
-    # --- dense attention of the same shape (torch SDPA: cuDNN / flash on sm_100)
-    if not args.no_dense and rank == 0:
-        try:
-            import torch.nn.functional as F
-
-            qd_ = q.clone().requires_grad_(True)
-            kd_ = k.clone().requires_grad_(True)
-            vd_ = v.clone().requires_grad_(True)
-
-            def dense_step():
-                o_ = F.scaled_dot_product_attention(qd_, kd_, vd_)
-                o_.backward(do)
-
-            for _ in range(2):
-                dense_step()
-            torch.cuda.synchronize()
-            ev0.record(stream)
-            for _ in range(3):
-                dense_step()
-            ev1.record(stream)
-            torch.cuda.synchronize()
-            dms = ev0.elapsed_time(ev1) / 3
-            out["dense"] = {"kind": "torch SDPA fwd+bwd (library dense kernel, same shape, bf16)",
-                            "ms_per_step": dms, "tflops": flops_step / (dms * 1e-3) / 1e12,
-                            "speedup_sla_vs_dense": dms / ms_max}
-        except Exception as e:  # pragma: no cover
-            out["dense"] = {"error": str(e)[:200]}
-    # --- CPU baseline: the reference's own path on a bounded sample (rank 0, N=1)
+        out["e2e"] = {"value": flops_unit * ne * world / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOPS",
+                      "ms_per_step": e2e_ms * U / ne, "h2d_bytes_per_step": hts.h2d_bytes() * U // ne,
+                      "d2h_bytes_per_step": hts.d2h_bytes() * U // ne, "chunks": len(hts.ranges),
+                      "api": "paper_2509_24006_b200.HostTrainStep (pinned host buffers)",
+                      "sample": ("all units of the rank" if ne == U else
+                                 f"{ne} of the rank's {U} units per step (pinned host footprint); "
+                                 f"time and bytes scaled by {U}/{ne}")}
+    # ---- CPU baseline: the reference's own path on a bounded sample (rank 0, N=1)
     if not args.no_cpu_baseline and rank == 0 and world == 1:
         try:
             threads = os.cpu_count() or 1
-            rcfg = CONFIGS[args.config]
-            if rcfg[2] % rcfg[4]:  # the reference needs b | N: time the padded length
-                rcfg = rcfg[:2] + ((rcfg[2] + rcfg[4] - 1) // rcfg[4] * rcfg[4],) + rcfg[3:]
-            tsec, kind, threads = time_reference_head(rcfg, threads)
-            out["cpu_baseline"] = {"value": dense_equiv_flops(1, 1, N, d) / tsec / 1e12, "unit": "TFLOPS",
+            rcfg = reference_cfg(args.config)
+            tsec, kind, threads = time_reference_unit(rcfg, threads, reference_unit_inputs(rcfg[2], d, 0))
+            out["cpu_baseline"] = {"value": dense_equiv_flops(1, 1, rcfg[2], d) / tsec / 1e12, "unit": "TFLOPS",
                                    "cores": threads, "kind": kind,
-                                   "sample": f"one (batch, head) unit of {B * H}: fwd+bwd f32 in {tsec:.2f} s"}
+                                   "sample": f"one (batch, head) unit of {runner.n_units}: fwd+bwd f32 in {tsec:.2f} s"}
         except Exception as e:  # pragma: no cover
             out["cpu_baseline"] = {"error": str(e)[:200]}
     if rank == 0:

@@ -92,11 +92,13 @@ void require_supported(const sla_b200_problem* p, const Dims& D) {
   if (!generic_supported(D, &why)) throw InvalidArgument(why);
 }
 
+// counts_launches: the call launches kernels, so sla_b200_last_launch_count() restarts at 0
+// (queries such as sla_b200_state_labels leave the previous call's count readable)
 template <typename F>
-int guarded(F&& f) {
+int guarded(F&& f, bool counts_launches = true) {
   try {
     g_last_error.clear();
-    g_launches = 0;
+    if (counts_launches) g_launches = 0;
     f();
     return SLA_B200_OK;
   } catch (const InvalidArgument& e) {
@@ -246,7 +248,7 @@ int sla_b200_validate(const sla_b200_problem* p) {
   return guarded([&] {
     const Dims D = resolve(p);
     require_supported(p, D);
-  });
+  }, false);
 }
 
 int sla_b200_sizes(const sla_b200_problem* p, size_t* state_bytes, size_t* workspace_bytes) {
@@ -258,7 +260,7 @@ int sla_b200_sizes(const sla_b200_problem* p, size_t* state_bytes, size_t* works
     const bool fast = use_fast(p, D);
     carve_state(D, fast, nullptr, s, state_bytes);
     carve_work(D, fast, nullptr, w, workspace_bytes);
-  });
+  }, false);
 }
 
 int sla_b200_query(const sla_b200_problem* p, sla_b200_info* info) {
@@ -272,7 +274,7 @@ int sla_b200_query(const sla_b200_problem* p, sla_b200_info* info) {
     info->t_m = D.Tm;
     info->t_n = D.Tn;
     info->gpu_launches = g_launches;
-  });
+  }, false);
 }
 
 int sla_b200_classify(const sla_b200_problem* p, const void* q, const void* k, int8_t* labels,
@@ -572,7 +574,7 @@ int sla_b200_state_labels(const sla_b200_problem* p, const void* state, const in
     StateBufs s;
     carve_state(D, use_fast(p, D), const_cast<void*>(state), s, nullptr);
     if (labels) *labels = s.labels;
-  });
+  }, false);
 }
 
 }  // extern "C"

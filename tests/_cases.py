@@ -54,3 +54,17 @@ def c2_qk(seed: int, is_peaked: bool, n: int = 32768, d: int = 128):
     if is_peaked:
         return bf(peaked(rng, n, d)), bf(peaked(rng, n, d))
     return bf(rng.gaussian(n, d)), bf(rng.gaussian(n, d))
+
+
+def log_err(key, err, **extra):
+    """Append a measured error to $SLA_PARITY_LOG (JSON lines) -- the source of the gates."""
+    import json
+    import os
+
+    path = os.environ.get("SLA_PARITY_LOG")
+    if not path:
+        return
+    row = {"test": os.environ.get("PYTEST_CURRENT_TEST", "").split(" ")[0], "key": key, "err": float(err)}
+    row.update(extra)
+    with open(path, "a") as f:
+        f.write(json.dumps(row) + "\n")

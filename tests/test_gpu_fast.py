@@ -1,17 +1,20 @@
 """GPU parity of the tcgen05 fast path (b_q = b_kv = 64, d in {64, 128}, bf16) against the C
 oracle on the same bf16-exact inputs, including the edge cases the reference pins.
 
-Tolerance: rel_diff (floor 1.0) <= 2e-2 for outputs and gradients -- bf16 operands (Q, K, V,
-P, phi(Q), H, W) with fp32 accumulation and bf16 outputs; lse within 2e-3 absolute."""
+Tolerance: rel_diff (floor 1.0) <= 1.2e-2 for outputs and gradients -- bf16 operands (Q, K, V,
+P, phi(Q), H, W) with fp32 accumulation and bf16 outputs; lse within 5e-6 absolute.  Measured on
+B200 (profiles/r02_parity_small.md): worst rel_diff 5.3e-3 (dq_total), lse 1.2e-6."""
 import numpy as np
 import pytest
 import torch
 
+import _cases as cases
 from oracle import oracle as O
 from paper_2509_24006_b200 import SLA, SlaConfig
 
 pytestmark = pytest.mark.gpu
-TOL = 2e-2
+TOL = 1.2e-2
+LSE_TOL = 5e-6
 
 
 def _inputs(seed, n, d, units=1):
@@ -46,18 +49,22 @@ def _check_unit(st, g, h, x, w, lab, phi, with_w=True, backward=True):
     f = lambda t: t.double().cpu().numpy()  # noqa: E731
     for name, got in (("o_s", st.o_s[0, h]), ("o_l", st.o_l[0, h])):
         err = O.rel_diff(f(got), want[name], 1.0)
+        cases.log_err(name, err, tol=TOL)
         assert err <= TOL, f"{name} {err:.3e}"
     if with_w:
         err = O.rel_diff(f(st.o[0, h]), want["o"], 1.0)
+        cases.log_err("o", err, tol=TOL)
         assert err <= TOL, f"o {err:.3e}"
     lse = st.lse[0, h].cpu().numpy()
     live = want["lse"] > -1e299
     assert (lse[~live] == np.float32(-1e30)).all()
     if live.any():
-        assert np.abs(lse[live] - want["lse"][live]).max() <= 2e-3
+        cases.log_err("lse", np.abs(lse[live] - want["lse"][live]).max(), tol=LSE_TOL)
+        assert np.abs(lse[live] - want["lse"][live]).max() <= LSE_TOL
     if backward:
         for name, got in (("dq_total", g.dq_total[0, h]), ("dk_total", g.dk_total[0, h]), ("dv", g.dv[0, h])):
             err = O.rel_diff(f(got), want[name], 1.0)
+            cases.log_err(name, err, tol=TOL)
             assert err <= TOL, f"{name} {err:.3e}"
     return want
 

@@ -5,7 +5,8 @@ Tolerances (rel_diff = max|a-b| / max(max|b|, 1), mat.hpp:169-178 with floor 1.0
   * labels: bit-exact (f64 mask path); the f32 mask variant may only flip near-ties.
   * f32 inputs (generic kernels, fp32 arithmetic): 1e-4, the reference's own f32 gate
     (acceptance_main.cpp:51-102).
-  * bf16 inputs (fp32 accumulation, bf16 outputs): 2e-2 for outputs and gradients.
+  * bf16 inputs (fp32 accumulation, bf16 outputs): 1.5e-2 for outputs and gradients (measured
+    worst 6.7e-3, dq_total at b = 64 d = 64; profiles/r02_parity_small.md), lse 1e-4.
 """
 import os
 
@@ -20,6 +21,8 @@ from paper_2509_24006_b200 import SLA, SlaConfig
 pytestmark = pytest.mark.gpu
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 DEV = "cuda"
+BF16_TOL = 1.5e-2
+BF16_LSE_TOL = 1e-4
 
 
 def _t(x, dtype):
@@ -53,6 +56,7 @@ def _run_step(x, b, phi, dtype, labels=None, k_h=5.0, k_l=10.0, generic=False, p
 def _close(got, want, tol, keys=("o", "o_s", "o_l", "dq_total", "dk_total", "dv", "dw")):
     for key in keys:
         err = O.rel_diff(got[key], want[key], 1.0)
+        cases.log_err(key, err, tol=tol)
         assert err <= tol, f"{key}: rel_diff {err:.3e} > {tol}"
 
 
@@ -60,6 +64,7 @@ def _lse_close(got, want, tol):
     live = want > -1e29
     assert np.all(got[~live] == np.float32(-1e30))
     if live.any():
+        cases.log_err("lse", np.abs(got[live] - want[live]).max(), tol=tol)
         assert np.abs(got[live] - want[live]).max() <= tol
 
 
@@ -149,8 +154,8 @@ def test_step_bf16_matches_oracle(c):
     x = {k: (O.to_bf16_exact(v) if v.dtype != np.int8 else v) for k, v in cases.small_inputs(c).items()}
     got, _ = _run_step(x, c["b"], c["phi"], torch.bfloat16, labels=x["labels"])
     want = O.step(x["q"], x["k"], x["v"], x["w"], x["do"], x["labels"], c["b"], c["b"], c["phi"])
-    _close(got, want, 2e-2)
-    _lse_close(got["lse"], want["lse"], 2e-3)
+    _close(got, want, BF16_TOL)
+    _lse_close(got["lse"], want["lse"], BF16_LSE_TOL)
 
 
 def test_step_parts_match_oracle():
@@ -168,9 +173,9 @@ def test_c1_step_bf16_matches_reference():
         x = cases.c1_inputs(h)
         got, op = _run_step(x, 64, cases.C1["phi"], torch.bfloat16)
         assert (got["labels"] == g[f"h{h}/labels"]).all()
-        _lse_close(got["lse"], g[f"h{h}/lse"], 2e-3)
+        _lse_close(got["lse"], g[f"h{h}/lse"], BF16_LSE_TOL)
         if h == 0:
-            _close(got, {k: g[f"h0/{k}"] for k in ("o", "dq_total", "dk_total", "dv", "dw")}, 2e-2,
+            _close(got, {k: g[f"h0/{k}"] for k in ("o", "dq_total", "dk_total", "dv", "dw")}, BF16_TOL,
                    keys=("o", "dq_total", "dk_total", "dv", "dw"))
 
 

@@ -1,7 +1,8 @@
-"""CPU tests of the multi-rank path (world_size 2, gloo): (batch x head) partitioning, the
-validation gather, and that sharded per-unit results equal the single-process run.  The per-unit
-compute here is the C oracle (test infrastructure) -- the property under test is the host-side
-sharding logic that bench.py and the GPU runner use with NCCL."""
+"""CPU tests of the multi-rank path (world_size 2, gloo): the same `ShardedStep` runner that
+bench.py drives with NCCL and `CudaUnits`, here with the per-unit compute plugged to the C
+oracle (test infrastructure).  Under test: the (batch x head) partition, the dW all-reduce over
+a head's batch elements split across ranks (backward.cpp:46 summed over the batch), and the
+validation gathers -- sharded results must equal the one-rank run bit for bit."""
 import os
 import socket
 
@@ -11,7 +12,10 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
+from paper_2509_24006_b200.runner import ShardedStep, UnitCompute, unit_seed
 from paper_2509_24006_b200.shard import batch_slices, gather_units, partition_units
+
+N, D, BLK = 64, 8, 16
 
 
 @pytest.mark.parametrize("n,world", [(12, 8), (320, 8), (5, 2), (2, 4), (1, 1)])
@@ -30,44 +34,83 @@ def test_batch_slices_order():
     assert pairs[0] == (3, 0) and pairs[-1] == (3, 39)
 
 
+class OracleUnits(UnitCompute):
+    """Per-unit fwd+bwd through the C oracle: O.step on seeded inputs (unit_seed)."""
+
+    def __init__(self, shard, heads):
+        self.shard, self.heads = shard, heads
+
+    def step(self):
+        from oracle import oracle as O
+
+        outs = {"o": [], "dq": [], "dk": [], "dv": []}
+        dws = []
+        for u in self.shard.units:
+            rng = O.Rng(unit_seed(700, u))
+            q, k, v, do = (rng.gaussian(N, D) for _ in range(4))
+            w = O.Rng(unit_seed(701, 1_000_000 + u % self.heads)).gaussian(D, D, 0.1)
+            lab = O.dynamic_labels(q, k, BLK, BLK, 25.0, 25.0)
+            r = O.step(q, k, v, w, do, lab, BLK, BLK, "softmax")
+            for nm, key in (("o", "o"), ("dq", "dq_total"), ("dk", "dk_total"), ("dv", "dv")):
+                outs[nm].append(r[key])
+            dws.append(r["dw"])
+        mk = lambda xs, shp: torch.tensor(np.stack(xs)) if xs else torch.zeros((0,) + shp, dtype=torch.float64)  # noqa: E731
+        self._out = {nm: mk(xs, (N, D)) for nm, xs in outs.items()}
+        self._dw = mk(dws, (D, D))
+
+    def dw_units(self):
+        return self._dw
+
+    def outputs(self):
+        return self._out
+
+
+def _run(batch, heads, world, rank):
+    st = ShardedStep(batch, heads, D, world, rank)
+    st.attach(OracleUnits(st.shard, heads))
+    st.step()
+    res = {"dw": st.dw.clone(), "sums": st.gather_checksums(), "dq": st.gather_outputs("dq")}
+    return res
+
+
 def _free_port():
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
         return sk.getsockname()[1]
 
 
-def _unit_result(u):
-    """A (batch, head) unit's forward output through the C oracle (seeded, deterministic)."""
-    from oracle import oracle as O
-
-    rng = O.Rng(700 + u)
-    n, d, b = 64, 8, 16
-    q, k, v = rng.gaussian(n, d), rng.gaussian(n, d), rng.gaussian(n, d)
-    lab = O.dynamic_labels(q, k, b, b, 25.0, 25.0)
-    st = O.forward(q, k, v, lab, b, b, "softmax")
-    return np.concatenate([st["o_s"], st["o_l"]], 1)
-
-
-def _worker(rank, world, port, n_units, out_path):
+def _worker(rank, world, port, batch, heads, out_path):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        shard = partition_units(n_units, world, rank)
-        local = torch.tensor(np.stack([_unit_result(u) for u in shard.units]) if shard.count else
-                             np.zeros((0, 64, 16)), dtype=torch.float64)
-        full = gather_units(local, shard, n_units)
+        res = _run(batch, heads, world, rank)
         if rank == 0:
-            np.save(out_path, full.numpy())
+            torch.save(res, out_path)
+        else:
+            assert res["sums"] is None and res["dq"] is None
+            torch.save(res["dw"], out_path + ".r1")
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n_units", [3, 4])
-def test_sharded_run_matches_single_process(tmp_path, n_units):
-    out = str(tmp_path / "gathered.npy")
-    mp.spawn(_worker, args=(2, _free_port(), n_units, out), nprocs=2, join=True)
-    got = np.load(out)
-    want = np.stack([_unit_result(u) for u in range(n_units)])
-    assert got.shape == want.shape
-    assert (got == want).all()
+@pytest.mark.parametrize("batch,heads", [(1, 3), (2, 2), (3, 1)])
+def test_sharded_step_matches_single_process(tmp_path, batch, heads):
+    """2 ranks (gloo) against 1: per-unit checksums, gathered dQ and the per-head dW (whose
+    batch elements straddle the ranks for (2, 2) and (3, 1)) must equal the one-rank run."""
+    out = str(tmp_path / "res.pt")
+    mp.spawn(_worker, args=(2, _free_port(), batch, heads, out), nprocs=2, join=True)
+    got = torch.load(out)
+    want = _run(batch, heads, 1, 0)
+    assert torch.equal(got["sums"], want["sums"])
+    assert torch.equal(got["dq"], want["dq"])
+    # dW: the all-reduce of per-rank partial sums may order the batch additions differently
+    assert torch.allclose(got["dw"], want["dw"], rtol=1e-12, atol=1e-14)
+    assert torch.allclose(torch.load(out + ".r1"), want["dw"], rtol=1e-12, atol=1e-14)
+
+
+def test_gather_units_uneven():
+    """gather_units on a single process (world 1) is the identity."""
+    s = partition_units(3, 1, 0)
+    x = torch.arange(6.0).view(3, 2)
+    assert torch.equal(gather_units(x, s, 3), x)
