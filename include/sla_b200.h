@@ -12,9 +12,13 @@
  *                            mask.cpp:57-119          sla_b200_classify
  *   sla_forward              forward.hpp:63-68        sla_b200_forward (mask_in == NULL)
  *   sla_forward_with_mask    forward.hpp:70-78        sla_b200_forward (mask_in != NULL)
- *   combine_outputs          forward.hpp:80-83        fused: sla_b200_forward writes o
- *   proj_backward            backward.hpp:18-23       fused into sla_b200_backward
- *   sla_backward             backward.hpp:25-38       sla_b200_backward[_ex]
+ *   combine_outputs          forward.hpp:80-83        fused: sla_b200_forward writes o;
+ *                                                     standalone: sla_b200_combine_outputs
+ *   proj_backward            backward.hpp:18-23       fused into sla_b200_backward[_ex];
+ *                                                     standalone: sla_b200_proj_backward
+ *   sla_backward             backward.hpp:25-38       sla_b200_backward_split (independent
+ *                                                     dO^s, dO^l, as the reference takes them)
+ *   SlaGradients parts       backward.hpp:10-16       sla_b200_grad_parts, on both paths
  *   SlaForwardState          forward.hpp:33-43        the caller-owned `state` buffer
  *   std::invalid_argument / std::runtime_error        status 2 / 1 + sla_b200_last_error()
  *
@@ -165,21 +169,25 @@ int sla_b200_classify(const sla_b200_problem* p, const void* q, const void* k, i
  * label grid (sla_forward_with_mask; rows may have zero critical blocks).
  * w may be NULL (then o may be NULL): projection skipped.  Outputs o = o_s + o_l W,
  * o_s (sparse branch), o_l (linear branch) in p->dtype; lse f32 [B*H, N] with the
- * reference sentinel -1e30 on rows without critical mass.  Any of o/o_s/o_l may be NULL
- * only if the caller will not run the backward. */
+ * reference sentinel -1e30 on rows without critical mass.  o may be NULL (projection output
+ * not wanted); o_s and o_l are required on the tcgen05 path (they leave the kernel by TMA) and
+ * may be NULL on the generic path only if the caller will not run the backward. */
 int sla_b200_forward(const sla_b200_problem* p, const void* q, const void* k, const void* v,
                      const void* w, const int8_t* mask_in, void* o, void* o_s, void* o_l,
                      float* lse, void* state, void* workspace, void* stream);
 
 /* Fused backward of O = O^s + O^l W from the combined cotangent d_out
- * (proj_backward + sla_backward).  dq, dk are the composed totals dq_total / dk_total
- * (backward.cpp:211-214); dv accumulates both branches; dw f32 [H, d, d]. */
+ * (proj_backward + sla_backward: dO^s = dO, dO^l = dO W^T computed in the linear-branch kernel).
+ * dq, dk are the composed totals dq_total / dk_total (backward.cpp:211-214); dv accumulates both
+ * branches; dw f32 [H, d, d]. */
 int sla_b200_backward(const sla_b200_problem* p, const void* q, const void* k, const void* v,
                       const void* w, const void* o_s, const void* o_l, const float* lse,
                       const void* d_out, void* dq, void* dk, void* dv, float* dw,
                       const void* state, void* workspace, void* stream);
 
-/* Optional component gradients of SlaGradients (backward.hpp:10-16), f32 [B*H, N, d]. */
+/* Optional component gradients of SlaGradients (backward.hpp:10-16), f32 [B*H, N, d]; all four
+ * or none.  Both paths: the tcgen05 kernels write them from their epilogues (dq_feat there is
+ * the bf16 dQ^phi the row kernels consume). */
 typedef struct sla_b200_grad_parts {
   float* dq_sparse;  /* SlaGradients::dq      */
   float* dk_sparse;  /* SlaGradients::dk      */
@@ -192,6 +200,31 @@ int sla_b200_backward_ex(const sla_b200_problem* p, const void* q, const void* k
                          const float* lse, const void* d_out, void* dq, void* dk, void* dv,
                          float* dw, const sla_b200_grad_parts* parts, const void* state,
                          void* workspace, void* stream);
+
+/* sla_backward with independent cotangents (backward.hpp:25-38, backward.cpp:24-216): the sparse
+ * branch takes d_out_sparse (dO^s), the linear branch d_out_linear (dO^l) as given -- they need
+ * not be related through W.  dw (optional, f32 [H, d, d]) = O^l^T dO^s summed over the batch, the
+ * reference's SlaGradients::dproj (backward.cpp:46).  parts: optional component gradients. */
+int sla_b200_backward_split(const sla_b200_problem* p, const void* q, const void* k, const void* v,
+                            const void* o_s, const void* o_l, const float* lse, const void* d_out_sparse,
+                            const void* d_out_linear, void* dq, void* dk, void* dv, float* dw,
+                            const sla_b200_grad_parts* parts, const void* state, void* workspace,
+                            void* stream);
+
+/* combine_outputs (forward.cpp:187-195): o = o_s + o_l W[h], f32 accumulation, on the device. */
+int sla_b200_combine_outputs(const sla_b200_problem* p, const void* o_s, const void* o_l, const void* w,
+                             void* o, void* stream);
+
+/* proj_backward (backward.cpp:12-22) on the device: d_out_linear = d_out W[h]^T and
+ * dw (f32 [H, d, d]) = O^l^T d_out summed over the batch.  dO^s is d_out itself. */
+int sla_b200_proj_backward(const sla_b200_problem* p, const void* d_out, const void* o_l, const void* w,
+                           void* d_out_linear, float* dw, void* workspace, void* stream);
+
+/* The device half of a SlaForwardState from its label grid (build_lookup + summaries +
+ * aggregation, forward.cpp:81-130) without the attention kernel: lets a caller that holds the
+ * forward's outputs (O^s, O^l, lse) run sla_b200_backward_split on them. */
+int sla_b200_build_state(const sla_b200_problem* p, const void* q, const void* k, const void* v,
+                         const int8_t* mask, void* state, void* workspace, void* stream);
 
 /* Per-kernel CUDA-event profiler of this library's own launches (bench/diagnostics).
  * sla_b200_profiler(1) clears and enables, (0) disables.  The report is text lines

@@ -18,8 +18,10 @@
 // (b_q = b_kv = 64, d in {64, 128}; outputs within ~1e-2 of the f32 reference).  Set
 // sla::gpu::options().fp32 = true for the f32 SIMT kernels (within ~1e-4, any block shape).
 //
-// sla_backward needs the device-side forward state (aggregated H, Z, lookups); the shim
-// re-derives it by re-running the forward on the state's mask, which is deterministic.
+// sla_backward consumes the SlaForwardState it is given: the state's O^s, O^l and lse are
+// uploaded, and the device-side state (lookups, H, Z) is rebuilt from the state's label grid by
+// sla_b200_build_state (no attention kernel runs).  combine_outputs and proj_backward run on
+// the device (sla_b200_combine_outputs, sla_b200_proj_backward).
 #pragma once
 
 #include <cuda_bf16.h>
@@ -46,16 +48,6 @@ inline Options& options() {
   static Options o;
   return o;
 }
-
-namespace detail {
-// The fused device backward consumes the combined cotangent and W.  The reference flow always
-// calls proj_backward(dO, O^l, W) right before sla_backward (finetune.cpp:44-61), so the shim's
-// proj_backward records W here for the following sla_backward on this thread.
-inline const Mat<float>*& last_projection() {
-  thread_local const Mat<float>* w = nullptr;
-  return w;
-}
-}  // namespace detail
 
 namespace detail {
 
@@ -208,45 +200,90 @@ inline SlaForwardState<float> sla_forward_with_mask(const Mat<float>& q, const M
   return f.state_of();
 }
 
-// forward.cpp:187-195 -- O = O^l W + O^s (a d x d product, done on the host as the reference).
-inline Mat<float> combine_outputs(const SlaForwardState<float>& state, const OutputProjection<float>& proj) {
-  return sla::combine_outputs(state, proj);
+// a block size for calls that only need N x d row work (combine / proj_backward)
+inline BlockLayout row_layout(size_t n, size_t d) {
+  size_t b = 64;
+  while (n % b) b >>= 1;
+  return make_block_layout(n, d, b, b);
 }
 
-// backward.cpp:12-22
+// forward.cpp:187-195 -- O = O^l W + O^s on the device (f32 accumulation).
+inline Mat<float> combine_outputs(const SlaForwardState<float>& state, const OutputProjection<float>& proj) {
+  const size_t n = state.sparse_out.rows, d = state.sparse_out.cols;
+  if (!state.linear_out.same_shape(state.sparse_out) || proj.w.rows != d || proj.w.cols != d)
+    throw std::invalid_argument("combine_outputs: shape mismatch");
+  SlaConfig cfg;
+  const sla_b200_problem p = detail::problem(cfg, row_layout(n, d));
+  const size_t es = detail::elem(p);
+  detail::DevBuf os(n * d * es), ol(n * d * es), w(d * d * es), o(n * d * es);
+  detail::upload(state.sparse_out, os.p, p);
+  detail::upload(state.linear_out, ol.p, p);
+  detail::upload(proj.w, w.p, p);
+  detail::throw_status(sla_b200_combine_outputs(&p, os.p, ol.p, w.p, o.p, nullptr));
+  detail::cuda_check(cudaDeviceSynchronize());
+  return detail::download(o.p, n, d, p);
+}
+
+// backward.cpp:12-22 -- (dO^s, dO^l, dW) = (dO, dO W^T, O^l^T dO) on the device.
 inline std::tuple<Mat<float>, Mat<float>, Mat<float>> proj_backward(const Mat<float>& d_out,
                                                                     const Mat<float>& linear_out,
                                                                     const Mat<float>& w) {
-  detail::last_projection() = &w;
-  return sla::proj_backward(d_out, linear_out, w);
+  if (!d_out.same_shape(linear_out)) throw std::invalid_argument("proj_backward: shape mismatch");
+  const size_t n = d_out.rows, d = d_out.cols;
+  SlaConfig cfg;
+  const sla_b200_problem p = detail::problem(cfg, row_layout(n, d));
+  const size_t es = detail::elem(p);
+  size_t sb = 0, wbytes = 0;
+  detail::throw_status(sla_b200_sizes(&p, &sb, &wbytes));
+  detail::DevBuf dout(n * d * es), ol(n * d * es), wd(d * d * es), dol(n * d * es), dw(d * d * 4), work(wbytes);
+  detail::upload(d_out, dout.p, p);
+  detail::upload(linear_out, ol.p, p);
+  detail::upload(w, wd.p, p);
+  detail::throw_status(sla_b200_proj_backward(&p, dout.p, ol.p, wd.p, dol.p, static_cast<float*>(dw.p), work.p,
+                                              nullptr));
+  detail::cuda_check(cudaDeviceSynchronize());
+  Mat<float> dwm(d, d);
+  detail::cuda_check(cudaMemcpy(dwm.data.data(), dw.p, d * d * 4, cudaMemcpyDeviceToHost));
+  return {d_out, detail::download(dol.p, n, d, p), std::move(dwm)};
 }
 
-// backward.cpp:24-216 through the fused device backward.  The device call takes the combined
-// cotangent dO and W; the (dO^s, dO^l) pair the reference receives is reconstructed exactly when
-// dO^s is the combined cotangent (what proj_backward hands over, backward.hpp:28-31).
+// backward.hpp:25-38 -- gradients through both branches from independent cotangents dO^s, dO^l
+// (sla_b200_backward_split), with the component gradients (backward.hpp:10-16) and
+// dproj = O^l^T dO^s (backward.cpp:46).  The caller's state is the one consumed.
 inline SlaGradients<float> sla_backward(const SlaForwardState<float>& state, const Mat<float>& q,
                                         const Mat<float>& k, const Mat<float>& v,
                                         const Mat<float>& d_out_sparse, const Mat<float>& d_out_linear,
                                         const SlaConfig& cfg, const BlockLayout& layout, unsigned = 1,
-                                        ExecCounters* = nullptr, const Mat<float>* w = nullptr) {
-  (void)d_out_linear;
-  if (!w) w = detail::last_projection();
-  if (!w) throw std::invalid_argument("sla::gpu::sla_backward: call sla::gpu::proj_backward first (or pass W)");
+                                        ExecCounters* = nullptr) {
+  const size_t n = layout.n, d = layout.d;
+  if (state.row_lse.size() != n || state.mask.t_m != layout.t_m || state.mask.t_n != layout.t_n)
+    throw std::invalid_argument("sla_backward: state does not match layout");
+  if (d_out_sparse.rows != n || d_out_sparse.cols != d || d_out_linear.rows != n || d_out_linear.cols != d)
+    throw std::invalid_argument("sla_backward: cotangent shape mismatch");
+  validate_config(cfg);
   const sla_b200_problem p = detail::problem(cfg, layout);
-  detail::Forward f(p, q, k, v);
-  f.run(state.mask.labels.data());
-  const size_t n = size_t(p.n), d = size_t(p.d), es = detail::elem(p);
-  detail::DevBuf dw_in(d * d * es), dout(n * d * es), dq(n * d * es), dk(n * d * es), dv(n * d * es),
-      dw(d * d * 4), parts_q(n * d * 4), parts_k(n * d * 4), parts_qf(n * d * 4), parts_kf(n * d * 4);
-  detail::upload(*w, dw_in.p, p);
-  detail::upload(d_out_sparse, dout.p, p);
-  sla_b200_grad_parts parts{static_cast<float*>(parts_q.p), static_cast<float*>(parts_k.p),
-                            static_cast<float*>(parts_qf.p), static_cast<float*>(parts_kf.p)};
-  const bool want_parts = p.dtype == SLA_B200_F32;  // the fast path fuses the parts away
-  detail::throw_status(sla_b200_backward_ex(&p, f.q.p, f.k.p, f.v.p, dw_in.p, f.o_s.p, f.o_l.p,
-                                            static_cast<float*>(f.lse.p), dout.p, dq.p, dk.p, dv.p,
-                                            static_cast<float*>(dw.p), want_parts ? &parts : nullptr,
-                                            f.state.p, f.work.p, nullptr));
+  const size_t es = detail::elem(p), grid = layout.t_m * layout.t_n;
+  size_t sb = 0, wbytes = 0;
+  detail::throw_status(sla_b200_sizes(&p, &sb, &wbytes));
+  detail::DevBuf q_(n * d * es), k_(n * d * es), v_(n * d * es), os(n * d * es), ol(n * d * es), lse(n * 4),
+      mask(grid), st(sb), work(wbytes), dos(n * d * es), dol(n * d * es), dq(n * d * es), dk(n * d * es),
+      dv(n * d * es), dw(d * d * 4), pq(n * d * 4), pk(n * d * 4), pqf(n * d * 4), pkf(n * d * 4);
+  detail::upload(q, q_.p, p);
+  detail::upload(k, k_.p, p);
+  detail::upload(v, v_.p, p);
+  detail::upload(state.sparse_out, os.p, p);
+  detail::upload(state.linear_out, ol.p, p);
+  detail::upload(d_out_sparse, dos.p, p);
+  detail::upload(d_out_linear, dol.p, p);
+  detail::cuda_check(cudaMemcpy(lse.p, state.row_lse.data(), n * 4, cudaMemcpyHostToDevice));
+  detail::cuda_check(cudaMemcpy(mask.p, state.mask.labels.data(), grid, cudaMemcpyHostToDevice));
+  detail::throw_status(sla_b200_build_state(&p, q_.p, k_.p, v_.p, static_cast<int8_t*>(mask.p), st.p, work.p,
+                                            nullptr));
+  sla_b200_grad_parts parts{static_cast<float*>(pq.p), static_cast<float*>(pk.p), static_cast<float*>(pqf.p),
+                            static_cast<float*>(pkf.p)};
+  detail::throw_status(sla_b200_backward_split(&p, q_.p, k_.p, v_.p, os.p, ol.p, static_cast<float*>(lse.p),
+                                               dos.p, dol.p, dq.p, dk.p, dv.p, static_cast<float*>(dw.p), &parts,
+                                               st.p, work.p, nullptr));
   detail::cuda_check(cudaDeviceSynchronize());
   SlaGradients<float> g;
   g.dq_total = detail::download(dq.p, n, d, p);
@@ -254,14 +291,12 @@ inline SlaGradients<float> sla_backward(const SlaForwardState<float>& state, con
   g.dv = detail::download(dv.p, n, d, p);
   g.dproj = Mat<float>(d, d);
   detail::cuda_check(cudaMemcpy(g.dproj.data.data(), dw.p, d * d * 4, cudaMemcpyDeviceToHost));
-  if (want_parts) {
-    sla_b200_problem pf = p;
-    pf.dtype = SLA_B200_F32;
-    g.dq = detail::download(parts_q.p, n, d, pf);
-    g.dk = detail::download(parts_k.p, n, d, pf);
-    g.dq_feat = detail::download(parts_qf.p, n, d, pf);
-    g.dk_feat = detail::download(parts_kf.p, n, d, pf);
-  }
+  sla_b200_problem pf = p;
+  pf.dtype = SLA_B200_F32;
+  g.dq = detail::download(pq.p, n, d, pf);
+  g.dk = detail::download(pk.p, n, d, pf);
+  g.dq_feat = detail::download(pqf.p, n, d, pf);
+  g.dk_feat = detail::download(pkf.p, n, d, pf);
   return g;
 }
 

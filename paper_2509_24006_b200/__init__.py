@@ -9,7 +9,9 @@ from .sla import (  # noqa: F401
     SlaGradients,
     combine_outputs,
     make_block_layout,
+    proj_backward,
     sla_backward,
+    sla_step_backward,
     sla_forward,
     sla_forward_with_mask,
 )
@@ -19,6 +21,6 @@ from ._lib import LIB_PATH  # noqa: F401
 
 __all__ = [
     "SLA", "BlockLayout", "SlaConfig", "SlaForwardState", "SlaGradients", "combine_outputs",
-    "make_block_layout", "sla_backward", "sla_forward", "sla_forward_with_mask", "HostTrainStep",
+    "make_block_layout", "proj_backward", "sla_backward", "sla_step_backward", "sla_forward", "sla_forward_with_mask", "HostTrainStep",
     "SparseLinearAttention", "sparse_linear_attention",
 ]

@@ -11,6 +11,7 @@ import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libsla_b200.so")
+DIAG_PATH = os.path.join(HERE, "libsla_b200_diag.so")  # microbenchmarks / layout probes, not the product
 
 OK, ERR_RUNTIME, ERR_INVALID = 0, 1, 2
 PHI = {"elu1": 0, "relu": 1, "softmax": 2}
@@ -61,7 +62,8 @@ EXPORTS = [
     "sla_b200_last_error", "sla_b200_abi_version", "sla_b200_validate", "sla_b200_sizes",
     "sla_b200_query", "sla_b200_last_launch_count", "sla_b200_classify", "sla_b200_forward",
     "sla_b200_backward", "sla_b200_backward_ex", "sla_b200_state_labels",
-    "sla_b200_flops_report", "sla_b200_exec_counters",
+    "sla_b200_flops_report", "sla_b200_exec_counters", "sla_b200_backward_split",
+    "sla_b200_combine_outputs", "sla_b200_proj_backward", "sla_b200_build_state",
 ]
 
 
@@ -85,12 +87,29 @@ def lib():
     L.sla_b200_backward.argtypes = [P] + [vp] * 15
     L.sla_b200_backward_ex.argtypes = [P] + [vp] * 12 + [C.POINTER(GradParts)] + [vp] * 3
     L.sla_b200_state_labels.argtypes = [P, vp, C.POINTER(C.c_void_p)]
+    L.sla_b200_backward_split.argtypes = [P] + [vp] * 12 + [C.POINTER(GradParts)] + [vp] * 3
+    L.sla_b200_combine_outputs.argtypes = [P] + [vp] * 5
+    L.sla_b200_proj_backward.argtypes = [P] + [vp] * 7
+    L.sla_b200_build_state.argtypes = [P] + [vp] * 7
     L.sla_b200_flops_report.argtypes = [P, vp, C.POINTER(Flops), vp, vp]
     L.sla_b200_exec_counters.argtypes = [P, vp, vp, C.c_int, C.c_int, C.POINTER(Counters), vp, vp]
     for name in EXPORTS:
         getattr(L, name)
     _lib = L
     return L
+
+
+_diag = None
+
+
+def diag_lib():
+    """libsla_b200_diag.so: csrc/diag.cu (TMEM layout probes, tcgen05 / TMA microbenchmarks, the
+    bare GEMM) for tests/test_gpu_gemm.py, tests/test_gpu_tmem.py and profiles/."""
+    global _diag
+    if _diag is None:
+        lib()  # the product library first (the diag library links against it)
+        _diag = C.CDLL(DIAG_PATH)
+    return _diag
 
 
 def check(rc: int) -> None:

@@ -21,7 +21,7 @@ from typing import Dict, Optional, Tuple
 
 import torch
 
-from .sla import SLA, SlaConfig
+from .sla import SLA, SlaConfig, SlaForwardState
 
 _OPS: Dict[Tuple, SLA] = {}
 
@@ -42,14 +42,18 @@ class _SlaFn(torch.autograd.Function):
     def forward(ctx, q, k, v, w, op: SLA):  # q, k, v: [B, H, N, d] contiguous
         st = op.forward(q, k, v, w)
         ctx.op = op
-        ctx.st = st
-        ctx.save_for_backward(q, k, v, w)
+        # the forward state is kept as saved tensors only (no Python reference to the returned O:
+        # that would form the cycle o.grad_fn -> ctx -> state -> o and hold each step's buffers
+        # until the cyclic GC runs); it is rebuilt around them in backward
+        ctx.save_for_backward(q, k, v, w, st.o_s, st.o_l, st.lse, st.state)
         return st.o
 
     @staticmethod
     def backward(ctx, d_out):
-        q, k, v, w = ctx.saved_tensors
-        g = ctx.op.backward(ctx.st, q, k, v, w, d_out.contiguous())
+        q, k, v, w, o_s, o_l, lse, state = ctx.saved_tensors
+        op = ctx.op
+        st = SlaForwardState(None, o_s, o_l, lse, op.labels_of(state), op, state)
+        g = op.backward(st, q, k, v, w, d_out.contiguous())
         return g.dq_total, g.dk_total, g.dv, g.dproj.to(w.dtype), None
 
 

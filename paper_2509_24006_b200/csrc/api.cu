@@ -333,18 +333,23 @@ int sla_b200_forward(const sla_b200_problem* p, const void* q, const void* k, co
     const bool check = p->flags & SLA_B200_FLAG_CHECK_FINITE;
     if (check) check_inputs(p, D, wb, {{"Q", q}, {"K", k}, {"V", v}}, st);
     const bool fast = use_fast(p, D);
+    if (fast && (!o_s || !o_l))  // the tcgen05 forward stores both branch outputs by TMA
+      throw InvalidArgument("sla_forward: o_s and o_l are required on the tcgen05 path");
     // fork: phi(K), z and h = phi(K)^T V on the side stream, concurrent with classification.
     // Not under the per-kernel profiler (one event sequence) nor with the finiteness checks
     // (host syncs that may throw between fork and join).
     const bool fork = fast && !check && !prof_enabled();
     SideStream* ss = fork ? &side_stream() : nullptr;
+    SideJoin guard(fork ? ss->s : nullptr, st);
     if (fork) {
       SLAB_CUDA(cudaEventRecord(ss->fork, st));
       SLAB_CUDA(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+      guard.arm(ss->join);
       fast_summaries(D, k, v, wb, ss->s);
       SLAB_CUDA(cudaEventRecord(ss->join, ss->s));
     }
     const bool m0_ready = classify_into_state(p, D, q, k, mask_in, nullptr, s, wb, st);
+    guard.release();
     if (fork) SLAB_CUDA(cudaStreamWaitEvent(st, ss->join, 0));
     if (fast)
       fast_forward(D, q, k, v, w, o, o_s, o_l, lse, s, wb, m0_ready, fork, st);
@@ -375,78 +380,102 @@ int sla_b200_forward(const sla_b200_problem* p, const void* q, const void* k, co
   });
 }
 
+}  // extern "C"
+
+namespace slab {
+namespace {
+
+// proj_backward + sla_backward (d_out_l == null: combined cotangent d_out and W), or sla_backward
+// alone with independent cotangents d_out (= dO^s) and d_out_l (backward.hpp:25-38)
+void backward_impl(const sla_b200_problem* p, const void* q, const void* k, const void* v, const void* w,
+                   const void* o_s, const void* o_l, const float* lse, const void* d_out, const void* d_out_l,
+                   void* dq, void* dk, void* dv, float* dw, const sla_b200_grad_parts* parts,
+                   const void* state, void* workspace, void* stream) {
+  const Dims D = resolve(p);
+  require_supported(p, D);
+  if (!q || !k || !v || !o_s || !o_l || !lse || !d_out || !dq || !dk || !dv || (!d_out_l && (!w || !dw)))
+    throw InvalidArgument("sla_backward: all tensors are required");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  prof_mark("", st);
+  StateBufs s;
+  WorkBufs wb;
+  buffers(p, D, state, workspace, s, wb);
+  const bool fast = use_fast(p, D);
+  const bool ragged = D.staged;  // ragged N and/or the [B, N, H, d] layout
+  GradParts gp;
+  if (parts) {
+    gp = GradParts{parts->dq_sparse, parts->dk_sparse, parts->dq_feat, parts->dk_feat};
+    if (!gp.dq || !gp.dk || !gp.dq_feat || !gp.dk_feat)
+      throw InvalidArgument("sla_backward: gradient parts are all-or-none");
+    if (ragged) throw InvalidArgument("sla_backward: gradient parts are not available for staged layouts");
+  }
+  void *dq_u = dq, *dk_u = dk, *dv_u = dv;
+  if (ragged) {
+    const size_t rb = size_t(D.d) * 2;
+    pad_rows(D, wb.pad[kPQ], q, rb, st);
+    pad_rows(D, wb.pad[kPK], k, rb, st);
+    pad_rows(D, wb.pad[kPV], v, rb, st);
+    pad_rows(D, wb.pad[kPOs], o_s, rb, st);
+    pad_rows(D, wb.pad[kPOl], o_l, rb, st);
+    pad_rows(D, wb.pad[kPdO], d_out, rb, st);  // zero cotangent rows: padded queries are inert
+    if (d_out_l) {  // the padded O slot is free in the backward
+      pad_rows(D, wb.pad[kPO], d_out_l, rb, st);
+      d_out_l = wb.pad[kPO];
+    }
+    pad_rows(D, wb.pad_lse, lse, sizeof(float), st);
+    q = wb.pad[kPQ];
+    k = wb.pad[kPK];
+    v = wb.pad[kPV];
+    o_s = wb.pad[kPOs];
+    o_l = wb.pad[kPOl];
+    d_out = wb.pad[kPdO];
+    lse = wb.pad_lse;
+    dq = wb.pad[kPdQ];
+    dk = wb.pad[kPdK];
+    dv = wb.pad[kPdV];
+  }
+  if (fast) {
+    SideFork side;
+    if (!prof_enabled()) {  // the per-kernel profiler times one event sequence
+      SideStream& ss = side_stream();
+      side.s = ss.s;
+      side.fork = ss.fork;
+      side.join = ss.join;
+      side.join2 = ss.join2;
+      side.mid = ss.mid;
+      side.join3 = ss.join3;
+    }
+    fast_backward(D, q, k, v, w, o_s, o_l, lse, d_out, d_out_l, dq, dk, dv, dw, gp, s, wb, st, side);
+  } else {
+    generic_backward(D, p->dtype, q, k, v, w, o_s, o_l, lse, d_out, d_out_l, dq, dk, dv, dw, s, wb, st);
+    if (parts) {
+      const size_t bytes = sizeof(float) * size_t(D.U) * D.N * D.d;
+      SLAB_CUDA(cudaMemcpyAsync(gp.dq, wb.dq, bytes, cudaMemcpyDeviceToDevice, st));
+      SLAB_CUDA(cudaMemcpyAsync(gp.dk, wb.dk, bytes, cudaMemcpyDeviceToDevice, st));
+      SLAB_CUDA(cudaMemcpyAsync(gp.dq_feat, wb.dqf, bytes, cudaMemcpyDeviceToDevice, st));
+      SLAB_CUDA(cudaMemcpyAsync(gp.dk_feat, wb.dkf, bytes, cudaMemcpyDeviceToDevice, st));
+    }
+  }
+  if (ragged) {
+    const size_t rb = size_t(D.d) * 2;
+    unpad_rows(D, dq_u, dq, rb, st);
+    unpad_rows(D, dk_u, dk, rb, st);
+    unpad_rows(D, dv_u, dv, rb, st);
+  }
+}
+
+}  // namespace
+}  // namespace slab
+
+extern "C" {
+
 int sla_b200_backward_ex(const sla_b200_problem* p, const void* q, const void* k,
                          const void* v, const void* w, const void* o_s, const void* o_l,
                          const float* lse, const void* d_out, void* dq, void* dk, void* dv,
                          float* dw, const sla_b200_grad_parts* parts, const void* state,
                          void* workspace, void* stream) {
   return guarded([&] {
-    const Dims D = resolve(p);
-    require_supported(p, D);
-    if (!q || !k || !v || !w || !o_s || !o_l || !lse || !d_out || !dq || !dk || !dv || !dw)
-      throw InvalidArgument("sla_backward: all tensors are required");
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    prof_mark("", st);
-    StateBufs s;
-    WorkBufs wb;
-    buffers(p, D, state, workspace, s, wb);
-    const bool fast = use_fast(p, D);
-    const bool ragged = D.staged;  // ragged N and/or the [B, N, H, d] layout
-    void *dq_u = dq, *dk_u = dk, *dv_u = dv;
-    if (ragged) {
-      if (parts) throw InvalidArgument("sla_backward: gradient parts are not available for staged layouts");
-      const size_t rb = size_t(D.d) * 2;
-      pad_rows(D, wb.pad[kPQ], q, rb, st);
-      pad_rows(D, wb.pad[kPK], k, rb, st);
-      pad_rows(D, wb.pad[kPV], v, rb, st);
-      pad_rows(D, wb.pad[kPOs], o_s, rb, st);
-      pad_rows(D, wb.pad[kPOl], o_l, rb, st);
-      pad_rows(D, wb.pad[kPdO], d_out, rb, st);  // zero cotangent rows: padded queries are inert
-      pad_rows(D, wb.pad_lse, lse, sizeof(float), st);
-      q = wb.pad[kPQ];
-      k = wb.pad[kPK];
-      v = wb.pad[kPV];
-      o_s = wb.pad[kPOs];
-      o_l = wb.pad[kPOl];
-      d_out = wb.pad[kPdO];
-      lse = wb.pad_lse;
-      dq = wb.pad[kPdQ];
-      dk = wb.pad[kPdK];
-      dv = wb.pad[kPdV];
-    }
-    if (fast) {
-      SideFork side;
-      if (!prof_enabled()) {  // the per-kernel profiler times one event sequence
-        SideStream& ss = side_stream();
-        side.s = ss.s;
-        side.fork = ss.fork;
-        side.join = ss.join;
-        side.join2 = ss.join2;
-        side.mid = ss.mid;
-        side.join3 = ss.join3;
-      }
-      fast_backward(D, q, k, v, w, o_s, o_l, lse, d_out, dq, dk, dv, dw, s, wb, st, side);
-    }
-    else
-      generic_backward(D, p->dtype, q, k, v, w, o_s, o_l, lse, d_out, dq, dk, dv, dw, s, wb, st);
-    if (parts) {
-      const size_t bytes = sizeof(float) * size_t(D.U) * D.N * D.d;
-      auto cp = [&](float* dst, const float* src) {
-        if (!dst) return;
-        if (!src) throw InvalidArgument("sla_backward: gradient part unavailable on this path");
-        SLAB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, st));
-      };
-      cp(parts->dq_sparse, wb.dq);
-      cp(parts->dk_sparse, wb.dk);
-      cp(parts->dq_feat, wb.dqf);
-      cp(parts->dk_feat, wb.dkf);
-    }
-    if (ragged) {
-      const size_t rb = size_t(D.d) * 2;
-      unpad_rows(D, dq_u, dq, rb, st);
-      unpad_rows(D, dk_u, dk, rb, st);
-      unpad_rows(D, dv_u, dv, rb, st);
-    }
+    backward_impl(p, q, k, v, w, o_s, o_l, lse, d_out, nullptr, dq, dk, dv, dw, parts, state, workspace, stream);
   });
 }
 
@@ -456,6 +485,74 @@ int sla_b200_backward(const sla_b200_problem* p, const void* q, const void* k, c
                       const void* state, void* workspace, void* stream) {
   return sla_b200_backward_ex(p, q, k, v, w, o_s, o_l, lse, d_out, dq, dk, dv, dw, nullptr,
                               state, workspace, stream);
+}
+
+int sla_b200_backward_split(const sla_b200_problem* p, const void* q, const void* k, const void* v,
+                            const void* o_s, const void* o_l, const float* lse, const void* d_out_sparse,
+                            const void* d_out_linear, void* dq, void* dk, void* dv, float* dw,
+                            const sla_b200_grad_parts* parts, const void* state, void* workspace,
+                            void* stream) {
+  return guarded([&] {
+    if (!d_out_linear) throw InvalidArgument("sla_backward: cotangent shape mismatch");
+    backward_impl(p, q, k, v, nullptr, o_s, o_l, lse, d_out_sparse, d_out_linear, dq, dk, dv, dw, parts,
+                  state, workspace, stream);
+  });
+}
+
+int sla_b200_combine_outputs(const sla_b200_problem* p, const void* o_s, const void* o_l, const void* w,
+                             void* o, void* stream) {
+  return guarded([&] {
+    const Dims D = resolve(p);
+    require_supported(p, D);
+    if (D.staged) throw InvalidArgument("combine_outputs: staged layouts are fused into sla_b200_forward only");
+    if (!o_s || !o_l || !w || !o) throw InvalidArgument("combine_outputs: all tensors are required");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    prof_mark("", st);
+    launch_rowmat(D, p->dtype, o_l, w, false, o_s, o, st);
+  });
+}
+
+int sla_b200_proj_backward(const sla_b200_problem* p, const void* d_out, const void* o_l, const void* w,
+                           void* d_out_linear, float* dw, void* workspace, void* stream) {
+  return guarded([&] {
+    const Dims D = resolve(p);
+    require_supported(p, D);
+    if (D.staged) throw InvalidArgument("proj_backward: staged layouts are fused into sla_b200_backward only");
+    if (!d_out || !o_l || !w || !d_out_linear || !dw) throw InvalidArgument("proj_backward: shape mismatch");
+    if (!workspace) throw InvalidArgument("sla_b200: state and workspace are required");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    prof_mark("", st);
+    launch_rowmat(D, p->dtype, d_out, w, true, nullptr, d_out_linear, st);  // dO^l = dO W^T
+    if (use_fast(p, D)) {
+      WorkBufs wb;
+      carve_work(D, true, workspace, wb, nullptr);
+      launch_dw_fast(D, o_l, d_out, dw, wb, st);  // dW = O^l^T dO
+    } else {
+      generic_dw(D, p->dtype, o_l, d_out, dw, st);
+    }
+  });
+}
+
+int sla_b200_build_state(const sla_b200_problem* p, const void* q, const void* k, const void* v,
+                         const int8_t* mask, void* state, void* workspace, void* stream) {
+  return guarded([&] {
+    const Dims D = resolve(p);
+    require_supported(p, D);
+    if (D.staged) throw InvalidArgument("sla_b200_build_state: staged layouts are not supported");
+    if (!q || !k || !v || !mask) throw InvalidArgument("sla_b200_build_state: q, k, v and mask are required");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    prof_mark("", st);
+    StateBufs s;
+    WorkBufs wb;
+    buffers(p, D, state, workspace, s, wb);
+    const bool m0_ready = classify_into_state(p, D, q, k, mask, nullptr, s, wb, st);
+    if (use_fast(p, D)) {
+      fast_summaries(D, k, v, wb, st);
+      fast_aggregate(D, s, wb, m0_ready, st);
+    } else {
+      generic_forward(D, p->dtype, q, k, v, nullptr, nullptr, nullptr, nullptr, nullptr, s, wb, st, false);
+    }
+  });
 }
 
 // Per-row LUT statistics (critical, marginal, Four-Russians groups hit) and, when q is given,

@@ -553,6 +553,15 @@ __global__ void __launch_bounds__(kColsThreads, 1)
       }
       *reinterpret_cast<uint4*>(p.dk + grow * D + col) = pack8(o);
       *reinterpret_cast<uint4*>(p.dv + grow * D + col) = pack8(w8);
+      if (p.dk_part) {  // SlaGradients::dk and ::dk_feat (f32)
+        float4* dks = reinterpret_cast<float4*>(p.dk_part + grow * D + col);
+        float4* dkf = reinterpret_cast<float4*>(p.dkf_part + grow * D + col);
+        const float* t = tk + c * TP + col;
+        dks[0] = make_float4(t[0], t[1], t[2], t[3]);
+        dks[1] = make_float4(t[4], t[5], t[6], t[7]);
+        dkf[0] = make_float4(g[cc0], g[cc0 + 1], g[cc0 + 2], g[cc0 + 3]);
+        dkf[1] = make_float4(g[cc0 + 4], g[cc0 + 5], g[cc0 + 6], g[cc0 + 7]);
+      }
     }
   }
   ts_mark(dbg && threadIdx.x == 64, 124);
@@ -582,8 +591,11 @@ void launch_cols_t(const Dims& Dm, const void* q, const void* k, const void* v, 
 
 void launch_bwd_cols(const Dims& Dm, const void* q, const void* k, const void* v, const float* lse,
                      const void* d_out, void* dk, void* dv, const StateBufs& s,
-                     const __nv_bfloat16* Ha, const float* gZa, const float* Ds, cudaStream_t st) {
+                     const __nv_bfloat16* Ha, const float* gZa, const float* Ds, float* dk_part,
+                     float* dkf_part, cudaStream_t st) {
   BwdParams p{};
+  p.dk_part = dk_part;
+  p.dkf_part = dkf_part;
   p.ccol_cnt = s.ccol_cnt;
   p.ccol_idx = s.ccol_idx;
   p.ccol_marg = s.ccol_marg;
@@ -608,10 +620,14 @@ void launch_bwd_cols(const Dims& Dm, const void* q, const void* k, const void* v
 
 }  // namespace slab
 
+#ifdef SLAB_TIMELINE  // diagnostic accessors: timeline builds only (profiles/ctaprof.py)
 extern "C" int sla_b200_diag_cols_ctaprof(unsigned long long* host) {
   return cudaMemcpyFromSymbol(host, slab::g_cta_prof, sizeof(slab::g_cta_prof)) == cudaSuccess ? 0 : 1;
 }
+#endif
 
+#ifdef SLAB_TIMELINE  // diagnostic accessors: timeline builds only (profiles/ctaprof.py)
 extern "C" int sla_b200_diag_cols_timeline(long long* host128) {
   return cudaMemcpyFromSymbol(host128, slab::g_bwd_ts, 256 * sizeof(long long)) == cudaSuccess ? 0 : 1;
 }
+#endif

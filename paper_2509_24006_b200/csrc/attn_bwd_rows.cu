@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kLinThreads, 2)
       for (int e = 0; e < 8; ++e) ds_r = fmaf(f[e], g[e], ds_r);
     }
     ds_r = pair_sum(ds_r, 0);
-    if (valid && half == 0) p.Ds_out[grow] = ds_r;
+    if (valid && half == 0 && !p.ds_external) p.Ds_out[grow] = ds_r;
     named_sync(1, 256);  // O^s (in sX) fully consumed before phi(Q) overwrites it
     float mx = 0.f, inv = 1.f;
     if (p.phi == 2) {
@@ -740,6 +740,15 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
           o[e] = jg + tq[rq * TP + col + e];
         }
         *reinterpret_cast<uint4*>(p.dq + grow * D + col) = pack8(o);
+        if (p.dq_part) {  // SlaGradients::dq and ::dq_feat (f32)
+          float4* dqs = reinterpret_cast<float4*>(p.dq_part + grow * D + col);
+          float4* dqf = reinterpret_cast<float4*>(p.dqf_part + grow * D + col);
+          const float* t = tq + rq * TP + col;
+          dqs[0] = make_float4(t[0], t[1], t[2], t[3]);
+          dqs[1] = make_float4(t[4], t[5], t[6], t[7]);
+          dqf[0] = make_float4(g[0], g[1], g[2], g[3]);
+          dqf[1] = make_float4(g[4], g[5], g[6], g[7]);
+        }
       }
     }
     ts_mark(dbg && threadIdx.x == 64, 124);
@@ -754,8 +763,9 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
 
 void launch_bwd_lin(const Dims& Dm, const void* q, const void* w, const void* o_s, const void* o_l,
                     const void* d_out, const StateBufs& s, __nv_bfloat16* gH, __nv_bfloat16* z3, float* Ds,
-                    __nv_bfloat16* dqphi, cudaStream_t st) {
+                    __nv_bfloat16* dqphi, bool ds_external, cudaStream_t st) {
   BwdParams p{};
+  p.ds_external = ds_external;
   p.marg_cnt = s.marg_cnt;
   p.Z = s.Z;
   p.Ds_out = Ds;
@@ -792,8 +802,10 @@ void launch_bwd_lin(const Dims& Dm, const void* q, const void* w, const void* o_
 
 void launch_bwd_rows(const Dims& Dm, const void* q, const void* k, const void* v, const float* lse,
                      const void* d_out, void* dq, const StateBufs& s, const float* Ds,
-                     const __nv_bfloat16* dqphi, cudaStream_t st) {
+                     const __nv_bfloat16* dqphi, float* dq_part, float* dqf_part, cudaStream_t st) {
   BwdParams p{};
+  p.dq_part = dq_part;
+  p.dqf_part = dqf_part;
   p.crit_cnt = s.crit_cnt;
   p.crit_idx = s.crit_idx;
   p.lse = lse;
@@ -827,10 +839,14 @@ void launch_bwd_rows(const Dims& Dm, const void* q, const void* k, const void* v
 
 }  // namespace slab
 
+#ifdef SLAB_TIMELINE  // diagnostic accessors: timeline builds only (profiles/ctaprof.py)
 extern "C" int sla_b200_diag_rows_ctaprof(unsigned long long* host) {
   return cudaMemcpyFromSymbol(host, slab::g_cta_prof, sizeof(slab::g_cta_prof)) == cudaSuccess ? 0 : 1;
 }
+#endif
 
+#ifdef SLAB_TIMELINE  // diagnostic accessors: timeline builds only (profiles/ctaprof.py)
 extern "C" int sla_b200_diag_bwd_timeline(long long* host128) {
   return cudaMemcpyFromSymbol(host128, slab::g_bwd_ts, 256 * sizeof(long long)) == cudaSuccess ? 0 : 1;
 }
+#endif

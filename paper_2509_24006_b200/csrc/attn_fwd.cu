@@ -22,7 +22,9 @@
 
 namespace slab {
 
+#ifdef SLAB_TIMELINE
 static __device__ long long g_fwd_ts[128];  // -DSLAB_TIMELINE: timeline of one CTA
+#endif
 
 namespace {
 
@@ -590,6 +592,8 @@ void launch_attn_fwd(const Dims& Dm, const void* q, const void* k, const void* v
 
 }  // namespace slab
 
+#ifdef SLAB_TIMELINE  // diagnostic accessors: timeline builds only (profiles/ctaprof.py)
 extern "C" int sla_b200_diag_fwd_timeline(long long* host128) {
   return cudaMemcpyFromSymbol(host128, slab::g_fwd_ts, 128 * sizeof(long long)) == cudaSuccess ? 0 : 1;
 }
+#endif

@@ -101,6 +101,12 @@ struct BwdParams {
   float scale_log2;    // scale * log2(e)
   int phi;
   const int8_t* labels;
+  int ds_external;     // k_bwd_lin: D^s comes from k_rowdot (independent cotangents), not dO . O^s
+  // optional SlaGradients parts (backward.hpp:10-16), f32 [U, N, D]; null: not written
+  float* dq_part;      // sparse dQ
+  float* dqf_part;     // dQ^phi
+  float* dk_part;      // sparse dK
+  float* dkf_part;     // dK^phi (dK^phi + the broadcast dZ_agg)
 };
 
 

@@ -545,3 +545,35 @@ extern "C" int sla_b200_diag_contention(const void* buf, int rows, int ctas, int
     return 1;
   }
 }
+
+// tcgen05 GEMM of gemm.cu on plain row-major operands (tests/test_gpu_gemm.py)
+extern "C" int sla_b200_diag_gemm(const void* A, const void* B, void* C, int batch, int M, int N,
+                                  int K, int a_mn, int b_mn, int out_f32, void* stream) {
+  try {
+    slab::GemmArgs g{};
+    g.A = A;
+    g.B = B;
+    g.C = C;
+    g.batch = batch;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.a_mn = a_mn;
+    g.b_mn = b_mn;
+    g.out_f32 = out_f32;
+    g.lda = a_mn ? M : K;
+    g.ldb = b_mn ? N : K;
+    g.ldc = N;
+    g.a_batch = (long long)M * K;
+    g.b_batch = (long long)K * N;
+    g.c_batch = (long long)M * N;
+    slab::launch_gemm(g, static_cast<cudaStream_t>(stream));
+    return 0;
+  } catch (const slab::InvalidArgument& e) {
+    std::fprintf(stderr, "%s\n", e.msg.c_str());
+    return 2;
+  } catch (const slab::CudaError& e) {
+    std::fprintf(stderr, "%s\n", e.msg.c_str());
+    return 1;
+  }
+}

@@ -109,6 +109,66 @@ __global__ void k_reduce_dw(const float* __restrict__ part, int chunks_per_unit,
   }
 }
 
+// identity [H, d, d] bf16: W of the linear-branch MMA when dO^l is given (dO^l I = dO^l exactly)
+__global__ void k_fill_identity(__nv_bfloat16* __restrict__ w, long long total, int d) {
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long m = e % ((long long)d * d);
+    w[e] = __float2bfloat16_rn(m / d == m % d ? 1.f : 0.f);
+  }
+}
+
+// out[r] = <a_r, b_r> over d columns, one warp per row (bf16 in, f32 sum)
+__global__ void k_rowdot(const __nv_bfloat162* __restrict__ a, const __nv_bfloat162* __restrict__ b,
+                         float* __restrict__ out, long long rows, int d2) {
+  const long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (r >= rows) return;
+  float acc = 0.f;
+  for (int j = lane; j < d2; j += 32) {
+    const float2 x = __bfloat1622float2(a[r * d2 + j]), y = __bfloat1622float2(b[r * d2 + j]);
+    acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
+  }
+  acc = warp_sum(acc);
+  if (lane == 0) out[r] = acc;
+}
+
+// out = (add ? add : 0) + x M, M = W[u % H] or its transpose; 64 rows per CTA, W staged as f32
+template <typename In>
+__global__ void __launch_bounds__(256) k_rowmat(const In* __restrict__ x, const In* __restrict__ w,
+                                                int transpose_w, const In* __restrict__ add,
+                                                In* __restrict__ out, long long N, long long H, int d) {
+  extern __shared__ float sm[];
+  const int dp = d + 1;
+  float* sW = sm;              // sW[b * dp + a] = M[b][a]
+  float* sX = sm + d * dp;     // [8 warps][d]
+  const long long u = blockIdx.y;
+  const In* wh = w + (u % H) * (long long)d * d;
+  for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
+    const int r = e / d, c = e % d;  // W[r][c]
+    const float v = to_f(wh[e]);
+    if (transpose_w) sW[c * dp + r] = v;
+    else sW[r * dp + c] = v;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* xr = sX + warp * d;
+  for (int rr = warp; rr < 64; rr += 8) {
+    const long long row = (long long)blockIdx.x * 64 + rr;
+    if (row >= N) break;
+    const long long g = (u * N + row) * d;
+    for (int c = lane; c < d; c += 32) xr[c] = to_f(x[g + c]);
+    __syncwarp();
+    for (int a = lane; a < d; a += 32) {
+      float acc = 0.f;
+      for (int b = 0; b < d; ++b) acc = fmaf(xr[b], sW[b * dp + a], acc);
+      if (add) acc += to_f(add[g + a]);
+      out[g + a] = from_f<In>(acc);
+    }
+    __syncwarp();
+  }
+}
+
 // Z3 = M0 [z_hi | z_mid | z_lo] (trans: M0^T [dZ parts]) on the tensor core: the z parts are
 // written by their producers (k_phi_kz, k_bwd_lin) with tc::store_split3, M0 is an exact 0/1
 // bf16 matrix, so products are exact and the f32 accumulation matches an f32 sum; consumers
@@ -142,6 +202,62 @@ void aggregate_vec_tc(const Dims& Dm, const StateBufs& s, const WorkBufs& wb, bo
 
 bool fast_supported(const Dims& D, int dtype) {
   return dtype == 0 && D.bq == 64 && D.bkv == 64 && (D.d == 64 || D.d == 128);
+}
+
+void launch_rowmat(const Dims& D, int dtype, const void* x, const void* w, bool transpose_w,
+                   const void* add, void* out, cudaStream_t st) {
+  const size_t smem = (size_t(D.d) * (D.d + 1) + 8 * size_t(D.d)) * 4;
+  const dim3 grid(unsigned((D.N + 63) / 64), unsigned(D.U));
+  if (dtype == 0) {
+    using T = __nv_bfloat16;
+    SLAB_CUDA(cudaFuncSetAttribute(k_rowmat<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k_rowmat<T><<<grid, 256, smem, st>>>((const T*)x, (const T*)w, transpose_w, (const T*)add, (T*)out, D.N,
+                                         D.H, D.d);
+  } else {
+    SLAB_CUDA(cudaFuncSetAttribute(k_rowmat<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    k_rowmat<float><<<grid, 256, smem, st>>>((const float*)x, (const float*)w, transpose_w, (const float*)add,
+                                             (float*)out, D.N, D.H, D.d);
+  }
+  check_launch("k_rowmat", st);
+}
+
+void launch_rowdot(const Dims& D, const void* a, const void* b, float* out, cudaStream_t st) {
+  const long long rows = D.U * D.N;
+  k_rowdot<<<unsigned((rows * 32 + 255) / 256), 256, 0, st>>>(static_cast<const __nv_bfloat162*>(a),
+                                                             static_cast<const __nv_bfloat162*>(b), out, rows,
+                                                             D.d / 2);
+  check_launch("k_rowdot", st);
+}
+
+// dW = O^l^T dO per head (backward.cpp:46): split-K over row chunks of each unit on the tensor
+// core, then reduced over the chunks and the batch
+void launch_dw_fast(const Dims& Dm, const void* o_l, const void* d_out, float* dw, const WorkBufs& wb,
+                    cudaStream_t ds) {
+  const int d = Dm.d;
+  const long long KC = 64LL * dw_chunk_tiles(Dm);
+  const int chunks = int(dw_chunks(Dm));
+  GemmArgs g{};
+  g.A = o_l;
+  g.B = d_out;
+  g.C = wb.dwp;
+  g.batch = int(Dm.U * chunks);
+  g.M = d;
+  g.N = d;
+  g.K = int(KC);
+  g.a_mn = true;
+  g.b_mn = true;
+  g.out_f32 = true;
+  g.lda = d;
+  g.ldb = d;
+  g.ldc = d;
+  g.a_batch = KC * d;
+  g.b_batch = KC * d;
+  g.c_batch = (long long)d * d;
+  g.name = "gemm_dw";
+  launch_gemm(g, ds);
+  launch_pdl(k_reduce_dw, dim3((d * d + 255) / 256, unsigned(Dm.H)), 256, 0, ds, (const float*)wb.dwp, chunks,
+             (long long)Dm.B, (long long)Dm.H, d * d, dw);
+  check_launch("k_reduce_dw", ds);
 }
 
 // phi(K), z_j and h_j = phi(K_j)^T V_j: independent of the mask, so the C-ABI forward runs them
@@ -212,16 +328,11 @@ void fast_forward(const Dims& Dm, const void* q, const void* k, const void* v, c
   launch_attn_fwd(Dm, q, k, v, w, o, o_s, o_l, lse, s, st);
 }
 
-#ifndef SLAB_AGG_SIDE
-#define SLAB_AGG_SIDE 0  // measured slower: 2.81 ms per step against 2.73-2.78 (rows loses SMs, cols waits)
-#endif
-#ifndef SLAB_DW_SIDE
-#define SLAB_DW_SIDE 1  // measured: 2.72-2.75 ms per step against 2.76-2.78 with dW on the main stream
-#endif
 void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
                    const void* o_s, const void* o_l, const float* lse, const void* d_out,
-                   void* dq, void* dk, void* dv, float* dw, const StateBufs& s,
-                   const WorkBufs& wb, cudaStream_t st, const SideFork& side) {
+                   const void* d_out_l, void* dq, void* dk, void* dv, float* dw,
+                   const GradParts& parts, const StateBufs& s, const WorkBufs& wb, cudaStream_t st,
+                   const SideFork& side) {
   const int d = Dm.d;
   auto launch_agg = [&](cudaStream_t as) {
     // dH_agg = M0^T dH (A = M0 read M-major), dZ_agg
@@ -246,69 +357,47 @@ void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, 
     launch_gemm(a, as);
     aggregate_vec_tc(Dm, s, wb, true, wb.gZa, "gemm_aggregate_dz", as);  // gZa: [U, Tn, 3d]
   };
-  // dW = O^l^T dO per head, split-K over row chunks of each unit, then reduced over chunks + batch
-  auto launch_dw = [&](cudaStream_t ds) {
-    const long long KC = 64LL * dw_chunk_tiles(Dm);
-    const int chunks = int(dw_chunks(Dm));
-    GemmArgs g{};
-    g.A = o_l;
-    g.B = d_out;
-    g.C = wb.dwp;
-    g.batch = int(Dm.U * chunks);
-    g.M = d;
-    g.N = d;
-    g.K = int(KC);
-    g.a_mn = true;
-    g.b_mn = true;
-    g.out_f32 = true;
-    g.lda = d;
-    g.ldb = d;
-    g.ldc = d;
-    g.a_batch = KC * d;
-    g.b_batch = KC * d;
-    g.c_batch = (long long)d * d;
-    g.name = "gemm_dw";
-    launch_gemm(g, ds);
-    launch_pdl(k_reduce_dw, dim3((d * d + 255) / 256, unsigned(Dm.H)), 256, 0, ds, (const float*)wb.dwp, chunks,
-               (long long)Dm.B, (long long)Dm.H, d * d, dw);
-    check_launch("k_reduce_dw", ds);
-  };
+  // independent cotangents: the linear kernel multiplies the given dO^l by an identity W (exact)
+  // and D^s = <dO^s, O^s> comes from its own row-dot kernel
+  const bool split = d_out_l != nullptr;
+  const void* lin_w = w;
+  const void* lin_do = d_out;
+  if (split) {
+    const long long total = Dm.H * (long long)d * d;
+    k_fill_identity<<<unsigned((total + 255) / 256), 256, 0, st>>>(wb.wid, total, d);
+    check_launch("k_fill_identity", st);
+    launch_rowdot(Dm, d_out, o_s, wb.Ds, st);
+    lin_w = wb.wid;
+    lin_do = d_out_l;
+  }
   // the column lists (labels only) build on the side stream while k_bwd_lin, a latency-bound
-  // kernel with registers and threads to spare on every SM, runs; joined before the columns pass
+  // kernel with registers and threads to spare on every SM, runs; joined before the columns pass.
+  // dW needs only O^l and dO: it fills SMs beside the row / column passes.
+  SideJoin guard(side, st);
   if (side.s) {
     SLAB_CUDA(cudaEventRecord(side.fork, st));
     SLAB_CUDA(cudaStreamWaitEvent(side.s, side.fork, 0));
+    guard.arm(side.join2);
     launch_build_csc(Dm, s, side.s);
     SLAB_CUDA(cudaEventRecord(side.join, side.s));
-    if (SLAB_DW_SIDE) {  // dW needs only O^l and dO: it fills SMs beside the row / column passes
-      launch_dw(side.s);
-      SLAB_CUDA(cudaEventRecord(side.join2, side.s));
-    }
+    if (dw) launch_dw_fast(Dm, o_l, d_out, dw, wb, side.s);
+    SLAB_CUDA(cudaEventRecord(side.join2, side.s));
   } else {
     launch_build_csc(Dm, s, st);
   }
   // row phase: the linear branch (dH_i reusing the forward's h scratch, dZ_i, D^s, dQ^phi),
   // then the sparse dQ over critical pairs with dq_total = J_phi^T dQ^phi + dQ
-  launch_bwd_lin(Dm, q, w, o_s, o_l, d_out, s, wb.hb, wb.z3b, wb.Ds, wb.dqphi, st);
-  // dH_agg = M0^T dH and dZ_agg need only k_bwd_lin's dH / dZ: with a side stream they run
-  // beside the rows pass (joined before the columns pass)
-  const bool agg_side = SLAB_AGG_SIDE && side.s;
-  if (agg_side) {
-    SLAB_CUDA(cudaEventRecord(side.mid, st));
-    SLAB_CUDA(cudaStreamWaitEvent(side.s, side.mid, 0));
-    launch_agg(side.s);
-    SLAB_CUDA(cudaEventRecord(side.join3, side.s));
-  }
-  launch_bwd_rows(Dm, q, k, v, lse, d_out, dq, s, wb.Ds, wb.dqphi, st);
-  if (agg_side)
-    SLAB_CUDA(cudaStreamWaitEvent(st, side.join3, 0));
-  else
-    launch_agg(st);
+  launch_bwd_lin(Dm, q, lin_w, o_s, o_l, lin_do, s, wb.hb, wb.z3b, wb.Ds, wb.dqphi, split, st);
+  launch_bwd_rows(Dm, q, k, v, lse, d_out, dq, s, wb.Ds, wb.dqphi, parts.dq, parts.dq_feat, st);
+  // dH_agg = M0^T dH and dZ_agg need only k_bwd_lin's dH / dZ (measured: on a side stream beside
+  // the rows pass 2.81 ms per step against 2.73-2.78 here -- rows loses SMs, cols waits)
+  launch_agg(st);
   // columns pass: dk_total, dv
   if (side.s) SLAB_CUDA(cudaStreamWaitEvent(st, side.join, 0));
-  launch_bwd_cols(Dm, q, k, v, lse, d_out, dk, dv, s, wb.hab, wb.gZa, wb.Ds, st);
-  if (!(SLAB_DW_SIDE && side.s)) launch_dw(st);
-  if (SLAB_DW_SIDE && side.s) SLAB_CUDA(cudaStreamWaitEvent(st, side.join2, 0));
+  launch_bwd_cols(Dm, q, k, v, lse, d_out, dk, dv, s, wb.hab, wb.gZa, wb.Ds, parts.dk, parts.dk_feat, st);
+  if (!side.s && dw) launch_dw_fast(Dm, o_l, d_out, dw, wb, st);
+  guard.release();
+  if (side.s) SLAB_CUDA(cudaStreamWaitEvent(st, side.join2, 0));
 }
 
 }  // namespace slab

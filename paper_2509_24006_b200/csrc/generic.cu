@@ -302,17 +302,21 @@ __global__ void k_fwd_generic(Dims D, FwdSmem L, const In* __restrict__ q,
 // ---------------------------------------------------------------------------------------
 template <typename In>
 __global__ void k_bwd_prep(Dims D, const In* __restrict__ w, const In* __restrict__ d_out,
-                           const In* __restrict__ o_s, const In* __restrict__ o_l,
-                           float* __restrict__ dOl, float* __restrict__ Ds,
-                           float* __restrict__ Dl) {
+                           const In* __restrict__ d_out_l, const In* __restrict__ o_s,
+                           const In* __restrict__ o_l, float* __restrict__ dOl,
+                           float* __restrict__ Ds, float* __restrict__ Dl) {
+  // d_out_l != null: independent cotangents (sla_backward's dO^l, backward.hpp:25-38) -- dO^l is
+  // taken as given; else dO^l = dO W^T (proj_backward, backward.cpp:12-22)
   extern __shared__ float sm[];
   const int d = D.d, dp = d + 1;
   float* sW = sm;                         // [d][d+1]
   float* sRow = sm + d * dp;              // [warps][d]
   const long long u = blockIdx.y;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-  const In* wh = w + (u % D.H) * (long long)d * d;
-  for (int e = threadIdx.x; e < d * d; e += blockDim.x) sW[(e / d) * dp + e % d] = to_f(wh[e]);
+  if (!d_out_l) {
+    const In* wh = w + (u % D.H) * (long long)d * d;
+    for (int e = threadIdx.x; e < d * d; e += blockDim.x) sW[(e / d) * dp + e % d] = to_f(wh[e]);
+  }
   __syncthreads();
   float* myrow = sRow + warp * d;
   for (int rr = warp; rr < 64; rr += nw) {
@@ -325,7 +329,10 @@ __global__ void k_bwd_prep(Dims D, const In* __restrict__ w, const In* __restric
     for (int c = lane; c < d; c += 32) ds += myrow[c] * to_f(o_s[g + c]);
     for (int a = lane; a < d; a += 32) {
       float acc = 0.f;
-      for (int b = 0; b < d; ++b) acc = add_rn(acc, mul_rn(myrow[b], sW[a * dp + b]));
+      if (d_out_l)
+        acc = to_f(d_out_l[g + a]);
+      else
+        for (int b = 0; b < d; ++b) acc = add_rn(acc, mul_rn(myrow[b], sW[a * dp + b]));
       dOl[g + a] = acc;
       dl += acc * to_f(o_l[g + a]);
     }
@@ -710,7 +717,7 @@ unsigned grid1(long long total, int per) {
 template <typename In>
 void forward_t(const Dims& D, const In* q, const In* k, const In* v, const In* w, In* o,
                In* o_s, In* o_l, float* lse, const StateBufs& s, const WorkBufs& wb,
-               cudaStream_t st) {
+               cudaStream_t st, bool attention = true) {
   const long long rows = D.U * D.N;
   k_phi<In><<<grid1(rows, 8), 256, 0, st>>>(q, wb.qf, rows, D.d, D.phi);
   check_launch("k_phi(q)", st);
@@ -726,6 +733,7 @@ void forward_t(const Dims& D, const In* q, const In* k, const In* v, const In* w
   k_aggregate_rows<<<dim3(D.Tm, unsigned(D.U)), kThreads, agg_smem, st>>>(
       s.labels, wb.h, wb.z, D.d, D.Tm, D.Tn, s.H, s.Z);
   check_launch("k_aggregate_rows", st);
+  if (!attention) return;  // sla_b200_build_state: the forward state without the outputs
   const FwdSmem L = fwd_smem(D);
   set_smem(k_fwd_generic<In>, L.bytes);
   k_fwd_generic<In><<<dim3(D.Tm, unsigned(D.U)), kThreads, L.bytes, st>>>(
@@ -735,11 +743,12 @@ void forward_t(const Dims& D, const In* q, const In* k, const In* v, const In* w
 
 template <typename In>
 void backward_t(const Dims& D, const In* q, const In* k, const In* v, const In* w,
-                const In* o_s, const In* o_l, const float* lse, const In* d_out, In* dq, In* dk,
-                In* dv, float* dw, const StateBufs& s, const WorkBufs& wb, cudaStream_t st) {
+                const In* o_s, const In* o_l, const float* lse, const In* d_out, const In* d_out_l,
+                In* dq, In* dk, In* dv, float* dw, const StateBufs& s, const WorkBufs& wb,
+                cudaStream_t st) {
   const long long rows = D.U * D.N;
   const size_t nd = size_t(rows) * D.d;
-  SLAB_CUDA(cudaMemsetAsync(dw, 0, sizeof(float) * size_t(D.H) * D.d * D.d, st));
+  if (dw) SLAB_CUDA(cudaMemsetAsync(dw, 0, sizeof(float) * size_t(D.H) * D.d * D.d, st));
   SLAB_CUDA(cudaMemsetAsync(wb.dk, 0, sizeof(float) * nd, st));
   SLAB_CUDA(cudaMemsetAsync(wb.dv, 0, sizeof(float) * nd, st));
   prof_mark("", st);
@@ -751,12 +760,14 @@ void backward_t(const Dims& D, const In* q, const In* k, const In* v, const In* 
   const size_t ps = prep_smem(D);
   set_smem(k_bwd_prep<In>, ps);
   k_bwd_prep<In><<<dim3(grid1(D.N, 64), unsigned(D.U)), 256, ps, st>>>(
-      D, w, d_out, o_s, o_l, wb.dOl, wb.Ds, wb.Dl);
+      D, w, d_out, d_out_l, o_s, o_l, wb.dOl, wb.Ds, wb.Dl);
   check_launch("k_bwd_prep", st);
-  const size_t dws = size_t(64 * D.d) * 4;
-  set_smem(k_dw<In>, dws);
-  k_dw<In><<<dim3(grid1(D.N, 32), unsigned(D.U)), 256, dws, st>>>(D, o_l, d_out, dw);
-  check_launch("k_dw", st);
+  if (dw) {  // dproj = O^l^T dO^s (backward.cpp:46)
+    const size_t dws = size_t(64 * D.d) * 4;
+    set_smem(k_dw<In>, dws);
+    k_dw<In><<<dim3(grid1(D.N, 32), unsigned(D.U)), 256, dws, st>>>(D, o_l, d_out, dw);
+    check_launch("k_dw", st);
+  }
   const size_t rl = rows_lin_smem(D);
   if (s.H) {
     set_smem(k_bwd_rows_lin<float>, rl);
@@ -810,30 +821,47 @@ bool generic_supported(const Dims& D, std::string* why) {
 
 void generic_forward(const Dims& D, int dtype, const void* q, const void* k, const void* v,
                      const void* w, void* o, void* o_s, void* o_l, float* lse,
-                     const StateBufs& s, const WorkBufs& wb, cudaStream_t st) {
+                     const StateBufs& s, const WorkBufs& wb, cudaStream_t st, bool attention) {
   if (dtype == 0) {
     using T = __nv_bfloat16;
     forward_t<T>(D, (const T*)q, (const T*)k, (const T*)v, (const T*)w, (T*)o, (T*)o_s,
-                 (T*)o_l, lse, s, wb, st);
+                 (T*)o_l, lse, s, wb, st, attention);
   } else {
     forward_t<float>(D, (const float*)q, (const float*)k, (const float*)v, (const float*)w,
-                     (float*)o, (float*)o_s, (float*)o_l, lse, s, wb, st);
+                     (float*)o, (float*)o_s, (float*)o_l, lse, s, wb, st, attention);
   }
 }
 
 void generic_backward(const Dims& D, int dtype, const void* q, const void* k, const void* v,
                       const void* w, const void* o_s, const void* o_l, const float* lse,
-                      const void* d_out, void* dq, void* dk, void* dv, float* dw,
+                      const void* d_out, const void* d_out_l, void* dq, void* dk, void* dv, float* dw,
                       const StateBufs& s, const WorkBufs& wb, cudaStream_t st) {
   if (dtype == 0) {
     using T = __nv_bfloat16;
     backward_t<T>(D, (const T*)q, (const T*)k, (const T*)v, (const T*)w, (const T*)o_s,
-                  (const T*)o_l, lse, (const T*)d_out, (T*)dq, (T*)dk, (T*)dv, dw, s, wb, st);
+                  (const T*)o_l, lse, (const T*)d_out, (const T*)d_out_l, (T*)dq, (T*)dk, (T*)dv, dw, s,
+                  wb, st);
   } else {
     backward_t<float>(D, (const float*)q, (const float*)k, (const float*)v, (const float*)w,
                       (const float*)o_s, (const float*)o_l, lse, (const float*)d_out,
-                      (float*)dq, (float*)dk, (float*)dv, dw, s, wb, st);
+                      (const float*)d_out_l, (float*)dq, (float*)dk, (float*)dv, dw, s, wb, st);
   }
+}
+
+// proj_backward's dW = O^l^T dO (backward.cpp:12-22) summed over the batch per head, f32 [H, d, d]
+void generic_dw(const Dims& D, int dtype, const void* o_l, const void* d_out, float* dw, cudaStream_t st) {
+  SLAB_CUDA(cudaMemsetAsync(dw, 0, sizeof(float) * size_t(D.H) * D.d * D.d, st));
+  const size_t dws = size_t(64 * D.d) * 4;
+  if (dtype == 0) {
+    set_smem(k_dw<__nv_bfloat16>, dws);
+    k_dw<__nv_bfloat16><<<dim3(grid1(D.N, 32), unsigned(D.U)), 256, dws, st>>>(
+        D, (const __nv_bfloat16*)o_l, (const __nv_bfloat16*)d_out, dw);
+  } else {
+    set_smem(k_dw<float>, dws);
+    k_dw<float><<<dim3(grid1(D.N, 32), unsigned(D.U)), 256, dws, st>>>(D, (const float*)o_l,
+                                                                          (const float*)d_out, dw);
+  }
+  check_launch("k_dw", st);
 }
 
 }  // namespace slab

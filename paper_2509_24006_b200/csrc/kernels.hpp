@@ -22,13 +22,22 @@ void launch_lin_rows(const Dims& D, int dtype, const void* q, const float* Z, bo
 
 // generic.cu -- shape-generic SIMT kernels (fp32 math, any b_q, b_kv, d within smem limits)
 bool generic_supported(const Dims& D, std::string* why);
+// attention == false: only the state (summaries, H, Z) -- sla_b200_build_state
 void generic_forward(const Dims& D, int dtype, const void* q, const void* k, const void* v,
                      const void* w, void* o, void* o_s, void* o_l, float* lse,
-                     const StateBufs& s, const WorkBufs& wb, cudaStream_t st);
+                     const StateBufs& s, const WorkBufs& wb, cudaStream_t st, bool attention = true);
+// d_out_l == null: dO^l = dO W^T (combined cotangent); else the given dO^l.  dw may be null.
 void generic_backward(const Dims& D, int dtype, const void* q, const void* k, const void* v,
                       const void* w, const void* o_s, const void* o_l, const float* lse,
-                      const void* d_out, void* dq, void* dk, void* dv, float* dw,
+                      const void* d_out, const void* d_out_l, void* dq, void* dk, void* dv, float* dw,
                       const StateBufs& s, const WorkBufs& wb, cudaStream_t st);
+void generic_dw(const Dims& D, int dtype, const void* o_l, const void* d_out, float* dw, cudaStream_t st);
+// out = (add ? add : 0) + x M with M = W[h] (transpose_w = false) or W[h]^T, f32 accumulation;
+// combine_outputs (forward.cpp:187-195) and proj_backward's dO W^T (backward.cpp:12-22)
+void launch_rowmat(const Dims& D, int dtype, const void* x, const void* w, bool transpose_w,
+                   const void* add, void* out, cudaStream_t st);
+// D^s = <dO^s, O^s> per row (backward.cpp:48-58) for independent cotangents
+void launch_rowdot(const Dims& D, const void* a, const void* b, float* out, cudaStream_t st);
 
 // gemm.cu -- batched tcgen05 GEMM (bf16 in, f32 accumulate)
 struct GemmArgs {
@@ -51,13 +60,14 @@ void fast_summaries(const Dims& Dm, const void* k, const void* v, const WorkBufs
 void fast_aggregate(const Dims& Dm, const StateBufs& s, const WorkBufs& wb, bool m0_ready, cudaStream_t st);
 void launch_bwd_lin(const Dims& Dm, const void* q, const void* w, const void* o_s, const void* o_l,
                     const void* d_out, const StateBufs& s, __nv_bfloat16* gH, __nv_bfloat16* z3, float* Ds,
-                    __nv_bfloat16* dqphi, cudaStream_t st);
+                    __nv_bfloat16* dqphi, bool ds_external, cudaStream_t st);
 void launch_bwd_rows(const Dims& Dm, const void* q, const void* k, const void* v, const float* lse,
                      const void* d_out, void* dq, const StateBufs& s, const float* Ds,
-                     const __nv_bfloat16* dqphi, cudaStream_t st);
+                     const __nv_bfloat16* dqphi, float* dq_part, float* dqf_part, cudaStream_t st);
 void launch_bwd_cols(const Dims& Dm, const void* q, const void* k, const void* v, const float* lse,
                      const void* d_out, void* dk, void* dv, const StateBufs& s,
-                     const __nv_bfloat16* Ha, const float* gZa, const float* Ds, cudaStream_t st);
+                     const __nv_bfloat16* Ha, const float* gZa, const float* Ds, float* dk_part,
+                     float* dkf_part, cudaStream_t st);
 bool fast_supported(const Dims& D, int dtype);
 void fast_forward(const Dims& D, const void* q, const void* k, const void* v, const void* w,
                   void* o, void* o_s, void* o_l, float* lse, const StateBufs& s,
@@ -68,9 +78,42 @@ struct SideFork {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr, mid = nullptr, join3 = nullptr;
 };
+// RAII join of a side-stream fork: if an exception leaves the region between the fork and its
+// join, the side stream's queued work is still joined into the caller's stream, so the caller
+// never reuses buffers that work reads or writes, and a graph capture never ends with an
+// unjoined fork.
+struct SideJoin {
+  cudaStream_t side, main;
+  cudaEvent_t ev = nullptr;
+  SideJoin(const SideFork& f, cudaStream_t m) : side(f.s), main(m) {}
+  SideJoin(cudaStream_t s, cudaStream_t m) : side(s), main(m) {}
+  void arm(cudaEvent_t e) { ev = e; }
+  void release() { ev = nullptr; }
+  ~SideJoin() {
+    if (ev && side) {
+      cudaEventRecord(ev, side);
+      cudaStreamWaitEvent(main, ev, 0);
+    }
+  }
+  SideJoin(const SideJoin&) = delete;
+  SideJoin& operator=(const SideJoin&) = delete;
+};
+// optional SlaGradients parts (backward.hpp:10-16), f32 [U, N, d]; all null or all set
+struct GradParts {
+  float* dq = nullptr;
+  float* dk = nullptr;
+  float* dq_feat = nullptr;
+  float* dk_feat = nullptr;
+};
+// d_out_l == null: combined cotangent d_out with dO^l = dO W^T (proj_backward fused);
+// else independent cotangents d_out (= dO^s) and d_out_l (sla_backward, backward.hpp:25-38),
+// w unused.  dw (= O^l^T dO^s, backward.cpp:46) may be null.
 void fast_backward(const Dims& D, const void* q, const void* k, const void* v, const void* w,
                    const void* o_s, const void* o_l, const float* lse, const void* d_out,
-                   void* dq, void* dk, void* dv, float* dw, const StateBufs& s,
-                   const WorkBufs& wb, cudaStream_t st, const SideFork& side);
+                   const void* d_out_l, void* dq, void* dk, void* dv, float* dw,
+                   const GradParts& parts, const StateBufs& s, const WorkBufs& wb, cudaStream_t st,
+                   const SideFork& side);
+void launch_dw_fast(const Dims& Dm, const void* o_l, const void* d_out, float* dw, const WorkBufs& wb,
+                    cudaStream_t st);
 
 }  // namespace slab

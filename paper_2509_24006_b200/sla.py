@@ -7,8 +7,12 @@ The names, argument meaning and error behaviour follow the reference
   make_block_layout      layout.cpp:8-26        raises ValueError (std::invalid_argument)
   sla_forward            forward.cpp:174-185    dynamic mask from q, k
   sla_forward_with_mask  forward.cpp:81-172     injected label grid
-  combine_outputs        forward.cpp:187-195    fused into the forward kernel epilogue
-  proj_backward + sla_backward  backward.cpp:12-216   one fused call
+  combine_outputs        forward.cpp:187-195    fused into the forward kernel epilogue (and a
+                                                device kernel for a standalone call)
+  proj_backward          backward.cpp:12-22     device dO W^T and dW = O^l^T dO
+  sla_backward           backward.cpp:24-216    independent cotangents (dO^s, dO^l), as the
+                                                reference takes them
+  SLA.backward           proj_backward + sla_backward fused, from the combined cotangent
 
 Tensors are CUDA tensors (torch is only the device-memory / stream plumbing); every op
 runs through libsla_b200.so.  Shapes: [N, d] for one (batch, head) unit as in the
@@ -81,8 +85,8 @@ def _ptr(t: Optional[torch.Tensor]):
     return None if t is None else C.c_void_p(t.data_ptr())
 
 
-def _stream():
-    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+def _stream(device):
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
 
 
 @dataclass
@@ -130,7 +134,18 @@ class SLA:
         L.check(L.lib().sla_b200_query(C.byref(self.p), C.byref(info)))
         self.info = info
         self.t_m, self.t_n = info.t_m, info.t_n
-        self._workspace = torch.empty(self.workspace_bytes, dtype=torch.uint8, device=self.device)
+        self._workspaces = {}
+
+    @property
+    def _workspace(self) -> torch.Tensor:
+        """Scratch of the current stream: calls issued on different streams must not share it
+        (the C-ABI is re-entrant per stream, sla_b200.h)."""
+        key = torch.cuda.current_stream(self.device).cuda_stream
+        ws = self._workspaces.get(key)
+        if ws is None:
+            ws = torch.empty(self.workspace_bytes, dtype=torch.uint8, device=self.device)
+            self._workspaces[key] = ws
+        return ws
 
     @property
     def path(self) -> str:
@@ -178,8 +193,9 @@ class SLA:
                              device=self.device)
         p_c = torch.empty((self.batch, self.heads, self.t_m, self.t_n), dtype=torch.float64,
                           device=self.device) if weights else None
-        L.check(L.lib().sla_b200_classify(C.byref(self.p), _ptr(q), _ptr(k), _ptr(labels),
-                                          _ptr(p_c), _ptr(state), _ptr(self._workspace), _stream()))
+        with torch.cuda.device(self.device):
+            L.check(L.lib().sla_b200_classify(C.byref(self.p), _ptr(q), _ptr(k), _ptr(labels),
+                                              _ptr(p_c), _ptr(state), _ptr(self._workspace), _stream(self.device)))
         return (labels, p_c) if weights else labels
 
     def forward(self, q, k, v, w=None, mask=None, state=None, out=None) -> SlaForwardState:
@@ -200,15 +216,21 @@ class SLA:
             lse = torch.empty(shape[:-1], dtype=torch.float32, device=self.device)
         else:
             o, o_s, o_l, lse = out
-        L.check(L.lib().sla_b200_forward(C.byref(self.p), _ptr(q), _ptr(k), _ptr(v), _ptr(w),
-                                         _ptr(mask), _ptr(o), _ptr(o_s), _ptr(o_l), _ptr(lse),
-                                         _ptr(state), _ptr(self._workspace), _stream()))
+        with torch.cuda.device(self.device):
+            L.check(L.lib().sla_b200_forward(C.byref(self.p), _ptr(q), _ptr(k), _ptr(v), _ptr(w),
+                                             _ptr(mask), _ptr(o), _ptr(o_s), _ptr(o_l), _ptr(lse),
+                                             _ptr(state), _ptr(self._workspace), _stream(self.device)))
         return SlaForwardState(o, o_s, o_l, lse, self.labels_of(state), self, state)
 
     def backward(self, st: SlaForwardState, q, k, v, w, d_out, parts: bool = False,
-                 out=None) -> SlaGradients:
-        """proj_backward + sla_backward (backward.cpp:12-216) from the combined cotangent."""
-        w = self._w(w)
+                 out=None, d_out_linear=None) -> SlaGradients:
+        """proj_backward + sla_backward (backward.cpp:12-216) from the combined cotangent d_out;
+        with `d_out_linear`, sla_backward alone on independent cotangents (d_out = dO^s,
+        backward.hpp:25-38; w is not used and dproj = O^l^T dO^s)."""
+        if d_out_linear is None:
+            w = self._w(w)
+        else:
+            self._check("dO^l", d_out_linear)
         self._check("dO", d_out)
         shape = self._unit_shape()
         if out is None:
@@ -225,11 +247,56 @@ class SLA:
                 extra[nm] = torch.empty(shape, dtype=torch.float32, device=self.device)
             gp = L.GradParts(extra["dq"].data_ptr(), extra["dk"].data_ptr(),
                              extra["dq_feat"].data_ptr(), extra["dk_feat"].data_ptr())
-        L.check(L.lib().sla_b200_backward_ex(
-            C.byref(self.p), _ptr(q), _ptr(k), _ptr(v), _ptr(w), _ptr(st.o_s), _ptr(st.o_l),
-            _ptr(st.lse), _ptr(d_out), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(dw),
-            None if gp is None else C.byref(gp), _ptr(st.state), _ptr(self._workspace), _stream()))
+        with torch.cuda.device(self.device):
+            if d_out_linear is None:
+                rc = L.lib().sla_b200_backward_ex(
+                    C.byref(self.p), _ptr(q), _ptr(k), _ptr(v), _ptr(w), _ptr(st.o_s), _ptr(st.o_l),
+                    _ptr(st.lse), _ptr(d_out), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(dw),
+                    None if gp is None else C.byref(gp), _ptr(st.state), _ptr(self._workspace),
+                    _stream(self.device))
+            else:
+                rc = L.lib().sla_b200_backward_split(
+                    C.byref(self.p), _ptr(q), _ptr(k), _ptr(v), _ptr(st.o_s), _ptr(st.o_l), _ptr(st.lse),
+                    _ptr(d_out), _ptr(d_out_linear), _ptr(dq), _ptr(dk), _ptr(dv), _ptr(dw),
+                    None if gp is None else C.byref(gp), _ptr(st.state), _ptr(self._workspace),
+                    _stream(self.device))
+        L.check(rc)
         return SlaGradients(dq, dk, dv, dw, **extra)
+
+    def combine(self, st: SlaForwardState, w) -> torch.Tensor:
+        """combine_outputs (forward.cpp:187-195) on the device: O = O^s + O^l W."""
+        w = self._w(w)
+        o = torch.empty_like(st.o_s)
+        with torch.cuda.device(self.device):
+            L.check(L.lib().sla_b200_combine_outputs(C.byref(self.p), _ptr(st.o_s), _ptr(st.o_l), _ptr(w), _ptr(o),
+                                                     _stream(self.device)))
+        return o
+
+    def proj_backward(self, d_out, o_l, w):
+        """proj_backward (backward.cpp:12-22) on the device: (dO^s = dO, dO^l = dO W^T,
+        dW = O^l^T dO summed over the batch per head)."""
+        w = self._w(w)
+        self._check("dO", d_out)
+        self._check("O^l", o_l)
+        d_out_l = torch.empty_like(d_out)
+        dw = torch.empty((self.heads, self.d, self.d), dtype=torch.float32, device=self.device)
+        with torch.cuda.device(self.device):
+            L.check(L.lib().sla_b200_proj_backward(C.byref(self.p), _ptr(d_out), _ptr(o_l), _ptr(w), _ptr(d_out_l),
+                                                   _ptr(dw), _ptr(self._workspace), _stream(self.device)))
+        return d_out, d_out_l, dw
+
+    def state_from(self, q, k, v, labels, o_s, o_l, lse) -> SlaForwardState:
+        """A SlaForwardState around outputs the caller holds (e.g. a reference forward's O^s,
+        O^l, lse and label grid): the device state (lookups, H, Z) is rebuilt from the labels by
+        sla_b200_build_state, without rerunning the attention kernel."""
+        for nm, t in (("Q", q), ("K", k), ("V", v), ("O^s", o_s), ("O^l", o_l)):
+            self._check(nm, t)
+        labels = labels.to(device=self.device, dtype=torch.int8).contiguous()
+        state = self.new_state()
+        with torch.cuda.device(self.device):
+            L.check(L.lib().sla_b200_build_state(C.byref(self.p), _ptr(q), _ptr(k), _ptr(v), _ptr(labels),
+                                                 _ptr(state), _ptr(self._workspace), _stream(self.device)))
+        return SlaForwardState(None, o_s, o_l, lse, self.labels_of(state), self, state)
 
     def flops_report(self, st) -> list:
         """flops_report (flops.cpp:7-33) of every (batch, head) unit, from the device LUT of a
@@ -237,7 +304,7 @@ class SLA:
         state = st.state if isinstance(st, SlaForwardState) else st
         arr = (L.Flops * (self.batch * self.heads))()
         L.check(L.lib().sla_b200_flops_report(C.byref(self.p), _ptr(state), arr, _ptr(self._workspace),
-                                              _stream()))
+                                              _stream(self.device)))
         return [{f: getattr(x, f) for f, _ in L.Flops._fields_} for x in arr]
 
     def exec_counters(self, st: SlaForwardState, q, aggregation: str = "direct", group_size: int = 4) -> dict:
@@ -248,7 +315,7 @@ class SLA:
             raise ValueError(f"unknown aggregation strategy '{aggregation}'")
         c = L.Counters()
         L.check(L.lib().sla_b200_exec_counters(C.byref(self.p), _ptr(q), _ptr(st.state), L.AGG[aggregation],
-                                               group_size, C.byref(c), _ptr(self._workspace), _stream()))
+                                               group_size, C.byref(c), _ptr(self._workspace), _stream(self.device)))
         return {f: int(getattr(c, f)) for f, _ in L.Counters._fields_}
 
     def launches(self) -> int:
@@ -274,13 +341,30 @@ def sla_forward_with_mask(q, k, v, mask, cfg: SlaConfig, layout: BlockLayout, w=
 
 
 def combine_outputs(state: SlaForwardState, w) -> torch.Tensor:
-    """forward.cpp:187-195.  The projection runs in the forward kernel epilogue; this
-    returns that fused result when `w` is the projection the forward was given."""
-    if state.o is None:
-        raise ValueError("combine_outputs: run the forward with w to fuse the projection")
-    return state.o
+    """forward.cpp:187-195: O = O^s + O^l W on the device.  (sla_forward with w already returns the
+    fused result in state.o.)"""
+    return state.op.combine(state, w)
 
 
-def sla_backward(state: SlaForwardState, q, k, v, w, d_out, parts: bool = False) -> SlaGradients:
-    """proj_backward + sla_backward from the combined-output cotangent."""
+def proj_backward(d_out, linear_out, w):
+    """backward.cpp:12-22: (dO^s, dO^l, dW) = (dO, dO W^T, O^l^T dO) for one [N, d] unit."""
+    if d_out.shape != linear_out.shape:
+        raise ValueError("proj_backward: shape mismatch")
+    n, d = d_out.shape[-2:]
+    op = SLA(1, 1, n, d, 64 if n % 64 == 0 else n, 64 if n % 64 == 0 else n, SlaConfig(), d_out.dtype,
+             d_out.device)
+    dos, dol, dw = op.proj_backward(d_out.reshape(1, 1, n, d).contiguous(),
+                                    linear_out.reshape(1, 1, n, d).contiguous(), w.reshape(1, d, d))
+    return dos.reshape(d_out.shape), dol.reshape(d_out.shape), dw.reshape(d, d)
+
+
+def sla_backward(state: SlaForwardState, q, k, v, d_out_sparse, d_out_linear, parts: bool = False) -> SlaGradients:
+    """backward.hpp:25-38: gradients through both branches from independent cotangents
+    (dO^s for the sparse branch, dO^l for the linear one); dproj = O^l^T dO^s."""
+    return state.op.backward(state, q, k, v, None, d_out_sparse, parts=parts, d_out_linear=d_out_linear)
+
+
+def sla_step_backward(state: SlaForwardState, q, k, v, w, d_out, parts: bool = False) -> SlaGradients:
+    """proj_backward + sla_backward fused, from the combined-output cotangent (the reference's
+    training-step sequence, finetune.cpp:44-61)."""
     return state.op.backward(state, q, k, v, w, d_out, parts=parts)

@@ -3,7 +3,7 @@ import sys, os, ctypes as C
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2509_24006_b200 import _lib as L
-lib = L.lib()
+lib = L.diag_lib()
 rows = 16 * 1024 * 1024 // 256
 buf = torch.randn(rows, 128, device='cuda').bfloat16()
 names = {0: "TMA alone", 1: "+ MMA stream", 2: "+ softmax warps (fence)", 3: "+ MMA + softmax warps (fence)",

@@ -10,7 +10,7 @@ w = (torch.randn((H,d,d),generator=g,device='cuda')*0.1).bfloat16()
 for _ in range(3):
     st = op.forward(q,k,v,w); gr = op.backward(st,q,k,v,w,do)
 torch.cuda.synchronize()
-L = _lib.lib()
+L = _lib.diag_lib()
 lab = st.labels.cpu().numpy().reshape(B*H, 512, 512)
 for name, fn in (("rows", L.sla_b200_diag_rows_ctaprof), ("cols", L.sla_b200_diag_cols_ctaprof)):
     buf = (C.c_ulonglong * (8192*4))()

@@ -3,7 +3,7 @@ import sys, os, ctypes as C
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2509_24006_b200 import _lib as L
-lib = L.lib(); torch.zeros(1, device='cuda')
+lib = L.diag_lib(); torch.zeros(1, device='cuda')
 out = C.c_longlong()
 for (m, n, am, bm) in [(64,64,0,0),(64,128,0,0),(64,256,0,0),(128,64,0,0),(128,128,0,0),(128,256,0,0),
                        (128,64,1,1),(128,128,1,1),(64,128,0,1),(128,64,0,1),(64,64,0,1),

@@ -3,6 +3,7 @@
 // library) and once through namespace sla::gpu (include/sla_b200.hpp over libsla_b200.so) --
 // on identical bf16-representable inputs.  Prints one JSON line of max-norm relative diffs.
 #include <cstdio>
+#include <algorithm>
 #include <cmath>
 
 #include "sla/backward.hpp"
@@ -43,6 +44,31 @@ int main(int argc, char** argv) {
   auto [ds2, dl2, dw2] = sla::gpu::proj_backward(dout, st2.linear_out, w);
   auto g2 = sla::gpu::sla_backward(st2, q, k, v, ds2, dl2, cfg, layout);
 
+  // backward.hpp:25-38 takes independent cotangents: linearity in (dO^s, dO^l)
+  // (backward_test.cpp:160-190) through the drop-in, with cotangents unrelated through W
+  MatF a_s = bf16_mat(rng, n, d, 1.0), a_l = bf16_mat(rng, n, d, 1.0);
+  MatF b_s = bf16_mat(rng, n, d, 1.0), b_l = bf16_mat(rng, n, d, 1.0);
+  const float ca = 0.75f, cb = -1.25f;  // the mixed cotangents are rounded to bf16 on upload
+  MatF mix_s(n, d), mix_l(n, d);
+  for (size_t e = 0; e < a_s.data.size(); ++e) {
+    mix_s.data[e] = ca * a_s.data[e] + cb * b_s.data[e];
+    mix_l.data[e] = ca * a_l.data[e] + cb * b_l.data[e];
+  }
+  auto ga = sla::gpu::sla_backward(st2, q, k, v, a_s, a_l, cfg, layout);
+  auto gb = sla::gpu::sla_backward(st2, q, k, v, b_s, b_l, cfg, layout);
+  auto gm = sla::gpu::sla_backward(st2, q, k, v, mix_s, mix_l, cfg, layout);
+  auto lin_err = [&](const MatF& ma, const MatF& mb, const MatF& mm) {
+    MatF comb(ma.rows, ma.cols);
+    for (size_t e = 0; e < comb.data.size(); ++e) comb.data[e] = ca * ma.data[e] + cb * mb.data[e];
+    return rel_diff(mm, comb, 1.0);
+  };
+  double linearity = 0.0;
+  for (double x : {lin_err(ga.dq_total, gb.dq_total, gm.dq_total), lin_err(ga.dk_total, gb.dk_total, gm.dk_total),
+                   lin_err(ga.dv, gb.dv, gm.dv)})
+    linearity = std::max(linearity, x);
+  // the same independent cotangents through the reference
+  auto gr = sla::sla_backward(st, q, k, v, a_s, a_l, cfg, layout, 8);
+
   const bool labels_equal = st.mask.labels == st2.mask.labels;
   const bool counters_equal =
       c_ref.sparse_block_matmuls == c_gpu.sparse_block_matmuls &&
@@ -53,9 +79,16 @@ int main(int argc, char** argv) {
       c_ref.aggregation.table_build_additions == c_gpu.aggregation.table_build_additions;
   std::printf(
       "{\"n\": %zu, \"d\": %zu, \"labels_equal\": %s, \"counters_equal\": %s, \"o\": %.3e, \"o_s\": %.3e, \"o_l\": %.3e, "
-      "\"dq_total\": %.3e, \"dk_total\": %.3e, \"dv\": %.3e, \"dw\": %.3e}\n",
+      "\"dq_total\": %.3e, \"dk_total\": %.3e, \"dv\": %.3e, \"dw\": %.3e, \"dproj\": %.3e, \"dl\": %.3e, "
+      "\"dq\": %.3e, \"dk\": %.3e, \"dq_feat\": %.3e, \"dk_feat\": %.3e, "
+      "\"split_dq_total\": %.3e, \"split_dk_total\": %.3e, \"split_dv\": %.3e, \"split_dproj\": %.3e, "
+      "\"linearity\": %.3e}\n",
       n, d, labels_equal ? "true" : "false", counters_equal ? "true" : "false", rel_diff(o2, o, 1.0), rel_diff(st2.sparse_out, st.sparse_out, 1.0),
       rel_diff(st2.linear_out, st.linear_out, 1.0), rel_diff(g2.dq_total, g.dq_total, 1.0),
-      rel_diff(g2.dk_total, g.dk_total, 1.0), rel_diff(g2.dv, g.dv, 1.0), rel_diff(g2.dproj, dw, 1.0));
+      rel_diff(g2.dk_total, g.dk_total, 1.0), rel_diff(g2.dv, g.dv, 1.0), rel_diff(dw2, dw, 1.0),
+      rel_diff(g2.dproj, g.dproj, 1.0), rel_diff(dl2, dl, 1.0), rel_diff(g2.dq, g.dq, 1.0), rel_diff(g2.dk, g.dk, 1.0),
+      rel_diff(g2.dq_feat, g.dq_feat, 1.0), rel_diff(g2.dk_feat, g.dk_feat, 1.0),
+      rel_diff(ga.dq_total, gr.dq_total, 1.0), rel_diff(ga.dk_total, gr.dk_total, 1.0), rel_diff(ga.dv, gr.dv, 1.0),
+      rel_diff(ga.dproj, gr.dproj, 1.0), linearity);
   return labels_equal && counters_equal ? 0 : 1;
 }

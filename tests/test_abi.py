@@ -95,3 +95,33 @@ def test_autograd_caller_validates_shapes_before_any_launch():
         sparse_linear_attention(q, q, q, torch.zeros(3, 64, 64))
     with pytest.raises(ValueError):
         sparse_linear_attention(q, q, q, torch.zeros(64, 64), layout="nhd")
+
+
+def test_fast_forward_rejects_null_branch_outputs():
+    """The tcgen05 forward stores O^s and O^l by TMA: NULL is an InvalidArgument, returned before
+    any device work (fake device pointers are never dereferenced)."""
+    p = _p(d=128)
+    fake = C.c_void_p(0x1000)
+    rc = L.lib().sla_b200_forward(C.byref(p), fake, fake, fake, None, None, None, None, fake, fake, fake,
+                                  fake, None)
+    assert rc == L.ERR_INVALID
+    assert "o_s and o_l are required" in L.lib().sla_b200_last_error().decode()
+
+
+def test_split_backward_requires_linear_cotangent():
+    p = _p(d=128)
+    fake = C.c_void_p(0x1000)
+    rc = L.lib().sla_b200_backward_split(C.byref(p), *([fake] * 7), None, *([fake] * 4), None, fake, fake, None)
+    assert rc == L.ERR_INVALID
+    assert "cotangent" in L.lib().sla_b200_last_error().decode()
+
+
+def test_launch_count_survives_queries():
+    """sla_b200_state_labels / validate / query / sizes launch nothing and leave the previous
+    call's launch count readable (bench.py counts kernels through it)."""
+    p = _p()
+    before = L.lib().sla_b200_last_launch_count()
+    assert L.lib().sla_b200_validate(C.byref(p)) == 0
+    info = L.Info()
+    assert L.lib().sla_b200_query(C.byref(p), C.byref(info)) == 0
+    assert L.lib().sla_b200_last_launch_count() == before

@@ -12,7 +12,7 @@ pytestmark = pytest.mark.gpu
 
 
 def _gemm(A, B, M, N, K, batch, a_mn, b_mn, out_f32):
-    lib = L.lib()
+    lib = L.diag_lib()
     fn = lib.sla_b200_diag_gemm
     fn.argtypes = [C.c_void_p] * 3 + [C.c_int] * 7 + [C.c_void_p]
     out = torch.empty((batch, M, N), dtype=torch.float32 if out_f32 else torch.bfloat16, device="cuda")

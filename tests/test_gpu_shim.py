@@ -19,5 +19,11 @@ def test_cpp_dropin_matches_reference(n, d, agg):
     assert out.returncode == 0, out.stdout + out.stderr
     r = json.loads(out.stdout.strip().splitlines()[-1])
     assert r["labels_equal"] and r["counters_equal"]
-    for key in ("o", "o_s", "o_l", "dq_total", "dk_total", "dv", "dw"):
-        assert r[key] <= 2e-2, (key, r[key])
+    # the reference's training-step sequence (combine_outputs, proj_backward and sla_backward all on
+    # the device), the SlaGradients parts, and sla_backward on independent cotangents (split_*)
+    for key in ("o", "o_s", "o_l", "dq_total", "dk_total", "dv", "dw", "dproj", "dl", "dq", "dk", "dq_feat",
+                "dk_feat", "split_dq_total", "split_dk_total", "split_dv", "split_dproj"):
+        assert r[key] <= 1.5e-2, (key, r[key])
+    # linearity in (dO^s, dO^l) (backward_test.cpp:160-190): exact up to the bf16 rounding of the
+    # mixed cotangents and of the bf16 gradients
+    assert r["linearity"] <= 1.5e-2, r["linearity"]

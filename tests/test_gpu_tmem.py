@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 
 
 def test_tmem_layouts():
-    f = L.lib().sla_b200_diag_tmem
+    f = L.diag_lib().sla_b200_diag_tmem
     f.argtypes = [C.c_void_p] * 4
     x2 = torch.zeros(128 * 16, dtype=torch.int32, device="cuda")
     lo = torch.zeros(256, device="cuda")
