@@ -273,6 +273,13 @@ __global__ void k_classify(const R* __restrict__ scores, int Tm,
 // (weight desc, column asc), with the distance >= EPL passes done by shuffles.  No block
 // barriers: a whole row is one warp's registers.
 // ---------------------------------------------------------------------------------------
+#ifndef SLAB_CLASSIFY_RANK
+#define SLAB_CLASSIFY_RANK 1  // 1: k_classify_rank (rank raw scores) for T <= 2048
+#endif
+// diagnostics: rows that took k_classify_rank's exact P_c path (null: not counted)
+static int* g_exact_counter = nullptr;
+int* classify_exact_counter() { return g_exact_counter; }
+void set_classify_exact_counter(int* p) { g_exact_counter = p; }
 #ifndef SLAB_CLASSIFY_SELECT
 #define SLAB_CLASSIFY_SELECT 1  // 1: quickselect of the two rank thresholds; 0: full bitonic sort
 #endif
@@ -504,6 +511,304 @@ __global__ void __launch_bounds__(256) k_classify_warp(const R* __restrict__ sco
 }
 
 // ---------------------------------------------------------------------------------------
+// K2 by ranking the raw pooled scores (T <= 2048): one warp per block row, the row in shared
+// memory with interleaved ownership (element j = 32 r + lane: conflict-free).
+//
+// P_c = g(S) with g(s) = round(exp(round(s - m)) / sum) (mask.cpp:65-79) is monotone
+// non-decreasing in s, so stable_sort's (P_c desc, j asc) order (mask.cpp:105-113) and the
+// (S desc, j asc) order put the same blocks on each side of a rank boundary whenever g
+// separates the scores next to it strictly.  Per boundary (rank n1 and rank T - n_neg) the
+// kernel finds A = S at rank K - 1 and B = S at rank K by quickselect and checks
+//   A > B:   g(A) > g(B);
+//   A == B:  g(min{s > A}) > g(A) > g(max{s < A})   (the tie class straddles the boundary),
+// where x > y => g(x) > g(y) is guaranteed once exp(x - m) > exp(y - m) (1 + 2^-50): the division
+// by the common sum cannot merge values a factor 1 + 2^-50 apart.  Then the labels follow from
+// the S-ranks and the row needs neither the T exponentials nor the sequential T-long normaliser.
+// Otherwise (near-ties, or P_c requested) the warp computes P_c exactly as k_classify_warp does
+// -- max-shifted exp, the ascending sequential normaliser, one rounded division -- and ranks P_c.
+// ---------------------------------------------------------------------------------------
+template <typename R>
+__device__ __forceinline__ bool g_separated(R x, R y, R m) {  // x > y: is g(x) > g(y) certain?
+  const R ex = exp_r(x - m), ey = exp_r(y - m);
+  constexpr R eps = sizeof(R) == 8 ? R(8.8817841970012523e-16) : R(9.5367431640625e-07);  // 2^-50, 2^-20
+  constexpr R tiny = sizeof(R) == 8 ? R(2.2250738585072014e-308) : R(1.17549435e-38f);
+  if (ey == R(0)) return ex >= tiny;  // p(x) = ex / sum (sum <= T) cannot underflow to 0
+  return ex > ey * (R(1) + eps);
+}
+
+// position of the n-th (0-based) set bit of m
+__device__ __forceinline__ int nth_set_bit(uint64_t m, int n) {
+  const uint32_t lo = uint32_t(m);
+  const int c = __popc(lo);
+  if (n < c) return int(__fns(lo, 0, n + 1));
+  return 32 + int(__fns(uint32_t(m >> 32), 0, n - c + 1));
+}
+
+// EPL > 0: the row lives in registers (EPL = T / 32 rounded up, compile-time: T <= 512);
+// EPL == 0: in shared memory (T <= 2048).  Element j = 32 r + lane either way.
+#define SLAB_RANK_FOR(r) _Pragma("unroll (EPL > 0 ? EPL : 1)") for (int r = 0; r < (EPL > 0 ? EPL : E); ++r)
+template <typename R, int EPL>
+__global__ void __launch_bounds__(256) k_classify_rank(const R* __restrict__ scores, long long rows, int Tn,
+                                                       int n1, int n_neg, int8_t* __restrict__ labels,
+                                                       int* __restrict__ crit_cnt, int* __restrict__ crit_idx,
+                                                       int* __restrict__ marg_cnt, double* __restrict__ p_c_out,
+                                                       __nv_bfloat16* __restrict__ m0, int m0_ld,
+                                                       int* __restrict__ exact_rows) {
+  pdl_entry();  // launched by launch_pdl
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int E = EPL > 0 ? EPL : (Tn + 31) >> 5;  // elements per lane (<= 64)
+  const int Tp = E * 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  R* v = reinterpret_cast<R*>(smem_raw) + (size_t)warp * Tp;  // the row (EPL == 0) / exact-path scratch
+  int8_t* lab = reinterpret_cast<int8_t*>(reinterpret_cast<R*>(smem_raw) + (size_t)8 * Tp) + (size_t)warp * Tp;
+  const long long row = (long long)blockIdx.x * 8 + warp;
+  if (row >= rows) return;
+  constexpr unsigned FULL = 0xffffffffu;
+  const R* srow = scores + row * Tn;
+  R key[EPL > 0 ? EPL : 1] = {};
+  auto val = [&](int r) -> R {
+    if constexpr (EPL > 0) return key[r];
+    else return v[32 * r + lane];
+  };
+  auto set = [&](int r, R x) {
+    if constexpr (EPL > 0) key[r] = x;
+    else v[32 * r + lane] = x;
+  };
+  uint64_t valid = 0;
+  R m = -R(INFINITY);
+  SLAB_RANK_FOR(r) {
+    const int j = 32 * r + lane;
+    const R x = j < Tn ? srow[j] : -R(INFINITY);
+    set(r, x);
+    if (j < Tn) {
+      valid |= uint64_t(1) << r;
+      m = x > m ? x : m;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const R other = __shfl_xor_sync(FULL, m, o);
+    m = other > m ? other : m;
+  }
+  __syncwarp();
+  // The value at 0-based rank K of the valid entries (descending), with #(>) and #(==).  The
+  // first step brackets rank K between two quantiles of a 32-entry sample (one per lane, sorted
+  // across the warp); then quickselect with pivots drawn from the remaining candidates.
+  auto select_desc = [&](int K, int& gt, int& eq) -> R {
+    uint64_t cm = valid;
+    int k = K, base_gt = 0;
+    {
+      R smp = (valid & 1u) ? val(0) : -R(INFINITY);
+#pragma unroll
+      for (int kk = 2; kk <= 32; kk <<= 1)
+#pragma unroll
+        for (int jj = kk >> 1; jj > 0; jj >>= 1) {
+          const R o = __shfl_xor_sync(FULL, smp, jj);
+          const bool keep_max = ((lane & jj) == 0) == ((lane & kk) == 0);
+          smp = keep_max ? (o > smp ? o : smp) : (o < smp ? o : smp);
+        }
+      const int q = int((long long)K * 32 / Tn);
+      const R hi = __shfl_sync(FULL, smp, q > 1 ? q - 2 : 0);
+      const R lo = __shfl_sync(FULL, smp, q < 29 ? q + 2 : 31);
+      uint64_t gm = 0, bm = 0;
+      SLAB_RANK_FOR(r) {
+        const R x = val(r);
+        gm |= uint64_t(x > hi) << r;
+        bm |= uint64_t(x >= lo && x <= hi) << r;
+      }
+      gm &= cm;
+      bm &= cm;
+      const int g = __reduce_add_sync(FULL, __popcll(gm));
+      const int b = __reduce_add_sync(FULL, __popcll(bm));
+      if (k < g) {
+        cm = gm;
+      } else if (k < g + b) {
+        cm = bm;
+        k -= g;
+        base_gt = g;
+      } else {
+        cm &= ~(gm | bm);
+        k -= g + b;
+        base_gt = g + b;
+      }
+    }
+    for (int it = 0;; ++it) {
+      const unsigned has = __ballot_sync(FULL, cm != 0u);
+      if (has == 0u) {  // only with non-finite scores: never hang
+        gt = eq = 0;
+        return -R(INFINITY);
+      }
+      const int rot = (it * 11) & 31;
+      const unsigned rm = rot ? (has >> rot) | (has << (32 - rot)) : has;
+      const int src = (__ffs(rm) - 1 + rot) & 31;
+      R mv = R(0);
+      if (lane == src) {
+        const int rr = nth_set_bit(cm, __popcll(cm) >> 1);  // the lane's median-index candidate
+        if constexpr (EPL > 0) {
+#pragma unroll
+          for (int r = 0; r < EPL; ++r)
+            if (r == rr) mv = key[r];
+        } else {
+          mv = v[32 * rr + lane];
+        }
+      }
+      const R pivot = __shfl_sync(FULL, mv, src);
+      uint64_t gm = 0, em = 0;
+      SLAB_RANK_FOR(r) {
+        const R x = val(r);
+        gm |= uint64_t(x > pivot) << r;
+        em |= uint64_t(x == pivot) << r;
+      }
+      gm &= cm;
+      em &= cm;
+      const int g = __reduce_add_sync(FULL, __popcll(gm));
+      const int e = __reduce_add_sync(FULL, __popcll(em));
+      if (k < g) {
+        cm = gm;
+      } else if (k < g + e) {
+        gt = base_gt + g;
+        eq = e;
+        return pivot;
+      } else {
+        k -= g + e;
+        base_gt += g + e;
+        cm &= ~(gm | em);
+      }
+    }
+  };
+  auto max_below = [&](R a, bool& found) -> R {  // max{valid x < a}
+    R best = -R(INFINITY);
+    bool f = false;
+    SLAB_RANK_FOR(r) {
+      const R x = val(r);
+      if (((valid >> r) & 1u) && x < a && (!f || x > best)) {
+        best = x;
+        f = true;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const R ob = __shfl_xor_sync(FULL, best, o);
+      const bool of = __shfl_xor_sync(FULL, f, o);
+      if (of && (!f || ob > best)) best = ob;
+      f = f || of;
+    }
+    found = f;
+    return best;
+  };
+  auto min_above = [&](R a) -> R {  // min{valid x > a} (the caller knows one exists)
+    R best = R(INFINITY);
+    SLAB_RANK_FOR(r) {
+      const R x = val(r);
+      if (((valid >> r) & 1u) && x > a && x < best) best = x;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const R ob = __shfl_xor_sync(FULL, best, o);
+      best = ob < best ? ob : best;
+    }
+    return best;
+  };
+  // ---- rank boundaries in the S domain, with the separation checks
+  const int K1 = n1, K2 = Tn - n_neg;  // in-set sizes: critical, non-negligible
+  int g1 = 0, e1 = 0, g2 = 0, e2 = 0;
+  R A1 = R(0), A2 = R(0);
+  bool exact = p_c_out != nullptr;
+  auto boundary_ok = [&](int K, R A, int g, int e) -> bool {  // A = the value at rank K - 1
+    if (K >= Tn) return true;  // nothing outside the set
+    if (g + e > K) {           // the tie class of A straddles the boundary
+      bool ok = true;
+      if (g > 0) ok = g_separated(min_above(A), A, m);
+      bool f;
+      const R lo = max_below(A, f);
+      if (f) ok = ok && g_separated(A, lo, m);
+      return ok;
+    }
+    bool f;
+    const R B = max_below(A, f);  // the value at rank K
+    return !f || g_separated(A, B, m);
+  };
+  if (!exact) {
+    A1 = select_desc(K1 - 1, g1, e1);
+    exact = !boundary_ok(K1, A1, g1, e1);
+    if (!exact && n_neg > 0) {
+      A2 = select_desc(K2 - 1, g2, e2);
+      exact = !boundary_ok(K2, A2, g2, e2);
+    }
+  }
+  if (exact) {  // P_c exactly as the reference computes it (mask.cpp:65-79), then rank P_c
+    if (exact_rows && lane == 0) atomicAdd(exact_rows, 1);
+    SLAB_RANK_FOR(r) {
+      const int j = 32 * r + lane;
+      const R e = j < Tn ? exp_r(val(r) - m) : R(0);
+      if (EPL > 0) set(r, e);
+      v[j] = e;  // shared copy for the sequential normaliser
+    }
+    __syncwarp();
+    R sum = R(0);
+    if (lane == 0)  // the reference's sequential ascending normaliser (mask.cpp:73-77)
+      for (int j = 0; j < Tn; ++j) sum = add_rn(sum, v[j]);
+    sum = __shfl_sync(FULL, sum, 0);
+    __syncwarp();
+    SLAB_RANK_FOR(r) {
+      const int j = 32 * r + lane;
+      if (j < Tn) {
+        const R p = div_rn(val(r), sum);
+        set(r, p);
+        if (p_c_out) p_c_out[row * Tn + j] = double(p);
+      } else {
+        set(r, -R(INFINITY));
+      }
+    }
+    __syncwarp();
+    A1 = select_desc(K1 - 1, g1, e1);
+    if (n_neg > 0) A2 = select_desc(K2 - 1, g2, e2);
+  }
+  // ---- labels: in-set = {x > A} plus the first K - #(x > A) ties of A in index order
+  int run1 = 0, run2 = 0;
+  const unsigned lt = (1u << lane) - 1u;
+  SLAB_RANK_FOR(r) {
+    const int j = 32 * r + lane;
+    const bool ok = j < Tn;
+    const R x = val(r);
+    const bool t1 = ok && x == A1, t2 = ok && n_neg > 0 && x == A2;
+    const unsigned b1 = __ballot_sync(FULL, t1), b2 = __ballot_sync(FULL, t2);
+    const bool crit = x > A1 || (t1 && run1 + __popc(b1 & lt) < K1 - g1);
+    const bool keep = n_neg == 0 || x > A2 || (t2 && run2 + __popc(b2 & lt) < K2 - g2);
+    run1 += __popc(b1);
+    run2 += __popc(b2);
+    if (ok) lab[j] = crit ? int8_t(1) : (keep ? int8_t(0) : int8_t(-1));
+  }
+  __syncwarp();
+  int8_t* lrow = labels + row * Tn;
+  for (int j = lane; j < Tn; j += 32) lrow[j] = lab[j];
+  if (m0) {  // fast path: the marginal indicator row (A operand of H = M0 h), bf16 pairs
+    __nv_bfloat162* mrow = reinterpret_cast<__nv_bfloat162*>(m0 + row * m0_ld);
+    for (int j2 = lane; j2 < m0_ld / 2; j2 += 32) {
+      const int j = 2 * j2;
+      mrow[j2] = __floats2bfloat162_rn(j < Tn && lab[j] == 0 ? 1.f : 0.f,
+                                       j + 1 < Tn && lab[j + 1] == 0 ? 1.f : 0.f);
+    }
+  }
+  int base = 0, marg = 0;
+  int* crow = crit_idx + row * Tn;
+  for (int j0 = 0; j0 < Tn; j0 += 32) {
+    const int j = j0 + lane;
+    const int l = j < Tn ? lab[j] : -1;
+    const unsigned bc = __ballot_sync(FULL, l == 1);
+    const unsigned bm = __ballot_sync(FULL, l == 0);
+    if (l == 1) crow[base + __popc(bc & lt)] = j;
+    base += __popc(bc);
+    marg += __popc(bm);
+  }
+  if (lane == 0) {
+    crit_cnt[row] = base;
+    marg_cnt[row] = marg;
+  }
+}
+#undef SLAB_RANK_FOR
+
+// ---------------------------------------------------------------------------------------
 // build_lookup for an injected label grid (mask.cpp:121-153); flags invalid labels.
 // ---------------------------------------------------------------------------------------
 __global__ void k_build_lut(const int8_t* __restrict__ labels, int Tm, int Tn,
@@ -631,6 +936,24 @@ static bool classify_t(const Dims& D, const In* q, const In* k, const StateBufs&
   const int P2 = next_pow2(D.Tn);
   const long long rows = D.U * (long long)D.Tm;
   const unsigned wblocks = unsigned((rows + 7) / 8);
+  if (SLAB_CLASSIFY_RANK && D.Tn <= 2048) {  // rank the raw scores (exact P_c only where needed)
+    const int Tp = (D.Tn + 31) / 32 * 32;
+    const size_t rsm = size_t(8) * Tp * (sizeof(R) + 1);
+    auto go = [&](auto kern) {
+      SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rsm)));
+      launch_pdl(kern, wblocks, 256, rsm, st, (const R*)scores, rows, D.Tn, D.n1, D.n_neg, s.labels, s.crit_cnt,
+                 s.crit_idx, s.marg_cnt, p_c, s.M0, int(m0_stride(D)), classify_exact_counter());
+      check_launch("k_classify", st);
+    };
+    const int E = Tp / 32;  // the row in registers up to T = 512
+    if (E <= 1) go(k_classify_rank<R, 1>);
+    else if (E <= 2) go(k_classify_rank<R, 2>);
+    else if (E <= 4) go(k_classify_rank<R, 4>);
+    else if (E <= 8) go(k_classify_rank<R, 8>);
+    else if (E <= 16) go(k_classify_rank<R, 16>);
+    else go(k_classify_rank<R, 0>);
+    return true;
+  }
   auto warp_rows = [&](auto kern) {
     launch_pdl(kern, wblocks, 256, 0, st, (const R*)scores, rows, D.Tn, D.n1, D.n_neg, s.labels, s.crit_cnt,
                s.crit_idx, s.marg_cnt, p_c, s.M0, int(m0_stride(D)));

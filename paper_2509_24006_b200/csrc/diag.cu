@@ -577,3 +577,10 @@ extern "C" int sla_b200_diag_gemm(const void* A, const void* B, void* C, int bat
     return 1;
   }
 }
+
+// rows of k_classify_rank that fall back to the exact P_c ranking are counted into *dev_counter
+// (a device int; null stops counting) -- tests/test_gpu_classify.py checks the fallback is rare
+extern "C" int sla_b200_diag_classify_exact(int* dev_counter) {
+  slab::set_classify_exact_counter(dev_counter);
+  return 0;
+}

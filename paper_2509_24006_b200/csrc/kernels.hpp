@@ -15,6 +15,9 @@ bool launch_classify(const Dims& D, int dtype, int mask_precision, const void* q
 void launch_build_lut(const Dims& D, const StateBufs& s, long long* bad, cudaStream_t st);
 void launch_build_csc(const Dims& D, const StateBufs& s, cudaStream_t st);
 void launch_build_m0(const Dims& D, const StateBufs& s, cudaStream_t st);
+// diagnostics (diag.cu): a device int counting the rows k_classify_rank resolved by exact P_c
+int* classify_exact_counter();
+void set_classify_exact_counter(int* p);
 // counters.cu: device accounting from the LUT (flops_report, ExecCounters)
 void launch_row_stats(const Dims& D, const int8_t* labels, int g, int4* out, cudaStream_t st);
 void launch_lin_rows(const Dims& D, int dtype, const void* q, const float* Z, bool z3,
