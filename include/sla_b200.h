@@ -43,7 +43,7 @@
 extern "C" {
 #endif
 
-#define SLA_B200_ABI_VERSION 1
+#define SLA_B200_ABI_VERSION 2
 
 /* status codes: mirror the reference CLI exit codes (tools/sla_main.cpp:564-570) */
 #define SLA_B200_OK 0
@@ -93,6 +93,11 @@ typedef struct sla_b200_problem {
   int32_t dtype;    /* SLA_B200_BF16 | SLA_B200_F32       */
   int32_t mask_precision; /* SLA_B200_MASK_*              */
   uint32_t flags;   /* SLA_B200_FLAG_*                    */
+  /* Rectangular view (ABI 2; 0 = n): key / value rows per unit when they differ from the query
+   * rows n -- a partitioned execution in which this call owns a range of query blocks against a
+   * range of key blocks (paper_2509_24006_b200/runner.py: sub-head and sequence sharding).
+   * One unit (batch = heads = 1), tcgen05 path only.  T_m = n / b_q, T_n = n_kv / b_kv. */
+  int64_t n_kv;
 } sla_b200_problem;
 
 /* Per-call execution summary (the device analogue of ExecCounters, forward.hpp:46-50). */
@@ -225,6 +230,23 @@ int sla_b200_proj_backward(const sla_b200_problem* p, const void* d_out, const v
  * forward's outputs (O^s, O^l, lse) run sla_b200_backward_split on them. */
 int sla_b200_build_state(const sla_b200_problem* p, const void* q, const void* k, const void* v,
                          const int8_t* mask, void* state, void* workspace, void* stream);
+
+/* The backward in two phases, for partitioned execution (n_kv views; runner.py):
+ *   rows (backward.cpp:46-120): for this call's query rows -- dq_total, dW partial (optional,
+ *     over these rows only), and the row summaries the column phase needs: ds_out = D^s
+ *     (f32 [U, N]), dh_out = dH_i (bf16 [U, T_m, d, d]), dz_out = dZ_i as three bf16 parts
+ *     (bf16 [U, T_m, 3 d]).  d_out_linear NULL: dO^l = d_out W^T; else the given dO^l (w unused).
+ *   cols (backward.cpp:122-199): for this call's key blocks against EVERY query row of the unit
+ *     (n = all rows, n_kv = these keys): lse, ds, dh, dz of all rows, the label grid of all rows
+ *     restricted to these key blocks ([U, T_m, T_n]); writes dk_total and dv of these keys.
+ *     `state` is scratch for this view (labels, column lists, M0). */
+int sla_b200_backward_rows(const sla_b200_problem* p, const void* q, const void* k, const void* v, const void* w,
+                           const void* o_s, const void* o_l, const float* lse, const void* d_out,
+                           const void* d_out_linear, void* dq, float* dw, float* ds_out, void* dh_out, void* dz_out,
+                           const void* state, void* workspace, void* stream);
+int sla_b200_backward_cols(const sla_b200_problem* p, const void* q, const void* k, const void* v, const float* lse,
+                           const void* d_out, const float* ds, const void* dh, const void* dz, const int8_t* labels,
+                           void* dk, void* dv, void* state, void* workspace, void* stream);
 
 /* Per-kernel CUDA-event profiler of this library's own launches (bench/diagnostics).
  * sla_b200_profiler(1) clears and enables, (0) disables.  The report is text lines

@@ -25,7 +25,7 @@ class Problem(C.Structure):
         ("batch", C.c_int64), ("heads", C.c_int64), ("n", C.c_int64), ("d", C.c_int64),
         ("b_q", C.c_int64), ("b_kv", C.c_int64), ("k_h", C.c_double), ("k_l", C.c_double),
         ("phi", C.c_int32), ("dtype", C.c_int32), ("mask_precision", C.c_int32),
-        ("flags", C.c_uint32),
+        ("flags", C.c_uint32), ("n_kv", C.c_int64),
     ]
 
 
@@ -64,6 +64,7 @@ EXPORTS = [
     "sla_b200_backward", "sla_b200_backward_ex", "sla_b200_state_labels",
     "sla_b200_flops_report", "sla_b200_exec_counters", "sla_b200_backward_split",
     "sla_b200_combine_outputs", "sla_b200_proj_backward", "sla_b200_build_state",
+    "sla_b200_backward_rows", "sla_b200_backward_cols",
 ]
 
 
@@ -91,6 +92,8 @@ def lib():
     L.sla_b200_combine_outputs.argtypes = [P] + [vp] * 5
     L.sla_b200_proj_backward.argtypes = [P] + [vp] * 7
     L.sla_b200_build_state.argtypes = [P] + [vp] * 7
+    L.sla_b200_backward_rows.argtypes = [P] + [vp] * 17
+    L.sla_b200_backward_cols.argtypes = [P] + [vp] * 14
     L.sla_b200_flops_report.argtypes = [P, vp, C.POINTER(Flops), vp, vp]
     L.sla_b200_exec_counters.argtypes = [P, vp, vp, C.c_int, C.c_int, C.POINTER(Counters), vp, vp]
     for name in EXPORTS:

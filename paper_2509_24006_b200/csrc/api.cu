@@ -43,6 +43,16 @@ Dims resolve(const sla_b200_problem* p) {
       throw InvalidArgument("make_block_layout: b_kv=" + std::to_string(p->b_kv) +
                             " does not divide N=" + std::to_string(p->n));
   }
+  if (p->n_kv < 0) throw InvalidArgument("make_block_layout: all sizes must be positive");
+  if (p->n_kv > 0 && p->n_kv != p->n) {  // rectangular: a query-row range against a key range
+    if (p->batch * p->heads != 1 || ragged || bnhd || (p->flags & (SLA_B200_FLAG_GENERIC | SLA_B200_FLAG_CHECK_FINITE)) ||
+        p->dtype != SLA_B200_BF16 || p->b_q != 64 || p->b_kv != 64 || (p->d != 64 && p->d != 128))
+      throw InvalidArgument("sla_b200: n_kv != n (a partitioned view) needs one unit on the tcgen05 path "
+                            "(bf16, b_q = b_kv = 64, d in {64, 128}, no staging or finiteness checks)");
+    if (p->n_kv % p->b_kv != 0)
+      throw InvalidArgument("make_block_layout: b_kv=" + std::to_string(p->b_kv) +
+                            " does not divide N=" + std::to_string(p->n_kv));
+  }
   if (!(p->k_h > 0.0 && p->k_h <= 100.0)) throw InvalidArgument("config: k_h must be in (0, 100]");
   if (!(p->k_l >= 0.0 && p->k_l < 100.0)) throw InvalidArgument("config: k_l must be in [0, 100)");
   if (p->k_h + p->k_l > 100.0) throw InvalidArgument("config: k_h + k_l must be <= 100");
@@ -59,11 +69,13 @@ Dims resolve(const sla_b200_problem* p) {
   D.bnhd = bnhd;
   D.staged = ragged || bnhd;
   D.N = ragged ? (p->n + 63) / 64 * 64 : p->n;
+  D.Nk = p->n_kv > 0 ? p->n_kv : D.N;
+  D.Nk_valid = p->n_kv > 0 ? p->n_kv : D.N_valid;
   D.d = int(p->d);
   D.bq = int(p->b_q);
   D.bkv = int(p->b_kv);
   D.Tm = int(D.N / p->b_q);
-  D.Tn = int(D.N / p->b_kv);
+  D.Tn = int(D.Nk / p->b_kv);
   D.phi = p->phi;
   if (D.Tn > 8192 || D.Tm > 65535)
     throw InvalidArgument("sla_b200: at most 8192 key blocks per row are supported");
@@ -496,6 +508,50 @@ int sla_b200_backward_split(const sla_b200_problem* p, const void* q, const void
     if (!d_out_linear) throw InvalidArgument("sla_backward: cotangent shape mismatch");
     backward_impl(p, q, k, v, nullptr, o_s, o_l, lse, d_out_sparse, d_out_linear, dq, dk, dv, dw, parts,
                   state, workspace, stream);
+  });
+}
+
+int sla_b200_backward_rows(const sla_b200_problem* p, const void* q, const void* k, const void* v, const void* w,
+                           const void* o_s, const void* o_l, const float* lse, const void* d_out,
+                           const void* d_out_linear, void* dq, float* dw, float* ds_out, void* dh_out, void* dz_out,
+                           const void* state, void* workspace, void* stream) {
+  return guarded([&] {
+    const Dims D = resolve(p);
+    require_supported(p, D);
+    if (!use_fast(p, D) || D.staged)
+      throw InvalidArgument("sla_b200_backward_rows: the tcgen05 path without staging only");
+    if (!q || !k || !v || !o_s || !o_l || !lse || !d_out || !dq || !ds_out || !dh_out || !dz_out ||
+        (!d_out_linear && !w))
+      throw InvalidArgument("sla_backward: all tensors are required");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    prof_mark("", st);
+    StateBufs s;
+    WorkBufs wb;
+    buffers(p, D, state, workspace, s, wb);
+    fast_backward_rows(D, q, k, v, w, o_s, o_l, lse, d_out, d_out_linear, dq, dw, s, wb,
+                       static_cast<__nv_bfloat16*>(dh_out), static_cast<__nv_bfloat16*>(dz_out), ds_out, st);
+  });
+}
+
+int sla_b200_backward_cols(const sla_b200_problem* p, const void* q, const void* k, const void* v, const float* lse,
+                           const void* d_out, const float* ds, const void* dh, const void* dz, const int8_t* labels,
+                           void* dk, void* dv, void* state, void* workspace, void* stream) {
+  return guarded([&] {
+    const Dims D = resolve(p);
+    require_supported(p, D);
+    if (!use_fast(p, D) || D.staged)
+      throw InvalidArgument("sla_b200_backward_cols: the tcgen05 path without staging only");
+    if (!q || !k || !v || !lse || !d_out || !ds || !dh || !dz || !labels || !dk || !dv)
+      throw InvalidArgument("sla_backward: all tensors are required");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    prof_mark("", st);
+    StateBufs s;
+    WorkBufs wb;
+    buffers(p, D, state, workspace, s, wb);
+    if (labels != s.labels)
+      SLAB_CUDA(cudaMemcpyAsync(s.labels, labels, size_t(D.U) * D.Tm * D.Tn, cudaMemcpyDeviceToDevice, st));
+    fast_backward_cols(D, q, k, v, lse, d_out, ds, static_cast<const __nv_bfloat16*>(dh),
+                       static_cast<const __nv_bfloat16*>(dz), dk, dv, s, wb, st);
   });
 }
 

@@ -575,11 +575,11 @@ template <int D>
 void launch_cols_t(const Dims& Dm, const void* q, const void* k, const void* v, const void* d_out,
                    const __nv_bfloat16* Ha, BwdParams p, cudaStream_t st) {
   CUtensorMap tq, tdo, tk, tv, th;
-  const uint64_t rows = uint64_t(Dm.U) * Dm.N;
+  const uint64_t rows = uint64_t(Dm.U) * Dm.N, krows = uint64_t(Dm.U) * Dm.Nk;
   make_tmap_bf16(&tq, q, D, rows, 1, D, 0, 64);
   make_tmap_bf16(&tdo, d_out, D, rows, 1, D, 0, 64);
-  make_tmap_bf16(&tk, k, D, rows, 1, D, 0, 64);
-  make_tmap_bf16(&tv, v, D, rows, 1, D, 0, 64);
+  make_tmap_bf16(&tk, k, D, krows, 1, D, 0, 64);
+  make_tmap_bf16(&tv, v, D, krows, 1, D, 0, 64);
   make_tmap_bf16(&th, Ha, D, uint64_t(Dm.U) * Dm.Tn * D, 1, D, 0, D);
   auto kern = k_bwd_cols<D>;
   SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ColsLayout<D>::kBytes));

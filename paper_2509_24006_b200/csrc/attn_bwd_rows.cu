@@ -819,14 +819,14 @@ void launch_bwd_rows(const Dims& Dm, const void* q, const void* k, const void* v
   p.scale = float(Dm.inv_sqrt_d);
   p.scale_log2 = float(Dm.inv_sqrt_d * 1.4426950408889634);
   p.phi = Dm.phi;
-  const uint64_t rows = uint64_t(Dm.U) * Dm.N;
+  const uint64_t rows = uint64_t(Dm.U) * Dm.N, krows = uint64_t(Dm.U) * Dm.Nk;
   CUtensorMap tq, tdo, tk, tv;
   auto go = [&](auto kern, int bytes, auto dd) {
     constexpr int D = decltype(dd)::value;
     make_tmap_bf16(&tq, q, D, rows, 1, D, 0, 64);
     make_tmap_bf16(&tdo, d_out, D, rows, 1, D, 0, 64);
-    make_tmap_bf16(&tk, k, D, rows, 1, D, 0, 64);
-    make_tmap_bf16(&tv, v, D, rows, 1, D, 0, 64);
+    make_tmap_bf16(&tk, k, D, krows, 1, D, 0, 64);
+    make_tmap_bf16(&tv, v, D, krows, 1, D, 0, 64);
     SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     launch_pdl(kern, dim3(Dm.Tm, unsigned(Dm.U)), kRowsThreads, bytes, st, tq, tdo, tk, tv, p);
     check_launch("k_bwd_rows", st);

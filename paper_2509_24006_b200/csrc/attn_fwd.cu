@@ -541,10 +541,10 @@ template <int D>
 void launch_t(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
               const __nv_bfloat16* Hb, FwdParams p, cudaStream_t st) {
   CUtensorMap tq, tk, tv, th, tw;
-  const uint64_t rows = uint64_t(Dm.U) * Dm.N;
+  const uint64_t rows = uint64_t(Dm.U) * Dm.N, krows = uint64_t(Dm.U) * Dm.Nk;
   make_tmap_bf16(&tq, q, D, rows, 1, D, 0, 64);
-  make_tmap_bf16(&tk, k, D, rows, 1, D, 0, 64);
-  make_tmap_bf16(&tv, v, D, rows, 1, D, 0, 64);
+  make_tmap_bf16(&tk, k, D, krows, 1, D, 0, 64);
+  make_tmap_bf16(&tv, v, D, krows, 1, D, 0, 64);
   make_tmap_bf16(&th, Hb, D, uint64_t(Dm.U) * Dm.Tm * D, 1, D, 0, D);
   if (w)
     make_tmap_bf16(&tw, w, D, uint64_t(Dm.H) * D, 1, D, 0, D);
@@ -583,7 +583,7 @@ void launch_attn_fwd(const Dims& Dm, const void* q, const void* k, const void* v
   p.scale_log2 = float(Dm.inv_sqrt_d * 1.4426950408889634);
   p.has_w = (w != nullptr && o != nullptr) ? 1 : 0;
   p.phi = Dm.phi;
-  p.kv_last = int(Dm.N_valid - (long long)(Dm.Tn - 1) * 64);
+  p.kv_last = int(Dm.Nk_valid - (long long)(Dm.Tn - 1) * 64);
   if (Dm.d == 128)
     launch_t<128>(Dm, q, k, v, w, s.Hb, p, st);
   else

@@ -119,8 +119,8 @@ inline void carve_work(const Dims& D, bool fast, void* base, WorkBufs& w, size_t
   w.Dl = c.take<float>(U * N);
   w.gZ = c.take<float>(U * Tm * d);
   if (fast) {  // tcgen05 path: bf16 operands, the backward writes its totals directly
-    w.hb = c.take<__nv_bfloat16>(U * Tn * d * d);
-    w.kfb = c.take<__nv_bfloat16>(U * N * d);
+    w.hb = c.take<__nv_bfloat16>(U * (Tm > Tn ? Tm : Tn) * d * d);  // h_j (forward), dH_i (backward)
+    w.kfb = c.take<__nv_bfloat16>(U * size_t(D.Nk) * d);
     w.hab = c.take<__nv_bfloat16>(U * Tn * d * d);
     w.gZa = c.take<float>(U * Tn * 3 * d);
     w.dwp = c.take<float>(U * dw_chunks(D) * d * d);

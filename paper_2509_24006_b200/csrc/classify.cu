@@ -6,6 +6,7 @@
 //
 // HBM-bound: Q and K are each read once (vectorised over d, coalesced across threads);
 // everything after pooling works on T x d / T x T data that lives in L2.
+#include <algorithm>
 #include <cfloat>
 #include <type_traits>
 
@@ -57,13 +58,17 @@ __global__ void k_pool(const In* __restrict__ x, R* __restrict__ out, long long 
 template <typename R>
 __global__ void __launch_bounds__(32) k_pool2_bf16(const __nv_bfloat16* __restrict__ q,
                                                    const __nv_bfloat16* __restrict__ k,
-                                                   R* __restrict__ pq, R* __restrict__ pk, long long N,
-                                                   int d, int b, int T, long long n_valid) {
+                                                   R* __restrict__ pq, R* __restrict__ pk, long long Nq,
+                                                   long long Nk, int d, int b, int Tq, int Tk,
+                                                   long long nq_valid, long long nk_valid) {
   pdl_entry();  // launched by launch_pdl
   const long long u = blockIdx.y;
   const int g = blockIdx.x;
   const __nv_bfloat16* x = blockIdx.z ? k : q;
   R* out = blockIdx.z ? pk : pq;
+  const long long N = blockIdx.z ? Nk : Nq, n_valid = blockIdx.z ? nk_valid : nq_valid;
+  const int T = blockIdx.z ? Tk : Tq;
+  if (g >= T) return;
   const __nv_bfloat16* base = x + (u * N + (long long)g * b) * d;
   const long long left = n_valid - (long long)g * b;
   const int rows = left < b ? int(left) : b;
@@ -914,7 +919,8 @@ static bool classify_t(const Dims& D, const In* q, const In* k, const StateBufs&
   bool pooled = false;
   if constexpr (std::is_same<In, __nv_bfloat16>::value) {
     if (D.d % 4 == 0 && D.bq == D.bkv) {
-      launch_pdl(k_pool2_bf16<R>, dim3(D.Tm, unsigned(D.U), 2), 32, 0, st, q, k, pq, pk, D.N, D.d, D.bq, D.Tm, D.N_valid);
+      launch_pdl(k_pool2_bf16<R>, dim3(std::max(D.Tm, D.Tn), unsigned(D.U), 2), 32, 0, st, q, k, pq, pk, D.N, D.Nk,
+                 D.d, D.bq, D.Tm, D.Tn, D.N_valid, D.Nk_valid);
       check_launch("k_pool", st);
       pooled = true;
     }
@@ -922,7 +928,7 @@ static bool classify_t(const Dims& D, const In* q, const In* k, const StateBufs&
   if (!pooled) {
     k_pool<R, In><<<dim3(D.Tm, unsigned(D.U)), pt, 0, st>>>(q, pq, D.N, D.d, D.bq, D.Tm, D.N_valid);
     check_launch("k_pool(q)", st);
-    k_pool<R, In><<<dim3(D.Tn, unsigned(D.U)), pt, 0, st>>>(k, pk, D.N, D.d, D.bkv, D.Tn, D.N_valid);
+    k_pool<R, In><<<dim3(D.Tn, unsigned(D.U)), pt, 0, st>>>(k, pk, D.Nk, D.d, D.bkv, D.Tn, D.Nk_valid);
     check_launch("k_pool(k)", st);
   }
   const size_t smem = classify_smem_bytes(D, sizeof(R) == 8);
@@ -937,21 +943,20 @@ static bool classify_t(const Dims& D, const In* q, const In* k, const StateBufs&
   const long long rows = D.U * (long long)D.Tm;
   const unsigned wblocks = unsigned((rows + 7) / 8);
   if (SLAB_CLASSIFY_RANK && D.Tn <= 2048) {  // rank the raw scores (exact P_c only where needed)
-    const int Tp = (D.Tn + 31) / 32 * 32;
-    const size_t rsm = size_t(8) * Tp * (sizeof(R) + 1);
-    auto go = [&](auto kern) {
+    const int E = (D.Tn + 31) / 32;  // the row in registers up to T = 512 (EPL = E rounded up to 2^k)
+    auto go = [&](auto kern, int epl) {
+      const size_t rsm = size_t(8) * 32 * (epl > 0 ? epl : E) * (sizeof(R) + 1);  // as the kernel carves it
       SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(rsm)));
       launch_pdl(kern, wblocks, 256, rsm, st, (const R*)scores, rows, D.Tn, D.n1, D.n_neg, s.labels, s.crit_cnt,
                  s.crit_idx, s.marg_cnt, p_c, s.M0, int(m0_stride(D)), classify_exact_counter());
       check_launch("k_classify", st);
     };
-    const int E = Tp / 32;  // the row in registers up to T = 512
-    if (E <= 1) go(k_classify_rank<R, 1>);
-    else if (E <= 2) go(k_classify_rank<R, 2>);
-    else if (E <= 4) go(k_classify_rank<R, 4>);
-    else if (E <= 8) go(k_classify_rank<R, 8>);
-    else if (E <= 16) go(k_classify_rank<R, 16>);
-    else go(k_classify_rank<R, 0>);
+    if (E <= 1) go(k_classify_rank<R, 1>, 1);
+    else if (E <= 2) go(k_classify_rank<R, 2>, 2);
+    else if (E <= 4) go(k_classify_rank<R, 4>, 4);
+    else if (E <= 8) go(k_classify_rank<R, 8>, 8);
+    else if (E <= 16) go(k_classify_rank<R, 16>, 16);
+    else go(k_classify_rank<R, 0>, 0);
     return true;
   }
   auto warp_rows = [&](auto kern) {

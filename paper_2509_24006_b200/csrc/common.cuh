@@ -14,7 +14,9 @@ namespace slab {
 struct Dims {
   int64_t U;     // units = batch * heads
   int64_t B, H;  // batch, heads
-  int64_t N;     // sequence length (rows per unit in the kernels' buffers; padded if ragged)
+  int64_t N;     // query rows per unit in the kernels' buffers (sequence length; padded if ragged)
+  int64_t Nk;    // key / value rows per unit (== N unless a rectangular problem, sla_b200_problem.n_kv)
+  int64_t Nk_valid;  // valid key rows per unit (== Nk unless ragged)
   int64_t N_valid;  // rows per unit in the caller's tensors (== N unless SLA_B200_FLAG_RAGGED)
   bool bnhd;        // caller tensors are [B, N, H, d] (SLA_B200_FLAG_BNHD)
   bool staged;      // ragged or bnhd: kernels run on unit-major zero-padded workspace copies

@@ -173,13 +173,13 @@ __global__ void __launch_bounds__(256) k_rowmat(const In* __restrict__ x, const 
 // written by their producers (k_phi_kz, k_bwd_lin) with tc::store_split3, M0 is an exact 0/1
 // bf16 matrix, so products are exact and the f32 accumulation matches an f32 sum; consumers
 // add the three output columns back (tc::load_sum3).
-void aggregate_vec_tc(const Dims& Dm, const StateBufs& s, const WorkBufs& wb, bool trans, float* out3,
+void aggregate_vec_tc(const Dims& Dm, const StateBufs& s, const __nv_bfloat16* z3, bool trans, float* out3,
                       const char* name, cudaStream_t st) {
   const int d = Dm.d;
   const int Mo = trans ? Dm.Tn : Dm.Tm, Kd = trans ? Dm.Tm : Dm.Tn;
   GemmArgs a{};
   a.A = s.M0;
-  a.B = wb.z3b;
+  a.B = z3;
   a.C = out3;
   a.batch = int(Dm.U);
   a.M = Mo;
@@ -266,10 +266,10 @@ void fast_summaries(const Dims& Dm, const void* k, const void* v, const WorkBufs
   const int d = Dm.d;
   if (d == 128)
     launch_pdl(k_phi_kz<128>, dim3(Dm.Tn, unsigned(Dm.U)), 256, 0, st,
-        static_cast<const __nv_bfloat16*>(k), wb.kfb, wb.z3b, Dm.N, Dm.Tn, Dm.phi, Dm.N_valid);
+        static_cast<const __nv_bfloat16*>(k), wb.kfb, wb.z3b, Dm.Nk, Dm.Tn, Dm.phi, Dm.Nk_valid);
   else
     launch_pdl(k_phi_kz<64>, dim3(Dm.Tn, unsigned(Dm.U)), 256, 0, st,
-        static_cast<const __nv_bfloat16*>(k), wb.kfb, wb.z3b, Dm.N, Dm.Tn, Dm.phi, Dm.N_valid);
+        static_cast<const __nv_bfloat16*>(k), wb.kfb, wb.z3b, Dm.Nk, Dm.Tn, Dm.phi, Dm.Nk_valid);
   check_launch("k_phi_kz", st);
   // h_j = phi(K_j)^T V_j: batch = every key block, M = N = d, K = 64 tokens
   GemmArgs g{};
@@ -317,7 +317,7 @@ void fast_aggregate(const Dims& Dm, const StateBufs& s, const WorkBufs& wb, bool
   a.c_batch = (long long)Dm.Tm * d * d;
   a.name = "gemm_aggregate";
   launch_gemm(a, st);
-  aggregate_vec_tc(Dm, s, wb, false, s.Z, "gemm_aggregate_z", st);  // s.Z: [U, Tm, 3d]
+  aggregate_vec_tc(Dm, s, wb.z3b, false, s.Z, "gemm_aggregate_z", st);  // s.Z: [U, Tm, 3d]
 }
 
 void fast_forward(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
@@ -328,37 +328,42 @@ void fast_forward(const Dims& Dm, const void* q, const void* k, const void* v, c
   launch_attn_fwd(Dm, q, k, v, w, o, o_s, o_l, lse, s, st);
 }
 
-void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
-                   const void* o_s, const void* o_l, const float* lse, const void* d_out,
-                   const void* d_out_l, void* dq, void* dk, void* dv, float* dw,
-                   const GradParts& parts, const StateBufs& s, const WorkBufs& wb, cudaStream_t st,
-                   const SideFork& side) {
+// dH_agg = M0^T dH and dZ_agg = M0^T dZ (A = M0 read M-major) from the row phase's dH_i / dZ_i
+static void launch_agg_t(const Dims& Dm, const StateBufs& s, const WorkBufs& wb, const __nv_bfloat16* gH,
+                         const __nv_bfloat16* z3, cudaStream_t as) {
   const int d = Dm.d;
-  auto launch_agg = [&](cudaStream_t as) {
-    // dH_agg = M0^T dH (A = M0 read M-major), dZ_agg
-    GemmArgs a{};
-    a.A = s.M0;
-    a.B = wb.hb;
-    a.C = wb.hab;
-    a.batch = int(Dm.U);
-    a.M = Dm.Tn;
-    a.N = d * d;
-    a.K = Dm.Tm;
-    a.a_mn = true;
-    a.b_mn = true;
-    a.out_f32 = false;
-    a.lda = m0_stride(Dm);
-    a.ldb = (long long)d * d;
-    a.ldc = (long long)d * d;
-    a.a_batch = (long long)Dm.Tm * m0_stride(Dm);
-    a.b_batch = (long long)Dm.Tm * d * d;
-    a.c_batch = (long long)Dm.Tn * d * d;
-    a.name = "gemm_aggregate_t";
-    launch_gemm(a, as);
-    aggregate_vec_tc(Dm, s, wb, true, wb.gZa, "gemm_aggregate_dz", as);  // gZa: [U, Tn, 3d]
-  };
-  // independent cotangents: the linear kernel multiplies the given dO^l by an identity W (exact)
-  // and D^s = <dO^s, O^s> comes from its own row-dot kernel
+  GemmArgs a{};
+  a.A = s.M0;
+  a.B = gH;
+  a.C = wb.hab;
+  a.batch = int(Dm.U);
+  a.M = Dm.Tn;
+  a.N = d * d;
+  a.K = Dm.Tm;
+  a.a_mn = true;
+  a.b_mn = true;
+  a.out_f32 = false;
+  a.lda = m0_stride(Dm);
+  a.ldb = (long long)d * d;
+  a.ldc = (long long)d * d;
+  a.a_batch = (long long)Dm.Tm * m0_stride(Dm);
+  a.b_batch = (long long)Dm.Tm * d * d;
+  a.c_batch = (long long)Dm.Tn * d * d;
+  a.name = "gemm_aggregate_t";
+  launch_gemm(a, as);
+  aggregate_vec_tc(Dm, s, z3, true, wb.gZa, "gemm_aggregate_dz", as);  // gZa: [U, Tn, 3d]
+}
+
+// row phase (backward.cpp:46-120): the linear branch (dH_i, dZ_i, D^s, dQ^phi) and the sparse dQ
+// with dq_total.  dH_i -> gH [U, Tm, d, d], dZ_i parts -> z3 [U, Tm, 3d], D^s -> Ds [U, N].
+// Independent cotangents: the linear kernel multiplies the given dO^l by an identity W (exact)
+// and D^s = <dO^s, O^s> comes from its own row-dot kernel.
+static void backward_rows_phase(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
+                                const void* o_s, const void* o_l, const float* lse, const void* d_out,
+                                const void* d_out_l, void* dq, const GradParts& parts, const StateBufs& s,
+                                const WorkBufs& wb, __nv_bfloat16* gH, __nv_bfloat16* z3, float* Ds,
+                                cudaStream_t st) {
+  const int d = Dm.d;
   const bool split = d_out_l != nullptr;
   const void* lin_w = w;
   const void* lin_do = d_out;
@@ -366,10 +371,19 @@ void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, 
     const long long total = Dm.H * (long long)d * d;
     k_fill_identity<<<unsigned((total + 255) / 256), 256, 0, st>>>(wb.wid, total, d);
     check_launch("k_fill_identity", st);
-    launch_rowdot(Dm, d_out, o_s, wb.Ds, st);
+    launch_rowdot(Dm, d_out, o_s, Ds, st);
     lin_w = wb.wid;
     lin_do = d_out_l;
   }
+  launch_bwd_lin(Dm, q, lin_w, o_s, o_l, lin_do, s, gH, z3, Ds, wb.dqphi, split, st);
+  launch_bwd_rows(Dm, q, k, v, lse, d_out, dq, s, Ds, wb.dqphi, parts.dq, parts.dq_feat, st);
+}
+
+void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
+                   const void* o_s, const void* o_l, const float* lse, const void* d_out,
+                   const void* d_out_l, void* dq, void* dk, void* dv, float* dw,
+                   const GradParts& parts, const StateBufs& s, const WorkBufs& wb, cudaStream_t st,
+                   const SideFork& side) {
   // the column lists (labels only) build on the side stream while k_bwd_lin, a latency-bound
   // kernel with registers and threads to spare on every SM, runs; joined before the columns pass.
   // dW needs only O^l and dO: it fills SMs beside the row / column passes.
@@ -385,19 +399,33 @@ void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, 
   } else {
     launch_build_csc(Dm, s, st);
   }
-  // row phase: the linear branch (dH_i reusing the forward's h scratch, dZ_i, D^s, dQ^phi),
-  // then the sparse dQ over critical pairs with dq_total = J_phi^T dQ^phi + dQ
-  launch_bwd_lin(Dm, q, lin_w, o_s, o_l, lin_do, s, wb.hb, wb.z3b, wb.Ds, wb.dqphi, split, st);
-  launch_bwd_rows(Dm, q, k, v, lse, d_out, dq, s, wb.Ds, wb.dqphi, parts.dq, parts.dq_feat, st);
-  // dH_agg = M0^T dH and dZ_agg need only k_bwd_lin's dH / dZ (measured: on a side stream beside
-  // the rows pass 2.81 ms per step against 2.73-2.78 here -- rows loses SMs, cols waits)
-  launch_agg(st);
+  backward_rows_phase(Dm, q, k, v, w, o_s, o_l, lse, d_out, d_out_l, dq, parts, s, wb, wb.hb, wb.z3b, wb.Ds, st);
+  // dH_agg and dZ_agg need only k_bwd_lin's dH / dZ (measured: on a side stream beside the rows
+  // pass 2.81 ms per step against 2.73-2.78 here -- rows loses SMs, cols waits)
+  launch_agg_t(Dm, s, wb, wb.hb, wb.z3b, st);
   // columns pass: dk_total, dv
   if (side.s) SLAB_CUDA(cudaStreamWaitEvent(st, side.join, 0));
   launch_bwd_cols(Dm, q, k, v, lse, d_out, dk, dv, s, wb.hab, wb.gZa, wb.Ds, parts.dk, parts.dk_feat, st);
   if (!side.s && dw) launch_dw_fast(Dm, o_l, d_out, dw, wb, st);
   guard.release();
   if (side.s) SLAB_CUDA(cudaStreamWaitEvent(st, side.join2, 0));
+}
+
+void fast_backward_rows(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
+                        const void* o_s, const void* o_l, const float* lse, const void* d_out,
+                        const void* d_out_l, void* dq, float* dw, const StateBufs& s, const WorkBufs& wb,
+                        __nv_bfloat16* gH, __nv_bfloat16* z3, float* Ds, cudaStream_t st) {
+  backward_rows_phase(Dm, q, k, v, w, o_s, o_l, lse, d_out, d_out_l, dq, GradParts{}, s, wb, gH, z3, Ds, st);
+  if (dw) launch_dw_fast(Dm, o_l, d_out, dw, wb, st);
+}
+
+void fast_backward_cols(const Dims& Dm, const void* q, const void* k, const void* v, const float* lse,
+                        const void* d_out, const float* Ds, const __nv_bfloat16* gH, const __nv_bfloat16* z3,
+                        void* dk, void* dv, const StateBufs& s, const WorkBufs& wb, cudaStream_t st) {
+  launch_build_m0(Dm, s, st);
+  launch_build_csc(Dm, s, st);
+  launch_agg_t(Dm, s, wb, gH, z3, st);
+  launch_bwd_cols(Dm, q, k, v, lse, d_out, dk, dv, s, wb.hab, wb.gZa, Ds, nullptr, nullptr, st);
 }
 
 }  // namespace slab

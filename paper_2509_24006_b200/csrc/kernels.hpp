@@ -118,5 +118,15 @@ void fast_backward(const Dims& D, const void* q, const void* k, const void* v, c
                    const SideFork& side);
 void launch_dw_fast(const Dims& Dm, const void* o_l, const void* d_out, float* dw, const WorkBufs& wb,
                     cudaStream_t st);
+// the two phases of fast_backward on their own, for partitioned execution (sla_b200_backward_rows /
+// _cols): rows writes dH_i, dZ_i parts and D^s to caller buffers; cols takes them for every query
+// row (and the state's labels) and produces dK / dV of its key blocks
+void fast_backward_rows(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
+                        const void* o_s, const void* o_l, const float* lse, const void* d_out,
+                        const void* d_out_l, void* dq, float* dw, const StateBufs& s, const WorkBufs& wb,
+                        __nv_bfloat16* gH, __nv_bfloat16* z3, float* Ds, cudaStream_t st);
+void fast_backward_cols(const Dims& Dm, const void* q, const void* k, const void* v, const float* lse,
+                        const void* d_out, const float* Ds, const __nv_bfloat16* gH, const __nv_bfloat16* z3,
+                        void* dk, void* dv, const StateBufs& s, const WorkBufs& wb, cudaStream_t st);
 
 }  // namespace slab

@@ -151,3 +151,126 @@ class ShardedStep:
         from .shard import gather_units
 
         return gather_units(self.compute.outputs()[name].contiguous(), self.shard, self.n_units, group=self.group)
+
+
+# ---------------------------------------------------------------------------------------------
+# Finer than a (batch, head) unit: one head split over ranks (SURVEY.md 8(e) "sub-head split",
+# 8(f) item 4 "sequence-sharded SLA").  Block rows and block columns of a unit are independent
+# (backward.cpp:68 row phase, :142 column phase), so rank r owns a range of query blocks R_r for
+# the forward and the row phase, and a range of key blocks C_r for the column phase.  The phases
+# exchange only row summaries: D^s, lse, dH_i, dZ_i and the label grid of every row (the column
+# phase of C_r needs them for all rows), and the per-rank dW partials are summed.
+#   mode "subhead":  Q, K, V, dO replicated on every rank (C2 / C3 over 8 GPUs: 12 heads x 8 ranges)
+#   mode "sequence": rank r holds only its token slice of Q, K, V, dO (context parallel): K and V
+#                    are all-gathered for the forward / row phase, Q and dO for the column phase
+# Every exchange is a rank-ordered concatenation along rows (`Exchange.gather_rows`) or a sum.
+# ---------------------------------------------------------------------------------------------
+class Exchange:
+    """Collectives of the partitioned head over torch.distributed (NCCL on GPUs, gloo on CPU)."""
+
+    def __init__(self, world: int, rank: int, group=None):
+        self.world, self.rank, self.group = world, rank, group
+
+    def gather_rows(self, x: torch.Tensor, counts: List[int]) -> torch.Tensor:
+        """Concatenate every rank's x (x.shape[0] == counts[rank]) along dim 0 in rank order."""
+        if self.world == 1:
+            return x
+        dev = x.device
+        if x.is_cuda and dist.get_backend(self.group) == "gloo":  # gloo moves host tensors
+            return self.gather_rows(x.cpu(), counts).to(dev)
+        big = max(counts)
+        pad = torch.zeros((big,) + tuple(x.shape[1:]), dtype=x.dtype, device=x.device)
+        pad[: x.shape[0]] = x
+        bufs = [torch.empty_like(pad) for _ in range(self.world)]
+        dist.all_gather(bufs, pad, group=self.group)
+        return torch.cat([b[:c] for b, c in zip(bufs, counts)], 0)
+
+    def sum(self, x: torch.Tensor) -> torch.Tensor:
+        if self.world > 1:
+            if x.is_cuda and dist.get_backend(self.group) == "gloo":
+                y = x.cpu()
+                dist.all_reduce(y, group=self.group)
+                x.copy_(y)
+            else:
+                dist.all_reduce(x, group=self.group)
+        return x
+
+
+def block_ranges(t: int, world: int) -> List[range]:
+    """Contiguous balanced block ranges of a T-block axis, one per rank."""
+    return [partition_units(t, world, r).units for r in range(world)]
+
+
+class HeadPartition:
+    """One rank's part of one head's fwd + bwd: query blocks R_r, key blocks C_r (64-row blocks).
+
+    The compute runs through two rectangular views of the library (sla_b200_problem.n_kv):
+    `fwd`: this rank's query rows against all keys; `cols`: all query rows against this rank's
+    keys.  Use `forward`, `backward_rows`, `exchange`, `backward_cols` in that order on every rank,
+    or `step` with an Exchange."""
+
+    def __init__(self, n: int, d: int, cfg, world: int, rank: int, device, block: int = 64):
+        from .sla import SLA
+
+        self.n, self.d, self.world, self.rank = n, d, world, rank
+        t = n // block
+        self.q_blocks = block_ranges(t, world)
+        self.k_blocks = block_ranges(t, world)
+        self.rows = [len(r) * block for r in self.q_blocks]
+        self.krows = [len(r) * block for r in self.k_blocks]
+        R, Cc = self.q_blocks[rank], self.k_blocks[rank]
+        self.r0, self.r1 = R.start * block, R.stop * block
+        self.c0, self.c1 = Cc.start * block, Cc.stop * block
+        self.cfg = cfg
+        self.fwd_op = SLA(1, 1, self.r1 - self.r0, d, block, block, cfg, torch.bfloat16, device, n_kv=n) \
+            if self.r1 > self.r0 else None
+        self.cols_op = SLA(1, 1, n, d, block, block, cfg, torch.bfloat16, device, n_kv=self.c1 - self.c0) \
+            if self.c1 > self.c0 else None
+
+    def forward(self, q_rows, k, v, w):
+        """q_rows [1, 1, rows_r, d]; k, v all keys [1, 1, N, d]; w [1, d, d]."""
+        self.st = self.fwd_op.forward(q_rows, k, v, w)
+        return self.st
+
+    def backward_rows(self, q_rows, k, v, w, do_rows, d_out_linear=None):
+        dq, dw, ds, dh, dz = self.fwd_op.backward_rows(self.st, q_rows, k, v, w, do_rows, d_out_linear)
+        self.part = {"ds": ds[0], "lse": self.st.lse.reshape(-1), "dh": dh[0], "dz": dz[0],
+                     "labels": self.st.labels.reshape(self.st.labels.shape[-2], -1)}
+        return dq, dw
+
+    def exchange(self, ex: "Exchange") -> Dict[str, torch.Tensor]:
+        """All rows' summaries, rank-ordered: D^s and lse by rows, dH / dZ / labels by block rows."""
+        br = [len(r) for r in self.q_blocks]
+        p = self.part
+        self.full = {"ds": ex.gather_rows(p["ds"], self.rows), "lse": ex.gather_rows(p["lse"], self.rows),
+                     "dh": ex.gather_rows(p["dh"], br), "dz": ex.gather_rows(p["dz"], br),
+                     "labels": ex.gather_rows(p["labels"], br)}
+        return self.full
+
+    def backward_cols(self, q, k_own, v_own, do, full=None):
+        """q, do: all query rows [1, 1, N, d]; k_own, v_own: this rank's keys [1, 1, c1 - c0, d]."""
+        f = full or self.full
+        t0, t1 = self.k_blocks[self.rank].start, self.k_blocks[self.rank].stop
+        labels = f["labels"][:, t0:t1].contiguous()
+        return self.cols_op.backward_cols(q, k_own, v_own, f["lse"].reshape(1, 1, -1), do, f["ds"].reshape(1, -1),
+                                          f["dh"].unsqueeze(0), f["dz"].unsqueeze(0), labels.unsqueeze(0))
+
+    def step(self, ex: "Exchange", q, k, v, w, do, mode: str = "subhead"):
+        """fwd + bwd of this rank's part.  mode "subhead": q, k, v, do are the full head on every
+        rank; "sequence": this rank's token slice (rows r0:r1 == keys c0:c1).  Returns
+        (o_rows, dq_rows, dk_own, dv_own, dw summed over the ranks)."""
+        if mode == "sequence":
+            q_rows, do_rows, k_own, v_own = q, do, k, v
+            k = ex.gather_rows(k_own[0, 0], self.krows).reshape(1, 1, self.n, self.d)
+            v = ex.gather_rows(v_own[0, 0], self.krows).reshape(1, 1, self.n, self.d)
+        else:
+            q_rows, do_rows = q[:, :, self.r0:self.r1], do[:, :, self.r0:self.r1]
+            k_own, v_own = k[:, :, self.c0:self.c1], v[:, :, self.c0:self.c1]
+        st = self.forward(q_rows.contiguous(), k, v, w)
+        dq, dw = self.backward_rows(q_rows.contiguous(), k, v, w, do_rows.contiguous())
+        self.exchange(ex)
+        if mode == "sequence":
+            q = ex.gather_rows(q_rows[0, 0], self.rows).reshape(1, 1, self.n, self.d)
+            do = ex.gather_rows(do_rows[0, 0], self.rows).reshape(1, 1, self.n, self.d)
+        dk, dv = self.backward_cols(q, k_own.contiguous(), v_own.contiguous(), do)
+        return st.o, dq, dk, dv, ex.sum(dw)

@@ -55,11 +55,12 @@ class BlockLayout:
     t_n: int = 0
 
 
-def _problem(batch, heads, n, d, b_q, b_kv, cfg: SlaConfig, dtype) -> L.Problem:
+def _problem(batch, heads, n, d, b_q, b_kv, cfg: SlaConfig, dtype, n_kv: int = 0) -> L.Problem:
     if cfg.phi not in L.PHI:
         raise ValueError(f"unknown feature map: {cfg.phi}")
     p = L.Problem()
     p.batch, p.heads, p.n, p.d, p.b_q, p.b_kv = batch, heads, n, d, b_q, b_kv
+    p.n_kv = n_kv
     p.k_h, p.k_l = float(cfg.k_h), float(cfg.k_l)
     p.phi = L.PHI[cfg.phi]
     if dtype == torch.bfloat16:
@@ -120,13 +121,16 @@ class SLA:
     """One SLA operator instance for a fixed problem shape: owns its state/workspace."""
 
     def __init__(self, batch: int, heads: int, n: int, d: int, b_q: int = 64, b_kv: int = 64,
-                 cfg: Optional[SlaConfig] = None, dtype=torch.bfloat16, device="cuda"):
+                 cfg: Optional[SlaConfig] = None, dtype=torch.bfloat16, device="cuda", n_kv: int = 0):
+        """n_kv (one unit only): a rectangular view -- n query rows against n_kv key rows, the
+        building block of partitioned execution (runner.py)."""
         self.cfg = cfg or SlaConfig()
         self.batch, self.heads, self.n, self.d = batch, heads, n, d
         self.b_q, self.b_kv = b_q, b_kv
         self.dtype = dtype
         self.device = torch.device(device)
-        self.p = _problem(batch, heads, n, d, b_q, b_kv, self.cfg, dtype)
+        self.n_kv = n_kv or n
+        self.p = _problem(batch, heads, n, d, b_q, b_kv, self.cfg, dtype, n_kv if n_kv != n else 0)
         sb, wb = C.c_size_t(), C.c_size_t()
         L.check(L.lib().sla_b200_sizes(C.byref(self.p), C.byref(sb), C.byref(wb)))
         self.state_bytes, self.workspace_bytes = sb.value, wb.value
@@ -156,6 +160,11 @@ class SLA:
         if self.cfg.bnhd:
             return (self.batch, self.n, self.heads, self.d)
         return (self.batch, self.heads, self.n, self.d)
+
+    def _kv_shape(self):
+        if self.cfg.bnhd:
+            return (self.batch, self.n_kv, self.heads, self.d)
+        return (self.batch, self.heads, self.n_kv, self.d)
 
     def _check(self, name, t, shape=None, dtype=None):
         shape = shape or self._unit_shape()
@@ -187,7 +196,7 @@ class SLA:
     def classify(self, q, k, weights: bool = False):
         """predict_compressed_weights + classify_mask (mask.cpp:57-119)."""
         self._check("Q", q)
-        self._check("K", k)
+        self._check("K", k, self._kv_shape())
         state = self.new_state()
         labels = torch.empty((self.batch, self.heads, self.t_m, self.t_n), dtype=torch.int8,
                              device=self.device)
@@ -200,8 +209,9 @@ class SLA:
 
     def forward(self, q, k, v, w=None, mask=None, state=None, out=None) -> SlaForwardState:
         """sla_forward (mask None) / sla_forward_with_mask, fused with combine_outputs."""
-        for nm, t in (("Q", q), ("K", k), ("V", v)):
-            self._check(nm, t)
+        self._check("Q", q)
+        self._check("K", k, self._kv_shape())
+        self._check("V", v, self._kv_shape())
         w = self._w(w)
         if mask is not None:
             mask = mask.to(device=self.device, dtype=torch.int8).contiguous()
@@ -262,6 +272,42 @@ class SLA:
                     _stream(self.device))
         L.check(rc)
         return SlaGradients(dq, dk, dv, dw, **extra)
+
+    # -- the backward in two phases, for partitioned execution (runner.py) ---------------
+    def backward_rows(self, st: SlaForwardState, q, k, v, w, d_out, d_out_linear=None, want_dw: bool = True):
+        """Row phase of this view's query rows (sla_b200_backward_rows): returns dq_total, the dW
+        partial over these rows (or None), and the row summaries the column phase of every key
+        range needs: D^s [N], dH_i [T_m, d, d] (bf16), dZ_i as three bf16 parts [T_m, 3 d]."""
+        if d_out_linear is None:
+            w = self._w(w)
+        dev, d = self.device, self.d
+        dq = torch.empty(self._unit_shape(), dtype=self.dtype, device=dev)
+        dw = torch.empty((self.heads, d, d), dtype=torch.float32, device=dev) if want_dw else None
+        U = self.batch * self.heads
+        ds = torch.empty((U, self.n), dtype=torch.float32, device=dev)
+        dh = torch.empty((U, self.t_m, d, d), dtype=torch.bfloat16, device=dev)
+        dz = torch.empty((U, self.t_m, 3 * d), dtype=torch.bfloat16, device=dev)
+        with torch.cuda.device(dev):
+            L.check(L.lib().sla_b200_backward_rows(
+                C.byref(self.p), _ptr(q), _ptr(k), _ptr(v), _ptr(w), _ptr(st.o_s), _ptr(st.o_l), _ptr(st.lse),
+                _ptr(d_out), _ptr(d_out_linear), _ptr(dq), _ptr(dw), _ptr(ds), _ptr(dh), _ptr(dz), _ptr(st.state),
+                _ptr(self._workspace), _stream(dev)))
+        return dq, dw, ds, dh, dz
+
+    def backward_cols(self, q, k, v, lse, d_out, ds, dh, dz, labels):
+        """Column phase of this view's key blocks against every query row (sla_b200_backward_cols):
+        q, d_out, lse, ds, dh, dz cover all query rows; labels [T_m, T_n] are all rows' labels
+        restricted to these key blocks.  Returns dk_total, dv of these keys."""
+        self._check("K", k, self._kv_shape())
+        dk = torch.empty(self._kv_shape(), dtype=self.dtype, device=self.device)
+        dv = torch.empty_like(dk)
+        labels = labels.to(device=self.device, dtype=torch.int8).contiguous()
+        state = self.new_state()
+        with torch.cuda.device(self.device):
+            L.check(L.lib().sla_b200_backward_cols(
+                C.byref(self.p), _ptr(q), _ptr(k), _ptr(v), _ptr(lse), _ptr(d_out), _ptr(ds), _ptr(dh), _ptr(dz),
+                _ptr(labels), _ptr(dk), _ptr(dv), _ptr(state), _ptr(self._workspace), _stream(self.device)))
+        return dk, dv
 
     def combine(self, st: SlaForwardState, w) -> torch.Tensor:
         """combine_outputs (forward.cpp:187-195) on the device: O = O^s + O^l W."""

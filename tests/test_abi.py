@@ -24,7 +24,7 @@ def test_library_exports_every_declared_symbol():
     assert len(names) >= 10
     for nm in names:
         assert hasattr(lib, nm), nm
-    assert lib.sla_b200_abi_version() == 1
+    assert lib.sla_b200_abi_version() == 2
 
 
 def _p(**kw):

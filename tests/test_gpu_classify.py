@@ -72,8 +72,8 @@ def test_duplicated_key_blocks(distinct):
     assert (lab == O.dynamic_labels(q, k, b, b, 5.0, 10.0)).all()
 
 
-@pytest.mark.parametrize("t_n,b,d", [(16, 64, 64), (100, 16, 32), (512, 64, 128), (1182, 64, 128), (2048, 16, 32),
-                                     (2049, 16, 32)])
+@pytest.mark.parametrize("t_n,b,d", [(16, 64, 64), (65, 64, 64), (100, 16, 32), (300, 16, 32), (512, 64, 128),
+                                     (600, 16, 32), (1182, 64, 128), (2048, 16, 32), (2049, 16, 32)])
 def test_rank_kernel_matches_reference_across_t(t_n, b, d):
     rng = O.Rng(5000 + t_n)
     n = t_n * b
