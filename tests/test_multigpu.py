@@ -114,3 +114,42 @@ def test_gather_units_uneven():
     s = partition_units(3, 1, 0)
     x = torch.arange(6.0).view(3, 2)
     assert torch.equal(gather_units(x, s, 3), x)
+
+
+def _exchange_worker(rank, world, port, out_path):
+    from paper_2509_24006_b200.runner import Exchange, block_ranges
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        t = 13  # block rows of one head, split 7 / 6
+        ranges = block_ranges(t, world)
+        mine = ranges[rank]
+        counts = [len(r) for r in ranges]
+        ex = Exchange(world, rank)
+        rows = torch.arange(mine.start, mine.stop, dtype=torch.float64).view(-1, 1).repeat(1, 3)
+        full = ex.gather_rows(rows, counts)
+        total = ex.sum(torch.full((2, 2), float(rank + 1)))
+        torch.save({"full": full, "total": total}, f"{out_path}.{rank}")
+    finally:
+        dist.destroy_process_group()
+
+
+def test_partition_exchange_gathers_rank_ordered_rows(tmp_path):
+    """runner.Exchange (the collectives of the sub-head / sequence-sharded head): uneven
+    rank-ordered row gathers and the dW sum, world size 2 over gloo."""
+    out = str(tmp_path / "ex")
+    mp.spawn(_exchange_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    for r in range(2):
+        res = torch.load(f"{out}.{r}")
+        assert torch.equal(res["full"][:, 0], torch.arange(13, dtype=torch.float64))
+        assert torch.equal(res["total"], torch.full((2, 2), 3.0))
+
+
+def test_block_ranges_cover_the_axis():
+    from paper_2509_24006_b200.runner import block_ranges
+
+    for t, w in ((512, 8), (13, 2), (1182, 8), (3, 4)):
+        rs = block_ranges(t, w)
+        assert [i for r in rs for i in r] == list(range(t))
