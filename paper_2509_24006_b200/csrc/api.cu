@@ -361,12 +361,19 @@ int sla_b200_forward(const sla_b200_problem* p, const void* q, const void* k, co
       SLAB_CUDA(cudaEventRecord(ss->join, ss->s));
     }
     const bool m0_ready = classify_into_state(p, D, q, k, mask_in, nullptr, s, wb, st);
-    guard.release();
-    if (fork) SLAB_CUDA(cudaStreamWaitEvent(st, ss->join, 0));
-    if (fast)
-      fast_forward(D, q, k, v, w, o, o_s, o_l, lse, s, wb, m0_ready, fork, st);
-    else
+    if (fast) {
+      SideFork side;
+      if (fork) {
+        side.s = ss->s;
+        side.join = ss->join;
+        side.mid = ss->mid;
+        side.join3 = ss->join3;
+      }
+      fast_forward(D, q, k, v, w, o, o_s, o_l, lse, s, wb, m0_ready, side, st);
+    } else {
       generic_forward(D, p->dtype, q, k, v, w, o, o_s, o_l, lse, s, wb, st);
+    }
+    guard.release();
     if (check) {  // forward.cpp:164-170
       const long long per = D.N * D.d;
       for (const void* out : {static_cast<const void*>(o_s), static_cast<const void*>(o_l)}) {

@@ -200,6 +200,10 @@ void aggregate_vec_tc(const Dims& Dm, const StateBufs& s, const __nv_bfloat16* z
 
 }  // namespace
 
+#ifndef SLAB_AGG_Z_SIDE
+#define SLAB_AGG_Z_SIDE 0  // Z / dZ aggregation on the side stream beside H / dH_agg: measured no gain (2.764-2.797 vs 2.773-2.776 ms)
+#endif
+
 bool fast_supported(const Dims& D, int dtype) {
   return dtype == 0 && D.bq == 64 && D.bkv == 64 && (D.d == 64 || D.d == 128);
 }
@@ -293,11 +297,9 @@ void fast_summaries(const Dims& Dm, const void* k, const void* v, const WorkBufs
   launch_gemm(g, st);
 }
 
-// H = M0 h, Z = M0 z (needs the mask); M0 itself unless the warp classifier wrote it
-void fast_aggregate(const Dims& Dm, const StateBufs& s, const WorkBufs& wb, bool m0_ready, cudaStream_t st) {
+// H = M0 . h per unit: M = Tm, N = d*d, K = Tn
+void fast_aggregate_h(const Dims& Dm, const StateBufs& s, const WorkBufs& wb, cudaStream_t st) {
   const int d = Dm.d;
-  // H = M0 . h per unit: M = Tm, N = d*d, K = Tn
-  if (!m0_ready) launch_build_m0(Dm, s, st);  // the warp classifier writes M0 itself
   GemmArgs a{};
   a.A = s.M0;
   a.B = wb.hb;
@@ -317,14 +319,34 @@ void fast_aggregate(const Dims& Dm, const StateBufs& s, const WorkBufs& wb, bool
   a.c_batch = (long long)Dm.Tm * d * d;
   a.name = "gemm_aggregate";
   launch_gemm(a, st);
+}
+
+// H = M0 h, Z = M0 z (needs the mask); M0 itself unless the classifier wrote it
+void fast_aggregate(const Dims& Dm, const StateBufs& s, const WorkBufs& wb, bool m0_ready, cudaStream_t st) {
+  if (!m0_ready) launch_build_m0(Dm, s, st);  // the classifier writes M0 itself
+  fast_aggregate_h(Dm, s, wb, st);
   aggregate_vec_tc(Dm, s, wb.z3b, false, s.Z, "gemm_aggregate_z", st);  // s.Z: [U, Tm, 3d]
 }
 
 void fast_forward(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
                   void* o, void* o_s, void* o_l, float* lse, const StateBufs& s,
-                  const WorkBufs& wb, bool m0_ready, bool summaries_done, cudaStream_t st) {
-  if (!summaries_done) fast_summaries(Dm, k, v, wb, st);
-  fast_aggregate(Dm, s, wb, m0_ready, st);
+                  const WorkBufs& wb, bool m0_ready, const SideFork& side, cudaStream_t st) {
+  if (!side.s) {
+    fast_summaries(Dm, k, v, wb, st);
+    fast_aggregate(Dm, s, wb, m0_ready, st);
+  } else if (!SLAB_AGG_Z_SIDE) {
+    SLAB_CUDA(cudaStreamWaitEvent(st, side.join, 0));
+    fast_aggregate(Dm, s, wb, m0_ready, st);
+  } else {  // Z = M0 z (a thin GEMM, N = 3d) on the side stream beside H = M0 h
+    if (!m0_ready) launch_build_m0(Dm, s, st);
+    SLAB_CUDA(cudaEventRecord(side.mid, st));
+    SLAB_CUDA(cudaStreamWaitEvent(side.s, side.mid, 0));  // M0 (the side has the z parts)
+    aggregate_vec_tc(Dm, s, wb.z3b, false, s.Z, "gemm_aggregate_z", side.s);
+    SLAB_CUDA(cudaEventRecord(side.join3, side.s));
+    SLAB_CUDA(cudaStreamWaitEvent(st, side.join, 0));  // h (summaries)
+    fast_aggregate_h(Dm, s, wb, st);
+    SLAB_CUDA(cudaStreamWaitEvent(st, side.join3, 0));
+  }
   launch_attn_fwd(Dm, q, k, v, w, o, o_s, o_l, lse, s, st);
 }
 
@@ -351,7 +373,7 @@ static void launch_agg_t(const Dims& Dm, const StateBufs& s, const WorkBufs& wb,
   a.c_batch = (long long)Dm.Tn * d * d;
   a.name = "gemm_aggregate_t";
   launch_gemm(a, as);
-  aggregate_vec_tc(Dm, s, z3, true, wb.gZa, "gemm_aggregate_dz", as);  // gZa: [U, Tn, 3d]
+  if (z3) aggregate_vec_tc(Dm, s, z3, true, wb.gZa, "gemm_aggregate_dz", as);  // gZa: [U, Tn, 3d]
 }
 
 // row phase (backward.cpp:46-120): the linear branch (dH_i, dZ_i, D^s, dQ^phi) and the sparse dQ
@@ -400,9 +422,19 @@ void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, 
     launch_build_csc(Dm, s, st);
   }
   backward_rows_phase(Dm, q, k, v, w, o_s, o_l, lse, d_out, d_out_l, dq, parts, s, wb, wb.hb, wb.z3b, wb.Ds, st);
-  // dH_agg and dZ_agg need only k_bwd_lin's dH / dZ (measured: on a side stream beside the rows
-  // pass 2.81 ms per step against 2.73-2.78 here -- rows loses SMs, cols waits)
-  launch_agg_t(Dm, s, wb, wb.hb, wb.z3b, st);
+  // dH_agg and dZ_agg need only k_bwd_lin's dH / dZ (measured: dH_agg on a side stream beside the
+  // rows pass 2.81 ms per step against 2.73-2.78 here -- rows loses SMs, cols waits); the thin
+  // dZ_agg GEMM runs on the side stream beside dH_agg
+  if (side.s && SLAB_AGG_Z_SIDE) {
+    SLAB_CUDA(cudaEventRecord(side.mid, st));
+    SLAB_CUDA(cudaStreamWaitEvent(side.s, side.mid, 0));
+    aggregate_vec_tc(Dm, s, wb.z3b, true, wb.gZa, "gemm_aggregate_dz", side.s);
+    SLAB_CUDA(cudaEventRecord(side.join3, side.s));
+    launch_agg_t(Dm, s, wb, wb.hb, nullptr, st);
+    SLAB_CUDA(cudaStreamWaitEvent(st, side.join3, 0));
+  } else {
+    launch_agg_t(Dm, s, wb, wb.hb, wb.z3b, st);
+  }
   // columns pass: dk_total, dv
   if (side.s) SLAB_CUDA(cudaStreamWaitEvent(st, side.join, 0));
   launch_bwd_cols(Dm, q, k, v, lse, d_out, dk, dv, s, wb.hab, wb.gZa, wb.Ds, parts.dk, parts.dk_feat, st);

@@ -61,6 +61,7 @@ void launch_attn_fwd(const Dims& Dm, const void* q, const void* k, const void* v
                      void* o, void* o_s, void* o_l, float* lse, const StateBufs& s, cudaStream_t st);
 void fast_summaries(const Dims& Dm, const void* k, const void* v, const WorkBufs& wb, cudaStream_t st);
 void fast_aggregate(const Dims& Dm, const StateBufs& s, const WorkBufs& wb, bool m0_ready, cudaStream_t st);
+void fast_aggregate_h(const Dims& Dm, const StateBufs& s, const WorkBufs& wb, cudaStream_t st);
 void launch_bwd_lin(const Dims& Dm, const void* q, const void* w, const void* o_s, const void* o_l,
                     const void* d_out, const StateBufs& s, __nv_bfloat16* gH, __nv_bfloat16* z3, float* Ds,
                     __nv_bfloat16* dqphi, bool ds_external, cudaStream_t st);
@@ -72,15 +73,17 @@ void launch_bwd_cols(const Dims& Dm, const void* q, const void* k, const void* v
                      const __nv_bfloat16* Ha, const float* gZa, const float* Ds, float* dk_part,
                      float* dkf_part, cudaStream_t st);
 bool fast_supported(const Dims& D, int dtype);
-void fast_forward(const Dims& D, const void* q, const void* k, const void* v, const void* w,
-                  void* o, void* o_s, void* o_l, float* lse, const StateBufs& s,
-                  const WorkBufs& wb, bool m0_ready, bool summaries_done, cudaStream_t st);
 // A side stream with fork / join events: work that only depends on the call's inputs runs
 // there, concurrent with latency-bound kernels on the caller's stream (s == nullptr: none).
 struct SideFork {
   cudaStream_t s = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr, join2 = nullptr, mid = nullptr, join3 = nullptr;
 };
+// side.s set: the caller already queued the summaries on side.s (completion: side.join); the
+// Z aggregation then runs there beside the H aggregation.  Otherwise everything runs on st.
+void fast_forward(const Dims& D, const void* q, const void* k, const void* v, const void* w,
+                  void* o, void* o_s, void* o_l, float* lse, const StateBufs& s,
+                  const WorkBufs& wb, bool m0_ready, const SideFork& side, cudaStream_t st);
 // RAII join of a side-stream fork: if an exception leaves the region between the fork and its
 // join, the side stream's queued work is still joined into the caller's stream, so the caller
 // never reuses buffers that work reads or writes, and a graph capture never ends with an
