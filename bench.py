@@ -431,10 +431,17 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one process per GPU over NCCL; with more ranks than GPUs (a multi-rank smoke run on a
+    # one-GPU box) ranks share devices and the collectives go over gloo
+    shared = world > torch.cuda.device_count()
+    local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     B, H, N, d, b, k_h, k_l, phi = CONFIGS[args.config]
     Bg = global_batch(args.config, world)
     cfg = SlaConfig(k_h=k_h, k_l=k_l, phi=phi, ragged=N % b != 0)
@@ -486,10 +493,15 @@ def run_ours(args):
             nm, t, cnt = ln.rsplit(" ", 2)
             kernels[nm] = (float(t), int(cnt))
     ms = ms_clean
-    t = torch.tensor([ms], device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    coll_dev = torch.device("cpu") if shared else dev  # gloo reduces host tensors
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], device=coll_dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ms_max = max_over_ranks(ms)
     flops_unit = dense_equiv_flops(1, 1, N, d)
     value = flops_unit * runner.n_units / (ms_max * 1e-3) / 1e12
 
@@ -536,11 +548,13 @@ def run_ours(args):
     if rank == 0:
         out["clocks"] = cl
     # ---- validation gather (after the timed region): per-unit checksums to rank 0 over NCCL
-    sums = runner.gather_checksums(device=dev)
+    sums = runner.gather_checksums(device=coll_dev)
     if rank == 0 and sums is not None:
         s = sums.double().cpu()
         out["validation"] = {"units": int(s.shape[0]), "checksum_first_unit": [float(x) for x in s[0]],
                              "checksum_all": [float(x) for x in s.sum(0)]}
+        if s.shape[0] <= 64:  # per unit: sum and sum |x| of o, dq, dk, dv
+            out["validation"]["checksums"] = s.tolist()
     # ---- dense attention of the same shape (rank 0): torch SDPA and the repo's own kernels
     if not args.no_dense and rank == 0:
         nd = min(U, 12)
@@ -580,10 +594,7 @@ def run_ours(args):
             e2e_step()
         ev1.record(stream)
         torch.cuda.synchronize()
-        t = torch.tensor([ev0.elapsed_time(ev1) / args.steps], device=dev)
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
+        e2e_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
         out["e2e"] = {"value": flops_unit * ne * world / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOPS",
                       "ms_per_step": e2e_ms * U / ne, "h2d_bytes_per_step": hts.h2d_bytes() * U // ne,
                       "d2h_bytes_per_step": hts.d2h_bytes() * U // ne, "chunks": len(hts.ranges),

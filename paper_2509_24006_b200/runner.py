@@ -120,7 +120,12 @@ class ShardedStep:
             idx = torch.tensor([u % self.heads for u in self.units], dtype=torch.long, device=part.device)
             dw.index_add_(0, idx, part.float())
         if self.world > 1:
-            dist.all_reduce(dw, group=self.group)
+            if dw.is_cuda and dist.get_backend(self.group) == "gloo":  # gloo moves host tensors
+                host = dw.cpu()
+                dist.all_reduce(host, group=self.group)
+                dw.copy_(host)
+            else:
+                dist.all_reduce(dw, group=self.group)
         self.dw = dw
         return dw
 

@@ -49,6 +49,9 @@ def gather_units(local: torch.Tensor, shard: Shard, n_units: int, group=None) ->
     world = shard.world
     if world == 1:
         return local
+    if local.is_cuda and dist.get_backend(group) == "gloo":  # gloo moves host tensors
+        out = gather_units(local.cpu(), shard, n_units, group)
+        return None if out is None else out.to(local.device)
     biggest = -(-n_units // world)
     pad = torch.zeros((biggest,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
     pad[: local.shape[0]] = local
