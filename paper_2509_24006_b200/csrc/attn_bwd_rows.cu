@@ -12,6 +12,8 @@
 //   then dq_total = J_phi(q)^T dQ^phi + dQ (backward.cpp:211-214).
 //   K pairs and V pairs stream through separate rings (3 and 2 slots): V frees as soon as dP
 //   is done, so the tensor pipe keeps S/dP of the next pair queued behind dQ of this one.
+#include <algorithm>
+
 #include "bwd_common.cuh"
 
 #ifndef SLAB_ROWS_POLY
@@ -363,6 +365,9 @@ struct RowsLayout {
 // 0.678 ms.
 // softmax-gradient warps: 8 (32 query columns each per lane quarter) or 16 (16 columns each);
 // (16 warps, for latency hiding, measured slower: TMEM-load and barrier traffic grow with them)
+#ifndef SLAB_ROWS_PERSIST
+#define SLAB_ROWS_PERSIST 1  // one CTA per SM walking the query blocks (0: one CTA per block)
+#endif
 #ifndef SLAB_ROWS_CW
 #define SLAB_ROWS_CW 8  // measured: 8 warps 0.600 ms, 16 warps 0.613
 #endif
@@ -402,24 +407,11 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   static_assert(8 + 2 * (L::KS + L::VS) <= 18, "barrier slots");
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int i = blockIdx.x;
-  const long long u = blockIdx.y;
-  const long long urow = u * p.Tm + i;
-  const int cnt = p.crit_cnt[urow];
-  const int* list = p.crit_idx + urow * p.Tn;
-  const int np = (cnt + 1) >> 1;
-  const int row0 = int(u * p.N) + i * 64;
-  const bool dbg = blockIdx.x == SLAB_DBG_X && blockIdx.y == 6;
-  ts_mark(dbg && threadIdx.x == 0, 127);
-  cta_mark(threadIdx.x == 0, 0);
-  // the first pair's key blocks, loaded alongside cnt (not after it) so the first K / V pair
-  // can leave before the TMEM allocation and the block barrier
-  int l0 = 0, l1 = 0;
-  if (threadIdx.x == 0) {
-    l0 = list[0];
-    l1 = list[min(1, p.Tn - 1)];
-  }
-
+  // Persistent: CTA b takes the query blocks (work items) b, b + gridDim.x, ... of the [U, Tm]
+  // grid (every item has the same n1 critical blocks under a dynamic mask).  Ring slots, TMEM
+  // buffers and barrier phases run on G = the CTA's pairs so far (G0) + the item's pair t, so no
+  // barrier is re-initialised between items; the per-item barriers (qdo_full, dq_done) take the
+  // item count's parity.  With gridDim.x == items every CTA runs one item (the grid launch).
   if (warp == 0) {
     if (lane == 0) {
       tc::mbar_init(qdo_full, 1);
@@ -440,9 +432,37 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         tc::mbar_init(v_empty + s, 1);
       }
       tc::fence_barrier_init();
-      // Q_i / dO_i and pair 0 (K and V) now; the producer loops start at pair 1
       tc::tma_prefetch(&tmK);
       tc::tma_prefetch(&tmV);
+    }
+    __syncwarp();
+    tc::tmem_alloc<512>(tmem_slot);
+  }
+  tc::tc_fence_before();
+  __syncthreads();
+  tc::tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t tDQT = tmem, tB0 = tmem + 128, tB1 = tmem + 256;  // dQ^T (M = D); S^T|dP^T pairs
+  int G0 = 0;  // pairs this CTA processed before the current item (32-bit: cheap % and / by constants)
+  int nit = 0;       // items this CTA processed before the current one
+  for (long long item = blockIdx.x; item < p.items; item += gridDim.x, ++nit) {
+  const int i = int(item % p.Tm);
+  const long long u = item / p.Tm;
+  const long long urow = u * p.Tm + i;
+  const int cnt = p.crit_cnt[urow];
+  const int* list = p.crit_idx + urow * p.Tn;
+  const int np = (cnt + 1) >> 1;
+  const int row0 = int(u * p.N) + i * 64;
+  const int ip = nit & 1;  // parity of the per-item barriers
+  const bool dbg = i == SLAB_DBG_X && u == 6;
+  ts_mark(dbg && threadIdx.x == 0, 127);
+  cta_mark(threadIdx.x == 0, 0, item);
+  if (warp == 0) {
+    if (lane == 0) {
+      // Q_i / dO_i and pair 0 (K and V) now; the producer loops start at pair 1.  Pair 0's
+      // slots were released by the previous item's last MMAs (all complete: dq_done).
+      const int l0 = list[0], l1 = list[min(1, p.Tn - 1)];
+      const int k0s = G0 % L::KS, v0s = G0 % L::VS;
       tc::mbar_expect_tx(qdo_full, 2 * L::kT);
 #pragma unroll
       for (int c = 0; c < D / 64; ++c) {
@@ -453,36 +473,33 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         const int r1 = int(u * p.N) + l0 * 64, r2 = int(u * p.N) + (cnt > 1 ? l1 : l0) * 64;
         ts_mark(dbg, 0);
         ts_mark(dbg, 112);
-        tc::mbar_expect_tx(k_full, L::kP);
-        tc::mbar_expect_tx(v_full, L::kP);
+        tc::mbar_expect_tx(k_full + k0s, L::kP);
+        tc::mbar_expect_tx(v_full + v0s, L::kP);
+        uint8_t* dk0 = sK + k0s * L::kP;
+        uint8_t* dv0 = sV + v0s * L::kP;
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
-          tc::tma_load_3d(sK + c * 16384, &tmK, k_full, 64 * c, r1, 0);
-          tc::tma_load_3d(sK + c * 16384 + 8192, &tmK, k_full, 64 * c, r2, 0);
+          tc::tma_load_3d(dk0 + c * 16384, &tmK, k_full + k0s, 64 * c, r1, 0);
+          tc::tma_load_3d(dk0 + c * 16384 + 8192, &tmK, k_full + k0s, 64 * c, r2, 0);
         }
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
-          tc::tma_load_3d(sV + c * 16384, &tmV, v_full, 64 * c, r1, 0);
-          tc::tma_load_3d(sV + c * 16384 + 8192, &tmV, v_full, 64 * c, r2, 0);
+          tc::tma_load_3d(dv0 + c * 16384, &tmV, v_full + v0s, 64 * c, r1, 0);
+          tc::tma_load_3d(dv0 + c * 16384 + 8192, &tmV, v_full + v0s, 64 * c, r2, 0);
         }
       }
     }
     __syncwarp();
-    tc::tmem_alloc<512>(tmem_slot);
   }
-  tc::tc_fence_before();
-  __syncthreads();
-  tc::tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t tDQT = tmem, tB0 = tmem + 128, tB1 = tmem + 256;  // dQ^T (M = D); S^T|dP^T pairs
 
   if (warp == 0 || warp == kRowsVWarp) {
 #ifdef SLAB_TIMELINE
     if (dbg && warp == 0 && lane == 1) {  // observer: true K / V pair arrival times
       for (int t = 0; t < np && t < 16; ++t) {
-        tc::mbar_wait(k_full + t % L::KS, (t / L::KS) & 1);
+        const int G = G0 + t;
+        tc::mbar_wait(k_full + G % L::KS, (G / L::KS) & 1);
         g_bwd_ts[80 + t] = clock64();
-        tc::mbar_wait(v_full + t % L::VS, (t / L::VS) & 1);
+        tc::mbar_wait(v_full + G % L::VS, (G / L::VS) & 1);
         g_bwd_ts[96 + t] = clock64();
       }
     }
@@ -494,9 +511,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         // an odd tail repeats its block (finite data); the compute warps zero its dS rows
         const int r1 = int(u * p.N) + list[2 * t] * 64;
         const int r2 = int(u * p.N) + list[min(2 * t + 1, cnt - 1)] * 64;
-        const int ks = t % L::KS, vs = t % L::VS;
+        const int G = G0 + t;
+        const int ks = G % L::KS, vs = G % L::VS;
         if (pid == 0) {
-          tc::mbar_wait(k_empty + ks, ((t / L::KS) & 1) ^ 1);
+          tc::mbar_wait(k_empty + ks, ((G / L::KS) & 1) ^ 1);
           tc::mbar_expect_tx(k_full + ks, L::kP);
           ts_mark(dbg && t < 16, t);
           uint8_t* dk = sK + ks * L::kP;
@@ -506,7 +524,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             tc::tma_load_3d(dk + c * 16384 + 8192, &tmK, k_full + ks, 64 * c, r2, 0);
           }
         } else {
-          tc::mbar_wait(v_empty + vs, ((t / L::VS) & 1) ^ 1);
+          tc::mbar_wait(v_empty + vs, ((G / L::VS) & 1) ^ 1);
           tc::mbar_expect_tx(v_full + vs, L::kP);
           ts_mark(dbg && t < 8, 112 + t);
           uint8_t* dv = sV + vs * L::kP;
@@ -527,50 +545,53 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     constexpr uint32_t id_st = tc::idesc_bf16(128, 64, false, false);  // pair x Q^T
     // K-major SW128 tile of `rows` rows: k-step kk (16 elements) starts at chunk kk/4, +32 B
     auto koff = [](int kk, int rows) { return uint32_t((kk >> 2) * rows * 128 + (kk & 3) * 32); };
-    tc::mbar_wait(qdo_full, 0);
-    cta_mark(lane == 0, 1);
+    tc::mbar_wait(qdo_full, ip);
+    cta_mark(lane == 0, 1, item);
     auto issue_sdp = [&](int t) {
-      const int ks = t % L::KS, vs = t % L::VS;
-      tc::mbar_wait(k_full + ks, (t / L::KS) & 1);
+      const int G = G0 + t;
+      const int ks = G % L::KS, vs = G % L::VS;
+      tc::mbar_wait(k_full + ks, (G / L::KS) & 1);
       tc::tc_fence_after();
       ts_mark(dbg && lane == 0 && t < 16, 16 + t);
-      const uint32_t tb = (t & 1) ? tB1 : tB0;
+      const uint32_t tb = (G & 1) ? tB1 : tB0;
       const uint64_t dk = tc::desc_add(dKk, ks * L::kP), dv = tc::desc_add(dVk, vs * L::kP);
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk)  // S^T on the K pair alone
         tc::mma_bf16_w(tb, tc::desc_add(dk, koff(kk, 128)), tc::desc_add(dQk, koff(kk, 64)), id_st, kk > 0);
-      tc::mma_commit_w(s_full + (t & 1));
-      tc::mbar_wait(v_full + vs, (t / L::VS) & 1);
+      tc::mma_commit_w(s_full + (G & 1));
+      tc::mbar_wait(v_full + vs, (G / L::VS) & 1);
       tc::tc_fence_after();
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk)
         tc::mma_bf16_w(tb + 64, tc::desc_add(dv, koff(kk, 128)), tc::desc_add(dDOk, koff(kk, 64)), id_st, kk > 0);
-      tc::mma_commit_w(sdp_full + (t & 1));
+      tc::mma_commit_w(sdp_full + (G & 1));
       tc::mma_commit_w(v_empty + vs);
       ts_mark(dbg && lane == 0 && t < 16, 208 + t);
     };
     // S^T/dP^T(t) as soon as its K / V pair landed and the softmax-gradient warps have read
     // TMEM buffer t&1 (sdp_free of t-2); dQ is issued by warp 11 independently
     for (int t = 0; t < np; ++t) {
-      if (t >= 2) tc::mbar_wait(sdp_free + (t & 1), ((t - 2) >> 1) & 1);
+      const int G = G0 + t;
+      if (G >= 2) tc::mbar_wait(sdp_free + (G & 1), ((G - 2) >> 1) & 1);
       issue_sdp(t);
     }
     __syncwarp();
   } else if (warp == kRowsDQWarp) {
     // dQ^T += [K_j1; K_j2]^T dS^T  (M = D, N = 64, K = 128) as soon as dS(t) is in smem
-    tc::mbar_wait(qdo_full, 0);
+    tc::mbar_wait(qdo_full, ip);
     const uint64_t dKm = tc::desc_mnmajor(tc::smem_u32(sK), 16384);
     const uint64_t dDSm = tc::desc_mnmajor(tc::smem_u32(sDS), 16384);
     constexpr uint32_t id_dqt = tc::idesc_bf16(D, 64, true, true);
     for (int t = 0; t < np; ++t) {
-      tc::mbar_wait(ds_full, t & 1);
+      const int G = G0 + t;
+      tc::mbar_wait(ds_full, G & 1);
       tc::tc_fence_after();
       ts_mark(dbg && lane == 0 && t < 16, 64 + t);
-      const uint64_t dk = tc::desc_add(dKm, (t % L::KS) * L::kP);
+      const uint64_t dk = tc::desc_add(dKm, (G % L::KS) * L::kP);
 #pragma unroll
       for (int kk = 0; kk < 8; ++kk)
         tc::mma_bf16_w(tDQT, tc::desc_add(dk, kk * 2048), tc::desc_add(dDSm, kk * 2048), id_dqt, (t | kk) != 0);
-      tc::mma_commit_w(k_empty + (t % L::KS));
+      tc::mma_commit_w(k_empty + (G % L::KS));
       tc::mma_commit_w(ds_empty);
       ts_mark(dbg && lane == 0 && t < 16, 224 + t);
     }
@@ -604,10 +625,11 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       // P = exp2(S log2e / sqrt(d) - lse log2e) from S^T alone, while dP^T may still wait for
       // its V pair; then dS = P (dP - D^s) / sqrt(d).  The per-query constants (lse log2e,
       // D^s / sqrt(d)) are shared-space vector loads.
-      tc::mbar_wait(s_full + (t & 1), (t >> 1) & 1);
+      const int G = G0 + t;
+      tc::mbar_wait(s_full + (G & 1), (G >> 1) & 1);
       tc::tc_fence_after();
       const bool live = c < 64 || 2 * t + 1 < cnt;
-      const uint32_t tb = ((t & 1) ? tB1 : tB0) + lane_base + CW * grp;
+      const uint32_t tb = ((G & 1) ? tB1 : tB0) + lane_base + CW * grp;
       const uint32_t a_l = tc::smem_u32(s_lse2) + 4u * uint32_t(CW * grp);
       const uint32_t a_d = tc::smem_u32(s_ds) + 4u * uint32_t(CW * grp);
       uint32_t pk[CW / 2];
@@ -628,7 +650,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
             }
           }
         }
-        tc::mbar_wait(sdp_full + (t & 1), (t >> 1) & 1);
+        tc::mbar_wait(sdp_full + (G & 1), (G >> 1) & 1);
         tc::tc_fence_after();
         ts_mark(dbg && threadIdx.x == 64 && t < 16, 32 + t);
         ts_mark(dbg && lane == 0 && t >= 4 && t < 8 && warp < 10, 192 + 8 * (t - 4) + (warp - 2));
@@ -637,7 +659,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         tc::tmem_ld_wait();
         tc::tc_fence_before();  // TMEM buffer t&1 may take S/dP(t+2)
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(sdp_free + (t & 1));
+        if (lane == 0) tc::mbar_arrive(sdp_free + (G & 1));
         ts_mark(dbg && threadIdx.x == 64 && t < 16, 240 + t);
         const float sc = p.scale;
 #pragma unroll
@@ -656,7 +678,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         }
       }
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 128 + t);
-      if (t >= 1) tc::mbar_wait(ds_empty, (t - 1) & 1);  // dQ of the previous pair has read dS
+      if (G >= 1) tc::mbar_wait(ds_empty, (G - 1) & 1);  // dQ of the previous pair has read dS
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 144 + t);
       const uint32_t a_ds_tile = tc::smem_u32(sDS);
 #pragma unroll
@@ -705,10 +727,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
 #pragma unroll
       for (int e = 0; e < DQ; ++e) x[e] *= inv;
     }
-    tc::mbar_wait(dq_done, 0);
+    tc::mbar_wait(dq_done, ip);
     tc::tc_fence_after();
     ts_mark(dbg && threadIdx.x == 64, 120);
-    cta_mark(threadIdx.x == 64, 2);
+    cta_mark(threadIdx.x == 64, 2, item);
     constexpr int TP = D + 1;  // with the chunk rotation: conflict-free row-wise reads
     float* tq = reinterpret_cast<float*>(sK);
     {
@@ -752,10 +774,13 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       }
     }
     ts_mark(dbg && threadIdx.x == 64, 124);
-    cta_mark(threadIdx.x == 64, 3);
+    cta_mark(threadIdx.x == 64, 3, item);
   }
+  G0 += np;
   tc::tc_fence_before();
-  __syncthreads();
+  __syncthreads();  // the item is done: smem (the dQ^T transpose in the K ring) and TMEM are free
+  tc::tc_fence_after();
+  }  // items
   if (warp == 0) tc::tmem_dealloc<512>(tmem);
 }
 
@@ -828,7 +853,10 @@ void launch_bwd_rows(const Dims& Dm, const void* q, const void* k, const void* v
     make_tmap_bf16(&tk, k, D, krows, 1, D, 0, 64);
     make_tmap_bf16(&tv, v, D, krows, 1, D, 0, 64);
     SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
-    launch_pdl(kern, dim3(Dm.Tm, unsigned(Dm.U)), kRowsThreads, bytes, st, tq, tdo, tk, tv, p);
+    const long long items = (long long)Dm.U * Dm.Tm;
+    p.items = items;
+    const unsigned grid = unsigned(SLAB_ROWS_PERSIST ? std::min<long long>(items, sm_count()) : items);
+    launch_pdl(kern, dim3(grid), kRowsThreads, bytes, st, tq, tdo, tk, tv, p);
     check_launch("k_bwd_rows", st);
   };
   if (Dm.d == 128)

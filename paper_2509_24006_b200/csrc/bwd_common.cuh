@@ -26,7 +26,8 @@ __device__ __forceinline__ void ts_mark(bool on, int slot) {  // -DSLAB_TIMELINE
 #endif
 }
 
-__device__ __forceinline__ void cta_mark(bool on, int slot) {  // -DSLAB_TIMELINE builds only
+// per work item (a CTA of a grid launch, or an item of a persistent CTA)
+__device__ __forceinline__ void cta_mark(bool on, int slot, long long id) {  // -DSLAB_TIMELINE builds only
 #ifdef SLAB_TIMELINE
   if (on) {
     unsigned long long v = clock64();
@@ -35,12 +36,16 @@ __device__ __forceinline__ void cta_mark(bool on, int slot) {  // -DSLAB_TIMELIN
       asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
       v |= (unsigned long long)sm << 56;
     }
-    g_cta_prof[(blockIdx.y * gridDim.x + blockIdx.x) & 8191][slot] = v;
+    g_cta_prof[id & 8191][slot] = v;
   }
 #else
   (void)on;
   (void)slot;
+  (void)id;
 #endif
+}
+__device__ __forceinline__ void cta_mark(bool on, int slot) {
+  cta_mark(on, slot, (long long)blockIdx.y * gridDim.x + blockIdx.x);
 }
 
 __device__ __forceinline__ float ex2f(float x) {
@@ -101,6 +106,7 @@ struct BwdParams {
   float scale_log2;    // scale * log2(e)
   int phi;
   const int8_t* labels;
+  long long items;     // persistent kernels: work items of the launch
   int ds_external;     // k_bwd_lin: D^s comes from k_rowdot (independent cotangents), not dO . O^s
   // optional SlaGradients parts (backward.hpp:10-16), f32 [U, N, D]; null: not written
   float* dq_part;      // sparse dQ

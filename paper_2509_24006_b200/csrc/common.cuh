@@ -133,6 +133,18 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
   cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);  // errors surface in check_launch
 }
 
+// streaming multiprocessors of the current device (persistent grids)
+inline int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 inline void check_launch(const char* what, cudaStream_t st) {
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
