@@ -32,12 +32,6 @@ namespace {
 #ifndef SLAB_COLS_POLY
 #define SLAB_COLS_POLY 0
 #endif
-// 1: the linear branch (dK^phi^T = dH_agg V^T, dV^T = dH_agg^T phi(K)^T) runs BEFORE the critical
-// loop, while the tensor pipe would otherwise idle on pair 0's loads, instead of as a serial
-// wait-MMA-commit chain after it; dH_agg is ring item 0 and phi(K) is built in the P buffer
-#ifndef SLAB_COLS_LIN_FIRST
-#define SLAB_COLS_LIN_FIRST 0  // measured: 0.928 ms against 0.842 (phi(K) and dH_agg delay pair 0)
-#endif
 #ifndef SLAB_COLS_DVFIRST  // 1: acc(t) issues dV^T first, P stored first (measured 0.881 vs 0.838 ms)
 #define SLAB_COLS_DVFIRST 0
 #endif
@@ -92,7 +86,6 @@ __global__ void __launch_bounds__(kColsThreads, 1)
   uint64_t* all_done = bars + 9;
   uint64_t* sdp_free = bars + 10;  // [2] (2-issuer mode) compute warps have read S|dP buffer t&1
   uint64_t* s_full = bars + 12;    // [2] S(t) alone is in TMEM (P's exponentials start early)
-  uint64_t* kf_free = bars + 14;   // lin-first: the linear MMAs have read phi(K) in the P buffer
   uint64_t* ring_full = bars + 16;        // [RS]
   uint64_t* ring_empty = bars + 16 + RS;  // [RS]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 16 + 2 * RS);
@@ -108,8 +101,6 @@ __global__ void __launch_bounds__(kColsThreads, 1)
   ts_mark(dbg && threadIdx.x == 0, 127);
   cta_mark(threadIdx.x == 0, 0);
   const bool has_lin = p.ccol_marg[ucol] > 0;  // some marginal row in this column (k_build_csc)
-  constexpr bool kLinFirst = SLAB_COLS_LIN_FIRST;
-  const int off = (kLinFirst && has_lin) ? 1 : 0;  // ring items: [dH_agg,] then Q / dO pairs
   ts_mark(dbg && threadIdx.x == 0, 126);
   const int kv0 = int(u * p.N) + j * 64;
   // pair 0's query blocks, loaded alongside cnt so its loads can leave before the TMEM
@@ -140,7 +131,6 @@ __global__ void __launch_bounds__(kColsThreads, 1)
       tc::mbar_init(sdp_free + 1, 8);
       tc::mbar_init(kf_ready, 8);
       tc::mbar_init(all_done, 1);
-      tc::mbar_init(kf_free, 1);
       tc::fence_barrier_init();
       // K_j / V_j and pair 0 (items 0 and 1) now; the producer loops start at pair 1
       tc::tma_prefetch(&tmQ);
@@ -151,22 +141,16 @@ __global__ void __launch_bounds__(kColsThreads, 1)
         tc::tma_load_3d(sK + c * 8192, &tmK, kv_full, 64 * c, kv0, 0);
         tc::tma_load_3d(sV + c * 8192, &tmV, kv_full, 64 * c, kv0, 0);
       }
-      if (off) {  // lin-first: dH_agg is item 0, D / 64 chunks of [D rows x 64]
-        tc::mbar_expect_tx(ring_full, D * D * 2);
-#pragma unroll
-        for (int c = 0; c < D / 64; ++c) tc::tma_load_3d(sRing + c * D * 128, &tmHa, ring_full, 64 * c, int(ucol * D), 0);
-      }
       if (np > 0) {
         const int r1 = int(u * p.N) + l0 * 64, r2 = int(u * p.N) + (cnt > 1 ? l1 : l0) * 64;
         ts_mark(dbg, 0);
 #pragma unroll
         for (int it = 0; it < 2; ++it) {
-          const int item = off + it;
-          tc::mbar_expect_tx(ring_full + item, L::kP);
+          tc::mbar_expect_tx(ring_full + it, L::kP);
 #pragma unroll
           for (int c = 0; c < D / 64; ++c) {
-            tc::tma_load_3d(sRing + item * L::kSlot + c * 16384, it ? &tmDO : &tmQ, ring_full + item, 64 * c, r1, 0);
-            tc::tma_load_3d(sRing + item * L::kSlot + c * 16384 + 8192, it ? &tmDO : &tmQ, ring_full + item, 64 * c, r2, 0);
+            tc::tma_load_3d(sRing + it * L::kSlot + c * 16384, it ? &tmDO : &tmQ, ring_full + it, 64 * c, r1, 0);
+            tc::tma_load_3d(sRing + it * L::kSlot + c * 16384 + 8192, it ? &tmDO : &tmQ, ring_full + it, 64 * c, r2, 0);
           }
         }
       }
@@ -199,7 +183,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
       for (int pp = 1; pp < np; ++pp) {  // pair 0 left before the block barrier
         const int r1 = int(u * p.N) + list[2 * pp] * 64;
         const int r2 = int(u * p.N) + list[min(2 * pp + 1, cnt - 1)] * 64;
-        const int item = off + 2 * pp + pid;
+        const int item = 2 * pp + pid;
         uint8_t* dst = acquire(item, L::kP);
         ts_mark(dbg && pid == 0 && pp < 16, pp);
         uint64_t* fb = ring_full + (item % RS);
@@ -209,7 +193,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
           tc::tma_load_3d(dst + c * 16384 + 8192, tm, fb, 64 * c, r2, 0);
         }
       }
-      if (!kLinFirst && has_lin && pid == 0) {  // dH_agg: the last item, D / 64 chunks of [D rows x 64]
+      if (has_lin && pid == 0) {  // dH_agg: the last item, D / 64 chunks of [D rows x 64]
         const int item = 2 * np;
         uint8_t* dst = acquire(item, D * D * 2);
 #pragma unroll
@@ -244,7 +228,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
     auto koff = [](int kk, int rows) { return uint32_t((kk >> 2) * rows * 128 + (kk & 3) * 32); };
     // acc(t): dK^T += Q_pair^T dS, then dV^T += dO_pair^T P  (M = D, N = 64 keys, K = 128)
     auto issue_acc = [&](int t) {
-      const int sq = (off + 2 * t) % RS, sdo = (off + 2 * t + 1) % RS;
+      const int sq = (2 * t) % RS, sdo = (2 * t + 1) % RS;
       const uint64_t dq = tc::desc_add(dRm, sq * L::kSlot), ddo = tc::desc_add(dRm, sdo * L::kSlot);
       const uint64_t dp = dPDm, dd = tc::desc_add(dPDm, 16384);
       auto dk = [&] {
@@ -261,8 +245,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
         tc::tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          tc::mma_bf16_w(tDVT, tc::desc_add(ddo, kk * 2048), tc::desc_add(dp, kk * 2048), id_acc,
-                         (off | t | kk) != 0);  // lin-first: dV^T already holds the linear part
+          tc::mma_bf16_w(tDVT, tc::desc_add(ddo, kk * 2048), tc::desc_add(dp, kk * 2048), id_acc, (t | kk) != 0);
         tc::mma_commit_w(ring_empty + sdo);
         tc::mma_commit_w(p_empty);
       };
@@ -279,7 +262,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
     if (warp == 1) {
       // S/dP(t) once its ring stage landed and the compute warps have read TMEM buffer t&1
       for (int ts = 0; ts < np; ++ts) {
-        const int iq = off + 2 * ts, ido = off + 2 * ts + 1;
+        const int iq = 2 * ts, ido = 2 * ts + 1;
         if (ts >= 2) tc::mbar_wait(sdp_free + (ts & 1), ((ts - 2) >> 1) & 1);
         tc::mbar_wait(ring_full + iq % RS, (iq / RS) & 1);
         tc::tc_fence_after();
@@ -300,18 +283,6 @@ __global__ void __launch_bounds__(kColsThreads, 1)
       }
       __syncwarp();
     } else {  // accumulation warp: dK^T(t) / dV^T(t) as soon as dS(t) / P(t) are in smem
-      if (off) {  // lin-first: the linear branch while pair 0 still loads
-        const uint32_t sh = wait_item(0);
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) tc::mma_bf16_w(tKPT, kdesc(sh, kk, D), kdesc(aV, kk, 64), id_kp, kk > 0);
-        tc::mbar_wait(kf_ready, 0);
-        tc::tc_fence_after();
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          tc::mma_bf16_w(tDVT, tc::desc_mnmajor(sh + kk * 2048, D * 128), kdesc(aKF, kk, 64), id_vl, kk > 0 ? 1u : 0u);
-        tc::mma_commit_w(ring_empty);  // item 0's slot
-        tc::mma_commit_w(kf_free);     // the P buffer may take P(0)
-      }
       for (int ta = 0; ta < np; ++ta) {
         ts_mark(dbg && lane == 0 && ta < 16, 96 + ta);
         issue_acc(ta);
@@ -326,7 +297,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
     }
     __syncwarp();
     if (warp == kAccWarp) {  // the linear part and all_done: same issuing thread as acc
-    if (!kLinFirst && has_lin) {
+    if (has_lin) {
       const int item = 2 * np;
       const uint32_t sh = wait_item(item);
       // dK^phi^T raw = dH_agg V^T (M = D over a, N = 64 keys, K = D over b): needs only dH_agg
@@ -352,64 +323,6 @@ __global__ void __launch_bounds__(kColsThreads, 1)
     const uint32_t lane_base = uint32_t(32 * q4) << 16;
     const int tid = threadIdx.x - 64;  // 0..255
     for (int a = tid; a < D; a += 256) zas[a] = has_lin ? tc::load_sum3(p.gZa + ucol * 3 * D + a, D) : 0.f;
-    // ---- phi(K_j) rows (4 threads per key row, D/4 columns each): statistics, then this
-    // thread's D/4 values in the per-sub rotated chunk order the final row-wise pass reads
-    // (conflict-free transposed tiles)
-    const int c = tid >> 2, c0 = (tid & 3) * (D / 4);
-    const int sub = tid & 3;
-    auto rot = [&](int cc) { return (cc + 8 * sub) & (D / 4 - 1); };
-    constexpr int DQ = D / 4;
-    auto phi_k_rows = [&](float (&kf)[DQ]) {
-      tc::mbar_wait(kv_full, 0);  // K_j must have landed even when no critical row came by
-      float mx = 0.f, inv = 1.f;
-      if (p.phi == 2) {
-        mx = -INFINITY;
-#pragma unroll
-        for (int cc = 0; cc < D / 4; cc += 8) {
-          float f[8];
-          unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, c0 + cc)), f);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) mx = fmaxf(mx, f[e]);
-        }
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        float se = 0.f;
-#pragma unroll
-        for (int cc = 0; cc < D / 4; cc += 8) {
-          float f[8];
-          unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, c0 + cc)), f);
-#pragma unroll
-          for (int e = 0; e < 8; ++e) se += __expf(f[e] - mx);
-        }
-        se += __shfl_xor_sync(0xffffffffu, se, 1);
-        se += __shfl_xor_sync(0xffffffffu, se, 2);
-        inv = 1.f / se;
-      }
-#pragma unroll
-      for (int cc0 = 0; cc0 < DQ; cc0 += 8) {
-        float f[8];
-        unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, c0 + rot(cc0))), f);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) kf[cc0 + e] = p.phi == 2 ? __expf(f[e] - mx) * inv : phi_elem(p.phi, f[e]);
-      }
-    };
-    auto store_kf_tile = [&](const float (&kf)[DQ]) {  // the bf16 phi(K_j) tile in the P buffer
-#pragma unroll
-      for (int cc0 = 0; cc0 < DQ; cc0 += 8) {
-        float f[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) f[e] = kf[cc0 + e];
-        *reinterpret_cast<uint4*>(sKF + tile_off(c, c0 + rot(cc0))) = pack8(f);
-      }
-      tc::fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(kf_ready);
-    };
-    if (off) {  // lin-first: the phi(K_j) tile for the linear MMAs before the loop
-      float kf0[DQ];
-      phi_k_rows(kf0);
-      store_kf_tile(kf0);
-    }
     // ---- loop: thread = query row rq of the pair (S / dP lanes), 32 key columns per group
     const int rq = 32 * q4 + lane;
     // per-query-row lse / D^s of pair t+1 are fetched during pair t (two dependent global
@@ -486,7 +399,6 @@ __global__ void __launch_bounds__(kColsThreads, 1)
       };
       auto store_p = [&] {
         if (t >= 1) tc::mbar_wait(p_empty, (t - 1) & 1);
-        else if (off) tc::mbar_wait(kf_free, 0);  // lin-first: phi(K) in this buffer has been read
 #pragma unroll
         for (int ch = 0; ch < 4; ++ch)
           tc::sts_u4(prow + tc::sw128_off(rq, 4 * grp + ch), make_uint4(pp[4 * ch], pp[4 * ch + 1], pp[4 * ch + 2], pp[4 * ch + 3]));
@@ -504,20 +416,68 @@ __global__ void __launch_bounds__(kColsThreads, 1)
       }
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 48 + t);
     }
-    // ---- phi(K_j) of this thread's D/4 columns (recomputed here in lin-first mode, where the
-    // tile was built before the loop): kept in registers for the Jacobian at the end
+    // ---- phi(K_j) rows (4 threads per key row, D/4 columns each): statistics + the bf16 tile
+    tc::mbar_wait(kv_full, 0);  // K_j must have landed even when no critical row came by
+    const int c = tid >> 2, c0 = (tid & 3) * (D / 4);
+    float mx = 0.f, inv = 1.f;
+    if (p.phi == 2) {
+      mx = -INFINITY;
+#pragma unroll
+      for (int cc = 0; cc < D / 4; cc += 8) {
+        float f[8];
+        unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, c0 + cc)), f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) mx = fmaxf(mx, f[e]);
+      }
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      float se = 0.f;
+#pragma unroll
+      for (int cc = 0; cc < D / 4; cc += 8) {
+        float f[8];
+        unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, c0 + cc)), f);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) se += __expf(f[e] - mx);
+      }
+      se += __shfl_xor_sync(0xffffffffu, se, 1);
+      se += __shfl_xor_sync(0xffffffffu, se, 2);
+      inv = 1.f / se;
+    }
+    // phi(K_j) of this thread's D/4 columns, in the per-sub rotated chunk order the final
+    // row-wise pass reads (conflict-free transposed tiles), computed while the last
+    // accumulation MMAs still run; kept in registers for the Jacobian at the end
+    const int sub = tid & 3;
+    auto rot = [&](int cc) { return (cc + 8 * sub) & (D / 4 - 1); };
+    constexpr int DQ = D / 4;
     float kf[DQ];
-    phi_k_rows(kf);
+#pragma unroll
+    for (int cc0 = 0; cc0 < DQ; cc0 += 8) {
+      float f[8];
+      unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, c0 + rot(cc0))), f);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) kf[cc0 + e] = p.phi == 2 ? __expf(f[e] - mx) * inv : phi_elem(p.phi, f[e]);
+    }
     tc::mbar_wait(acc_done, 0);  // the P / dS buffers are free
     ts_mark(dbg && threadIdx.x == 64, 120);
     cta_mark(threadIdx.x == 64, 2);
-    if (!kLinFirst && has_lin) store_kf_tile(kf);
+    if (has_lin) {
+#pragma unroll
+      for (int cc0 = 0; cc0 < DQ; cc0 += 8) {
+        float f[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) f[e] = kf[cc0 + e];
+        *reinterpret_cast<uint4*>(sKF + tile_off(c, c0 + rot(cc0))) = pack8(f);
+      }
+      tc::fence_proxy_async();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(kf_ready);
+    }
     // ---- transpose dK^T, dV^T, dK^phi^T (lane = column a) into smem [key row][a].  dK^T is final
     // at acc_done, so it goes first, while the linear MMAs still run; its region avoids the ring
     // slot holding dH_agg (item 2 np), which those MMAs read until all_done.
     constexpr int TP = D + 1;  // with the chunk rotation below: conflict-free row-wise reads
     const int hs = (2 * np) % RS;
-    const bool tk_low = !kLinFirst && has_lin && (hs == 2 || hs == 3);
+    const bool tk_low = has_lin && (hs == 2 || hs == 3);
     float* tbase = reinterpret_cast<float*>(sRing);
     float* tk = tk_low ? tbase : tbase + 2 * 64 * TP;
     float* tv = tk_low ? tbase + 64 * TP : tbase;
@@ -632,8 +592,9 @@ void launch_cols_t(const Dims& Dm, const void* q, const void* k, const void* v, 
 void launch_bwd_cols(const Dims& Dm, const void* q, const void* k, const void* v, const float* lse,
                      const void* d_out, void* dk, void* dv, const StateBufs& s,
                      const __nv_bfloat16* Ha, const float* gZa, const float* Ds, float* dk_part,
-                     float* dkf_part, cudaStream_t st) {
+                     float* dkf_part, int* work, cudaStream_t st) {
   BwdParams p{};
+  p.work = work;  // unused: one CTA per key block (a persistent variant spilled)
   p.dk_part = dk_part;
   p.dkf_part = dkf_part;
   p.ccol_cnt = s.ccol_cnt;

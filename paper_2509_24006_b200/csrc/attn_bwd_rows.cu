@@ -445,6 +445,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   const uint32_t tDQT = tmem, tB0 = tmem + 128, tB1 = tmem + 256;  // dQ^T (M = D); S^T|dP^T pairs
   int G0 = 0;  // pairs this CTA processed before the current item (32-bit: cheap % and / by constants)
   int nit = 0;       // items this CTA processed before the current one
+#pragma unroll 1
   for (long long item = blockIdx.x; item < p.items; item += gridDim.x, ++nit) {
   const int i = int(item % p.Tm);
   const long long u = item / p.Tm;

@@ -437,7 +437,7 @@ void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, 
   }
   // columns pass: dk_total, dv
   if (side.s) SLAB_CUDA(cudaStreamWaitEvent(st, side.join, 0));
-  launch_bwd_cols(Dm, q, k, v, lse, d_out, dk, dv, s, wb.hab, wb.gZa, wb.Ds, parts.dk, parts.dk_feat, st);
+  launch_bwd_cols(Dm, q, k, v, lse, d_out, dk, dv, s, wb.hab, wb.gZa, wb.Ds, parts.dk, parts.dk_feat, wb.work_ctr, st);
   if (!side.s && dw) launch_dw_fast(Dm, o_l, d_out, dw, wb, st);
   guard.release();
   if (side.s) SLAB_CUDA(cudaStreamWaitEvent(st, side.join2, 0));
@@ -457,7 +457,7 @@ void fast_backward_cols(const Dims& Dm, const void* q, const void* k, const void
   launch_build_m0(Dm, s, st);
   launch_build_csc(Dm, s, st);
   launch_agg_t(Dm, s, wb, gH, z3, st);
-  launch_bwd_cols(Dm, q, k, v, lse, d_out, dk, dv, s, wb.hab, wb.gZa, Ds, nullptr, nullptr, st);
+  launch_bwd_cols(Dm, q, k, v, lse, d_out, dk, dv, s, wb.hab, wb.gZa, Ds, nullptr, nullptr, wb.work_ctr, st);
 }
 
 }  // namespace slab

@@ -71,7 +71,7 @@ void launch_bwd_rows(const Dims& Dm, const void* q, const void* k, const void* v
 void launch_bwd_cols(const Dims& Dm, const void* q, const void* k, const void* v, const float* lse,
                      const void* d_out, void* dk, void* dv, const StateBufs& s,
                      const __nv_bfloat16* Ha, const float* gZa, const float* Ds, float* dk_part,
-                     float* dkf_part, cudaStream_t st);
+                     float* dkf_part, int* work, cudaStream_t st);
 bool fast_supported(const Dims& D, int dtype);
 // A side stream with fork / join events: work that only depends on the call's inputs runs
 // there, concurrent with latency-bound kernels on the caller's stream (s == nullptr: none).
