@@ -68,6 +68,10 @@ Dims resolve(const sla_b200_problem* p) {
   D.N_valid = p->n;
   D.bnhd = bnhd;
   D.staged = ragged || bnhd;
+  // the caller's [*, N, d] tensors and lse, addressed in place by the kernels (RowLayout)
+  D.rl.mode = bnhd ? 2 : (ragged ? 1 : 0);
+  D.rl.H = int(p->heads);
+  D.rl.nv = p->n;
   D.N = ragged ? (p->n + 63) / 64 * 64 : p->n;
   D.Nk = p->n_kv > 0 ? p->n_kv : D.N;
   D.Nk_valid = p->n_kv > 0 ? p->n_kv : D.N_valid;
@@ -156,7 +160,7 @@ void check_inputs(const sla_b200_problem* p, const Dims& D, const WorkBufs& w,
     launch_check_finite(D, p->dtype, x, w.err, st);
     const long long bad = read_slot(w.err, st);
     if (bad != LLONG_MAX) {
-      const long long per = D.N * D.d;
+      const long long per = D.N_valid * D.d;  // the caller's rows (ragged: N_valid per unit)
       const long long u = bad / per, rc = bad % per;
       std::string msg = std::string("sla_forward: ") + name + " has non-finite entry at (" +
                         std::to_string(rc / D.d) + ", " + std::to_string(rc % D.d) + ")";
@@ -164,43 +168,6 @@ void check_inputs(const sla_b200_problem* p, const Dims& D, const WorkBufs& w,
       throw InvalidArgument(msg);
     }
   }
-}
-
-// Staged problems (ragged N and/or [B, N, H, d] callers): the kernels run on unit-major
-// [U, N, row] copies with zero tail rows.  An SM gather / scatter kernel (the copy engines
-// behind cudaMemcpy2DAsync moved these ~1 GB per step at a fraction of HBM speed).
-template <typename T>
-__global__ void k_stage_rows(T* __restrict__ dst, const T* __restrict__ src, long long U, long long H,
-                             long long n_pad, long long n_valid, int row_elems, bool bnhd, bool to_unit) {
-  const long long rows = to_unit ? n_pad : n_valid;
-  const long long total = U * rows * row_elems;
-  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total;
-       e += (long long)gridDim.x * blockDim.x) {
-    const int ce = int(e % row_elems);
-    const long long rr = e / row_elems, r = rr % rows, u = rr / rows;
-    const long long caller = bnhd ? ((u / H) * n_valid + r) * H + (u % H) : u * n_valid + r;
-    const long long unit = u * n_pad + r;
-    if (to_unit)
-      dst[unit * row_elems + ce] = r < n_valid ? src[caller * row_elems + ce] : T{};
-    else
-      dst[caller * row_elems + ce] = src[unit * row_elems + ce];
-  }
-}
-void stage_rows(const Dims& D, void* dst, const void* src, size_t row_bytes, bool to_unit, cudaStream_t st) {
-  if (row_bytes % 16 == 0) {
-    k_stage_rows<uint4><<<148 * 8, 256, 0, st>>>(static_cast<uint4*>(dst), static_cast<const uint4*>(src), D.U, D.H,
-                                                 D.N, D.N_valid, int(row_bytes / 16), D.bnhd, to_unit);
-  } else {
-    k_stage_rows<uint32_t><<<148 * 8, 256, 0, st>>>(static_cast<uint32_t*>(dst), static_cast<const uint32_t*>(src),
-                                                    D.U, D.H, D.N, D.N_valid, int(row_bytes / 4), D.bnhd, to_unit);
-  }
-  check_launch("k_stage_rows", st);
-}
-void pad_rows(const Dims& D, void* dst, const void* src, size_t row_bytes, cudaStream_t st) {
-  stage_rows(D, dst, src, row_bytes, true, st);
-}
-void unpad_rows(const Dims& D, void* dst, const void* src, size_t row_bytes, cudaStream_t st) {
-  stage_rows(D, dst, src, row_bytes, false, st);
 }
 
 // returns true when the fast path's marginal indicator M0 was written along with the labels
@@ -299,13 +266,6 @@ int sla_b200_classify(const sla_b200_problem* p, const void* q, const void* k, i
     StateBufs s;
     WorkBufs w;
     buffers(p, D, state, workspace, s, w);
-    if (D.staged) {
-      const size_t rb = size_t(D.d) * 2;
-      pad_rows(D, w.pad[kPQ], q, rb, st);
-      pad_rows(D, w.pad[kPK], k, rb, st);
-      q = w.pad[kPQ];
-      k = w.pad[kPK];
-    }
     if (p->flags & SLA_B200_FLAG_CHECK_FINITE) check_inputs(p, D, w, {{"Q", q}, {"K", k}}, st);
     launch_classify(D, p->dtype, p->mask_precision, q, k, s, w, p_c, st);
     if (labels && labels != s.labels)
@@ -326,22 +286,6 @@ int sla_b200_forward(const sla_b200_problem* p, const void* q, const void* k, co
     StateBufs s;
     WorkBufs wb;
     buffers(p, D, state, workspace, s, wb);
-    const bool ragged = D.staged;  // ragged N and/or the [B, N, H, d] layout
-    void *o_u = o, *o_s_u = o_s, *o_l_u = o_l;
-    float* lse_u = lse;
-    if (ragged) {  // run on zero-padded copies; only rows < N_valid go back
-      const size_t rb = size_t(D.d) * 2;
-      pad_rows(D, wb.pad[kPQ], q, rb, st);
-      pad_rows(D, wb.pad[kPK], k, rb, st);
-      pad_rows(D, wb.pad[kPV], v, rb, st);
-      q = wb.pad[kPQ];
-      k = wb.pad[kPK];
-      v = wb.pad[kPV];
-      o = o ? wb.pad[kPO] : nullptr;
-      o_s = wb.pad[kPOs];
-      o_l = wb.pad[kPOl];
-      lse = wb.pad_lse;
-    }
     const bool check = p->flags & SLA_B200_FLAG_CHECK_FINITE;
     if (check) check_inputs(p, D, wb, {{"Q", q}, {"K", k}, {"V", v}}, st);
     const bool fast = use_fast(p, D);
@@ -389,13 +333,6 @@ int sla_b200_forward(const sla_b200_problem* p, const void* q, const void* k, co
         }
       }
     }
-    if (ragged) {
-      const size_t rb = size_t(D.d) * 2;
-      if (o_u) unpad_rows(D, o_u, o, rb, st);
-      if (o_s_u) unpad_rows(D, o_s_u, o_s, rb, st);
-      if (o_l_u) unpad_rows(D, o_l_u, o_l, rb, st);
-      unpad_rows(D, lse_u, lse, sizeof(float), st);
-    }
   });
 }
 
@@ -420,38 +357,12 @@ void backward_impl(const sla_b200_problem* p, const void* q, const void* k, cons
   WorkBufs wb;
   buffers(p, D, state, workspace, s, wb);
   const bool fast = use_fast(p, D);
-  const bool ragged = D.staged;  // ragged N and/or the [B, N, H, d] layout
   GradParts gp;
   if (parts) {
     gp = GradParts{parts->dq_sparse, parts->dk_sparse, parts->dq_feat, parts->dk_feat};
     if (!gp.dq || !gp.dk || !gp.dq_feat || !gp.dk_feat)
       throw InvalidArgument("sla_backward: gradient parts are all-or-none");
-    if (ragged) throw InvalidArgument("sla_backward: gradient parts are not available for staged layouts");
-  }
-  void *dq_u = dq, *dk_u = dk, *dv_u = dv;
-  if (ragged) {
-    const size_t rb = size_t(D.d) * 2;
-    pad_rows(D, wb.pad[kPQ], q, rb, st);
-    pad_rows(D, wb.pad[kPK], k, rb, st);
-    pad_rows(D, wb.pad[kPV], v, rb, st);
-    pad_rows(D, wb.pad[kPOs], o_s, rb, st);
-    pad_rows(D, wb.pad[kPOl], o_l, rb, st);
-    pad_rows(D, wb.pad[kPdO], d_out, rb, st);  // zero cotangent rows: padded queries are inert
-    if (d_out_l) {  // the padded O slot is free in the backward
-      pad_rows(D, wb.pad[kPO], d_out_l, rb, st);
-      d_out_l = wb.pad[kPO];
-    }
-    pad_rows(D, wb.pad_lse, lse, sizeof(float), st);
-    q = wb.pad[kPQ];
-    k = wb.pad[kPK];
-    v = wb.pad[kPV];
-    o_s = wb.pad[kPOs];
-    o_l = wb.pad[kPOl];
-    d_out = wb.pad[kPdO];
-    lse = wb.pad_lse;
-    dq = wb.pad[kPdQ];
-    dk = wb.pad[kPdK];
-    dv = wb.pad[kPdV];
+    if (D.staged) throw InvalidArgument("sla_backward: gradient parts are not available for ragged / [B, N, H, d] layouts");
   }
   if (fast) {
     SideFork side;
@@ -474,12 +385,6 @@ void backward_impl(const sla_b200_problem* p, const void* q, const void* k, cons
       SLAB_CUDA(cudaMemcpyAsync(gp.dq_feat, wb.dqf, bytes, cudaMemcpyDeviceToDevice, st));
       SLAB_CUDA(cudaMemcpyAsync(gp.dk_feat, wb.dkf, bytes, cudaMemcpyDeviceToDevice, st));
     }
-  }
-  if (ragged) {
-    const size_t rb = size_t(D.d) * 2;
-    unpad_rows(D, dq_u, dq, rb, st);
-    unpad_rows(D, dk_u, dk, rb, st);
-    unpad_rows(D, dv_u, dv, rb, st);
   }
 }
 
@@ -638,10 +543,6 @@ RowStats row_stats(const sla_b200_problem* p, const Dims& D, const void* q, cons
   RowStats r;
   r.rows.resize(rows);
   if (q) {
-    if (D.staged) {
-      pad_rows(D, w.pad[kPQ], q, size_t(D.d) * 2, st);
-      q = w.pad[kPQ];
-    }
     launch_lin_rows(D, p->dtype, q, s.Z, use_fast(p, D), dstats, dlin, st);
     r.lin.resize(rows);
     SLAB_CUDA(cudaMemcpyAsync(r.lin.data(), dlin, rows * sizeof(int), cudaMemcpyDeviceToHost, st));

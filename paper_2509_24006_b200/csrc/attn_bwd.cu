@@ -102,7 +102,6 @@ __global__ void __launch_bounds__(kColsThreads, 1)
   cta_mark(threadIdx.x == 0, 0);
   const bool has_lin = p.ccol_marg[ucol] > 0;  // some marginal row in this column (k_build_csc)
   ts_mark(dbg && threadIdx.x == 0, 126);
-  const int kv0 = int(u * p.N) + j * 64;
   // pair 0's query blocks, loaded alongside cnt so its loads can leave before the TMEM
   // allocation and the block barrier
   int l0 = 0, l1 = 0;
@@ -138,19 +137,20 @@ __global__ void __launch_bounds__(kColsThreads, 1)
       tc::mbar_expect_tx(kv_full, 2 * L::kT);
 #pragma unroll
       for (int c = 0; c < D / 64; ++c) {
-        tc::tma_load_3d(sK + c * 8192, &tmK, kv_full, 64 * c, kv0, 0);
-        tc::tma_load_3d(sV + c * 8192, &tmV, kv_full, 64 * c, kv0, 0);
+        tc::tma_load_rows(sK + c * 8192, &tmK, kv_full, 64 * c, u, j * 64, p.N, p.rl);
+        tc::tma_load_rows(sV + c * 8192, &tmV, kv_full, 64 * c, u, j * 64, p.N, p.rl);
       }
       if (np > 0) {
-        const int r1 = int(u * p.N) + l0 * 64, r2 = int(u * p.N) + (cnt > 1 ? l1 : l0) * 64;
+        const int r1 = l0 * 64, r2 = (cnt > 1 ? l1 : l0) * 64;  // query rows within the unit
         ts_mark(dbg, 0);
 #pragma unroll
         for (int it = 0; it < 2; ++it) {
           tc::mbar_expect_tx(ring_full + it, L::kP);
 #pragma unroll
           for (int c = 0; c < D / 64; ++c) {
-            tc::tma_load_3d(sRing + it * L::kSlot + c * 16384, it ? &tmDO : &tmQ, ring_full + it, 64 * c, r1, 0);
-            tc::tma_load_3d(sRing + it * L::kSlot + c * 16384 + 8192, it ? &tmDO : &tmQ, ring_full + it, 64 * c, r2, 0);
+            tc::tma_load_rows(sRing + it * L::kSlot + c * 16384, it ? &tmDO : &tmQ, ring_full + it, 64 * c, u, r1, p.N, p.rl);
+            tc::tma_load_rows(sRing + it * L::kSlot + c * 16384 + 8192, it ? &tmDO : &tmQ, ring_full + it, 64 * c, u, r2, p.N,
+                              p.rl);
           }
         }
       }
@@ -181,16 +181,16 @@ __global__ void __launch_bounds__(kColsThreads, 1)
       };
       const CUtensorMap* tm = pid ? &tmDO : &tmQ;
       for (int pp = 1; pp < np; ++pp) {  // pair 0 left before the block barrier
-        const int r1 = int(u * p.N) + list[2 * pp] * 64;
-        const int r2 = int(u * p.N) + list[min(2 * pp + 1, cnt - 1)] * 64;
+        const int r1 = list[2 * pp] * 64;  // query rows within the unit
+        const int r2 = list[min(2 * pp + 1, cnt - 1)] * 64;
         const int item = 2 * pp + pid;
         uint8_t* dst = acquire(item, L::kP);
         ts_mark(dbg && pid == 0 && pp < 16, pp);
         uint64_t* fb = ring_full + (item % RS);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
-          tc::tma_load_3d(dst + c * 16384, tm, fb, 64 * c, r1, 0);
-          tc::tma_load_3d(dst + c * 16384 + 8192, tm, fb, 64 * c, r2, 0);
+          tc::tma_load_rows(dst + c * 16384, tm, fb, 64 * c, u, r1, p.N, p.rl);
+          tc::tma_load_rows(dst + c * 16384 + 8192, tm, fb, 64 * c, u, r2, p.N, p.rl);
         }
       }
       if (has_lin && pid == 0) {  // dH_agg: the last item, D / 64 chunks of [D rows x 64]
@@ -333,7 +333,8 @@ __global__ void __launch_bounds__(kColsThreads, 1)
     float lse_n = 0.f, ds_n = 0.f;
     if (np > 0) {
       const long long r0 = row_of(0);
-      lse_n = p.lse[r0];
+      const long long c0r = caller_row(p.rl, u, r0 - u * p.N, p.N);  // the caller's lse in place
+      lse_n = c0r >= 0 ? p.lse[c0r] : 0.f;
       ds_n = p.Ds[r0];
     }
     for (int t = 0; t < np; ++t) {
@@ -342,7 +343,8 @@ __global__ void __launch_bounds__(kColsThreads, 1)
       const float dss = ds_n * p.scale;  // D^s / sqrt(d)
       if (t + 1 < np) {
         const long long r1 = row_of(t + 1);
-        lse_n = p.lse[r1];
+        const long long c1r = caller_row(p.rl, u, r1 - u * p.N, p.N);
+        lse_n = c1r >= 0 ? p.lse[c1r] : 0.f;
         ds_n = p.Ds[r1];
       }
       // P from S alone (the exponentials run while dP(t) may still wait for its dO pair)
@@ -524,7 +526,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
 #pragma unroll
       for (int e = 0; e < 8; ++e) g[cc0 + e] = has_lin ? tkp[c * TP + col + e] + zas[col + e] : 0.f;
     }
-    const long long grow = (long long)kv0 + c;
+    const long long grow = caller_row(p.rl, u, (long long)j * 64 + c, p.N);  // -1: past a ragged N
     float jg[DQ];
     if (p.phi == 2) {
       float dot = 0.f;
@@ -551,8 +553,10 @@ __global__ void __launch_bounds__(kColsThreads, 1)
         o[e] = jg[cc0 + e] + tk[c * TP + col + e];
         w8[e] = tv[c * TP + col + e];
       }
-      *reinterpret_cast<uint4*>(p.dk + grow * D + col) = pack8(o);
-      *reinterpret_cast<uint4*>(p.dv + grow * D + col) = pack8(w8);
+      if (grow >= 0) {
+        *reinterpret_cast<uint4*>(p.dk + grow * D + col) = pack8(o);
+        *reinterpret_cast<uint4*>(p.dv + grow * D + col) = pack8(w8);
+      }
       if (p.dk_part) {  // SlaGradients::dk and ::dk_feat (f32)
         float4* dks = reinterpret_cast<float4*>(p.dk_part + grow * D + col);
         float4* dkf = reinterpret_cast<float4*>(p.dkf_part + grow * D + col);
@@ -575,11 +579,10 @@ template <int D>
 void launch_cols_t(const Dims& Dm, const void* q, const void* k, const void* v, const void* d_out,
                    const __nv_bfloat16* Ha, BwdParams p, cudaStream_t st) {
   CUtensorMap tq, tdo, tk, tv, th;
-  const uint64_t rows = uint64_t(Dm.U) * Dm.N, krows = uint64_t(Dm.U) * Dm.Nk;
-  make_tmap_bf16(&tq, q, D, rows, 1, D, 0, 64);
-  make_tmap_bf16(&tdo, d_out, D, rows, 1, D, 0, 64);
-  make_tmap_bf16(&tk, k, D, krows, 1, D, 0, 64);
-  make_tmap_bf16(&tv, v, D, krows, 1, D, 0, 64);
+  make_tmap_rows(&tq, q, D, Dm.U, Dm.N, p.rl, 64);
+  make_tmap_rows(&tdo, d_out, D, Dm.U, Dm.N, p.rl, 64);
+  make_tmap_rows(&tk, k, D, Dm.U, Dm.Nk, p.rl, 64);
+  make_tmap_rows(&tv, v, D, Dm.U, Dm.Nk, p.rl, 64);
   make_tmap_bf16(&th, Ha, D, uint64_t(Dm.U) * Dm.Tn * D, 1, D, 0, D);
   auto kern = k_bwd_cols<D>;
   SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ColsLayout<D>::kBytes));
@@ -594,6 +597,7 @@ void launch_bwd_cols(const Dims& Dm, const void* q, const void* k, const void* v
                      const __nv_bfloat16* Ha, const float* gZa, const float* Ds, float* dk_part,
                      float* dkf_part, int* work, cudaStream_t st) {
   BwdParams p{};
+  p.rl = Dm.rl;
   p.work = work;  // unused: one CTA per key block (a persistent variant spilled)
   p.dk_part = dk_part;
   p.dkf_part = dkf_part;

@@ -112,14 +112,14 @@ __global__ void __launch_bounds__(kLinThreads, 2)
       tc::mbar_expect_tx(qdo_full, 2 * L::kT);
 #pragma unroll
       for (int c = 0; c < D / 64; ++c) {
-        tc::tma_load_3d(sQ + c * 8192, &tmQ, qdo_full, 64 * c, row0, 0);
-        tc::tma_load_3d(sDO + c * 8192, &tmDO, qdo_full, 64 * c, row0, 0);
+        tc::tma_load_rows(sQ + c * 8192, &tmQ, qdo_full, 64 * c, u, i * 64, p.N, p.rl);
+        tc::tma_load_rows(sDO + c * 8192, &tmDO, qdo_full, 64 * c, u, i * 64, p.N, p.rl);
       }
       tc::mbar_expect_tx(o_full, 2 * L::kT);
 #pragma unroll
       for (int c = 0; c < D / 64; ++c) {
-        tc::tma_load_3d(sX + c * 8192, &tmOS, o_full, 64 * c, row0, 0);
-        tc::tma_load_3d(sDOL + c * 8192, &tmOL, o_full, 64 * c, row0, 0);
+        tc::tma_load_rows(sX + c * 8192, &tmOS, o_full, 64 * c, u, i * 64, p.N, p.rl);
+        tc::tma_load_rows(sDOL + c * 8192, &tmOL, o_full, 64 * c, u, i * 64, p.N, p.rl);
       }
       tc::mbar_expect_tx(w_full, D * D * 2);
       const int h = int(u % p.H);
@@ -467,11 +467,11 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       tc::mbar_expect_tx(qdo_full, 2 * L::kT);
 #pragma unroll
       for (int c = 0; c < D / 64; ++c) {
-        tc::tma_load_3d(sQ + c * 8192, &tmQ, qdo_full, 64 * c, row0, 0);
-        tc::tma_load_3d(sDO + c * 8192, &tmDO, qdo_full, 64 * c, row0, 0);
+        tc::tma_load_rows(sQ + c * 8192, &tmQ, qdo_full, 64 * c, u, i * 64, p.N, p.rl);
+        tc::tma_load_rows(sDO + c * 8192, &tmDO, qdo_full, 64 * c, u, i * 64, p.N, p.rl);
       }
       if (np > 0) {
-        const int r1 = int(u * p.N) + l0 * 64, r2 = int(u * p.N) + (cnt > 1 ? l1 : l0) * 64;
+        const int r1 = l0 * 64, r2 = (cnt > 1 ? l1 : l0) * 64;  // key rows within the unit
         ts_mark(dbg, 0);
         ts_mark(dbg, 112);
         tc::mbar_expect_tx(k_full + k0s, L::kP);
@@ -480,13 +480,13 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         uint8_t* dv0 = sV + v0s * L::kP;
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
-          tc::tma_load_3d(dk0 + c * 16384, &tmK, k_full + k0s, 64 * c, r1, 0);
-          tc::tma_load_3d(dk0 + c * 16384 + 8192, &tmK, k_full + k0s, 64 * c, r2, 0);
+          tc::tma_load_rows(dk0 + c * 16384, &tmK, k_full + k0s, 64 * c, u, r1, p.N, p.rl);
+          tc::tma_load_rows(dk0 + c * 16384 + 8192, &tmK, k_full + k0s, 64 * c, u, r2, p.N, p.rl);
         }
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
-          tc::tma_load_3d(dv0 + c * 16384, &tmV, v_full + v0s, 64 * c, r1, 0);
-          tc::tma_load_3d(dv0 + c * 16384 + 8192, &tmV, v_full + v0s, 64 * c, r2, 0);
+          tc::tma_load_rows(dv0 + c * 16384, &tmV, v_full + v0s, 64 * c, u, r1, p.N, p.rl);
+          tc::tma_load_rows(dv0 + c * 16384 + 8192, &tmV, v_full + v0s, 64 * c, u, r2, p.N, p.rl);
         }
       }
     }
@@ -510,8 +510,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       const int pid = warp == 0 ? 0 : 1;
       for (int t = 1; t < np; ++t) {  // pair 0 left before the block barrier
         // an odd tail repeats its block (finite data); the compute warps zero its dS rows
-        const int r1 = int(u * p.N) + list[2 * t] * 64;
-        const int r2 = int(u * p.N) + list[min(2 * t + 1, cnt - 1)] * 64;
+        const int r1 = list[2 * t] * 64;  // key rows within the unit
+        const int r2 = list[min(2 * t + 1, cnt - 1)] * 64;
         const int G = G0 + t;
         const int ks = G % L::KS, vs = G % L::VS;
         if (pid == 0) {
@@ -521,8 +521,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
           uint8_t* dk = sK + ks * L::kP;
 #pragma unroll
           for (int c = 0; c < D / 64; ++c) {
-            tc::tma_load_3d(dk + c * 16384, &tmK, k_full + ks, 64 * c, r1, 0);
-            tc::tma_load_3d(dk + c * 16384 + 8192, &tmK, k_full + ks, 64 * c, r2, 0);
+            tc::tma_load_rows(dk + c * 16384, &tmK, k_full + ks, 64 * c, u, r1, p.N, p.rl);
+            tc::tma_load_rows(dk + c * 16384 + 8192, &tmK, k_full + ks, 64 * c, u, r2, p.N, p.rl);
           }
         } else {
           tc::mbar_wait(v_empty + vs, ((G / L::VS) & 1) ^ 1);
@@ -531,8 +531,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
           uint8_t* dv = sV + vs * L::kP;
 #pragma unroll
           for (int c = 0; c < D / 64; ++c) {
-            tc::tma_load_3d(dv + c * 16384, &tmV, v_full + vs, 64 * c, r1, 0);
-            tc::tma_load_3d(dv + c * 16384 + 8192, &tmV, v_full + vs, 64 * c, r2, 0);
+            tc::tma_load_rows(dv + c * 16384, &tmV, v_full + vs, 64 * c, u, r1, p.N, p.rl);
+            tc::tma_load_rows(dv + c * 16384 + 8192, &tmV, v_full + vs, 64 * c, u, r2, p.N, p.rl);
           }
         }
       }
@@ -617,7 +617,10 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       for (int i = 0; i < DQ / 8; ++i)
         gq[i] = *reinterpret_cast<const uint4*>(src + ((8 * i + 8 * sub) & (DQ - 1)));
     }
-    if (tid < 64) s_lse2[tid] = p.lse[(long long)row0 + tid] * 1.4426950408889634f;
+    if (tid < 64) {  // the caller's lse (0 for rows past a ragged N: their dO is zero-filled)
+      const long long cr = caller_row(p.rl, u, (long long)i * 64 + tid, p.N);
+      s_lse2[tid] = cr >= 0 ? p.lse[cr] * 1.4426950408889634f : 0.f;
+    }
     else if (tid < 128) s_ds[tid - 64] = p.Ds[(long long)row0 + tid - 64] * p.scale;  // D^s / sqrt(d)
     named_sync(1, NCT);
     const int c = 32 * q4 + lane;  // key row of the pair (c < 64: block j1, else j2)
@@ -747,7 +750,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     }
     named_sync(1, NCT);
     {
-      const long long grow = (long long)row0 + rq;
+      const long long grow = caller_row(p.rl, u, (long long)i * 64 + rq, p.N);  // -1: past a ragged N
 #pragma unroll
       for (int cc0 = 0; cc0 < DQ; cc0 += 8) {
         const int col = c0 + rot(cc0);
@@ -762,7 +765,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
           else jg = xe > 0.f ? g[e] : 0.f;
           o[e] = jg + tq[rq * TP + col + e];
         }
-        *reinterpret_cast<uint4*>(p.dq + grow * D + col) = pack8(o);
+        if (grow >= 0) *reinterpret_cast<uint4*>(p.dq + grow * D + col) = pack8(o);
         if (p.dq_part) {  // SlaGradients::dq and ::dq_feat (f32)
           float4* dqs = reinterpret_cast<float4*>(p.dq_part + grow * D + col);
           float4* dqf = reinterpret_cast<float4*>(p.dqf_part + grow * D + col);
@@ -792,6 +795,7 @@ void launch_bwd_lin(const Dims& Dm, const void* q, const void* w, const void* o_
                     __nv_bfloat16* dqphi, bool ds_external, cudaStream_t st) {
   BwdParams p{};
   p.ds_external = ds_external;
+  p.rl = Dm.rl;
   p.marg_cnt = s.marg_cnt;
   p.Z = s.Z;
   p.Ds_out = Ds;
@@ -805,16 +809,15 @@ void launch_bwd_lin(const Dims& Dm, const void* q, const void* w, const void* o_
   p.Tn = Dm.Tn;
   p.H = int(Dm.H);
   p.phi = Dm.phi;
-  const uint64_t rows = uint64_t(Dm.U) * Dm.N;
   CUtensorMap tq, tdo, tw, th, tos, tol, tgh;
   auto go = [&](auto kern, int bytes, auto dd) {
     constexpr int D = decltype(dd)::value;
-    make_tmap_bf16(&tq, q, D, rows, 1, D, 0, 64);
-    make_tmap_bf16(&tdo, d_out, D, rows, 1, D, 0, 64);
+    make_tmap_rows(&tq, q, D, Dm.U, Dm.N, p.rl, 64);
+    make_tmap_rows(&tdo, d_out, D, Dm.U, Dm.N, p.rl, 64);
     make_tmap_bf16(&tw, w, D, uint64_t(Dm.H) * D, 1, D, 0, D);
     make_tmap_bf16(&th, s.Hb, D, uint64_t(Dm.U) * Dm.Tm * D, 1, D, 0, D);
-    make_tmap_bf16(&tos, o_s, D, rows, 1, D, 0, 64);
-    make_tmap_bf16(&tol, o_l, D, rows, 1, D, 0, 64);
+    make_tmap_rows(&tos, o_s, D, Dm.U, Dm.N, p.rl, 64);
+    make_tmap_rows(&tol, o_l, D, Dm.U, Dm.N, p.rl, 64);
     make_tmap_bf16(&tgh, gH, D, uint64_t(Dm.U) * Dm.Tm * D, 1, D, 0, D);  // dH_i boxes [D rows][64]
     SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     launch_pdl(kern, dim3(Dm.Tm, unsigned(Dm.U)), kLinThreads, bytes, st, tq, tdo, tw, th, tos, tol, tgh, p);
@@ -830,6 +833,7 @@ void launch_bwd_rows(const Dims& Dm, const void* q, const void* k, const void* v
                      const void* d_out, void* dq, const StateBufs& s, const float* Ds,
                      const __nv_bfloat16* dqphi, float* dq_part, float* dqf_part, cudaStream_t st) {
   BwdParams p{};
+  p.rl = Dm.rl;
   p.dq_part = dq_part;
   p.dqf_part = dqf_part;
   p.crit_cnt = s.crit_cnt;
@@ -845,14 +849,13 @@ void launch_bwd_rows(const Dims& Dm, const void* q, const void* k, const void* v
   p.scale = float(Dm.inv_sqrt_d);
   p.scale_log2 = float(Dm.inv_sqrt_d * 1.4426950408889634);
   p.phi = Dm.phi;
-  const uint64_t rows = uint64_t(Dm.U) * Dm.N, krows = uint64_t(Dm.U) * Dm.Nk;
   CUtensorMap tq, tdo, tk, tv;
   auto go = [&](auto kern, int bytes, auto dd) {
     constexpr int D = decltype(dd)::value;
-    make_tmap_bf16(&tq, q, D, rows, 1, D, 0, 64);
-    make_tmap_bf16(&tdo, d_out, D, rows, 1, D, 0, 64);
-    make_tmap_bf16(&tk, k, D, krows, 1, D, 0, 64);
-    make_tmap_bf16(&tv, v, D, krows, 1, D, 0, 64);
+    make_tmap_rows(&tq, q, D, Dm.U, Dm.N, p.rl, 64);
+    make_tmap_rows(&tdo, d_out, D, Dm.U, Dm.N, p.rl, 64);
+    make_tmap_rows(&tk, k, D, Dm.U, Dm.Nk, p.rl, 64);
+    make_tmap_rows(&tv, v, D, Dm.U, Dm.Nk, p.rl, 64);
     SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
     const long long items = (long long)Dm.U * Dm.Tm;
     p.items = items;

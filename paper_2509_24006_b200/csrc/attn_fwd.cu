@@ -70,6 +70,7 @@ struct FwdParams {
   int has_w;
   int phi;
   int kv_last;  // valid keys in the last key block (64 unless ragged N)
+  RowLayout rl; // the caller's q, k, v, o, o_s, o_l, lse (read / written in place)
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -118,7 +119,6 @@ __global__ void __launch_bounds__(192, 2)
   const int* list = p.crit_idx + urow * p.Tn;
   const bool has_lin = p.marg_cnt[urow] > 0;
   const bool has_w = p.has_w != 0;
-  const int row0 = int(u * p.N) + i * 64;  // row in the [U*N, D] view
   const bool dbg = blockIdx.x == 100 && blockIdx.y == 6;
   fts(dbg && threadIdx.x == 0, 127);
 
@@ -148,7 +148,7 @@ __global__ void __launch_bounds__(192, 2)
       // continues with K(0), H_i, ...)
       tc::mbar_expect_tx(q_full, L::kQ);
 #pragma unroll
-      for (int c = 0; c < NC; ++c) tc::tma_load_3d(sQ + c * 8192, &tmQ, q_full, 64 * c, row0, 0);
+      for (int c = 0; c < NC; ++c) tc::tma_load_rows(sQ + c * 8192, &tmQ, q_full, 64 * c, u, i * 64, p.N, p.rl);
     }
     __syncwarp();
     tc::tmem_alloc<256>(tmem_slot);
@@ -174,10 +174,10 @@ __global__ void __launch_bounds__(192, 2)
         return base + s * L::kTile;
       };
       auto load_kv = [&](const CUtensorMap* tm, uint64_t* full, uint64_t* empty, uint8_t* base, int& it, int t) {
-        const int kv_row = int(u * p.N) + list[t] * 64;
+        const int kv_r = list[t] * 64;  // key row within the unit
         uint8_t* dst = take(full, empty, base, it, L::kTile);
 #pragma unroll
-        for (int c = 0; c < NC; ++c) tc::tma_load_3d(dst + c * 8192, tm, full + (it % RS), 64 * c, kv_row, 0);
+        for (int c = 0; c < NC; ++c) tc::tma_load_rows(dst + c * 8192, tm, full + (it % RS), 64 * c, u, kv_r, p.N, p.rl);
         ++it;
       };
       if (cnt > 0) load_kv(&tmK, k_full, k_empty, sK, kit, 0);
@@ -287,7 +287,6 @@ __global__ void __launch_bounds__(192, 2)
     const int r = 16 * q4 + (lane & 15);
     const int hh = lane >> 4;
     const uint32_t lane_base = uint32_t(32 * q4) << 16;
-    const long long grow = (long long)row0 + r;  // global row in [U*N, D]
     constexpr int DH = D / 2;                    // columns per half row
     auto dcol = [&](int c0) { return hh * DH + c0; };  // first column of chunk c0 of my half
     if (has_lin) {  // Z_i -> smem (one coalesced row instead of per-thread dependent loads)
@@ -474,7 +473,10 @@ __global__ void __launch_bounds__(192, 2)
       }
       if (has_w) tc::tmem_st32_x2<DH>(tO + lane_base + c0, o);
     }
-    if (hh == 0) p.lse[grow] = l > 0.f ? (m_used + __log2f(l)) * 0.69314718055994531f : kLseSentinel;
+    if (hh == 0) {  // the caller's lse row (none past a ragged N)
+      const long long cr = caller_row(p.rl, u, (long long)i * 64 + r, p.N);
+      if (cr >= 0) p.lse[cr] = l > 0.f ? (m_used + __log2f(l)) * 0.69314718055994531f : kLseSentinel;
+    }
     if (has_w) {
       tc::tmem_st_wait();
       // X <- O^l (bf16), the A operand of O^l W: my half row, from registers
@@ -523,9 +525,9 @@ __global__ void __launch_bounds__(192, 2)
     if (threadIdx.x == 64) {
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
-        tc::tma_store_3d(&tmOs, sQ + c * 8192, 64 * c, row0, 0);
-        tc::tma_store_3d(&tmOl, sPX + c * 8192, 64 * c, row0, 0);
-        if (has_w) tc::tma_store_3d(&tmO, sV + c * 8192, 64 * c, row0, 0);
+        tc::tma_store_rows(&tmOs, sQ + c * 8192, 64 * c, u, i * 64, p.N, p.rl);
+        tc::tma_store_rows(&tmOl, sPX + c * 8192, 64 * c, u, i * 64, p.N, p.rl);
+        if (has_w) tc::tma_store_rows(&tmO, sV + c * 8192, 64 * c, u, i * 64, p.N, p.rl);
       }
       tc::bulk_commit();
       tc::bulk_wait_read<0>();  // smem may be released; the writes complete with the grid
@@ -541,20 +543,19 @@ template <int D>
 void launch_t(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
               const __nv_bfloat16* Hb, FwdParams p, cudaStream_t st) {
   CUtensorMap tq, tk, tv, th, tw;
-  const uint64_t rows = uint64_t(Dm.U) * Dm.N, krows = uint64_t(Dm.U) * Dm.Nk;
-  make_tmap_bf16(&tq, q, D, rows, 1, D, 0, 64);
-  make_tmap_bf16(&tk, k, D, krows, 1, D, 0, 64);
-  make_tmap_bf16(&tv, v, D, krows, 1, D, 0, 64);
+  make_tmap_rows(&tq, q, D, Dm.U, Dm.N, p.rl, 64);
+  make_tmap_rows(&tk, k, D, Dm.U, Dm.Nk, p.rl, 64);
+  make_tmap_rows(&tv, v, D, Dm.U, Dm.Nk, p.rl, 64);
   make_tmap_bf16(&th, Hb, D, uint64_t(Dm.U) * Dm.Tm * D, 1, D, 0, D);
   if (w)
     make_tmap_bf16(&tw, w, D, uint64_t(Dm.H) * D, 1, D, 0, D);
   else
     tw = th;
   CUtensorMap to, tos, tol;  // output boxes [64 rows][64 cols]
-  make_tmap_bf16(&tos, p.o_s, D, rows, 1, D, 0, 64);
-  make_tmap_bf16(&tol, p.o_l, D, rows, 1, D, 0, 64);
+  make_tmap_rows(&tos, p.o_s, D, Dm.U, Dm.N, p.rl, 64);
+  make_tmap_rows(&tol, p.o_l, D, Dm.U, Dm.N, p.rl, 64);
   if (p.o)
-    make_tmap_bf16(&to, p.o, D, rows, 1, D, 0, 64);
+    make_tmap_rows(&to, p.o, D, Dm.U, Dm.N, p.rl, 64);
   else
     to = tos;
   auto kern = k_attn_fwd<D>;
@@ -584,6 +585,7 @@ void launch_attn_fwd(const Dims& Dm, const void* q, const void* k, const void* v
   p.has_w = (w != nullptr && o != nullptr) ? 1 : 0;
   p.phi = Dm.phi;
   p.kv_last = int(Dm.Nk_valid - (long long)(Dm.Tn - 1) * 64);
+  p.rl = Dm.rl;
   if (Dm.d == 128)
     launch_t<128>(Dm, q, k, v, w, s.Hb, p, st);
   else

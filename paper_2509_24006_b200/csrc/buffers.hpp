@@ -59,11 +59,7 @@ struct WorkBufs {
   __nv_bfloat16* z3b = nullptr;    // fast path: z_j / dZ_i split into 3 bf16 parts [U, T, 3d]
   __nv_bfloat16* wid = nullptr;    // fast path: identity W [H, d, d] (backward with independent cotangents)
   int* work_ctr = nullptr;         // fast path: dynamic work counter of the persistent columns pass
-  // ragged N: the caller's [U, N_valid, d] tensors padded to [U, N, d] (zero tail rows)
-  __nv_bfloat16* pad[11] = {};     // q k v o o_s o_l dO dq dk dv (bf16), see RaggedSlot
-  float* pad_lse = nullptr;        // [U, N]
 };
-enum RaggedSlot { kPQ, kPK, kPV, kPO, kPOs, kPOl, kPdO, kPdQ, kPdK, kPdV };
 
 // split-K factor of the fast path's dW GEMM: row chunks of 64*c rows, c | N/64, c <= 32
 inline int dw_chunk_tiles(const Dims& D) {
@@ -130,10 +126,6 @@ inline void carve_work(const Dims& D, bool fast, void* base, WorkBufs& w, size_t
     w.z3b = c.take<__nv_bfloat16>(U * T * 3 * d);
     w.wid = c.take<__nv_bfloat16>(size_t(D.H) * d * d);
     w.work_ctr = c.take<int>(4);
-    if (D.staged) {
-      for (int i = kPQ; i <= kPdV; ++i) w.pad[i] = c.take<__nv_bfloat16>(U * N * d);
-      w.pad_lse = c.take<float>(U * N);
-    }
   } else {  // generic SIMT path: f32 scratch for every intermediate
     w.qf = c.take<float>(U * N * d);
     w.kf = c.take<float>(U * N * d);

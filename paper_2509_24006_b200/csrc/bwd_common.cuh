@@ -107,6 +107,7 @@ struct BwdParams {
   int phi;
   const int8_t* labels;
   long long items;     // persistent kernels: work items of the launch
+  RowLayout rl;        // the caller's q, k, v, dO, o_s, o_l, lse, dq, dk, dv (in place)
   int* work;           // k_bwd_cols: dynamic work counter (zeroed before the launch)
   int ds_external;     // k_bwd_lin: D^s comes from k_rowdot (independent cotangents), not dO . O^s
   // optional SlaGradients parts (backward.hpp:10-16), f32 [U, N, D]; null: not written

@@ -38,16 +38,16 @@ __global__ void k_check_finite(const In* __restrict__ x, long long total,
 // ---------------------------------------------------------------------------------------
 template <typename R, typename In>
 __global__ void k_pool(const In* __restrict__ x, R* __restrict__ out, long long N, int d, int b,
-                       int T, long long n_valid) {
+                       int T, long long n_valid, RowLayout rl) {
   const long long u = blockIdx.y;
   const int g = blockIdx.x;
-  const In* base = x + (u * N + (long long)g * b) * d;
   // ragged N (SLA_B200_FLAG_RAGGED): the last block's mean is over its valid rows only
   const long long left = n_valid - (long long)g * b;
   const int rows = left < b ? int(left) : b;
   for (int c = threadIdx.x; c < d; c += blockDim.x) {
     R acc = R(0);
-    for (int r = 0; r < rows; ++r) acc = add_rn(acc, R(to_f(base[(long long)r * d + c])));
+    for (int r = 0; r < rows; ++r)
+      acc = add_rn(acc, R(to_f(x[caller_row(rl, u, (long long)g * b + r, N) * d + c])));
     out[(u * T + g) * d + c] = div_rn(acc, R(rows));
   }
 }
@@ -60,7 +60,7 @@ __global__ void __launch_bounds__(32) k_pool2_bf16(const __nv_bfloat16* __restri
                                                    const __nv_bfloat16* __restrict__ k,
                                                    R* __restrict__ pq, R* __restrict__ pk, long long Nq,
                                                    long long Nk, int d, int b, int Tq, int Tk,
-                                                   long long nq_valid, long long nk_valid) {
+                                                   long long nq_valid, long long nk_valid, RowLayout rl) {
   pdl_entry();  // launched by launch_pdl
   const long long u = blockIdx.y;
   const int g = blockIdx.x;
@@ -69,13 +69,12 @@ __global__ void __launch_bounds__(32) k_pool2_bf16(const __nv_bfloat16* __restri
   const long long N = blockIdx.z ? Nk : Nq, n_valid = blockIdx.z ? nk_valid : nq_valid;
   const int T = blockIdx.z ? Tk : Tq;
   if (g >= T) return;
-  const __nv_bfloat16* base = x + (u * N + (long long)g * b) * d;
   const long long left = n_valid - (long long)g * b;
   const int rows = left < b ? int(left) : b;
   for (int c = 4 * threadIdx.x; c < d; c += 128) {
     R a0 = R(0), a1 = R(0), a2 = R(0), a3 = R(0);
     for (int r = 0; r < rows; ++r) {
-      const uint2 v = *reinterpret_cast<const uint2*>(base + (long long)r * d + c);
+      const uint2 v = *reinterpret_cast<const uint2*>(x + caller_row(rl, u, (long long)g * b + r, N) * d + c);
       const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
       const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
       a0 = add_rn(a0, R(f0.x));
@@ -903,7 +902,7 @@ static void check_finite_t(const In* x, long long total, long long* slot, cudaSt
 
 void launch_check_finite(const Dims& D, int dtype, const void* x, long long* slot,
                          cudaStream_t st) {
-  const long long total = D.U * D.N * D.d;
+  const long long total = D.U * D.N_valid * D.d;  // the caller's elements (ragged: N_valid rows)
   if (dtype == 0)
     check_finite_t(static_cast<const __nv_bfloat16*>(x), total, slot, st);
   else
@@ -920,15 +919,15 @@ static bool classify_t(const Dims& D, const In* q, const In* k, const StateBufs&
   if constexpr (std::is_same<In, __nv_bfloat16>::value) {
     if (D.d % 4 == 0 && D.bq == D.bkv) {
       launch_pdl(k_pool2_bf16<R>, dim3(std::max(D.Tm, D.Tn), unsigned(D.U), 2), 32, 0, st, q, k, pq, pk, D.N, D.Nk,
-                 D.d, D.bq, D.Tm, D.Tn, D.N_valid, D.Nk_valid);
+                 D.d, D.bq, D.Tm, D.Tn, D.N_valid, D.Nk_valid, D.rl);
       check_launch("k_pool", st);
       pooled = true;
     }
   }
   if (!pooled) {
-    k_pool<R, In><<<dim3(D.Tm, unsigned(D.U)), pt, 0, st>>>(q, pq, D.N, D.d, D.bq, D.Tm, D.N_valid);
+    k_pool<R, In><<<dim3(D.Tm, unsigned(D.U)), pt, 0, st>>>(q, pq, D.N, D.d, D.bq, D.Tm, D.N_valid, D.rl);
     check_launch("k_pool(q)", st);
-    k_pool<R, In><<<dim3(D.Tn, unsigned(D.U)), pt, 0, st>>>(k, pk, D.Nk, D.d, D.bkv, D.Tn, D.Nk_valid);
+    k_pool<R, In><<<dim3(D.Tn, unsigned(D.U)), pt, 0, st>>>(k, pk, D.Nk, D.d, D.bkv, D.Tn, D.Nk_valid, D.rl);
     check_launch("k_pool(k)", st);
   }
   const size_t smem = classify_smem_bytes(D, sizeof(R) == 8);

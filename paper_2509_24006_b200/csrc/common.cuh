@@ -10,6 +10,26 @@
 
 namespace slab {
 
+// Row layout of a CALLER tensor [*, rows, row_elems] that the kernels address as (unit u, row r):
+//   0: unit-major with the kernels' row count N per unit (flat row u * N + r)
+//   1: unit-major ragged, nv rows per unit (SLA_B200_FLAG_RAGGED): rows r >= nv do not exist
+//   2: token-major [B, nv, H, .] (SLA_B200_FLAG_BNHD): unit u = b * H + h
+// Tensor maps over modes 1 / 2 are 3-D [U][nv][d] / 4-D [B][nv][H][d]: TMA zero-fills the rows
+// r >= nv of a box on loads and clips them on stores, so the kernels read and write the caller's
+// tensors in place (no padded copies).
+struct RowLayout {
+  int mode = 0;
+  int H = 1;
+  long long nv = 0;
+};
+// element-row index of (u, r) in the caller tensor, -1 when the row does not exist
+__host__ __device__ __forceinline__ long long caller_row(const RowLayout& rl, long long u, long long r, long long N) {
+  if (rl.mode == 0) return u * N + r;
+  if (r >= rl.nv) return -1;
+  if (rl.mode == 1) return u * rl.nv + r;
+  return ((u / rl.H) * rl.nv + r) * rl.H + (u % rl.H);
+}
+
 // Derived problem dimensions (resolved once on the host from sla_b200_problem).
 struct Dims {
   int64_t U;     // units = batch * heads
@@ -17,6 +37,7 @@ struct Dims {
   int64_t N;     // query rows per unit in the kernels' buffers (sequence length; padded if ragged)
   int64_t Nk;    // key / value rows per unit (== N unless a rectangular problem, sla_b200_problem.n_kv)
   int64_t Nk_valid;  // valid key rows per unit (== Nk unless ragged)
+  RowLayout rl;      // layout of the caller's [*, N, d] tensors and lse (mode 0: the kernels' own)
   int64_t N_valid;  // rows per unit in the caller's tensors (== N unless SLA_B200_FLAG_RAGGED)
   bool bnhd;        // caller tensors are [B, N, H, d] (SLA_B200_FLAG_BNHD)
   bool staged;      // ragged or bnhd: kernels run on unit-major zero-padded workspace copies

@@ -39,7 +39,7 @@ __global__ void k_row_stats(const int8_t* __restrict__ labels, long long rows, i
 template <typename T>
 __global__ void k_lin_rows(const T* __restrict__ q, const float* __restrict__ Z, int z3,
                            const int4* __restrict__ stats, int N, int n_valid, int d, int bq,
-                           int Tm, int phi, int* __restrict__ lin_rows) {
+                           int Tm, int phi, int* __restrict__ lin_rows, RowLayout rl) {
   const int i = blockIdx.x, u = blockIdx.y;
   const long long urow = (long long)u * Tm + i;
   if (threadIdx.x == 0) lin_rows[urow] = 0;
@@ -51,7 +51,7 @@ __global__ void k_lin_rows(const T* __restrict__ q, const float* __restrict__ Z,
   for (int rr = warp; rr < bq; rr += nw) {
     const int r = i * bq + rr;
     if (r >= n_valid) break;
-    const T* qr = q + ((long long)u * N + r) * d;
+    const T* qr = q + caller_row(rl, u, r, N) * d;
     float mx = -INFINITY, se = 0.f;
     if (phi == 2) {  // per-row softmax over the d features (feature_map.cpp:22-40)
       for (int a = lane; a < d; a += 32) mx = fmaxf(mx, to_f(qr[a]));
@@ -84,10 +84,10 @@ void launch_lin_rows(const Dims& D, int dtype, const void* q, const float* Z, bo
   const dim3 grid(unsigned(D.Tm), unsigned(D.U));
   if (dtype == 0)
     k_lin_rows<__nv_bfloat16><<<grid, 256, 0, st>>>(static_cast<const __nv_bfloat16*>(q), Z, z3, stats,
-                                                   int(D.N), int(D.N_valid), D.d, D.bq, D.Tm, D.phi, lin_rows);
+                                                   int(D.N), int(D.N_valid), D.d, D.bq, D.Tm, D.phi, lin_rows, D.rl);
   else
     k_lin_rows<float><<<grid, 256, 0, st>>>(static_cast<const float*>(q), Z, z3, stats, int(D.N),
-                                           int(D.N_valid), D.d, D.bq, D.Tm, D.phi, lin_rows);
+                                           int(D.N_valid), D.d, D.bq, D.Tm, D.phi, lin_rows, D.rl);
   check_launch("k_lin_rows", st);
 }
 

@@ -20,7 +20,7 @@ template <int D>
 __global__ void __launch_bounds__(256) k_phi_kz(const __nv_bfloat16* __restrict__ k,
                                                 __nv_bfloat16* __restrict__ kfb,
                                                 __nv_bfloat16* __restrict__ z3b, long long N, int Tn, int phi,
-                                                long long n_valid) {
+                                                long long n_valid, RowLayout rl) {
   pdl_entry();  // launched by launch_pdl
   constexpr int C = D / 32;
   __shared__ float zpart[8][D];
@@ -34,10 +34,12 @@ __global__ void __launch_bounds__(256) k_phi_kz(const __nv_bfloat16* __restrict_
   using V = typename std::conditional<C == 4, uint2, uint32_t>::type;
   static_assert(C == 2 || C == 4, "d in {64, 128}");
   const long long rin0 = (long long)j * 64 + warp * 8;
-  const V* src = reinterpret_cast<const V*>(k + (u * N + rin0) * D) + lane;
   V raw[8];
 #pragma unroll
-  for (int rr = 0; rr < 8; ++rr) raw[rr] = src[rr * (D / C)];
+  for (int rr = 0; rr < 8; ++rr) {  // the caller's K in place (rows past a ragged N do not exist)
+    const long long cr = caller_row(rl, u, rin0 + rr, N);
+    raw[rr] = cr >= 0 && rin0 + rr < n_valid ? reinterpret_cast<const V*>(k + cr * D)[lane] : V{};
+  }
 #pragma unroll
   for (int rr = 0; rr < 8; ++rr) {
     const long long rin = rin0 + rr;  // row within the unit
@@ -120,13 +122,14 @@ __global__ void k_fill_identity(__nv_bfloat16* __restrict__ w, long long total, 
 
 // out[r] = <a_r, b_r> over d columns, one warp per row (bf16 in, f32 sum)
 __global__ void k_rowdot(const __nv_bfloat162* __restrict__ a, const __nv_bfloat162* __restrict__ b,
-                         float* __restrict__ out, long long rows, int d2) {
-  const long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+                         float* __restrict__ out, long long rows, int d2, long long N, RowLayout rl) {
+  const long long r = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;  // [U, N] kernel row
   const int lane = threadIdx.x & 31;
   if (r >= rows) return;
+  const long long cr = caller_row(rl, r / N, r % N, N);  // the caller's a, b in place
   float acc = 0.f;
-  for (int j = lane; j < d2; j += 32) {
-    const float2 x = __bfloat1622float2(a[r * d2 + j]), y = __bfloat1622float2(b[r * d2 + j]);
+  for (int j = lane; cr >= 0 && j < d2; j += 32) {
+    const float2 x = __bfloat1622float2(a[cr * d2 + j]), y = __bfloat1622float2(b[cr * d2 + j]);
     acc = fmaf(x.x, y.x, fmaf(x.y, y.y, acc));
   }
   acc = warp_sum(acc);
@@ -229,7 +232,7 @@ void launch_rowdot(const Dims& D, const void* a, const void* b, float* out, cuda
   const long long rows = D.U * D.N;
   k_rowdot<<<unsigned((rows * 32 + 255) / 256), 256, 0, st>>>(static_cast<const __nv_bfloat162*>(a),
                                                              static_cast<const __nv_bfloat162*>(b), out, rows,
-                                                             D.d / 2);
+                                                             D.d / 2, D.N, D.rl);
   check_launch("k_rowdot", st);
 }
 
@@ -258,6 +261,10 @@ void launch_dw_fast(const Dims& Dm, const void* o_l, const void* d_out, float* d
   g.b_batch = KC * d;
   g.c_batch = (long long)d * d;
   g.name = "gemm_dw";
+  g.a_rl = Dm.rl;  // O^l and dO in place: chunk c of unit u
+  g.b_rl = Dm.rl;
+  g.a_rpu = g.b_rpu = chunks;
+  g.units = Dm.U;
   launch_gemm(g, ds);
   launch_pdl(k_reduce_dw, dim3((d * d + 255) / 256, unsigned(Dm.H)), 256, 0, ds, (const float*)wb.dwp, chunks,
              (long long)Dm.B, (long long)Dm.H, d * d, dw);
@@ -270,10 +277,10 @@ void fast_summaries(const Dims& Dm, const void* k, const void* v, const WorkBufs
   const int d = Dm.d;
   if (d == 128)
     launch_pdl(k_phi_kz<128>, dim3(Dm.Tn, unsigned(Dm.U)), 256, 0, st,
-        static_cast<const __nv_bfloat16*>(k), wb.kfb, wb.z3b, Dm.Nk, Dm.Tn, Dm.phi, Dm.Nk_valid);
+        static_cast<const __nv_bfloat16*>(k), wb.kfb, wb.z3b, Dm.Nk, Dm.Tn, Dm.phi, Dm.Nk_valid, Dm.rl);
   else
     launch_pdl(k_phi_kz<64>, dim3(Dm.Tn, unsigned(Dm.U)), 256, 0, st,
-        static_cast<const __nv_bfloat16*>(k), wb.kfb, wb.z3b, Dm.Nk, Dm.Tn, Dm.phi, Dm.Nk_valid);
+        static_cast<const __nv_bfloat16*>(k), wb.kfb, wb.z3b, Dm.Nk, Dm.Tn, Dm.phi, Dm.Nk_valid, Dm.rl);
   check_launch("k_phi_kz", st);
   // h_j = phi(K_j)^T V_j: batch = every key block, M = N = d, K = 64 tokens
   GemmArgs g{};
@@ -294,6 +301,9 @@ void fast_summaries(const Dims& Dm, const void* k, const void* v, const WorkBufs
   g.b_batch = 64LL * d;
   g.c_batch = (long long)d * d;
   g.name = "gemm_summaries";
+  g.b_rl = Dm.rl;  // V in place: key block j of unit u is chunk j of u's rows
+  g.b_rpu = Dm.Tn;
+  g.units = Dm.U;
   launch_gemm(g, st);
 }
 

@@ -45,7 +45,8 @@ template <int BM, int BN, bool A_MN, bool B_MN, typename OutT, bool MC = false>
 __global__ void __launch_bounds__(224, 1)
     k_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
            const __grid_constant__ CUtensorMap tc_out,
-           OutT* __restrict__ C, int M, int N, int K, int batch, long long c_batch, int ldc) {
+           OutT* __restrict__ C, int M, int N, int K, int batch, long long c_batch, int ldc,
+           RowLayout arl, RowLayout brl, int a_rpu, int b_rpu) {
   pdl_entry();  // launched by launch_pdl
   using L = GemmSmem<BM, BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -110,7 +111,11 @@ __global__ void __launch_bounds__(224, 1)
           const int k0 = kb * kBK;
           if (loads_a) {
             tc::mbar_expect_tx(&full[s], L::kA);
-            if (A_MN) {
+            if (A_MN && arl.mode) {  // a caller tensor in place: chunk b % a_rpu of unit b / a_rpu
+#pragma unroll
+              for (int c = 0; c < BM / 64; ++c)
+                tc::tma_load_rows(sa + c * 8192, &ta, &full[s], m0 + 64 * c, b / a_rpu, (b % a_rpu) * K + k0, 0, arl);
+            } else if (A_MN) {
 #pragma unroll
               for (int c = 0; c < BM / 64; ++c) tc::tma_load_3d(sa + c * 8192, &ta, &full[s], m0 + 64 * c, k0, b);
             } else {
@@ -123,6 +128,10 @@ __global__ void __launch_bounds__(224, 1)
 #pragma unroll
               for (int c = rank * (BN / 128); c < (rank + 1) * (BN / 128); ++c)
                 tc::tma_load_3d_mc(sb + c * 8192, &tb, &full[s], n0 + 64 * c, k0, b, uint16_t(3));
+            } else if (B_MN && brl.mode) {
+#pragma unroll
+              for (int c = 0; c < BN / 64; ++c)
+                tc::tma_load_rows(sb + c * 8192, &tb, &full[s], n0 + 64 * c, b / b_rpu, (b % b_rpu) * K + k0, 0, brl);
             } else if (B_MN) {
 #pragma unroll
               for (int c = 0; c < BN / 64; ++c) tc::tma_load_3d(sb + c * 8192, &tb, &full[s], n0 + 64 * c, k0, b);
@@ -272,11 +281,17 @@ template <int BM, int BN, bool A_MN, bool B_MN, typename OutT, bool MC = false>
 void launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
   CUtensorMap ta, tb;
   // A: K-major -> tensor [batch][M][K], box [BM][64]; M-major -> [batch][K][M], box [64][64]
-  if (A_MN)
+  if (g.a_rl.mode && !A_MN) throw InvalidArgument("sla_b200 gemm: in-place A must be M-major");
+  if (g.b_rl.mode && !B_MN) throw InvalidArgument("sla_b200 gemm: in-place B must be N-major");
+  if (g.a_rl.mode)
+    make_tmap_rows(&ta, g.A, g.M, g.units, 0, g.a_rl, 64);
+  else if (A_MN)
     make_tmap_bf16(&ta, g.A, g.M, g.K, g.batch, g.lda, g.a_batch, 64);
   else
     make_tmap_bf16(&ta, g.A, g.K, g.M, g.batch, g.lda, g.a_batch, BM);
-  if (B_MN)
+  if (g.b_rl.mode)
+    make_tmap_rows(&tb, g.B, g.N, g.units, 0, g.b_rl, 64);
+  else if (B_MN)
     make_tmap_bf16(&tb, g.B, g.N, g.K, g.batch, g.ldb, g.b_batch, 64);
   else
     make_tmap_bf16(&tb, g.B, g.K, g.N, g.batch, g.ldb, g.b_batch, BN);
@@ -305,10 +320,12 @@ void launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
     attr[1].val.programmaticStreamSerializationAllowed = SLAB_PDL;
     cfg.attrs = attr;
     cfg.numAttrs = 2;
-    cudaLaunchKernelEx(&cfg, kern, ta, tb, tcm, static_cast<OutT*>(g.C), g.M, g.N, g.K, g.batch, g.c_batch, g.ldc);
+    cudaLaunchKernelEx(&cfg, kern, ta, tb, tcm, static_cast<OutT*>(g.C), g.M, g.N, g.K, g.batch, g.c_batch, g.ldc,
+                       g.a_rl, g.b_rl, g.a_rpu, g.b_rpu);
   } else {
     const int grid = int(std::min<long long>(tiles, sms));
-    launch_pdl(kern, grid, 224, smem, st, ta, tb, tcm, static_cast<OutT*>(g.C), g.M, g.N, g.K, g.batch, g.c_batch, g.ldc);
+    launch_pdl(kern, grid, 224, smem, st, ta, tb, tcm, static_cast<OutT*>(g.C), g.M, g.N, g.K, g.batch, g.c_batch, g.ldc,
+               g.a_rl, g.b_rl, g.a_rpu, g.b_rpu);
   }
   check_launch(g.name ? g.name : "k_gemm", st);
 }
@@ -349,6 +366,23 @@ void dispatch_tile(const GemmArgs& g, cudaStream_t st) {
 }
 
 }  // namespace
+
+bool make_tmap_rows(CUtensorMap* map, const void* base, uint64_t d, long long U, long long N,
+                    const RowLayout& rl, uint32_t box_rows) {
+  if (rl.mode == 0) return make_tmap_bf16(map, base, d, uint64_t(U) * uint64_t(N), 1, d, 0, box_rows);
+  if (rl.mode == 1) return make_tmap_bf16(map, base, d, uint64_t(rl.nv), uint64_t(U), d, uint64_t(rl.nv) * d, box_rows);
+  const uint64_t H = uint64_t(rl.H), B = uint64_t(U) / H, nv = uint64_t(rl.nv);
+  cuuint64_t dims[4] = {d, H, nv, B};
+  cuuint64_t strides[3] = {d * 2, H * d * 2, nv * H * d * 2};
+  cuuint32_t box[4] = {64, 1, box_rows, 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    throw CudaError("cuTensorMapEncodeTiled (4-D) failed (" + std::to_string(int(r)) + ")");
+  return true;
+}
 
 bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t outer,
                     uint64_t row_stride_elems, uint64_t outer_stride_elems, uint32_t box_rows) {

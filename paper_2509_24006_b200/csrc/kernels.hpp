@@ -52,6 +52,12 @@ struct GemmArgs {
   long long lda, ldb, ldc;          // row strides in elements
   long long a_batch, b_batch, c_batch;  // batch strides in elements
   const char* name;
+  // Caller tensors read in place (RowLayout mode 1 / 2, M- / N-major operands only): batch b is
+  // K-row chunk b % rpu of unit b / rpu -- rows (b % rpu) * K + k of a [U][nv][d] or
+  // [B][nv][H][d] tensor, rows >= nv zero-filled by TMA.  `units` = U.
+  RowLayout a_rl, b_rl;
+  int a_rpu = 1, b_rpu = 1;
+  long long units = 1;
 };
 void launch_gemm(const GemmArgs& g, cudaStream_t st);
 

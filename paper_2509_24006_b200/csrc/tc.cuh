@@ -108,6 +108,15 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
       : "memory");
 }
 
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+
 // the same load multicast to the CTAs of `mask` in the cluster (same smem offset and barrier
 // offset in each; every destination's barrier receives complete_tx for the bytes it got)
 __device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
@@ -134,6 +143,28 @@ __device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void*
           reinterpret_cast<uint64_t>(map)),
       "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
       : "memory");
+}
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void* src, int c0, int c1, int c2,
+                                             int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5}], [%1];" ::"l"(
+          reinterpret_cast<uint64_t>(map)),
+      "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+// A [64-row x 64-col] box of a caller tensor at (column c, unit u, row r) under its RowLayout
+// (make_tmap_rows builds the matching map)
+__device__ __forceinline__ void tma_load_rows(void* dst, const CUtensorMap* map, uint64_t* bar, int c, long long u,
+                                              int r, long long N, const RowLayout& rl) {
+  if (rl.mode == 0) tma_load_3d(dst, map, bar, c, int(u * N + r), 0);
+  else if (rl.mode == 1) tma_load_3d(dst, map, bar, c, r, int(u));
+  else tma_load_4d(dst, map, bar, c, int(u % rl.H), r, int(u / rl.H));
+}
+__device__ __forceinline__ void tma_store_rows(const CUtensorMap* map, const void* src, int c, long long u, int r,
+                                               long long N, const RowLayout& rl) {
+  if (rl.mode == 0) tma_store_3d(map, src, c, int(u * N + r), 0);
+  else if (rl.mode == 1) tma_store_3d(map, src, c, r, int(u));
+  else tma_store_4d(map, src, c, int(u % rl.H), r, int(u / rl.H));
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // wait until at most N committed bulk groups still READ their smem source
@@ -390,5 +421,9 @@ __host__ __device__ constexpr bool poly_slot(int e, int n) { return n > 0 && e %
 bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows,
                     uint64_t outer, uint64_t row_stride_elems, uint64_t outer_stride_elems,
                     uint32_t box_rows);
+// a caller tensor with rows of d bf16 under RowLayout rl (U units, N kernel rows per unit):
+// mode 0 [U*N][d], mode 1 [U][nv][d], mode 2 [B][nv][H][d]; boxes [box_rows][64 cols]
+bool make_tmap_rows(CUtensorMap* map, const void* base, uint64_t d, long long U, long long N,
+                    const RowLayout& rl, uint32_t box_rows);
 
 }  // namespace slab

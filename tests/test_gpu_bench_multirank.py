@@ -18,7 +18,10 @@ def _bench(*args):
     cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--config", "c1", "--steps", "2", "--warmup", "3",
            "--no-dense", "--no-cpu-baseline", "--no-e2e", *args]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
-    assert out.returncode == 0, out.stderr[-3000:]
+    if out.returncode != 0 and os.path.isdir(os.path.join(ROOT, "gpurun_out")):
+        with open(os.path.join(ROOT, "gpurun_out", "multirank_failure.log"), "w") as f:
+            f.write(out.stdout + "\n---- stderr ----\n" + out.stderr)
+    assert out.returncode == 0, out.stderr[:3000] + "\n...\n" + out.stderr[-2000:]
     return json.loads(out.stdout.strip().splitlines()[-1])
 
 
