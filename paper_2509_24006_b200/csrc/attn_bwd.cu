@@ -93,6 +93,8 @@ __global__ void __launch_bounds__(kColsThreads, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int j = blockIdx.x;
   const long long u = blockIdx.y;
+  const RowTma rt = row_tma(p.rl, u, p.N);
+  const RowMap rm = row_map(p.rl, u, p.N);
   const long long ucol = u * p.Tn + j;
   const int cnt = p.ccol_cnt[ucol];
   const int np = (cnt + 1) >> 1;
@@ -137,8 +139,8 @@ __global__ void __launch_bounds__(kColsThreads, 1)
       tc::mbar_expect_tx(kv_full, 2 * L::kT);
 #pragma unroll
       for (int c = 0; c < D / 64; ++c) {
-        tc::tma_load_rows(sK + c * 8192, &tmK, kv_full, 64 * c, u, j * 64, p.N, p.rl);
-        tc::tma_load_rows(sV + c * 8192, &tmV, kv_full, 64 * c, u, j * 64, p.N, p.rl);
+        tc::tma_load_rows(sK + c * 8192, &tmK, kv_full, 64 * c, j * 64, rt);
+        tc::tma_load_rows(sV + c * 8192, &tmV, kv_full, 64 * c, j * 64, rt);
       }
       if (np > 0) {
         const int r1 = l0 * 64, r2 = (cnt > 1 ? l1 : l0) * 64;  // query rows within the unit
@@ -148,9 +150,8 @@ __global__ void __launch_bounds__(kColsThreads, 1)
           tc::mbar_expect_tx(ring_full + it, L::kP);
 #pragma unroll
           for (int c = 0; c < D / 64; ++c) {
-            tc::tma_load_rows(sRing + it * L::kSlot + c * 16384, it ? &tmDO : &tmQ, ring_full + it, 64 * c, u, r1, p.N, p.rl);
-            tc::tma_load_rows(sRing + it * L::kSlot + c * 16384 + 8192, it ? &tmDO : &tmQ, ring_full + it, 64 * c, u, r2, p.N,
-                              p.rl);
+            tc::tma_load_rows(sRing + it * L::kSlot + c * 16384, it ? &tmDO : &tmQ, ring_full + it, 64 * c, r1, rt);
+            tc::tma_load_rows(sRing + it * L::kSlot + c * 16384 + 8192, it ? &tmDO : &tmQ, ring_full + it, 64 * c, r2, rt);
           }
         }
       }
@@ -189,8 +190,8 @@ __global__ void __launch_bounds__(kColsThreads, 1)
         uint64_t* fb = ring_full + (item % RS);
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
-          tc::tma_load_rows(dst + c * 16384, tm, fb, 64 * c, u, r1, p.N, p.rl);
-          tc::tma_load_rows(dst + c * 16384 + 8192, tm, fb, 64 * c, u, r2, p.N, p.rl);
+          tc::tma_load_rows(dst + c * 16384, tm, fb, 64 * c, r1, rt);
+          tc::tma_load_rows(dst + c * 16384 + 8192, tm, fb, 64 * c, r2, rt);
         }
       }
       if (has_lin && pid == 0) {  // dH_agg: the last item, D / 64 chunks of [D rows x 64]
@@ -333,7 +334,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
     float lse_n = 0.f, ds_n = 0.f;
     if (np > 0) {
       const long long r0 = row_of(0);
-      const long long c0r = caller_row(p.rl, u, r0 - u * p.N, p.N);  // the caller's lse in place
+      const long long c0r = rm.row(r0 - u * p.N);  // the caller's lse in place
       lse_n = c0r >= 0 ? p.lse[c0r] : 0.f;
       ds_n = p.Ds[r0];
     }
@@ -343,7 +344,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
       const float dss = ds_n * p.scale;  // D^s / sqrt(d)
       if (t + 1 < np) {
         const long long r1 = row_of(t + 1);
-        const long long c1r = caller_row(p.rl, u, r1 - u * p.N, p.N);
+        const long long c1r = rm.row(r1 - u * p.N);
         lse_n = c1r >= 0 ? p.lse[c1r] : 0.f;
         ds_n = p.Ds[r1];
       }
@@ -526,7 +527,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
 #pragma unroll
       for (int e = 0; e < 8; ++e) g[cc0 + e] = has_lin ? tkp[c * TP + col + e] + zas[col + e] : 0.f;
     }
-    const long long grow = caller_row(p.rl, u, (long long)j * 64 + c, p.N);  // -1: past a ragged N
+    const long long grow = rm.row((long long)j * 64 + c);  // -1: past a ragged N
     float jg[DQ];
     if (p.phi == 2) {
       float dot = 0.f;

@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(kLinThreads, 2)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x;
   const long long u = blockIdx.y;
+  const RowTma rt = row_tma(p.rl, u, p.N);
   const long long urow = u * p.Tm + i;
   const bool has_lin = p.marg_cnt[urow] > 0;
   const int row0 = int(u * p.N) + i * 64;
@@ -112,14 +113,14 @@ __global__ void __launch_bounds__(kLinThreads, 2)
       tc::mbar_expect_tx(qdo_full, 2 * L::kT);
 #pragma unroll
       for (int c = 0; c < D / 64; ++c) {
-        tc::tma_load_rows(sQ + c * 8192, &tmQ, qdo_full, 64 * c, u, i * 64, p.N, p.rl);
-        tc::tma_load_rows(sDO + c * 8192, &tmDO, qdo_full, 64 * c, u, i * 64, p.N, p.rl);
+        tc::tma_load_rows(sQ + c * 8192, &tmQ, qdo_full, 64 * c, i * 64, rt);
+        tc::tma_load_rows(sDO + c * 8192, &tmDO, qdo_full, 64 * c, i * 64, rt);
       }
       tc::mbar_expect_tx(o_full, 2 * L::kT);
 #pragma unroll
       for (int c = 0; c < D / 64; ++c) {
-        tc::tma_load_rows(sX + c * 8192, &tmOS, o_full, 64 * c, u, i * 64, p.N, p.rl);
-        tc::tma_load_rows(sDOL + c * 8192, &tmOL, o_full, 64 * c, u, i * 64, p.N, p.rl);
+        tc::tma_load_rows(sX + c * 8192, &tmOS, o_full, 64 * c, i * 64, rt);
+        tc::tma_load_rows(sDOL + c * 8192, &tmOL, o_full, 64 * c, i * 64, rt);
       }
       tc::mbar_expect_tx(w_full, D * D * 2);
       const int h = int(u % p.H);
@@ -449,6 +450,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
   for (long long item = blockIdx.x; item < p.items; item += gridDim.x, ++nit) {
   const int i = int(item % p.Tm);
   const long long u = item / p.Tm;
+  const RowTma rt = row_tma(p.rl, u, p.N);
+  const RowMap rm = row_map(p.rl, u, p.N);
   const long long urow = u * p.Tm + i;
   const int cnt = p.crit_cnt[urow];
   const int* list = p.crit_idx + urow * p.Tn;
@@ -467,8 +470,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
       tc::mbar_expect_tx(qdo_full, 2 * L::kT);
 #pragma unroll
       for (int c = 0; c < D / 64; ++c) {
-        tc::tma_load_rows(sQ + c * 8192, &tmQ, qdo_full, 64 * c, u, i * 64, p.N, p.rl);
-        tc::tma_load_rows(sDO + c * 8192, &tmDO, qdo_full, 64 * c, u, i * 64, p.N, p.rl);
+        tc::tma_load_rows(sQ + c * 8192, &tmQ, qdo_full, 64 * c, i * 64, rt);
+        tc::tma_load_rows(sDO + c * 8192, &tmDO, qdo_full, 64 * c, i * 64, rt);
       }
       if (np > 0) {
         const int r1 = l0 * 64, r2 = (cnt > 1 ? l1 : l0) * 64;  // key rows within the unit
@@ -480,13 +483,13 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         uint8_t* dv0 = sV + v0s * L::kP;
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
-          tc::tma_load_rows(dk0 + c * 16384, &tmK, k_full + k0s, 64 * c, u, r1, p.N, p.rl);
-          tc::tma_load_rows(dk0 + c * 16384 + 8192, &tmK, k_full + k0s, 64 * c, u, r2, p.N, p.rl);
+          tc::tma_load_rows(dk0 + c * 16384, &tmK, k_full + k0s, 64 * c, r1, rt);
+          tc::tma_load_rows(dk0 + c * 16384 + 8192, &tmK, k_full + k0s, 64 * c, r2, rt);
         }
 #pragma unroll
         for (int c = 0; c < D / 64; ++c) {
-          tc::tma_load_rows(dv0 + c * 16384, &tmV, v_full + v0s, 64 * c, u, r1, p.N, p.rl);
-          tc::tma_load_rows(dv0 + c * 16384 + 8192, &tmV, v_full + v0s, 64 * c, u, r2, p.N, p.rl);
+          tc::tma_load_rows(dv0 + c * 16384, &tmV, v_full + v0s, 64 * c, r1, rt);
+          tc::tma_load_rows(dv0 + c * 16384 + 8192, &tmV, v_full + v0s, 64 * c, r2, rt);
         }
       }
     }
@@ -521,8 +524,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
           uint8_t* dk = sK + ks * L::kP;
 #pragma unroll
           for (int c = 0; c < D / 64; ++c) {
-            tc::tma_load_rows(dk + c * 16384, &tmK, k_full + ks, 64 * c, u, r1, p.N, p.rl);
-            tc::tma_load_rows(dk + c * 16384 + 8192, &tmK, k_full + ks, 64 * c, u, r2, p.N, p.rl);
+            tc::tma_load_rows(dk + c * 16384, &tmK, k_full + ks, 64 * c, r1, rt);
+            tc::tma_load_rows(dk + c * 16384 + 8192, &tmK, k_full + ks, 64 * c, r2, rt);
           }
         } else {
           tc::mbar_wait(v_empty + vs, ((G / L::VS) & 1) ^ 1);
@@ -531,8 +534,8 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
           uint8_t* dv = sV + vs * L::kP;
 #pragma unroll
           for (int c = 0; c < D / 64; ++c) {
-            tc::tma_load_rows(dv + c * 16384, &tmV, v_full + vs, 64 * c, u, r1, p.N, p.rl);
-            tc::tma_load_rows(dv + c * 16384 + 8192, &tmV, v_full + vs, 64 * c, u, r2, p.N, p.rl);
+            tc::tma_load_rows(dv + c * 16384, &tmV, v_full + vs, 64 * c, r1, rt);
+            tc::tma_load_rows(dv + c * 16384 + 8192, &tmV, v_full + vs, 64 * c, r2, rt);
           }
         }
       }
@@ -618,7 +621,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
         gq[i] = *reinterpret_cast<const uint4*>(src + ((8 * i + 8 * sub) & (DQ - 1)));
     }
     if (tid < 64) {  // the caller's lse (0 for rows past a ragged N: their dO is zero-filled)
-      const long long cr = caller_row(p.rl, u, (long long)i * 64 + tid, p.N);
+      const long long cr = rm.row((long long)i * 64 + tid);
       s_lse2[tid] = cr >= 0 ? p.lse[cr] * 1.4426950408889634f : 0.f;
     }
     else if (tid < 128) s_ds[tid - 64] = p.Ds[(long long)row0 + tid - 64] * p.scale;  // D^s / sqrt(d)
@@ -750,7 +753,7 @@ __global__ void __launch_bounds__(kRowsThreads, 1)
     }
     named_sync(1, NCT);
     {
-      const long long grow = caller_row(p.rl, u, (long long)i * 64 + rq, p.N);  // -1: past a ragged N
+      const long long grow = rm.row((long long)i * 64 + rq);  // -1: past a ragged N
 #pragma unroll
       for (int cc0 = 0; cc0 < DQ; cc0 += 8) {
         const int col = c0 + rot(cc0);

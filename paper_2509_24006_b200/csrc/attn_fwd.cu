@@ -114,6 +114,8 @@ __global__ void __launch_bounds__(192, 2)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int i = blockIdx.x;
   const long long u = blockIdx.y;
+  const RowTma rt = row_tma(p.rl, u, p.N);
+  const RowMap rm = row_map(p.rl, u, p.N);
   const long long urow = u * p.Tm + i;
   const int cnt = p.crit_cnt[urow];
   const int* list = p.crit_idx + urow * p.Tn;
@@ -148,7 +150,7 @@ __global__ void __launch_bounds__(192, 2)
       // continues with K(0), H_i, ...)
       tc::mbar_expect_tx(q_full, L::kQ);
 #pragma unroll
-      for (int c = 0; c < NC; ++c) tc::tma_load_rows(sQ + c * 8192, &tmQ, q_full, 64 * c, u, i * 64, p.N, p.rl);
+      for (int c = 0; c < NC; ++c) tc::tma_load_rows(sQ + c * 8192, &tmQ, q_full, 64 * c, i * 64, rt);
     }
     __syncwarp();
     tc::tmem_alloc<256>(tmem_slot);
@@ -177,7 +179,7 @@ __global__ void __launch_bounds__(192, 2)
         const int kv_r = list[t] * 64;  // key row within the unit
         uint8_t* dst = take(full, empty, base, it, L::kTile);
 #pragma unroll
-        for (int c = 0; c < NC; ++c) tc::tma_load_rows(dst + c * 8192, tm, full + (it % RS), 64 * c, u, kv_r, p.N, p.rl);
+        for (int c = 0; c < NC; ++c) tc::tma_load_rows(dst + c * 8192, tm, full + (it % RS), 64 * c, kv_r, rt);
         ++it;
       };
       if (cnt > 0) load_kv(&tmK, k_full, k_empty, sK, kit, 0);
@@ -474,7 +476,7 @@ __global__ void __launch_bounds__(192, 2)
       if (has_w) tc::tmem_st32_x2<DH>(tO + lane_base + c0, o);
     }
     if (hh == 0) {  // the caller's lse row (none past a ragged N)
-      const long long cr = caller_row(p.rl, u, (long long)i * 64 + r, p.N);
+      const long long cr = rm.row((long long)i * 64 + r);
       if (cr >= 0) p.lse[cr] = l > 0.f ? (m_used + __log2f(l)) * 0.69314718055994531f : kLseSentinel;
     }
     if (has_w) {
@@ -525,9 +527,9 @@ __global__ void __launch_bounds__(192, 2)
     if (threadIdx.x == 64) {
 #pragma unroll
       for (int c = 0; c < NC; ++c) {
-        tc::tma_store_rows(&tmOs, sQ + c * 8192, 64 * c, u, i * 64, p.N, p.rl);
-        tc::tma_store_rows(&tmOl, sPX + c * 8192, 64 * c, u, i * 64, p.N, p.rl);
-        if (has_w) tc::tma_store_rows(&tmO, sV + c * 8192, 64 * c, u, i * 64, p.N, p.rl);
+        tc::tma_store_rows(&tmOs, sQ + c * 8192, 64 * c, i * 64, rt);
+        tc::tma_store_rows(&tmOl, sPX + c * 8192, 64 * c, i * 64, rt);
+        if (has_w) tc::tma_store_rows(&tmO, sV + c * 8192, 64 * c, i * 64, rt);
       }
       tc::bulk_commit();
       tc::bulk_wait_read<0>();  // smem may be released; the writes complete with the grid

@@ -44,10 +44,12 @@ __global__ void k_pool(const In* __restrict__ x, R* __restrict__ out, long long 
   // ragged N (SLA_B200_FLAG_RAGGED): the last block's mean is over its valid rows only
   const long long left = n_valid - (long long)g * b;
   const int rows = left < b ? int(left) : b;
+  const RowMap rm = row_map(rl, u, N);
+  const In* base = x + (rm.base + (long long)g * b * rm.stride) * d;  // rows < `rows` all exist
+  const long long rs = rm.stride * d;
   for (int c = threadIdx.x; c < d; c += blockDim.x) {
     R acc = R(0);
-    for (int r = 0; r < rows; ++r)
-      acc = add_rn(acc, R(to_f(x[caller_row(rl, u, (long long)g * b + r, N) * d + c])));
+    for (int r = 0; r < rows; ++r) acc = add_rn(acc, R(to_f(base[r * rs + c])));
     out[(u * T + g) * d + c] = div_rn(acc, R(rows));
   }
 }
@@ -71,10 +73,14 @@ __global__ void __launch_bounds__(32) k_pool2_bf16(const __nv_bfloat16* __restri
   if (g >= T) return;
   const long long left = n_valid - (long long)g * b;
   const int rows = left < b ? int(left) : b;
+  const RowMap rm = row_map(rl, u, N);
+  const __nv_bfloat16* base = x + (rm.base + (long long)g * b * rm.stride) * d;  // rows < `rows` all exist
+  const long long rs = rm.stride * d;
   for (int c = 4 * threadIdx.x; c < d; c += 128) {
     R a0 = R(0), a1 = R(0), a2 = R(0), a3 = R(0);
-    for (int r = 0; r < rows; ++r) {
-      const uint2 v = *reinterpret_cast<const uint2*>(x + caller_row(rl, u, (long long)g * b + r, N) * d + c);
+    const __nv_bfloat16* xr = base + c;
+    for (int r = 0; r < rows; ++r, xr += rs) {
+      const uint2 v = *reinterpret_cast<const uint2*>(xr);
       const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
       const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
       a0 = add_rn(a0, R(f0.x));

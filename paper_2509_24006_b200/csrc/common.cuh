@@ -29,6 +29,28 @@ __host__ __device__ __forceinline__ long long caller_row(const RowLayout& rl, lo
   if (rl.mode == 1) return u * rl.nv + r;
   return ((u / rl.H) * rl.nv + r) * rl.H + (u % rl.H);
 }
+// The same map for one unit, resolved once per CTA: caller row of kernel row r is
+// base + r * stride when r < nv.  Hot loops use this (no per-row layout branches or divisions;
+// inlining caller_row into the attention kernels cost 7-8 % of their time).
+struct RowMap {
+  long long base, stride, nv;
+  __host__ __device__ __forceinline__ long long row(long long r) const { return r < nv ? base + r * stride : -1; }
+};
+__host__ __device__ __forceinline__ RowMap row_map(const RowLayout& rl, long long u, long long N) {
+  if (rl.mode == 0) return RowMap{u * N, 1, N};
+  if (rl.mode == 1) return RowMap{u * rl.nv, 1, rl.nv};
+  return RowMap{(u / rl.H) * rl.nv * rl.H + u % rl.H, rl.H, rl.nv};
+}
+// 4-D tensor-map coordinates {col, h, y0 + r, z} of unit u's kernel row r (make_tmap_rows
+// builds every caller-tensor map as 4-D: [z][rows][h][d]), resolved once per CTA
+struct RowTma {
+  int h, y0, z;
+};
+__host__ __device__ __forceinline__ RowTma row_tma(const RowLayout& rl, long long u, long long N) {
+  if (rl.mode == 0) return RowTma{0, int(u * N), 0};
+  if (rl.mode == 1) return RowTma{0, 0, int(u)};
+  return RowTma{int(u % rl.H), 0, int(u / rl.H)};
+}
 
 // Derived problem dimensions (resolved once on the host from sla_b200_problem).
 struct Dims {

@@ -35,10 +35,18 @@ __global__ void __launch_bounds__(256) k_phi_kz(const __nv_bfloat16* __restrict_
   static_assert(C == 2 || C == 4, "d in {64, 128}");
   const long long rin0 = (long long)j * 64 + warp * 8;
   V raw[8];
+  const RowMap rm = row_map(rl, u, N);  // the caller's K in place (rows past a ragged N do not exist)
+  const V* src = reinterpret_cast<const V*>(k + (rm.base + rin0 * rm.stride) * D) + lane;
+  const long long rs = rm.stride * (D / C);
+  if (rin0 + 8 <= n_valid && rm.stride == 1) {  // unit-major rows: constant strides
 #pragma unroll
-  for (int rr = 0; rr < 8; ++rr) {  // the caller's K in place (rows past a ragged N do not exist)
-    const long long cr = caller_row(rl, u, rin0 + rr, N);
-    raw[rr] = cr >= 0 && rin0 + rr < n_valid ? reinterpret_cast<const V*>(k + cr * D)[lane] : V{};
+    for (int rr = 0; rr < 8; ++rr) raw[rr] = src[rr * (D / C)];
+  } else if (rin0 + 8 <= n_valid) {
+#pragma unroll
+    for (int rr = 0; rr < 8; ++rr) raw[rr] = src[rr * rs];
+  } else {
+#pragma unroll
+    for (int rr = 0; rr < 8; ++rr) raw[rr] = rin0 + rr < n_valid ? src[rr * rs] : V{};
   }
 #pragma unroll
   for (int rr = 0; rr < 8; ++rr) {

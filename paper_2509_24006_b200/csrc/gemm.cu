@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(224, 1)
             if (A_MN && arl.mode) {  // a caller tensor in place: chunk b % a_rpu of unit b / a_rpu
 #pragma unroll
               for (int c = 0; c < BM / 64; ++c)
-                tc::tma_load_rows(sa + c * 8192, &ta, &full[s], m0 + 64 * c, b / a_rpu, (b % a_rpu) * K + k0, 0, arl);
+                tc::tma_load_rows(sa + c * 8192, &ta, &full[s], m0 + 64 * c, (b % a_rpu) * K + k0, row_tma(arl, b / a_rpu, 0));
             } else if (A_MN) {
 #pragma unroll
               for (int c = 0; c < BM / 64; ++c) tc::tma_load_3d(sa + c * 8192, &ta, &full[s], m0 + 64 * c, k0, b);
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(224, 1)
             } else if (B_MN && brl.mode) {
 #pragma unroll
               for (int c = 0; c < BN / 64; ++c)
-                tc::tma_load_rows(sb + c * 8192, &tb, &full[s], n0 + 64 * c, b / b_rpu, (b % b_rpu) * K + k0, 0, brl);
+                tc::tma_load_rows(sb + c * 8192, &tb, &full[s], n0 + 64 * c, (b % b_rpu) * K + k0, row_tma(brl, b / b_rpu, 0));
             } else if (B_MN) {
 #pragma unroll
               for (int c = 0; c < BN / 64; ++c) tc::tma_load_3d(sb + c * 8192, &tb, &full[s], n0 + 64 * c, k0, b);
@@ -369,18 +369,37 @@ void dispatch_tile(const GemmArgs& g, cudaStream_t st) {
 
 bool make_tmap_rows(CUtensorMap* map, const void* base, uint64_t d, long long U, long long N,
                     const RowLayout& rl, uint32_t box_rows) {
-  if (rl.mode == 0) return make_tmap_bf16(map, base, d, uint64_t(U) * uint64_t(N), 1, d, 0, box_rows);
-  if (rl.mode == 1) return make_tmap_bf16(map, base, d, uint64_t(rl.nv), uint64_t(U), d, uint64_t(rl.nv) * d, box_rows);
-  const uint64_t H = uint64_t(rl.H), B = uint64_t(U) / H, nv = uint64_t(rl.nv);
-  cuuint64_t dims[4] = {d, H, nv, B};
-  cuuint64_t strides[3] = {d * 2, H * d * 2, nv * H * d * 2};
+  // always 4-D {d, h, rows, z} so the kernels address every layout as (c, t.h, t.y0 + r, t.z)
+  // (row_tma) without branching: mode 0 [U*N][d], mode 1 [U][nv][d], mode 2 [B][nv][H][d]
+  uint64_t dims_h = 1, rows, outer;
+  uint64_t s_h = d * 2, s_row, s_outer;
+  if (rl.mode == 0) {
+    rows = uint64_t(U) * uint64_t(N);
+    outer = 1;
+    s_row = d * 2;
+    s_outer = rows * d * 2;
+  } else if (rl.mode == 1) {
+    rows = uint64_t(rl.nv);
+    outer = uint64_t(U);
+    s_row = d * 2;
+    s_outer = rows * d * 2;
+  } else {
+    dims_h = uint64_t(rl.H);
+    rows = uint64_t(rl.nv);
+    outer = uint64_t(U) / dims_h;
+    s_h = d * 2;
+    s_row = dims_h * d * 2;
+    s_outer = rows * dims_h * d * 2;
+  }
+  cuuint64_t dims[4] = {d, dims_h, rows, outer};
+  cuuint64_t strides[3] = {s_h, s_row, s_outer};
   cuuint32_t box[4] = {64, 1, box_rows, 1};
   cuuint32_t estr[4] = {1, 1, 1, 1};
   CUresult r = encode_fn()(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void*>(base), dims, strides, box,
                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
-    throw CudaError("cuTensorMapEncodeTiled (4-D) failed (" + std::to_string(int(r)) + ")");
+    throw CudaError("cuTensorMapEncodeTiled (4-D rows) failed (" + std::to_string(int(r)) + ")");
   return true;
 }
 

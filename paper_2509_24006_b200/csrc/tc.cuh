@@ -152,19 +152,14 @@ __device__ __forceinline__ void tma_store_4d(const CUtensorMap* map, const void*
       "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
 }
-// A [64-row x 64-col] box of a caller tensor at (column c, unit u, row r) under its RowLayout
-// (make_tmap_rows builds the matching map)
-__device__ __forceinline__ void tma_load_rows(void* dst, const CUtensorMap* map, uint64_t* bar, int c, long long u,
-                                              int r, long long N, const RowLayout& rl) {
-  if (rl.mode == 0) tma_load_3d(dst, map, bar, c, int(u * N + r), 0);
-  else if (rl.mode == 1) tma_load_3d(dst, map, bar, c, r, int(u));
-  else tma_load_4d(dst, map, bar, c, int(u % rl.H), r, int(u / rl.H));
+// A [64-row x 64-col] box of a caller tensor at (column c, kernel row r) of the unit whose
+// coordinates t holds (row_tma; make_tmap_rows builds the matching 4-D map)
+__device__ __forceinline__ void tma_load_rows(void* dst, const CUtensorMap* map, uint64_t* bar, int c, int r,
+                                              const RowTma& t) {
+  tma_load_4d(dst, map, bar, c, t.h, t.y0 + r, t.z);
 }
-__device__ __forceinline__ void tma_store_rows(const CUtensorMap* map, const void* src, int c, long long u, int r,
-                                               long long N, const RowLayout& rl) {
-  if (rl.mode == 0) tma_store_3d(map, src, c, int(u * N + r), 0);
-  else if (rl.mode == 1) tma_store_3d(map, src, c, r, int(u));
-  else tma_store_4d(map, src, c, int(u % rl.H), r, int(u / rl.H));
+__device__ __forceinline__ void tma_store_rows(const CUtensorMap* map, const void* src, int c, int r, const RowTma& t) {
+  tma_store_4d(map, src, c, t.h, t.y0 + r, t.z);
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 // wait until at most N committed bulk groups still READ their smem source
