@@ -13,6 +13,8 @@
 // softmax / epilogue (row r = 16*(warp%4) + lane, lanes 0-15: the M=64 TMEM layout).
 // The K/V ring also carries H_i (before the loop) and W (after it) as ring items.
 // Lazy rescaling: O is rescaled only when the running max grows by more than 2^8.
+#include <cstdlib>
+
 #include "kernels.hpp"
 #include "tc.cuh"
 
@@ -588,7 +590,15 @@ void launch_attn_fwd(const Dims& Dm, const void* q, const void* k, const void* v
   p.phi = Dm.phi;
   p.kv_last = int(Dm.Nk_valid - (long long)(Dm.Tn - 1) * 64);
   p.rl = Dm.rl;
-  if (Dm.d == 128)
+  // SLA_B200_FWD_PAIR=1: the key-block-pair kernel (attn_fwd_pair.cu) at d = 128.  Off by
+  // default: measured 0.66 ms against 0.527 for this kernel (C3), see DESIGN.md section 8.
+  static const bool pair = [] {
+    const char* e = getenv("SLA_B200_FWD_PAIR");
+    return e && e[0] == '1';
+  }();
+  if (Dm.d == 128 && pair)
+    launch_attn_fwd_pair(Dm, q, k, v, w, o, o_s, o_l, lse, s, st);
+  else if (Dm.d == 128)
     launch_t<128>(Dm, q, k, v, w, s.Hb, p, st);
   else
     launch_t<64>(Dm, q, k, v, w, s.Hb, p, st);

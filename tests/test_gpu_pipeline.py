@@ -40,3 +40,37 @@ def test_host_pipeline_matches_device_path(B, H, chunks):
         else:
             torch.testing.assert_close(hdw, gr.dproj.cpu(), rtol=1e-5, atol=1e-5)
     assert hts.launches > 0
+
+
+@pytest.mark.parametrize("chunks", [3, 4])
+def test_pipelined_calls_overlap_and_stay_exact(chunks):
+    """pipelined=True: three back-to-back calls on two alternating input sets (no host sync, slots
+    and the W / dW buffers rotating across calls), then finish(): every call's outputs equal the
+    device path's for its own inputs."""
+    B, H, n, d = 1, 4, 1024, 128
+    cfg = SlaConfig(k_h=10, k_l=20, phi="softmax")
+    g = torch.Generator(device="cuda").manual_seed(11)
+    shape = (B, H, n, d)
+    op = SLA(B, H, n, d, 64, 64, cfg, torch.bfloat16)
+    sets, want = [], []
+    for _ in range(2):
+        q, k, v, do = (torch.randn(shape, generator=g, device="cuda").bfloat16() for _ in range(4))
+        w = (torch.randn((H, d, d), generator=g, device="cuda") * 0.1).bfloat16()
+        st = op.forward(q, k, v, w)
+        gr = op.backward(st, q, k, v, w, do)
+        want.append([t.cpu() for t in (st.o, gr.dq_total, gr.dk_total, gr.dv, gr.dproj)])
+        sets.append([t.cpu().pin_memory() for t in (q, k, v, w, do)])
+    torch.cuda.synchronize()
+    hts = HostTrainStep(B, H, n, d, 64, 64, cfg, torch.bfloat16, "cuda", chunks=chunks, pipelined=True)
+    outs = []
+    for call in range(3):
+        hq, hk, hv, hw, hdo = sets[call % 2]
+        o = [torch.empty(shape, dtype=torch.bfloat16).pin_memory() for _ in range(4)]
+        o.append(torch.empty((H, d, d), dtype=torch.float32).pin_memory())
+        hts(hq, hk, hv, hw, hdo, *o)
+        outs.append(o)
+    hts.finish()
+    torch.cuda.synchronize()
+    for call, o in enumerate(outs):
+        for got, ref in zip(o, want[call % 2]):
+            assert torch.equal(got, ref), f"call {call}"
