@@ -592,11 +592,13 @@ void launch_attn_fwd(const Dims& Dm, const void* q, const void* k, const void* v
   p.rl = Dm.rl;
   // SLA_B200_FWD_PAIR=1: the key-block-pair kernel (attn_fwd_pair.cu) at d = 128.  Off by
   // default: measured 0.66 ms against 0.527 for this kernel (C3), see DESIGN.md section 8.
-  static const bool pair = [] {
+  static const int pair = [] {
     const char* e = getenv("SLA_B200_FWD_PAIR");
-    return e && e[0] == '1';
+    return e ? atoi(e) : 0;
   }();
-  if (Dm.d == 128 && pair)
+  if (Dm.d == 128 && pair == 2)
+    launch_attn_fwd_pp(Dm, q, k, v, w, o, o_s, o_l, lse, s, st);
+  else if (Dm.d == 128 && pair == 1)
     launch_attn_fwd_pair(Dm, q, k, v, w, o, o_s, o_l, lse, s, st);
   else if (Dm.d == 128)
     launch_t<128>(Dm, q, k, v, w, s.Hb, p, st);

@@ -68,6 +68,9 @@ void launch_attn_fwd(const Dims& Dm, const void* q, const void* k, const void* v
 // attn_fwd_pair.cu: d = 128, key-block pairs with a transposed accumulator
 void launch_attn_fwd_pair(const Dims& Dm, const void* q, const void* k, const void* v, const void* w, void* o,
                           void* o_s, void* o_l, float* lse, const StateBufs& s, cudaStream_t st);
+// attn_fwd_pp.cu: d = 128, persistent (one CTA per SM), key-block pairs, overlapped epilogue
+void launch_attn_fwd_pp(const Dims& Dm, const void* q, const void* k, const void* v, const void* w, void* o,
+                        void* o_s, void* o_l, float* lse, const StateBufs& s, cudaStream_t st);
 void fast_summaries(const Dims& Dm, const void* k, const void* v, const WorkBufs& wb, cudaStream_t st);
 void fast_aggregate(const Dims& Dm, const StateBufs& s, const WorkBufs& wb, bool m0_ready, cudaStream_t st);
 void fast_aggregate_h(const Dims& Dm, const StateBufs& s, const WorkBufs& wb, cudaStream_t st);
