@@ -1,16 +1,19 @@
-// attn_bwd.cu -- the fused SLA backward on tcgen05: the COLUMNS pass (backward.cpp:142-199).
+// attn_bwd_cols2.cu -- the COLUMNS pass (backward.cpp:142-199) with row-major accumulators:
+// dK_j += dS^T Q_pair and dV_j += P^T dO_pair as M = 64 (key rows) x N = d MMAs, so the
+// epilogue reads each key row of dK, dV, dK^phi straight from TMEM (no shared-memory transposes)
+// and applies the phi-Jacobian row-wise.  The accumulation MMAs cost 8 x 64 cycles instead of
+// 8 x 50 per pair; the loop is bound by the Q / dO stream, not by them.  Selected by
+// SLA_B200_COLS=2; otherwise as attn_bwd.cu.
 // The rows pass and the linear-branch kernel live in attn_bwd_rows.cu.  Together they mirror
 // the reference's deterministic two-phase design (backward.cpp:68-120 and 142-199); no atomics.
 //
-// k_bwd_cols<D>: one CTA per (unit, key block j)
+// k_bwd_cols2<D>: one CTA per (unit, key block j)
 //   sparse dV_j += P^T dO_i, dK_j += dS^T Q_i over the critical rows (CSC list),
 //   linear dK^phi_j = V_j dH_agg^T + dZ_agg, dV_j += phi(K_j) dH_agg (dH_agg = M0^T dH),
 //   dk_total = J_phi(k)^T dK^phi + dK and dv written once.
 //
 // Warp roles: warps 0 and 10 TMA (Q pairs / dO pairs, since one issuing warp's TMA stream caps
 // at ~40 B/cycle), warps 1 and 11 MMA, warps 2-9 compute.
-#include <cstdlib>
-
 #include "bwd_common.cuh"
 
 namespace slab {
@@ -37,8 +40,21 @@ namespace {
 #ifndef SLAB_COLS_DVFIRST  // 1: acc(t) issues dV^T first, P stored first (measured 0.881 vs 0.838 ms)
 #define SLAB_COLS_DVFIRST 0
 #endif
+// DQ = D/4 consecutive columns of my row half in the M = 64 TMEM layout: threads 0-15 read
+// columns [c, c + DQ), threads 16-31 [c + D/2, c + D/2 + DQ) of the same lanes
 template <int D>
-struct ColsLayout {
+__device__ __forceinline__ void ld_rowq(uint32_t taddr, uint32_t (&r)[D / 4]);
+template <>
+__device__ __forceinline__ void ld_rowq<128>(uint32_t taddr, uint32_t (&r)[32]) {
+  tc::tmem_ld32_x2<64>(taddr, r);
+}
+template <>
+__device__ __forceinline__ void ld_rowq<64>(uint32_t taddr, uint32_t (&r)[16]) {
+  tc::tmem_ld16_x2<32>(taddr, r);
+}
+
+template <int D>
+struct Cols2Layout {
   static constexpr int kT = 64 * D * 2;    // 64-row tile
   static constexpr int kP = 128 * D * 2;   // 128-row pair tile
   static constexpr int oK = 0, oV = kT;
@@ -47,7 +63,8 @@ struct ColsLayout {
   static constexpr int kSlots = 5;
   static constexpr int oPD = oRing + kSlots * kSlot;  // [P 16 KB | dS 16 KB]; phi(K) aliases
   static constexpr int oZA = oPD + 32768;             // float [D] dZ_agg
-  static constexpr int oBar = oZA + 4 * D;
+  static constexpr int oX = oZA + 4 * D;              // float [2][2][64]: row partials exchanged between warp pairs
+  static constexpr int oBar = oX + 1024;
   static constexpr int kBytes = oBar + 256 + 1024;
   static_assert(kBytes <= 232448, "smem");
   static_assert(D * D * 2 <= kSlot && 3 * 64 * (D + 1) * 4 <= kSlots * kSlot, "ring reuse");
@@ -62,11 +79,11 @@ constexpr int kColsThreads = 32 * 12;
 
 template <int D>
 __global__ void __launch_bounds__(kColsThreads, 1)
-    k_bwd_cols(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
+    k_bwd_cols2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
                const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                const __grid_constant__ CUtensorMap tmHa, BwdParams p) {
   pdl_entry();  // launched by launch_pdl
-  using L = ColsLayout<D>;
+  using L = Cols2Layout<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sK = smem + L::oK;
@@ -165,9 +182,9 @@ __global__ void __launch_bounds__(kColsThreads, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // dV^T [0,64), dK^T [64,128) (M = D); S|dP pair buffers at 128 and 256 (M = 128);
-  // dK^phi^T at [384, 448) (M = D)
-  const uint32_t tDVT = tmem, tDKT = tmem + 64, tB0 = tmem + 128, tB1 = tmem + 256, tKPT = tmem + 384;
+  // dV [0,128), dK [128,256) (M = 64 key rows, N = D); S|dP pair buffers at 256 and 384
+  // (M = 128); dK^phi (M = 64) in the first S|dP buffer once the loop is done
+  const uint32_t tDVT = tmem, tDKT = tmem + 128, tB0 = tmem + 256, tB1 = tmem + 384, tKPT = tB0;
 
   if (warp == 0 || (warp >= 10 && warp < kAccWarp)) {
     // No L2 prefetch of the column's Q / dO tiles: prefetches queue in the TMA unit ahead of
@@ -208,9 +225,9 @@ __global__ void __launch_bounds__(kColsThreads, 1)
     const uint32_t aK = tc::smem_u32(sK), aV = tc::smem_u32(sV), aKF = tc::smem_u32(sKF);
     const uint32_t aR = tc::smem_u32(sRing), aPD = tc::smem_u32(sPD);
     constexpr uint32_t id_s = tc::idesc_bf16(128, 64, false, false);   // pair x K^T
-    constexpr uint32_t id_acc = tc::idesc_bf16(D, 64, true, true);     // pair^T x P
-    constexpr uint32_t id_kp = tc::idesc_bf16(D, 64, false, false);    // dH_agg x V^T
-    constexpr uint32_t id_vl = tc::idesc_bf16(D, 64, true, false);     // dH_agg^T x phi(K)^T
+    constexpr uint32_t id_acc = tc::idesc_bf16(64, D, true, true);     // P^T x dO_pair, dS^T x Q_pair
+    constexpr uint32_t id_kp = tc::idesc_bf16(64, D, false, false);    // V x dH_agg^T
+    constexpr uint32_t id_vl = tc::idesc_bf16(64, D, false, true);     // phi(K) x dH_agg
     auto wait_item = [&](int item) -> uint32_t {
       const int s = item % RS;
       tc::mbar_wait(ring_full + s, (item / RS) & 1);
@@ -238,8 +255,8 @@ __global__ void __launch_bounds__(kColsThreads, 1)
         tc::mbar_wait_w(ds_full, t & 1);
         tc::tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          tc::mma_bf16_w(tDKT, tc::desc_add(dq, kk * 2048), tc::desc_add(dd, kk * 2048), id_acc, (t | kk) != 0);
+        for (int kk = 0; kk < 8; ++kk)  // A = dS^T (MN-major [q][key] tile), B = Q_pair (MN-major, d chunks 16 KB apart)
+          tc::mma_bf16_w(tDKT, tc::desc_add(dd, kk * 2048), tc::desc_add(dq, kk * 2048), id_acc, (t | kk) != 0);
         tc::mma_commit_w(ring_empty + sq);  // dO(t+2) refills this slot
         tc::mma_commit_w(ds_empty);
       };
@@ -247,8 +264,8 @@ __global__ void __launch_bounds__(kColsThreads, 1)
         tc::mbar_wait_w(p_full, t & 1);
         tc::tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
-          tc::mma_bf16_w(tDVT, tc::desc_add(ddo, kk * 2048), tc::desc_add(dp, kk * 2048), id_acc, (t | kk) != 0);
+        for (int kk = 0; kk < 8; ++kk)  // A = P^T, B = dO_pair
+          tc::mma_bf16_w(tDVT, tc::desc_add(dp, kk * 2048), tc::desc_add(ddo, kk * 2048), id_acc, (t | kk) != 0);
         tc::mma_commit_w(ring_empty + sdo);
         tc::mma_commit_w(p_empty);
       };
@@ -303,16 +320,16 @@ __global__ void __launch_bounds__(kColsThreads, 1)
     if (has_lin) {
       const int item = 2 * np;
       const uint32_t sh = wait_item(item);
-      // dK^phi^T raw = dH_agg V^T (M = D over a, N = 64 keys, K = D over b): needs only dH_agg
+      // dK^phi raw = V_j dH_agg^T (M = 64 keys, N = D over a, K = D over b): needs only dH_agg
       // and V_j, so it runs while the compute warps still write the phi(K_j) tile
 #pragma unroll
-      for (int kk = 0; kk < D / 16; ++kk) tc::mma_bf16_w(tKPT, kdesc(sh, kk, D), kdesc(aV, kk, 64), id_kp, kk > 0);
+      for (int kk = 0; kk < D / 16; ++kk) tc::mma_bf16_w(tKPT, kdesc(aV, kk, 64), kdesc(sh, kk, D), id_kp, kk > 0);
       tc::mbar_wait(kf_ready, 0);
       tc::tc_fence_after();
-      // dV^T += dH_agg^T phi(K)^T (M = D over b, N = 64 keys, K = D over a)
+      // dV += phi(K_j) dH_agg (M = 64 keys, N = D over b, K = D over a)
 #pragma unroll
       for (int kk = 0; kk < D / 16; ++kk)
-        tc::mma_bf16_w(tDVT, tc::desc_mnmajor(sh + kk * 2048, D * 128), kdesc(aKF, kk, 64), id_vl,
+        tc::mma_bf16_w(tDVT, kdesc(aKF, kk, 64), tc::desc_mnmajor(sh + kk * 2048, D * 128), id_vl,
                        (np > 0 || kk > 0) ? 1u : 0u);
       tc::mma_commit_w(ring_empty + (item % RS));
       __syncwarp();
@@ -421,153 +438,140 @@ __global__ void __launch_bounds__(kColsThreads, 1)
       }
       ts_mark(dbg && threadIdx.x == 64 && t < 16, 48 + t);
     }
-    // ---- phi(K_j) rows (4 threads per key row, D/4 columns each): statistics + the bf16 tile
-    tc::mbar_wait(kv_full, 0);  // K_j must have landed even when no critical row came by
-    const int c = tid >> 2, c0 = (tid & 3) * (D / 4);
-    float mx = 0.f, inv = 1.f;
-    if (p.phi == 2) {
-      mx = -INFINITY;
-#pragma unroll
-      for (int cc = 0; cc < D / 4; cc += 8) {
-        float f[8];
-        unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, c0 + cc)), f);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) mx = fmaxf(mx, f[e]);
-      }
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-      float se = 0.f;
-#pragma unroll
-      for (int cc = 0; cc < D / 4; cc += 8) {
-        float f[8];
-        unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, c0 + cc)), f);
-#pragma unroll
-        for (int e = 0; e < 8; ++e) se += __expf(f[e] - mx);
-      }
-      se += __shfl_xor_sync(0xffffffffu, se, 1);
-      se += __shfl_xor_sync(0xffffffffu, se, 2);
-      inv = 1.f / se;
-    }
-    // phi(K_j) of this thread's D/4 columns, in the per-sub rotated chunk order the final
-    // row-wise pass reads (conflict-free transposed tiles), computed while the last
-    // accumulation MMAs still run; kept in registers for the Jacobian at the end
-    const int sub = tid & 3;
-    auto rot = [&](int cc) { return (cc + 8 * sub) & (D / 4 - 1); };
+    // ---- epilogue, row-wise from TMEM.  Thread: key row r of block j (M = 64 layout: lanes
+    // 0-15 of its warp's quarter), column half hh, column quarter grp of that half -> 32 of the D
+    // columns; a row's 4 threads combine partials with shfl(16) and the partner warp (smem).
+    const int r = 16 * q4 + (lane & 15);
+    const int hh = lane >> 4;
+    const int col0 = hh * (D / 2) + grp * (D / 4);  // D / 4 columns: 32 (D = 128) or 16 (D = 64)
     constexpr int DQ = D / 4;
+    const uint32_t aXc = tc::smem_u32(smem + L::oX);
+    int xb = 0;  // exchange buffer parity
+    auto row_combine = [&](float v, bool is_max) -> float {
+      v = is_max ? fmaxf(v, __shfl_xor_sync(0xffffffffu, v, 16)) : v + __shfl_xor_sync(0xffffffffu, v, 16);
+      const uint32_t a = aXc + uint32_t((xb * 2 + grp) * 256 + 4 * r);
+      if (hh == 0) asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+      named_sync(3 + q4, 64);  // this warp and its partner (same TMEM quarter)
+      float o;
+      asm volatile("ld.shared.f32 %0, [%1];" : "=f"(o) : "r"(a + (grp ? -256 : 256)));
+      xb ^= 1;
+      return is_max ? fmaxf(v, o) : v + o;
+    };
+    tc::mbar_wait(kv_full, 0);  // K_j must have landed even when no critical row came by
     float kf[DQ];
 #pragma unroll
-    for (int cc0 = 0; cc0 < DQ; cc0 += 8) {
+    for (int cc = 0; cc < DQ; cc += 8) {
       float f[8];
-      unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(c, c0 + rot(cc0))), f);
+      unpack8(*reinterpret_cast<const uint4*>(sK + tile_off(r, col0 + cc)), f);
 #pragma unroll
-      for (int e = 0; e < 8; ++e) kf[cc0 + e] = p.phi == 2 ? __expf(f[e] - mx) * inv : phi_elem(p.phi, f[e]);
+      for (int e = 0; e < 8; ++e) kf[cc + e] = f[e];
+    }
+    if (p.phi == 2) {  // per-row softmax over d (feature_map.cpp:22-40)
+      float mx = -INFINITY;
+#pragma unroll
+      for (int e = 0; e < DQ; ++e) mx = fmaxf(mx, kf[e]);
+      mx = row_combine(mx, true);
+      float se = 0.f;
+#pragma unroll
+      for (int e = 0; e < DQ; ++e) {
+        kf[e] = __expf(kf[e] - mx);
+        se += kf[e];
+      }
+      const float inv = 1.f / row_combine(se, false);
+#pragma unroll
+      for (int e = 0; e < DQ; ++e) kf[e] *= inv;
+    } else {
+#pragma unroll
+      for (int e = 0; e < DQ; ++e) kf[e] = phi_elem(p.phi, kf[e]);
     }
     tc::mbar_wait(acc_done, 0);  // the P / dS buffers are free
     ts_mark(dbg && threadIdx.x == 64, 120);
     cta_mark(threadIdx.x == 64, 2);
-    if (has_lin) {
+    if (has_lin) {  // the phi(K_j) tile: A operand of dV += phi(K_j) dH_agg
 #pragma unroll
-      for (int cc0 = 0; cc0 < DQ; cc0 += 8) {
+      for (int cc = 0; cc < DQ; cc += 8) {
         float f[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) f[e] = kf[cc0 + e];
-        *reinterpret_cast<uint4*>(sKF + tile_off(c, c0 + rot(cc0))) = pack8(f);
+        for (int e = 0; e < 8; ++e) f[e] = kf[cc + e];
+        *reinterpret_cast<uint4*>(sKF + tile_off(r, col0 + cc)) = pack8(f);
       }
       tc::fence_proxy_async();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(kf_ready);
     }
-    // ---- transpose dK^T, dV^T, dK^phi^T (lane = column a) into smem [key row][a].  dK^T is final
-    // at acc_done, so it goes first, while the linear MMAs still run; its region avoids the ring
-    // slot holding dH_agg (item 2 np), which those MMAs read until all_done.
-    constexpr int TP = D + 1;  // with the chunk rotation below: conflict-free row-wise reads
-    const int hs = (2 * np) % RS;
-    const bool tk_low = has_lin && (hs == 2 || hs == 3);
-    float* tbase = reinterpret_cast<float*>(sRing);
-    float* tk = tk_low ? tbase : tbase + 2 * 64 * TP;
-    float* tv = tk_low ? tbase + 64 * TP : tbase;
-    float* tkp = tk_low ? tbase + 2 * 64 * TP : tbase + 64 * TP;
-    const int acol = D == 128 ? 32 * q4 + lane : 16 * q4 + lane;
-    const bool avalid = D == 128 || lane < 16;
-    {
-      tc::tc_fence_after();
-      uint32_t a[32];
-      if (np > 0) tc::tmem_ld32(tDKT + lane_base + 32 * grp, a);
-      tc::tmem_ld_wait();
-      if (avalid) {
-#pragma unroll
-        for (int e = 0; e < 32; ++e) tk[(32 * grp + e) * TP + acol] = np > 0 ? __uint_as_float(a[e]) : 0.f;
-      }
-    }
-    ts_mark(dbg && threadIdx.x == 64, 121);
     tc::mbar_wait(all_done, 0);
     tc::tc_fence_after();
     ts_mark(dbg && threadIdx.x == 64, 122);
-    {
-      uint32_t b[32], e3[32];
-      if (np > 0 || has_lin) tc::tmem_ld32(tDVT + lane_base + 32 * grp, b);
-      if (has_lin) tc::tmem_ld32(tKPT + lane_base + 32 * grp, e3);
-      tc::tmem_ld_wait();
-      if (avalid) {
-#pragma unroll
-        for (int e = 0; e < 32; ++e) {
-          const int kr = 32 * grp + e;
-          tv[kr * TP + acol] = (np > 0 || has_lin) ? __uint_as_float(b[e]) : 0.f;
-          tkp[kr * TP + acol] = has_lin ? __uint_as_float(e3[e]) : 0.f;
-        }
-      }
-    }
-    named_sync(1, 256);
-    ts_mark(dbg && threadIdx.x == 64, 123);
-    // ---- dk_total = J_phi(k)^T (dK^phi + dZ_agg) + dK ; dv  (row-wise, 4 threads per row)
-    // The Jacobian needs only phi(k): softmax J^T g = phi (g - <phi, g>); elu1 J = 1 where
-    // k >= 0 (phi >= 1) else phi; relu J = 1 where phi > 0.
+    const uint32_t tcol = lane_base + uint32_t(grp * DQ);  // my columns: hh * D/2 via the x2 offset
+    named_sync(1, 256);  // zas (dZ_agg) written by all compute threads at entry
+    // ---- dk_total = J_phi(k)^T (dK^phi + dZ_agg) + dK ; dv
     float g[DQ];
+    {
+      uint32_t t32[DQ];
+      if (has_lin) {
+        ld_rowq<D>(tKPT + tcol, t32);
+        tc::tmem_ld_wait();
+      }
 #pragma unroll
-    for (int cc0 = 0; cc0 < DQ; cc0 += 8) {
-      const int col = c0 + rot(cc0);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) g[cc0 + e] = has_lin ? tkp[c * TP + col + e] + zas[col + e] : 0.f;
+      for (int e = 0; e < DQ; ++e) g[e] = has_lin ? __uint_as_float(t32[e]) + zas[col0 + e] : 0.f;
     }
-    const long long grow = rm.row((long long)j * 64 + c);  // -1: past a ragged N
-    float jg[DQ];
-    if (p.phi == 2) {
+    if (p.phi == 2) {  // softmax: J^T g = phi (g - <phi, g>)
       float dot = 0.f;
 #pragma unroll
       for (int e = 0; e < DQ; ++e) dot = fmaf(kf[e], g[e], dot);
-      dot += __shfl_xor_sync(0xffffffffu, dot, 1);
-      dot += __shfl_xor_sync(0xffffffffu, dot, 2);
+      dot = row_combine(dot, false);
 #pragma unroll
-      for (int e = 0; e < DQ; ++e) jg[e] = kf[e] * (g[e] - dot);
-    } else if (p.phi == 0) {
+      for (int e = 0; e < DQ; ++e) kf[e] = kf[e] * (g[e] - dot);
+    } else if (p.phi == 0) {  // elu1: J = 1 where k >= 0 (phi >= 1) else phi
 #pragma unroll
-      for (int e = 0; e < DQ; ++e) jg[e] = kf[e] >= 1.f ? g[e] : kf[e] * g[e];
-    } else {
+      for (int e = 0; e < DQ; ++e) kf[e] = kf[e] >= 1.f ? g[e] : kf[e] * g[e];
+    } else {  // relu: J = 1 where phi > 0
 #pragma unroll
-      for (int e = 0; e < DQ; ++e) jg[e] = kf[e] > 0.f ? g[e] : 0.f;
+      for (int e = 0; e < DQ; ++e) kf[e] = kf[e] > 0.f ? g[e] : 0.f;
     }
-    ts_mark(dbg && threadIdx.x == 64, 118);
+    const long long grow = rm.row((long long)j * 64 + r);  // -1: past a ragged N
+    {
+      uint32_t t32[DQ];
+      if (np > 0) {
+        ld_rowq<D>(tDKT + tcol, t32);
+        tc::tmem_ld_wait();
+      }
+      if (p.dk_part && grow >= 0) {  // SlaGradients::dk and ::dk_feat (f32)
+        float4* dks = reinterpret_cast<float4*>(p.dk_part + grow * D + col0);
+        float4* dkf = reinterpret_cast<float4*>(p.dkf_part + grow * D + col0);
 #pragma unroll
-    for (int cc0 = 0; cc0 < DQ; cc0 += 8) {
-      const int col = c0 + rot(cc0);
-      float o[8], w8[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        o[e] = jg[cc0 + e] + tk[c * TP + col + e];
-        w8[e] = tv[c * TP + col + e];
+        for (int e = 0; e < DQ; e += 4) {
+          dks[e / 4] = np > 0 ? make_float4(__uint_as_float(t32[e]), __uint_as_float(t32[e + 1]), __uint_as_float(t32[e + 2]),
+                                            __uint_as_float(t32[e + 3]))
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+          dkf[e / 4] = make_float4(g[e], g[e + 1], g[e + 2], g[e + 3]);
+        }
       }
       if (grow >= 0) {
-        *reinterpret_cast<uint4*>(p.dk + grow * D + col) = pack8(o);
-        *reinterpret_cast<uint4*>(p.dv + grow * D + col) = pack8(w8);
+#pragma unroll
+        for (int cc = 0; cc < DQ; cc += 8) {
+          float o[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) o[e] = kf[cc + e] + (np > 0 ? __uint_as_float(t32[cc + e]) : 0.f);
+          *reinterpret_cast<uint4*>(p.dk + grow * D + col0 + cc) = pack8(o);
+        }
       }
-      if (p.dk_part) {  // SlaGradients::dk and ::dk_feat (f32)
-        float4* dks = reinterpret_cast<float4*>(p.dk_part + grow * D + col);
-        float4* dkf = reinterpret_cast<float4*>(p.dkf_part + grow * D + col);
-        const float* t = tk + c * TP + col;
-        dks[0] = make_float4(t[0], t[1], t[2], t[3]);
-        dks[1] = make_float4(t[4], t[5], t[6], t[7]);
-        dkf[0] = make_float4(g[cc0], g[cc0 + 1], g[cc0 + 2], g[cc0 + 3]);
-        dkf[1] = make_float4(g[cc0 + 4], g[cc0 + 5], g[cc0 + 6], g[cc0 + 7]);
+    }
+    {
+      uint32_t t32[DQ];
+      const bool any = np > 0 || has_lin;
+      if (any) {
+        ld_rowq<D>(tDVT + tcol, t32);
+        tc::tmem_ld_wait();
+      }
+      if (grow >= 0) {
+#pragma unroll
+        for (int cc = 0; cc < DQ; cc += 8) {
+          float o[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) o[e] = any ? __uint_as_float(t32[cc + e]) : 0.f;
+          *reinterpret_cast<uint4*>(p.dv + grow * D + col0 + cc) = pack8(o);
+        }
       }
     }
   }
@@ -579,7 +583,7 @@ __global__ void __launch_bounds__(kColsThreads, 1)
 }
 
 template <int D>
-void launch_cols_t(const Dims& Dm, const void* q, const void* k, const void* v, const void* d_out,
+void launch_cols2_t(const Dims& Dm, const void* q, const void* k, const void* v, const void* d_out,
                    const __nv_bfloat16* Ha, BwdParams p, cudaStream_t st) {
   CUtensorMap tq, tdo, tk, tv, th;
   make_tmap_rows(&tq, q, D, Dm.U, Dm.N, p.rl, 64);
@@ -587,28 +591,18 @@ void launch_cols_t(const Dims& Dm, const void* q, const void* k, const void* v, 
   make_tmap_rows(&tk, k, D, Dm.U, Dm.Nk, p.rl, 64);
   make_tmap_rows(&tv, v, D, Dm.U, Dm.Nk, p.rl, 64);
   make_tmap_bf16(&th, Ha, D, uint64_t(Dm.U) * Dm.Tn * D, 1, D, 0, D);
-  auto kern = k_bwd_cols<D>;
-  SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ColsLayout<D>::kBytes));
-  launch_pdl(kern, dim3(Dm.Tn, unsigned(Dm.U)), kColsThreads, ColsLayout<D>::kBytes, st, tq, tdo, tk, tv, th, p);
-  check_launch("k_bwd_cols", st);
+  auto kern = k_bwd_cols2<D>;
+  SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cols2Layout<D>::kBytes));
+  launch_pdl(kern, dim3(Dm.Tn, unsigned(Dm.U)), kColsThreads, Cols2Layout<D>::kBytes, st, tq, tdo, tk, tv, th, p);
+  check_launch("k_bwd_cols", st);  // same profiler name as attn_bwd.cu
 }
 
 }  // namespace
 
-void launch_bwd_cols(const Dims& Dm, const void* q, const void* k, const void* v, const float* lse,
+void launch_bwd_cols2(const Dims& Dm, const void* q, const void* k, const void* v, const float* lse,
                      const void* d_out, void* dk, void* dv, const StateBufs& s,
                      const __nv_bfloat16* Ha, const float* gZa, const float* Ds, float* dk_part,
                      float* dkf_part, int* work, cudaStream_t st) {
-  // row-major accumulators (attn_bwd_cols2.cu) by default: C3 0.867 -> 0.836 ms (A/B on one
-  // box); SLA_B200_COLS=1 selects this file's transposed-accumulator kernel
-  static const int variant = [] {
-    const char* e = getenv("SLA_B200_COLS");
-    return e ? atoi(e) : 2;
-  }();
-  if (variant == 2) {
-    launch_bwd_cols2(Dm, q, k, v, lse, d_out, dk, dv, s, Ha, gZa, Ds, dk_part, dkf_part, work, st);
-    return;
-  }
   BwdParams p{};
   p.rl = Dm.rl;
   p.work = work;  // unused: one CTA per key block (a persistent variant spilled)
@@ -631,21 +625,10 @@ void launch_bwd_cols(const Dims& Dm, const void* q, const void* k, const void* v
   p.scale_log2 = float(Dm.inv_sqrt_d * 1.4426950408889634);
   p.phi = Dm.phi;
   if (Dm.d == 128)
-    launch_cols_t<128>(Dm, q, k, v, d_out, Ha, p, st);
+    launch_cols2_t<128>(Dm, q, k, v, d_out, Ha, p, st);
   else
-    launch_cols_t<64>(Dm, q, k, v, d_out, Ha, p, st);
+    launch_cols2_t<64>(Dm, q, k, v, d_out, Ha, p, st);
 }
 
 }  // namespace slab
 
-#ifdef SLAB_TIMELINE  // diagnostic accessors: timeline builds only (profiles/ctaprof.py)
-extern "C" int sla_b200_diag_cols_ctaprof(unsigned long long* host) {
-  return cudaMemcpyFromSymbol(host, slab::g_cta_prof, sizeof(slab::g_cta_prof)) == cudaSuccess ? 0 : 1;
-}
-#endif
-
-#ifdef SLAB_TIMELINE  // diagnostic accessors: timeline builds only (profiles/ctaprof.py)
-extern "C" int sla_b200_diag_cols_timeline(long long* host128) {
-  return cudaMemcpyFromSymbol(host128, slab::g_bwd_ts, 256 * sizeof(long long)) == cudaSuccess ? 0 : 1;
-}
-#endif

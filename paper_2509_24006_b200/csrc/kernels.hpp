@@ -80,6 +80,10 @@ void launch_bwd_lin(const Dims& Dm, const void* q, const void* w, const void* o_
 void launch_bwd_rows(const Dims& Dm, const void* q, const void* k, const void* v, const float* lse,
                      const void* d_out, void* dq, const StateBufs& s, const float* Ds,
                      const __nv_bfloat16* dqphi, float* dq_part, float* dqf_part, cudaStream_t st);
+void launch_bwd_cols2(const Dims& Dm, const void* q, const void* k, const void* v, const float* lse,
+                      const void* d_out, void* dk, void* dv, const StateBufs& s,
+                      const __nv_bfloat16* Ha, const float* gZa, const float* Ds, float* dk_part,
+                      float* dkf_part, int* work, cudaStream_t st);
 void launch_bwd_cols(const Dims& Dm, const void* q, const void* k, const void* v, const float* lse,
                      const void* d_out, void* dk, void* dv, const StateBufs& s,
                      const __nv_bfloat16* Ha, const float* gZa, const float* Ds, float* dk_part,
