@@ -81,7 +81,8 @@ template <int D>
 __global__ void __launch_bounds__(kColsThreads, 1)
     k_bwd_cols2(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmDO,
                const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
-               const __grid_constant__ CUtensorMap tmHa, BwdParams p) {
+               const __grid_constant__ CUtensorMap tmHa, const __grid_constant__ CUtensorMap tmDKo,
+               const __grid_constant__ CUtensorMap tmDVo, BwdParams p) {
   pdl_entry();  // launched by launch_pdl
   using L = Cols2Layout<D>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -547,14 +548,14 @@ __global__ void __launch_bounds__(kColsThreads, 1)
           dkf[e / 4] = make_float4(g[e], g[e + 1], g[e + 2], g[e + 3]);
         }
       }
-      if (grow >= 0) {
+      // dk staged as a K-major SW128 tile in the P / dS region (free since all_done: its phi(K)
+      // tile has been consumed), stored by TMA (coalesced; rows past a ragged N are clipped)
 #pragma unroll
-        for (int cc = 0; cc < DQ; cc += 8) {
-          float o[8];
+      for (int cc = 0; cc < DQ; cc += 8) {
+        float o[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) o[e] = kf[cc + e] + (np > 0 ? __uint_as_float(t32[cc + e]) : 0.f);
-          *reinterpret_cast<uint4*>(p.dk + grow * D + col0 + cc) = pack8(o);
-        }
+        for (int e = 0; e < 8; ++e) o[e] = kf[cc + e] + (np > 0 ? __uint_as_float(t32[cc + e]) : 0.f);
+        *reinterpret_cast<uint4*>(sPD + tile_off(r, col0 + cc)) = pack8(o);
       }
     }
     {
@@ -564,15 +565,24 @@ __global__ void __launch_bounds__(kColsThreads, 1)
         ld_rowq<D>(tDVT + tcol, t32);
         tc::tmem_ld_wait();
       }
-      if (grow >= 0) {
 #pragma unroll
-        for (int cc = 0; cc < DQ; cc += 8) {
-          float o[8];
+      for (int cc = 0; cc < DQ; cc += 8) {
+        float o[8];
 #pragma unroll
-          for (int e = 0; e < 8; ++e) o[e] = any ? __uint_as_float(t32[cc + e]) : 0.f;
-          *reinterpret_cast<uint4*>(p.dv + grow * D + col0 + cc) = pack8(o);
-        }
+        for (int e = 0; e < 8; ++e) o[e] = any ? __uint_as_float(t32[cc + e]) : 0.f;
+        *reinterpret_cast<uint4*>(sPD + 16384 + tile_off(r, col0 + cc)) = pack8(o);
       }
+    }
+    tc::fence_proxy_async();
+    named_sync(1, 256);
+    if (tid == 0) {
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        tc::tma_store_rows(&tmDKo, sPD + c * 8192, 64 * c, j * 64, rt);
+        tc::tma_store_rows(&tmDVo, sPD + 16384 + c * 8192, 64 * c, j * 64, rt);
+      }
+      tc::bulk_commit();
+      tc::bulk_wait_read<0>();  // smem may be released; the writes complete with the grid
     }
   }
   ts_mark(dbg && threadIdx.x == 64, 124);
@@ -585,15 +595,17 @@ __global__ void __launch_bounds__(kColsThreads, 1)
 template <int D>
 void launch_cols2_t(const Dims& Dm, const void* q, const void* k, const void* v, const void* d_out,
                    const __nv_bfloat16* Ha, BwdParams p, cudaStream_t st) {
-  CUtensorMap tq, tdo, tk, tv, th;
+  CUtensorMap tq, tdo, tk, tv, th, tdk, tdv;
   make_tmap_rows(&tq, q, D, Dm.U, Dm.N, p.rl, 64);
   make_tmap_rows(&tdo, d_out, D, Dm.U, Dm.N, p.rl, 64);
   make_tmap_rows(&tk, k, D, Dm.U, Dm.Nk, p.rl, 64);
   make_tmap_rows(&tv, v, D, Dm.U, Dm.Nk, p.rl, 64);
   make_tmap_bf16(&th, Ha, D, uint64_t(Dm.U) * Dm.Tn * D, 1, D, 0, D);
+  make_tmap_rows(&tdk, p.dk, D, Dm.U, Dm.Nk, p.rl, 64);  // outputs: key rows (n_kv views: Nk)
+  make_tmap_rows(&tdv, p.dv, D, Dm.U, Dm.Nk, p.rl, 64);
   auto kern = k_bwd_cols2<D>;
   SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cols2Layout<D>::kBytes));
-  launch_pdl(kern, dim3(Dm.Tn, unsigned(Dm.U)), kColsThreads, Cols2Layout<D>::kBytes, st, tq, tdo, tk, tv, th, p);
+  launch_pdl(kern, dim3(Dm.Tn, unsigned(Dm.U)), kColsThreads, Cols2Layout<D>::kBytes, st, tq, tdo, tk, tv, th, tdk, tdv, p);
   check_launch("k_bwd_cols", st);  // same profiler name as attn_bwd.cu
 }
 
@@ -632,3 +644,12 @@ void launch_bwd_cols2(const Dims& Dm, const void* q, const void* k, const void* 
 
 }  // namespace slab
 
+
+#ifdef SLAB_TIMELINE  // diagnostic accessors: timeline builds only (profiles/ctaprof.py)
+extern "C" int sla_b200_diag_cols2_ctaprof(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, slab::g_cta_prof, sizeof(slab::g_cta_prof)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int sla_b200_diag_cols2_timeline(long long* host128) {
+  return cudaMemcpyFromSymbol(host128, slab::g_bwd_ts, 256 * sizeof(long long)) == cudaSuccess ? 0 : 1;
+}
+#endif

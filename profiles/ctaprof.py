@@ -12,7 +12,10 @@ for _ in range(3):
 torch.cuda.synchronize()
 L = _lib.diag_lib()
 lab = st.labels.cpu().numpy().reshape(B*H, 512, 512)
-for name, fn in (("rows", L.sla_b200_diag_rows_ctaprof), ("cols", L.sla_b200_diag_cols_ctaprof)):
+cols_v2 = os.environ.get("SLA_B200_COLS", "2") == "2"  # the default columns kernel (attn_bwd_cols2.cu)
+cols_prof = L.sla_b200_diag_cols2_ctaprof if cols_v2 else L.sla_b200_diag_cols_ctaprof
+cols_tl = L.sla_b200_diag_cols2_timeline if cols_v2 else L.sla_b200_diag_cols_timeline
+for name, fn in (("rows", L.sla_b200_diag_rows_ctaprof), ("cols", cols_prof)):
     buf = (C.c_ulonglong * (8192*4))()
     assert fn(buf) == 0
     a = np.frombuffer(buf, dtype=np.uint64).reshape(8192, 4)[:512*12].copy()
@@ -34,7 +37,7 @@ for name, fn in (("rows", L.sla_b200_diag_rows_ctaprof), ("cols", L.sla_b200_dia
 
 # single-CTA (blockIdx 100, unit 6) event timelines (ts_mark slots, clock64)
 for name, fn, cols in (("rows", L.sla_b200_diag_bwd_timeline, [("ldK", 0), ("ldV", 112), ("Kin", 80), ("Vin", 96), ("sdp", 16), ("sdp_r", 208), ("got", 32), ("ldw", 240), ("math", 128), ("empty", 144), ("dS", 48), ("acc", 64), ("acc_r", 224)]),
-                       ("cols", L.sla_b200_diag_cols_timeline, [("ld", 0), ("in", 80), ("sdp", 16), ("got", 32), ("math", 128), ("empty", 144), ("PdS", 48), ("acc", 96), ("adone", 64)])):
+                       ("cols", cols_tl, [("ld", 0), ("in", 80), ("sdp", 16), ("got", 32), ("math", 128), ("empty", 144), ("PdS", 48), ("acc", 96), ("adone", 64)])):
     buf = (C.c_longlong * 256)()
     assert fn(buf) == 0
     t = np.frombuffer(buf, dtype=np.int64).copy(); t0 = t[127]
