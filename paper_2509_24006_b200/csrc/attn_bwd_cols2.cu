@@ -14,6 +14,8 @@
 //
 // Warp roles: warps 0 and 10 TMA (Q pairs / dO pairs, since one issuing warp's TMA stream caps
 // at ~40 B/cycle), warps 1 and 11 MMA, warps 2-9 compute.
+#include <cstdlib>
+
 #include "bwd_common.cuh"
 
 namespace slab {

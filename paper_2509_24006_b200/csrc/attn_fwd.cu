@@ -590,16 +590,14 @@ void launch_attn_fwd(const Dims& Dm, const void* q, const void* k, const void* v
   p.phi = Dm.phi;
   p.kv_last = int(Dm.Nk_valid - (long long)(Dm.Tn - 1) * 64);
   p.rl = Dm.rl;
-  // SLA_B200_FWD_PAIR=1: the key-block-pair kernel (attn_fwd_pair.cu) at d = 128.  Off by
-  // default: measured 0.66 ms against 0.527 for this kernel (C3), see DESIGN.md section 8.
+  // SLA_B200_FWD_PAIR=2: the persistent key-block-pair kernel (attn_fwd_pp.cu) at d = 128.  Off
+  // by default: measured 0.86 ms against 0.527 for this kernel (C3), see DESIGN.md section 8.
   static const int pair = [] {
     const char* e = getenv("SLA_B200_FWD_PAIR");
     return e ? atoi(e) : 0;
   }();
   if (Dm.d == 128 && pair == 2)
     launch_attn_fwd_pp(Dm, q, k, v, w, o, o_s, o_l, lse, s, st);
-  else if (Dm.d == 128 && pair == 1)
-    launch_attn_fwd_pair(Dm, q, k, v, w, o, o_s, o_l, lse, s, st);
   else if (Dm.d == 128)
     launch_t<128>(Dm, q, k, v, w, s.Hb, p, st);
   else

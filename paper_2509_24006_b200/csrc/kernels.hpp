@@ -65,9 +65,6 @@ void launch_gemm(const GemmArgs& g, cudaStream_t st);
 inline long long m0_stride(const Dims& D) { return (D.Tn + 7) / 8 * 8; }  // 16-byte rows for TMA
 void launch_attn_fwd(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
                      void* o, void* o_s, void* o_l, float* lse, const StateBufs& s, cudaStream_t st);
-// attn_fwd_pair.cu: d = 128, key-block pairs with a transposed accumulator
-void launch_attn_fwd_pair(const Dims& Dm, const void* q, const void* k, const void* v, const void* w, void* o,
-                          void* o_s, void* o_l, float* lse, const StateBufs& s, cudaStream_t st);
 // attn_fwd_pp.cu: d = 128, persistent (one CTA per SM), key-block pairs, overlapped epilogue
 void launch_attn_fwd_pp(const Dims& Dm, const void* q, const void* k, const void* v, const void* w, void* o,
                         void* o_s, void* o_l, float* lse, const StateBufs& s, cudaStream_t st);
