@@ -37,6 +37,9 @@ namespace {
 constexpr int kD = 128;
 constexpr int kThreads = 480;
 constexpr int kRS = 9;  // ring slots
+#ifndef SLAB_PP_POLY
+#define SLAB_PP_POLY 0  // measured: 0 0.817 ms, 3 0.872, 2 0.907 (and a parity failure at 3)
+#endif
 
 struct PPLayout {
   static constexpr int kTile = 16384;
@@ -436,8 +439,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const bool live = b.tiles(pp) == 2 || hh == 0;
         const int kvalid = !live ? 0 : ((p.kv_last < 64 && b.list[2 * pp + hh] == p.Tn - 1) ? p.kv_last - 32 * sub : 32);
         float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        if (kvalid == 32) {  // the common case: no masked column
 #pragma unroll
-        for (int e = 0; e < 32; ++e) m4[e & 3] = fmaxf(m4[e & 3], e < kvalid ? sa[e] : -INFINITY);
+          for (int e = 0; e < 32; ++e) m4[e & 3] = fmaxf(m4[e & 3], sa[e]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) m4[e & 3] = fmaxf(m4[e & 3], e < kvalid ? sa[e] : -INFINITY);
+        }
         float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
         mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 16));
         const uint32_t rmx = aRmax + uint32_t(((g & 1) * 2 + sub) * 256 + 4 * r);
@@ -451,13 +459,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float m_fin = (pp == 0 || need) ? m_new : m_used;
         float ps0 = 0.f, ps1 = 0.f;
         uint32_t pk[16];
+        // every SLAB_PP_POLY-th exponential on the FMA pipe (the MUFU's 16 / clock / SM is the
+        // softmax stage's throughput limit: 8192 exponentials per pair)
+        auto pexp = [&](int e) {
+          const float x = sa[e] * sc - m_fin;
+          return tc::poly_slot(e, SLAB_PP_POLY) ? tc::ex2_poly(x) : ex2(x);
+        };
+        if (kvalid == 32) {
 #pragma unroll
-        for (int e = 0; e < 32; e += 2) {
-          const float p0 = e < kvalid ? ex2(sa[e] * sc - m_fin) : 0.f;
-          const float p1 = e + 1 < kvalid ? ex2(sa[e + 1] * sc - m_fin) : 0.f;
-          ps0 += p0;
-          ps1 += p1;
-          pk[e >> 1] = tc::pack_bf16(p0, p1);
+          for (int e = 0; e < 32; e += 2) {
+            const float p0 = pexp(e), p1 = pexp(e + 1);
+            ps0 += p0;
+            ps1 += p1;
+            pk[e >> 1] = tc::pack_bf16(p0, p1);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; e += 2) {
+            const float p0 = e < kvalid ? ex2(sa[e] * sc - m_fin) : 0.f;
+            const float p1 = e + 1 < kvalid ? ex2(sa[e + 1] * sc - m_fin) : 0.f;
+            ps0 += p0;
+            ps1 += p1;
+            pk[e >> 1] = tc::pack_bf16(p0, p1);
+          }
         }
         fpp_mark(stp, sbase_ + 3);  // exps done
         if (g >= 2) tc::mbar_wait(pv_done + par(g), uint32_t(((g >> 1) - 1) & 1));  // P buffer g&1 is free
