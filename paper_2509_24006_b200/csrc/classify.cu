@@ -79,15 +79,23 @@ __global__ void __launch_bounds__(32) k_pool2_bf16(const __nv_bfloat16* __restri
   for (int c = 4 * threadIdx.x; c < d; c += 128) {
     R a0 = R(0), a1 = R(0), a2 = R(0), a3 = R(0);
     const __nv_bfloat16* xr = base + c;
-    for (int r = 0; r < rows; ++r, xr += rs) {
-      const uint2 v = *reinterpret_cast<const uint2*>(xr);
+    auto acc = [&](const uint2& v) {
       const float2 f0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.x));
       const float2 f1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&v.y));
       a0 = add_rn(a0, R(f0.x));
       a1 = add_rn(a1, R(f0.y));
       a2 = add_rn(a2, R(f1.x));
       a3 = add_rn(a3, R(f1.y));
+    };
+    int r = 0;
+    for (; r + 16 <= rows; r += 16, xr += 16 * rs) {  // 16 rows' loads in flight, then the ascending sums
+      uint2 v[16];
+#pragma unroll
+      for (int e = 0; e < 16; ++e) v[e] = *reinterpret_cast<const uint2*>(xr + e * rs);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) acc(v[e]);
     }
+    for (; r < rows; ++r, xr += rs) acc(*reinterpret_cast<const uint2*>(xr));
     R* o = out + (u * T + g) * d + c;
     o[0] = div_rn(a0, R(rows));
     o[1] = div_rn(a1, R(rows));
