@@ -115,57 +115,83 @@ __global__ void __launch_bounds__(32) k_pool2_bf16(const __nv_bfloat16* __restri
 // per CTA (each thread a 4x4 patch, strided by 16 rows / columns).  Every element is still ONE sequential ascending-c dot
 // with separately rounded mul and add (mat.hpp:83-97), so the values are bit-identical to
 // the reference's; tiling only shares the pooled rows through shared memory.
-#ifndef SLAB_SCORES_REGS
-#define SLAB_SCORES_REGS 96  // 64 spills; 80-128 all 0.083 ms (was 0.116 with the 4-way-conflicted tiling)
-#endif
+// K1b (f64 path): 64 x 64 score tile per CTA of 128 threads, 4 rows x 8 columns per thread
+// (12 shared-memory reads per 32 multiply-adds: the tile is FP64-issue bound, not smem bound),
+// the pooled rows staged in 32-column chunks by cp.async into two buffers (chunk c+1 lands while
+// chunk c is multiplied).  Operation order as mat.hpp:83-97: ascending c, mul and add rounded
+// separately, then * 1/sqrt(d).
 template <typename R>
-__global__ void __maxnreg__(SLAB_SCORES_REGS) k_scores(const R* __restrict__ pq, const R* __restrict__ pk,
+__global__ void __launch_bounds__(128) k_scores(const R* __restrict__ pq, const R* __restrict__ pk,
                                                 int d, int Tm, int Tn, R inv_sqrt_d,
                                                 R* __restrict__ s) {
   pdl_entry();  // launched by launch_pdl
-  constexpr int CK = 32;
-  __shared__ R sa[64][CK + 1];
-  __shared__ R sb[64][CK + 1];
+  constexpr int CK = 32, PITCH = CK + 1;
+  extern __shared__ __align__(16) unsigned char scores_smem[];  // R [2][64][PITCH] twice
+  auto sa = reinterpret_cast<R(*)[64][PITCH]>(scores_smem);
+  auto sb = reinterpret_cast<R(*)[64][PITCH]>(scores_smem + sizeof(R) * 2 * 64 * PITCH);
   const long long u = blockIdx.z;
   const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  R acc[4][4];
+  const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;  // rows ty + 16a, columns tx + 8b
+  R acc[4][8];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = R(0);
+    for (int b = 0; b < 8; ++b) acc[a][b] = R(0);
   const R* pqu = pq + u * (long long)Tm * d;
   const R* pku = pk + u * (long long)Tn * d;
-  for (int c0 = 0; c0 < d; c0 += CK) {
-    const int ck = min(CK, d - c0);
-    __syncthreads();
-    for (int e = threadIdx.x; e < 64 * CK; e += 256) {
+  const int nch = (d + CK - 1) / CK;
+  auto stage = [&](int ch, int buf) {  // rows past T and columns past d as zeros
+    const int c0 = ch * CK;
+    for (int e = threadIdx.x; e < 64 * CK; e += 128) {
       const int r = e / CK, c = e % CK;
-      sa[r][c] = (i0 + r < Tm && c < ck) ? pqu[(long long)(i0 + r) * d + c0 + c] : R(0);
-      sb[r][c] = (j0 + r < Tn && c < ck) ? pku[(long long)(j0 + r) * d + c0 + c] : R(0);
+      R* da = &sa[buf][r][c];
+      R* db = &sb[buf][r][c];
+      if (i0 + r < Tm && c0 + c < d)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(da))),
+                     "l"(pqu + (long long)(i0 + r) * d + c0 + c)
+                     : "memory");
+      else
+        *da = R(0);
+      if (j0 + r < Tn && c0 + c < d)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(db))),
+                     "l"(pku + (long long)(j0 + r) * d + c0 + c)
+                     : "memory");
+      else
+        *db = R(0);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  stage(0, 0);
+  for (int ch = 0; ch < nch; ++ch) {
+    const int buf = ch & 1;
+    if (ch + 1 < nch) {
+      stage(ch + 1, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
+    const int ck = min(CK, d - ch * CK);
     for (int c = 0; c < ck; ++c) {
-      // rows ty + 16a / columns tx + 16b: with the 33-element row pitch the 16 column reads of a
-      // warp hit 16 distinct 8-byte bank pairs (rows 4 apart collided 4-way)
-      R av[4], bv[4];
+      R av[4], bv[8];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) av[a] = sa[ty + 16 * a][c];
+      for (int a = 0; a < 4; ++a) av[a] = sa[buf][ty + 16 * a][c];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) bv[b] = sb[tx + 16 * b][c];
+      for (int b = 0; b < 8; ++b) bv[b] = sb[buf][tx + 8 * b][c];
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = add_rn(acc[a][b], mul_rn(av[a], bv[b]));
+        for (int b = 0; b < 8; ++b) acc[a][b] = add_rn(acc[a][b], mul_rn(av[a], bv[b]));
     }
+    __syncthreads();  // buffer buf is restaged two chunks later
   }
 #pragma unroll
   for (int a = 0; a < 4; ++a) {
     const int i = i0 + ty + 16 * a;
     if (i >= Tm) continue;
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int j = j0 + tx + 16 * b;
+    for (int b = 0; b < 8; ++b) {
+      const int j = j0 + tx + 8 * b;
       if (j < Tn) s[(u * Tm + i) * (long long)Tn + j] = mul_rn(acc[a][b], inv_sqrt_d);
     }
   }
@@ -949,7 +975,9 @@ static bool classify_t(const Dims& D, const In* q, const In* k, const StateBufs&
     SLAB_CUDA(cudaFuncSetAttribute(k_classify<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    int(smem)));
   R* scores = reinterpret_cast<R*>(w.p_c);
-  launch_pdl(k_scores<R>, dim3((D.Tn + 63) / 64, (D.Tm + 63) / 64, unsigned(D.U)), 256, 0, st,
+  const int scores_smem = int(sizeof(R)) * 4 * 64 * 33;
+  SLAB_CUDA(cudaFuncSetAttribute(k_scores<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, scores_smem));
+  launch_pdl(k_scores<R>, dim3((D.Tn + 63) / 64, (D.Tm + 63) / 64, unsigned(D.U)), 128, scores_smem, st,
              (const R*)pq, (const R*)pk, D.d, D.Tm, D.Tn, R(D.inv_sqrt_d), scores);
   check_launch("k_scores", st);
   const int P2 = next_pow2(D.Tn);
