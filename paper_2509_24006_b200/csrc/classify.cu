@@ -147,14 +147,14 @@ __global__ void __launch_bounds__(128) k_scores(const R* __restrict__ pq, const 
       R* da = &sa[buf][r][c];
       R* db = &sb[buf][r][c];
       if (i0 + r < Tm && c0 + c < d)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(da))),
-                     "l"(pqu + (long long)(i0 + r) * d + c0 + c)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(da))),
+                     "l"(pqu + (long long)(i0 + r) * d + c0 + c), "n"(int(sizeof(R)))
                      : "memory");
       else
         *da = R(0);
       if (j0 + r < Tn && c0 + c < d)
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(db))),
-                     "l"(pku + (long long)(j0 + r) * d + c0 + c)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(db))),
+                     "l"(pku + (long long)(j0 + r) * d + c0 + c), "n"(int(sizeof(R)))
                      : "memory");
       else
         *db = R(0);
