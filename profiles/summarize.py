@@ -38,7 +38,10 @@ def short(name: str) -> str:
     if m:
         return "k_aggregate_z" if m.group(2) == "0" else "k_aggregate_dz"
     m = re.search(r"\b(k_[A-Za-z0-9_]+)", name)
-    return m.group(1) if m else name[:40]
+    if not m:
+        return name[:40]
+    # kernels whose bench.py / profiler name differs from the symbol (variants of one stage)
+    return {"k_bwd_cols2": "k_bwd_cols", "k_attn_fwd_pp": "k_attn_fwd"}.get(m.group(1), m.group(1))
 
 
 def launches(path: str):
