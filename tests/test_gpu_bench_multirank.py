@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 def _bench(*args):
     cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--config", "c1", "--steps", "2", "--warmup", "3",
-           "--no-dense", "--no-cpu-baseline", "--no-e2e", *args]
+           "--no-dense", "--no-cpu-baseline", "--no-e2e", "--no-sustained", *args]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     if out.returncode != 0 and os.path.isdir(os.path.join(ROOT, "gpurun_out")):
         with open(os.path.join(ROOT, "gpurun_out", "multirank_failure.log"), "w") as f:
