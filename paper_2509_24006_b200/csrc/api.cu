@@ -3,6 +3,7 @@
 // classes (status 2 = std::invalid_argument, 1 = std::runtime_error).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <string>
 #include <unordered_map>
@@ -171,6 +172,15 @@ void check_inputs(const sla_b200_problem* p, const Dims& D, const WorkBufs& w,
 }
 
 // returns true when the fast path's marginal indicator M0 was written along with the labels
+// SLA_B200_NO_SIDE=1: every kernel on the caller's stream (A/B runs of the side-stream overlap)
+bool side_streams_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("SLA_B200_NO_SIDE");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+
 // A non-blocking side stream (and fork / join events) per device and host thread.  The forward
 // runs the mask-independent key summaries there while the classification chain, which is
 // latency- and FP64-bound and leaves most of each SM idle, runs on the caller's stream.
@@ -294,7 +304,7 @@ int sla_b200_forward(const sla_b200_problem* p, const void* q, const void* k, co
     // fork: phi(K), z and h = phi(K)^T V on the side stream, concurrent with classification.
     // Not under the per-kernel profiler (one event sequence) nor with the finiteness checks
     // (host syncs that may throw between fork and join).
-    const bool fork = fast && !check && !prof_enabled();
+    const bool fork = fast && !check && !prof_enabled() && side_streams_enabled();
     SideStream* ss = fork ? &side_stream() : nullptr;
     SideJoin guard(fork ? ss->s : nullptr, st);
     if (fork) {
@@ -366,7 +376,7 @@ void backward_impl(const sla_b200_problem* p, const void* q, const void* k, cons
   }
   if (fast) {
     SideFork side;
-    if (!prof_enabled()) {  // the per-kernel profiler times one event sequence
+    if (!prof_enabled() && side_streams_enabled()) {  // the per-kernel profiler times one event sequence
       SideStream& ss = side_stream();
       side.s = ss.s;
       side.fork = ss.fork;
