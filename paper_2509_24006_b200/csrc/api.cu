@@ -207,19 +207,20 @@ SideStream& side_stream() {
 
 bool classify_into_state(const sla_b200_problem* p, const Dims& D, const void* q, const void* k,
                          const int8_t* mask_in, double* p_c, const StateBufs& s,
-                         const WorkBufs& w, cudaStream_t st) {
+                         const WorkBufs& w, cudaStream_t st, cudaEvent_t after_pool = nullptr) {
   if (mask_in) {
     const size_t bytes = size_t(D.U) * D.Tm * D.Tn;
     if (mask_in != s.labels)
       SLAB_CUDA(cudaMemcpyAsync(s.labels, mask_in, bytes, cudaMemcpyDeviceToDevice, st));
     const bool check = p->flags & SLA_B200_FLAG_CHECK_FINITE;
     if (check) reset_slot(w.err + 1, st);
+    if (after_pool) SLAB_CUDA(cudaEventRecord(after_pool, st));
     launch_build_lut(D, s, check ? w.err + 1 : nullptr, st);
     if (check && read_slot(w.err + 1, st) != LLONG_MAX)
       throw InvalidArgument("build_lookup: label must be -1, 0 or 1");
     return false;
   }
-  return launch_classify(D, p->dtype, p->mask_precision, q, k, s, w, p_c, st);
+  return launch_classify(D, p->dtype, p->mask_precision, q, k, s, w, p_c, st, after_pool);
 }
 
 }  // namespace
@@ -307,14 +308,15 @@ int sla_b200_forward(const sla_b200_problem* p, const void* q, const void* k, co
     const bool fork = fast && !check && !prof_enabled() && side_streams_enabled();
     SideStream* ss = fork ? &side_stream() : nullptr;
     SideJoin guard(fork ? ss->s : nullptr, st);
+    // the side stream forks after the pooling kernel: phi(K) / summaries and the pooling are
+    // both HBM-bound, the scores and rank kernels after it are not
+    const bool m0_ready = classify_into_state(p, D, q, k, mask_in, nullptr, s, wb, st, fork ? ss->fork : nullptr);
     if (fork) {
-      SLAB_CUDA(cudaEventRecord(ss->fork, st));
       SLAB_CUDA(cudaStreamWaitEvent(ss->s, ss->fork, 0));
       guard.arm(ss->join);
       fast_summaries(D, k, v, wb, ss->s);
       SLAB_CUDA(cudaEventRecord(ss->join, ss->s));
     }
-    const bool m0_ready = classify_into_state(p, D, q, k, mask_in, nullptr, s, wb, st);
     if (fast) {
       SideFork side;
       if (fork) {

@@ -951,7 +951,7 @@ void launch_check_finite(const Dims& D, int dtype, const void* x, long long* slo
 
 template <typename R, typename In>
 static bool classify_t(const Dims& D, const In* q, const In* k, const StateBufs& s,
-                       const WorkBufs& w, double* p_c, cudaStream_t st) {
+                       const WorkBufs& w, double* p_c, cudaStream_t st, cudaEvent_t after_pool) {
   R* pq = reinterpret_cast<R*>(w.pq);
   R* pk = reinterpret_cast<R*>(w.pk);
   const int pt = D.d < 256 ? ((D.d + 31) / 32) * 32 : 256;
@@ -970,6 +970,7 @@ static bool classify_t(const Dims& D, const In* q, const In* k, const StateBufs&
     k_pool<R, In><<<dim3(D.Tn, unsigned(D.U)), pt, 0, st>>>(k, pk, D.Nk, D.d, D.bkv, D.Tn, D.Nk_valid, D.rl);
     check_launch("k_pool(k)", st);
   }
+  if (after_pool) SLAB_CUDA(cudaEventRecord(after_pool, st));  // (the caller forks its side stream here)
   const size_t smem = classify_smem_bytes(D, sizeof(R) == 8);
   if (smem > 48 * 1024)
     SLAB_CUDA(cudaFuncSetAttribute(k_classify<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1021,20 +1022,21 @@ static bool classify_t(const Dims& D, const In* q, const In* k, const StateBufs&
 }
 
 bool launch_classify(const Dims& D, int dtype, int mask_precision, const void* q, const void* k,
-                     const StateBufs& s, const WorkBufs& w, double* p_c, cudaStream_t st) {
+                     const StateBufs& s, const WorkBufs& w, double* p_c, cudaStream_t st,
+                     cudaEvent_t after_pool) {
   // the f32 variant computes 1/sqrt(d) in f32 as well
   if (dtype == 0) {
     auto qb = static_cast<const __nv_bfloat16*>(q);
     auto kb = static_cast<const __nv_bfloat16*>(k);
     if (mask_precision == 0)
-      return classify_t<double>(D, qb, kb, s, w, p_c, st);
-    return classify_t<float>(D, qb, kb, s, w, p_c, st);
+      return classify_t<double>(D, qb, kb, s, w, p_c, st, after_pool);
+    return classify_t<float>(D, qb, kb, s, w, p_c, st, after_pool);
   } else {
     auto qf = static_cast<const float*>(q);
     auto kf = static_cast<const float*>(k);
     if (mask_precision == 0)
-      return classify_t<double>(D, qf, kf, s, w, p_c, st);
-    return classify_t<float>(D, qf, kf, s, w, p_c, st);
+      return classify_t<double>(D, qf, kf, s, w, p_c, st, after_pool);
+    return classify_t<float>(D, qf, kf, s, w, p_c, st, after_pool);
   }
 }
 

@@ -11,7 +11,8 @@ void launch_check_finite(const Dims& D, int dtype, const void* x, long long* slo
                          cudaStream_t st);
 // returns true when it also wrote the fast path's marginal indicator M0 (s.M0 non-null)
 bool launch_classify(const Dims& D, int dtype, int mask_precision, const void* q, const void* k,
-                     const StateBufs& s, const WorkBufs& w, double* p_c, cudaStream_t st);
+                     const StateBufs& s, const WorkBufs& w, double* p_c, cudaStream_t st,
+                     cudaEvent_t after_pool = nullptr);
 void launch_build_lut(const Dims& D, const StateBufs& s, long long* bad, cudaStream_t st);
 void launch_build_csc(const Dims& D, const StateBufs& s, cudaStream_t st);
 void launch_build_m0(const Dims& D, const StateBufs& s, cudaStream_t st);
