@@ -592,7 +592,7 @@ __device__ __forceinline__ int nth_set_bit(uint64_t m, int n) {
 // EPL == 0: in shared memory (T <= 2048).  Element j = 32 r + lane either way.
 #define SLAB_RANK_FOR(r) _Pragma("unroll (EPL > 0 ? EPL : 1)") for (int r = 0; r < (EPL > 0 ? EPL : E); ++r)
 template <typename R, int EPL>
-__global__ void __launch_bounds__(256, 3) k_classify_rank(const R* __restrict__ scores, long long rows, int Tn,
+__global__ void __launch_bounds__(256, (EPL > 8 || EPL == 0) ? 2 : 3) k_classify_rank(const R* __restrict__ scores, long long rows, int Tn,
                                                        int n1, int n_neg, int8_t* __restrict__ labels,
                                                        int* __restrict__ crit_cnt, int* __restrict__ crit_idx,
                                                        int* __restrict__ marg_cnt, double* __restrict__ p_c_out,
