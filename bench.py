@@ -68,6 +68,8 @@ def parse():
     ap.add_argument("--no-dense", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-sustained", action="store_true")
+    ap.add_argument("--no-graph", action="store_true",
+                    help="time the eager step instead of its CUDA-graph replay")
     ap.add_argument("--e2e-chunks", type=int, default=12)
     return ap.parse_args()
 
@@ -272,8 +274,8 @@ def config_json(name, world=1):
     return {"workload": f"{name}: SLA fwd+bwd, B={Bg} H={H} N={N} d={d} b_q=b_kv={b} k_h={k_h}% k_l={k_l}% phi={phi}",
             "batch": Bg, "heads": H, "n": N, "d": d, "block": b, "k_h": k_h, "k_l": k_l, "phi": phi,
             "units": Bg * H, "units_per_rank": -(-Bg * H // world),
-            "n_note": ("N = 32760 as-is through SLA_B200_FLAG_RAGGED (zero-padded unit copies inside the "
-                       "timed region); the reference arm times N = 32768") if N % b else
+            "n_note": ("N = 32760 as-is through SLA_B200_FLAG_RAGGED (read and written in place, TMA zero "
+                       "fill past N); the reference arm times N = 32768") if N % b else
                       "N padded from 32760/75600 to a multiple of 64 (make_block_layout rejects ragged N)",
             "l2": "inputs (Q,K,V,dO = 4 x B*H*N*d*2 bytes) exceed the 126 MB L2; no flush needed",
             "parallelism": (f"{Bg * H} (batch x head) units partitioned over {world} rank(s) "
@@ -459,14 +461,41 @@ def run_ours(args):
     lab_stats = {"critical_blocks": crit, "marginal_blocks": int((labels == 0).sum())}
     stream = torch.cuda.current_stream()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # The rank's fwd+bwd (every kernel of the step, side-stream fork / join included) captured
+    # once into a CUDA graph and replayed per step; the dW reduction (a collective when world > 1)
+    # stays eager.  Eager launching leaves the device idle between dependent kernels on some hosts
+    # (profiles/host_probe.py: 2.93-3.04 eager vs 2.71 ms graph on one box, with the host only
+    # 0.2-0.5 ms per step into the enqueue).
+    graph = None
+    graph_launches = 0
+    if not args.no_graph:
+        n0 = comp.launches
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            comp.step()
+        graph_launches = comp.launches - n0
+        graph.replay()
+        runner.reduce_dw()
+        torch.cuda.synchronize()
 
-    def timed(n):
+    def step_once():
+        if graph is not None:
+            graph.replay()
+            comp.launches += graph_launches
+            runner.reduce_dw()
+        else:
+            runner.step()
+
+    def timed(n, eager=False):
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize()
         ev0.record(stream)
         for _ in range(n):
-            runner.step()
+            if eager:
+                runner.step()
+            else:
+                step_once()
         ev1.record(stream)
         torch.cuda.synchronize()
         if world > 1:
@@ -480,12 +509,13 @@ def run_ours(args):
         comp.launches = 0
         ms_clean = timed(args.steps)
         launches = comp.launches // args.steps
+        ms_eager = timed(args.steps, eager=True) if graph is not None else ms_clean
         # then the per-kernel breakdown pass (CUDA events after every launch), after the board
         # has idled back to the power state the first pass started from (a second pass run
         # back to back measured 0.15-0.3 ms per step slower at the same SM clock)
         time.sleep(3.0)
         L.lib().sla_b200_profiler(1)
-        ms_prof = timed(args.steps)
+        ms_prof = timed(args.steps, eager=True)  # per-launch events need the eager step
         buf = C.create_string_buffer(1 << 16)
         L.lib().sla_b200_profiler_report(buf, 1 << 16)
         L.lib().sla_b200_profiler(0)
@@ -545,6 +575,9 @@ def run_ours(args):
         "gpu_launches": launches * args.steps, "gpu_launches_per_step": launches,
         "roofline": roof, "kernels": table, "mask": lab_stats,
         "ms_per_step_profiled": ms_prof,
+        "launch": ("CUDA graph: the rank's fwd+bwd captured once, replayed per step (dW reduction eager)"
+                   if graph is not None else "eager"),
+        "ms_per_step_eager": max_over_ranks(ms_eager),
     }
     if rank == 0:
         out["clocks"] = cl

@@ -102,6 +102,7 @@ class ShardedStep:
         self.shard = partition_units(self.n_units, world, rank)
         self.compute: Optional[UnitCompute] = None
         self.dw: Optional[torch.Tensor] = None
+        self._dw_idx: Dict[torch.device, torch.Tensor] = {}
 
     @property
     def units(self) -> List[int]:
@@ -117,7 +118,10 @@ class ShardedStep:
         part = self.compute.dw_units()
         dw = torch.zeros((self.heads, self.d, self.d), dtype=torch.float32, device=part.device)
         if self.shard.count:
-            idx = torch.tensor([u % self.heads for u in self.units], dtype=torch.long, device=part.device)
+            idx = self._dw_idx.get(part.device)
+            if idx is None:  # built once per device: no host->device copy inside a step (graph capture)
+                idx = torch.tensor([u % self.heads for u in self.units], dtype=torch.long, device=part.device)
+                self._dw_idx[part.device] = idx
             dw.index_add_(0, idx, part.float())
         if self.world > 1:
             if dw.is_cuda and dist.get_backend(self.group) == "gloo":  # gloo moves host tensors
