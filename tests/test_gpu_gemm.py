@@ -45,3 +45,32 @@ def test_gemm_matches_fp32_matmul(a_mn, b_mn, M, N, K, batch, out_f32):
     tol = 1e-3 if out_f32 else 1e-2
     err = ((out - ref).abs().max() / ref.abs().max().clamp_min(1.0)).item()
     assert err <= tol, err
+
+
+@pytest.mark.parametrize("M,N,K,batch,a_mn", [
+    (512, 192, 512, 12, False),   # Z = M0 z at d = 64 (BN = 64 tiles)
+    (512, 384, 512, 12, True),    # dZ_agg at d = 128 (M-major M0, BN = 128)
+    (16, 16384, 16, 1, True),     # a partitioned view's dH_agg (BM = 64, K tail)
+    (64, 4096, 200, 3, False),
+    (128, 128, 32768, 12, True),  # split-K shaped dW chunks
+    (16, 384, 128, 1, True),      # a partitioned view's dZ_agg (BM = 64, BN = 128)
+    (16, 192, 128, 1, True),      # ... at d = 64 (BM = 64, BN = 64)
+    (48, 384, 512, 2, False),
+    (64, 64, 64, 6144, True),     # h_j = phi(K_j)^T V_j at d = 64 (BM = BN = 64), every key block
+    (128, 128, 64, 6144, True),   # ... at d = 128
+])
+@pytest.mark.parametrize("out_f32", [True, False])
+def test_gemm_is_deterministic(M, N, K, batch, a_mn, out_f32):
+    """Repeated launches of the same GEMM give bit-identical outputs (no races between the
+    producer, MMA and epilogue roles), and match an fp32 matmul."""
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    A = torch.randn((batch, M, K), device="cuda", generator=g).to(torch.bfloat16)
+    B = torch.randn((batch, K, N), device="cuda", generator=g).to(torch.bfloat16)
+    A_in = A.transpose(1, 2).contiguous() if a_mn else A.contiguous()
+    first = _gemm(A_in, B.contiguous(), M, N, K, batch, a_mn, True, out_f32)
+    for _ in range(12):
+        again = _gemm(A_in, B.contiguous(), M, N, K, batch, a_mn, True, out_f32)
+        assert torch.equal(again, first)
+    ref = A.float() @ B.float()
+    err = ((first.float() - ref).abs().max() / ref.abs().max().clamp_min(1.0)).item()
+    assert err <= (1e-3 if out_f32 else 1e-2), err
