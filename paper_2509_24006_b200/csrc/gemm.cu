@@ -175,6 +175,10 @@ __global__ void __launch_bounds__(224, 1)
     // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
     const int q = warp & 3;
     int lt = 0;
+    // output chunks staged so far by this CTA: the staging-buffer parity runs across tiles (with
+    // BN = 64 a tile is one chunk, and restarting the parity per tile would overwrite the buffer
+    // the previous tile's TMA store may still be reading)
+    int oc = 0;
     for (long long t = unit0; t < total; t += ustep, ++lt) {
       int n0, m0, b;
       coords(t, n0, m0, b);
@@ -188,16 +192,16 @@ __global__ void __launch_bounds__(224, 1)
         // (coalesced; row-per-thread global stores were as slow as the MMAs of the tile)
         const uint32_t ob = tc::smem_u32(smem + L::oOut);
 #pragma unroll 1
-        for (int c = 0; c < BN / 64; ++c) {
+        for (int c = 0; c < BN / 64; ++c, ++oc) {
           uint32_t r0[32], r1[32];
           const uint32_t ta0 = tmem + ab * BN + (uint32_t(32 * q) << 16) + 64 * c;
           tc::tmem_ld32(ta0, r0);
           tc::tmem_ld32(ta0 + 32, r1);
           tc::tmem_ld_wait();
-          // staging buffer (c & 1) is free once the store issued two chunks ago has read it
+          // staging buffer (oc & 1) is free once the store issued two chunks ago has read it
           if (threadIdx.x == 64) tc::bulk_wait_read<1>();
           asm volatile("bar.sync 1, 128;" ::: "memory");
-          const uint32_t buf = ob + (c & 1) * L::kOut;
+          const uint32_t buf = ob + (oc & 1) * L::kOut;
           if (BM == 128 || lane < 16) {
 #pragma unroll
             for (int ch = 0; ch < 8; ++ch) {
@@ -213,7 +217,7 @@ __global__ void __launch_bounds__(224, 1)
           tc::fence_proxy_async();
           asm volatile("bar.sync 1, 128;" ::: "memory");
           if (threadIdx.x == 64) {
-            tc::tma_store_3d(&tc_out, smem + L::oOut + (c & 1) * L::kOut, n0 + 64 * c, m0, b);
+            tc::tma_store_3d(&tc_out, smem + L::oOut + (oc & 1) * L::kOut, n0 + 64 * c, m0, b);
             tc::bulk_commit();
           }
         }
