@@ -10,7 +10,8 @@
 // the normalised O^s in TMEM.
 //
 // Warp roles (192 threads): warp 0 TMA producer, warp 1 MMA issuer (one thread), warps 2-5
-// softmax / epilogue (row r = 16*(warp%4) + lane, lanes 0-15: the M=64 TMEM layout).
+// softmax / epilogue (row r = 16*(warp%4) + (lane & 15); lanes 0-15 / 16-31 take the two column
+// halves through the 16x32bx2 TMEM shape).
 // The K/V ring also carries H_i (before the loop) and W (after it) as ring items.
 // Lazy rescaling: O is rescaled only when the running max grows by more than 2^8.
 #include <cstdlib>
