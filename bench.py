@@ -451,6 +451,11 @@ def run_ours(args):
     runner = ShardedStep(Bg, H, d, world, rank)
     comp = CudaUnits(runner.shard, H, N, d, b, cfg, dev)
     runner.attach(comp)
+    # every step runs on one side stream: eager steps and the graph capture below then share the
+    # operator's per-stream workspace (a capture on another stream would allocate a second one --
+    # 52 GB at c5)
+    torch.cuda.synchronize()
+    torch.cuda.set_stream(torch.cuda.Stream(dev))
     U = runner.shard.count
 
     for _ in range(args.warmup):
@@ -471,7 +476,7 @@ def run_ours(args):
     if not args.no_graph:
         n0 = comp.launches
         graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
+        with torch.cuda.graph(graph, stream=torch.cuda.current_stream()):
             comp.step()
         graph_launches = comp.launches - n0
         graph.replay()
@@ -623,6 +628,7 @@ def run_ours(args):
         ho = [torch.empty(shape, dtype=torch.bfloat16, pin_memory=True) for _ in range(4)]
         hdw = torch.empty((ne, d, d), dtype=torch.float32, pin_memory=True)
         runner.compute = None
+        graph = None  # the captured step's buffers and private pool go with it
         del comp
         torch.cuda.empty_cache()
         # pipelined: step k+1's uploads overlap step k's last downloads (every step still copies
