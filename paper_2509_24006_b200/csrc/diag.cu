@@ -204,6 +204,72 @@ __global__ void k_diag_mma_rate(int m, int n, int a_mn, int b_mn, int reps, long
 }  // namespace
 }  // namespace slab
 
+// (3b) the same for a cta_group::2 pair (cluster of 2): the leader issues `reps` M = 256 x N x 16
+// MMAs over both CTAs' smem (each holds 128 rows of A and N/2 columns of B, K-major)
+namespace slab {
+namespace {
+__global__ void k_diag_mma_pair_rate(int n, int reps, long long* out) {
+  extern __shared__ __align__(1024) uint8_t sm_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint32_t slot;
+  __shared__ uint64_t bar;
+  const int warp = threadIdx.x >> 5;
+  const uint32_t rank = tc::cluster_rank();
+  for (int e = threadIdx.x; e < (128 + 128) * 64 / 8; e += blockDim.x)
+    reinterpret_cast<uint4*>(sm)[e] = make_uint4(0x3c003c00u, 0, 0x3c003c00u, 0);
+  tc::fence_proxy_async();
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::fence_barrier_init();
+  }
+  tc::cluster_sync();
+  if (warp == 0) tc::tmem_alloc_pair<256>(&slot);
+  tc::tc_fence_before();
+  tc::cluster_sync();
+  tc::tc_fence_after();
+  if (threadIdx.x == 0) {
+    const long long t0 = clock64();
+    if (rank == 0) {
+      const uint32_t a = tc::smem_u32(sm), b = a + 128 * 128;
+      const uint32_t id = tc::idesc_bf16(256, n, false, false);
+      for (int r = 0; r < reps; ++r) {
+        const int kk = r & 3;
+        tc::mma_bf16_pair(slot, tc::desc_kmajor(a + kk * 32), tc::desc_kmajor(b + kk * 32), id, r > 0);
+      }
+      tc::mma_commit_pair_mc(&bar, uint16_t(3));
+    }
+    tc::mbar_wait(&bar, 0);
+    if (rank == 0) out[0] = clock64() - t0;
+  }
+  tc::tc_fence_before();
+  tc::cluster_sync();
+  if (warp == 0) tc::tmem_dealloc_pair<256>(slot);
+}
+}  // namespace
+}  // namespace slab
+
+extern "C" int sla_b200_diag_mma_pair_rate(int n, int reps, long long* host_cycles) {
+  long long* d = nullptr;
+  if (cudaMalloc(&d, sizeof(long long)) != cudaSuccess) return 1;
+  const int bytes = (128 + 128) * 128 + 1024;
+  cudaFuncSetAttribute(slab::k_diag_mma_pair_rate, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = bytes;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  if (cudaLaunchKernelEx(&cfg, slab::k_diag_mma_pair_rate, n, reps, d) != cudaSuccess) return 1;
+  int rc = cudaMemcpy(host_cycles, d, sizeof(long long), cudaMemcpyDeviceToHost) == cudaSuccess ? 0 : 1;
+  cudaFree(d);
+  return rc;
+}
+
 extern "C" int sla_b200_diag_mma_rate(int m, int n, int a_mn, int b_mn, int reps, long long* host_cycles) {
   long long* d = nullptr;
   if (cudaMalloc(&d, sizeof(long long)) != cudaSuccess) return 1;
