@@ -21,15 +21,19 @@ namespace slab {
 namespace {
 
 constexpr int kStages = 4;
+#ifndef SLAB_GEMM_P2_STAGES
+#define SLAB_GEMM_P2_STAGES 6  // a P2 stage is 32 KB (A 16 KB + half of B 16 KB)
+#endif
 constexpr int kBK = 64;  // K elements per stage (one 128-byte swizzle row of bf16)
 
-template <int BM, int BN>
+template <int BM, int BN, int ST = kStages>
 struct GemmSmem {
+  static constexpr int kStagesN = ST;
   static constexpr int kA = BM * kBK * 2;
   static constexpr int kB = BN * kBK * 2;
   static constexpr int kStage = kA + kB;
   static constexpr int kOut = BM * 64 * 2;  // one [BM][64] bf16 output box (TMA-store staging)
-  static constexpr int oOut = kStages * kStage;
+  static constexpr int oOut = ST * kStage;
   static constexpr int kBytes = oOut + 2 * kOut + 1024 /*align*/ + 256 /*barriers*/;
   static_assert(kBytes <= 232448, "smem");
 };
@@ -41,14 +45,21 @@ struct GemmSmem {
 // loads half of the pair's B k-block and multicasts it to both, so B crosses L2 -> SM once per
 // pair (the aggregation GEMMs are L2-bandwidth-bound).  A stage is refilled only after BOTH
 // CTAs' MMAs released it (every MMA commit arrives on the empty barrier of both CTAs).
-template <int BM, int BN, bool A_MN, bool B_MN, typename OutT, bool MC = false>
+// P2: a cta_group::2 pair -- the leader issues M = 2*BM MMAs over both CTAs' smem; each CTA
+// holds its own BM rows of A and half (BN/2 columns) of B.  Every TMA load completes on the
+// leader's full barrier; the leader's commits arrive on both CTAs' empty / tfull barriers; both
+// epilogues arrive on the leader's tempty.
+template <int BM, int BN, bool A_MN, bool B_MN, typename OutT, bool MC = false, bool P2 = false>
 __global__ void __launch_bounds__(224, 1)
     k_gemm(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
            const __grid_constant__ CUtensorMap tc_out,
            OutT* __restrict__ C, int M, int N, int K, int batch, long long c_batch, int ldc,
            RowLayout arl, RowLayout brl, int a_rpu, int b_rpu) {
   pdl_entry();  // launched by launch_pdl
-  using L = GemmSmem<BM, BN>;
+  static_assert(!(MC && P2), "one pairing mode");
+  using L = GemmSmem<BM, P2 ? BN / 2 : BN, P2 ? SLAB_GEMM_P2_STAGES : kStages>;  // P2: a stage holds half of B
+  constexpr int kStages = L::kStagesN;
+  constexpr bool PAIRED = MC || P2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::oOut + 2 * L::kOut);
@@ -61,10 +72,10 @@ __global__ void __launch_bounds__(224, 1)
   const int nk = (K + kBK - 1) / kBK;
   const int tiles_n = N / BN, tiles_m = (M + BM - 1) / BM;
   // work units: tiles, or (MC) pairs of M-adjacent tiles, one per CTA of the cluster
-  const int rank = MC ? int(tc::cluster_rank()) : 0;
-  const long long unit0 = MC ? blockIdx.x / 2 : blockIdx.x;
-  const long long ustep = MC ? gridDim.x / 2 : gridDim.x;
-  const int units_m = MC ? tiles_m / 2 : tiles_m;
+  const int rank = PAIRED ? int(tc::cluster_rank()) : 0;
+  const long long unit0 = PAIRED ? blockIdx.x / 2 : blockIdx.x;
+  const long long ustep = PAIRED ? gridDim.x / 2 : gridDim.x;
+  const int units_m = PAIRED ? tiles_m / 2 : tiles_m;
   const long long total = (long long)tiles_n * units_m * batch;
 
   if (warp == 0) {
@@ -72,27 +83,30 @@ __global__ void __launch_bounds__(224, 1)
       tc::tma_prefetch(&ta);
       tc::tma_prefetch(&tb);
       for (int s = 0; s < kStages; ++s) {
-        tc::mbar_init(&full[s], 2);              // one arrive.expect_tx per producer
+        tc::mbar_init(&full[s], P2 ? 4 : 2);     // one arrive.expect_tx per producer (P2: of both CTAs)
         tc::mbar_init(&empty[s], MC ? 2 : 1);    // (MC) both CTAs' MMA commits
       }
       for (int s = 0; s < 2; ++s) {
         tc::mbar_init(&tfull[s], 1);
-        tc::mbar_init(&tempty[s], 4);
+        tc::mbar_init(&tempty[s], P2 ? 8 : 4);  // (P2) both CTAs' epilogue warps
       }
       tc::fence_barrier_init();
     }
     __syncwarp();
-    tc::tmem_alloc<2 * BN>(tmem_slot);
+    if constexpr (P2)
+      tc::tmem_alloc_pair<2 * BN>(tmem_slot);
+    else
+      tc::tmem_alloc<2 * BN>(tmem_slot);
   }
   tc::tc_fence_before();
   __syncthreads();
-  if (MC) tc::cluster_sync();  // the peer's barriers are initialised before any multicast / remote arrive
+  if (PAIRED) tc::cluster_sync();  // the peer's barriers are initialised before any multicast / remote arrive
   tc::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
   auto coords = [&](long long t, int& n0, int& m0, int& b) {
     n0 = int(t % tiles_n) * BN;
-    m0 = (MC ? 2 * int((t / tiles_n) % units_m) + rank : int((t / tiles_n) % units_m)) * BM;
+    m0 = (PAIRED ? 2 * int((t / tiles_n) % units_m) + rank : int((t / tiles_n) % units_m)) * BM;
     b = int(t / ((long long)tiles_n * units_m));
   };
 
@@ -109,6 +123,25 @@ __global__ void __launch_bounds__(224, 1)
           uint8_t* sa = smem + s * L::kStage;
           uint8_t* sb = sa + L::kA;
           const int k0 = kb * kBK;
+          if constexpr (P2) {  // own half, completing on the leader's full barrier
+            const uint32_t lf = tc::mapa_shared(tc::smem_u32(&full[s]), 0);
+            if (loads_a) {
+              tc::mbar_expect_tx_cluster_relaxed(lf, L::kA);
+              if (A_MN) {
+#pragma unroll
+                for (int c = 0; c < BM / 64; ++c) tc::tma_load_3d_pair(sa + c * 8192, &ta, lf, m0 + 64 * c, k0, b);
+              } else {
+                tc::tma_load_3d_pair(sa, &ta, lf, k0, m0, b);
+              }
+            } else {
+              static_assert(!P2 || (B_MN && BN % 128 == 0), "P2: N-major B, 64-column chunks per half");
+              tc::mbar_expect_tx_cluster_relaxed(lf, L::kB);
+#pragma unroll
+              for (int c = 0; c < BN / 128; ++c)
+                tc::tma_load_3d_pair(sb + c * 8192, &tb, lf, n0 + rank * (BN / 2) + 64 * c, k0, b);
+            }
+            continue;
+          }
           if (loads_a) {
             tc::mbar_expect_tx(&full[s], L::kA);
             if (A_MN && arl.mode) {  // a caller tensor in place: chunk b % a_rpu of unit b / a_rpu
@@ -143,7 +176,10 @@ __global__ void __launch_bounds__(224, 1)
       }
     }
   } else if (warp == 1) {
-    constexpr uint32_t idesc = tc::idesc_bf16(BM, BN, A_MN, B_MN);
+    if (P2 && rank != 0) {
+      // the pair's MMAs are issued by the leader
+    } else {
+    constexpr uint32_t idesc = tc::idesc_bf16(P2 ? 2 * BM : BM, BN, A_MN, B_MN);
     int kc = 0, lt = 0;
     for (long long t = unit0; t < total; t += ustep, ++lt) {
       const int ab = lt & 1;
@@ -160,16 +196,29 @@ __global__ void __launch_bounds__(224, 1)
           const uint64_t a0 = A_MN ? tc::desc_mnmajor(sa, 8192) : tc::desc_kmajor(sa);
           const uint64_t b0 = B_MN ? tc::desc_mnmajor(sb, 8192) : tc::desc_kmajor(sb);
 #pragma unroll
-          for (int kk = 0; kk < kBK / 16; ++kk)
-            tc::mma_bf16_w(acc, tc::desc_add(a0, A_MN ? kk * 2048 : kk * 32), tc::desc_add(b0, B_MN ? kk * 2048 : kk * 32),
-                           idesc, (kb | kk) != 0);
-          if (MC)
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            const uint64_t da = tc::desc_add(a0, A_MN ? kk * 2048 : kk * 32);
+            const uint64_t db = tc::desc_add(b0, B_MN ? kk * 2048 : kk * 32);
+            if constexpr (P2)
+              tc::mma_bf16_pair_w(acc, da, db, idesc, (kb | kk) != 0);
+            else
+              tc::mma_bf16_w(acc, da, db, idesc, (kb | kk) != 0);
+          }
+          if (P2)
+            tc::mma_commit_pair_mc_w(&empty[s], uint16_t(3));
+          else if (MC)
             tc::mma_commit_mc_w(&empty[s], uint16_t(3));
           else
             tc::mma_commit_w(&empty[s]);
-          if (kb == nk - 1) tc::mma_commit_w(&tfull[ab]);
+          if (kb == nk - 1) {
+            if (P2)
+              tc::mma_commit_pair_mc_w(&tfull[ab], uint16_t(3));
+            else
+              tc::mma_commit_w(&tfull[ab]);
+          }
         }
       }
+    }
     }
   } else if (warp <= 5) {
     // epilogue warps 2..5 -> TMEM lane quarter (warp % 4)
@@ -223,7 +272,12 @@ __global__ void __launch_bounds__(224, 1)
         }
         tc::tc_fence_before();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&tempty[ab]);
+        if (lane == 0) {
+          if (P2)
+            tc::mbar_arrive_cluster_relaxed(tc::mapa_shared(tc::smem_u32(&tempty[ab]), 0));  // TMEM reads waited (wait::ld)
+          else
+            tc::mbar_arrive(&tempty[ab]);
+        }
         continue;
       }
       OutT* crow = C + (long long)b * c_batch + (long long)(m0 + row) * ldc + n0;
@@ -254,14 +308,24 @@ __global__ void __launch_bounds__(224, 1)
       }
       tc::tc_fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&tempty[ab]);
+      if (lane == 0) {
+        if (P2)
+          tc::mbar_arrive_cluster_relaxed(tc::mapa_shared(tc::smem_u32(&tempty[ab]), 0));  // TMEM reads waited (wait::ld)
+        else
+          tc::mbar_arrive(&tempty[ab]);
+      }
     }
   }
   if (threadIdx.x == 64) tc::bulk_wait_read<0>();
   tc::tc_fence_before();
   __syncthreads();
-  if (MC) tc::cluster_sync();  // no remote arrive may target a CTA that has exited
-  if (warp == 0) tc::tmem_dealloc<2 * BN>(tmem);
+  if (PAIRED) tc::cluster_sync();  // no remote arrive may target a CTA that has exited
+  if (warp == 0) {
+    if constexpr (P2)
+      tc::tmem_dealloc_pair<2 * BN>(tmem);
+    else
+      tc::tmem_dealloc<2 * BN>(tmem);
+  }
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -281,7 +345,7 @@ EncodeFn encode_fn() {
   return fn;
 }
 
-template <int BM, int BN, bool A_MN, bool B_MN, typename OutT, bool MC = false>
+template <int BM, int BN, bool A_MN, bool B_MN, typename OutT, bool MC = false, bool P2 = false>
 void launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
   CUtensorMap ta, tb;
   // A: K-major -> tensor [batch][M][K], box [BM][64]; M-major -> [batch][K][M], box [64][64]
@@ -302,13 +366,13 @@ void launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
   CUtensorMap tcm{};
   if (sizeof(OutT) == 2)  // output boxes [BM rows][64 cols] of C [batch][M][ldc]
     make_tmap_bf16(&tcm, g.C, g.N, g.M, g.batch, g.ldc, g.c_batch, BM);
-  auto kern = k_gemm<BM, BN, A_MN, B_MN, OutT, MC>;
-  constexpr int smem = GemmSmem<BM, BN>::kBytes;
+  auto kern = k_gemm<BM, BN, A_MN, B_MN, OutT, MC, P2>;
+  constexpr int smem = GemmSmem<BM, P2 ? BN / 2 : BN, P2 ? SLAB_GEMM_P2_STAGES : kStages>::kBytes;
   SLAB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   const long long tiles = (long long)(g.N / BN) * ((g.M + BM - 1) / BM) * g.batch;
   static int sms = 0;
   if (!sms) SLAB_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-  if (MC) {  // 2-CTA clusters, one tile pair per cluster at a time
+  if (MC || P2) {  // 2-CTA clusters, one tile pair per cluster at a time
     const int grid = int(std::min<long long>(tiles, sms)) & ~1;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
@@ -334,6 +398,9 @@ void launch_gemm_t(const GemmArgs& g, cudaStream_t st) {
   check_launch(g.name ? g.name : "k_gemm", st);
 }
 
+#ifndef SLAB_GEMM_2SM
+#define SLAB_GEMM_2SM 1  // cta_group::2 pairs for the aggregation GEMMs (takes precedence over MC)
+#endif
 #ifndef SLAB_GEMM_MC
 #define SLAB_GEMM_MC 1  // measured: gemm_aggregate_t 0.098 -> 0.093 ms, gemm_aggregate 0.098 -> 0.097
 #endif
@@ -342,6 +409,11 @@ void dispatch_major(const GemmArgs& g, cudaStream_t st) {
   // B multicast across 2-CTA clusters where the tile grid pairs up (the aggregation GEMMs)
   if constexpr (BM == 128 && BN == 256 && sizeof(OutT) == 2) {
     const int tiles_m = (g.M + BM - 1) / BM;
+    if (SLAB_GEMM_2SM && g.b_mn && tiles_m % 2 == 0 && g.M % BM == 0 && !g.a_rl.mode && !g.b_rl.mode) {
+      if (g.a_mn) launch_gemm_t<BM, BN, true, true, OutT, false, true>(g, st);
+      else launch_gemm_t<BM, BN, false, true, OutT, false, true>(g, st);
+      return;
+    }
     if (SLAB_GEMM_MC && g.b_mn && tiles_m % 2 == 0 && g.M % BM == 0) {
       if (g.a_mn) launch_gemm_t<BM, BN, true, true, OutT, true>(g, st);
       else launch_gemm_t<BM, BN, false, true, OutT, true>(g, st);
