@@ -20,7 +20,7 @@ from collections import defaultdict
 HERE = os.path.dirname(os.path.abspath(__file__))
 
 # ncu kernel (template instance) -> bench.py / profiler name
-GEMM_NAMES = {  # template arguments BM, BN, A_MN, B_MN, OutT (the trailing multicast flag dropped)
+GEMM_NAMES = {  # template arguments BM, BN, A_MN, B_MN, OutT (the trailing MC / P2 flags dropped)
     "k_gemm<128, 128, 1, 1, __nv_bfloat16>": "gemm_summaries",
     "k_gemm<128, 256, 0, 1, __nv_bfloat16>": "gemm_aggregate",
     "k_gemm<128, 256, 1, 1, __nv_bfloat16>": "gemm_aggregate_t",
@@ -32,7 +32,7 @@ GEMM_NAMES = {  # template arguments BM, BN, A_MN, B_MN, OutT (the trailing mult
 def short(name: str) -> str:
     m = re.search(r"(k_gemm<[^>]*>)", name)
     if m:
-        key = re.sub(r", [01]>$", ">", m.group(1))
+        key = re.sub(r"(, [01])+>$", ">", m.group(1))  # the multicast / CTA-pair flags dropped
         return GEMM_NAMES.get(key, m.group(1))
     m = re.search(r"(k_aggregate_vec)<(\d)>", name)
     if m:
