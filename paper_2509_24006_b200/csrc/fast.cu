@@ -5,6 +5,7 @@
 //       Z = sum over marginal z_j (ascending, f32)              k_aggregate_z
 //   K5  fused sparse + linear + projection forward              attn_fwd.cu
 // References: summaries.cpp:17-42, aggregation.cpp:40-56, forward.cpp:81-195.
+#include <cstdlib>
 #include <type_traits>
 
 #include "kernels.hpp"
@@ -398,11 +399,13 @@ static void launch_agg_t(const Dims& Dm, const StateBufs& s, const WorkBufs& wb,
 // with dq_total.  dH_i -> gH [U, Tm, d, d], dZ_i parts -> z3 [U, Tm, 3d], D^s -> Ds [U, N].
 // Independent cotangents: the linear kernel multiplies the given dO^l by an identity W (exact)
 // and D^s = <dO^s, O^s> comes from its own row-dot kernel.
+// rows_st: the stream of the sparse dQ pass (k_bwd_rows), ordered after k_bwd_lin on st through
+// `after_lin` (null: st)
 static void backward_rows_phase(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
                                 const void* o_s, const void* o_l, const float* lse, const void* d_out,
                                 const void* d_out_l, void* dq, const GradParts& parts, const StateBufs& s,
                                 const WorkBufs& wb, __nv_bfloat16* gH, __nv_bfloat16* z3, float* Ds,
-                                cudaStream_t st) {
+                                cudaStream_t st, cudaStream_t rows_st = nullptr, cudaEvent_t after_lin = nullptr) {
   const int d = Dm.d;
   const bool split = d_out_l != nullptr;
   const void* lin_w = w;
@@ -416,7 +419,21 @@ static void backward_rows_phase(const Dims& Dm, const void* q, const void* k, co
     lin_do = d_out_l;
   }
   launch_bwd_lin(Dm, q, lin_w, o_s, o_l, lin_do, s, gH, z3, Ds, wb.dqphi, split, st);
-  launch_bwd_rows(Dm, q, k, v, lse, d_out, dq, s, Ds, wb.dqphi, parts.dq, parts.dq_feat, st);
+  if (rows_st) {
+    SLAB_CUDA(cudaEventRecord(after_lin, st));
+    SLAB_CUDA(cudaStreamWaitEvent(rows_st, after_lin, 0));
+  }
+  launch_bwd_rows(Dm, q, k, v, lse, d_out, dq, s, Ds, wb.dqphi, parts.dq, parts.dq_feat, rows_st ? rows_st : st);
+}
+
+// SLA_B200_ROWS_SIDE=1 (A/B switch): the sparse dQ pass runs on the side stream, beside the dH
+// aggregation and the columns pass (neither reads its output)
+static bool rows_on_side() {
+  static const bool on = [] {
+    const char* e = getenv("SLA_B200_ROWS_SIDE");
+    return e && e[0] == '1';
+  }();
+  return on;
 }
 
 void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, const void* w,
@@ -439,11 +456,13 @@ void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, 
   } else {
     launch_build_csc(Dm, s, st);
   }
-  backward_rows_phase(Dm, q, k, v, w, o_s, o_l, lse, d_out, d_out_l, dq, parts, s, wb, wb.hb, wb.z3b, wb.Ds, st);
+  const bool rside = side.s && rows_on_side();
+  backward_rows_phase(Dm, q, k, v, w, o_s, o_l, lse, d_out, d_out_l, dq, parts, s, wb, wb.hb, wb.z3b, wb.Ds, st,
+                      rside ? side.s : nullptr, rside ? side.mid : nullptr);
   // dH_agg and dZ_agg need only k_bwd_lin's dH / dZ (measured: dH_agg on a side stream beside the
   // rows pass 2.81 ms per step against 2.73-2.78 here -- rows loses SMs, cols waits); the thin
   // dZ_agg GEMM runs on the side stream beside dH_agg
-  if (side.s && SLAB_AGG_Z_SIDE) {
+  if (side.s && SLAB_AGG_Z_SIDE && !rside) {
     SLAB_CUDA(cudaEventRecord(side.mid, st));
     SLAB_CUDA(cudaStreamWaitEvent(side.s, side.mid, 0));
     aggregate_vec_tc(Dm, s, wb.z3b, true, wb.gZa, "gemm_aggregate_dz", side.s);
@@ -457,6 +476,7 @@ void fast_backward(const Dims& Dm, const void* q, const void* k, const void* v, 
   if (side.s) SLAB_CUDA(cudaStreamWaitEvent(st, side.join, 0));
   launch_bwd_cols(Dm, q, k, v, lse, d_out, dk, dv, s, wb.hab, wb.gZa, wb.Ds, parts.dk, parts.dk_feat, wb.work_ctr, st);
   if (!side.s && dw) launch_dw_fast(Dm, o_l, d_out, dw, wb, st);
+  if (rside) SLAB_CUDA(cudaEventRecord(side.join2, side.s));  // after the rows pass
   guard.release();
   if (side.s) SLAB_CUDA(cudaStreamWaitEvent(st, side.join2, 0));
 }
