@@ -419,6 +419,7 @@ def dense_comparators(units_q, units_k, units_v, units_do, stream, flops_per_uni
 
 
 E2E_MAX_UNITS = 24  # pinned host footprint: 8 [N, d] bf16 tensors per unit
+E2E_PASSES = 3  # e2e timed passes of K steps each; the median pass is reported
 
 
 def run_ours(args):
@@ -644,17 +645,23 @@ def run_ours(args):
             e2e_step()
         hts.finish()
         torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        ev0.record(stream)
-        for _ in range(args.steps):
-            e2e_step()
-        hts.finish()
-        ev1.record(stream)
-        torch.cuda.synchronize()
-        e2e_ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+        # three passes of K steps (PCIe throughput drifts between runs on one box); the median pass
+        # is the value, every pass is listed
+        passes = []
+        for _ in range(E2E_PASSES):
+            if world > 1:
+                dist.barrier()
+            ev0.record(stream)
+            for _ in range(args.steps):
+                e2e_step()
+            hts.finish()
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            passes.append(max_over_ranks(ev0.elapsed_time(ev1) / args.steps))
+        e2e_ms = sorted(passes)[len(passes) // 2]
         out["e2e"] = {"value": flops_unit * ne * world / (e2e_ms * 1e-3) / 1e12, "unit": "TFLOPS",
-                      "ms_per_step": e2e_ms * U / ne, "h2d_bytes_per_step": hts.h2d_bytes() * U // ne,
+                      "ms_per_step": e2e_ms * U / ne, "passes_ms_per_step": [round(x * U / ne, 4) for x in passes],
+                      "h2d_bytes_per_step": hts.h2d_bytes() * U // ne,
                       "d2h_bytes_per_step": hts.d2h_bytes() * U // ne, "chunks": len(hts.ranges),
                       "api": "paper_2509_24006_b200.HostTrainStep (pinned host buffers, pipelined: step k+1's "
                              "H2D overlaps step k's D2H)",
