@@ -71,6 +71,7 @@ def parse():
     ap.add_argument("--no-graph", action="store_true",
                     help="time the eager step instead of its CUDA-graph replay")
     ap.add_argument("--e2e-chunks", type=int, default=12)
+    ap.add_argument("--e2e-slots", type=int, default=3)
     return ap.parse_args()
 
 
@@ -636,7 +637,7 @@ def run_ours(args):
         # its own inputs in and its outputs out inside the timed region; finish() orders the
         # timing stream after the last step)
         hts = HostTrainStep(1, ne, N, d, b, b, cfg, torch.bfloat16, dev, chunks=min(args.e2e_chunks, ne),
-                            pipelined=True)
+                            slots=args.e2e_slots, pipelined=True)
 
         def e2e_step():
             hts(hs[0], hs[1], hs[2], hw, hs[3], ho[0], ho[1], ho[2], ho[3], hdw)
