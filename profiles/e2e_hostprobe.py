@@ -1,5 +1,10 @@
+"""Host enqueue time per pipelined HostTrainStep call (C3, 12 and 3 chunks) against the device
+time per step: the host must stay ahead of the copies for the e2e step to reach its floor.
+
+    python profiles/e2e_hostprobe.py
+"""
 import sys, time, torch
-sys.path.insert(0, '.')
+sys.path.insert(0, __import__('os').path.dirname(__import__('os').path.dirname(__import__('os').path.abspath(__file__))))
 from paper_2509_24006_b200 import HostTrainStep, SlaConfig
 H,N,d=12,32768,128
 cfg=SlaConfig(k_h=5,k_l=10,phi="softmax")
