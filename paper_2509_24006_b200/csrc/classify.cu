@@ -604,7 +604,6 @@ __global__ void __launch_bounds__(256, (EPL > 8 || EPL == 0) ? 2 : 3) k_classify
   const int Tp = E * 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   R* v = reinterpret_cast<R*>(smem_raw) + (size_t)warp * Tp;  // the row (EPL == 0) / exact-path scratch
-  int8_t* lab = reinterpret_cast<int8_t*>(reinterpret_cast<R*>(smem_raw) + (size_t)8 * Tp) + (size_t)warp * Tp;
   const long long row = (long long)blockIdx.x * 8 + warp;
   if (row >= rows) return;
   constexpr unsigned FULL = 0xffffffffu;
@@ -808,42 +807,31 @@ __global__ void __launch_bounds__(256, (EPL > 8 || EPL == 0) ? 2 : 3) k_classify
     A1 = select_desc(K1 - 1, g1, e1);
     if (n_neg > 0) A2 = select_desc(K2 - 1, g2, e2);
   }
-  // ---- labels: in-set = {x > A} plus the first K - #(x > A) ties of A in index order
-  int run1 = 0, run2 = 0;
+  // ---- labels: in-set = {x > A} plus the first K - #(x > A) ties of A in index order; the label
+  // row, the marginal indicator row (bf16 0/1, the A operand of H = M0 h) and the ascending
+  // critical list are written in the same pass (element j = 32 r + lane: coalesced per r)
+  int run1 = 0, run2 = 0, base = 0, marg = 0;
   const unsigned lt = (1u << lane) - 1u;
+  int8_t* lrow = labels + row * Tn;
+  int* crow = crit_idx + row * Tn;
+  __nv_bfloat16* mrow = m0 ? m0 + row * m0_ld : nullptr;
   SLAB_RANK_FOR(r) {
     const int j = 32 * r + lane;
     const bool ok = j < Tn;
     const R x = val(r);
     const bool t1 = ok && x == A1, t2 = ok && n_neg > 0 && x == A2;
     const unsigned b1 = __ballot_sync(FULL, t1), b2 = __ballot_sync(FULL, t2);
-    const bool crit = x > A1 || (t1 && run1 + __popc(b1 & lt) < K1 - g1);
+    const bool crit = ok && (x > A1 || (t1 && run1 + __popc(b1 & lt) < K1 - g1));
     const bool keep = n_neg == 0 || x > A2 || (t2 && run2 + __popc(b2 & lt) < K2 - g2);
     run1 += __popc(b1);
     run2 += __popc(b2);
-    if (ok) lab[j] = crit ? int8_t(1) : (keep ? int8_t(0) : int8_t(-1));
-  }
-  __syncwarp();
-  int8_t* lrow = labels + row * Tn;
-  for (int j = lane; j < Tn; j += 32) lrow[j] = lab[j];
-  if (m0) {  // fast path: the marginal indicator row (A operand of H = M0 h), bf16 pairs
-    __nv_bfloat162* mrow = reinterpret_cast<__nv_bfloat162*>(m0 + row * m0_ld);
-    for (int j2 = lane; j2 < m0_ld / 2; j2 += 32) {
-      const int j = 2 * j2;
-      mrow[j2] = __floats2bfloat162_rn(j < Tn && lab[j] == 0 ? 1.f : 0.f,
-                                       j + 1 < Tn && lab[j + 1] == 0 ? 1.f : 0.f);
-    }
-  }
-  int base = 0, marg = 0;
-  int* crow = crit_idx + row * Tn;
-  for (int j0 = 0; j0 < Tn; j0 += 32) {
-    const int j = j0 + lane;
-    const int l = j < Tn ? lab[j] : -1;
-    const unsigned bc = __ballot_sync(FULL, l == 1);
-    const unsigned bm = __ballot_sync(FULL, l == 0);
-    if (l == 1) crow[base + __popc(bc & lt)] = j;
+    const bool mg = ok && !crit && keep;
+    if (ok) lrow[j] = crit ? int8_t(1) : (keep ? int8_t(0) : int8_t(-1));
+    if (mrow && j < m0_ld) mrow[j] = __float2bfloat16_rn(mg ? 1.f : 0.f);
+    const unsigned bc = __ballot_sync(FULL, crit);
+    if (crit) crow[base + __popc(bc & lt)] = j;
     base += __popc(bc);
-    marg += __popc(bm);
+    marg += __popc(__ballot_sync(FULL, mg));
   }
   if (lane == 0) {
     crit_cnt[row] = base;
